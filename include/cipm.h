@@ -1,0 +1,161 @@
+/*
+ * libcipm — C ABI of the B200-native (sm_100a) interior-point hot path.
+ *
+ * Drop-in boundary for the per-iteration work of the reference solver
+ * (/root/reference/pkg/src/conic_ipm).  Every entry point below names the
+ * reference interface it replaces; the Python host
+ * (paper_2412_19027_b200/solver.py) calls them through ctypes in the same
+ * order as the reference loop (ipm.py:427-482).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; host pointers unless documented;
+ *  - every function returns an int status: CIPM_OK (0) or a negative
+ *    CIPM_E_* code; nothing throws or aborts across the ABI;
+ *  - numerical failures detected on the device are latched in a device error
+ *    word and surface as the return code of the next synchronising call
+ *    (cipm_residuals, cipm_step_combined, cipm_sync);
+ *  - one context = one problem instance = one CUDA stream; not re-entrant.
+ */
+#ifndef CIPM_H
+#define CIPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (mapped to exception types by paper_2412_19027_b200/exceptions.py) */
+#define CIPM_OK 0
+#define CIPM_E_SCALING (-1)        /* ScalingFailure        (cones/scaling.py:79,154)   */
+#define CIPM_E_STEP (-2)           /* StepTooSmall          (cones/steps.py:97,106; ipm.py:366) */
+#define CIPM_E_FACTOR (-3)         /* FactorizationFailure  (kkt/system.py:259-260)     */
+#define CIPM_E_DENOM (-4)          /* DegenerateDenominator (ipm.py:331-332)            */
+#define CIPM_E_INTERIOR (-5)       /* LostInterior          (ipm.py:374-377)            */
+#define CIPM_E_DOMAIN (-6)         /* DomainError           (cones/scaling.py:372,379)  */
+#define CIPM_E_PATTERN (-7)        /* PatternMismatch                                   */
+#define CIPM_E_DIM (-8)            /* DimensionMismatch                                 */
+#define CIPM_E_CUDA (-20)          /* CUDA runtime failure                              */
+#define CIPM_E_ARG (-21)           /* invalid argument                                  */
+
+/* precision modes (kkt/system.py:28-29) */
+#define CIPM_FULL 0
+#define CIPM_MIXED 1
+
+/* device scalar block layout (cipm_read_scalars) */
+enum {
+    CIPM_SC_TAU = 0, CIPM_SC_KAPPA, CIPM_SC_MU,
+    CIPM_SC_GTAU,                 /* κ + q'x + b'z + x'Px/τ                          */
+    CIPM_SC_XPX, CIPM_SC_QX, CIPM_SC_BZ,
+    CIPM_SC_NRM_GX,               /* max |g_x / Dc|                                  */
+    CIPM_SC_NRM_ATZ,              /* max |A'z / Dc|                                  */
+    CIPM_SC_NRM_PX,               /* max |P x / Dc|                                  */
+    CIPM_SC_NRM_XU,               /* max |Dc x|                                      */
+    CIPM_SC_NRM_GZ,               /* max |g_z / Dr|                                  */
+    CIPM_SC_NRM_AXS,              /* max |(A x + s) / Dr|                            */
+    CIPM_SC_NRM_ZU,               /* max |Dr z|                                      */
+    CIPM_SC_NRM_SU,               /* max |s / Dr|                                    */
+    CIPM_SC_DEN,                  /* τ-step denominator (ipm.py:328-330)             */
+    CIPM_SC_DTAU_A, CIPM_SC_DKAPPA_A, CIPM_SC_DTAU_C, CIPM_SC_DKAPPA_C,
+    CIPM_SC_ALPHA_A, CIPM_SC_SIGMA, CIPM_SC_ALPHA_C, CIPM_SC_ALPHA_FINAL,
+    CIPM_SC_T0, CIPM_SC_T1, CIPM_SC_T2, CIPM_SC_T3, CIPM_SC_T4, CIPM_SC_T5, CIPM_SC_T6, CIPM_SC_T7,
+    CIPM_SC_ALPHA_WORK,           /* running step bound (atomic min)                 */
+    CIPM_SC_SZ,                   /* s'z                                             */
+    CIPM_SC_BUMPS,                /* dynamically regularised pivots (last factor)    */
+    CIPM_SC_REFINE_STEPS,         /* refinement steps of the last solve              */
+    CIPM_SC_COUNT = 64
+};
+
+typedef struct cipm_symbolic cipm_symbolic;
+typedef struct cipm_ctx cipm_ctx;
+
+/* Problem structure after cone reordering (problem.py:177-210): rows are
+ * [zero | nonneg | SOC... | exp... | pow... | PSD...]; offsets are row indices
+ * into the m conic rows. */
+typedef struct {
+    int64_t n, m;
+    const int64_t *p_rowptr, *p_colidx;   /* P, full symmetric CSR (n x n)  */
+    const int64_t *a_rowptr, *a_colidx;   /* A, CSR (m x n)                 */
+    int64_t zero_dim, nonneg_dim;
+    int64_t n_soc;  const int64_t *soc_off, *soc_dim;
+    int64_t n_exp;  const int64_t *exp_off;
+    int64_t n_pow;  const int64_t *pow_off; const double *pow_alpha;
+    int64_t n_psd;  const int64_t *psd_off, *psd_side;
+} cipm_problem_desc;
+
+typedef struct {
+    int precision;                 /* CIPM_FULL | CIPM_MIXED                         */
+    double delta_s, delta_d;       /* static / dynamic regularisation (system.py:35-42) */
+    double beta, backtrack, step_scale;     /* ipm.py:63-65                          */
+    double refine_abs, refine_rel; int refine_max;   /* RefinementSettings            */
+    int device;
+    void *stream;                  /* cudaStream_t (NULL = create a private stream)  */
+} cipm_settings;
+
+typedef struct {
+    int64_t dim, nsuper, nnz_l, nnz_storage, n_updates, max_width, max_rows, height;
+    double flops;
+} cipm_symbolic_info;
+
+int cipm_version(void);
+
+/* --- symbolic analysis (replaces kkt/system.py:87-148 + :188-240, ordering.py:15-53) --- */
+int cipm_symbolic_create(const cipm_problem_desc *desc, int ordering, cipm_symbolic **out);
+int cipm_symbolic_info_get(const cipm_symbolic *sym, cipm_symbolic_info *info);
+/* copy a named symbolic array ("perm", "sn_col", "sn_rptr", "sn_rows", "sn_loff", "sn_parent",
+ * "upd_ptr", "upd_src", "upd_p0", "upd_p1", "order", "map_p", "map_a", "map_diag", "map_hblk") */
+int cipm_symbolic_array(const cipm_symbolic *sym, const char *name, void *dst, int64_t *count);
+void cipm_symbolic_destroy(cipm_symbolic *sym);
+/* the reference's exact minimum-degree order of a symmetric pattern (ordering.py:15-53) */
+int cipm_min_degree(int64_t dim, const int64_t *rowptr, const int64_t *colidx, int32_t *perm);
+
+/* --- context (replaces Solver.__init__ device state, ipm.py:150-171, and KKTSystem) --- */
+int cipm_ctx_create(const cipm_problem_desc *desc, const cipm_symbolic *sym,
+                    const cipm_settings *settings, cipm_ctx **out);
+/* scaled problem values + equilibration (problem.py:222-284 output); H2D copy */
+int cipm_ctx_set_values(cipm_ctx *ctx, const double *p_values, const double *a_values,
+                        const double *q, const double *b, const double *d_row,
+                        const double *d_col, double c_obj);
+void cipm_ctx_destroy(cipm_ctx *ctx);
+int cipm_sync(cipm_ctx *ctx);
+int cipm_device_bytes(const cipm_ctx *ctx, int64_t *bytes);
+
+/* --- Algorithm-1 steps (ipm.py:411-482) --- */
+int cipm_init_iterate(cipm_ctx *ctx);                     /* unit_init, set.py:91-112       */
+int cipm_residuals(cipm_ctx *ctx, double *scalars_out);   /* ipm.py:233-280 + G rows :284   */
+int cipm_save_best(cipm_ctx *ctx);                        /* best = state.copy()  ipm.py:430 */
+int cipm_update_scaling(cipm_ctx *ctx);                   /* scaling.py:229-251             */
+int cipm_factor(cipm_ctx *ctx);                           /* set_scaling + numeric_factor   */
+int cipm_solve_affine(cipm_ctx *ctx, int *refine_steps);  /* col2 + affine directions       */
+int cipm_step_affine(cipm_ctx *ctx);                      /* step_length + centering        */
+int cipm_solve_combined(cipm_ctx *ctx, int *refine_steps);/* combined_rhs + directions      */
+int cipm_step_combined(cipm_ctx *ctx, double *alpha);     /* combined_step_size ipm.py:350  */
+int cipm_take_step(cipm_ctx *ctx);                        /* take_step ipm.py:368           */
+int cipm_read_scalars(cipm_ctx *ctx, double *out);
+/* which: 0 = current iterate, 1 = best iterate.  x (n), z (m), s (m), tkm[3] = τ, κ, μ */
+int cipm_get_iterate(cipm_ctx *ctx, int which, double *x, double *z, double *s, double *tkm);
+int cipm_set_iterate(cipm_ctx *ctx, const double *x, const double *z, const double *s, const double *tkm);
+
+/* --- operator-level seams (tests / observers) --- */
+/* refined KKT solve of K x = rhs with the current factor (system.py:279-314) */
+int cipm_kkt_solve(cipm_ctx *ctx, const double *rhs, double *x, int *steps, double *residual);
+/* H v with the current scaling (scaling.py:254-274) */
+int cipm_apply_h(cipm_ctx *ctx, const double *v, double *out);
+/* dense -H block values as scattered into the factor (for tests): returns the
+ * diagonal over zero+nonneg rows and the concatenated upper triangles of blocks */
+int cipm_scaling_values(cipm_ctx *ctx, double *diag, double *blocks);
+/* directions of the last affine / combined solve: dx (n), dz (m), ds (m), dtk[2] */
+int cipm_get_direction(cipm_ctx *ctx, int combined, double *dx, double *dz, double *ds, double *dtk);
+/* copy a named device vector ("x","z","s","gx","gz","dsc","col2","sol1","nn_h","hv") to the host */
+int cipm_get_vector(cipm_ctx *ctx, const char *name, double *out, int64_t *count);
+/* per-cone batched SOC residuals t^2 - |u|^2 with the reference's fixed order (steps.py:136-175) */
+int cipm_soc_residuals(cipm_ctx *ctx, const double *x, double *out);
+/* kernel launches issued since the last reset (bench accounting) */
+int cipm_launch_count(cipm_ctx *ctx, int64_t *count, int reset);
+/* CUDA-event time (ms) of the last numeric factorisation and last triangular solve */
+int cipm_kernel_times(cipm_ctx *ctx, double *factor_ms, double *solve_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIPM_H */

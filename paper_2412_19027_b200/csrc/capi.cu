@@ -1,0 +1,732 @@
+// C ABI of libcipm (include/cipm.h): context lifetime, host<->device plumbing
+// and the Algorithm-1 step entry points.  Each entry point enqueues kernels on
+// the context's stream; the ones that must return a decision to the host
+// (residual scalars, refinement convergence, backtracking outcomes, take_step)
+// synchronise once and return the latched device error word.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.hpp"
+#include "symbolic.hpp"
+
+namespace cipm {
+// launchers defined in vec.cu that are not in ctx.hpp
+void k_nsym_resolve(Ctx& c);
+void k_step_store(Ctx& c, int which);
+void k_nb_resolve(Ctx& c, int g0, int nk);
+void k_kkt_residual_one(Ctx& c, int q);
+void k_refine_init_one(Ctx& c, int q);
+void k_copy(Ctx& c, const double* src, double* dst, int64_t n);
+int factor_grid(Ctx& c);
+int solve_grid(Ctx& c);
+}  // namespace cipm
+
+using namespace cipm;
+
+struct cipm_symbolic {
+    Symbolic s;
+};
+
+struct cipm_ctx {
+    Ctx c;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(Ctx& c, T** p, int64_t count) {
+    *p = nullptr;
+    size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+    cudaError_t e = cudaMalloc((void**)p, bytes);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[cipm] cudaMalloc(%zu) failed: %s\n", bytes, cudaGetErrorString(e));
+        return CIPM_E_CUDA;
+    }
+    c.allocations.push_back((void*)*p);
+    cudaMemsetAsync(*p, 0, bytes, c.stream);
+    return CIPM_OK;
+}
+
+template <typename T, typename S>
+int upload(Ctx& c, T** p, const S* host, int64_t count) {
+    int rc = dalloc(c, p, count);
+    if (rc) return rc;
+    if (count <= 0) return CIPM_OK;
+    std::vector<T> tmp((size_t)count);
+    for (int64_t i = 0; i < count; ++i) tmp[i] = (T)host[i];
+    CIPM_CUDA(cudaMemcpy(*p, tmp.data(), sizeof(T) * count, cudaMemcpyHostToDevice));
+    return CIPM_OK;
+}
+
+int sync_err(Ctx& c) {
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(cudaGetLastError());
+    CIPM_CUDA(cudaMemcpy(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost));
+    return *c.h_err;
+}
+
+int read_sc(Ctx& c) {
+    CIPM_CUDA(cudaMemcpyAsync(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(cudaGetLastError());
+    return *c.h_err;
+}
+
+// refined solve of rb[q], q < nrhs; result in rbest[q]
+int refine(Ctx& c, int nrhs, int* steps_out) {
+    for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    int active[2] = {1, nrhs > 1 ? 1 : 0};
+    int steps = 0;
+    for (int step = 1; step <= c.refine_max; ++step) {
+        k_refine_step(c, nrhs, active);
+        for (int q = 0; q < nrhs; ++q)
+            if (active[q]) k_kkt_residual_one(c, q);
+        CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
+        CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        CIPM_CUDA(cudaStreamSynchronize(c.stream));
+        if (*c.h_err) return *c.h_err;
+        steps = step;
+        bool any = false;
+        for (int q = 0; q < nrhs; ++q) {
+            if (active[q] && c.h_rstate[8 * q + 4] != 0.0) active[q] = 0;
+            any = any || active[q];
+        }
+        if (!any) break;
+    }
+    if (steps_out) *steps_out = steps;
+    c.h_sc[CIPM_SC_REFINE_STEPS] = steps;
+    return CIPM_OK;
+}
+
+int step_length(Ctx& c, int which) {
+    k_step_init(c, which);
+    k_step_bound(c, c.dz[which], c.ds[which]);
+    k_step_finish(c, which);
+    if (c.nsym) {
+        for (int batch = 0; batch < 8; ++batch) {
+            CIPM_CUDA(cudaMemsetAsync(c.mask, 0xff, sizeof(unsigned int), c.stream));
+            k_nsym_feasible_mask(c, c.dz[which], c.ds[which], 32 * batch);
+            k_nsym_resolve(c);
+            int e = read_sc(c);
+            if (e) return e;
+            if (c.h_sc[CIPM_SC_T7] == 0.0) break;
+        }
+    }
+    k_step_store(c, which);
+    return CIPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cipm_version(void) { return 100; }
+
+int cipm_min_degree(int64_t dim, const int64_t* rowptr, const int64_t* colidx, int32_t* perm) {
+    // treat the pattern as K with n = dim, m = 0 and no blocks: the graph is the symmetrised pattern
+    SymbolicOptions opt;
+    Symbolic s;
+    std::vector<int64_t> arp(1, 0);
+    int rc = analyze(dim, 0, rowptr, colidx, arp.data(), nullptr, 0, 0, nullptr, nullptr, opt, s);
+    if (rc) return rc;
+    for (int64_t k = 0; k < dim; ++k) perm[k] = s.md_perm[k];
+    return CIPM_OK;
+}
+
+static void blocks_of(const cipm_problem_desc* d, std::vector<int64_t>& off, std::vector<int64_t>& dim) {
+    for (int64_t i = 0; i < d->n_soc; ++i) { off.push_back(d->soc_off[i]); dim.push_back(d->soc_dim[i]); }
+    for (int64_t i = 0; i < d->n_exp; ++i) { off.push_back(d->exp_off[i]); dim.push_back(3); }
+    for (int64_t i = 0; i < d->n_pow; ++i) { off.push_back(d->pow_off[i]); dim.push_back(3); }
+    for (int64_t i = 0; i < d->n_psd; ++i) {
+        off.push_back(d->psd_off[i]);
+        dim.push_back(d->psd_side[i] * (d->psd_side[i] + 1) / 2);
+    }
+}
+
+int cipm_symbolic_create(const cipm_problem_desc* d, int ordering, cipm_symbolic** out) {
+    if (!d || !out) return CIPM_E_ARG;
+    auto* h = new cipm_symbolic();
+    std::vector<int64_t> off, dim;
+    blocks_of(d, off, dim);
+    SymbolicOptions opt;
+    opt.ordering = ordering;
+    int rc = analyze(d->n, d->m, d->p_rowptr, d->p_colidx, d->a_rowptr, d->a_colidx, d->zero_dim + d->nonneg_dim,
+                     (int64_t)off.size(), off.data(), dim.data(), opt, h->s);
+    if (rc) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return CIPM_OK;
+}
+
+int cipm_symbolic_info_get(const cipm_symbolic* sym, cipm_symbolic_info* info) {
+    if (!sym || !info) return CIPM_E_ARG;
+    const Symbolic& s = sym->s;
+    info->dim = s.dim;
+    info->nsuper = s.nsuper;
+    info->nnz_l = s.nnz_l;
+    info->nnz_storage = s.nnz_storage;
+    info->n_updates = s.n_updates;
+    info->max_width = s.max_width;
+    info->max_rows = s.max_rows;
+    info->height = s.height;
+    info->flops = s.flops;
+    return CIPM_OK;
+}
+
+int cipm_symbolic_array(const cipm_symbolic* sym, const char* name, void* dst, int64_t* count) {
+    if (!sym || !name) return CIPM_E_ARG;
+    const Symbolic& s = sym->s;
+    std::string nm(name);
+    const void* src = nullptr;
+    int64_t cnt = 0;
+    size_t es = 0;
+#define ARR(NAME, VEC)                                           \
+    if (nm == NAME) { src = VEC.data(); cnt = (int64_t)VEC.size(); es = sizeof(VEC[0]); }
+    ARR("perm", s.perm)
+    ARR("md_perm", s.md_perm)
+    ARR("sn_col", s.sn_col)
+    ARR("sn_rptr", s.sn_rptr)
+    ARR("sn_rows", s.sn_rows)
+    ARR("sn_loff", s.sn_loff)
+    ARR("sn_parent", s.sn_parent)
+    ARR("upd_ptr", s.upd_ptr)
+    ARR("upd_src", s.upd_src)
+    ARR("upd_p0", s.upd_p0)
+    ARR("upd_p1", s.upd_p1)
+    ARR("order", s.order)
+    ARR("map_p", s.map_p)
+    ARR("map_a", s.map_a)
+    ARR("map_diag", s.map_diag)
+    ARR("map_hblk", s.map_hblk)
+#undef ARR
+    if (!es) return CIPM_E_ARG;
+    if (count) *count = cnt;
+    if (dst && cnt) memcpy(dst, src, es * (size_t)cnt);
+    return CIPM_OK;
+}
+
+void cipm_symbolic_destroy(cipm_symbolic* sym) { delete sym; }
+
+int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const cipm_settings* st, cipm_ctx** out) {
+    if (!d || !symh || !st || !out) return CIPM_E_ARG;
+    for (int64_t i = 0; i < d->n_psd; ++i)
+        if (d->psd_side[i] > 16) {
+            fprintf(stderr, "[cipm] PSD side %lld > 16 is not supported by the device kernels\n",
+                    (long long)d->psd_side[i]);
+            return CIPM_E_ARG;
+        }
+    auto* h = new cipm_ctx();
+    Ctx& c = h->c;
+    c.device = st->device;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    if (st->stream) {
+        c.stream = (cudaStream_t)st->stream;
+    } else {
+        CIPM_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.own_stream = true;
+    }
+    c.n = d->n;
+    c.m = d->m;
+    c.dim = d->n + d->m;
+    c.precision = st->precision;
+    c.delta_s = st->delta_s;
+    c.delta_d = st->delta_d;
+    c.beta = st->beta;
+    c.backtrack = st->backtrack;
+    c.step_scale = st->step_scale;
+    c.refine_abs = st->refine_abs;
+    c.refine_rel = st->refine_rel;
+    c.refine_max = st->refine_max;
+    c.zero_dim = d->zero_dim;
+    c.nonneg_dim = d->nonneg_dim;
+    c.lin = d->zero_dim + d->nonneg_dim;
+    c.nsoc = d->n_soc;
+    c.nexp = d->n_exp;
+    c.npow = d->n_pow;
+    c.npsd = d->n_psd;
+    c.nsym = c.nexp + c.npow;
+    c.p_nnz = d->p_rowptr[d->n];
+    c.a_nnz = d->a_rowptr[d->m];
+    int rc = 0;
+#define TRY(x)                  \
+    do {                        \
+        rc = (x);               \
+        if (rc) {               \
+            cipm_ctx_destroy(h); \
+            return rc;          \
+        }                       \
+    } while (0)
+
+    // cone tables
+    std::vector<int64_t> soc_h(c.nsoc), psd_m(c.npsd), psd_l(c.npsd), psd_h(c.npsd);
+    int64_t hp = 0;
+    c.soc_rows = 0;
+    for (int64_t i = 0; i < c.nsoc; ++i) {
+        soc_h[i] = hp;
+        hp += d->soc_dim[i] * (d->soc_dim[i] + 1) / 2;
+        c.soc_rows += d->soc_dim[i];
+    }
+    c.nsym_hbase = hp;
+    hp += 6 * c.nsym;
+    int64_t mp = 0, lp = 0;
+    c.psd_max_side = 0;
+    double psd_deg = 0;
+    for (int64_t i = 0; i < c.npsd; ++i) {
+        int64_t sd = d->psd_side[i];
+        psd_m[i] = mp;
+        psd_l[i] = lp;
+        psd_h[i] = hp;
+        mp += sd * sd;
+        lp += sd;
+        int64_t tdim = sd * (sd + 1) / 2;
+        hp += tdim * (tdim + 1) / 2;
+        c.psd_max_side = std::max<int>(c.psd_max_side, (int)sd);
+        psd_deg += (double)sd;
+    }
+    c.hblk_total = hp;
+    c.psd_mat_total = mp;
+    c.psd_lam_total = lp;
+    c.nu = (double)c.nonneg_dim + (double)c.nsoc + 3.0 * (double)c.nsym + psd_deg;
+    TRY(upload(c, &c.soc_off, d->soc_off, c.nsoc));
+    TRY(upload(c, &c.soc_dim, d->soc_dim, c.nsoc));
+    TRY(upload(c, &c.soc_hptr, soc_h.data(), c.nsoc));
+    TRY(upload(c, &c.exp_off, d->exp_off, c.nexp));
+    TRY(upload(c, &c.pow_off, d->pow_off, c.npow));
+    TRY(upload(c, &c.pow_alpha, d->pow_alpha, c.npow));
+    TRY(upload(c, &c.psd_off, d->psd_off, c.npsd));
+    TRY(upload(c, &c.psd_side, d->psd_side, c.npsd));
+    TRY(upload(c, &c.psd_mptr, psd_m.data(), c.npsd));
+    TRY(upload(c, &c.psd_lptr, psd_l.data(), c.npsd));
+    TRY(upload(c, &c.psd_hptr, psd_h.data(), c.npsd));
+
+    // problem patterns (+ transpose of A)
+    TRY(upload(c, &c.p_rp, d->p_rowptr, c.n + 1));
+    TRY(upload(c, &c.p_ci, d->p_colidx, c.p_nnz));
+    TRY(dalloc(c, &c.p_v, c.p_nnz));
+    TRY(upload(c, &c.a_rp, d->a_rowptr, c.m + 1));
+    TRY(upload(c, &c.a_ci, d->a_colidx, c.a_nnz));
+    TRY(dalloc(c, &c.a_v, c.a_nnz));
+    {
+        std::vector<int64_t> trp(c.n + 1, 0), tci(c.a_nnz), tsrc(c.a_nnz);
+        for (int64_t p = 0; p < c.a_nnz; ++p) trp[d->a_colidx[p] + 1]++;
+        for (int64_t j = 0; j < c.n; ++j) trp[j + 1] += trp[j];
+        std::vector<int64_t> fill(trp.begin(), trp.end() - 1);
+        for (int64_t r = 0; r < c.m; ++r)
+            for (int64_t p = d->a_rowptr[r]; p < d->a_rowptr[r + 1]; ++p) {
+                int64_t t = fill[d->a_colidx[p]]++;
+                tci[t] = r;
+                tsrc[t] = p;
+            }
+        TRY(upload(c, &c.at_rp, trp.data(), c.n + 1));
+        TRY(upload(c, &c.at_ci, tci.data(), c.a_nnz));
+        TRY(upload(c, &c.at_src, tsrc.data(), c.a_nnz));
+        TRY(dalloc(c, &c.at_v, c.a_nnz));
+    }
+    TRY(dalloc(c, &c.q, c.n));
+    TRY(dalloc(c, &c.b, c.m));
+    TRY(dalloc(c, &c.dr, c.m));
+    TRY(dalloc(c, &c.dc, c.n));
+
+    // iterate / work
+    TRY(dalloc(c, &c.x, c.n));
+    TRY(dalloc(c, &c.z, c.m));
+    TRY(dalloc(c, &c.s, c.m));
+    TRY(dalloc(c, &c.bx, c.n));
+    TRY(dalloc(c, &c.bz, c.m));
+    TRY(dalloc(c, &c.bs, c.m));
+    TRY(dalloc(c, &c.gx, c.n));
+    TRY(dalloc(c, &c.gz, c.m));
+    for (int k = 0; k < 2; ++k) {
+        TRY(dalloc(c, &c.dx[k], c.n));
+        TRY(dalloc(c, &c.dz[k], c.m));
+        TRY(dalloc(c, &c.ds[k], c.m));
+    }
+    TRY(dalloc(c, &c.col2, c.dim));
+    TRY(dalloc(c, &c.sol1, c.dim));
+    TRY(dalloc(c, &c.dsc, c.m));
+    TRY(dalloc(c, &c.wn, c.n));
+    TRY(dalloc(c, &c.wn2, c.n));
+    TRY(dalloc(c, &c.wm, c.m));
+    TRY(dalloc(c, &c.hv, c.hblk_total));
+
+    // scaling state
+    TRY(dalloc(c, &c.nn_h, c.nonneg_dim));
+    TRY(dalloc(c, &c.nn_w, c.nonneg_dim));
+    TRY(dalloc(c, &c.nn_lam, c.nonneg_dim));
+    TRY(dalloc(c, &c.soc_w, c.soc_rows));
+    TRY(dalloc(c, &c.soc_lam, c.soc_rows));
+    TRY(dalloc(c, &c.soc_eta, c.nsoc));
+    TRY(dalloc(c, &c.ns_h, 9 * c.nsym));
+    TRY(dalloc(c, &c.ns_grad, 3 * c.nsym));
+    TRY(dalloc(c, &c.ns_hess, 9 * c.nsym));
+    TRY(dalloc(c, &c.ns_zt, 3 * c.nsym));
+    TRY(dalloc(c, &c.psd_r, c.psd_mat_total));
+    TRY(dalloc(c, &c.psd_rinv, c.psd_mat_total));
+    TRY(dalloc(c, &c.psd_q, c.psd_mat_total));
+    TRY(dalloc(c, &c.psd_lam, c.psd_lam_total));
+
+    // symbolic -> device
+    const Symbolic& S = symh->s;
+    if (S.dim != c.dim) {
+        cipm_ctx_destroy(h);
+        return CIPM_E_DIM;
+    }
+    c.host_sym = S;
+    c.sym.nsuper = S.nsuper;
+    c.sym.nnz_storage = S.nnz_storage;
+    TRY(upload(c, &c.sym.perm, S.perm.data(), c.dim));
+    TRY(upload(c, &c.sym.sn_col, S.sn_col.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.sn_rptr, S.sn_rptr.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.sn_rows, S.sn_rows.data(), (int64_t)S.sn_rows.size()));
+    TRY(upload(c, &c.sym.sn_loff, S.sn_loff.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.sn_parent, S.sn_parent.data(), S.nsuper));
+    TRY(upload(c, &c.sym.sn_nchild, S.sn_nchild.data(), S.nsuper));
+    TRY(upload(c, &c.sym.upd_ptr, S.upd_ptr.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.upd_src, S.upd_src.data(), (int64_t)S.upd_src.size()));
+    TRY(upload(c, &c.sym.upd_p0, S.upd_p0.data(), (int64_t)S.upd_p0.size()));
+    TRY(upload(c, &c.sym.upd_p1, S.upd_p1.data(), (int64_t)S.upd_p1.size()));
+    TRY(upload(c, &c.sym.order, S.order.data(), S.nsuper));
+    TRY(upload(c, &c.sym.sign, S.sign.data(), c.dim));
+    TRY(upload(c, &c.sym.map_p, S.map_p.data(), (int64_t)S.map_p.size()));
+    TRY(upload(c, &c.sym.map_a, S.map_a.data(), (int64_t)S.map_a.size()));
+    TRY(upload(c, &c.sym.map_diag, S.map_diag.data(), c.dim));
+    TRY(upload(c, &c.sym.map_hblk, S.map_hblk.data(), (int64_t)S.map_hblk.size()));
+    if ((int64_t)S.map_hblk.size() != c.hblk_total) {
+        fprintf(stderr, "[cipm] H block map size mismatch (%zu vs %lld)\n", S.map_hblk.size(),
+                (long long)c.hblk_total);
+        cipm_ctx_destroy(h);
+        return CIPM_E_DIM;
+    }
+    const size_t es = c.precision == CIPM_FULL ? sizeof(double) : sizeof(float);
+    {
+        void* p = nullptr;
+        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(S.nnz_storage, 1)));
+        c.allocations.push_back(p);
+        c.lval = p;
+        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(S.nnz_storage, 1)));
+        c.allocations.push_back(p);
+        c.lbase = p;
+        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(c.dim, 1)));
+        c.allocations.push_back(p);
+        c.dvec = p;
+        CIPM_CUDA(cudaMalloc(&p, es * 2 * std::max<int64_t>(c.dim, 1)));
+        c.allocations.push_back(p);
+        c.rt = p;
+    }
+    TRY(dalloc(c, &c.fac_count, S.nsuper));
+    TRY(dalloc(c, &c.bwd_done, S.nsuper));
+    TRY(dalloc(c, &c.tickets, 4));
+    TRY(dalloc(c, &c.sn_maxd, S.nsuper));
+    TRY(dalloc(c, &c.bumps, 1));
+    TRY(dalloc(c, &c.rb, 2 * c.dim));
+    TRY(dalloc(c, &c.rx, 2 * c.dim));
+    TRY(dalloc(c, &c.rr, 2 * c.dim));
+    TRY(dalloc(c, &c.rbest, 2 * c.dim));
+    TRY(dalloc(c, &c.rstate, 16));
+    TRY(dalloc(c, &c.partials, (int64_t)kMaxRedBlocks * 16));
+    TRY(dalloc(c, &c.counter, 1));
+    TRY(dalloc(c, &c.sc, CIPM_SC_COUNT));
+    TRY(dalloc(c, &c.err, 1));
+    TRY(dalloc(c, &c.nb, 64));
+    TRY(dalloc(c, &c.mask, 4));
+    CIPM_CUDA(cudaMallocHost((void**)&c.h_sc, sizeof(double) * CIPM_SC_COUNT));
+    CIPM_CUDA(cudaMallocHost((void**)&c.h_err, sizeof(int)));
+    CIPM_CUDA(cudaMallocHost((void**)&c.h_rstate, sizeof(double) * 16));
+    for (int i = 0; i < 4; ++i) CIPM_CUDA(cudaEventCreate(&c.ev[i]));
+    c.factor_blocks = factor_grid(c);
+    c.solve_blocks = solve_grid(c);
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    *out = h;
+#undef TRY
+    return CIPM_OK;
+}
+
+int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const double* q, const double* b,
+                        const double* dr, const double* dc, double c_obj) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    if (c.p_nnz) CIPM_CUDA(cudaMemcpyAsync(c.p_v, pv, sizeof(double) * c.p_nnz, cudaMemcpyHostToDevice, c.stream));
+    if (c.a_nnz) {
+        CIPM_CUDA(cudaMemcpyAsync(c.a_v, av, sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice, c.stream));
+        std::vector<int64_t> src(c.a_nnz);
+        CIPM_CUDA(cudaMemcpy(src.data(), c.at_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyDeviceToHost));
+        std::vector<double> tv(c.a_nnz);
+        for (int64_t t = 0; t < c.a_nnz; ++t) tv[t] = av[src[t]];
+        CIPM_CUDA(cudaMemcpy(c.at_v, tv.data(), sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice));
+    }
+    CIPM_CUDA(cudaMemcpyAsync(c.q, q, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.b, b, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.dr, dr, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.dc, dc, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+    c.c_obj = c_obj;
+    k_build_base(c);
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    return CIPM_OK;
+}
+
+void cipm_ctx_destroy(cipm_ctx* h) {
+    if (!h) return;
+    Ctx& c = h->c;
+    cudaSetDevice(c.device);
+    if (c.stream) cudaStreamSynchronize(c.stream);
+    for (void* p : c.allocations) cudaFree(p);
+    if (c.h_sc) cudaFreeHost(c.h_sc);
+    if (c.h_err) cudaFreeHost(c.h_err);
+    if (c.h_rstate) cudaFreeHost(c.h_rstate);
+    for (int i = 0; i < 4; ++i)
+        if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+    if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
+    delete h;
+}
+
+int cipm_sync(cipm_ctx* h) {
+    if (!h) return CIPM_E_ARG;
+    return sync_err(h->c);
+}
+
+int cipm_device_bytes(const cipm_ctx* h, int64_t* bytes) {
+    if (!h || !bytes) return CIPM_E_ARG;
+    size_t f = 0, t = 0;
+    cudaMemGetInfo(&f, &t);
+    *bytes = (int64_t)(t - f);
+    return CIPM_OK;
+}
+
+int cipm_init_iterate(cipm_ctx* h) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    k_init_iterate(c);
+    return read_sc(c);
+}
+
+int cipm_residuals(cipm_ctx* h, double* out) {
+    Ctx& c = h->c;
+    k_residuals(c);
+    int e = read_sc(c);
+    if (out) memcpy(out, c.h_sc, sizeof(double) * CIPM_SC_COUNT);
+    return e;
+}
+
+int cipm_save_best(cipm_ctx* h) {
+    k_copy_best(h->c);
+    return CIPM_OK;
+}
+
+int cipm_update_scaling(cipm_ctx* h) {
+    k_update_scaling(h->c);
+    return CIPM_OK;
+}
+
+int cipm_factor(cipm_ctx* h) {
+    Ctx& c = h->c;
+    k_assemble(c);
+    return k_factor(c);
+}
+
+int cipm_solve_affine(cipm_ctx* h, int* steps) {
+    Ctx& c = h->c;
+    k_affine_rhs(c);
+    int e = refine(c, 2, steps);
+    if (e) return e;
+    k_copy(c, c.rbest, c.col2, c.dim);
+    k_copy(c, c.rbest + c.dim, c.sol1, c.dim);
+    k_directions_prep_den(c);
+    k_recover_direction(c, 0, c.sol1, 0.0);
+    return CIPM_OK;
+}
+
+int cipm_step_affine(cipm_ctx* h) { return step_length(h->c, 0); }
+
+int cipm_solve_combined(cipm_ctx* h, int* steps) {
+    Ctx& c = h->c;
+    k_combined_ds(c, c.dz[0], c.ds[0]);
+    k_combined_rhs(c);
+    int e = refine(c, 1, steps);
+    if (e) return e;
+    k_copy(c, c.rbest, c.sol1, c.dim);
+    k_recover_direction(c, 1, c.sol1, 0.0);
+    return CIPM_OK;
+}
+
+int cipm_step_combined(cipm_ctx* h, double* alpha) {
+    Ctx& c = h->c;
+    int e = step_length(c, 1);
+    if (e) return e;
+    const int nk = 8;
+    for (int g0 = 0; g0 < 4096; g0 += nk) {
+        k_mu_candidates(c, g0, nk);
+        k_neighborhood_mask(c, g0, nk);
+        k_nb_resolve(c, g0, nk);
+        e = read_sc(c);
+        if (e) return e;
+        if (c.h_sc[CIPM_SC_T7] == 0.0) break;
+    }
+    if (alpha) *alpha = c.h_sc[CIPM_SC_ALPHA_FINAL];
+    return CIPM_OK;
+}
+
+int cipm_take_step(cipm_ctx* h) {
+    Ctx& c = h->c;
+    k_take_step(c);
+    return read_sc(c);
+}
+
+int cipm_read_scalars(cipm_ctx* h, double* out) {
+    int e = read_sc(h->c);
+    if (out) memcpy(out, h->c.h_sc, sizeof(double) * CIPM_SC_COUNT);
+    return e;
+}
+
+int cipm_get_iterate(cipm_ctx* h, int which, double* x, double* z, double* s, double* tkm) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    const double* px = which ? c.bx : c.x;
+    const double* pz = which ? c.bz : c.z;
+    const double* ps = which ? c.bs : c.s;
+    if (x) CIPM_CUDA(cudaMemcpy(x, px, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (z) CIPM_CUDA(cudaMemcpy(z, pz, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (s) CIPM_CUDA(cudaMemcpy(s, ps, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (tkm) {
+        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        tkm[0] = c.h_sc[CIPM_SC_TAU];
+        tkm[1] = c.h_sc[CIPM_SC_KAPPA];
+        tkm[2] = c.h_sc[CIPM_SC_MU];
+    }
+    return CIPM_OK;
+}
+
+int cipm_set_iterate(cipm_ctx* h, const double* x, const double* z, const double* s, const double* tkm) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (x) CIPM_CUDA(cudaMemcpy(c.x, x, sizeof(double) * c.n, cudaMemcpyHostToDevice));
+    if (z) CIPM_CUDA(cudaMemcpy(c.z, z, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (s) CIPM_CUDA(cudaMemcpy(c.s, s, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (tkm) {
+        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        c.h_sc[CIPM_SC_TAU] = tkm[0];
+        c.h_sc[CIPM_SC_KAPPA] = tkm[1];
+        c.h_sc[CIPM_SC_MU] = tkm[2];
+        CIPM_CUDA(cudaMemcpy(c.sc, c.h_sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyHostToDevice));
+    }
+    return CIPM_OK;
+}
+
+int cipm_kkt_solve(cipm_ctx* h, const double* rhs, double* x, int* steps, double* residual) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaMemcpyAsync(c.rb, rhs, sizeof(double) * c.dim, cudaMemcpyHostToDevice, c.stream));
+    int e = refine(c, 1, steps);
+    if (e) return e;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(cudaMemcpy(x, c.rbest, sizeof(double) * c.dim, cudaMemcpyDeviceToHost));
+    if (residual) *residual = c.h_rstate[7];
+    return CIPM_OK;
+}
+
+int cipm_apply_h(cipm_ctx* h, const double* v, double* out) {
+    Ctx& c = h->c;
+    double *dv = nullptr, *dout = nullptr;
+    CIPM_CUDA(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(c.m, 1)));
+    CIPM_CUDA(cudaMalloc(&dout, sizeof(double) * std::max<int64_t>(c.m, 1)));
+    CIPM_CUDA(cudaMemcpy(dv, v, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    k_apply_h(c, dv, dout, 0.0, nullptr, 1.0);
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(cudaMemcpy(out, dout, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    cudaFree(dv);
+    cudaFree(dout);
+    return *c.h_err;
+}
+
+int cipm_scaling_values(cipm_ctx* h, double* diag, double* blocks) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (diag) {
+        std::vector<double> tmp(c.lin, 0.0);
+        if (c.nonneg_dim)
+            CIPM_CUDA(cudaMemcpy(tmp.data() + c.zero_dim, c.nn_h, sizeof(double) * c.nonneg_dim,
+                                 cudaMemcpyDeviceToHost));
+        memcpy(diag, tmp.data(), sizeof(double) * c.lin);
+    }
+    if (blocks && c.hblk_total) CIPM_CUDA(cudaMemcpy(blocks, c.hv, sizeof(double) * c.hblk_total, cudaMemcpyDeviceToHost));
+    return sync_err(c);
+}
+
+int cipm_get_direction(cipm_ctx* h, int combined, double* dx, double* dz, double* ds, double* dtk) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    const int w = combined ? 1 : 0;
+    if (dx) CIPM_CUDA(cudaMemcpy(dx, c.dx[w], sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (dz) CIPM_CUDA(cudaMemcpy(dz, c.dz[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (ds) CIPM_CUDA(cudaMemcpy(ds, c.ds[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (dtk) {
+        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        dtk[0] = c.h_sc[w ? CIPM_SC_DTAU_C : CIPM_SC_DTAU_A];
+        dtk[1] = c.h_sc[w ? CIPM_SC_DKAPPA_C : CIPM_SC_DKAPPA_A];
+    }
+    return CIPM_OK;
+}
+
+int cipm_get_vector(cipm_ctx* h, const char* name, double* out, int64_t* count) {
+    Ctx& c = h->c;
+    std::string nm(name ? name : "");
+    const double* src = nullptr;
+    int64_t cnt = 0;
+    if (nm == "x") { src = c.x; cnt = c.n; }
+    else if (nm == "z") { src = c.z; cnt = c.m; }
+    else if (nm == "s") { src = c.s; cnt = c.m; }
+    else if (nm == "gx") { src = c.gx; cnt = c.n; }
+    else if (nm == "gz") { src = c.gz; cnt = c.m; }
+    else if (nm == "dsc") { src = c.dsc; cnt = c.m; }
+    else if (nm == "col2") { src = c.col2; cnt = c.dim; }
+    else if (nm == "sol1") { src = c.sol1; cnt = c.dim; }
+    else if (nm == "nn_h") { src = c.nn_h; cnt = c.nonneg_dim; }
+    else if (nm == "hv") { src = c.hv; cnt = c.hblk_total; }
+    else return CIPM_E_ARG;
+    if (count) *count = cnt;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (out && cnt) CIPM_CUDA(cudaMemcpy(out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    return CIPM_OK;
+}
+
+int cipm_soc_residuals(cipm_ctx* h, const double* x, double* out) {
+    Ctx& c = h->c;
+    double *dx = nullptr, *dout = nullptr;
+    CIPM_CUDA(cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(c.m, 1)));
+    CIPM_CUDA(cudaMalloc(&dout, sizeof(double) * std::max<int64_t>(c.nsoc, 1)));
+    CIPM_CUDA(cudaMemcpy(dx, x, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    k_soc_residuals(c, dx, dout);
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.nsoc) CIPM_CUDA(cudaMemcpy(out, dout, sizeof(double) * c.nsoc, cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dout);
+    return CIPM_OK;
+}
+
+int cipm_launch_count(cipm_ctx* h, int64_t* count, int reset) {
+    if (count) *count = h->c.launches;
+    if (reset) h->c.launches = 0;
+    return CIPM_OK;
+}
+
+int cipm_kernel_times(cipm_ctx* h, double* factor_ms, double* solve_ms) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, c.ev[0], c.ev[1]) != cudaSuccess) a = -1.f;
+    if (cudaEventElapsedTime(&b, c.ev[2], c.ev[3]) != cudaSuccess) b = -1.f;
+    cudaGetLastError();
+    if (factor_ms) *factor_ms = a;
+    if (solve_ms) *solve_ms = b;
+    return CIPM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Shared device-side definitions for libcipm (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/cipm.h"
+
+namespace cipm {
+
+constexpr int kThreads = 256;
+constexpr int kMaxRedBlocks = 1184;     // 148 SMs x 8 — fixed grid => deterministic reductions
+constexpr double kMinStep = 1e-11;
+
+#define CIPM_CUDA(call)                                                              \
+    do {                                                                             \
+        cudaError_t e__ = (call);                                                    \
+        if (e__ != cudaSuccess) {                                                    \
+            fprintf(stderr, "[cipm] CUDA error %s at %s:%d: %s\n", #call, __FILE__, \
+                    __LINE__, cudaGetErrorString(e__));                              \
+            return CIPM_E_CUDA;                                                      \
+        }                                                                            \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device scalar block: every per-iteration scalar lives here (no host round
+// trip unless the host needs a decision).  Field order is part of the ABI of
+// cipm_read_scalars() (see include/cipm.h CIPM_SC_*).
+// ---------------------------------------------------------------------------
+struct Scalars {
+    double v[CIPM_SC_COUNT];
+};
+
+// ordered min on non-negative doubles (bit pattern is monotone)
+__device__ __forceinline__ void atomic_min_pos(double* addr, double val) {
+    if (!(val >= 0.0)) val = 0.0;   // NaN / negative -> 0 (forces StepTooSmall)
+    atomicMin(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(val));
+}
+
+__device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
+
+// ---------------------------------------------------------------------------
+// deterministic multi-value reduction: each block writes K partials, the last
+// block to arrive combines them in block order (fixed grid => bitwise
+// reproducible), then calls the finaliser.
+// ---------------------------------------------------------------------------
+enum RedOp { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
+
+template <int K>
+struct RedSpec {
+    int op[K];
+};
+
+__device__ __forceinline__ double red_apply(int op, double a, double b) {
+    if (op == RED_SUM) return a + b;
+    if (op == RED_MAX) return fmax(a, b);
+    return fmin(a, b);
+}
+
+__device__ __forceinline__ double red_identity(int op) {
+    if (op == RED_SUM) return 0.0;
+    if (op == RED_MAX) return -INFINITY;
+    return INFINITY;
+}
+
+// block reduce K values held per thread into lane 0 of warp 0; returns true on thread 0
+template <int K>
+__device__ __forceinline__ void block_reduce(double (&vals)[K], const int (&ops)[K], double* smem) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double v = vals[k];
+        for (int o = 16; o > 0; o >>= 1) v = red_apply(ops[k], v, __shfl_down_sync(0xffffffffu, v, o));
+        if (lane == 0) smem[warp * K + k] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double v = lane < nw ? smem[lane * K + k] : red_identity(ops[k]);
+            for (int o = 16; o > 0; o >>= 1) v = red_apply(ops[k], v, __shfl_down_sync(0xffffffffu, v, o));
+            vals[k] = v;
+        }
+    }
+    __syncthreads();
+}
+
+// Write block partials; the last block combines.  Returns true (on thread 0 of
+// the last block) with `out` holding the grid-wide result.
+template <int K>
+__device__ bool grid_reduce(double (&vals)[K], const int (&ops)[K], double* partials,
+                            unsigned int* counter, double (&out)[K]) {
+    __shared__ double smem[32 * K];
+    __shared__ bool last;
+    block_reduce<K>(vals, ops, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) partials[blockIdx.x * K + k] = vals[k];
+        __threadfence();
+        unsigned int t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    if (threadIdx.x == 0) {
+        __threadfence();
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double acc = red_identity(ops[k]);
+            for (unsigned int b = 0; b < gridDim.x; ++b)
+                acc = red_apply(ops[k], acc, __ldcg(partials + b * K + k));
+            out[k] = acc;
+        }
+        *counter = 0u;
+        return true;
+    }
+    return false;
+}
+
+inline int red_grid(int64_t n) {
+    int64_t b = (n + kThreads - 1) / kThreads;
+    if (b < 1) b = 1;
+    if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+    return (int)b;
+}
+
+inline int grid_for(int64_t n, int threads = kThreads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > (1 << 30)) b = 1 << 30;
+    return (int)b;
+}
+
+}  // namespace cipm

@@ -1,0 +1,165 @@
+// Device-resident state of one problem instance (one cipm_ctx).
+//
+// HBM layout (structure of arrays, one flat buffer per field):
+//   problem   P (CSR full), A (CSR), A' (CSR of the transpose), q, b, Dr, Dc
+//   iterate   x (n), z (m), s (m), best copies, G rows, directions
+//   scaling   nonneg h/w/λ (nnd); SOC w/λ (rows), η (cones);
+//             exp/pow H(9)/∇f(3)/∇²f(9)/z̃(3) per cone; PSD R/R⁻¹/Q (side²), λ (side)
+//   factor    supernodal panels (T = double | float), base image, D, schedule
+//   scalars   Scalars block + error word + reduction partials
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "symbolic.hpp"
+
+namespace cipm {
+
+struct DevSymbolic {
+    int32_t nsuper = 0;
+    int32_t* perm = nullptr;        // dim: permuted position -> original index
+    int32_t* sn_col = nullptr;      // nsuper+1
+    int64_t* sn_rptr = nullptr;     // nsuper+1
+    int32_t* sn_rows = nullptr;
+    int64_t* sn_loff = nullptr;     // nsuper+1
+    int32_t* sn_parent = nullptr;
+    int32_t* sn_nchild = nullptr;
+    int64_t* upd_ptr = nullptr;
+    int32_t* upd_src = nullptr;
+    int32_t* upd_p0 = nullptr;
+    int32_t* upd_p1 = nullptr;
+    int32_t* order = nullptr;
+    int8_t* sign = nullptr;         // permuted order
+    int64_t* map_p = nullptr;
+    int64_t* map_a = nullptr;
+    int64_t* map_diag = nullptr;
+    int64_t* map_hblk = nullptr;
+    int64_t nnz_storage = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t n = 0, m = 0, dim = 0;
+    int precision = CIPM_FULL;
+    double delta_s = 1e-8, delta_d = 0.0, beta = 1e-6, backtrack = 0.8, step_scale = 0.99;
+    double refine_abs = 1e-12, refine_rel = 1e-12;
+    int refine_max = 10;
+    int64_t zero_dim = 0, nonneg_dim = 0, lin = 0;
+    int64_t nsoc = 0, nexp = 0, npow = 0, npsd = 0, soc_rows = 0, nsym = 0;
+    int64_t psd_mat_total = 0, psd_lam_total = 0, hblk_total = 0;
+    int psd_max_side = 0;
+    double nu = 0.0;                 // barrier degree
+    double c_obj = 1.0;
+    int64_t p_nnz = 0, a_nnz = 0;
+
+    // cone tables
+    int32_t *soc_off = nullptr, *soc_dim = nullptr;      // row offsets (z coordinates)
+    int64_t* soc_hptr = nullptr;                         // into map_hblk per SOC
+    int32_t* exp_off = nullptr;
+    int32_t* pow_off = nullptr;
+    double* pow_alpha = nullptr;
+    int32_t *psd_off = nullptr, *psd_side = nullptr;
+    int64_t *psd_mptr = nullptr, *psd_lptr = nullptr, *psd_hptr = nullptr;
+    int64_t nsym_hbase = 0;                              // map_hblk base of exp/pow blocks
+
+    // problem data (scaled)
+    int64_t *p_rp = nullptr, *p_ci = nullptr;
+    double* p_v = nullptr;
+    int64_t *a_rp = nullptr, *a_ci = nullptr;
+    double* a_v = nullptr;
+    int64_t *at_rp = nullptr, *at_ci = nullptr, *at_src = nullptr;
+    double* at_v = nullptr;
+    double *q = nullptr, *b = nullptr, *dr = nullptr, *dc = nullptr;
+
+    // iterate and work vectors
+    double *x = nullptr, *z = nullptr, *s = nullptr;
+    double *bx = nullptr, *bz = nullptr, *bs = nullptr;
+    double best_tkm[3] = {0, 0, 0};
+    double *gx = nullptr, *gz = nullptr;
+    double *dx[2] = {nullptr, nullptr}, *dz[2] = {nullptr, nullptr}, *ds[2] = {nullptr, nullptr};
+    double *col2 = nullptr, *sol1 = nullptr;             // dim each ([x; z] order)
+    double* dsc = nullptr;                               // combined d_s (m)
+    double *wn = nullptr, *wn2 = nullptr;                // n-sized scratch
+    double* wm = nullptr;                                // m-sized scratch
+    double* hv = nullptr;                                // upper triangles of every dense H block
+
+    // scaling state
+    double *nn_h = nullptr, *nn_w = nullptr, *nn_lam = nullptr;
+    double *soc_w = nullptr, *soc_lam = nullptr, *soc_eta = nullptr;
+    double *ns_h = nullptr, *ns_grad = nullptr, *ns_hess = nullptr, *ns_zt = nullptr;
+    double *psd_r = nullptr, *psd_rinv = nullptr, *psd_q = nullptr, *psd_lam = nullptr;
+
+    // factor
+    Symbolic host_sym;               // copy kept for stats / host-side checks
+    DevSymbolic sym;
+    void* lval = nullptr;            // panels (T)
+    void* lbase = nullptr;           // base image: P, A, static regularisation (T)
+    void* dvec = nullptr;            // D (T), permuted order
+    int32_t* fac_count = nullptr;    // children finished (factor / forward solve)
+    int32_t* bwd_done = nullptr;     // backward solve completion flags
+    int32_t* tickets = nullptr;      // [0] factor, [1] forward, [2] backward
+    double* sn_maxd = nullptr;       // subtree max |D|
+    int32_t* bumps = nullptr;
+    int factor_blocks = 0, solve_blocks = 0;
+
+    // refinement (up to 2 right-hand sides, [rhs][dim])
+    double *rb = nullptr, *rx = nullptr, *rr = nullptr, *rbest = nullptr;
+    void* rt = nullptr;              // permuted work vector (T)
+    double* rstate = nullptr;        // per rhs: best, prev, ups, target, done, improved, steps, resid
+    int32_t* rflags = nullptr;       // per rhs: active (host-visible via rstate)
+
+    // reductions / scalars
+    double* partials = nullptr;
+    unsigned int* counter = nullptr;
+    double* sc = nullptr;            // CIPM_SC_COUNT doubles
+    int* err = nullptr;
+    double* nb = nullptr;            // neighbourhood sums [2][32]
+    unsigned int* mask = nullptr;    // candidate masks
+    double* h_sc = nullptr;          // pinned host copy of sc
+    int* h_err = nullptr;
+    double* h_rstate = nullptr;
+
+    int64_t launches = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float factor_ms = 0.f, solve_ms = 0.f;
+
+    std::vector<void*> allocations;
+};
+
+// ---- launchers (implemented in vec.cu / cones.cu / ldl.cu) ----
+// vec.cu
+void k_init_iterate(Ctx& c);
+void k_residuals(Ctx& c);
+void k_copy_best(Ctx& c);
+void k_directions_prep_den(Ctx& c);          // den of the τ-step (col2 fixed per iteration)
+void k_affine_rhs(Ctx& c);                   // rb[1] = [gx; -(gz - s)], rb[0] = [-q; b]
+void k_combined_rhs(Ctx& c);                 // rb[0] = [f gx; -(f gz - dsc)]
+void k_recover_direction(Ctx& c, int which, const double* sol, double dkappa_rhs_slot_is_combined);
+void k_take_step(Ctx& c);
+void k_step_init(Ctx& c, int which);         // α bound from τ/κ
+void k_step_finish(Ctx& c, int which);       // α check + σ
+void k_kkt_residual(Ctx& c, int nrhs, const int* active_host);
+void k_mu_candidates(Ctx& c, int k0, int nk);
+// cones.cu
+void k_update_scaling(Ctx& c);
+void k_scatter_h(Ctx& c);
+void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta);
+void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a);
+void k_step_bound(Ctx& c, const double* dz, const double* ds);
+void k_nsym_feasible_mask(Ctx& c, const double* dz, const double* ds, int k0);
+void k_neighborhood_mask(Ctx& c, int k0, int nk);
+void k_membership(Ctx& c);
+void k_soc_residuals(Ctx& c, const double* x, double* out);
+void k_scaling_values(Ctx& c, double* diag, double* blocks);
+// ldl.cu
+void k_build_base(Ctx& c);
+void k_assemble(Ctx& c);
+int k_factor(Ctx& c);
+void k_refine_step(Ctx& c, int nrhs, const int* active_host);
+
+}  // namespace cipm

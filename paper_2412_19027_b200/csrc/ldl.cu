@@ -1,0 +1,505 @@
+// Supernodal quasi-definite LDL' on sm_100a: numeric refactorisation and
+// triangular solves (replaces kkt/ldl.py:37-104 and kkt/system.py:246-271).
+//
+// Scheduling: one persistent launch per phase.  Tasks (supernodes) are handed
+// out by an atomic ticket in a fixed topological order (leaves first), and a
+// task spins on per-supernode dependency counters until its inputs are final.
+// A task only ever waits on tasks with smaller tickets, which are already held
+// by running CTAs/warps, so the scheme cannot deadlock; there is one launch per
+// factorisation / solve instead of one per elimination-tree level.
+//
+// Numerics: left-looking (fan-in).  Supernode J gathers the updates of every
+// descendant K listed in its update list in a fixed order, then factors its
+// dense panel.  No atomics touch floating-point data, so factors and solutions
+// are bitwise reproducible run to run (SPEC kkt-solver "Determinism").
+// Dynamic regularisation (ldl.py:79-87): a pivot with |d| < δs + δd·runmax is
+// replaced by ±bound with the sign of its block; runmax is the largest |D| in
+// the supernode's subtree computed so far (the sequential reference uses all
+// earlier pivots; δd = eps² makes the term negligible — DESIGN.md).
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+namespace cipm {
+
+namespace {
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) {
+    return __ldcg(p);
+}
+
+// ---------------------------------------------------------------------------
+// base image / assembly
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void scatter_vals(T* base, const int64_t* map, const double* vals, int64_t cnt) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    int64_t p = map[i];
+    if (p >= 0) base[p] = (T)vals[i];
+}
+
+template <typename T>
+__global__ void add_static_reg(T* base, const int64_t* map_diag, int64_t n, int64_t dim, double delta_s) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= dim) return;
+    T reg = (T)delta_s;
+    T sgn = i < n ? (T)1 : (T)-1;
+    base[map_diag[i]] = base[map_diag[i]] + sgn * reg;
+}
+
+// ---------------------------------------------------------------------------
+// numeric factorisation
+// ---------------------------------------------------------------------------
+
+struct FactorArgs {
+    int32_t nsuper;
+    const int32_t* order;
+    const int32_t* sn_col;
+    const int64_t* sn_rptr;
+    const int32_t* sn_rows;
+    const int64_t* sn_loff;
+    const int32_t* sn_parent;
+    const int32_t* sn_nchild;
+    const int64_t* upd_ptr;
+    const int32_t* upd_src;
+    const int32_t* upd_p0;
+    const int32_t* upd_p1;
+    const int8_t* sign;
+    int32_t* count;
+    int32_t* ticket;
+    double* maxd;
+    int32_t* bumps;
+    int* err;
+    double delta_s, delta_d;
+};
+
+constexpr int kRelCap = 2048;
+
+__device__ __forceinline__ int find_row(const int32_t* rows, int r, int32_t key) {
+    int lo = 0, hi = r;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (rows[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec) {
+    __shared__ int s_task;
+    __shared__ int s_rel[kRelCap];
+    __shared__ double s_piv;
+    __shared__ double s_runmax;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (;;) {
+        if (tid == 0) s_task = atomicAdd(a.ticket, 1);
+        __syncthreads();
+        const int t = s_task;
+        if (t >= a.nsuper) return;
+        const int J = a.order[t];
+        if (tid == 0) {
+            const int need = a.sn_nchild[J];
+            while (ld_acquire(a.count + J) < need) __nanosleep(100);
+        }
+        __syncthreads();
+
+        const int c0 = a.sn_col[J];
+        const int w = a.sn_col[J + 1] - c0;
+        const int64_t r0 = a.sn_rptr[J];
+        const int r = (int)(a.sn_rptr[J + 1] - r0);
+        const int32_t* rowsJ = a.sn_rows + r0;
+        T* L = lval + a.sn_loff[J];
+        double runmax = 0.0;
+
+        // 1. gather descendant updates in list order
+        for (int64_t u = a.upd_ptr[J]; u < a.upd_ptr[J + 1]; ++u) {
+            const int K = a.upd_src[u];
+            const int p0 = a.upd_p0[u], p1 = a.upd_p1[u];
+            const int kc0 = a.sn_col[K];
+            const int wK = a.sn_col[K + 1] - kc0;
+            const int64_t kr0 = a.sn_rptr[K];
+            const int rK = (int)(a.sn_rptr[K + 1] - kr0);
+            const int32_t* rowsK = a.sn_rows + kr0;
+            const T* LK = lval + a.sn_loff[K];
+            const T* DK = dvec + kc0;
+            const int nrow = rK - p0, ncol = p1 - p0;
+            runmax = fmax(runmax, ldcg(a.maxd + K));
+            const bool cached = nrow <= kRelCap;
+            if (cached)
+                for (int i = tid; i < nrow; i += nt) s_rel[i] = find_row(rowsJ, r, rowsK[p0 + i]);
+            __syncthreads();
+            const int64_t total = (int64_t)nrow * ncol;
+            for (int64_t idx = tid; idx < total; idx += nt) {
+                const int i = (int)(idx % nrow);
+                const int cc = (int)(idx / nrow);
+                if (i < cc) continue;
+                T acc = (T)0;
+                for (int k = 0; k < wK; ++k)
+                    acc += ldcg(LK + (int64_t)k * rK + p0 + i) * ldcg(DK + k) * ldcg(LK + (int64_t)k * rK + p0 + cc);
+                const int tr = cached ? s_rel[i] : find_row(rowsJ, r, rowsK[p0 + i]);
+                const int tc = rowsK[p0 + cc] - c0;
+                L[(int64_t)tc * r + tr] -= acc;
+            }
+            __syncthreads();
+        }
+
+        // 2. dense LDL' of the panel (right-looking inside the panel)
+        if (tid == 0) s_runmax = runmax;
+        __syncthreads();
+        for (int j = 0; j < w; ++j) {
+            if (tid == 0) {
+                double d = (double)L[(int64_t)j * r + j];
+                const double bound = a.delta_s + a.delta_d * s_runmax;
+                if (fabs(d) < bound) {
+                    d = a.sign[c0 + j] > 0 ? bound : -bound;
+                    atomicAdd(a.bumps, 1);
+                }
+                T dt = (T)d;
+                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+                dvec[c0 + j] = dt;
+                L[(int64_t)j * r + j] = (T)1;
+                s_piv = (double)dt;
+                s_runmax = fmax(s_runmax, fabs(d));
+            }
+            __syncthreads();
+            const T d = (T)s_piv;
+            T* Lj = L + (int64_t)j * r;
+            for (int i = j + 1 + tid; i < r; i += nt) Lj[i] = Lj[i] / d;
+            __syncthreads();
+            const int rem_c = w - j - 1;
+            if (rem_c > 0) {
+                const int64_t total = (int64_t)rem_c * (r - j - 1);
+                for (int64_t idx = tid; idx < total; idx += nt) {
+                    const int i = j + 1 + (int)(idx % (r - j - 1));
+                    const int c = j + 1 + (int)(idx / (r - j - 1));
+                    if (i < c) continue;
+                    L[(int64_t)c * r + i] -= Lj[i] * d * Lj[c];
+                }
+            }
+            __syncthreads();
+        }
+        // 3. publish
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            a.maxd[J] = s_runmax;
+            __threadfence();
+            const int P = a.sn_parent[J];
+            if (P >= 0) atomicAdd(a.count + P, 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// triangular solves, one warp per supernode task
+// ---------------------------------------------------------------------------
+
+struct SolveArgs {
+    int32_t nsuper;
+    int64_t dim;
+    const int32_t* order;
+    const int32_t* sn_col;
+    const int64_t* sn_rptr;
+    const int32_t* sn_rows;
+    const int64_t* sn_loff;
+    const int32_t* sn_parent;
+    const int32_t* sn_nchild;
+    const int64_t* upd_ptr;
+    const int32_t* upd_src;
+    const int32_t* upd_p0;
+    const int32_t* upd_p1;
+    int32_t* count;     // forward: children done; backward: done flags
+    int32_t* ticket;
+    int act0, act1;     // active right-hand sides
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.nsuper) return;
+        const int J = a.order[t];
+        if (lane == 0) {
+            const int need = a.sn_nchild[J];
+            while (ld_acquire(a.count + J) < need) __nanosleep(32);
+        }
+        __syncwarp();
+        const int c0 = a.sn_col[J];
+        const int w = a.sn_col[J + 1] - c0;
+        const int64_t r0 = a.sn_rptr[J];
+        const int r = (int)(a.sn_rptr[J + 1] - r0);
+        const T* L = lval + a.sn_loff[J];
+        for (int q = 0; q < 2; ++q) {
+            if (!(q == 0 ? a.act0 : a.act1)) continue;
+            T* xv = x + (int64_t)q * a.dim;
+            T* xJ = xv + c0;
+            for (int64_t u = a.upd_ptr[J]; u < a.upd_ptr[J + 1]; ++u) {
+                const int K = a.upd_src[u];
+                const int p0 = a.upd_p0[u], p1 = a.upd_p1[u];
+                const int kc0 = a.sn_col[K];
+                const int wK = a.sn_col[K + 1] - kc0;
+                const int64_t kr0 = a.sn_rptr[K];
+                const int rK = (int)(a.sn_rptr[K + 1] - kr0);
+                const T* LK = lval + a.sn_loff[K];
+                const int32_t* rowsK = a.sn_rows + kr0;
+                for (int c = p0 + lane; c < p1; c += 32) {
+                    T acc = (T)0;
+                    for (int k = 0; k < wK; ++k) acc += LK[(int64_t)k * rK + c] * __ldcg(xv + kc0 + k);
+                    xJ[rowsK[c] - c0] -= acc;
+                }
+                __syncwarp();
+            }
+            for (int j = 0; j < w; ++j) {
+                const T xj = xJ[j];
+                __syncwarp();
+                for (int i = j + 1 + lane; i < w; i += 32) xJ[i] -= L[(int64_t)j * r + i] * xj;
+                __syncwarp();
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            const int P = a.sn_parent[J];
+            if (P >= 0) atomicAdd(a.count + P, 1);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __restrict__ lval,
+                                                       const T* __restrict__ dvec, T* x) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.nsuper) return;
+        const int J = a.order[a.nsuper - 1 - t];
+        const int P = a.sn_parent[J];
+        if (lane == 0 && P >= 0)
+            while (ld_acquire(a.count + P) == 0) __nanosleep(32);
+        __syncwarp();
+        const int c0 = a.sn_col[J];
+        const int w = a.sn_col[J + 1] - c0;
+        const int64_t r0 = a.sn_rptr[J];
+        const int r = (int)(a.sn_rptr[J + 1] - r0);
+        const int32_t* rowsJ = a.sn_rows + r0;
+        const T* L = lval + a.sn_loff[J];
+        for (int q = 0; q < 2; ++q) {
+            if (!(q == 0 ? a.act0 : a.act1)) continue;
+            T* xv = x + (int64_t)q * a.dim;
+            T* xJ = xv + c0;
+            for (int j = lane; j < w; j += 32) xJ[j] = xJ[j] / dvec[c0 + j];   // D solve (ldl.py:101-102)
+            __syncwarp();
+            for (int j = 0; j < w; ++j) {
+                const T* Lj = L + (int64_t)j * r;
+                T acc = (T)0;
+                for (int i = w + lane; i < r; i += 32) acc += Lj[i] * __ldcg(xv + rowsJ[i]);
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+                if (lane == 0) xJ[j] -= acc;
+            }
+            __syncwarp();
+            for (int j = w - 1; j >= 0; --j) {
+                const T* Lj = L + (int64_t)j * r;
+                T acc = (T)0;
+                for (int i = j + 1 + lane; i < w; i += 32) acc += Lj[i] * xJ[i];
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+                if (lane == 0) xJ[j] -= acc;
+                __syncwarp();
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(a.count + J, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// refinement glue: permute / accumulate
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void gather_perm(const double* __restrict__ r, T* __restrict__ t, const int32_t* __restrict__ perm,
+                            int64_t dim, int act0, int act1) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= dim) return;
+    const int32_t p = perm[k];
+    if (act0) t[k] = (T)r[p];
+    if (act1) t[dim + k] = (T)r[dim + p];
+}
+
+template <typename T>
+__global__ void scatter_add_perm(double* __restrict__ x, const T* __restrict__ t, const int32_t* __restrict__ perm,
+                                 int64_t dim, int act0, int act1) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= dim) return;
+    const int32_t p = perm[k];
+    if (act0) x[p] = x[p] + (double)t[k];
+    if (act1) x[dim + p] = x[dim + p] + (double)t[dim + k];
+}
+
+SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1) {
+    SolveArgs a;
+    a.nsuper = c.sym.nsuper;
+    a.dim = c.dim;
+    a.order = c.sym.order;
+    a.sn_col = c.sym.sn_col;
+    a.sn_rptr = c.sym.sn_rptr;
+    a.sn_rows = c.sym.sn_rows;
+    a.sn_loff = c.sym.sn_loff;
+    a.sn_parent = c.sym.sn_parent;
+    a.sn_nchild = c.sym.sn_nchild;
+    a.upd_ptr = c.sym.upd_ptr;
+    a.upd_src = c.sym.upd_src;
+    a.upd_p0 = c.sym.upd_p0;
+    a.upd_p1 = c.sym.upd_p1;
+    a.count = count;
+    a.ticket = ticket;
+    a.act0 = act0;
+    a.act1 = act1;
+    return a;
+}
+
+template <typename T>
+void build_base_t(Ctx& c) {
+    T* base = (T*)c.lbase;
+    cudaMemsetAsync(base, 0, sizeof(T) * c.sym.nnz_storage, c.stream);
+    if (c.p_nnz) {
+        scatter_vals<T><<<grid_for(c.p_nnz), kThreads, 0, c.stream>>>(base, c.sym.map_p, c.p_v, c.p_nnz);
+        c.launches++;
+    }
+    if (c.a_nnz) {
+        scatter_vals<T><<<grid_for(c.a_nnz), kThreads, 0, c.stream>>>(base, c.sym.map_a, c.a_v, c.a_nnz);
+        c.launches++;
+    }
+    add_static_reg<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(base, c.sym.map_diag, c.n, c.dim, c.delta_s);
+    c.launches++;
+}
+
+template <typename T>
+int factor_t(Ctx& c) {
+    FactorArgs a;
+    a.nsuper = c.sym.nsuper;
+    a.order = c.sym.order;
+    a.sn_col = c.sym.sn_col;
+    a.sn_rptr = c.sym.sn_rptr;
+    a.sn_rows = c.sym.sn_rows;
+    a.sn_loff = c.sym.sn_loff;
+    a.sn_parent = c.sym.sn_parent;
+    a.sn_nchild = c.sym.sn_nchild;
+    a.upd_ptr = c.sym.upd_ptr;
+    a.upd_src = c.sym.upd_src;
+    a.upd_p0 = c.sym.upd_p0;
+    a.upd_p1 = c.sym.upd_p1;
+    a.sign = c.sym.sign;
+    a.count = c.fac_count;
+    a.ticket = c.tickets;
+    a.maxd = c.sn_maxd;
+    a.bumps = c.bumps;
+    a.err = c.err;
+    a.delta_s = c.delta_s;
+    a.delta_d = c.delta_d;
+    cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
+    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
+    cudaMemsetAsync(c.bumps, 0, sizeof(int32_t), c.stream);
+    cudaEventRecord(c.ev[0], c.stream);
+    factor_kernel<T><<<c.factor_blocks, 256, 0, c.stream>>>(a, (T*)c.lval, (T*)c.dvec);
+    cudaEventRecord(c.ev[1], c.stream);
+    c.launches++;
+    return CIPM_OK;
+}
+
+template <typename T>
+void refine_solve_t(Ctx& c, int act0, int act1) {
+    T* t = (T*)c.rt;
+    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1);
+    cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
+    cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
+    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
+    cudaEventRecord(c.ev[2], c.stream);
+    SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
+    forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t);
+    SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
+    backward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+    cudaEventRecord(c.ev[3], c.stream);
+    scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1);
+    c.launches += 4;
+}
+
+}  // namespace
+
+void k_build_base(Ctx& c) {
+    if (c.precision == CIPM_FULL) build_base_t<double>(c);
+    else build_base_t<float>(c);
+}
+
+void k_assemble(Ctx& c) {
+    const size_t es = c.precision == CIPM_FULL ? sizeof(double) : sizeof(float);
+    cudaMemcpyAsync(c.lval, c.lbase, es * c.sym.nnz_storage, cudaMemcpyDeviceToDevice, c.stream);
+    k_scatter_h(c);
+}
+
+int k_factor(Ctx& c) {
+    return c.precision == CIPM_FULL ? factor_t<double>(c) : factor_t<float>(c);
+}
+
+// one refinement correction: x += solve(r) for the active right-hand sides
+void k_refine_step(Ctx& c, int nrhs, const int* active) {
+    const int a0 = active[0], a1 = nrhs > 1 ? active[1] : 0;
+    if (c.precision == CIPM_FULL) refine_solve_t<double>(c, a0, a1);
+    else refine_solve_t<float>(c, a0, a1);
+}
+
+}  // namespace cipm
+
+namespace cipm {
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+int factor_grid(Ctx& c) {
+    int per = 0;
+    if (c.precision == CIPM_FULL)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<double>, 256, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<float>, 256, 0);
+    if (per < 1) per = 1;
+    int64_t g = (int64_t)sm_count() * per;
+    if (g > c.sym.nsuper) g = c.sym.nsuper;
+    return (int)(g < 1 ? 1 : g);
+}
+
+int solve_grid(Ctx& c) {
+    int per = 0;
+    if (c.precision == CIPM_FULL)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<double>, 256, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<float>, 256, 0);
+    if (per < 1) per = 1;
+    int64_t g = (int64_t)sm_count() * per;
+    int64_t need = (c.sym.nsuper + 7) / 8;
+    if (g > need) g = need;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace cipm

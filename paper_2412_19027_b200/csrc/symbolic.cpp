@@ -1,0 +1,429 @@
+// Host symbolic analysis for the supernodal LDL' (see symbolic.hpp).
+//
+// Ordering: the exact-external-degree greedy minimum degree of the reference
+// (kkt/ordering.py:15-53: explicit elimination graph, (degree, index) heap
+// order) so the elimination tree matches the CPU solver's; the permutation is
+// then postordered, which is an equivalent reordering (same fill, same tree).
+// A dense-tail shortcut keeps it fast: once the minimum-degree node touches
+// every remaining node, the remainder is a clique and the reference order of
+// a clique with equal degrees is ascending index.
+#include "symbolic.hpp"
+
+#include <algorithm>
+#include <functional>
+#include <numeric>
+#include <queue>
+#include <utility>
+
+namespace cipm {
+namespace {
+
+struct Graph {
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> idx;
+};
+
+// symmetric adjacency (no self loops, deduplicated) of the KKT pattern
+Graph kkt_graph(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const int64_t* arp,
+                const int64_t* aci, int64_t nblocks, const int64_t* boff, const int64_t* bdim) {
+    const int64_t dim = n + m;
+    std::vector<int64_t> deg(dim + 1, 0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = prp[i]; p < prp[i + 1]; ++p)
+            if (pci[p] != i) { deg[i]++; deg[pci[p]]++; }
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t p = arp[r]; p < arp[r + 1]; ++p) { deg[aci[p]]++; deg[n + r]++; }
+    for (int64_t b = 0; b < nblocks; ++b)
+        for (int64_t a = 0; a < bdim[b]; ++a) deg[n + boff[b] + a] += 2 * (bdim[b] - 1);
+    std::vector<int64_t> ptr(dim + 1, 0);
+    for (int64_t i = 0; i < dim; ++i) ptr[i + 1] = ptr[i] + deg[i];
+    std::vector<int32_t> idx(ptr[dim]);
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    auto add = [&](int64_t u, int64_t v) { idx[fill[u]++] = (int32_t)v; };
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = prp[i]; p < prp[i + 1]; ++p)
+            if (pci[p] != i) { add(i, pci[p]); add(pci[p], i); }
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t p = arp[r]; p < arp[r + 1]; ++p) { add(aci[p], n + r); add(n + r, aci[p]); }
+    for (int64_t b = 0; b < nblocks; ++b)
+        for (int64_t a = 0; a < bdim[b]; ++a)
+            for (int64_t c = 0; c < bdim[b]; ++c)
+                if (a != c) { add(n + boff[b] + a, n + boff[b] + c); add(n + boff[b] + c, n + boff[b] + a); }
+    Graph g;
+    g.ptr.assign(dim + 1, 0);
+    g.idx.reserve(idx.size());
+    for (int64_t i = 0; i < dim; ++i) {
+        auto b = idx.begin() + ptr[i], e = idx.begin() + ptr[i + 1];
+        std::sort(b, e);
+        auto u = std::unique(b, e);
+        g.idx.insert(g.idx.end(), b, u);
+        g.ptr[i + 1] = (int64_t)g.idx.size();
+    }
+    return g;
+}
+
+std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim) {
+    std::vector<std::vector<int32_t>> adj(dim);
+    for (int64_t i = 0; i < dim; ++i) adj[i].assign(g.idx.begin() + g.ptr[i], g.idx.begin() + g.ptr[i + 1]);
+    std::vector<char> alive(dim, 1);
+    std::vector<int64_t> mark(dim, -1);
+    using Item = std::pair<int64_t, int32_t>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int64_t i = 0; i < dim; ++i) heap.emplace((int64_t)adj[i].size(), (int32_t)i);
+    std::vector<int32_t> perm;
+    perm.reserve(dim);
+    std::vector<int32_t> nbrs;
+    int64_t remaining = dim, stamp = 0;
+    while ((int64_t)perm.size() < dim) {
+        Item it = heap.top();
+        heap.pop();
+        int32_t v = it.second;
+        if (!alive[v] || it.first != (int64_t)adj[v].size()) continue;
+        if (it.first == remaining - 1 && remaining > 2) {
+            // v touches every remaining node: after eliminating it the rest is a
+            // clique with equal degrees, eliminated in ascending index order.
+            perm.push_back(v);
+            alive[v] = 0;
+            for (int64_t i = 0; i < dim; ++i)
+                if (alive[i]) perm.push_back((int32_t)i);
+            break;
+        }
+        perm.push_back(v);
+        alive[v] = 0;
+        remaining--;
+        nbrs.clear();
+        for (int32_t u : adj[v])
+            if (alive[u]) nbrs.push_back(u);
+        for (int32_t u : nbrs) {
+            auto& au = adj[u];
+            for (size_t t = 0; t < au.size(); ++t)
+                if (au[t] == v) { au[t] = au.back(); au.pop_back(); break; }
+        }
+        for (size_t a = 0; a < nbrs.size(); ++a) {
+            int32_t u = nbrs[a];
+            ++stamp;
+            for (int32_t x : adj[u]) mark[x] = stamp;
+            for (size_t b = a + 1; b < nbrs.size(); ++b) {
+                int32_t w = nbrs[b];
+                if (mark[w] != stamp) {
+                    adj[u].push_back(w);
+                    adj[w].push_back(u);
+                }
+            }
+        }
+        for (int32_t u : nbrs) heap.emplace((int64_t)adj[u].size(), u);
+        std::vector<int32_t>().swap(adj[v]);
+    }
+    return perm;
+}
+
+// upper CSC of the permuted pattern: column c holds rows r < c
+void permuted_upper(const Graph& g, const std::vector<int32_t>& iperm, int64_t dim,
+                    std::vector<int64_t>& cp, std::vector<int32_t>& ci) {
+    cp.assign(dim + 1, 0);
+    for (int64_t i = 0; i < dim; ++i)
+        for (int64_t p = g.ptr[i]; p < g.ptr[i + 1]; ++p) {
+            int32_t pi = iperm[i], pj = iperm[g.idx[p]];
+            if (pi < pj) cp[pj + 1]++;
+        }
+    for (int64_t c = 0; c < dim; ++c) cp[c + 1] += cp[c];
+    ci.assign(cp[dim], 0);
+    std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
+    for (int64_t i = 0; i < dim; ++i)
+        for (int64_t p = g.ptr[i]; p < g.ptr[i + 1]; ++p) {
+            int32_t pi = iperm[i], pj = iperm[g.idx[p]];
+            if (pi < pj) ci[fill[pj]++] = pi;
+        }
+    for (int64_t c = 0; c < dim; ++c) std::sort(ci.begin() + cp[c], ci.begin() + cp[c + 1]);
+}
+
+std::vector<int32_t> etree(const std::vector<int64_t>& cp, const std::vector<int32_t>& ci, int64_t dim) {
+    std::vector<int32_t> parent(dim, -1), anc(dim, -1);
+    for (int64_t c = 0; c < dim; ++c) {
+        for (int64_t p = cp[c]; p < cp[c + 1]; ++p) {
+            int32_t r = ci[p];
+            while (r != -1 && r < c) {
+                int32_t next = anc[r];
+                anc[r] = (int32_t)c;
+                if (next == -1) { parent[r] = (int32_t)c; break; }
+                r = next;
+            }
+        }
+    }
+    return parent;
+}
+
+std::vector<int32_t> postorder(const std::vector<int32_t>& parent, int64_t dim) {
+    std::vector<int32_t> head(dim, -1), next(dim, -1);
+    for (int64_t j = dim - 1; j >= 0; --j) {       // children in ascending order
+        if (parent[j] == -1) continue;
+        next[j] = head[parent[j]];
+        head[parent[j]] = (int32_t)j;
+    }
+    std::vector<int32_t> post;
+    post.reserve(dim);
+    std::vector<int32_t> stack;
+    for (int64_t r = 0; r < dim; ++r) {
+        if (parent[r] != -1) continue;
+        stack.push_back((int32_t)r);
+        while (!stack.empty()) {
+            int32_t t = stack.back();
+            int32_t c = head[t];
+            if (c == -1) {
+                post.push_back(t);
+                stack.pop_back();
+            } else {
+                head[t] = next[c];
+                stack.push_back(c);
+            }
+        }
+    }
+    return post;
+}
+
+}  // namespace
+
+int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const int64_t* arp,
+            const int64_t* aci, int64_t lin, int64_t nblocks, const int64_t* boff, const int64_t* bdim,
+            const SymbolicOptions& opt, Symbolic& S) {
+    const int64_t dim = n + m;
+    S.n = n;
+    S.m = m;
+    S.dim = dim;
+    Graph g = kkt_graph(n, m, prp, pci, arp, aci, nblocks, boff, bdim);
+
+    std::vector<int32_t> perm;
+    if (opt.ordering == 1) {
+        perm.resize(dim);
+        std::iota(perm.begin(), perm.end(), 0);
+    } else {
+        perm = minimum_degree(g, dim);
+    }
+    S.md_perm = perm;
+    std::vector<int32_t> iperm(dim);
+    for (int64_t k = 0; k < dim; ++k) iperm[perm[k]] = (int32_t)k;
+
+    std::vector<int64_t> cp;
+    std::vector<int32_t> ci;
+    permuted_upper(g, iperm, dim, cp, ci);
+    std::vector<int32_t> parent = etree(cp, ci, dim);
+    std::vector<int32_t> post = postorder(parent, dim);
+    {
+        std::vector<int32_t> p2(dim);
+        for (int64_t k = 0; k < dim; ++k) p2[k] = perm[post[k]];
+        perm.swap(p2);
+        for (int64_t k = 0; k < dim; ++k) iperm[perm[k]] = (int32_t)k;
+        permuted_upper(g, iperm, dim, cp, ci);
+        parent = etree(cp, ci, dim);
+    }
+    S.perm = perm;
+    S.iperm = iperm;
+    S.sign.resize(dim);
+    for (int64_t k = 0; k < dim; ++k) S.sign[k] = perm[k] < n ? 1 : -1;
+
+    // column structures of L (strict lower), row-by-row reach through the etree
+    std::vector<int64_t> cnt(dim, 0);
+    std::vector<int32_t> flag(dim, -1);
+    for (int64_t j = 0; j < dim; ++j) {
+        flag[j] = (int32_t)j;
+        for (int64_t p = cp[j]; p < cp[j + 1]; ++p)
+            for (int32_t i = ci[p]; flag[i] != j; i = parent[i]) { cnt[i]++; flag[i] = (int32_t)j; }
+    }
+    std::vector<int64_t> lp(dim + 1, 0);
+    for (int64_t j = 0; j < dim; ++j) lp[j + 1] = lp[j] + cnt[j];
+    std::vector<int32_t> li(lp[dim]);
+    {
+        std::vector<int64_t> fill(lp.begin(), lp.end() - 1);
+        std::fill(flag.begin(), flag.end(), -1);
+        for (int64_t j = 0; j < dim; ++j) {
+            flag[j] = (int32_t)j;
+            for (int64_t p = cp[j]; p < cp[j + 1]; ++p)
+                for (int32_t i = ci[p]; flag[i] != j; i = parent[i]) { li[fill[i]++] = (int32_t)j; flag[i] = (int32_t)j; }
+        }
+    }
+    S.nnz_l = lp[dim];
+    S.flops = 0.0;
+    for (int64_t j = 0; j < dim; ++j) S.flops += 2.0 * (double)cnt[j] * (double)cnt[j];
+
+    // fundamental supernodes
+    std::vector<int32_t> nchild(dim, 0);
+    for (int64_t j = 0; j < dim; ++j)
+        if (parent[j] != -1) nchild[parent[j]]++;
+    std::vector<int32_t> fstart;
+    for (int64_t j = 0; j < dim; ++j) {
+        bool cont = j > 0 && parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && nchild[j] == 1;
+        if (!cont) fstart.push_back((int32_t)j);
+    }
+    const int64_t nf = (int64_t)fstart.size();
+    fstart.push_back((int32_t)dim);
+    std::vector<int32_t> fsn(dim);
+    for (int64_t s = 0; s < nf; ++s)
+        for (int32_t j = fstart[s]; j < fstart[s + 1]; ++j) fsn[j] = (int32_t)s;
+    std::vector<int32_t> fparent(nf, -1);
+    for (int64_t s = 0; s < nf; ++s) {
+        int32_t last = fstart[s + 1] - 1;
+        fparent[s] = parent[last] == -1 ? -1 : fsn[parent[last]];
+    }
+    // relaxed amalgamation, top-down with union-find representatives
+    std::vector<int32_t> rep(nf);
+    std::iota(rep.begin(), rep.end(), 0);
+    std::function<int32_t(int32_t)> find = [&](int32_t x) {
+        while (rep[x] != x) { rep[x] = rep[rep[x]]; x = rep[x]; }
+        return x;
+    };
+    std::vector<int64_t> first(nf), width(nf), offr(nf), truenz(nf);
+    for (int64_t s = 0; s < nf; ++s) {
+        first[s] = fstart[s];
+        width[s] = fstart[s + 1] - fstart[s];
+        offr[s] = cnt[fstart[s + 1] - 1];                 // rows below the last column
+        int64_t t = 0;
+        for (int32_t j = fstart[s]; j < fstart[s + 1]; ++j) t += cnt[j] + 1;
+        truenz[s] = t;
+    }
+    for (int64_t s = nf - 2; s >= 0; --s) {
+        if (fparent[s] == -1) continue;
+        int32_t P = find(fparent[s]);
+        if (fstart[s + 1] != first[P]) continue;         // not adjacent
+        int64_t w = width[s] + width[P];
+        int64_t r = w + offr[P];
+        double size = (double)w * (double)r - 0.5 * (double)w * (double)(w - 1);
+        double zeros = size - (double)(truenz[s] + truenz[P]);
+        double frac = size > 0 ? zeros / size : 0.0;
+        bool ok = w <= opt.relax_small || (w <= opt.relax_mid && frac <= opt.relax_mid_frac) ||
+                  (w <= opt.relax_big && frac <= opt.relax_big_frac);
+        if (!ok) continue;
+        rep[s] = P;
+        first[P] = first[s];
+        width[P] = w;
+        truenz[P] += truenz[s];
+    }
+    // final supernodes in column order
+    std::vector<int32_t> sid(nf, -1);
+    int32_t ns = 0;
+    for (int64_t s = 0; s < nf; ++s) {
+        int32_t r = find((int32_t)s);
+        if (sid[r] == -1) sid[r] = -2;  // placeholder
+    }
+    S.sn_col.clear();
+    S.col2sn.assign(dim, -1);
+    for (int64_t j = 0; j < dim; ++j) {
+        int32_t r = find(fsn[j]);
+        if (sid[r] < 0) {
+            sid[r] = ns++;
+            S.sn_col.push_back((int32_t)j);
+        }
+        S.col2sn[j] = sid[r];
+    }
+    S.sn_col.push_back((int32_t)dim);
+    S.nsuper = ns;
+    // row lists: own columns then union of column structures beyond the last column
+    S.sn_rptr.assign(ns + 1, 0);
+    S.sn_rows.clear();
+    std::fill(flag.begin(), flag.end(), -1);
+    std::vector<int32_t> tmp;
+    for (int32_t J = 0; J < ns; ++J) {
+        int32_t c0 = S.sn_col[J], c1 = S.sn_col[J + 1];
+        tmp.clear();
+        for (int32_t j = c0; j < c1; ++j)
+            for (int64_t p = lp[j]; p < lp[j + 1]; ++p) {
+                int32_t r = li[p];
+                if (r >= c1 && flag[r] != J) { flag[r] = J; tmp.push_back(r); }
+            }
+        std::sort(tmp.begin(), tmp.end());
+        for (int32_t j = c0; j < c1; ++j) S.sn_rows.push_back(j);
+        S.sn_rows.insert(S.sn_rows.end(), tmp.begin(), tmp.end());
+        S.sn_rptr[J + 1] = (int64_t)S.sn_rows.size();
+    }
+    S.sn_loff.assign(ns + 1, 0);
+    S.max_width = S.max_rows = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+        int64_t w = S.sn_col[J + 1] - S.sn_col[J];
+        int64_t r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+        S.sn_loff[J + 1] = S.sn_loff[J] + w * r;
+        S.max_width = std::max(S.max_width, w);
+        S.max_rows = std::max(S.max_rows, r);
+    }
+    S.nnz_storage = S.sn_loff[ns];
+    S.sn_parent.assign(ns, -1);
+    S.sn_nchild.assign(ns, 0);
+    for (int32_t J = 0; J < ns; ++J) {
+        int64_t w = S.sn_col[J + 1] - S.sn_col[J];
+        int64_t r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+        if (r > w) {
+            S.sn_parent[J] = S.col2sn[S.sn_rows[S.sn_rptr[J] + w]];
+            S.sn_nchild[S.sn_parent[J]]++;
+        }
+    }
+    // update lists (K -> J), K ascending inside each J
+    std::vector<int64_t> ucount(ns + 1, 0);
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<int64_t> fillp;
+        if (pass == 1) {
+            S.upd_ptr.assign(ns + 1, 0);
+            for (int32_t J = 0; J < ns; ++J) S.upd_ptr[J + 1] = S.upd_ptr[J] + ucount[J];
+            S.upd_src.assign(S.upd_ptr[ns], 0);
+            S.upd_p0.assign(S.upd_ptr[ns], 0);
+            S.upd_p1.assign(S.upd_ptr[ns], 0);
+            fillp.assign(S.upd_ptr.begin(), S.upd_ptr.end() - 1);
+        }
+        for (int32_t K = 0; K < ns; ++K) {
+            int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+            int64_t r0 = S.sn_rptr[K], r = S.sn_rptr[K + 1] - r0;
+            int64_t p = w;
+            while (p < r) {
+                int32_t J = S.col2sn[S.sn_rows[r0 + p]];
+                int64_t q = p;
+                while (q < r && S.col2sn[S.sn_rows[r0 + q]] == J) ++q;
+                if (pass == 0) {
+                    ucount[J]++;
+                } else {
+                    int64_t t = fillp[J]++;
+                    S.upd_src[t] = K;
+                    S.upd_p0[t] = (int32_t)p;
+                    S.upd_p1[t] = (int32_t)q;
+                }
+                p = q;
+            }
+        }
+    }
+    S.n_updates = S.upd_ptr[ns];
+    // levels and topological order
+    S.level.assign(ns, 0);
+    for (int32_t J = 0; J < ns; ++J)
+        if (S.sn_parent[J] != -1) S.level[S.sn_parent[J]] = std::max(S.level[S.sn_parent[J]], S.level[J] + 1);
+    S.height = 0;
+    for (int32_t J = 0; J < ns; ++J) S.height = std::max(S.height, S.level[J] + 1);
+    S.order.resize(ns);
+    std::iota(S.order.begin(), S.order.end(), 0);
+    std::stable_sort(S.order.begin(), S.order.end(),
+                     [&](int32_t a, int32_t b) { return S.level[a] < S.level[b]; });
+
+    // scatter maps: K(i,j) (original indices) -> panel position
+    auto pos = [&](int64_t i, int64_t j) -> int64_t {
+        int32_t a = iperm[i], b = iperm[j];
+        int32_t row = std::max(a, b), col = std::min(a, b);
+        int32_t J = S.col2sn[col];
+        const int32_t* rows = S.sn_rows.data() + S.sn_rptr[J];
+        int64_t r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+        int64_t lr = std::lower_bound(rows, rows + r, row) - rows;
+        return S.sn_loff[J] + (int64_t)(col - S.sn_col[J]) * r + lr;
+    };
+    S.map_p.assign(prp[n], -1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = prp[i]; p < prp[i + 1]; ++p)
+            if (pci[p] >= i) S.map_p[p] = pos(i, pci[p]);
+    S.map_a.assign(arp[m], 0);
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t p = arp[r]; p < arp[r + 1]; ++p) S.map_a[p] = pos(aci[p], n + r);
+    S.map_diag.assign(dim, 0);
+    for (int64_t i = 0; i < dim; ++i) S.map_diag[i] = pos(i, i);
+    S.map_hblk.clear();
+    for (int64_t b = 0; b < nblocks; ++b)
+        for (int64_t rl = 0; rl < bdim[b]; ++rl)
+            for (int64_t cl = rl; cl < bdim[b]; ++cl)
+                S.map_hblk.push_back(pos(n + boff[b] + rl, n + boff[b] + cl));
+    (void)lin;
+    return 0;
+}
+
+}  // namespace cipm

@@ -1,0 +1,69 @@
+// Host-side symbolic analysis of the quasi-definite KKT matrix
+//     K = [ P   A' ]
+//         [ A  -H  ]
+// run once per sparsity pattern (reference: kkt/system.py:87-148 pattern,
+// :188-240 symbolic_factor, kkt/ordering.py:15-53 ordering, kkt/ldl.py:20-34).
+//
+// Output is a *supernodal* description consumed by the sm_100a numeric
+// factorisation and triangular solves: supernodes are contiguous column ranges
+// of the (postordered) permuted matrix with a shared sorted row list; each panel
+// is stored dense column-major (rows x width) in one flat value array.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace cipm {
+
+struct SymbolicOptions {
+    int ordering = 0;          // 0 = exact minimum degree (reference order), 1 = natural
+    int relax_small = 8;       // always merge a child into its parent up to this width
+    int relax_mid = 32;        // ... up to this width if zero fraction <= relax_mid_frac
+    double relax_mid_frac = 0.3;
+    int relax_big = 64;        // ... up to this width if zero fraction <= relax_big_frac
+    double relax_big_frac = 0.05;
+};
+
+struct Symbolic {
+    int64_t n = 0, m = 0, dim = 0;
+    // permutation: position k of the factor holds original KKT index perm[k]
+    std::vector<int32_t> perm, iperm;
+    std::vector<int32_t> md_perm;          // raw minimum-degree order (before postordering)
+    std::vector<int8_t> sign;              // +1 x rows, -1 z rows (permuted order)
+    // supernodes
+    int32_t nsuper = 0;
+    std::vector<int32_t> sn_col;           // nsuper+1: first column, width = sn_col[J+1]-sn_col[J]
+    std::vector<int64_t> sn_rptr;          // nsuper+1: into sn_rows
+    std::vector<int32_t> sn_rows;          // sorted permuted row indices (first w = own columns)
+    std::vector<int64_t> sn_loff;          // nsuper+1: panel offsets in the value array
+    std::vector<int32_t> sn_parent;        // -1 for roots
+    std::vector<int32_t> sn_nchild;
+    std::vector<int32_t> col2sn;           // dim
+    // update lists (left-looking): updates into J come from (src, p0, p1)
+    std::vector<int64_t> upd_ptr;          // nsuper+1
+    std::vector<int32_t> upd_src, upd_p0, upd_p1;
+    // schedule
+    std::vector<int32_t> order;            // topological order (leaves first, by level)
+    std::vector<int32_t> level;            // per supernode, 0 = leaf
+    int32_t height = 0;
+    // scatter maps into the panel value array (int64 positions)
+    std::vector<int64_t> map_p;            // P CSR nnz; -1 for strictly-lower entries
+    std::vector<int64_t> map_a;            // A CSR nnz (entry (n+r, j) of K stored at L(col j? ...))
+    std::vector<int64_t> map_diag;         // dim, original index order: diagonal slot of K_ii
+    std::vector<int64_t> map_hblk;         // sum_b d_b(d_b+1)/2: upper entries (rl<=cl) per block
+    // statistics
+    int64_t nnz_l = 0;                     // true strict-lower nnz of L
+    int64_t nnz_storage = 0;               // dense panel elements
+    double flops = 0.0;                    // 2 * sum_j c_j^2 with c_j strict-lower count
+    int64_t max_width = 0, max_rows = 0;
+    int64_t n_updates = 0;
+};
+
+// Pattern inputs: P full CSR (n x n), A CSR (m x n); lin = zero_dim + nonneg_dim;
+// blocks (offset, dim) in K's z-row coordinates for every SOC/exp/pow/PSD cone.
+int analyze(int64_t n, int64_t m,
+            const int64_t* p_rowptr, const int64_t* p_colidx,
+            const int64_t* a_rowptr, const int64_t* a_colidx,
+            int64_t lin, int64_t nblocks, const int64_t* blk_off, const int64_t* blk_dim,
+            const SymbolicOptions& opt, Symbolic& out);
+
+}  // namespace cipm

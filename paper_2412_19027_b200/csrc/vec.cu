@@ -1,0 +1,625 @@
+// Vector / SpMV / reduction kernels of the IPM iteration.
+//
+// Fusion (SURVEY.md §7 "Residual/G fusion"): the unscaled residuals of
+// ipm.py:233-251 and the Eq.(9) infeasibility norms of ipm.py:263-280 are
+// diagonal rescalings of the scaled G rows of ipm.py:284-292, so ONE pass over
+// P and A' (n rows) and ONE pass over A (m rows) per iteration produce G, the
+// residual norms, the objectives and every infeasibility quantity, against six
+// A-class passes in the reference.  All reductions are two-level with a fixed
+// grid (bitwise reproducible).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+namespace cipm {
+
+namespace {
+
+__device__ __forceinline__ double csr_row(const int64_t* rp, const int64_t* ci, const double* v, const double* x,
+                                          int64_t i) {
+    double acc = 0.0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) acc += v[p] * x[ci[p]];
+    return acc;
+}
+
+// ------------------------------- init --------------------------------------
+
+__global__ void init_nonneg(double* s, double* z, int64_t nn0, int64_t nnd) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nnd) { s[nn0 + i] = 1.0; z[nn0 + i] = 1.0; }
+}
+
+__global__ void init_cones(const int32_t* soc_off, int64_t nsoc, const int32_t* exp_off, int64_t nexp,
+                           const int32_t* pow_off, const double* pow_alpha, int64_t npow, const int32_t* psd_off,
+                           const int32_t* psd_side, int64_t npsd, double* s, double* z) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const double eu[3] = {-1.051383945322714, 0.556409619469370, 1.258967884768947};
+    if (c < nsoc) { s[soc_off[c]] = 1.0; z[soc_off[c]] = 1.0; return; }
+    c -= nsoc;
+    if (c < nexp) {
+        for (int i = 0; i < 3; ++i) { s[exp_off[c] + i] = eu[i]; z[exp_off[c] + i] = eu[i]; }
+        return;
+    }
+    c -= nexp;
+    if (c < npow) {
+        double a = pow_alpha[c];
+        double pt[3] = {sqrt(1.0 + a), sqrt(2.0 - a), 0.0};
+        for (int i = 0; i < 3; ++i) { s[pow_off[c] + i] = pt[i]; z[pow_off[c] + i] = pt[i]; }
+        return;
+    }
+    c -= npow;
+    if (c < npsd) {
+        int n = psd_side[c], k = psd_off[c];
+        for (int j = 0; j < n; ++j) { s[k] = 1.0; z[k] = 1.0; k += n - j; }
+    }
+}
+
+// μ = (s'z + τκ)/(ν+1); also SZ
+__global__ void mu_kernel(const double* s, const double* z, int64_t m, double nu1, double* partials,
+                          unsigned int* counter, double* sc) {
+    double vals[1] = {0.0};
+    const int ops[1] = {RED_SUM};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        vals[0] += s[i] * z[i];
+    double out[1];
+    if (grid_reduce<1>(vals, ops, partials, counter, out)) {
+        sc[CIPM_SC_SZ] = out[0];
+        sc[CIPM_SC_MU] = (out[0] + sc[CIPM_SC_TAU] * sc[CIPM_SC_KAPPA]) / nu1;
+    }
+}
+
+__global__ void set_tk(double* sc) {
+    sc[CIPM_SC_TAU] = 1.0;
+    sc[CIPM_SC_KAPPA] = 1.0;
+}
+
+// ----------------------------- residuals -----------------------------------
+
+struct ResidN {
+    int64_t n;
+    const int64_t *prp, *pci;
+    const double* pv;
+    const int64_t *atrp, *atci;
+    const double* atv;
+    const double *x, *z, *q, *dc;
+    double* gx;
+};
+
+__global__ void resid_n(ResidN a, double* sc, double* partials, unsigned int* counter) {
+    const double tau = sc[CIPM_SC_TAU];
+    double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const int ops[6] = {RED_SUM, RED_SUM, RED_MAX, RED_MAX, RED_MAX, RED_MAX};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double px = csr_row(a.prp, a.pci, a.pv, a.x, i);
+        const double atz = csr_row(a.atrp, a.atci, a.atv, a.z, i);
+        const double g = -((px + atz) + a.q[i] * tau);
+        a.gx[i] = g;
+        const double xi = a.x[i], dci = a.dc[i];
+        v[0] += xi * px;
+        v[1] += a.q[i] * xi;
+        v[2] = fmax(v[2], fabs(g / dci));
+        v[3] = fmax(v[3], fabs(atz / dci));
+        v[4] = fmax(v[4], fabs(px / dci));
+        v[5] = fmax(v[5], fabs(dci * xi));
+    }
+    double out[6];
+    if (grid_reduce<6>(v, ops, partials, counter, out)) {
+        sc[CIPM_SC_XPX] = out[0];
+        sc[CIPM_SC_QX] = out[1];
+        sc[CIPM_SC_NRM_GX] = out[2];
+        sc[CIPM_SC_NRM_ATZ] = out[3];
+        sc[CIPM_SC_NRM_PX] = out[4];
+        sc[CIPM_SC_NRM_XU] = out[5];
+    }
+}
+
+struct ResidM {
+    int64_t m;
+    const int64_t *arp, *aci;
+    const double* av;
+    const double *x, *z, *s, *b, *dr;
+    double* gz;
+};
+
+__global__ void resid_m(ResidM a, double* sc, double* partials, unsigned int* counter) {
+    const double tau = sc[CIPM_SC_TAU];
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const int ops[5] = {RED_SUM, RED_MAX, RED_MAX, RED_MAX, RED_MAX};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double ax = csr_row(a.arp, a.aci, a.av, a.x, i);
+        const double si = a.s[i], dri = a.dr[i];
+        const double g = (si + ax) - a.b[i] * tau;
+        a.gz[i] = g;
+        v[0] += a.b[i] * a.z[i];
+        v[1] = fmax(v[1], fabs(g / dri));
+        v[2] = fmax(v[2], fabs((ax + si) / dri));
+        v[3] = fmax(v[3], fabs(dri * a.z[i]));
+        v[4] = fmax(v[4], fabs(si / dri));
+    }
+    double out[5];
+    if (grid_reduce<5>(v, ops, partials, counter, out)) {
+        sc[CIPM_SC_BZ] = out[0];
+        sc[CIPM_SC_NRM_GZ] = out[1];
+        sc[CIPM_SC_NRM_AXS] = out[2];
+        sc[CIPM_SC_NRM_ZU] = out[3];
+        sc[CIPM_SC_NRM_SU] = out[4];
+        // g_tau = κ + q'x + b'z + x'Px/τ  (ipm.py:290-291)
+        sc[CIPM_SC_GTAU] = ((sc[CIPM_SC_KAPPA] + sc[CIPM_SC_QX]) + out[0]) + sc[CIPM_SC_XPX] / tau;
+    }
+}
+
+// ------------------------------ copies -------------------------------------
+
+__global__ void copy2(const double* a, double* b, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+
+// ----------------------------- rhs build -----------------------------------
+
+// rb0 = [-q; b] (col2), rb1 = [gx; -(gz - s)] (affine)
+__global__ void affine_rhs(const double* q, const double* b, const double* gx, const double* gz, const double* s,
+                           double* rb, int64_t n, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t dim = n + m;
+    if (i >= dim) return;
+    if (i < n) {
+        rb[i] = -q[i];
+        rb[dim + i] = gx[i];
+    } else {
+        rb[i] = b[i - n];
+        rb[dim + i] = -(gz[i - n] - s[i - n]);
+    }
+}
+
+// combined: rb0 = [f gx; -(f gz - d_s)], f = 1 - σ
+__global__ void combined_rhs(const double* gx, const double* gz, const double* dsc, const double* sc, double* rb,
+                             int64_t n, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n + m) return;
+    const double f = 1.0 - sc[CIPM_SC_SIGMA];
+    if (i < n) rb[i] = f * gx[i];
+    else rb[i] = -(f * gz[i - n] - dsc[i - n]);
+}
+
+// ------------------------- direction recovery ------------------------------
+
+// T0 = q'dx1, T1 = ξ'P dx1 (n rows); T2 = b'dz1 (m rows)
+__global__ void dir_dots_n(const int64_t* prp, const int64_t* pci, const double* pv, const double* dx1,
+                           const double* x, const double* q, int64_t n, double* sc, double* partials,
+                           unsigned int* counter) {
+    const double tau = sc[CIPM_SC_TAU];
+    double v[2] = {0.0, 0.0};
+    const int ops[2] = {RED_SUM, RED_SUM};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double pd = csr_row(prp, pci, pv, dx1, i);
+        v[0] += q[i] * dx1[i];
+        v[1] += (x[i] / tau) * pd;
+    }
+    double out[2];
+    if (grid_reduce<2>(v, ops, partials, counter, out)) {
+        sc[CIPM_SC_T0] = out[0];
+        sc[CIPM_SC_T1] = out[1];
+    }
+}
+
+__global__ void dot_m(const double* b, const double* v, int64_t m, double* dst, double* partials,
+                      unsigned int* counter) {
+    double vals[1] = {0.0};
+    const int ops[1] = {RED_SUM};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        vals[0] += b[i] * v[i];
+    double out[1];
+    if (grid_reduce<1>(vals, ops, partials, counter, out)) *dst = out[0];
+}
+
+// denominator pieces (once per factorisation): T3 = diff'P diff, T4 = dx2'P dx2, T5 = q'dx2
+__global__ void den_dots_n(const int64_t* prp, const int64_t* pci, const double* pv, const double* dx2,
+                           const double* x, const double* q, int64_t n, double* sc, double* partials,
+                           unsigned int* counter) {
+    const double tau = sc[CIPM_SC_TAU];
+    double v[3] = {0.0, 0.0, 0.0};
+    const int ops[3] = {RED_SUM, RED_SUM, RED_SUM};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double pdiff = 0.0, pdx2 = 0.0;
+        for (int64_t p = prp[i]; p < prp[i + 1]; ++p) {
+            const int64_t j = pci[p];
+            pdiff += pv[p] * (dx2[j] - x[j] / tau);
+            pdx2 += pv[p] * dx2[j];
+        }
+        v[0] += (dx2[i] - x[i] / tau) * pdiff;
+        v[1] += dx2[i] * pdx2;
+        v[2] += q[i] * dx2[i];
+    }
+    double out[3];
+    if (grid_reduce<3>(v, ops, partials, counter, out)) {
+        sc[CIPM_SC_T3] = out[0];
+        sc[CIPM_SC_T4] = out[1];
+        sc[CIPM_SC_T5] = out[2];
+    }
+}
+
+__global__ void den_finish(double* sc, int* err) {
+    const double tau = sc[CIPM_SC_TAU], kappa = sc[CIPM_SC_KAPPA];
+    // ipm.py:328-330, T6 = b'dz2
+    sc[CIPM_SC_DEN] = (((kappa / tau + sc[CIPM_SC_T3]) - sc[CIPM_SC_T4]) - sc[CIPM_SC_T5]) - sc[CIPM_SC_T6];
+    (void)err;
+}
+
+// Δτ, Δκ (ipm.py:325-337); which = 0 affine, 1 combined
+__global__ void tau_step(double* sc, int which, int* err) {
+    const double tau = sc[CIPM_SC_TAU], kappa = sc[CIPM_SC_KAPPA], mu = sc[CIPM_SC_MU];
+    double d_tau, d_kappa;
+    if (which == 0) {
+        d_tau = sc[CIPM_SC_GTAU];
+        d_kappa = kappa * tau;
+    } else {
+        const double sigma = sc[CIPM_SC_SIGMA];
+        d_tau = (1.0 - sigma) * sc[CIPM_SC_GTAU];
+        d_kappa = (kappa * tau + sc[CIPM_SC_DKAPPA_A] * sc[CIPM_SC_DTAU_A]) - sigma * mu;
+    }
+    const double num = (((d_tau - d_kappa / tau) + sc[CIPM_SC_T0]) + sc[CIPM_SC_T2]) + 2.0 * sc[CIPM_SC_T1];
+    const double den = sc[CIPM_SC_DEN];
+    if (fabs(den) < 1e-14 || !(den == den)) set_error(err, CIPM_E_DENOM);
+    const double dt = num / den;
+    const double dk = -(d_kappa + kappa * dt) / tau;
+    sc[which == 0 ? CIPM_SC_DTAU_A : CIPM_SC_DTAU_C] = dt;
+    sc[which == 0 ? CIPM_SC_DKAPPA_A : CIPM_SC_DKAPPA_C] = dk;
+}
+
+__global__ void combine_dir(const double* sol, const double* col2, const double* sc, int which, double* dx,
+                            double* dz, int64_t n, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n + m) return;
+    const double dt = sc[which == 0 ? CIPM_SC_DTAU_A : CIPM_SC_DTAU_C];
+    const double v = sol[i] + dt * col2[i];
+    if (i < n) dx[i] = v;
+    else dz[i - n] = v;
+}
+
+// --------------------------- step lengths ----------------------------------
+
+__global__ void step_init(double* sc, int which) {
+    const double dt = sc[which == 0 ? CIPM_SC_DTAU_A : CIPM_SC_DTAU_C];
+    const double dk = sc[which == 0 ? CIPM_SC_DKAPPA_A : CIPM_SC_DKAPPA_C];
+    double a = 1.0;
+    if (dt < 0.0) a = fmin(a, -sc[CIPM_SC_TAU] / dt);
+    if (dk < 0.0) a = fmin(a, -sc[CIPM_SC_KAPPA] / dk);
+    if (!(a >= 0.0)) a = 0.0;
+    sc[CIPM_SC_ALPHA_WORK] = a;
+}
+
+__global__ void step_check(double* sc, int* err) {
+    if (!(sc[CIPM_SC_ALPHA_WORK] >= kMinStep)) set_error(err, CIPM_E_STEP);
+}
+
+// pick the first feasible of 32 candidates α·bt^k (steps.py:100-106)
+__global__ void nsym_resolve(double* sc, unsigned int* mask, double bt, int* err) {
+    const unsigned int m = *mask;
+    double a = sc[CIPM_SC_ALPHA_WORK];
+    sc[CIPM_SC_T7] = 0.0;
+    for (int k = 0; k < 32; ++k) {
+        if (!(a >= kMinStep)) { set_error(err, CIPM_E_STEP); return; }
+        if (m & (1u << k)) { sc[CIPM_SC_ALPHA_WORK] = a; return; }
+        a *= bt;
+    }
+    sc[CIPM_SC_ALPHA_WORK] = a;   // next batch starts here
+    sc[CIPM_SC_T7] = 1.0;         // pending
+    *mask = 0xffffffffu;
+}
+
+__global__ void step_store(double* sc, int which) {
+    const double a = sc[CIPM_SC_ALPHA_WORK];
+    if (which == 0) {
+        sc[CIPM_SC_ALPHA_A] = a;
+        sc[CIPM_SC_SIGMA] = pow(1.0 - a, 3.0);
+    } else {
+        sc[CIPM_SC_ALPHA_C] = a;
+    }
+}
+
+// neighbourhood pass 1: μ_k and the aggregate nonneg test for nk candidates
+// α_k = base·bt^k, a_k = scale·α_k (ipm.py:355-366, scaling.py:369-374)
+struct MuCand {
+    const double *s, *z, *ds, *dz;
+    int64_t m, nn0, nnd;
+    double nu1, beta, bt, scale;
+    int nk, g0;       // candidates in this batch, global index of the first
+};
+
+__global__ void mu_candidates(MuCand a, double* sc, double* nb, unsigned int* mask, int* err, double* partials,
+                              unsigned int* counter) {
+    double steps[8];
+    double al = sc[CIPM_SC_ALPHA_WORK];
+    for (int k = 0; k < 8; ++k) { steps[k] = a.scale * al; al *= a.bt; }
+    double v[16];
+    int ops[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { v[k] = 0.0; ops[k] = RED_SUM; }
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const double si = a.s[i], zi = a.z[i], dsi = a.ds[i], dzi = a.dz[i];
+        const bool nn = i >= a.nn0 && i < a.nn0 + a.nnd;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= a.nk) break;
+            const double st = si + steps[k] * dsi, zt = zi + steps[k] * dzi;
+            const double p = st * zt;
+            v[k] += p;
+            if (nn) {
+                if (!(st > 0.0) || !(zt > 0.0)) bad = true;
+                v[8 + k] += 1.0 / p;
+            }
+        }
+    }
+    if (bad) set_error(err, CIPM_E_DOMAIN);
+    double out[16];
+    if (grid_reduce<16>(v, ops, partials, counter, out)) {
+        unsigned int bits = 0xffffffffu;
+        double alk = sc[CIPM_SC_ALPHA_WORK];
+        for (int k = 0; k < a.nk; ++k) {
+            const double step = a.scale * alk;
+            const double tt = sc[CIPM_SC_TAU] + step * sc[CIPM_SC_DTAU_C];
+            const double kt = sc[CIPM_SC_KAPPA] + step * sc[CIPM_SC_DKAPPA_C];
+            const double mu_t = (out[k] + tt * kt) / a.nu1;
+            nb[k] = mu_t;
+            nb[16 + k] = step;
+            nb[32 + k] = alk;
+            if (a.nnd && (double)a.nnd / out[8 + k] < a.beta * mu_t) bits &= ~(1u << k);
+            alk *= a.bt;
+        }
+        *mask = bits;
+    }
+}
+
+__global__ void nb_resolve(double* sc, const double* nb, unsigned int* mask, int nk, int g0, double bt, int* err) {
+    const unsigned int m = *mask;
+    sc[CIPM_SC_T7] = 0.0;
+    for (int k = 0; k < nk; ++k) {
+        const double ak = nb[32 + k];
+        if (g0 + k > 0 && !(ak >= kMinStep)) { set_error(err, CIPM_E_STEP); return; }
+        if (m & (1u << k)) { sc[CIPM_SC_ALPHA_FINAL] = ak; return; }
+    }
+    sc[CIPM_SC_ALPHA_WORK] = nb[32 + nk - 1] * bt;
+    sc[CIPM_SC_T7] = 1.0;   // pending: evaluate the next batch
+}
+
+// ---------------------------- take_step ------------------------------------
+
+__global__ void take_step_vec(double* x, double* z, double* s, const double* dx, const double* dz, const double* ds,
+                              const double* sc, double scale, int64_t n, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const double a = scale * sc[CIPM_SC_ALPHA_FINAL];
+    if (i < n) x[i] = x[i] + a * dx[i];
+    if (i < m) {
+        z[i] = z[i] + a * dz[i];
+        s[i] = s[i] + a * ds[i];
+    }
+}
+
+__global__ void take_step_scalars(double* sc, double scale, int* err) {
+    const double a = scale * sc[CIPM_SC_ALPHA_FINAL];
+    const double t = sc[CIPM_SC_TAU] + a * sc[CIPM_SC_DTAU_C];
+    const double k = sc[CIPM_SC_KAPPA] + a * sc[CIPM_SC_DKAPPA_C];
+    sc[CIPM_SC_TAU] = t;
+    sc[CIPM_SC_KAPPA] = k;
+    if (!(t > 0.0) || !(k > 0.0)) set_error(err, CIPM_E_INTERIOR);
+}
+
+// --------------------------- KKT residual ----------------------------------
+
+// r1 = b1 - (P x1 + A' x2)
+__global__ void kkt_res_n(const int64_t* prp, const int64_t* pci, const double* pv, const int64_t* atrp,
+                          const int64_t* atci, const double* atv, const double* xv, const double* bv, double* rv,
+                          int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double kx = csr_row(prp, pci, pv, xv, i) + csr_row(atrp, atci, atv, xv + n, i);
+    rv[i] = bv[i] - kx;
+}
+
+// t2 = b2 - A x1   (H x2 is added by the cone kernels)
+__global__ void kkt_res_m(const int64_t* arp, const int64_t* aci, const double* av, const double* xv,
+                          const double* bv, double* rv, int64_t n, int64_t m) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    rv[n + i] = bv[n + i] - csr_row(arp, aci, av, xv, i);
+}
+
+// ‖r‖∞ and the refinement controller of system.py:298-314 for one rhs
+__global__ void refine_control(const double* rv, int64_t dim, double* st, double* partials, unsigned int* counter) {
+    double v[1] = {0.0};
+    const int ops[1] = {RED_MAX};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
+        v[0] = fmax(v[0], fabs(rv[i]));
+    double out[1];
+    if (grid_reduce<1>(v, ops, partials, counter, out)) {
+        // st: 0 best, 1 prev, 2 ups, 3 target, 4 done, 5 improved, 6 steps, 7 resid
+        const double rn = dim ? out[0] : 0.0;
+        st[6] += 1.0;
+        st[5] = 0.0;
+        if (rn < st[0]) { st[0] = rn; st[5] = 1.0; }
+        if (rn <= st[3]) { st[4] = 1.0; st[7] = rn; return; }
+        if (rn > st[1]) {
+            st[2] += 1.0;
+            if (st[2] >= 2.0) { st[4] = 2.0; st[7] = st[0]; return; }
+        } else {
+            st[2] = 0.0;
+        }
+        st[1] = rn;
+        st[7] = st[0];
+    }
+}
+
+__global__ void copy_if_improved(const double* src, double* dst, const double* st, int64_t n) {
+    if (st[5] == 0.0) return;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+// target = t_abs + t_rel ‖b‖∞, reset state
+__global__ void refine_init(const double* bv, int64_t dim, double* st, double t_abs, double t_rel, double* partials,
+                            unsigned int* counter) {
+    double v[1] = {0.0};
+    const int ops[1] = {RED_MAX};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
+        v[0] = fmax(v[0], fabs(bv[i]));
+    double out[1];
+    if (grid_reduce<1>(v, ops, partials, counter, out)) {
+        st[0] = INFINITY;
+        st[1] = INFINITY;
+        st[2] = 0.0;
+        st[3] = t_abs + t_rel * (dim ? out[0] : 0.0);
+        st[4] = 0.0;
+        st[5] = 0.0;
+        st[6] = 0.0;
+        st[7] = INFINITY;
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+
+void k_init_iterate(Ctx& c) {
+    cudaMemsetAsync(c.x, 0, sizeof(double) * c.n, c.stream);
+    cudaMemsetAsync(c.s, 0, sizeof(double) * c.m, c.stream);
+    cudaMemsetAsync(c.z, 0, sizeof(double) * c.m, c.stream);
+    if (c.nonneg_dim) {
+        init_nonneg<<<grid_for(c.nonneg_dim), kThreads, 0, c.stream>>>(c.s, c.z, c.zero_dim, c.nonneg_dim);
+        c.launches++;
+    }
+    const int64_t nc = c.nsoc + c.nexp + c.npow + c.npsd;
+    if (nc) {
+        init_cones<<<grid_for(nc), kThreads, 0, c.stream>>>(c.soc_off, c.nsoc, c.exp_off, c.nexp, c.pow_off,
+                                                            c.pow_alpha, c.npow, c.psd_off, c.psd_side, c.npsd, c.s,
+                                                            c.z);
+        c.launches++;
+    }
+    set_tk<<<1, 1, 0, c.stream>>>(c.sc);
+    mu_kernel<<<red_grid(c.m), kThreads, 0, c.stream>>>(c.s, c.z, c.m, c.nu + 1.0, c.partials, c.counter, c.sc);
+    c.launches += 2;
+}
+
+void k_residuals(Ctx& c) {
+    ResidN a{c.n, c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, c.x, c.z, c.q, c.dc, c.gx};
+    resid_n<<<red_grid(c.n), kThreads, 0, c.stream>>>(a, c.sc, c.partials, c.counter);
+    ResidM b{c.m, c.a_rp, c.a_ci, c.a_v, c.x, c.z, c.s, c.b, c.dr, c.gz};
+    resid_m<<<red_grid(c.m), kThreads, 0, c.stream>>>(b, c.sc, c.partials, c.counter);
+    c.launches += 2;
+}
+
+void k_copy_best(Ctx& c) {
+    cudaMemcpyAsync(c.bx, c.x, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream);
+    cudaMemcpyAsync(c.bz, c.z, sizeof(double) * c.m, cudaMemcpyDeviceToDevice, c.stream);
+    cudaMemcpyAsync(c.bs, c.s, sizeof(double) * c.m, cudaMemcpyDeviceToDevice, c.stream);
+}
+
+void k_affine_rhs(Ctx& c) {
+    affine_rhs<<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.q, c.b, c.gx, c.gz, c.s, c.rb, c.n, c.m);
+    c.launches++;
+}
+
+void k_combined_rhs(Ctx& c) {
+    combined_rhs<<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.gx, c.gz, c.dsc, c.sc, c.rb, c.n, c.m);
+    c.launches++;
+}
+
+void k_directions_prep_den(Ctx& c) {
+    den_dots_n<<<red_grid(c.n), kThreads, 0, c.stream>>>(c.p_rp, c.p_ci, c.p_v, c.col2, c.x, c.q, c.n, c.sc,
+                                                         c.partials, c.counter);
+    dot_m<<<red_grid(c.m), kThreads, 0, c.stream>>>(c.b, c.col2 + c.n, c.m, c.sc + CIPM_SC_T6, c.partials, c.counter);
+    den_finish<<<1, 1, 0, c.stream>>>(c.sc, c.err);
+    c.launches += 3;
+}
+
+// sol = [dx1; dz1]; fills dx/dz/ds of direction `which` (0 affine, 1 combined)
+void k_recover_direction(Ctx& c, int which, const double* sol, double) {
+    dir_dots_n<<<red_grid(c.n), kThreads, 0, c.stream>>>(c.p_rp, c.p_ci, c.p_v, sol, c.x, c.q, c.n, c.sc, c.partials,
+                                                         c.counter);
+    dot_m<<<red_grid(c.m), kThreads, 0, c.stream>>>(c.b, sol + c.n, c.m, c.sc + CIPM_SC_T2, c.partials, c.counter);
+    tau_step<<<1, 1, 0, c.stream>>>(c.sc, which, c.err);
+    combine_dir<<<grid_for(c.dim), kThreads, 0, c.stream>>>(sol, c.col2, c.sc, which, c.dx[which], c.dz[which], c.n,
+                                                           c.m);
+    c.launches += 4;
+    // Δs = -d_s - H Δz  (d_s = s for the affine step, the combined d_s otherwise)
+    k_apply_h(c, c.dz[which], c.ds[which], -1.0, which == 0 ? c.s : c.dsc, -1.0);
+}
+
+void k_step_init(Ctx& c, int which) {
+    step_init<<<1, 1, 0, c.stream>>>(c.sc, which);
+    c.launches++;
+}
+
+void k_step_finish(Ctx& c, int which) {
+    step_check<<<1, 1, 0, c.stream>>>(c.sc, c.err);
+    c.launches++;
+    (void)which;
+}
+
+// exported helpers for capi.cu
+void k_nsym_resolve(Ctx& c) {
+    nsym_resolve<<<1, 1, 0, c.stream>>>(c.sc, c.mask, c.backtrack, c.err);
+    c.launches++;
+}
+
+void k_step_store(Ctx& c, int which) {
+    step_store<<<1, 1, 0, c.stream>>>(c.sc, which);
+    c.launches++;
+}
+
+void k_mu_candidates(Ctx& c, int g0, int nk) {
+    MuCand a{c.s, c.z, c.ds[1], c.dz[1], c.m, c.zero_dim, c.nonneg_dim, c.nu + 1.0, c.beta, c.backtrack,
+             c.step_scale, nk, g0};
+    mu_candidates<<<red_grid(c.m), kThreads, 0, c.stream>>>(a, c.sc, c.nb, c.mask, c.err, c.partials, c.counter);
+    c.launches++;
+}
+
+void k_nb_resolve(Ctx& c, int g0, int nk) {
+    nb_resolve<<<1, 1, 0, c.stream>>>(c.sc, c.nb, c.mask, nk, g0, c.backtrack, c.err);
+    c.launches++;
+}
+
+void k_take_step(Ctx& c) {
+    const int64_t mx = c.n > c.m ? c.n : c.m;
+    take_step_vec<<<grid_for(mx), kThreads, 0, c.stream>>>(c.x, c.z, c.s, c.dx[1], c.dz[1], c.ds[1], c.sc,
+                                                           c.step_scale, c.n, c.m);
+    take_step_scalars<<<1, 1, 0, c.stream>>>(c.sc, c.step_scale, c.err);
+    c.launches += 2;
+    k_membership(c);
+    mu_kernel<<<red_grid(c.m), kThreads, 0, c.stream>>>(c.s, c.z, c.m, c.nu + 1.0, c.partials, c.counter, c.sc);
+    c.launches++;
+}
+
+// r = b - K x for rhs q (K = [P A'; A -H], unregularised, FP64)
+void k_kkt_residual_one(Ctx& c, int q) {
+    const double* xv = c.rx + (int64_t)q * c.dim;
+    const double* bv = c.rb + (int64_t)q * c.dim;
+    double* rv = c.rr + (int64_t)q * c.dim;
+    kkt_res_n<<<grid_for(c.n), kThreads, 0, c.stream>>>(c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, xv, bv, rv,
+                                                        c.n);
+    kkt_res_m<<<grid_for(c.m), kThreads, 0, c.stream>>>(c.a_rp, c.a_ci, c.a_v, xv, bv, rv, c.n, c.m);
+    c.launches += 2;
+    k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0);
+    refine_control<<<red_grid(c.dim), kThreads, 0, c.stream>>>(rv, c.dim, c.rstate + 8 * q, c.partials, c.counter);
+    copy_if_improved<<<grid_for(c.dim), kThreads, 0, c.stream>>>(xv, c.rbest + (int64_t)q * c.dim, c.rstate + 8 * q,
+                                                                 c.dim);
+    c.launches += 2;
+}
+
+void k_refine_init_one(Ctx& c, int q) {
+    double* bv = c.rb + (int64_t)q * c.dim;
+    cudaMemsetAsync(c.rx + (int64_t)q * c.dim, 0, sizeof(double) * c.dim, c.stream);
+    cudaMemsetAsync(c.rbest + (int64_t)q * c.dim, 0, sizeof(double) * c.dim, c.stream);
+    cudaMemcpyAsync(c.rr + (int64_t)q * c.dim, bv, sizeof(double) * c.dim, cudaMemcpyDeviceToDevice, c.stream);
+    refine_init<<<red_grid(c.dim), kThreads, 0, c.stream>>>(bv, c.dim, c.rstate + 8 * q, c.refine_abs, c.refine_rel,
+                                                            c.partials, c.counter);
+    c.launches++;
+}
+
+void k_copy(Ctx& c, const double* src, double* dst, int64_t n) {
+    cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream);
+}
+
+}  // namespace cipm

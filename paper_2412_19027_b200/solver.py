@@ -1,0 +1,400 @@
+"""B200 drop-in for the reference ``conic_ipm.ipm`` (Solver / solve).
+
+The host keeps the reference's control flow (``pkg/src/conic_ipm/ipm.py``):
+setup (validate → reorder → equilibrate → KKT symbolic analysis, ipm.py:150-171),
+then the Algorithm-1 loop (ipm.py:411-496) with identical termination,
+infeasibility, stall, best-iterate and recovery rules.  Every per-iteration
+vector operation runs on the GPU through the C ABI (``include/cipm.h``); the
+host only sees the scalar block (one read per iteration plus the reads the
+refinement / backtracking decisions need).
+
+There is no CPU fallback: constructing a Solver without the native library or
+without a CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .exceptions import ConicError, PatternMismatch
+from .model import Equilibration, ProblemData, equilibrate, reorder_cones, unscale_solution, validate
+from .native import SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, require_device
+from .settings import (ALMOST_OPTIMAL_FACTOR, FULL, MIXED, STALL_IMPROVEMENT, STALL_WINDOW, SolveResult,
+                       SolverSettings, Status, default_dynamic_reg, default_static_reg)
+
+
+@dataclass
+class Residuals:
+    """Unscaled residual summary (reference ipm.py:98-114, norms only)."""
+
+    g_p: float
+    g_d: float
+    norm_rp: float
+    norm_rd: float
+    norm_xbar: float
+    norm_sbar: float
+    norm_zbar: float
+
+    @property
+    def gap(self) -> float:
+        return abs(self.g_p - self.g_d)
+
+
+@dataclass
+class IterateState:
+    x: np.ndarray
+    z: np.ndarray
+    s: np.ndarray
+    tau: float
+    kappa: float
+    mu: float
+
+    @property
+    def xi(self) -> np.ndarray:
+        return self.x / self.tau
+
+    def copy(self) -> "IterateState":
+        return IterateState(self.x.copy(), self.z.copy(), self.s.copy(), self.tau, self.kappa, self.mu)
+
+
+class DeviceScaling:
+    """Observer view of the scaling state (reference ScalingState subset: kkt_values / dense)."""
+
+    def __init__(self, solver: "Solver"):
+        self._solver = solver
+        lay = solver.layout
+        lin = lay.zero_dim + lay.nonneg_dim
+        ctx = solver._ctx
+        nn_h = solver._vector("nn_h")
+        self.diag = np.zeros(lin)
+        self.diag[lay.zero_dim:] = nn_h
+        hv = solver._vector("hv")
+        self.blocks = []
+        k = 0
+        for off, d in solver._block_list():
+            iu, ju = np.triu_indices(d)
+            blk = np.zeros((d, d))
+            cnt = d * (d + 1) // 2
+            blk[iu, ju] = hv[k:k + cnt]
+            blk[ju, iu] = hv[k:k + cnt]
+            k += cnt
+            self.blocks.append((off, blk))
+        del ctx
+
+    def kkt_values(self):
+        return self.diag, self.blocks
+
+    def dense(self) -> np.ndarray:
+        m = self._solver.layout.m
+        h = np.zeros((m, m))
+        h[np.arange(len(self.diag)), np.arange(len(self.diag))] = self.diag
+        for off, blk in self.blocks:
+            d = blk.shape[0]
+            h[off:off + d, off:off + d] = blk
+        return h
+
+
+class Solver:
+    """One problem instance: setup once on the host + GPU, solve and re-solve."""
+
+    def __init__(self, problem: ProblemData, settings: SolverSettings | None = None, device: int = 0,
+                 ordering: int = 0):
+        self.settings = settings or SolverSettings()
+        torch = require_device()
+        self.device = device
+        t0 = time.perf_counter()
+        validate(problem)
+        self._original = problem.copy()
+        reordered, perm = reorder_cones(problem)
+        self._perm = perm
+        self._reordered = reordered
+        self._equilibrate(reordered)
+        self.layout = Layout(self._scaled.cones)
+        self.nu = self.layout.degree
+        self.n, self.m = self._scaled.n, self._scaled.m
+        self.symbolic = SymbolicAnalysis(self._scaled.P, self._scaled.A, self.layout, ordering=ordering)
+        st = self.settings
+        prec = st.precision
+        cs = Settings()
+        cs.precision = 0 if prec == FULL else 1
+        cs.delta_s = default_static_reg(prec) if st.delta_s is None else st.delta_s
+        cs.delta_d = default_dynamic_reg(prec) if st.delta_d is None else st.delta_d
+        if prec == MIXED:
+            # the reference casts δ to float32 before use (system.py:253-258)
+            cs.delta_s = float(np.float32(cs.delta_s))
+            cs.delta_d = float(np.float32(cs.delta_d))
+        cs.beta, cs.backtrack, cs.step_scale = st.beta, st.backtrack, st.step_scale
+        cs.refine_abs, cs.refine_rel, cs.refine_max = (st.refinement.t_abs, st.refinement.t_rel,
+                                                       st.refinement.t_max)
+        cs.device = device
+        cs.stream = None
+        torch.cuda.set_device(device)
+        self._ctx = DeviceContext(self.symbolic, cs)
+        self._upload_values()
+        self.num_symbolic = 1
+        self.setup_seconds = time.perf_counter() - t0
+        self._sc = np.zeros(64)
+        self.last_refine_steps = []
+
+    # -- data plumbing --------------------------------------------------------
+
+    def _equilibrate(self, reordered):
+        if self.settings.do_equilibrate:
+            self._scaled, self._equil = equilibrate(reordered)
+        else:
+            self._scaled, self._equil = reordered.copy(), Equilibration.identity(reordered.m, reordered.n)
+        qr, br = reordered.q, reordered.b
+        self._norm_q = float(np.max(np.abs(qr))) if qr.size else 0.0
+        self._norm_b = float(np.max(np.abs(br))) if br.size else 0.0
+
+    def _upload_values(self):
+        sp_, e = self._scaled, self._equil
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                      (sp_.P.values, sp_.A.values, sp_.q, sp_.b, e.d_row, e.d_col)]
+        k = self._keep
+        self._ctx.call("cipm_ctx_set_values", pdbl(k[0]), pdbl(k[1]), pdbl(k[2]), pdbl(k[3]), pdbl(k[4]),
+                       pdbl(k[5]), float(e.c_obj))
+
+    def update_data(self, P=None, A=None, q=None, b=None) -> None:
+        """Parametric re-solve (reference ipm.py:187-221): same patterns, fresh
+        equilibration, value-only upload; the symbolic analysis is reused."""
+        prob = self._original
+        if P is not None:
+            if not (np.array_equal(P.rowptr, prob.P.rowptr) and np.array_equal(P.colidx, prob.P.colidx)):
+                raise PatternMismatch("P pattern differs from the setup pattern")
+            prob.P = P.copy()
+        if A is not None:
+            if not (np.array_equal(A.rowptr, prob.A.rowptr) and np.array_equal(A.colidx, prob.A.colidx)):
+                raise PatternMismatch("A pattern differs from the setup pattern")
+            prob.A = A.copy()
+        if q is not None:
+            if len(q) != prob.n:
+                raise PatternMismatch("q length changed")
+            prob.q = np.asarray(q, dtype=np.float64).copy()
+        if b is not None:
+            if len(b) != prob.m:
+                raise PatternMismatch("b length changed")
+            prob.b = np.asarray(b, dtype=np.float64).copy()
+        validate(prob)
+        self._reordered, _ = reorder_cones(prob)
+        self._equilibrate(self._reordered)
+        self._upload_values()
+
+    def _block_list(self):
+        lay = self.layout
+        out = [(int(o), int(d)) for o, d in zip(lay.soc_off, lay.soc_dim)]
+        out += [(int(o), 3) for o in lay.exp_off]
+        out += [(int(o), 3) for o in lay.pow_off]
+        out += [(int(o), int(s) * (int(s) + 1) // 2) for o, s in zip(lay.psd_off, lay.psd_side)]
+        return out
+
+    def _vector(self, name: str) -> np.ndarray:
+        from .native import lib
+        cnt = ctypes.c_int64(0)
+        lib().cipm_get_vector(self._ctx.handle, name.encode(), None, ctypes.byref(cnt))
+        out = np.zeros(cnt.value)
+        self._ctx.call("cipm_get_vector", name.encode(), pdbl(out), ctypes.byref(cnt))
+        return out
+
+    def _to_user_rows(self, v):
+        out = np.empty_like(v)
+        out[self._perm] = v
+        return out
+
+    def _state(self, which: int = 0) -> IterateState:
+        x, z, s = np.zeros(self.n), np.zeros(self.m), np.zeros(self.m)
+        tkm = np.zeros(3)
+        self._ctx.call("cipm_get_iterate", which, pdbl(x), pdbl(z), pdbl(s), pdbl(tkm))
+        return IterateState(x, z, s, float(tkm[0]), float(tkm[1]), float(tkm[2]))
+
+    # -- residuals ------------------------------------------------------------
+
+    def _residuals(self, sc) -> Residuals:
+        """Eq.(7) quantities from the fused device reductions (scaled-space identities)."""
+        tau, c = sc[SC["TAU"]], self._equil.c_obj
+        xpx, qx, bz = sc[SC["XPX"]], sc[SC["QX"]], sc[SC["BZ"]]
+        hq = 0.5 * xpx / (c * tau * tau)
+        return Residuals(g_p=hq + qx / (c * tau), g_d=-hq - bz / (c * tau),
+                         norm_rp=sc[SC["NRM_GZ"]] / tau, norm_rd=sc[SC["NRM_GX"]] / (c * tau),
+                         norm_xbar=sc[SC["NRM_XU"]] / tau, norm_sbar=sc[SC["NRM_SU"]] / tau,
+                         norm_zbar=sc[SC["NRM_ZU"]] / (c * tau))
+
+    def _ratios(self, r: Residuals):
+        return (r.norm_rp / max(1.0, self._norm_b + r.norm_xbar + r.norm_sbar),
+                r.norm_rd / max(1.0, self._norm_q + r.norm_xbar + r.norm_zbar),
+                r.gap / max(1.0, min(abs(r.g_p), abs(r.g_d))))
+
+    def _converged(self, r: Residuals, eps: float) -> bool:
+        a, b, c = self._ratios(r)
+        return a < eps and b < eps and c < eps
+
+    def _infeasible(self, sc):
+        """Eq.(9) tests on the unscaled, un-normalised iterate (ipm.py:263-280)."""
+        eps = self.settings.eps_inf
+        c = self._equil.c_obj
+        bz = sc[SC["BZ"]] / c
+        qx = sc[SC["QX"]] / c
+        nx, nz, ns = sc[SC["NRM_XU"]], sc[SC["NRM_ZU"]] / c, sc[SC["NRM_SU"]]
+        atz = sc[SC["NRM_ATZ"]] / c if self.n else 0.0
+        if atz < -eps * max(1.0, nx + nz) * bz and bz < -eps:
+            return Status.PRIMAL_INFEASIBLE
+        px = sc[SC["NRM_PX"]] / c if self.n else 0.0
+        axs = sc[SC["NRM_AXS"]]
+        if px < -eps * max(1.0, nx) * bz and axs < -eps * max(1.0, nx + ns) * qx and qx < -eps:
+            return Status.DUAL_INFEASIBLE
+        return None
+
+    # -- recovery -------------------------------------------------------------
+
+    def _recover(self, which, res: Residuals, status, iterations, secs, tkm=None) -> SolveResult:
+        st = self._state(which)
+        if tkm is not None:
+            st.tau, st.kappa, st.mu = tkm
+        x_u, z_u, s_u = unscale_solution(st.x, st.z, st.s, self._equil)
+        cert = None
+        if status not in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
+            x_o, z_o, s_o = x_u / st.tau, self._to_user_rows(z_u / st.tau), self._to_user_rows(s_u / st.tau)
+        else:
+            x_o, z_o, s_o = x_u, self._to_user_rows(z_u), self._to_user_rows(s_u)
+            if status == Status.PRIMAL_INFEASIBLE:
+                cert = z_o / abs(float(self._original.b @ z_o))
+            else:
+                cert = x_o / abs(float(self._original.q @ x_o))
+        return SolveResult(status=status, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=res.g_p,
+                           obj_dual=res.g_d, iterations=iterations, setup_seconds=self.setup_seconds,
+                           solve_seconds=secs, norm_rp=res.norm_rp, norm_rd=res.norm_rd, gap=res.gap,
+                           tau=st.tau, kappa=st.kappa, mu_initial=self._mu_initial, mu_final=st.mu)
+
+    # -- main loop ------------------------------------------------------------
+
+    def solve(self, observer=None) -> SolveResult:
+        t_start = time.perf_counter()
+        cfg = self.settings
+        ctx = self._ctx
+        sc = self._sc
+        ctx.call("cipm_init_iterate")
+        ctx.call("cipm_read_scalars", pdbl(sc))
+        self._mu_initial = float(sc[SC["MU"]])
+        best_score = np.inf
+        best_res = None
+        best_tkm = None
+        stall = [np.inf, np.inf, np.inf, 0]
+        res = None
+        status = None
+        iterations = 0
+        steps = ctypes.c_int(0)
+        alpha = ctypes.c_double(0.0)
+        self.last_refine_steps = []
+        try:
+            for it in range(cfg.max_iter + 1):
+                ctx.call("cipm_residuals", pdbl(sc))
+                tau, kappa, mu = float(sc[SC["TAU"]]), float(sc[SC["KAPPA"]]), float(sc[SC["MU"]])
+                res = self._residuals(sc)
+                score = max(self._ratios(res))
+                if score < best_score or best_res is None:
+                    if score < best_score:
+                        best_score = score
+                    best_res = res
+                    best_tkm = (tau, kappa, mu)
+                    ctx.call("cipm_save_best")
+                if cfg.verbose:
+                    print(f"iter {it:3d}  mu={mu:9.2e}  rp={res.norm_rp:9.2e}  "
+                          f"rd={res.norm_rd:9.2e}  gap={res.gap:9.2e}  tau={tau:8.2e}")
+                if self._converged(res, cfg.eps_feas):
+                    status = Status.OPTIMAL
+                    break
+                inf_status = self._infeasible(sc)
+                if inf_status is not None:
+                    status = inf_status
+                    break
+                if it >= cfg.max_iter:
+                    status = Status.MAX_ITERATIONS
+                    break
+                if time.perf_counter() - t_start > cfg.time_limit:
+                    status = Status.TIME_LIMIT
+                    break
+                improved = (mu < STALL_IMPROVEMENT * stall[0] or res.norm_rp < STALL_IMPROVEMENT * stall[1]
+                            or res.norm_rd < STALL_IMPROVEMENT * stall[2])
+                stall[0] = min(stall[0], mu)
+                stall[1] = min(stall[1], res.norm_rp)
+                stall[2] = min(stall[2], res.norm_rd)
+                stall[3] = 0 if improved else stall[3] + 1
+                if stall[3] >= STALL_WINDOW:
+                    status = Status.INSUFFICIENT_PROGRESS
+                    break
+
+                state_before = self._state(0) if observer is not None else None
+                ctx.call("cipm_update_scaling")
+                ctx.call("cipm_factor")
+                ctx.call("cipm_solve_affine", ctypes.byref(steps))
+                s_aff = steps.value
+                ctx.call("cipm_step_affine")
+                ctx.call("cipm_solve_combined", ctypes.byref(steps))
+                s_comb = steps.value
+                ctx.call("cipm_step_combined", ctypes.byref(alpha))
+                self.last_refine_steps.append((s_aff, s_comb))
+                if observer is not None:
+                    observer(self._observer_doc(it, state_before))
+                ctx.call("cipm_take_step")
+                iterations = it + 1
+        except (ConicError, np.linalg.LinAlgError) as err:
+            if cfg.verbose:
+                print(f"numerical error: {err}")
+            status = Status.NUMERICAL_ERROR
+
+        secs = time.perf_counter() - t_start
+        if status in (Status.OPTIMAL, Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
+            return self._recover(0, res, status, iterations, secs)
+        if best_res is not None and self._converged(best_res, ALMOST_OPTIMAL_FACTOR * cfg.eps_feas):
+            status = Status.ALMOST_OPTIMAL
+        if best_res is None:
+            raise ConicError("solve failed before the first residual evaluation")
+        return self._recover(1, best_res, status, iterations, secs, tkm=best_tkm)
+
+    def _observer_doc(self, it, state: IterateState) -> dict:
+        sc = np.zeros(64)
+        self._ctx.call("cipm_read_scalars", pdbl(sc))
+
+        def direction(which):
+            dx, dz, ds, dtk = np.zeros(self.n), np.zeros(self.m), np.zeros(self.m), np.zeros(2)
+            self._ctx.call("cipm_get_direction", which, pdbl(dx), pdbl(dz), pdbl(ds), pdbl(dtk))
+            return dx, dz, float(dtk[0]), ds, float(dtk[1])
+
+        gx, gz = self._vector("gx"), self._vector("gz")
+        sigma = float(sc[SC["SIGMA"]])
+        f = 1.0 - sigma
+        da = direction(0)
+        d_aff = (gx, gz, float(sc[SC["GTAU"]]), state.s.copy(), state.kappa * state.tau)
+        d_kappa_c = state.kappa * state.tau + da[4] * da[2] - sigma * state.mu
+        d_comb = (f * gx, f * gz, f * float(sc[SC["GTAU"]]), self._vector("dsc"), d_kappa_c)
+        return dict(iteration=it, state=state, scaling=DeviceScaling(self), d_affine=d_aff,
+                    delta_affine=da, d_combined=d_comb, delta_combined=direction(1),
+                    alpha_affine=float(sc[SC["ALPHA_A"]]), sigma=sigma,
+                    alpha_combined=float(sc[SC["ALPHA_FINAL"]]))
+
+    def close(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None:
+            ctx.close()
+            self._ctx = None
+        sym = getattr(self, "symbolic", None)
+        if sym is not None:
+            sym.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(problem: ProblemData, settings: SolverSettings | None = None, observer=None) -> SolveResult:
+    """Validate, set up on the GPU and solve one problem instance (reference ipm.py:499-502)."""
+    s = Solver(problem, settings)
+    try:
+        return s.solve(observer=observer)
+    finally:
+        s.close()

@@ -1,0 +1,84 @@
+"""GPU parity: the CUDA path against the reference's golden results and the oracle.
+
+Parity contract (BASELINE.json north_star): same termination status, iteration
+count within ±1, primal/dual objective within 1e-6 relative, final residuals
+meeting the same tolerances.
+"""
+import numpy as np
+import pytest
+
+from golden_io import instance_names, load_instance, problem_from_doc
+from oracle import OracleSolver
+from paper_2412_19027_b200.settings import SolverSettings
+
+pytestmark = pytest.mark.gpu
+
+NAMES = instance_names()
+
+
+def settings_of(doc):
+    s = doc["settings"]
+    return SolverSettings(eps_feas=s["eps_feas"], precision=s["precision"], max_iter=s["max_iter"])
+
+
+def rel(a, b):
+    return abs(a - b) / max(1.0, abs(b))
+
+
+def check_parity(res, ref, iters_tol=1):
+    assert res.status == ref["status"], (res.status, ref["status"])
+    assert abs(res.iterations - ref["iterations"]) <= iters_tol, (res.iterations, ref["iterations"])
+    if ref["status"] in ("optimal", "almost_optimal"):
+        assert rel(res.obj_primal, ref["obj_primal"]) <= 1e-6
+        assert rel(res.obj_dual, ref["obj_dual"]) <= 1e-6
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_matches_reference_golden(name, gpu):
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance(name)
+    prob = problem_from_doc(doc)
+    s = Solver(prob, settings_of(doc))
+    res = s.solve()
+    s.close()
+    check_parity(res, doc["result"])
+    if res.status == "optimal":
+        x_ref = np.array(doc["result"]["x"])
+        assert np.max(np.abs(res.x - x_ref)) <= 1e-4 * max(1.0, np.max(np.abs(x_ref)))
+    if res.status == "primal_infeasible":
+        np.testing.assert_allclose(res.certificate, doc["result"]["certificate"], atol=1e-6)
+
+
+def test_gpu_reproducible(gpu):
+    """Fixed-order reductions + dependency-ordered factorisation: bitwise identical reruns."""
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance("lp_150x300")
+    s = Solver(problem_from_doc(doc), settings_of(doc))
+    r1 = s.solve()
+    r2 = s.solve()
+    s.close()
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(r1.x, r2.x)
+    np.testing.assert_array_equal(r1.z, r2.z)
+
+
+def test_gpu_update_data_reuses_symbolic(gpu):
+    """SPEC AC9: parametric re-solves match fresh solves, symbolic analysis once."""
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance("lp_60x120")
+    prob = problem_from_doc(doc)
+    cfg = settings_of(doc)
+    s = Solver(prob, cfg)
+    rng = np.random.default_rng(3)
+    for k in range(3):
+        q = prob.q * (1.0 + 0.05 * rng.standard_normal(prob.n))
+        s.update_data(q=q)
+        r = s.solve()
+        p2 = prob.copy()
+        p2.q = q
+        o = OracleSolver(p2, cfg).solve()
+        assert r.status == o.status
+        assert abs(r.iterations - o.iterations) <= 1
+        assert rel(r.obj_primal, o.obj_primal) <= 1e-6
+    assert s.num_symbolic == 1
+    s.close()

@@ -1,0 +1,117 @@
+"""CPU tests of the native boundary: the library loads, exports every symbol of
+include/cipm.h, and the host symbolic analysis is correct (no GPU needed)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from golden_io import instance_names, load_instance, problem_from_doc
+import supernodal_model as SM
+from oracle import OracleSolver
+from oracle import cones as C
+from paper_2412_19027_b200 import model, native
+from paper_2412_19027_b200.settings import SolverSettings
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "cipm.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void)\s+(cipm_\w+)\s*\(", txt, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = native.lib()
+    syms = header_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(native.exported_symbols())
+    assert L.cipm_version() >= 100
+
+
+def _scaled(name):
+    prob = problem_from_doc(load_instance(name))
+    r, _ = model.reorder_cones(prob)
+    s, _ = model.equilibrate(r)
+    return prob, s
+
+
+@pytest.mark.parametrize("name", [n for n in instance_names() if not n.startswith("dual_inf")])
+def test_min_degree_matches_reference_order(name):
+    prob, s = _scaled(name)
+    sym = native.SymbolicAnalysis(s.P, s.A, native.Layout(s.cones))
+    o = OracleSolver(prob, SolverSettings())
+    np.testing.assert_array_equal(sym.array("md_perm"), o.kkt.perm)
+    assert sym.info()["nnz_l"] == o.kkt.nnz_l
+
+
+@pytest.mark.parametrize("name", ["lp_20x40", "socp_10", "psd_4x3", "exppow_20_8", "mpc_s0", "lasso_40x160"])
+def test_supernodal_structure_reconstructs_kkt(name):
+    _, s = _scaled(name)
+    lay = native.Layout(s.cones)
+    sym = native.SymbolicAnalysis(s.P, s.A, lay)
+    olay = C.ConeLayout.from_specs(s.cones)
+    s0, z0 = C.unit_start(olay)
+    sc = C.update_scaling(olay, s0, z0, 1.0)
+    diag, blocks = sc.kkt_blocks()
+    rng = np.random.default_rng(0)
+    diag = diag.copy()
+    diag[lay.zero_dim:] *= rng.uniform(0.1, 10, lay.nonneg_dim)
+    hb = np.concatenate([b[np.triu_indices(b.shape[0])] for _, b in blocks]) if blocks else np.zeros(0)
+    n = s.n
+    reg = 1e-3
+    vals = SM.assemble(sym, n, s.P, s.A, diag, hb, reg)
+    perm = sym.array("perm")
+    dim = len(perm)
+    L, D = SM.factor(sym, vals, np.where(perm < n, 1, -1), 1e-14)
+    Ld = SM.dense_factor(sym, L, D)
+    K = np.zeros((dim, dim))
+    K[:n, :n] = s.P.toarray()
+    A = s.A.toarray()
+    K[n:, :n] = A
+    K[:n, n:] = A.T
+    H = sc.dense().copy()
+    H[np.arange(len(diag)), np.arange(len(diag))] = diag
+    K[n:, n:] = -H
+    K += np.diag(np.where(np.arange(dim) < n, reg, -reg))
+    Kp = K[np.ix_(perm, perm)]
+    assert np.abs(Ld @ np.diag(D) @ Ld.T - Kp).max() < 1e-10 * max(1.0, np.abs(Kp).max())
+
+
+def test_symbolic_invariants():
+    _, s = _scaled("lp_150x300")
+    sym = native.SymbolicAnalysis(s.P, s.A, native.Layout(s.cones))
+    col, rptr, rows = sym.array("sn_col"), sym.array("sn_rptr"), sym.array("sn_rows")
+    par = sym.array("sn_parent")
+    order = sym.array("order")
+    ns = len(col) - 1
+    pos = np.empty(ns, dtype=np.int64)
+    pos[order] = np.arange(ns)
+    for J in range(ns):
+        w = col[J + 1] - col[J]
+        rj = rows[rptr[J]:rptr[J + 1]]
+        assert np.array_equal(rj[:w], np.arange(col[J], col[J + 1]))
+        assert np.all(np.diff(rj) > 0)
+        if par[J] >= 0:
+            assert pos[par[J]] > pos[J]          # topological order
+            assert col[par[J]] <= rj[w] < col[par[J] + 1]
+    # every scatter position is unique
+    mp = sym.array("map_p")
+    allpos = np.concatenate([mp[mp >= 0], sym.array("map_a"), sym.array("map_diag"), sym.array("map_hblk")])
+    # P diagonal and map_diag coincide for x rows; everything else is unique
+    assert len(np.unique(np.concatenate([sym.array("map_a"), sym.array("map_diag")]))) == \
+        len(sym.array("map_a")) + len(sym.array("map_diag"))
+    assert allpos.max() < sym.info()["nnz_storage"]
+
+
+def test_min_degree_entry_point_on_arrow():
+    # 5x5 arrow (dense last row/col): MD eliminates the leaves first, spike last (SPEC kkt-solver example)
+    import scipy.sparse as sp
+    a = np.eye(5)
+    a[4, :] = 1
+    a[:, 4] = 1
+    m = sp.csr_matrix(a)
+    perm = native.min_degree(m.indptr, m.indices)
+    assert perm[-1] == 4 or perm[-2] == 4
