@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IPM hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_lasso] [--impl ours|reference]
+
+A *step* is one complete solve (Algorithm 1 from the unit start point to
+termination at ε_feas = 1e-8) of the configured synthetic instance.  The
+headline metric is IPM iterations per second of the whole job; solve time per
+instance is reported alongside.  The default workload is BASELINE.json
+configs[1] (C2: lasso with 50k features × 200k rows, FP32 LDL' + FP64
+iterative refinement).
+
+value     — device-resident inputs (problem uploaded once), CUDA-event timed per
+            step on the solver stream, L2 flushed between steps (256 MiB write).
+e2e       — through the public API with host buffers: Solver.update_data(q, b)
+            (host equilibration + H2D upload) + Solver.solve() (D2H of x, z, s),
+            CUDA-event timed on the same stream.
+roofline  — the dominant kernel class (supernodal triangular solves or the
+            numeric factorisation), algorithmic bytes / event-timed duration.
+cpu_baseline — the CPU oracle (oracle/, a restatement of the reference solver;
+            its parity is pinned bit-for-bit to the reference's golden
+            fixtures) on the same instance, single thread, bounded sample.
+
+Multi-GPU (torchrun): a single problem does not shard, so N>1
+runs N independent replicas (weak scaling), timed as the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ipm_iterations_per_s"
+UNIT = "iter/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2_lasso")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--eps", type=float, default=1e-8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-max-iters", type=int, default=0, help=argparse.SUPPRESS)
+    return ap.parse_args()
+
+
+def workload(config):
+    from paper_2412_19027_b200 import generators as G
+    spec = G.CONFIGS[config]
+    desc = {"c1_lp": "C1 random sparse LP n=2000 m=4000 (1000 zero + 3000 nonneg)",
+            "c2_lasso": "C2 lasso 50k features x 200k rows (n=300k, m=300k), fp32 LDL' + fp64 IR",
+            "c3_socp": "C3 SOCP 100k cones dim U{3..10}",
+            "c4_exppow": "C4 50k exp + 20k pow cones",
+            "c5a_psd": "C5a 10k PSD cones side 6"}[config]
+    return spec, desc
+
+
+def settings_for(config, eps):
+    from paper_2412_19027_b200 import generators as G
+    from paper_2412_19027_b200.settings import SolverSettings
+    return SolverSettings(eps_feas=eps, precision=G.CONFIGS[config]["precision"])
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle restatement of the reference), run in a subprocess
+# ---------------------------------------------------------------------------
+
+def cpu_worker(args):
+    from oracle.ipm import OracleSolver
+    from paper_2412_19027_b200 import generators as G
+    prob = G.build(args.config)
+    cfg = settings_for(args.config, args.eps)
+    t0 = time.perf_counter()
+    solver = OracleSolver(prob, cfg)
+    setup = time.perf_counter() - t0
+    cap = args.cpu_max_iters or None
+    res = solver.solve(max_iterations_run=cap)
+    out = {"setup_s": setup, "solve_s": res.solve_seconds, "iterations": res.iterations,
+           "status": res.status, "obj": res.obj_primal}
+    print("CPUWORKER " + json.dumps(out), flush=True)
+
+
+def run_cpu_sample(args, max_iters):
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               CUDA_VISIBLE_DEVICES="")
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--config", args.config,
+           "--eps", str(args.eps), "--cpu-max-iters", str(max_iters)]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1800)
+    for line in out.stdout.splitlines():
+        if line.startswith("CPUWORKER "):
+            return json.loads(line[len("CPUWORKER "):])
+    raise RuntimeError(f"cpu worker failed: {out.stderr[-2000:]}")
+
+
+def cpu_iters_for_budget(args):
+    """Bounded sample: a 2-iteration probe sets the per-iteration cost, then the
+    sample runs as many iterations as fit in the CPU budget (at least 2)."""
+    probe = run_cpu_sample(args, 2)
+    per = probe["solve_s"] / max(1, probe["iterations"])
+    k = int(max(2, min(200, args.cpu_budget_s / max(per, 1e-6))))
+    return probe, k
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_19027_b200 import generators as G
+    from paper_2412_19027_b200.native import pdbl
+    from paper_2412_19027_b200.solver import Solver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    spec, desc = workload(args.config)
+    prob = G.build(args.config)
+    cfg = settings_for(args.config, args.eps)
+    solver = Solver(prob, cfg, device=local)
+    ctx = solver._ctx
+    info = solver.symbolic.info()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+
+    for _ in range(args.warmup):
+        res = solver.solve()
+    torch.cuda.synchronize()
+
+    ms = ctypes.c_double(0.0)
+    ctx.call("cipm_profile", 1)
+    ctx.call("cipm_launch_count", None, 1)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    iters = []
+    statuses = set()
+    for _ in range(args.steps):
+        flush.fill_(1.0)                 # L2 flush (256 MiB) outside the timed window
+        torch.cuda.synchronize()
+        ctx.call("cipm_timer", 0, None)
+        res = solver.solve()
+        ctx.call("cipm_timer", 1, ctypes.byref(ms))
+        step_ms.append(ms.value)
+        iters.append(res.iterations)
+        statuses.add(res.status)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctypes.c_int64(0)
+    ctx.call("cipm_launch_count", ctypes.byref(launches), 1)
+    kst = np.zeros(5)
+    ctx.call("cipm_kernel_stats", pdbl(kst))
+    ctx.call("cipm_profile", 0)
+
+    total_s = sum(step_ms) / 1e3
+    total_it = sum(iters)
+    if world > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = float(t.item())
+        it_t = torch.tensor([float(total_it)], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+        total_it_all = float(it_t.item())
+    else:
+        total_it_all = float(total_it)
+    value = total_it_all / total_s
+
+    # ---- e2e through the public API with host buffers ----
+    q_host = np.ascontiguousarray(prob.q)
+    b_host = np.ascontiguousarray(prob.b)
+    e2e_ms = []
+    e2e_it = 0
+    ctx.call("cipm_io_bytes", None, None, 1)
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        ctx.call("cipm_timer", 0, None)
+        solver.update_data(q=q_host, b=b_host)
+        r = solver.solve()
+        _ = (r.x.sum(), r.z.sum(), r.s.sum())
+        ctx.call("cipm_timer", 1, ctypes.byref(ms))
+        e2e_ms.append(ms.value)
+        e2e_it += r.iterations
+    h2d = ctypes.c_int64(0)
+    d2h = ctypes.c_int64(0)
+    ctx.call("cipm_io_bytes", ctypes.byref(h2d), ctypes.byref(d2h), 1)
+    e2e_s = sum(e2e_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = e2e_it * world / e2e_s
+
+    # ---- roofline of the dominant kernel class ----
+    hbm, peak_kind = peaks()
+    es = 4 if cfg.precision == "mixed" else 8
+    fac_ms, fac_n, sol_ms, sol_n, rhs_n = kst
+    nnz_l, dim = info["nnz_l"], info["dim"]
+    if sol_ms >= fac_ms and sol_n > 0:
+        # per right-hand side: L and L' sweeps read (value + int32 index) per nnz, plus 4 vector passes
+        bytes_per_rhs = 2 * (es + 4) * nnz_l + 4 * es * dim
+        achieved = bytes_per_rhs * (rhs_n / sol_n) / (sol_ms / sol_n / 1e3) / 1e9
+        dom = {"kernel": "supernodal triangular solve (forward_kernel + backward_kernel)",
+               "launches": int(sol_n), "avg_ms": sol_ms / sol_n,
+               "bytes_per_launch": bytes_per_rhs * rhs_n / sol_n,
+               "share_of_step": sol_ms / (sum(step_ms) or 1)}
+    else:
+        # numeric factorisation: write L (value + index) + read the assembled K values
+        bytes_fac = (es + 4) * nnz_l + es * info["nnz_storage"]
+        achieved = bytes_fac / (fac_ms / fac_n / 1e3) / 1e9
+        dom = {"kernel": "supernodal numeric factorisation (factor_kernel)", "launches": int(fac_n),
+               "avg_ms": fac_ms / fac_n, "bytes_per_launch": bytes_fac,
+               "share_of_step": fac_ms / (sum(step_ms) or 1),
+               "tflops": info["flops"] / (fac_ms / fac_n / 1e3) / 1e12}
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": ncu_traffic(args.config), "peak_source": peak_kind, "dominant": dom,
+            "factor_ms_avg": fac_ms / fac_n if fac_n else None,
+            "solve_ms_avg_per_pair": sol_ms / sol_n if sol_n else None}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sum(step_ms) / len(step_ms), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 iterate / f32 LDL' + f64 refinement" if cfg.precision == "mixed" else "f64",
+        "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
+        "config": {"workload": desc, "config": args.config, "n": prob.n, "m": prob.m, "nnz_A": prob.A.nnz,
+                   "precision": cfg.precision, "eps_feas": args.eps, "status": sorted(statuses),
+                   "iterations_per_solve": total_it / max(1, args.steps),
+                   "solve_time_s": sum(step_ms) / 1e3 / args.steps,
+                   "setup_s": solver.setup_seconds, "nnz_L": nnz_l, "supernodes": info["nsuper"],
+                   "etree_height_supernodes": info["height"], "F_LDL_gflop": info["flops"] / 1e9,
+                   "l2": "flushed between steps (256 MiB write), inputs resident in HBM",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d.value // max(1, args.steps),
+                "d2h_bytes_per_step": d2h.value // max(1, args.steps),
+                "path": "Solver.update_data(q, b) host arrays + Solver.solve() -> host x, z, s"},
+        "gpu_launches": int(launches.value),
+        "roofline": roof,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            probe, k = cpu_iters_for_budget(args)
+            sample = run_cpu_sample(args, k)
+            cpu_val = sample["iterations"] / sample["solve_s"]
+            line["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": 1, "kind": "port",
+                                    "sample": f"oracle restatement of the reference, {sample['iterations']} IPM "
+                                              f"iterations of {args.config} (setup {sample['setup_s']:.1f}s "
+                                              f"excluded), 1 thread",
+                                    "cpu_solve_s_per_iter": sample["solve_s"] / max(1, sample["iterations"])}
+        except Exception as e:  # never lose the GPU line over the CPU leg
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+                                    "sample": f"failed: {e}"[:300]}
+    solver.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle (the reference itself cannot travel to the box)
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec, desc = workload(args.config)
+    probe, k = cpu_iters_for_budget(args)
+    cores = 1
+    it_total, secs = 0, 0.0
+    for i in range(args.warmup + args.steps):
+        s = run_cpu_sample(args, min(k, 200))
+        if i >= args.warmup:
+            it_total += s["iterations"]
+            secs += s["solve_s"]
+    value = it_total / secs
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (seeded generator)",
+            "config": {"workload": desc, "config": args.config, "eps_feas": args.eps},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"oracle restatement (bit-exact vs the reference on the golden fixtures), "
+                                       f"up to {k} IPM iterations per step, setup excluded, 1 thread"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.cpu_worker:
+        cpu_worker(args)
+        return
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

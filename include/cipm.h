@@ -150,8 +150,18 @@ int cipm_get_direction(cipm_ctx *ctx, int combined, double *dx, double *dz, doub
 int cipm_get_vector(cipm_ctx *ctx, const char *name, double *out, int64_t *count);
 /* per-cone batched SOC residuals t^2 - |u|^2 with the reference's fixed order (steps.py:136-175) */
 int cipm_soc_residuals(cipm_ctx *ctx, const double *x, double *out);
+/* host<->device bytes moved by the API since the last reset (bench e2e accounting) */
+int cipm_io_bytes(cipm_ctx *ctx, int64_t *h2d, int64_t *d2h, int reset);
 /* kernel launches issued since the last reset (bench accounting) */
 int cipm_launch_count(cipm_ctx *ctx, int64_t *count, int reset);
+/* per-launch CUDA-event timing of the factorisation and triangular-solve kernels:
+ * cipm_profile(enable) clears and (de)activates; cipm_kernel_stats returns
+ * out[5] = {factor ms total, factor launches, solve ms total, solve launch pairs, rhs solved} */
+int cipm_profile(cipm_ctx *ctx, int enable);
+int cipm_kernel_stats(cipm_ctx *ctx, double *out);
+/* CUDA events on the context stream: op 0 records the start, op 1 the stop and
+ * returns the elapsed milliseconds */
+int cipm_timer(cipm_ctx *ctx, int op, double *ms);
 /* CUDA-event time (ms) of the last numeric factorisation and last triangular solve */
 int cipm_kernel_times(cipm_ctx *ctx, double *factor_ms, double *solve_ms);
 

@@ -134,14 +134,18 @@ class OracleKKT:
         self._fresh = False
 
     # symbolic analysis (system.py:188-240)
-    def symbolic_factor(self):
+    def symbolic_factor(self, perm=None):
+        """``perm`` (test hook) replaces the minimum-degree order, e.g. to probe
+        ordering sensitivity as in SURVEY.md §8(c)."""
         if self._symbolic_done:
             return
         L = lib()
         dim = self.dim
-        perm = np.empty(dim, dtype=np.int64)
-        if L.oracle_min_degree(dim, _p(self.rowptr), _p(self.colidx), _p(perm)) != 0:
-            raise MemoryError("oracle min-degree allocation failed")
+        if perm is None:
+            perm = np.empty(dim, dtype=np.int64)
+            if L.oracle_min_degree(dim, _p(self.rowptr), _p(self.colidx), _p(perm)) != 0:
+                raise MemoryError("oracle min-degree allocation failed")
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
         iperm = np.empty(dim, dtype=np.int64)
         iperm[perm] = np.arange(dim, dtype=np.int64)
         self.perm, self.iperm = perm, iperm

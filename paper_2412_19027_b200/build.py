@@ -23,6 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["capi.cu", "ldl.cu", "cones.cu", "vec.cu"]
 CPP_SOURCES = ["symbolic.cpp"]
+NO_FMAD = {"cones.cu"}
 
 
 def _headers():
@@ -44,7 +45,10 @@ def _compile(src, force):
     if not force and not _stale(obj, path):
         return obj
     if src.endswith(".cu"):
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        # cone kernels: no FMA contraction, so the barrier / BFGS / conjugate-point
+        # arithmetic rounds like the reference's numpy (exp/pow status parity)
+        extra = ["-fmad=false"] if src in NO_FMAD else []
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra, "-Xcompiler", "-fPIC",
                "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include"), "-c", path, "-o", obj]
     else:
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-I", os.path.join(ROOT, "include"),

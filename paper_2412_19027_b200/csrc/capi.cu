@@ -71,6 +71,7 @@ int sync_err(Ctx& c) {
 }
 
 int read_sc(Ctx& c) {
+    c.d2h_bytes += sizeof(double) * CIPM_SC_COUNT + sizeof(int);
     CIPM_CUDA(cudaMemcpyAsync(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost, c.stream));
     CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
@@ -87,6 +88,7 @@ int refine(Ctx& c, int nrhs, int* steps_out) {
         k_refine_step(c, nrhs, active);
         for (int q = 0; q < nrhs; ++q)
             if (active[q]) k_kkt_residual_one(c, q);
+        c.d2h_bytes += sizeof(double) * 16 + sizeof(int);
         CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
         CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         CIPM_CUDA(cudaStreamSynchronize(c.stream));
@@ -206,6 +208,13 @@ int cipm_symbolic_array(const cipm_symbolic* sym, const char* name, void* dst, i
     ARR("map_a", s.map_a)
     ARR("map_diag", s.map_diag)
     ARR("map_hblk", s.map_hblk)
+    ARR("cb_off", s.cb_off)
+    ARR("push_pos", s.push_pos)
+    ARR("irow_ptr", s.irow_ptr)
+    ARR("inbox_tgt", s.inbox_tgt)
+    ARR("cv_off", s.cv_off)
+    ARR("vpush_pos", s.vpush_pos)
+    ARR("vcol_ptr", s.vcol_ptr)
 #undef ARR
     if (!es) return CIPM_E_ARG;
     if (count) *count = cnt;
@@ -399,6 +408,15 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(upload(c, &c.sym.map_a, S.map_a.data(), (int64_t)S.map_a.size()));
     TRY(upload(c, &c.sym.map_diag, S.map_diag.data(), c.dim));
     TRY(upload(c, &c.sym.map_hblk, S.map_hblk.data(), (int64_t)S.map_hblk.size()));
+    TRY(upload(c, &c.sym.cb_off, S.cb_off.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.push_pos, S.push_pos.data(), (int64_t)S.push_pos.size()));
+    TRY(upload(c, &c.sym.irow_ptr, S.irow_ptr.data(), (int64_t)S.irow_ptr.size()));
+    TRY(upload(c, &c.sym.inbox_tgt, S.inbox_tgt.data(), (int64_t)S.inbox_tgt.size()));
+    TRY(upload(c, &c.sym.cv_off, S.cv_off.data(), S.nsuper + 1));
+    TRY(upload(c, &c.sym.vpush_pos, S.vpush_pos.data(), (int64_t)S.vpush_pos.size()));
+    TRY(upload(c, &c.sym.vcol_ptr, S.vcol_ptr.data(), (int64_t)S.vcol_ptr.size()));
+    c.sym.ninbox = S.cb_off[S.nsuper];
+    c.sym.nv = S.cv_off[S.nsuper];
     if ((int64_t)S.map_hblk.size() != c.hblk_total) {
         fprintf(stderr, "[cipm] H block map size mismatch (%zu vs %lld)\n", S.map_hblk.size(),
                 (long long)c.hblk_total);
@@ -420,6 +438,12 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         CIPM_CUDA(cudaMalloc(&p, es * 2 * std::max<int64_t>(c.dim, 1)));
         c.allocations.push_back(p);
         c.rt = p;
+        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(c.sym.ninbox, 1)));
+        c.allocations.push_back(p);
+        c.inbox = p;
+        CIPM_CUDA(cudaMalloc(&p, es * 2 * std::max<int64_t>(c.sym.nv, 1)));
+        c.allocations.push_back(p);
+        c.vin = p;
     }
     TRY(dalloc(c, &c.fac_count, S.nsuper));
     TRY(dalloc(c, &c.bwd_done, S.nsuper));
@@ -468,6 +492,7 @@ int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const d
     CIPM_CUDA(cudaMemcpyAsync(c.dr, dr, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
     CIPM_CUDA(cudaMemcpyAsync(c.dc, dc, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
     c.c_obj = c_obj;
+    c.h2d_bytes += (int64_t)sizeof(double) * (c.p_nnz + 2 * c.a_nnz + 2 * c.n + 2 * c.m);
     k_build_base(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
     return CIPM_OK;
@@ -484,6 +509,9 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     if (c.h_rstate) cudaFreeHost(c.h_rstate);
     for (int i = 0; i < 4; ++i)
         if (c.ev[i]) cudaEventDestroy(c.ev[i]);
+    for (auto e : c.ev_pool) cudaEventDestroy(e);
+    if (c.t_start) cudaEventDestroy(c.t_start);
+    if (c.t_stop) cudaEventDestroy(c.t_stop);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
     delete h;
 }
@@ -590,6 +618,7 @@ int cipm_read_scalars(cipm_ctx* h, double* out) {
 int cipm_get_iterate(cipm_ctx* h, int which, double* x, double* z, double* s, double* tkm) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    c.d2h_bytes += (int64_t)sizeof(double) * ((x ? c.n : 0) + (z ? c.m : 0) + (s ? c.m : 0) + (tkm ? CIPM_SC_COUNT : 0));
     const double* px = which ? c.bx : c.x;
     const double* pz = which ? c.bz : c.z;
     const double* ps = which ? c.bs : c.s;
@@ -711,9 +740,69 @@ int cipm_soc_residuals(cipm_ctx* h, const double* x, double* out) {
     return CIPM_OK;
 }
 
+int cipm_io_bytes(cipm_ctx* h, int64_t* h2d, int64_t* d2h, int reset) {
+    if (h2d) *h2d = h->c.h2d_bytes;
+    if (d2h) *d2h = h->c.d2h_bytes;
+    if (reset) h->c.h2d_bytes = h->c.d2h_bytes = 0;
+    return CIPM_OK;
+}
+
 int cipm_launch_count(cipm_ctx* h, int64_t* count, int reset) {
     if (count) *count = h->c.launches;
     if (reset) h->c.launches = 0;
+    return CIPM_OK;
+}
+
+int cipm_profile(cipm_ctx* h, int enable) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    c.profile = enable != 0;
+    c.solve_rhs = 0;
+    c.ev_factor.clear();
+    c.ev_solve.clear();
+    return CIPM_OK;
+}
+
+int cipm_kernel_stats(cipm_ctx* h, double* out) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    double fs = 0.0, ss = 0.0;
+    for (auto& pr : c.ev_factor) {
+        float ms = 0.f;
+        CIPM_CUDA(cudaEventElapsedTime(&ms, c.ev_pool[pr.first], c.ev_pool[pr.second]));
+        fs += ms;
+    }
+    for (auto& pr : c.ev_solve) {
+        float ms = 0.f;
+        CIPM_CUDA(cudaEventElapsedTime(&ms, c.ev_pool[pr.first], c.ev_pool[pr.second]));
+        ss += ms;
+    }
+    out[0] = fs;
+    out[1] = (double)c.ev_factor.size();
+    out[2] = ss;
+    out[3] = (double)c.ev_solve.size();
+    out[4] = (double)c.solve_rhs;
+    c.solve_rhs = 0;
+    c.ev_factor.clear();
+    c.ev_solve.clear();
+    return CIPM_OK;
+}
+
+int cipm_timer(cipm_ctx* h, int op, double* ms) {
+    Ctx& c = h->c;
+    if (!c.t_start) {
+        CIPM_CUDA(cudaEventCreate(&c.t_start));
+        CIPM_CUDA(cudaEventCreate(&c.t_stop));
+    }
+    if (op == 0) {
+        CIPM_CUDA(cudaEventRecord(c.t_start, c.stream));
+        return CIPM_OK;
+    }
+    CIPM_CUDA(cudaEventRecord(c.t_stop, c.stream));
+    CIPM_CUDA(cudaEventSynchronize(c.t_stop));
+    float v = 0.f;
+    CIPM_CUDA(cudaEventElapsedTime(&v, c.t_start, c.t_stop));
+    if (ms) *ms = v;
     return CIPM_OK;
 }
 

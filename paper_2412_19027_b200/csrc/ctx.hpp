@@ -37,7 +37,15 @@ struct DevSymbolic {
     int64_t* map_a = nullptr;
     int64_t* map_diag = nullptr;
     int64_t* map_hblk = nullptr;
+    int64_t* cb_off = nullptr;
+    int64_t* push_pos = nullptr;
+    int64_t* irow_ptr = nullptr;
+    int32_t* inbox_tgt = nullptr;
+    int64_t* cv_off = nullptr;
+    int64_t* vpush_pos = nullptr;
+    int64_t* vcol_ptr = nullptr;
     int64_t nnz_storage = 0;
+    int64_t ninbox = 0, nv = 0;
 };
 
 struct Ctx {
@@ -105,7 +113,9 @@ struct Ctx {
     int32_t* tickets = nullptr;      // [0] factor, [1] forward, [2] backward
     double* sn_maxd = nullptr;       // subtree max |D|
     int32_t* bumps = nullptr;
-    int factor_blocks = 0, solve_blocks = 0;
+    void* inbox = nullptr;           // factor contribution inbox (T)
+    void* vin = nullptr;             // solve contribution inbox, 2 x nv (T)
+    int factor_blocks = 0, solve_blocks = 0, factor_smem = 0;
 
     // refinement (up to 2 right-hand sides, [rhs][dim])
     double *rb = nullptr, *rx = nullptr, *rr = nullptr, *rbest = nullptr;
@@ -125,11 +135,27 @@ struct Ctx {
     double* h_rstate = nullptr;
 
     int64_t launches = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;   // host<->device traffic of the public API
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // profiling: CUDA-event pairs around every factorisation / triangular-solve launch
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_factor, ev_solve;
+    int64_t solve_rhs = 0;            // right-hand sides processed by the profiled solve launches
+    cudaEvent_t t_start = nullptr, t_stop = nullptr;
     float factor_ms = 0.f, solve_ms = 0.f;
 
     std::vector<void*> allocations;
 };
+
+inline cudaEvent_t pooled_event(Ctx& c, size_t idx) {
+    while (c.ev_pool.size() <= idx) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c.ev_pool.push_back(e);
+    }
+    return c.ev_pool[idx];
+}
 
 // ---- launchers (implemented in vec.cu / cones.cu / ldl.cu) ----
 // vec.cu

@@ -60,7 +60,16 @@ __global__ void add_static_reg(T* base, const int64_t* map_diag, int64_t n, int6
 }
 
 // ---------------------------------------------------------------------------
-// numeric factorisation
+// numeric factorisation (push/pull inbox scheme)
+//
+// Task J (one CTA): wait until its children are done; copy its panel to shared
+// memory; gather its inbox — every contribution block entry of every descendant
+// that lands in J, pre-sorted by (row, column, source) so each thread owns one
+// panel row and accumulates runs in registers (no atomics, no barriers, fixed
+// order); factor the dense panel; write L and D; then compute its own packed
+// contribution block C_J = L_off D L_off' and scatter it into the ancestors'
+// inboxes.  The expensive dot products therefore run in the producer, spread
+// over many CTAs, instead of serially in the consumer.
 // ---------------------------------------------------------------------------
 
 struct FactorArgs {
@@ -68,39 +77,33 @@ struct FactorArgs {
     const int32_t* order;
     const int32_t* sn_col;
     const int64_t* sn_rptr;
-    const int32_t* sn_rows;
     const int64_t* sn_loff;
     const int32_t* sn_parent;
     const int32_t* sn_nchild;
-    const int64_t* upd_ptr;
-    const int32_t* upd_src;
-    const int32_t* upd_p0;
-    const int32_t* upd_p1;
+    const int64_t* cb_off;
+    const int64_t* push_pos;
+    const int64_t* irow_ptr;
+    const int32_t* inbox_tgt;
     const int8_t* sign;
     int32_t* count;
     int32_t* ticket;
-    double* maxd;
+    double* maxd;        // max |D| over the subtree, accumulated by the children (atomic max)
     int32_t* bumps;
     int* err;
     double delta_s, delta_d;
+    int64_t smem_cap;    // panel elements that fit the dynamic shared memory
 };
 
-constexpr int kRelCap = 2048;
-
-__device__ __forceinline__ int find_row(const int32_t* rows, int r, int32_t key) {
-    int lo = 0, hi = r;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (rows[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+__device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec) {
+__global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+                                                     T* __restrict__ inbox) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sp = reinterpret_cast<T*>(smem_raw);
     __shared__ int s_task;
-    __shared__ int s_rel[kRelCap];
     __shared__ double s_piv;
     __shared__ double s_runmax;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -112,104 +115,115 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
         const int J = a.order[t];
         if (tid == 0) {
             const int need = a.sn_nchild[J];
-            while (ld_acquire(a.count + J) < need) __nanosleep(100);
+            while (ld_acquire(a.count + J) < need) __nanosleep(64);
+            s_runmax = __ldcg(a.maxd + J);
         }
         __syncthreads();
-
         const int c0 = a.sn_col[J];
         const int w = a.sn_col[J + 1] - c0;
         const int64_t r0 = a.sn_rptr[J];
         const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const int32_t* rowsJ = a.sn_rows + r0;
+        const int o = r - w;
         T* L = lval + a.sn_loff[J];
-        double runmax = 0.0;
+        const int64_t psize = (int64_t)r * w;
+        const bool in_smem = psize <= a.smem_cap;
+        T* P = in_smem ? sp : L;
+        if (in_smem)
+            for (int64_t i = tid; i < psize; i += nt) sp[i] = L[i];
+        __syncthreads();
 
-        // 1. gather descendant updates in list order
-        for (int64_t u = a.upd_ptr[J]; u < a.upd_ptr[J + 1]; ++u) {
-            const int K = a.upd_src[u];
-            const int p0 = a.upd_p0[u], p1 = a.upd_p1[u];
-            const int kc0 = a.sn_col[K];
-            const int wK = a.sn_col[K + 1] - kc0;
-            const int64_t kr0 = a.sn_rptr[K];
-            const int rK = (int)(a.sn_rptr[K + 1] - kr0);
-            const int32_t* rowsK = a.sn_rows + kr0;
-            const T* LK = lval + a.sn_loff[K];
-            const T* DK = dvec + kc0;
-            const int nrow = rK - p0, ncol = p1 - p0;
-            runmax = fmax(runmax, ldcg(a.maxd + K));
-            const bool cached = nrow <= kRelCap;
-            if (cached)
-                for (int i = tid; i < nrow; i += nt) s_rel[i] = find_row(rowsJ, r, rowsK[p0 + i]);
-            __syncthreads();
-            const int64_t total = (int64_t)nrow * ncol;
-            for (int64_t idx = tid; idx < total; idx += nt) {
-                const int i = (int)(idx % nrow);
-                const int cc = (int)(idx / nrow);
-                if (i < cc) continue;
-                T acc = (T)0;
-                for (int k = 0; k < wK; ++k)
-                    acc += ldcg(LK + (int64_t)k * rK + p0 + i) * ldcg(DK + k) * ldcg(LK + (int64_t)k * rK + p0 + cc);
-                const int tr = cached ? s_rel[i] : find_row(rowsJ, r, rowsK[p0 + i]);
-                const int tc = rowsK[p0 + cc] - c0;
-                L[(int64_t)tc * r + tr] -= acc;
+        // 1. gather the inbox: thread per panel row, register runs per target column
+        for (int tr = tid; tr < r; tr += nt) {
+            const int64_t lo = a.irow_ptr[r0 + tr], hi = a.irow_ptr[r0 + tr + 1];
+            int cur = -1;
+            T acc = (T)0;
+            for (int64_t e = lo; e < hi; ++e) {
+                const int tg = a.inbox_tgt[e];
+                const T v = __ldcg(inbox + e);
+                if (tg != cur) {
+                    if (cur >= 0) P[cur] -= acc;
+                    cur = tg;
+                    acc = v;
+                } else {
+                    acc += v;
+                }
             }
-            __syncthreads();
+            if (cur >= 0) P[cur] -= acc;
         }
+        __syncthreads();
 
         // 2. dense LDL' of the panel (right-looking inside the panel)
-        if (tid == 0) s_runmax = runmax;
-        __syncthreads();
         for (int j = 0; j < w; ++j) {
             if (tid == 0) {
-                double d = (double)L[(int64_t)j * r + j];
+                double d = (double)P[(int64_t)j * r + j];
                 const double bound = a.delta_s + a.delta_d * s_runmax;
                 if (fabs(d) < bound) {
                     d = a.sign[c0 + j] > 0 ? bound : -bound;
                     atomicAdd(a.bumps, 1);
                 }
-                T dt = (T)d;
+                const T dt = (T)d;
                 if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
                 dvec[c0 + j] = dt;
-                L[(int64_t)j * r + j] = (T)1;
+                P[(int64_t)j * r + j] = (T)1;
                 s_piv = (double)dt;
                 s_runmax = fmax(s_runmax, fabs(d));
             }
             __syncthreads();
             const T d = (T)s_piv;
-            T* Lj = L + (int64_t)j * r;
-            for (int i = j + 1 + tid; i < r; i += nt) Lj[i] = Lj[i] / d;
+            T* Pj = P + (int64_t)j * r;
+            for (int i = j + 1 + tid; i < r; i += nt) Pj[i] = Pj[i] / d;
             __syncthreads();
             const int rem_c = w - j - 1;
             if (rem_c > 0) {
-                const int64_t total = (int64_t)rem_c * (r - j - 1);
+                const int rows = r - j - 1;
+                const int64_t total = (int64_t)rem_c * rows;
                 for (int64_t idx = tid; idx < total; idx += nt) {
-                    const int i = j + 1 + (int)(idx % (r - j - 1));
-                    const int c = j + 1 + (int)(idx / (r - j - 1));
+                    const int i = j + 1 + (int)(idx % rows);
+                    const int c = j + 1 + (int)(idx / rows);
                     if (i < c) continue;
-                    L[(int64_t)c * r + i] -= Lj[i] * d * Lj[c];
+                    P[(int64_t)c * r + i] -= Pj[i] * d * Pj[c];
                 }
             }
             __syncthreads();
         }
-        // 3. publish
+
+        // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
+        if (in_smem)
+            for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
+        if (o > 0) {
+            const T* Dj = dvec + c0;
+            const int64_t base = a.cb_off[J];
+            const int64_t tot = (int64_t)o * o;
+            for (int64_t idx = tid; idx < tot; idx += nt) {
+                const int aa = (int)(idx % o), bb = (int)(idx / o);
+                if (aa < bb) continue;
+                T acc = (T)0;
+                for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * Dj[k] * P[(int64_t)k * r + w + bb];
+                const int64_t tpk = (int64_t)bb * o - (int64_t)bb * (bb - 1) / 2 + (aa - bb);
+                inbox[a.push_pos[base + tpk]] = acc;
+            }
+        }
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-            a.maxd[J] = s_runmax;
-            __threadfence();
-            const int P = a.sn_parent[J];
-            if (P >= 0) atomicAdd(a.count + P, 1);
+            const int Pn = a.sn_parent[J];
+            if (Pn >= 0) {
+                atomic_max_pos(a.maxd + Pn, s_runmax);
+                __threadfence();
+                atomicAdd(a.count + Pn, 1);
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// triangular solves, one warp per supernode task
+// triangular solves, one warp per supernode task (push/pull for the forward sweep)
 // ---------------------------------------------------------------------------
 
 struct SolveArgs {
     int32_t nsuper;
     int64_t dim;
+    int64_t nv;          // vector inbox length per right-hand side
     const int32_t* order;
     const int32_t* sn_col;
     const int64_t* sn_rptr;
@@ -217,17 +231,16 @@ struct SolveArgs {
     const int64_t* sn_loff;
     const int32_t* sn_parent;
     const int32_t* sn_nchild;
-    const int64_t* upd_ptr;
-    const int32_t* upd_src;
-    const int32_t* upd_p0;
-    const int32_t* upd_p1;
-    int32_t* count;     // forward: children done; backward: done flags
+    const int64_t* cv_off;
+    const int64_t* vpush_pos;
+    const int64_t* vcol_ptr;
+    int32_t* count;      // forward: children done; backward: done flags
     int32_t* ticket;
-    int act0, act1;     // active right-hand sides
+    int act0, act1;      // active right-hand sides
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x) {
+__global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
@@ -245,32 +258,52 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
         const int64_t r0 = a.sn_rptr[J];
         const int r = (int)(a.sn_rptr[J + 1] - r0);
         const T* L = lval + a.sn_loff[J];
+        const int64_t cvo = a.cv_off[J];
         for (int q = 0; q < 2; ++q) {
             if (!(q == 0 ? a.act0 : a.act1)) continue;
-            T* xv = x + (int64_t)q * a.dim;
-            T* xJ = xv + c0;
-            for (int64_t u = a.upd_ptr[J]; u < a.upd_ptr[J + 1]; ++u) {
-                const int K = a.upd_src[u];
-                const int p0 = a.upd_p0[u], p1 = a.upd_p1[u];
-                const int kc0 = a.sn_col[K];
-                const int wK = a.sn_col[K + 1] - kc0;
-                const int64_t kr0 = a.sn_rptr[K];
-                const int rK = (int)(a.sn_rptr[K + 1] - kr0);
-                const T* LK = lval + a.sn_loff[K];
-                const int32_t* rowsK = a.sn_rows + kr0;
-                for (int c = p0 + lane; c < p1; c += 32) {
+            T* xJ = x + (int64_t)q * a.dim + c0;
+            T* vq = vin + (int64_t)q * a.nv;
+            if (w <= 32) {
+                T xr = (T)0;
+                if (lane < w) {
                     T acc = (T)0;
-                    for (int k = 0; k < wK; ++k) acc += LK[(int64_t)k * rK + c] * __ldcg(xv + kc0 + k);
-                    xJ[rowsK[c] - c0] -= acc;
+                    for (int64_t e = a.vcol_ptr[c0 + lane]; e < a.vcol_ptr[c0 + lane + 1]; ++e) acc += __ldcg(vq + e);
+                    xr = xJ[lane] - acc;
+                }
+                for (int j = 0; j < w; ++j) {
+                    const T xj = __shfl_sync(0xffffffffu, xr, j);
+                    if (lane > j && lane < w) xr -= L[(int64_t)j * r + lane] * xj;
+                }
+                if (lane < w) xJ[lane] = xr;
+                for (int i0 = w; i0 < r; i0 += 32) {
+                    const int i = i0 + lane;
+                    T acc = (T)0;
+                    for (int k = 0; k < w; ++k) {
+                        const T xk = __shfl_sync(0xffffffffu, xr, k);
+                        if (i < r) acc += L[(int64_t)k * r + i] * xk;
+                    }
+                    if (i < r) vq[a.vpush_pos[cvo + i - w]] = acc;
+                }
+            } else {
+                for (int j = lane; j < w; j += 32) {
+                    T acc = (T)0;
+                    for (int64_t e = a.vcol_ptr[c0 + j]; e < a.vcol_ptr[c0 + j + 1]; ++e) acc += __ldcg(vq + e);
+                    xJ[j] -= acc;
                 }
                 __syncwarp();
+                for (int j = 0; j < w; ++j) {
+                    const T xj = xJ[j];
+                    __syncwarp();
+                    for (int i = j + 1 + lane; i < w; i += 32) xJ[i] -= L[(int64_t)j * r + i] * xj;
+                    __syncwarp();
+                }
+                for (int i = w + lane; i < r; i += 32) {
+                    T acc = (T)0;
+                    for (int k = 0; k < w; ++k) acc += L[(int64_t)k * r + i] * xJ[k];
+                    vq[a.vpush_pos[cvo + i - w]] = acc;
+                }
             }
-            for (int j = 0; j < w; ++j) {
-                const T xj = xJ[j];
-                __syncwarp();
-                for (int i = j + 1 + lane; i < w; i += 32) xJ[i] -= L[(int64_t)j * r + i] * xj;
-                __syncwarp();
-            }
+            __syncwarp();
         }
         __threadfence();
         __syncwarp();
@@ -305,23 +338,36 @@ __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __r
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xv = x + (int64_t)q * a.dim;
             T* xJ = xv + c0;
-            for (int j = lane; j < w; j += 32) xJ[j] = xJ[j] / dvec[c0 + j];   // D solve (ldl.py:101-102)
-            __syncwarp();
-            for (int j = 0; j < w; ++j) {
-                const T* Lj = L + (int64_t)j * r;
-                T acc = (T)0;
-                for (int i = w + lane; i < r; i += 32) acc += Lj[i] * __ldcg(xv + rowsJ[i]);
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-                if (lane == 0) xJ[j] -= acc;
-            }
-            __syncwarp();
-            for (int j = w - 1; j >= 0; --j) {
-                const T* Lj = L + (int64_t)j * r;
-                T acc = (T)0;
-                for (int i = j + 1 + lane; i < w; i += 32) acc += Lj[i] * xJ[i];
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-                if (lane == 0) xJ[j] -= acc;
+            if (w <= 32) {
+                T xr = lane < w ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
+                for (int i = w; i < r; ++i) {
+                    const T xi = __ldcg(xv + rowsJ[i]);
+                    if (lane < w) xr -= L[(int64_t)lane * r + i] * xi;
+                }
+                for (int j = w - 1; j >= 0; --j) {
+                    const T xj = __shfl_sync(0xffffffffu, xr, j);
+                    if (lane < j) xr -= L[(int64_t)lane * r + j] * xj;
+                }
+                if (lane < w) xJ[lane] = xr;
+            } else {
+                for (int j = lane; j < w; j += 32) xJ[j] = xJ[j] / dvec[c0 + j];
                 __syncwarp();
+                for (int j = 0; j < w; ++j) {
+                    const T* Lj = L + (int64_t)j * r;
+                    T acc = (T)0;
+                    for (int i = w + lane; i < r; i += 32) acc += Lj[i] * __ldcg(xv + rowsJ[i]);
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+                    if (lane == 0) xJ[j] -= acc;
+                }
+                __syncwarp();
+                for (int j = w - 1; j >= 0; --j) {
+                    const T* Lj = L + (int64_t)j * r;
+                    T acc = (T)0;
+                    for (int i = j + 1 + lane; i < w; i += 32) acc += Lj[i] * xJ[i];
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+                    if (lane == 0) xJ[j] -= acc;
+                    __syncwarp();
+                }
             }
         }
         __threadfence();
@@ -358,6 +404,7 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     SolveArgs a;
     a.nsuper = c.sym.nsuper;
     a.dim = c.dim;
+    a.nv = c.sym.nv;
     a.order = c.sym.order;
     a.sn_col = c.sym.sn_col;
     a.sn_rptr = c.sym.sn_rptr;
@@ -365,10 +412,9 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.sn_loff = c.sym.sn_loff;
     a.sn_parent = c.sym.sn_parent;
     a.sn_nchild = c.sym.sn_nchild;
-    a.upd_ptr = c.sym.upd_ptr;
-    a.upd_src = c.sym.upd_src;
-    a.upd_p0 = c.sym.upd_p0;
-    a.upd_p1 = c.sym.upd_p1;
+    a.cv_off = c.sym.cv_off;
+    a.vpush_pos = c.sym.vpush_pos;
+    a.vcol_ptr = c.sym.vcol_ptr;
     a.count = count;
     a.ticket = ticket;
     a.act0 = act0;
@@ -399,14 +445,13 @@ int factor_t(Ctx& c) {
     a.order = c.sym.order;
     a.sn_col = c.sym.sn_col;
     a.sn_rptr = c.sym.sn_rptr;
-    a.sn_rows = c.sym.sn_rows;
     a.sn_loff = c.sym.sn_loff;
     a.sn_parent = c.sym.sn_parent;
     a.sn_nchild = c.sym.sn_nchild;
-    a.upd_ptr = c.sym.upd_ptr;
-    a.upd_src = c.sym.upd_src;
-    a.upd_p0 = c.sym.upd_p0;
-    a.upd_p1 = c.sym.upd_p1;
+    a.cb_off = c.sym.cb_off;
+    a.push_pos = c.sym.push_pos;
+    a.irow_ptr = c.sym.irow_ptr;
+    a.inbox_tgt = c.sym.inbox_tgt;
     a.sign = c.sym.sign;
     a.count = c.fac_count;
     a.ticket = c.tickets;
@@ -415,12 +460,21 @@ int factor_t(Ctx& c) {
     a.err = c.err;
     a.delta_s = c.delta_s;
     a.delta_d = c.delta_d;
+    a.smem_cap = c.factor_smem / (int64_t)sizeof(T);
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
+    cudaMemsetAsync(c.sn_maxd, 0, sizeof(double) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
     cudaMemsetAsync(c.bumps, 0, sizeof(int32_t), c.stream);
-    cudaEventRecord(c.ev[0], c.stream);
-    factor_kernel<T><<<c.factor_blocks, 256, 0, c.stream>>>(a, (T*)c.lval, (T*)c.dvec);
-    cudaEventRecord(c.ev[1], c.stream);
+    int e0 = 0;
+    if (c.profile) {
+        e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
+        cudaEventRecord(pooled_event(c, e0), c.stream);
+    }
+    factor_kernel<T><<<c.factor_blocks, 256, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+    if (c.profile) {
+        cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
+        c.ev_factor.emplace_back(e0, e0 + 1);
+    }
     c.launches++;
     return CIPM_OK;
 }
@@ -432,12 +486,19 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
-    cudaEventRecord(c.ev[2], c.stream);
+    int e0 = 0;
+    if (c.profile) {
+        e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
+        cudaEventRecord(pooled_event(c, e0), c.stream);
+    }
     SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
-    forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t);
+    forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
     backward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
-    cudaEventRecord(c.ev[3], c.stream);
+    if (c.profile) {
+        cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
+        c.ev_solve.emplace_back(e0, e0 + 1);
+    }
     scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1);
     c.launches += 4;
 }
@@ -462,6 +523,7 @@ int k_factor(Ctx& c) {
 // one refinement correction: x += solve(r) for the active right-hand sides
 void k_refine_step(Ctx& c, int nrhs, const int* active) {
     const int a0 = active[0], a1 = nrhs > 1 ? active[1] : 0;
+    if (c.profile) c.solve_rhs += a0 + a1;
     if (c.precision == CIPM_FULL) refine_solve_t<double>(c, a0, a1);
     else refine_solve_t<float>(c, a0, a1);
 }
@@ -478,11 +540,20 @@ static int sm_count() {
 }
 
 int factor_grid(Ctx& c) {
+    // dynamic shared memory: the largest panel below 96 KiB; bigger panels run in place
+    const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
+    int64_t cap = c.host_sym.max_panel * es;
+    if (cap > 96 * 1024) cap = 96 * 1024;
+    if (cap < 1024) cap = 1024;
+    c.factor_smem = (int)cap;
     int per = 0;
-    if (c.precision == CIPM_FULL)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<double>, 256, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<float>, 256, 0);
+    if (c.precision == CIPM_FULL) {
+        cudaFuncSetAttribute(factor_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.factor_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<double>, 256, c.factor_smem);
+    } else {
+        cudaFuncSetAttribute(factor_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.factor_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<float>, 256, c.factor_smem);
+    }
     if (per < 1) per = 1;
     int64_t g = (int64_t)sm_count() * per;
     if (g > c.sym.nsuper) g = c.sym.nsuper;

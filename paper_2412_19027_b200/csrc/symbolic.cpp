@@ -153,12 +153,19 @@ std::vector<int32_t> etree(const std::vector<int64_t>& cp, const std::vector<int
     return parent;
 }
 
-std::vector<int32_t> postorder(const std::vector<int32_t>& parent, int64_t dim) {
+// postorder; children are visited in ascending (weight, index) order so the
+// child with the largest column count — the chain continuation of a dense
+// tail — is numbered immediately before its parent and can join its supernode
+std::vector<int32_t> postorder(const std::vector<int32_t>& parent, const std::vector<int64_t>& weight,
+                               int64_t dim) {
+    std::vector<int32_t> kids(dim);
+    std::iota(kids.begin(), kids.end(), 0);
+    std::stable_sort(kids.begin(), kids.end(), [&](int32_t a, int32_t b) { return weight[a] > weight[b]; });
     std::vector<int32_t> head(dim, -1), next(dim, -1);
-    for (int64_t j = dim - 1; j >= 0; --j) {       // children in ascending order
+    for (int32_t j : kids) {                        // push heaviest first -> visited last
         if (parent[j] == -1) continue;
         next[j] = head[parent[j]];
-        head[parent[j]] = (int32_t)j;
+        head[parent[j]] = j;
     }
     std::vector<int32_t> post;
     post.reserve(dim);
@@ -207,7 +214,16 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     std::vector<int32_t> ci;
     permuted_upper(g, iperm, dim, cp, ci);
     std::vector<int32_t> parent = etree(cp, ci, dim);
-    std::vector<int32_t> post = postorder(parent, dim);
+    std::vector<int64_t> cnt0(dim, 0);
+    {
+        std::vector<int32_t> fl(dim, -1);
+        for (int64_t j = 0; j < dim; ++j) {
+            fl[j] = (int32_t)j;
+            for (int64_t p = cp[j]; p < cp[j + 1]; ++p)
+                for (int32_t i = ci[p]; fl[i] != j; i = parent[i]) { cnt0[i]++; fl[i] = (int32_t)j; }
+        }
+    }
+    std::vector<int32_t> post = postorder(parent, cnt0, dim);
     {
         std::vector<int32_t> p2(dim);
         for (int64_t k = 0; k < dim; ++k) p2[k] = perm[post[k]];
@@ -251,7 +267,9 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         if (parent[j] != -1) nchild[parent[j]]++;
     std::vector<int32_t> fstart;
     for (int64_t j = 0; j < dim; ++j) {
-        bool cont = j > 0 && parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1 && nchild[j] == 1;
+        // columns j-1, j share a structure when j is j-1's parent and the counts nest;
+        // other subtrees may attach to j (they become children of the supernode)
+        bool cont = j > 0 && parent[j - 1] == j && cnt[j - 1] == cnt[j] + 1;
         if (!cont) fstart.push_back((int32_t)j);
     }
     const int64_t nf = (int64_t)fstart.size();
@@ -342,6 +360,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         S.sn_loff[J + 1] = S.sn_loff[J] + w * r;
         S.max_width = std::max(S.max_width, w);
         S.max_rows = std::max(S.max_rows, r);
+        S.max_panel = std::max(S.max_panel, w * r);
     }
     S.nnz_storage = S.sn_loff[ns];
     S.sn_parent.assign(ns, -1);
@@ -387,6 +406,99 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         }
     }
     S.n_updates = S.upd_ptr[ns];
+    // inbox maps for the push/pull factorisation and forward solve
+    {
+        S.cb_off.assign(ns + 1, 0);
+        S.cv_off.assign(ns + 1, 0);
+        for (int32_t K = 0; K < ns; ++K) {
+            int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+            int64_t o = (S.sn_rptr[K + 1] - S.sn_rptr[K]) - w;
+            S.cb_off[K + 1] = S.cb_off[K] + o * (o + 1) / 2;
+            S.cv_off[K + 1] = S.cv_off[K] + o;
+        }
+        const int64_t nrec = S.cb_off[ns];
+        const int64_t nrow_all = (int64_t)S.sn_rows.size();
+        // pass 1: count entries per (J, tr) bucket (global row slot = sn_rptr[J] + tr)
+        std::vector<int64_t> cnt_row(nrow_all + 1, 0);
+        std::vector<int32_t> tr_of;   // per K scratch: local row in the target supernode
+        for (int pass = 0; pass < 2; ++pass) {
+            std::vector<int64_t> fillp;
+            if (pass == 1) {
+                S.irow_ptr.assign(nrow_all + 1, 0);
+                for (int64_t t = 0; t < nrow_all; ++t) S.irow_ptr[t + 1] = S.irow_ptr[t] + cnt_row[t];
+                S.push_pos.assign(nrec, 0);
+                S.inbox_tgt.assign(nrec, 0);
+                fillp.assign(S.irow_ptr.begin(), S.irow_ptr.end() - 1);
+            }
+            for (int32_t K = 0; K < ns; ++K) {
+                const int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+                const int64_t r0 = S.sn_rptr[K];
+                const int64_t o = (S.sn_rptr[K + 1] - r0) - w;
+                if (o == 0) continue;
+                const int32_t* offrows = S.sn_rows.data() + r0 + w;
+                // target supernode and its local row for every off row
+                std::vector<int32_t> tJ(o), tloc(o);
+                for (int64_t a = 0; a < o; ++a) tJ[a] = S.col2sn[offrows[a]];
+                int64_t t = 0;
+                for (int64_t b = 0; b < o; ++b) {
+                    const int32_t J = tJ[b];
+                    const int32_t c0 = S.sn_col[J];
+                    const int32_t* rowsJ = S.sn_rows.data() + S.sn_rptr[J];
+                    const int64_t rJ = S.sn_rptr[J + 1] - S.sn_rptr[J];
+                    const int32_t tc = offrows[b] - c0;
+                    for (int64_t a = b; a < o; ++a, ++t) {
+                        const int32_t tr = (int32_t)(std::lower_bound(rowsJ, rowsJ + rJ, offrows[a]) - rowsJ);
+                        const int64_t slot = S.sn_rptr[J] + tr;
+                        if (pass == 0) {
+                            cnt_row[slot]++;
+                        } else {
+                            const int64_t e = fillp[slot]++;
+                            S.push_pos[S.cb_off[K] + t] = e;
+                            S.inbox_tgt[e] = (int32_t)(tc * rJ + tr);
+                        }
+                    }
+                }
+            }
+        }
+        // within each row bucket: order by target column (stable: source K ascending)
+        {
+            std::vector<int64_t> inv(nrec);
+            for (int64_t p = 0; p < nrec; ++p) inv[S.push_pos[p]] = p;
+            std::vector<int64_t> idx;
+            std::vector<int32_t> tg;
+            std::vector<int64_t> src;
+            for (int64_t t = 0; t < nrow_all; ++t) {
+                const int64_t lo = S.irow_ptr[t], hi = S.irow_ptr[t + 1];
+                if (hi - lo < 2) continue;
+                idx.resize(hi - lo);
+                std::iota(idx.begin(), idx.end(), lo);
+                std::stable_sort(idx.begin(), idx.end(),
+                                 [&](int64_t x, int64_t y) { return S.inbox_tgt[x] < S.inbox_tgt[y]; });
+                tg.resize(hi - lo);
+                src.resize(hi - lo);
+                for (int64_t k = 0; k < hi - lo; ++k) { tg[k] = S.inbox_tgt[idx[k]]; src[k] = inv[idx[k]]; }
+                for (int64_t k = 0; k < hi - lo; ++k) {
+                    S.inbox_tgt[lo + k] = tg[k];
+                    S.push_pos[src[k]] = lo + k;
+                }
+            }
+        }
+        // vector inbox: bucket by target column, source K ascending
+        S.vcol_ptr.assign(dim + 1, 0);
+        for (int32_t K = 0; K < ns; ++K) {
+            const int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+            for (int64_t p = S.sn_rptr[K] + w; p < S.sn_rptr[K + 1]; ++p) S.vcol_ptr[S.sn_rows[p] + 1]++;
+        }
+        for (int64_t j = 0; j < dim; ++j) S.vcol_ptr[j + 1] += S.vcol_ptr[j];
+        S.vpush_pos.assign(S.cv_off[ns], 0);
+        std::vector<int64_t> vf(S.vcol_ptr.begin(), S.vcol_ptr.end() - 1);
+        for (int32_t K = 0; K < ns; ++K) {
+            const int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+            int64_t a = 0;
+            for (int64_t p = S.sn_rptr[K] + w; p < S.sn_rptr[K + 1]; ++p, ++a)
+                S.vpush_pos[S.cv_off[K] + a] = vf[S.sn_rows[p]]++;
+        }
+    }
     // levels and topological order
     S.level.assign(ns, 0);
     for (int32_t J = 0; J < ns; ++J)

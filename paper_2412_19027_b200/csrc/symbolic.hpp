@@ -41,6 +41,21 @@ struct Symbolic {
     // update lists (left-looking): updates into J come from (src, p0, p1)
     std::vector<int64_t> upd_ptr;          // nsuper+1
     std::vector<int32_t> upd_src, upd_p0, upd_p1;
+    // push/pull "inbox" maps (see ldl.cu):
+    //  factor — supernode K's packed lower contribution block C_K = L_off D L_off'
+    //  (column-major over b' then a' >= b', offset cb_off[K]) is scattered to
+    //  inbox positions push_pos[cb_off[K] + t]; supernode J gathers its inbox rows
+    //  irow_ptr[sn_rptr[J] + tr] .. (+1) sorted by (target column, source K), each
+    //  entry subtracting from panel offset inbox_tgt[e] (= tc * r_J + tr).
+    std::vector<int64_t> cb_off;           // nsuper+1 (packed lower (r-w)(r-w+1)/2 per supernode)
+    std::vector<int64_t> push_pos;         // cb_off[nsuper]
+    std::vector<int64_t> irow_ptr;         // sn_rows.size()+1
+    std::vector<int32_t> inbox_tgt;        // cb_off[nsuper]
+    //  solves — supernode K's off-row contributions v (offset cv_off[K] = sum (r-w))
+    //  go to vpush_pos[cv_off[K] + a]; column j of the factor gathers vcol_ptr[j]..
+    std::vector<int64_t> cv_off;           // nsuper+1
+    std::vector<int64_t> vpush_pos;        // cv_off[nsuper]
+    std::vector<int64_t> vcol_ptr;         // dim+1
     // schedule
     std::vector<int32_t> order;            // topological order (leaves first, by level)
     std::vector<int32_t> level;            // per supernode, 0 = leaf
@@ -54,7 +69,7 @@ struct Symbolic {
     int64_t nnz_l = 0;                     // true strict-lower nnz of L
     int64_t nnz_storage = 0;               // dense panel elements
     double flops = 0.0;                    // 2 * sum_j c_j^2 with c_j strict-lower count
-    int64_t max_width = 0, max_rows = 0;
+    int64_t max_width = 0, max_rows = 0, max_panel = 0;
     int64_t n_updates = 0;
 };
 

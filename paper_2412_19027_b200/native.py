@@ -88,7 +88,11 @@ _SIGS = {
     "cipm_get_vector": ([c_void_p, ctypes.c_char_p, P_DBL, P_I64], ctypes.c_int),
     "cipm_soc_residuals": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
     "cipm_launch_count": ([c_void_p, P_I64, ctypes.c_int], ctypes.c_int),
+    "cipm_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_kernel_times": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_profile": ([c_void_p, ctypes.c_int], ctypes.c_int),
+    "cipm_kernel_stats": ([c_void_p, P_DBL], ctypes.c_int),
+    "cipm_timer": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
 }
 
 _lib = None
@@ -196,7 +200,7 @@ class SymbolicAnalysis:
         cnt = c_i64(0)
         raise_for_status(lib().cipm_symbolic_array(self.handle, name.encode(), None, ctypes.byref(cnt)))
         dt = np.int32 if name in ("perm", "md_perm", "sn_col", "sn_rows", "sn_parent", "upd_src", "upd_p0",
-                                  "upd_p1", "order") else np.int64
+                                  "upd_p1", "order", "inbox_tgt") else np.int64
         out = np.empty(cnt.value, dtype=dt)
         if cnt.value:
             raise_for_status(lib().cipm_symbolic_array(self.handle, name.encode(),

@@ -89,3 +89,46 @@ def dense_factor(sym, L, D):
         for j in range(w):
             Ld[rows[r0 + j + 1:r0 + r], c0 + j] = pan[j + 1:, j]
     return Ld
+
+
+def factor_inbox(sym, vals, sign_perm, delta_s):
+    """Model of the device push/pull factorisation (inbox maps of the symbolic analysis)."""
+    col = sym.array("sn_col")
+    rptr = sym.array("sn_rptr")
+    loff = sym.array("sn_loff")
+    order = sym.array("order")
+    cb_off = sym.array("cb_off")
+    push = sym.array("push_pos")
+    irow = sym.array("irow_ptr")
+    tgt = sym.array("inbox_tgt")
+    inbox = np.zeros(int(cb_off[-1]))
+    L = vals.copy()
+    D = np.zeros(int(col[-1]))
+    for J in order:
+        c0, w = col[J], col[J + 1] - col[J]
+        r0, r = rptr[J], rptr[J + 1] - rptr[J]
+        flat = L[loff[J]:loff[J] + w * r].copy()            # column-major panel, flat index tc*r + tr
+        for tr in range(r):
+            for e in range(irow[r0 + tr], irow[r0 + tr + 1]):
+                flat[tgt[e]] -= inbox[e]
+        pan = flat.reshape(w, r).T
+        for j in range(w):
+            d = pan[j, j]
+            if abs(d) < delta_s:
+                d = delta_s if sign_perm[c0 + j] > 0 else -delta_s
+            D[c0 + j] = d
+            pan[j, j] = 1.0
+            pan[j + 1:, j] /= d
+            for c in range(j + 1, w):
+                pan[c:, c] -= pan[c:, j] * d * pan[c, j]
+        L[loff[J]:loff[J] + w * r] = pan.T.ravel()
+        o = r - w
+        if o:
+            off = pan[w:, :]
+            C = (off * D[c0:c0 + w]) @ off.T
+            t = 0
+            for b in range(o):
+                for a in range(b, o):
+                    inbox[push[cb_off[J] + t]] = C[a, b]
+                    t += 1
+    return L, D

@@ -66,7 +66,9 @@ def test_supernodal_structure_reconstructs_kkt(name):
     perm = sym.array("perm")
     dim = len(perm)
     L, D = SM.factor(sym, vals, np.where(perm < n, 1, -1), 1e-14)
-    Ld = SM.dense_factor(sym, L, D)
+    L2, D2 = SM.factor_inbox(sym, vals, np.where(perm < n, 1, -1), 1e-14)
+    assert np.allclose(L, L2, rtol=1e-9, atol=1e-12) and np.allclose(D, D2, rtol=1e-9, atol=1e-12)
+    Ld = SM.dense_factor(sym, L2, D2)
     K = np.zeros((dim, dim))
     K[:n, :n] = s.P.toarray()
     A = s.A.toarray()
