@@ -51,9 +51,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--eps", type=float, default=1e-8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-iters", type=int, default=200,
+                    help="cap on IPM iterations per CPU solve (bounded sample)")
     ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-max-iters", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-solves", type=int, default=1, help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-impl", default="reference", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -128,43 +131,86 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle restatement of the reference), run in a subprocess
+# CPU baseline: the UNMODIFIED reference solver (conic_ipm, pip-installed into
+# baseline/_ref — see DESIGN.md "Reference arm"), else the oracle restatement
+# (oracle/, bit-exact vs the reference on the golden fixtures).  Runs in a
+# subprocess pinned to one thread: the reference is sequential (numba kernels,
+# Python cone loops), SURVEY.md §8(d).
 # ---------------------------------------------------------------------------
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "conic_ipm"))
+
+
+def _to_reference(ref, p):
+    conv = {"zero": lambda c: ref.zero_cone(c.dim), "nonneg": lambda c: ref.nonneg_cone(c.dim),
+            "soc": lambda c: ref.soc_cone(c.dim), "exp": lambda c: ref.exp_cone(),
+            "pow": lambda c: ref.pow_cone(c.alpha), "psd": lambda c: ref.psd_cone(c.side)}
+    P = ref.CsrMatrix(p.P.nrows, p.P.ncols, p.P.rowptr, p.P.colidx, p.P.values)
+    A = ref.CsrMatrix(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.colidx, p.A.values)
+    return ref.ProblemData(P, A, p.q, p.b, [conv[c.kind](c) for c in p.cones])
+
+
 def cpu_worker(args):
-    from oracle.ipm import OracleSolver
+    """One process: setup once, then `--cpu-solves` bounded solves of at most
+    `--cpu-max-iters` IPM iterations each; one JSON line per solve."""
     from paper_2412_19027_b200 import generators as G
     prob = G.build(args.config)
-    cfg = settings_for(args.config, args.eps)
-    t0 = time.perf_counter()
-    solver = OracleSolver(prob, cfg)
-    setup = time.perf_counter() - t0
-    cap = args.cpu_max_iters or None
-    res = solver.solve(max_iterations_run=cap)
-    out = {"setup_s": setup, "solve_s": res.solve_seconds, "iterations": res.iterations,
-           "status": res.status, "obj": res.obj_primal}
-    print("CPUWORKER " + json.dumps(out), flush=True)
+    cap = args.cpu_max_iters or 200
+    if args.cpu_impl == "reference":
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/cipm_numba_cache")
+        sys.dont_write_bytecode = True
+        sys.path.insert(0, REF_DIR)
+        import conic_ipm as ref
+        prec = G.CONFIGS[args.config]["precision"]
+        # numba JIT warm-up on a tiny instance (PAPER.md:761-762), outside any timing
+        warm = _to_reference(ref, G.gen_lp(20, 40, seed=1))
+        ref.Solver(warm, ref.SolverSettings(eps_feas=args.eps, precision=prec)).solve()
+        t0 = time.perf_counter()
+        solver = ref.Solver(_to_reference(ref, prob), ref.SolverSettings(eps_feas=args.eps, precision=prec,
+                                                                         max_iter=cap))
+        setup = time.perf_counter() - t0
+        run = solver.solve
+    else:
+        from oracle.ipm import OracleSolver
+        cfg = settings_for(args.config, args.eps)
+        t0 = time.perf_counter()
+        solver = OracleSolver(prob, cfg)
+        setup = time.perf_counter() - t0
+
+        def run():
+            return solver.solve(max_iterations_run=cap)
+    for _ in range(max(1, args.cpu_solves)):
+        res = run()
+        out = {"impl": args.cpu_impl, "setup_s": setup, "solve_s": res.solve_seconds,
+               "iterations": res.iterations, "status": res.status, "obj": res.obj_primal}
+        print("CPUWORKER " + json.dumps(out), flush=True)
 
 
-def run_cpu_sample(args, max_iters):
+def run_cpu(args, max_iters, solves=1, impl=None):
+    impl = impl or ("reference" if reference_available() else "port")
     env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
-               CUDA_VISIBLE_DEVICES="")
+               NUMBA_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
     cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--config", args.config,
-           "--eps", str(args.eps), "--cpu-max-iters", str(max_iters)]
-    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1800)
-    for line in out.stdout.splitlines():
-        if line.startswith("CPUWORKER "):
-            return json.loads(line[len("CPUWORKER "):])
-    raise RuntimeError(f"cpu worker failed: {out.stderr[-2000:]}")
+           "--eps", str(args.eps), "--cpu-max-iters", str(max_iters), "--cpu-solves", str(solves),
+           "--cpu-impl", impl]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=3600)
+    res = [json.loads(line[len("CPUWORKER "):]) for line in out.stdout.splitlines()
+           if line.startswith("CPUWORKER ")]
+    if not res:
+        raise RuntimeError(f"cpu worker failed: {out.stderr[-2000:]}")
+    return impl, res
 
 
-def cpu_iters_for_budget(args):
-    """Bounded sample: a 2-iteration probe sets the per-iteration cost, then the
-    sample runs as many iterations as fit in the CPU budget (at least 2)."""
-    probe = run_cpu_sample(args, 2)
-    per = probe["solve_s"] / max(1, probe["iterations"])
-    k = int(max(2, min(200, args.cpu_budget_s / max(per, 1e-6))))
-    return probe, k
+def cpu_sample(args):
+    """Bounded sample for the cpu_baseline key: one solve capped at `--cpu-iters`
+    IPM iterations (setup excluded from the rate)."""
+    impl, res = run_cpu(args, args.cpu_iters, 1)
+    r = res[0]
+    return impl, r
 
 
 # ---------------------------------------------------------------------------
@@ -341,16 +387,18 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            probe, k = cpu_iters_for_budget(args)
-            sample = run_cpu_sample(args, k)
-            cpu_val = sample["iterations"] / sample["solve_s"]
-            line["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": 1, "kind": "port",
-                                    "sample": f"oracle restatement of the reference, {sample['iterations']} IPM "
-                                              f"iterations of {args.config} (setup {sample['setup_s']:.1f}s "
-                                              f"excluded), 1 thread",
-                                    "cpu_solve_s_per_iter": sample["solve_s"] / max(1, sample["iterations"])}
+            impl, r = cpu_sample(args)
+            cpu_val = r["iterations"] / r["solve_s"]
+            what = ("the unmodified reference conic_ipm (baseline/_ref)" if impl == "reference"
+                    else "the oracle restatement of the reference")
+            line["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": 1, "kind": impl,
+                                    "sample": f"{what}: first {r['iterations']} IPM iterations of {args.config} "
+                                              f"(status {r['status']}), setup {r['setup_s']:.1f}s excluded, "
+                                              f"1 thread of a {os.cpu_count()}-core host",
+                                    "cpu_solve_s_per_iter": r["solve_s"] / max(1, r["iterations"]),
+                                    "setup_s": r["setup_s"]}
         except Exception as e:  # never lose the GPU line over the CPU leg
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"failed: {e}"[:300]}
     solver.close()
     if rank == 0:
@@ -364,29 +412,38 @@ def run_ours(args):
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
+    """--impl reference: rank 0 times the reference's own CPU solver (setup once,
+    then W warm-up + K timed solves, each capped at --cpu-iters iterations)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     spec, desc = workload(args.config)
-    probe, k = cpu_iters_for_budget(args)
-    cores = 1
-    it_total, secs = 0, 0.0
-    for i in range(args.warmup + args.steps):
-        s = run_cpu_sample(args, min(k, 200))
-        if i >= args.warmup:
-            it_total += s["iterations"]
-            secs += s["solve_s"]
+    impl, res = run_cpu(args, args.cpu_iters, args.warmup + args.steps)
+    timed = res[args.warmup:]
+    it_total = sum(r["iterations"] for r in timed)
+    secs = sum(r["solve_s"] for r in timed)
     value = it_total / secs
+    what = ("unmodified reference conic_ipm from baseline/_ref" if impl == "reference"
+            else "oracle restatement of the reference (bit-exact on the golden fixtures)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-            "data": "synthetic (seeded generator)",
-            "config": {"workload": desc, "config": args.config, "eps_feas": args.eps},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"oracle restatement (bit-exact vs the reference on the golden fixtures), "
-                                       f"up to {k} IPM iterations per step, setup excluded, 1 thread"},
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 iterate / f32 LDL' + f64 refinement" if G_precision(args.config) == "mixed" else "f64",
+            "impl": "reference", "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
+            "config": {"workload": desc, "config": args.config, "eps_feas": args.eps,
+                       "status": sorted({r["status"] for r in timed}),
+                       "iterations_per_solve": it_total / max(1, len(timed)),
+                       "setup_s": timed[0]["setup_s"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": impl,
+                             "sample": f"{what}: each step one solve capped at {args.cpu_iters} IPM iterations, "
+                                       f"setup excluded, 1 thread of a {os.cpu_count()}-core host"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def G_precision(config):
+    from paper_2412_19027_b200 import generators as G
+    return G.CONFIGS[config]["precision"]
 
 
 def main():

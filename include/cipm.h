@@ -68,6 +68,7 @@ enum {
 
 typedef struct cipm_symbolic cipm_symbolic;
 typedef struct cipm_ctx cipm_ctx;
+typedef struct cipm_batch cipm_batch;
 
 /* Problem structure after cone reordering (problem.py:177-210): rows are
  * [zero | nonneg | SOC... | exp... | pow... | PSD...]; offsets are row indices
@@ -164,6 +165,30 @@ int cipm_kernel_stats(cipm_ctx *ctx, double *out);
 int cipm_timer(cipm_ctx *ctx, int op, double *ms);
 /* CUDA-event time (ms) of the last numeric factorisation and last triangular solve */
 int cipm_kernel_times(cipm_ctx *ctx, double *factor_ms, double *solve_ms);
+
+/* --- batched independent instances sharing one pattern (C5b; replaces the
+ * reference's per-instance Solver loop under bench --jobs, bench.py:98-113).
+ * Zero + nonnegative cones, full precision.  One CTA runs one instance's whole
+ * IPM (ipm.py:411-496) on the device.  Values are the per-instance SCALED data
+ * (after reorder_cones + equilibrate, problem.py:177-284), instance-major:
+ * V = [P values | A values] (count x (nnzP + nnzA)), q (count x n), b, Dr
+ * (count x m), Dc (count x n), c_obj / norm_q / norm_b (count; the norms are
+ * ‖q‖∞, ‖b‖∞ of the reordered unscaled data, ipm.py:184-185). --- */
+int cipm_batch_create(const cipm_problem_desc *desc, int count, const cipm_settings *settings,
+                      double eps_feas, double eps_inf, int max_iter, cipm_batch **out);
+/* info[6] = {count, n, m, nnz(L), shared bytes per instance CTA, in shared memory (1) or workspace (0)} */
+int cipm_batch_info(const cipm_batch *b, int64_t *info);
+int cipm_batch_set_values(cipm_batch *b, const double *V, const double *q, const double *bvec,
+                          const double *d_row, const double *d_col, const double *c_obj,
+                          const double *norm_q, const double *norm_b);
+/* run every instance to termination; *ms = CUDA-event time of the launch */
+int cipm_batch_solve(cipm_batch *b, double *ms);
+/* status[count] (0 optimal, 1 primal_inf, 2 dual_inf, 3 almost_optimal, 4 max_iterations,
+ * 6 insufficient_progress, 7 numerical_error); res[count][9] = {g_p, g_d, ‖r_p‖, ‖r_d‖, τ, κ, μ,
+ * μ_initial, iterations}; x/z/s: the reported (current or best) SCALED iterate */
+int cipm_batch_results(cipm_batch *b, int32_t *status, double *res, double *x, double *z, double *s);
+int cipm_batch_io_bytes(cipm_batch *b, int64_t *h2d, int64_t *d2h, int reset);
+void cipm_batch_destroy(cipm_batch *b);
 
 #ifdef __cplusplus
 }

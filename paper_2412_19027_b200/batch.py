@@ -1,0 +1,225 @@
+"""Batched independent instances on one GPU (C5b).
+
+``BatchSolver(problems, settings).solve()`` solves many problems that share
+one sparsity pattern (e.g. the MPC QPs of the paper's §4.6, or one parametric
+family) and returns one reference-compatible ``SolveResult`` per instance —
+the same results the reference produces when it runs ``Solver(p).solve()``
+for each instance (its ``bench --jobs`` mode, bench.py:98-113).
+
+Host side (once per batch): validation, cone reordering and a Ruiz
+equilibration vectorised across instances (bitwise the per-instance
+``model.equilibrate``), then ONE launch of the device kernel in which each CTA
+runs one instance's whole Algorithm-1 loop (csrc/batch.cu).  Multi-GPU:
+one process per GPU, each with its own contiguous shard of instances and no
+collective on the solve path (bench.py --config c5b_mpc under torchrun).
+
+Scope: zero + nonnegative cones (LP/QP), full precision.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from .exceptions import ConicError, PatternMismatch, raise_for_status
+from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, reorder_cones, validate
+from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, require_device
+from .settings import FULL, SolveResult, SolverSettings, Status, default_dynamic_reg, default_static_reg
+
+RUIZ_ITERS = 10
+_STATUS = {0: Status.OPTIMAL, 1: Status.PRIMAL_INFEASIBLE, 2: Status.DUAL_INFEASIBLE, 3: Status.ALMOST_OPTIMAL,
+           4: Status.MAX_ITERATIONS, 6: Status.INSUFFICIENT_PROGRESS, 7: Status.NUMERICAL_ERROR}
+
+
+def _rows(rowptr):
+    return np.repeat(np.arange(len(rowptr) - 1, dtype=np.int64), np.diff(rowptr))
+
+
+def equilibrate_batch(P, A, pv, av, q, b, iters=RUIZ_ITERS):
+    """Ruiz equilibration of B instances at once (problem.py:222-284 restated on
+    (B, nnz) arrays; zero + nonneg cones so there is no block-uniform step).
+    Elementwise identical to ``model.equilibrate`` per instance."""
+    B, n, m = q.shape[0], P.nrows, A.nrows
+    p_rows, p_cols = _rows(P.rowptr), P.colidx
+    a_rows, a_cols = _rows(A.rowptr), A.colidx
+    pv, av, qc, bc = pv.copy(), av.copy(), q.copy(), b.copy()
+    d_col = np.ones((B, n))
+    d_row = np.ones((B, m))
+    inst_p = np.arange(B)[:, None]
+    for _ in range(iters):
+        cnorm = np.zeros((B, n))
+        if pv.shape[1]:
+            np.maximum.at(cnorm, (np.broadcast_to(inst_p, pv.shape), np.broadcast_to(p_cols, pv.shape)), np.abs(pv))
+        if av.shape[1]:
+            np.maximum.at(cnorm, (np.broadcast_to(inst_p, av.shape), np.broadcast_to(a_cols, av.shape)), np.abs(av))
+        rnorm = np.zeros((B, m))
+        if av.shape[1]:
+            np.maximum.at(rnorm, (np.broadcast_to(inst_p, av.shape), np.broadcast_to(a_rows, av.shape)), np.abs(av))
+        cstep = np.where(cnorm > 0, 1.0 / np.sqrt(np.where(cnorm > 0, cnorm, 1.0)), 1.0)
+        rstep = np.where(rnorm > 0, 1.0 / np.sqrt(np.where(rnorm > 0, rnorm, 1.0)), 1.0)
+        new_dcol = np.clip(d_col * cstep, SCALE_MIN, SCALE_MAX)
+        new_drow = np.clip(d_row * rstep, SCALE_MIN, SCALE_MAX)
+        cstep = new_dcol / d_col
+        rstep = new_drow / d_row
+        d_col, d_row = new_dcol, new_drow
+        pv = (cstep[:, p_rows] * pv) * cstep[:, p_cols]
+        av = (rstep[:, a_rows] * av) * cstep[:, a_cols]
+        qc *= cstep
+        bc *= rstep
+    qmax = np.max(np.abs(qc), axis=1) if n else np.zeros(B)
+    c_obj = np.where(qmax == 0.0, 1.0, np.clip(1.0 / np.where(qmax == 0.0, 1.0, qmax), SCALE_MIN, SCALE_MAX))
+    pv = pv * c_obj[:, None]
+    qc = qc * c_obj[:, None]
+    return pv, av, qc, bc, d_row, d_col, c_obj
+
+
+class BatchSolver:
+    """Many same-pattern instances, one device launch (one CTA per instance)."""
+
+    def __init__(self, problems, settings: SolverSettings | None = None, device: int = 0):
+        if not problems:
+            raise ConicError("empty batch")
+        self.settings = st = settings or SolverSettings()
+        if st.precision != FULL:
+            raise ConicError("batched instances run the full-precision factorisation")
+        torch = require_device()
+        torch.cuda.set_device(device)
+        t0 = time.perf_counter()
+        first = problems[0]
+        for p in problems:
+            validate(p)
+            if not (np.array_equal(p.P.rowptr, first.P.rowptr) and np.array_equal(p.P.colidx, first.P.colidx)
+                    and np.array_equal(p.A.rowptr, first.A.rowptr) and np.array_equal(p.A.colidx, first.A.colidx)
+                    and list(p.cones) == list(first.cones)):
+                raise PatternMismatch("batched instances must share one sparsity pattern and cone list")
+        if any(c.kind not in (ZERO, NONNEG) for c in first.cones):
+            raise ConicError("batched instances support zero + nonnegative cones only")
+        self.problems = [p.copy() for p in problems]
+        self.count = len(problems)
+        ref0, self._perm = reorder_cones(first)
+        self._pattern = ref0
+        self.layout = Layout(ref0.cones)
+        self.n, self.m = ref0.n, ref0.m
+        cs = Settings()
+        cs.precision = 0
+        cs.delta_s = default_static_reg(FULL) if st.delta_s is None else st.delta_s
+        cs.delta_d = default_dynamic_reg(FULL) if st.delta_d is None else st.delta_d
+        cs.beta, cs.backtrack, cs.step_scale = st.beta, st.backtrack, st.step_scale
+        cs.refine_abs, cs.refine_rel, cs.refine_max = (st.refinement.t_abs, st.refinement.t_rel,
+                                                       st.refinement.t_max)
+        cs.device = device
+        cs.stream = None
+        self._desc, self._keep = make_desc(ref0.P, ref0.A, self.layout)
+        h = c_void_p()
+        rc = lib().cipm_batch_create(ctypes.byref(self._desc), self.count, ctypes.byref(cs), st.eps_feas,
+                                     st.eps_inf, st.max_iter, ctypes.byref(h))
+        raise_for_status(rc, "batch creation")
+        self.handle = h
+        self._upload()
+        self.setup_seconds = time.perf_counter() - t0
+        self.last_kernel_ms = 0.0
+
+    def _upload(self):
+        perm = self._perm
+        P, A = self._pattern.P, self._pattern.A
+        # rows of A are permuted identically in every instance: gather the values once per instance
+        a_src = self._a_src = _take_rows_src(self.problems[0].A, perm)
+        pv = np.stack([p.P.values for p in self.problems])
+        av = np.stack([p.A.values[a_src] for p in self.problems])
+        q = np.stack([p.q for p in self.problems])
+        b = np.stack([p.b[perm] for p in self.problems])
+        self._norm_q = np.max(np.abs(q), axis=1) if self.n else np.zeros(self.count)
+        self._norm_b = np.max(np.abs(b), axis=1) if self.m else np.zeros(self.count)
+        pv_s, av_s, q_s, b_s, d_row, d_col, c_obj = equilibrate_batch(P, A, pv, av, q, b)
+        self._d_row, self._d_col, self._c_obj = d_row, d_col, c_obj
+        self._host = [np.ascontiguousarray(a) for a in
+                      (np.concatenate([pv_s, av_s], axis=1), q_s, b_s, d_row, d_col, c_obj, self._norm_q,
+                       self._norm_b)]
+        rc = lib().cipm_batch_set_values(self.handle, *[pdbl(a) for a in self._host])
+        raise_for_status(rc, "batch upload")
+
+    def update_data(self, q=None, b=None):
+        """Parametric re-solve of every instance (same patterns): q, b as (count, n) / (count, m)."""
+        for k, p in enumerate(self.problems):
+            if q is not None:
+                p.q = np.asarray(q[k], dtype=np.float64).copy()
+            if b is not None:
+                p.b = np.asarray(b[k], dtype=np.float64).copy()
+        self._upload()
+
+    def info(self) -> dict:
+        out = np.zeros(6, dtype=np.int64)
+        raise_for_status(lib().cipm_batch_info(self.handle, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return dict(zip(("count", "n", "m", "nnz_l", "smem_bytes", "in_smem"), (int(v) for v in out)))
+
+    def run(self) -> float:
+        """Device solve of every instance; returns the CUDA-event time (ms)."""
+        ms = ctypes.c_double(0.0)
+        raise_for_status(lib().cipm_batch_solve(self.handle, ctypes.byref(ms)), "batch solve")
+        self.last_kernel_ms = ms.value
+        return ms.value
+
+    def results(self, secs: float | None = None):
+        c, n, m = self.count, self.n, self.m
+        status = np.zeros(c, dtype=np.int32)
+        res = np.zeros((c, 9))
+        x, z, s = np.zeros((c, n)), np.zeros((c, m)), np.zeros((c, m))
+        raise_for_status(lib().cipm_batch_results(self.handle, status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                  pdbl(res), pdbl(x), pdbl(z), pdbl(s)), "batch results")
+        secs = self.last_kernel_ms / 1e3 if secs is None else secs
+        out = []
+        inv = self._perm
+        for k in range(c):
+            st = _STATUS[int(status[k])]
+            g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = res[k]
+            x_u = self._d_col[k] * x[k]
+            z_u = self._d_row[k] * z[k] / self._c_obj[k]
+            s_u = s[k] / self._d_row[k]
+            cert = None
+            if st in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
+                x_o, z_o, s_o = x_u, _user_rows(z_u, inv), _user_rows(s_u, inv)
+                if st == Status.PRIMAL_INFEASIBLE:
+                    cert = z_o / abs(float(self.problems[k].b @ z_o))
+                else:
+                    cert = x_o / abs(float(self.problems[k].q @ x_o))
+            else:
+                x_o, z_o, s_o = x_u / tau, _user_rows(z_u / tau, inv), _user_rows(s_u / tau, inv)
+            out.append(SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=float(g_p),
+                                   obj_dual=float(g_d), iterations=int(iters), setup_seconds=self.setup_seconds,
+                                   solve_seconds=secs, norm_rp=float(rp), norm_rd=float(rd),
+                                   gap=abs(float(g_p) - float(g_d)), tau=float(tau), kappa=float(kappa),
+                                   mu_initial=float(mu0), mu_final=float(mu)))
+        return out
+
+    def solve(self):
+        t0 = time.perf_counter()
+        self.run()
+        return self.results(time.perf_counter() - t0)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().cipm_batch_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _take_rows_src(A, rows):
+    rows = np.asarray(rows, dtype=np.int64)
+    counts = A.rowptr[rows + 1] - A.rowptr[rows]
+    rp = np.zeros(len(rows) + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    if not rp[-1]:
+        return np.zeros(0, dtype=np.int64)
+    return np.repeat(A.rowptr[rows] - rp[:-1], counts) + np.arange(rp[-1], dtype=np.int64)
+
+
+def _user_rows(v, perm):
+    out = np.empty_like(v)
+    out[perm] = v
+    return out

@@ -1,0 +1,910 @@
+// Batched independent instances (C5b: 8 x 256 MPC QPs): one CTA runs one
+// instance's whole homogeneous-embedding IPM (Algorithm 1, reference
+// ipm.py:411-496) on the device — no host round trip per iteration.
+//
+// All instances share one sparsity pattern, so the pattern tables (P, A, A',
+// the permuted KKT CSC, the elimination schedule) live once in global memory
+// (L1/L2 resident, read by every CTA) and every per-instance vector lives in
+// the CTA's shared memory (or in a per-instance global workspace when an
+// instance is too large for 227 KB).
+//
+// Scope: zero + nonnegative cones (LP / QP), the MPC family of the paper's
+// §4.6.  Arithmetic follows the reference step for step:
+//   residuals / termination / infeasibility   ipm.py:233-280 (fused scaled-G form)
+//   stall, best iterate, almost-optimal        ipm.py:429-457, :489-496
+//   nonneg NT scaling                          cones/scaling.py:231-240
+//   KKT values + ±δs, up-looking LDL' with the
+//     dynamic-regularisation bump              kkt/system.py:246-263, kkt/ldl.py:37-88
+//   iterative refinement                       kkt/system.py:279-314
+//   directions (two-column, P-norm Δτ)         ipm.py:309-338
+//   step length (τ/κ + ray) and neighbourhood  cones/steps.py:79-116, ipm.py:350-366
+//   take_step + membership                     ipm.py:368-379
+// The factorisation uses the reference's own minimum-degree order and the
+// reference's up-looking visiting order (precomputed schedule), single thread,
+// FMA contraction off (built with -fmad=false), so D and L round like the
+// CPU solver's.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "batch.hpp"
+
+namespace cipm {
+
+namespace {
+
+constexpr int BT = 128;            // threads per instance CTA
+constexpr int NW = BT / 32;
+
+enum BStatus {
+    BS_OPTIMAL = 0, BS_PRIMAL_INF = 1, BS_DUAL_INF = 2, BS_ALMOST = 3, BS_MAXIT = 4,
+    BS_INSUFFICIENT = 6, BS_NUMERICAL = 7
+};
+
+struct Red {
+    double* buf;   // NW * 16 doubles in shared memory
+};
+
+// block-wide fixed-order reduction of K values (sum / max per op mask bit: 1 = max)
+template <int K>
+__device__ __forceinline__ void breduce(double (&v)[K], unsigned maxmask, double* sbuf) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double a = v[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double b = __shfl_down_sync(0xffffffffu, a, o);
+            a = ((maxmask >> k) & 1u) ? fmax(a, b) : a + b;
+        }
+        if (lane == 0) sbuf[warp * K + k] = a;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double a = sbuf[k];
+        for (int w = 1; w < NW; ++w) a = ((maxmask >> k) & 1u) ? fmax(a, sbuf[w * K + k]) : a + sbuf[w * K + k];
+        v[k] = a;
+    }
+    __syncthreads();
+}
+
+struct Inst {
+    // shared-memory (or workspace) vectors
+    double *x, *z, *s, *dx[2], *dz[2], *ds[2], *gx, *gz, *col2, *sol, *rb, *rx, *rr, *rbest, *t, *dsc, *h, *w, *lam,
+        *V, *lx, *d, *y;
+};
+
+__device__ __forceinline__ double csr_dot(const int32_t* rp, const int32_t* ci, const double* v, const double* x,
+                                          int i) {
+    double acc = 0.0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) acc += v[p] * x[ci[p]];
+    return acc;
+}
+
+// A' row i: values live in V (A part) at at_src
+__device__ __forceinline__ double csrt_dot(const int32_t* rp, const int32_t* ci, const int32_t* src,
+                                           const double* va, const double* x, int i) {
+    double acc = 0.0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) acc += va[src[p]] * x[ci[p]];
+    return acc;
+}
+
+__device__ void carve(const BatchPattern& pt, double* base, Inst& I) {
+    const int n = pt.n, m = pt.m, dim = n + m;
+    double* p = base;
+    auto take = [&](int cnt) { double* q = p; p += (cnt + 1) & ~1; return q; };
+    I.x = take(n); I.z = take(m); I.s = take(m);
+    for (int k = 0; k < 2; ++k) { I.dx[k] = take(n); I.dz[k] = take(m); I.ds[k] = take(m); }
+    I.gx = take(n); I.gz = take(m);
+    I.col2 = take(dim); I.sol = take(dim);
+    I.rb = take(dim); I.rx = take(dim); I.rr = take(dim); I.rbest = take(dim); I.t = take(dim);
+    I.dsc = take(m); I.h = take(m); I.w = take(m); I.lam = take(m);
+    I.V = take(pt.nnz_p + pt.nnz_a);
+    I.lx = take(pt.nnz_l); I.d = take(dim); I.y = take(dim);
+}
+
+// ------------------------- factorisation (thread 0) -------------------------
+// reference kkt/ldl.py:37-88 restated over the precomputed up-looking schedule
+__device__ int factor_seq(const BatchPattern& pt, Inst& I, double delta_s, double delta_d) {
+    const int dim = pt.n + pt.m;
+    double* y = I.y;
+    double run_max = 0.0;
+    int bumped = 0;
+    for (int j = 0; j < dim; ++j) y[j] = 0.0;
+    for (int j = 0; j < dim; ++j) {
+        for (int p = pt.cp[j]; p < pt.cp[j + 1]; ++p) {
+            const int i = pt.ci[p];
+            const int src = pt.csrc[p];
+            double v = 0.0;
+            if (src >= 0) v = I.V[src];
+            else if (src <= -2) v = -I.h[-src - 2];
+            if (i == j) v = v + (pt.sign[j] > 0 ? delta_s : -delta_s);
+            y[i] += v;
+        }
+        double dj = y[j];
+        y[j] = 0.0;
+        for (int u = pt.up_ptr[j]; u < pt.up_ptr[j + 1]; ++u) {
+            const int i = pt.up_i[u];
+            const int p2 = pt.up_p2[u];
+            const double yi = y[i];
+            y[i] = 0.0;
+            for (int p = pt.lp[i]; p < p2; ++p) y[pt.li[p]] -= I.lx[p] * yi;
+            const double l_ji = yi / I.d[i];
+            dj -= l_ji * yi;
+            I.lx[p2] = l_ji;
+        }
+        const double bound = delta_s + delta_d * run_max;
+        if (fabs(dj) < bound) {
+            dj = pt.sign[j] > 0 ? bound : -bound;
+            ++bumped;
+        }
+        if (dj == 0.0) return -1;
+        I.d[j] = dj;
+        if (fabs(dj) > run_max) run_max = fabs(dj);
+    }
+    return bumped;
+}
+
+// x += solve(r): permute, L / D / L' sweeps (kkt/ldl.py:91-104), permute back (thread 0)
+__device__ void ldl_solve_add(const BatchPattern& pt, Inst& I, const double* r, double* x) {
+    const int dim = pt.n + pt.m;
+    double* t = I.t;
+    for (int k = 0; k < dim; ++k) t[k] = r[pt.perm[k]];
+    for (int j = 0; j < dim; ++j) {
+        const double xj = t[j];
+        for (int p = pt.lp[j]; p < pt.lp[j + 1]; ++p) t[pt.li[p]] -= I.lx[p] * xj;
+    }
+    for (int j = 0; j < dim; ++j) t[j] /= I.d[j];
+    for (int j = dim - 1; j >= 0; --j) {
+        double acc = t[j];
+        for (int p = pt.lp[j]; p < pt.lp[j + 1]; ++p) acc -= I.lx[p] * t[pt.li[p]];
+        t[j] = acc;
+    }
+    for (int k = 0; k < dim; ++k) x[pt.perm[k]] += t[k];
+}
+
+struct Ctl {
+    double tau, kappa, mu, gtau, sigma;
+    double dtau[2], dkappa[2];
+    double alpha;
+    int err;          // 0 ok, else numerical error
+    int done;
+    int steps;
+};
+
+// ---------------------------- the kernel -----------------------------------
+__global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, int count) {
+    extern __shared__ __align__(16) double bsm[];
+    __shared__ double sred[NW * 16];
+    __shared__ Ctl C;
+    __shared__ double sv[8];
+    const int inst = blockIdx.x;
+    if (inst >= count) return;
+    const int tid = threadIdx.x;
+    const int n = pt.n, m = pt.m, dim = n + m;
+    const int z0 = pt.zero_dim, nnd = pt.nonneg_dim;
+    Inst I;
+    carve(pt, bd.use_smem ? bsm : bd.workspace + (int64_t)inst * bd.ws_stride, I);
+    const double* gV = bd.V + (int64_t)inst * (pt.nnz_p + pt.nnz_a);
+    const double* q = bd.q + (int64_t)inst * n;
+    const double* b = bd.b + (int64_t)inst * m;
+    const double* dr = bd.dr + (int64_t)inst * m;
+    const double* dc = bd.dc + (int64_t)inst * n;
+    const double cobj = bd.c_obj[inst], norm_q = bd.norm_q[inst], norm_b = bd.norm_b[inst];
+    double* bx = bd.best_x + (int64_t)inst * n;
+    double* bz_ = bd.best_z + (int64_t)inst * m;
+    double* bs = bd.best_s + (int64_t)inst * m;
+    const double* Va = I.V + pt.nnz_p;
+    const double nu1 = (double)nnd + 1.0;
+    const double eps_feas = bd.eps_feas, eps_inf = bd.eps_inf;
+
+    for (int k = tid; k < pt.nnz_p + pt.nnz_a; k += BT) I.V[k] = gV[k];
+    // unit start (set.py:91-112): x = 0, zero block 0, nonneg 1
+    for (int k = tid; k < n; k += BT) I.x[k] = 0.0;
+    for (int k = tid; k < m; k += BT) {
+        const double u = (k >= z0 && k < z0 + nnd) ? 1.0 : 0.0;
+        I.s[k] = u;
+        I.z[k] = u;
+        I.h[k] = 0.0;
+    }
+    __syncthreads();
+    {
+        double v[1] = {0.0};
+        for (int k = tid; k < m; k += BT) v[0] += I.s[k] * I.z[k];
+        breduce<1>(v, 0u, sred);
+        if (tid == 0) {
+            C.tau = 1.0;
+            C.kappa = 1.0;
+            C.mu = (v[0] + 1.0) / nu1;
+            C.err = 0;
+            C.done = 0;
+        }
+    }
+    __syncthreads();
+    const double mu0 = C.mu;
+    double best_score = INFINITY;
+    double best_r[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // g_p g_d rp rd tau kappa mu valid r1 r2 r3
+    double cur_r[4] = {0, 0, 0, 0};
+    double st_mu = INFINITY, st_rp = INFINITY, st_rd = INFINITY;
+    int stall = 0;
+    int status = -1;
+    int iterations = 0;
+
+    for (int it = 0; it <= bd.max_iter; ++it) {
+        // ---- residuals through the scaled G rows (vec.cu resid_n / resid_m) ----
+        const double tau = C.tau, kappa = C.kappa, mu = C.mu;
+        double vn[6] = {0, 0, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int i = tid; i < n; i += BT) {
+            const double px = csr_dot(pt.p_rp, pt.p_ci, I.V, I.x, i);
+            const double atz = csrt_dot(pt.at_rp, pt.at_ci, pt.at_src, Va, I.z, i);
+            const double g = -((px + atz) + q[i] * tau);
+            I.gx[i] = g;
+            const double xi = I.x[i], dci = dc[i];
+            vn[0] += xi * px;
+            vn[1] += q[i] * xi;
+            vn[2] = fmax(vn[2], fabs(g / dci));
+            vn[3] = fmax(vn[3], fabs(atz / dci));
+            vn[4] = fmax(vn[4], fabs(px / dci));
+            vn[5] = fmax(vn[5], fabs(dci * xi));
+        }
+        breduce<6>(vn, 0x3cu, sred);
+        double vm[5] = {0, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int i = tid; i < m; i += BT) {
+            const double ax = csr_dot(pt.a_rp, pt.a_ci, Va, I.x, i);
+            const double si = I.s[i], dri = dr[i];
+            const double g = (si + ax) - b[i] * tau;
+            I.gz[i] = g;
+            vm[0] += b[i] * I.z[i];
+            vm[1] = fmax(vm[1], fabs(g / dri));
+            vm[2] = fmax(vm[2], fabs((ax + si) / dri));
+            vm[3] = fmax(vm[3], fabs(dri * I.z[i]));
+            vm[4] = fmax(vm[4], fabs(si / dri));
+        }
+        breduce<5>(vm, 0x1eu, sred);
+        const double xpx = vn[0], qx = vn[1], bzv = vm[0];
+        const double nrm_xu = n ? vn[5] : 0.0, nrm_zu = m ? vm[3] : 0.0, nrm_su = m ? vm[4] : 0.0;
+        const double gtau = ((kappa + qx) + bzv) + xpx / tau;
+        const double hq = 0.5 * xpx / (cobj * tau * tau);
+        const double g_p = hq + qx / (cobj * tau), g_d = -hq - bzv / (cobj * tau);
+        const double rp = (m ? vm[1] : 0.0) / tau, rd = (n ? vn[2] : 0.0) / (cobj * tau);
+        const double xbar = nrm_xu / tau, sbar = nrm_su / tau, zbar = nrm_zu / (cobj * tau);
+        const double gap = fabs(g_p - g_d);
+        const double r1 = rp / fmax(1.0, norm_b + xbar + sbar);
+        const double r2 = rd / fmax(1.0, norm_q + xbar + zbar);
+        const double r3 = gap / fmax(1.0, fmin(fabs(g_p), fabs(g_d)));
+        const double score = fmax(r1, fmax(r2, r3));
+        cur_r[0] = g_p; cur_r[1] = g_d; cur_r[2] = rp; cur_r[3] = rd;
+        if (score < best_score || best_r[7] == 0.0) {
+            if (score < best_score) best_score = score;
+            best_r[0] = g_p; best_r[1] = g_d; best_r[2] = rp; best_r[3] = rd;
+            best_r[4] = tau; best_r[5] = kappa; best_r[6] = mu; best_r[7] = 1.0;
+            best_r[8] = r1; best_r[9] = r2; best_r[10] = r3;
+            for (int k = tid; k < n; k += BT) bx[k] = I.x[k];
+            for (int k = tid; k < m; k += BT) { bz_[k] = I.z[k]; bs[k] = I.s[k]; }
+        }
+        if (r1 < eps_feas && r2 < eps_feas && r3 < eps_feas) { status = BS_OPTIMAL; break; }
+        {   // Eq.(9) (ipm.py:263-280) on the unscaled, un-normalised iterate
+            const double bz_u = bzv / cobj, qx_u = qx / cobj;
+            const double nx = nrm_xu, nz = nrm_zu / cobj, ns = nrm_su;
+            const double atz = n ? vn[3] / cobj : 0.0;
+            if (atz < -eps_inf * fmax(1.0, nx + nz) * bz_u && bz_u < -eps_inf) { status = BS_PRIMAL_INF; break; }
+            const double pxn = n ? vn[4] / cobj : 0.0;
+            const double axs = m ? vm[2] : 0.0;
+            if (pxn < -eps_inf * fmax(1.0, nx) * bz_u && axs < -eps_inf * fmax(1.0, nx + ns) * qx_u &&
+                qx_u < -eps_inf) { status = BS_DUAL_INF; break; }
+        }
+        if (it >= bd.max_iter) { status = BS_MAXIT; break; }
+        {
+            const bool improved = mu < STALL_IMP * st_mu || rp < STALL_IMP * st_rp || rd < STALL_IMP * st_rd;
+            st_mu = fmin(st_mu, mu);
+            st_rp = fmin(st_rp, rp);
+            st_rd = fmin(st_rd, rd);
+            stall = improved ? 0 : stall + 1;
+            if (stall >= 5) { status = BS_INSUFFICIENT; break; }
+        }
+        // ---- nonneg NT scaling (scaling.py:231-240) ----
+        for (int k = tid; k < nnd; k += BT) {
+            const double sk = I.s[z0 + k], zk = I.z[z0 + k];
+            if (!(sk > 0.0) || !(zk > 0.0)) C.err = 1;
+            I.h[z0 + k] = sk / zk;
+            I.w[z0 + k] = sqrt(sk / zk);
+            I.lam[z0 + k] = sqrt(sk * zk);
+        }
+        __syncthreads();
+        if (C.err) { status = BS_NUMERICAL; break; }
+        // ---- numeric factorisation ----
+        if (tid == 0) {
+            const int bumped = factor_seq(pt, I, bd.delta_s, bd.delta_d);
+            if (bumped < 0) C.err = 1;
+        }
+        __syncthreads();
+        if (C.err) { status = BS_NUMERICAL; break; }
+
+        // refined solve of K x = rb into `out` (system.py:279-314); K x from P, A, H
+        auto refined = [&](double* out) {
+            double bn[1] = {-INFINITY};
+            for (int k = tid; k < dim; k += BT) {
+                bn[0] = fmax(bn[0], fabs(I.rb[k]));
+                I.rx[k] = 0.0;
+                I.rr[k] = I.rb[k];
+                out[k] = 0.0;
+            }
+            breduce<1>(bn, 1u, sred);
+            const double target = bd.refine_abs + bd.refine_rel * (dim ? bn[0] : 0.0);
+            double best = INFINITY, prev = INFINITY;
+            int ups = 0;
+            for (int step = 1; step <= bd.refine_max; ++step) {
+                if (tid == 0) ldl_solve_add(pt, I, I.rr, I.rx);
+                __syncthreads();
+                double rn[1] = {-INFINITY};
+                for (int i = tid; i < n; i += BT) {
+                    const double kx = csr_dot(pt.p_rp, pt.p_ci, I.V, I.rx, i) +
+                                      csrt_dot(pt.at_rp, pt.at_ci, pt.at_src, Va, I.rx + n, i);
+                    const double r = I.rb[i] - kx;
+                    I.rr[i] = r;
+                    rn[0] = fmax(rn[0], fabs(r));
+                }
+                for (int i = tid; i < m; i += BT) {
+                    double r = I.rb[n + i] - csr_dot(pt.a_rp, pt.a_ci, Va, I.rx, i);
+                    r = r + I.h[i] * I.rx[n + i];
+                    I.rr[n + i] = r;
+                    rn[0] = fmax(rn[0], fabs(r));
+                }
+                breduce<1>(rn, 1u, sred);
+                const double r = dim ? rn[0] : 0.0;
+                if (r < best) {
+                    best = r;
+                    for (int k = tid; k < dim; k += BT) out[k] = I.rx[k];
+                }
+                if (r <= target) {
+                    for (int k = tid; k < dim; k += BT) out[k] = I.rx[k];
+                    break;
+                }
+                if (r > prev) {
+                    if (++ups >= 2) break;
+                } else {
+                    ups = 0;
+                }
+                prev = r;
+                __syncthreads();
+            }
+            __syncthreads();
+        };
+
+        // col2 = K \ [-q; b]
+        for (int k = tid; k < dim; k += BT) I.rb[k] = k < n ? -q[k] : b[k - n];
+        __syncthreads();
+        refined(I.col2);
+        // τ-step denominator pieces (fixed per iteration)
+        double dn[5] = {0, 0, 0, 0, 0};
+        for (int i = tid; i < n; i += BT) {
+            double pdiff = 0.0, pdx2 = 0.0;
+            for (int p = pt.p_rp[i]; p < pt.p_rp[i + 1]; ++p) {
+                const int jx = pt.p_ci[p];
+                pdiff += I.V[p] * (I.col2[jx] - I.x[jx] / tau);
+                pdx2 += I.V[p] * I.col2[jx];
+            }
+            dn[0] += (I.col2[i] - I.x[i] / tau) * pdiff;
+            dn[1] += I.col2[i] * pdx2;
+            dn[2] += q[i] * I.col2[i];
+        }
+        for (int i = tid; i < m; i += BT) dn[3] += b[i] * I.col2[n + i];
+        breduce<5>(dn, 0u, sred);
+        const double den = (((kappa / tau + dn[0]) - dn[1]) - dn[2]) - dn[3];
+        if (fabs(den) < 1e-14 || !(den == den)) { status = BS_NUMERICAL; break; }
+
+        // direction recovery (ipm.py:309-338); which 0 affine, 1 combined
+        auto recover = [&](int which, double d_tau, double d_kappa, const double* d_s) {
+            double dd[3] = {0, 0, 0};
+            for (int i = tid; i < n; i += BT) {
+                const double pd = csr_dot(pt.p_rp, pt.p_ci, I.V, I.sol, i);
+                dd[0] += q[i] * I.sol[i];
+                dd[1] += (I.x[i] / tau) * pd;
+            }
+            for (int i = tid; i < m; i += BT) dd[2] += b[i] * I.sol[n + i];
+            breduce<3>(dd, 0u, sred);
+            const double num = (((d_tau - d_kappa / tau) + dd[0]) + dd[2]) + 2.0 * dd[1];
+            const double dt = num / den;
+            const double dk = -(d_kappa + kappa * dt) / tau;
+            for (int k = tid; k < n; k += BT) I.dx[which][k] = I.sol[k] + dt * I.col2[k];
+            for (int k = tid; k < m; k += BT) {
+                const double dzk = I.sol[n + k] + dt * I.col2[n + k];
+                I.dz[which][k] = dzk;
+                I.ds[which][k] = -d_s[k] - I.h[k] * dzk;     // Δs = -d_s - H Δz
+            }
+            if (tid == 0) { C.dtau[which] = dt; C.dkappa[which] = dk; }
+            __syncthreads();
+        };
+        // step to the boundary (steps.py:79-116): τ/κ + nonneg ray
+        auto step_length = [&](int which) -> double {
+            const double dt = C.dtau[which], dk = C.dkappa[which];
+            double a = 1.0;
+            if (dt < 0.0) a = fmin(a, -tau / dt);
+            if (dk < 0.0) a = fmin(a, -kappa / dk);
+            double v[1] = {INFINITY};
+            for (int k = tid; k < nnd; k += BT) {
+                const double dzk = I.dz[which][z0 + k], dsk = I.ds[which][z0 + k];
+                if (dzk < 0.0) v[0] = fmin(v[0], -I.z[z0 + k] / dzk);
+                if (dsk < 0.0) v[0] = fmin(v[0], -I.s[z0 + k] / dsk);
+            }
+            // min-reduction (max of negatives)
+            v[0] = -v[0];
+            breduce<1>(v, 1u, sred);
+            return fmin(a, -v[0]);
+        };
+
+        // ---- affine direction ----
+        for (int k = tid; k < dim; k += BT) I.rb[k] = k < n ? I.gx[k] : -(I.gz[k - n] - I.s[k - n]);
+        __syncthreads();
+        refined(I.sol);
+        recover(0, gtau, kappa * tau, I.s);
+        const double alpha_a = step_length(0);
+        if (alpha_a < 1e-11) { status = BS_NUMERICAL; break; }
+        const double sigma = pow(1.0 - alpha_a, 3.0);
+        const double f = 1.0 - sigma;
+        // ---- combined d_s (scaling.py:277-320, nonneg part) ----
+        for (int k = tid; k < m; k += BT) {
+            double o = 0.0;
+            if (k >= z0 && k < z0 + nnd) {
+                const double lam2 = I.s[k] * I.z[k];
+                const double eta = I.ds[0][k] * I.dz[0][k];
+                o = I.w[k] * ((lam2 + eta) - sigma * mu) / I.lam[k];
+            }
+            I.dsc[k] = o;
+        }
+        __syncthreads();
+        const double dkap_c = (kappa * tau + C.dkappa[0] * C.dtau[0]) - sigma * mu;
+        for (int k = tid; k < dim; k += BT) I.rb[k] = k < n ? f * I.gx[k] : -(f * I.gz[k - n] - I.dsc[k - n]);
+        __syncthreads();
+        refined(I.sol);
+        recover(1, f * gtau, dkap_c, I.dsc);
+        double alpha = step_length(1);
+        if (alpha < 1e-11) { status = BS_NUMERICAL; break; }
+        // ---- neighbourhood backtracking (ipm.py:350-366, scaling.py:364-374) ----
+        bool ok = false;
+        for (int tries = 0; tries < 4096; ++tries) {
+            const double a = bd.step_scale * alpha;
+            double v[3] = {0.0, 0.0, 0.0};
+            for (int k = tid; k < m; k += BT) {
+                const double st = I.s[k] + a * I.ds[1][k], zt = I.z[k] + a * I.dz[1][k];
+                const double pz = st * zt;
+                v[0] += pz;
+                if (k >= z0 && k < z0 + nnd) {
+                    if (!(st > 0.0) || !(zt > 0.0)) v[2] = 1.0;
+                    v[1] += 1.0 / pz;
+                }
+            }
+            breduce<3>(v, 0u, sred);
+            if (v[2] != 0.0) break;   // DomainError
+            const double mu_t = (v[0] + (tau + a * C.dtau[1]) * (kappa + a * C.dkappa[1])) / nu1;
+            if (!(nnd && (double)nnd / v[1] < bd.beta * mu_t)) { ok = true; break; }
+            alpha *= bd.backtrack;
+            if (alpha < 1e-11) break;
+        }
+        if (!ok) { status = BS_NUMERICAL; break; }
+        // ---- take_step (ipm.py:368-379) ----
+        const double a = bd.step_scale * alpha;
+        for (int k = tid; k < n; k += BT) I.x[k] = I.x[k] + a * I.dx[1][k];
+        double mv[2] = {0.0, 0.0};
+        for (int k = tid; k < m; k += BT) {
+            const double zk = I.z[k] + a * I.dz[1][k];
+            const double sk = I.s[k] + a * I.ds[1][k];
+            I.z[k] = zk;
+            I.s[k] = sk;
+            if (k < z0 && sk != 0.0) mv[1] = 1.0;
+            if (k >= z0 && k < z0 + nnd && (!(sk > 0.0) || !(zk > 0.0))) mv[1] = 1.0;
+            mv[0] += sk * zk;
+        }
+        breduce<2>(mv, 0u, sred);
+        const double nt = tau + a * C.dtau[1], nk = kappa + a * C.dkappa[1];
+        if (!(nt > 0.0) || !(nk > 0.0) || mv[1] != 0.0) { status = BS_NUMERICAL; break; }
+        if (tid == 0) {
+            C.tau = nt;
+            C.kappa = nk;
+            C.mu = (mv[0] + nt * nk) / nu1;
+        }
+        __syncthreads();
+        iterations = it + 1;
+    }
+    __syncthreads();
+    // ---- outputs: the host recovers (unscale, un-permute, certificates) ----
+    const bool terminal = status == BS_OPTIMAL || status == BS_PRIMAL_INF || status == BS_DUAL_INF;
+    int final_status = status;
+    const double* px = I.x;
+    const double* pz = I.z;
+    const double* ps = I.s;
+    double res[9];
+    if (terminal) {
+        res[0] = cur_r[0]; res[1] = cur_r[1]; res[2] = cur_r[2]; res[3] = cur_r[3];
+        res[4] = C.tau; res[5] = C.kappa; res[6] = C.mu;
+    } else {
+        // best iterate; ALMOST_OPTIMAL if it meets 10ε (ipm.py:489-496)
+        px = bx; pz = bz_; ps = bs;
+        for (int k = 0; k < 7; ++k) res[k] = best_r[k];
+        const double e10 = 10.0 * eps_feas;
+        if (best_r[7] != 0.0 && best_r[8] < e10 && best_r[9] < e10 && best_r[10] < e10) final_status = BS_ALMOST;
+    }
+    res[7] = mu0;
+    res[8] = (double)iterations;
+    __syncthreads();
+    double* ox = bd.out_x + (int64_t)inst * n;
+    double* oz = bd.out_z + (int64_t)inst * m;
+    double* os = bd.out_s + (int64_t)inst * m;
+    for (int k = tid; k < n; k += BT) ox[k] = px[k];
+    for (int k = tid; k < m; k += BT) { oz[k] = pz[k]; os[k] = ps[k]; }
+    if (tid == 0) {
+        bd.out_status[inst] = final_status;
+        for (int k = 0; k < 9; ++k) bd.out_res[(int64_t)inst * 9 + k] = res[k];
+    }
+}
+
+}  // namespace
+
+size_t batch_smem_doubles(const BatchPattern& pt) {
+    const int64_t n = pt.n, m = pt.m, dim = n + m;
+    auto r2 = [](int64_t c) { return (c + 1) & ~int64_t(1); };
+    return (size_t)(r2(n) * 4 + r2(m) * 12 + r2(dim) * 7 + r2(pt.nnz_p + pt.nnz_a) + r2(pt.nnz_l) + r2(dim) * 2);
+}
+
+int batch_launch(const BatchPattern& pt, const BatchData& bd, int count, cudaStream_t stream, int smem_bytes) {
+    if (smem_bytes > 0) {
+        CIPM_CUDA(cudaFuncSetAttribute(batch_ipm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    }
+    batch_ipm<<<count, BT, smem_bytes > 0 ? smem_bytes : 0, stream>>>(pt, bd, count);
+    CIPM_CUDA(cudaGetLastError());
+    return CIPM_OK;
+}
+
+}  // namespace cipm
+
+// ===========================================================================
+// host side: pattern analysis (once) + the C ABI (include/cipm.h cipm_batch_*)
+// ===========================================================================
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "symbolic.hpp"
+
+struct cipm_batch {
+    cipm::BatchPattern pt;
+    cipm::BatchData bd;
+    int count = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int smem_bytes = 0;
+    std::vector<void*> allocs;
+    std::vector<int32_t> h_perm;
+    int64_t h2d = 0, d2h = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+template <typename T>
+int bup(cipm_batch* h, const T** dst, const std::vector<T>& v) {
+    void* p = nullptr;
+    CIPM_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(v.size(), 1)));
+    h->allocs.push_back(p);
+    if (!v.empty()) CIPM_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    *dst = (const T*)p;
+    return CIPM_OK;
+}
+
+template <typename T>
+int balloc(cipm_batch* h, T** dst, int64_t count) {
+    void* p = nullptr;
+    CIPM_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(count, 1)));
+    h->allocs.push_back(p);
+    *dst = (T*)p;
+    return CIPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings* st, double eps_feas,
+                      double eps_inf, int max_iter, cipm_batch** out) {
+    using namespace cipm;
+    if (!d || !st || !out || count <= 0) return CIPM_E_ARG;
+    if (d->n_soc || d->n_exp || d->n_pow || d->n_psd) {
+        fprintf(stderr, "[cipm] batched instances support zero + nonnegative cones only\n");
+        return CIPM_E_ARG;
+    }
+    if (st->precision != CIPM_FULL) {
+        fprintf(stderr, "[cipm] batched instances run the full-precision factorisation\n");
+        return CIPM_E_ARG;
+    }
+    const int64_t n = d->n, m = d->m, dim = n + m;
+    const int64_t nnzp = d->p_rowptr[n], nnza = d->a_rowptr[m];
+    auto* h = new cipm_batch();
+    h->count = count;
+    h->device = st->device;
+    CIPM_CUDA(cudaSetDevice(h->device));
+    if (st->stream) {
+        h->stream = (cudaStream_t)st->stream;
+    } else {
+        CIPM_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    // K upper pattern with value sources (kkt/system.py:87-148)
+    std::vector<int64_t> key;
+    std::vector<int32_t> ksrc;
+    key.reserve(n + nnzp + nnza + m);
+    std::vector<std::pair<int64_t, int32_t>> ent;
+    for (int64_t i = 0; i < n; ++i) ent.emplace_back(i * dim + i, -1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = d->p_rowptr[i]; p < d->p_rowptr[i + 1]; ++p)
+            if (d->p_colidx[p] >= i) ent.emplace_back(i * dim + d->p_colidx[p], (int32_t)p);
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t p = d->a_rowptr[r]; p < d->a_rowptr[r + 1]; ++p)
+            ent.emplace_back(d->a_colidx[p] * dim + (n + r), (int32_t)(nnzp + p));
+    for (int64_t i = 0; i < m; ++i) ent.emplace_back((n + i) * dim + (n + i), (int32_t)(-2 - i));
+    std::stable_sort(ent.begin(), ent.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    // unique keys; a P diagonal entry overrides the structural x-diagonal slot
+    std::vector<int64_t> kr, kc;
+    std::vector<int32_t> src;
+    for (size_t e = 0; e < ent.size(); ++e) {
+        if (!key.empty() && key.back() == ent[e].first) {
+            if (ent[e].second != -1) src.back() = ent[e].second;
+            continue;
+        }
+        key.push_back(ent[e].first);
+        src.push_back(ent[e].second);
+    }
+    std::vector<int64_t> krp(dim + 1, 0), kci(key.size());
+    for (size_t e = 0; e < key.size(); ++e) {
+        krp[key[e] / dim + 1]++;
+        kci[e] = key[e] % dim;
+    }
+    for (int64_t i = 0; i < dim; ++i) krp[i + 1] += krp[i];
+    // the reference's minimum-degree order of that pattern (ordering.py:15-53)
+    std::vector<int32_t> perm(dim);
+    {
+        int rc = cipm_min_degree(dim, krp.data(), kci.data(), perm.data());
+        if (rc) { delete h; return rc; }
+    }
+    std::vector<int32_t> iperm(dim);
+    for (int64_t k = 0; k < dim; ++k) iperm[perm[k]] = (int32_t)k;
+    // permuted upper CSC sorted by (column, row) (system.py:198-219)
+    const int64_t nk = (int64_t)key.size();
+    std::vector<int64_t> rr(nk), cc(nk), ord(nk);
+    for (int64_t e = 0; e < nk; ++e) {
+        const int64_t pi = iperm[key[e] / dim], pj = iperm[key[e] % dim];
+        rr[e] = std::min(pi, pj);
+        cc[e] = std::max(pi, pj);
+    }
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return cc[a] != cc[b] ? cc[a] < cc[b] : rr[a] < rr[b]; });
+    std::vector<int32_t> cp(dim + 1, 0), ci(nk), csrc(nk);
+    for (int64_t t = 0; t < nk; ++t) {
+        ci[t] = (int32_t)rr[ord[t]];
+        csrc[t] = src[ord[t]];
+        cp[cc[ord[t]] + 1]++;
+    }
+    for (int64_t j = 0; j < dim; ++j) cp[j + 1] += cp[j];
+    std::vector<int8_t> sign(dim);
+    for (int64_t k = 0; k < dim; ++k) sign[k] = perm[k] < n ? 1 : -1;
+    // etree + column counts (ldl.py:20-34), then the up-looking visiting schedule (ldl.py:37-88)
+    std::vector<int32_t> parent(dim, -1), flag(dim, -1), lnz(dim, 0);
+    for (int64_t j = 0; j < dim; ++j) {
+        flag[j] = (int32_t)j;
+        for (int32_t p = cp[j]; p < cp[j + 1]; ++p)
+            for (int32_t i = ci[p]; flag[i] != j; i = parent[i]) {
+                if (parent[i] == -1) parent[i] = (int32_t)j;
+                lnz[i]++;
+                flag[i] = (int32_t)j;
+            }
+    }
+    std::vector<int32_t> lp(dim + 1, 0);
+    for (int64_t j = 0; j < dim; ++j) lp[j + 1] = lp[j] + lnz[j];
+    const int64_t nnzl = lp[dim];
+    std::vector<int32_t> li(nnzl), upp(dim + 1, 0), upi, up2, cnt(dim, 0), pattern(dim);
+    upi.reserve(nnzl);
+    up2.reserve(nnzl);
+    std::fill(flag.begin(), flag.end(), -1);
+    for (int64_t j = 0; j < dim; ++j) {
+        int64_t top = dim;
+        flag[j] = (int32_t)j;
+        for (int32_t p = cp[j]; p < cp[j + 1]; ++p) {
+            int32_t i = ci[p];
+            int64_t len = 0;
+            while (flag[i] != j) { pattern[len++] = i; flag[i] = (int32_t)j; i = parent[i]; }
+            while (len > 0) pattern[--top] = pattern[--len];
+        }
+        for (int64_t t = top; t < dim; ++t) {
+            const int32_t i = pattern[t];
+            const int32_t p2 = lp[i] + cnt[i];
+            upi.push_back(i);
+            up2.push_back(p2);
+            li[p2] = (int32_t)j;
+            cnt[i]++;
+        }
+        upp[j + 1] = (int32_t)upi.size();
+    }
+    // CSR / transposed patterns (int32)
+    std::vector<int32_t> prp(d->p_rowptr, d->p_rowptr + n + 1), pci(d->p_colidx, d->p_colidx + nnzp);
+    std::vector<int32_t> arp(d->a_rowptr, d->a_rowptr + m + 1), aci(d->a_colidx, d->a_colidx + nnza);
+    std::vector<int32_t> trp(n + 1, 0), tci(nnza), tsrc(nnza);
+    for (int64_t p = 0; p < nnza; ++p) trp[aci[p] + 1]++;
+    for (int64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
+    {
+        std::vector<int32_t> fill(trp.begin(), trp.end() - 1);
+        for (int64_t r = 0; r < m; ++r)
+            for (int32_t p = arp[r]; p < arp[r + 1]; ++p) {
+                const int32_t t = fill[aci[p]]++;
+                tci[t] = (int32_t)r;
+                tsrc[t] = p;
+            }
+    }
+    BatchPattern& pt = h->pt;
+    pt.n = (int)n;
+    pt.m = (int)m;
+    pt.zero_dim = (int)d->zero_dim;
+    pt.nonneg_dim = (int)d->nonneg_dim;
+    pt.nnz_p = (int)nnzp;
+    pt.nnz_a = (int)nnza;
+    pt.nnz_l = (int)nnzl;
+    int rc = 0;
+#define BTRY(x)           \
+    do {                  \
+        rc = (x);         \
+        if (rc) {         \
+            cipm_batch_destroy(h); \
+            return rc;    \
+        }                 \
+    } while (0)
+    BTRY(bup(h, &pt.p_rp, prp));
+    BTRY(bup(h, &pt.p_ci, pci));
+    BTRY(bup(h, &pt.a_rp, arp));
+    BTRY(bup(h, &pt.a_ci, aci));
+    BTRY(bup(h, &pt.at_rp, trp));
+    BTRY(bup(h, &pt.at_ci, tci));
+    BTRY(bup(h, &pt.at_src, tsrc));
+    BTRY(bup(h, &pt.cp, cp));
+    BTRY(bup(h, &pt.ci, ci));
+    BTRY(bup(h, &pt.csrc, csrc));
+    BTRY(bup(h, &pt.sign, sign));
+    BTRY(bup(h, &pt.perm, perm));
+    BTRY(bup(h, &pt.lp, lp));
+    BTRY(bup(h, &pt.li, li));
+    BTRY(bup(h, &pt.up_ptr, upp));
+    BTRY(bup(h, &pt.up_i, upi));
+    BTRY(bup(h, &pt.up_p2, up2));
+    h->h_perm = perm;
+    // per-instance buffers
+    BatchData& bd = h->bd;
+    const int64_t nv = nnzp + nnza;
+    double* tmp = nullptr;
+    BTRY(balloc(h, &tmp, count * nv)); bd.V = tmp;
+    BTRY(balloc(h, &tmp, count * n)); bd.q = tmp;
+    BTRY(balloc(h, &tmp, count * m)); bd.b = tmp;
+    BTRY(balloc(h, &tmp, count * m)); bd.dr = tmp;
+    BTRY(balloc(h, &tmp, count * n)); bd.dc = tmp;
+    BTRY(balloc(h, &tmp, count)); bd.c_obj = tmp;
+    BTRY(balloc(h, &tmp, count)); bd.norm_q = tmp;
+    BTRY(balloc(h, &tmp, count)); bd.norm_b = tmp;
+    BTRY(balloc(h, &bd.best_x, count * n));
+    BTRY(balloc(h, &bd.best_z, count * m));
+    BTRY(balloc(h, &bd.best_s, count * m));
+    BTRY(balloc(h, &bd.out_x, count * n));
+    BTRY(balloc(h, &bd.out_z, count * m));
+    BTRY(balloc(h, &bd.out_s, count * m));
+    BTRY(balloc(h, &bd.out_res, count * 9));
+    BTRY(balloc(h, &bd.out_status, count));
+    const size_t nd = batch_smem_doubles(pt);
+    const size_t bytes = nd * sizeof(double);
+    if (bytes <= 200 * 1024) {
+        bd.use_smem = 1;
+        h->smem_bytes = (int)bytes;
+    } else {
+        bd.use_smem = 0;
+        bd.ws_stride = (int64_t)nd;
+        BTRY(balloc(h, &bd.workspace, (int64_t)count * (int64_t)nd));
+        h->smem_bytes = 0;
+    }
+    bd.eps_feas = eps_feas;
+    bd.eps_inf = eps_inf;
+    bd.max_iter = max_iter;
+    bd.delta_s = st->delta_s;
+    bd.delta_d = st->delta_d;
+    bd.beta = st->beta;
+    bd.backtrack = st->backtrack;
+    bd.step_scale = st->step_scale;
+    bd.refine_abs = st->refine_abs;
+    bd.refine_rel = st->refine_rel;
+    bd.refine_max = st->refine_max;
+    CIPM_CUDA(cudaEventCreate(&h->ev0));
+    CIPM_CUDA(cudaEventCreate(&h->ev1));
+#undef BTRY
+    *out = h;
+    return CIPM_OK;
+}
+
+int cipm_batch_info(const cipm_batch* h, int64_t* info) {
+    if (!h || !info) return CIPM_E_ARG;
+    info[0] = h->count;
+    info[1] = h->pt.n;
+    info[2] = h->pt.m;
+    info[3] = h->pt.nnz_l;
+    info[4] = h->smem_bytes;
+    info[5] = h->bd.use_smem;
+    return CIPM_OK;
+}
+
+int cipm_batch_set_values(cipm_batch* h, const double* V, const double* q, const double* b, const double* dr,
+                          const double* dc, const double* c_obj, const double* norm_q, const double* norm_b) {
+    if (!h) return CIPM_E_ARG;
+    const int64_t c = h->count, n = h->pt.n, m = h->pt.m, nv = (int64_t)h->pt.nnz_p + h->pt.nnz_a;
+    CIPM_CUDA(cudaSetDevice(h->device));
+    auto cp = [&](const double* dst, const double* src, int64_t cnt) -> int {
+        CIPM_CUDA(cudaMemcpyAsync((void*)dst, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, h->stream));
+        h->h2d += (int64_t)sizeof(double) * cnt;
+        return CIPM_OK;
+    };
+    int rc = cp(h->bd.V, V, c * nv);
+    if (!rc) rc = cp(h->bd.q, q, c * n);
+    if (!rc) rc = cp(h->bd.b, b, c * m);
+    if (!rc) rc = cp(h->bd.dr, dr, c * m);
+    if (!rc) rc = cp(h->bd.dc, dc, c * n);
+    if (!rc) rc = cp(h->bd.c_obj, c_obj, c);
+    if (!rc) rc = cp(h->bd.norm_q, norm_q, c);
+    if (!rc) rc = cp(h->bd.norm_b, norm_b, c);
+    return rc;
+}
+
+int cipm_batch_solve(cipm_batch* h, double* ms) {
+    if (!h) return CIPM_E_ARG;
+    CIPM_CUDA(cudaSetDevice(h->device));
+    CIPM_CUDA(cudaEventRecord(h->ev0, h->stream));
+    int rc = cipm::batch_launch(h->pt, h->bd, h->count, h->stream, h->smem_bytes);
+    if (rc) return rc;
+    CIPM_CUDA(cudaEventRecord(h->ev1, h->stream));
+    CIPM_CUDA(cudaEventSynchronize(h->ev1));
+    CIPM_CUDA(cudaGetLastError());
+    if (ms) {
+        float v = 0.f;
+        CIPM_CUDA(cudaEventElapsedTime(&v, h->ev0, h->ev1));
+        *ms = v;
+    }
+    return CIPM_OK;
+}
+
+int cipm_batch_results(cipm_batch* h, int32_t* status, double* res, double* x, double* z, double* s) {
+    if (!h) return CIPM_E_ARG;
+    const int64_t c = h->count, n = h->pt.n, m = h->pt.m;
+    CIPM_CUDA(cudaSetDevice(h->device));
+    CIPM_CUDA(cudaStreamSynchronize(h->stream));
+    if (status) CIPM_CUDA(cudaMemcpy(status, h->bd.out_status, sizeof(int32_t) * c, cudaMemcpyDeviceToHost));
+    if (res) CIPM_CUDA(cudaMemcpy(res, h->bd.out_res, sizeof(double) * c * 9, cudaMemcpyDeviceToHost));
+    if (x) CIPM_CUDA(cudaMemcpy(x, h->bd.out_x, sizeof(double) * c * n, cudaMemcpyDeviceToHost));
+    if (z) CIPM_CUDA(cudaMemcpy(z, h->bd.out_z, sizeof(double) * c * m, cudaMemcpyDeviceToHost));
+    if (s) CIPM_CUDA(cudaMemcpy(s, h->bd.out_s, sizeof(double) * c * m, cudaMemcpyDeviceToHost));
+    h->d2h += (int64_t)(status ? 4 * c : 0) + (int64_t)sizeof(double) * ((res ? 9 * c : 0) + (x ? c * n : 0) +
+                                                                         (z ? c * m : 0) + (s ? c * m : 0));
+    return CIPM_OK;
+}
+
+int cipm_batch_io_bytes(cipm_batch* h, int64_t* h2d, int64_t* d2h, int reset) {
+    if (!h) return CIPM_E_ARG;
+    if (h2d) *h2d = h->h2d;
+    if (d2h) *d2h = h->d2h;
+    if (reset) h->h2d = h->d2h = 0;
+    return CIPM_OK;
+}
+
+void cipm_batch_destroy(cipm_batch* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (void* p : h->allocs) cudaFree(p);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // extern "C"

@@ -445,6 +445,15 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         c.allocations.push_back(p);
         c.vin = p;
     }
+    {
+        int64_t inv_total = 0, flag_total = 0;
+        tail_setup(c, &inv_total, &flag_total);
+        void* p = nullptr;
+        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(inv_total, 1)));
+        c.allocations.push_back(p);
+        c.tinv = p;
+        TRY(dalloc(c, &c.tflags, flag_total));
+    }
     TRY(dalloc(c, &c.fac_count, S.nsuper));
     TRY(dalloc(c, &c.bwd_done, S.nsuper));
     TRY(dalloc(c, &c.tickets, 4));

@@ -39,6 +39,30 @@ __device__ __forceinline__ void atomic_min_pos(double* addr, double val) {
 
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
 
+// Dependency flags between CTAs/warps of one persistent launch.  Poll with a
+// relaxed load (no per-poll L1 invalidation — ld.acquire compiles to
+// LDG.STRONG + CCTL.IVALL, which thrashes the SM's L1 for every other warp),
+// then order the following reads with one fence.  Data produced by other CTAs
+// is read with ld.cg (L2) anyway.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void wait_ge(const int* p, int need) {
+    if (ld_relaxed(p) < need) {
+        do {
+            __nanosleep(32);
+        } while (ld_relaxed(p) < need);
+    }
+    __threadfence();
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // deterministic multi-value reduction: each block writes K partials, the last
 // block to arrive combines them in block order (fixed grid => bitwise
@@ -102,15 +126,19 @@ __device__ bool grid_reduce(double (&vals)[K], const int (&ops)[K], double* part
     }
     __syncthreads();
     if (!last) return false;
-    if (threadIdx.x == 0) {
-        __threadfence();
+    __threadfence();
+    // last block: thread t folds blocks t, t+nt, ... (fixed order), then a fixed tree
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double acc = red_identity(ops[k]);
-            for (unsigned int b = 0; b < gridDim.x; ++b)
-                acc = red_apply(ops[k], acc, __ldcg(partials + b * K + k));
-            out[k] = acc;
-        }
+    for (int k = 0; k < K; ++k) {
+        double acc = red_identity(ops[k]);
+        for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+            acc = red_apply(ops[k], acc, __ldcg(partials + b * K + k));
+        vals[k] = acc;
+    }
+    block_reduce<K>(vals, ops, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) out[k] = vals[k];
         *counter = 0u;
         return true;
     }

@@ -48,6 +48,12 @@ struct DevSymbolic {
     int64_t ninbox = 0, nv = 0;
 };
 
+// one supernode of the dense tail (dense.cu), in topological order
+struct TailNode {
+    int32_t J = 0, c0 = 0, w = 0, r = 0, parent = -1, nbd = 0;
+    int64_t r0 = 0, loff = 0, inv_off = 0, flag_off = 0;
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -116,6 +122,11 @@ struct Ctx {
     void* inbox = nullptr;           // factor contribution inbox (T)
     void* vin = nullptr;             // solve contribution inbox, 2 x nv (T)
     int factor_blocks = 0, solve_blocks = 0, factor_smem = 0;
+    // dense tail (dense.cu)
+    std::vector<TailNode> tail;
+    void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)
+    int32_t* tflags = nullptr;       // per tail node: fwd flags, bwd flags, 2 tickets
+    int64_t tflag_total = 0;
 
     // refinement (up to 2 right-hand sides, [rhs][dim])
     double *rb = nullptr, *rx = nullptr, *rr = nullptr, *rbest = nullptr;
@@ -187,5 +198,10 @@ void k_build_base(Ctx& c);
 void k_assemble(Ctx& c);
 int k_factor(Ctx& c);
 void k_refine_step(Ctx& c, int nrhs, const int* active_host);
+// dense.cu
+void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total);
+void k_tail_factor(Ctx& c);
+void k_tail_forward(Ctx& c, void* x, int act0, int act1);
+void k_tail_backward(Ctx& c, void* x, int act0, int act1);
 
 }  // namespace cipm

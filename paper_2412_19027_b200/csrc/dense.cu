@@ -1,0 +1,630 @@
+// Dense "tail" of the supernodal LDL' (replaces the wide-supernode share of
+// kkt/ldl.py:37-104 / kkt/system.py:246-271).
+//
+// Supernodes that are wide (w >= 64) or have a large contribution block
+// (o >= 512) — and all their ancestors — are too big for one CTA of the
+// persistent kernel in ldl.cu (the C1 LP's 1787-column root, the C4 exp/pow
+// 5143-column root).  They run here after the persistent phase, one supernode
+// at a time in topological order, as a blocked right-looking dense LDL' over
+// the panel (r rows x w columns, column-major, ld = r) in HBM:
+//
+//   tail_gather   inbox -> panel (warp per row, fixed-order segmented sums)
+//   for each 64-column block kb:
+//     tail_diag   64x64 diagonal block: unblocked LDL' with the reference's
+//                 dynamic-regularisation rule (ldl.py:79-87), one CTA
+//     tail_trsm   rows below: L21 = A21 L11^-T D^-1 (thread per row)
+//     tail_gemm   trailing panel columns -= L21 D L21'   (FP64: DMMA
+//                 mma.sync.m8n8k4 tensor-core tiles; FP32: FFMA tiles)
+//   tail_inv      explicit inverses of the unit-lower diagonal blocks (solves)
+//   tail_gemm     contribution block C = L_off D L_off' pushed to the ancestors'
+//                 inboxes (same GEMM, scatter epilogue)
+//
+// Triangular solves of a tail supernode are single multi-CTA launches: one CTA
+// per 64-row block, ordered by an atomic ticket and synchronised with
+// per-block release/acquire flags (a wavefront over the diagonal blocks);
+// the diagonal solves are GEMVs with the precomputed block inverses.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+namespace cipm {
+
+namespace {
+
+constexpr int TB = 64;   // tail block size (columns / rows)
+
+__device__ __forceinline__ void wait_flag(const int* p) { wait_ge(p, 1); }
+
+// ---------------------------------------------------------------------------
+// inbox gather: warp per panel row; entries of a row are sorted by target
+// (column-major panel offset), equal targets contiguous (one per source).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) tail_gather(T* __restrict__ L, int r, const int64_t* __restrict__ irow,
+                                                   const int32_t* __restrict__ tgt, const T* __restrict__ inbox) {
+    const int lane = threadIdx.x & 31;
+    const int tr = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (tr >= r) return;
+    const int64_t lo = irow[tr], hi = irow[tr + 1];
+    int carry_t = -1;
+    T carry = (T)0;
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t e = base + lane;
+        const bool valid = e < hi;
+        const int tg = valid ? tgt[e] : -(lane + 2);
+        T v = valid ? __ldcg(inbox + e) : (T)0;
+        const int t0 = __shfl_sync(0xffffffffu, tg, 0);
+        if (carry_t >= 0 && t0 != carry_t) {
+            if (lane == 0) L[carry_t] -= carry;
+            carry_t = -1;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int tp = __shfl_up_sync(0xffffffffu, tg, off);
+            const T vp = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off && tp == tg) v += vp;
+        }
+        const int tn = __shfl_down_sync(0xffffffffu, tg, 1);
+        const bool is_end = lane == 31 || tn != tg;
+        const bool more = base + 32 < hi;
+        T tot = v;
+        if (valid && is_end && tg == carry_t) tot += carry;
+        if (valid && is_end && !(lane == 31 && more)) L[tg] -= tot;
+        const int t31 = __shfl_sync(0xffffffffu, tg, 31);
+        const T v31 = __shfl_sync(0xffffffffu, tot, 31);
+        if (more) {
+            carry_t = t31;
+            carry = v31;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// diagonal block: unblocked LDL' of the nb x nb block at (kb, kb)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int kb, int nb, int c0,
+                                                 T* __restrict__ dvec, const int8_t* __restrict__ sign,
+                                                 double* maxd, int32_t* bumps, int* err, double delta_s,
+                                                 double delta_d) {
+    __shared__ T S[TB][TB + 1];      // S[i][j], i >= j
+    __shared__ double s_piv, s_runmax;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    T* B = L + (int64_t)kb * r + kb;
+    for (int idx = tid; idx < nb * nb; idx += nt) {
+        const int i = idx % nb, j = idx / nb;
+        if (i >= j) S[i][j] = B[(int64_t)j * r + i];
+    }
+    if (tid == 0) s_runmax = *maxd;
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+        if (tid == 0) {
+            double d = (double)S[j][j];
+            const double bound = delta_s + delta_d * s_runmax;
+            if (fabs(d) < bound) {
+                d = sign[c0 + kb + j] > 0 ? bound : -bound;
+                atomicAdd(bumps, 1);
+            }
+            const T dt = (T)d;
+            if (dt == (T)0) set_error(err, CIPM_E_FACTOR);
+            dvec[c0 + kb + j] = dt;
+            S[j][j] = (T)1;
+            s_piv = (double)dt;
+            s_runmax = fmax(s_runmax, fabs(d));
+        }
+        __syncthreads();
+        const T d = (T)s_piv;
+        for (int i = j + 1 + tid; i < nb; i += nt) S[i][j] = S[i][j] / d;
+        __syncthreads();
+        const int rem = nb - j - 1;
+        const int tot = rem * rem;
+        for (int idx = tid; idx < tot; idx += nt) {
+            const int i = j + 1 + idx % rem, c = j + 1 + idx / rem;
+            if (i >= c) S[i][c] -= S[i][j] * d * S[c][j];
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < nb * nb; idx += nt) {
+        const int i = idx % nb, j = idx / nb;
+        if (i >= j) B[(int64_t)j * r + i] = S[i][j];
+    }
+    if (tid == 0) *maxd = s_runmax;
+}
+
+// ---------------------------------------------------------------------------
+// rows below the diagonal block: l_i = a_i L11^-T D^-1 (thread per row)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) tail_trsm(T* __restrict__ L, int r, int kb, int nb, int row_begin,
+                                                 const T* __restrict__ dblk) {
+    // dynamic smem: U[k][j] = d_k * L11[j][k] (k < j), then the CTA's rows As[t][j]
+    extern __shared__ __align__(16) unsigned char tsm_raw[];
+    T* U = reinterpret_cast<T*>(tsm_raw);                 // TB x (TB+1)
+    T* As = U + TB * (TB + 1);                            // 128 x (TB+1)
+    __shared__ T dinv[TB];
+    const T* B = L + (int64_t)kb * r + kb;
+    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+        const int j = idx % TB, k = idx / TB;
+        U[k * (TB + 1) + j] = (j > k && j < nb) ? dblk[k] * B[(int64_t)k * r + j] : (T)0;
+    }
+    for (int k = threadIdx.x; k < TB; k += blockDim.x) dinv[k] = k < nb ? (T)1 / dblk[k] : (T)0;
+    const int i0 = row_begin + blockIdx.x * blockDim.x;
+    const int nrows = min((int)blockDim.x, r - i0);
+    // coalesced load of the 128 x nb row block (column-major in global)
+    for (int idx = threadIdx.x; idx < nrows * nb; idx += blockDim.x) {
+        const int t = idx % nrows, j = idx / nrows;
+        As[t * (TB + 1) + j] = L[(int64_t)(kb + j) * r + i0 + t];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nrows) {
+        T* a = As + t * (TB + 1);
+        for (int j = 0; j < nb; ++j) {
+            T v = a[j];
+            const T* Uj = U + j;
+            for (int k = 0; k < j; ++k) v -= a[k] * Uj[k * (TB + 1)];
+            a[j] = v * dinv[j];
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nrows * nb; idx += blockDim.x) {
+        const int tt = idx % nrows, j = idx / nrows;
+        L[(int64_t)(kb + j) * r + i0 + tt] = As[tt * (TB + 1) + j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// C (M x N, lower: i + diag_off >= j) op= A (M x K) * diag(d) * B (N x K)'
+// A, B column-major with leading dimensions lda / ldb.  MODE 0: C -= acc in
+// place (ld = ldc).  MODE 1: inbox[push_pos[i,j packed]] = acc.
+// 64x64 CTA tile, 4 warps of 32x32, BK = 16; FP64 uses DMMA m8n8k4.
+// ---------------------------------------------------------------------------
+constexpr int GB = 64, GK = 16, GP = GB + 4;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) tail_gemm(const T* __restrict__ A, int lda, const T* __restrict__ Bm, int ldb,
+                                                 const T* __restrict__ d, int M, int N, int K, int diag_off,
+                                                 T* __restrict__ C, int ldc, const int64_t* __restrict__ push_pos,
+                                                 T* __restrict__ inbox) {
+    const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
+    if (m0 + GB - 1 + diag_off < n0) return;      // tile strictly above the diagonal
+    __shared__ __align__(16) T As[GK][GP];
+    __shared__ __align__(16) T Bs[GK][GP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int li = tid & 63, lk = tid >> 6;   // loader: row li, k = lk + 2t
+    for (int k0 = 0; k0 < K; k0 += GK) {
+#pragma unroll
+        for (int t = 0; t < GK / 2; ++t) {
+            const int k = lk + 2 * t;
+            const int gk = k0 + k;
+            T av = (T)0, bv = (T)0;
+            if (gk < K) {
+                if (m0 + li < M) av = A[(int64_t)gk * lda + m0 + li];
+                if (n0 + li < N) bv = Bm[(int64_t)gk * ldb + n0 + li] * d[gk];
+            }
+            As[k][li] = av;
+            Bs[k][li] = bv;
+        }
+        __syncthreads();
+        if constexpr (std::is_same<T, double>::value) {
+#pragma unroll
+            for (int kk = 0; kk < GK; kk += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) af[a] = As[kk + (lane & 3)][wm * 32 + a * 8 + (lane >> 2)];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) bf[b] = Bs[kk + (lane & 3)][wn * 32 + b * 8 + (lane >> 2)];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            }
+        } else {
+            // FP32 (mixed mode): same fragment ownership, FFMA accumulation
+#pragma unroll 4
+            for (int k = 0; k < GK; ++k) {
+                float af[4], bf[4][2];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) af[a] = As[k][wm * 32 + a * 8 + (lane >> 2)];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    bf[b][0] = Bs[k][wn * 32 + b * 8 + (lane & 3) * 2];
+                    bf[b][1] = Bs[k][wn * 32 + b * 8 + (lane & 3) * 2 + 1];
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        acc[a][b][0] += (double)(af[a] * bf[b][0]);
+                        acc[a][b][1] += (double)(af[a] * bf[b][1]);
+                    }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = m0 + wm * 32 + a * 8 + (lane >> 2);
+                const int j = n0 + wn * 32 + b * 8 + (lane & 3) * 2 + e;
+                if (i >= M || j >= N || i + diag_off < j) continue;
+                if (MODE == 0) {
+                    T* p = C + (int64_t)j * ldc + i;
+                    *p = *p - (T)acc[a][b][e];
+                } else {
+                    const int64_t tpk = (int64_t)j * M - (int64_t)j * (j - 1) / 2 + (i - j);
+                    inbox[push_pos[tpk]] = (T)acc[a][b][e];
+                }
+            }
+}
+
+// explicit inverse of each unit-lower diagonal block (row-major, lower incl. diagonal);
+// thread t owns column t of the inverse and builds it in the output buffer
+template <typename T>
+__global__ void __launch_bounds__(TB) tail_inv(const T* __restrict__ L, int r, int w, T* __restrict__ inv) {
+    __shared__ T Ls[TB][TB + 1];
+    const int b = blockIdx.x;
+    const int kb = b * TB;
+    const int nb = min(TB, w - kb);
+    const T* B = L + (int64_t)kb * r + kb;
+    T* out = inv + (int64_t)b * TB * TB;
+    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
+        const int i = idx % TB, j = idx / TB;
+        Ls[i][j] = (i > j && i < nb) ? B[(int64_t)j * r + i] : (T)0;
+        out[idx] = (T)0;
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nb) {
+        out[t * TB + t] = (T)1;
+        for (int i = t + 1; i < nb; ++i) {
+            T v = (T)0;
+            for (int k = t; k < i; ++k) v -= Ls[i][k] * out[k * TB + t];
+            out[i * TB + t] = v;
+        }
+    }
+}
+
+__global__ void tail_finish(double* maxd, int32_t* count, int J, int parent) {
+    if (parent >= 0) {
+        const double v = maxd[J];
+        atomicMax(reinterpret_cast<unsigned long long*>(maxd + parent), (unsigned long long)__double_as_longlong(v));
+        atomicAdd(count + parent, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// triangular solves of one tail supernode
+// ---------------------------------------------------------------------------
+struct TailSolveArgs {
+    int c0, w, r, nbd;
+    int64_t dim, nv, cvo;
+    const int32_t* rows;       // sn_rows + r0 (permuted row indices)
+    const int64_t* vcol_ptr;
+    const int64_t* vpush_pos;
+    int* flags;                // nbd flags
+    int* ticket;
+    int* done;                 // backward: solve-done flag of the supernode (persistent-kernel protocol)
+    int act0, act1;
+};
+
+// forward: CTA per row block (diag blocks 0..nbd-1, then off-row blocks)
+template <typename T>
+__global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a, const T* __restrict__ L, const T* __restrict__ inv,
+                                                T* x, T* vin) {
+    __shared__ int s_b;
+    __shared__ T acc[2][TB];
+    __shared__ T xs[2][TB];
+    __shared__ T part[4][2][TB];
+    const int tid = threadIdx.x, ri = tid & 63, kp = tid >> 6;
+    if (tid == 0) s_b = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int b = s_b;
+    const bool diag = b < a.nbd;
+    const int row0 = diag ? b * TB : a.w + (b - a.nbd) * TB;
+    const int rend = diag ? min(a.w, row0 + TB) : a.r;
+    const int nrow = min(TB, rend - row0);
+    const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    if (kp == 0) {
+        for (int q = 0; q < 2; ++q) {
+            T v = (T)0;
+            if (act[q] && ri < nrow && diag) {
+                const int col = a.c0 + row0 + ri;
+                v = x[q * a.dim + col];
+                const T* vq = vin + q * a.nv;
+                for (int64_t e = a.vcol_ptr[col]; e < a.vcol_ptr[col + 1]; ++e) v -= __ldcg(vq + e);
+            }
+            acc[q][ri] = v;
+        }
+    }
+    __syncthreads();
+    const int nblk = diag ? b : a.nbd;
+    for (int kb = 0; kb < nblk; ++kb) {
+        if (tid == 0) wait_flag(a.flags + kb);
+        __syncthreads();
+        const int kc = kb * TB, kn = min(TB, a.w - kc);
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, k = tid & 63;
+            xs[q][k] = (act[q] && k < kn) ? __ldcg(x + q * a.dim + a.c0 + kc + k) : (T)0;
+        }
+        __syncthreads();
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nrow) {
+            const T* Lr = L + (int64_t)kc * a.r + row0 + ri;
+            for (int k = kp; k < kn; k += 4) {
+                const T l = Lr[(int64_t)k * a.r];
+                p0 += l * xs[0][k];
+                p1 += l * xs[1][k];
+            }
+        }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (kp == 0)
+            for (int q = 0; q < 2; ++q)
+                acc[q][ri] -= ((part[0][q][ri] + part[1][q][ri]) + part[2][q][ri]) + part[3][q][ri];
+        __syncthreads();
+    }
+    if (diag) {
+        // x_b = inv(L_bb) * acc (row-major lower inverse)
+        const T* I = inv + (int64_t)b * TB * TB;
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nrow)
+            for (int t = kp; t <= ri; t += 4) {
+                const T iv = I[ri * TB + t];
+                p0 += iv * acc[0][t];
+                p1 += iv * acc[1][t];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (kp == 0 && ri < nrow)
+            for (int q = 0; q < 2; ++q)
+                if (act[q]) x[q * a.dim + a.c0 + row0 + ri] = ((part[0][q][ri] + part[1][q][ri]) + part[2][q][ri]) + part[3][q][ri];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_release(a.flags + b, 1);
+    } else if (kp == 0 && ri < nrow) {
+        const int64_t pos = a.vpush_pos[a.cvo + (row0 + ri - a.w)];
+        for (int q = 0; q < 2; ++q)
+            if (act[q]) vin[q * a.nv + pos] = -acc[q][ri];
+    }
+}
+
+// backward: CTA per column block, last block first
+template <typename T>
+__global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a, const T* __restrict__ L, const T* __restrict__ inv,
+                                                const T* __restrict__ dvec, T* x) {
+    __shared__ int s_b;
+    __shared__ T acc[2][TB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_b = a.nbd - 1 - atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int b = s_b;
+    const int col0 = b * TB;
+    const int ncol = min(TB, a.w - col0);
+    const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    // off rows (ancestors' x is final)
+    for (int j = warp; j < ncol; j += 8) {
+        const T* Lc = L + (int64_t)(col0 + j) * a.r;
+        T s0 = (T)0, s1 = (T)0;
+        for (int i = a.w + lane; i < a.r; i += 32) {
+            const T l = Lc[i];
+            const int gi = a.rows[i];
+            if (act[0]) s0 += l * __ldcg(x + gi);
+            if (act[1]) s1 += l * __ldcg(x + a.dim + gi);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            s0 += __shfl_down_sync(0xffffffffu, s0, o);
+            s1 += __shfl_down_sync(0xffffffffu, s1, o);
+        }
+        if (lane == 0) {
+            const int gc = a.c0 + col0 + j;
+            const T dj = dvec[gc];
+            acc[0][j] = act[0] ? __ldcg(x + gc) / dj - s0 : (T)0;
+            acc[1][j] = act[1] ? __ldcg(x + a.dim + gc) / dj - s1 : (T)0;
+        }
+    }
+    // later own blocks
+    for (int kb = a.nbd - 1; kb > b; --kb) {
+        if (tid == 0) wait_flag(a.flags + kb);
+        __syncthreads();
+        const int r0 = kb * TB, rn = min(TB, a.w - r0);
+        for (int j = warp; j < ncol; j += 8) {
+            const T* Lc = L + (int64_t)(col0 + j) * a.r + r0;
+            T s0 = (T)0, s1 = (T)0;
+            for (int i = lane; i < rn; i += 32) {
+                const T l = Lc[i];
+                if (act[0]) s0 += l * __ldcg(x + a.c0 + r0 + i);
+                if (act[1]) s1 += l * __ldcg(x + a.dim + a.c0 + r0 + i);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                s0 += __shfl_down_sync(0xffffffffu, s0, o);
+                s1 += __shfl_down_sync(0xffffffffu, s1, o);
+            }
+            if (lane == 0) {
+                acc[0][j] -= s0;
+                acc[1][j] -= s1;
+            }
+        }
+    }
+    __syncthreads();
+    // x_b = inv(L_bb)' * acc
+    if (tid < 2 * TB) {
+        const int q = tid >> 6, j = tid & 63;
+        if (act[q] && j < ncol) {
+            const T* I = inv + (int64_t)b * TB * TB;
+            T v = (T)0;
+            for (int t = j; t < ncol; ++t) v += I[t * TB + j] * acc[q][t];
+            x[q * a.dim + a.c0 + col0 + j] = v;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        st_release(a.flags + b, 1);
+        if (b == 0) st_release(a.done, 1);
+    }
+}
+
+template <typename T>
+constexpr int trsm_smem() {
+    return (int)sizeof(T) * (TB + 128) * (TB + 1);
+}
+
+template <typename T>
+void tail_factor_t(Ctx& c) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tail_trsm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem<T>());
+        attr = true;
+    }
+    T* L = (T*)c.lval;
+    T* D = (T*)c.dvec;
+    T* inbox = (T*)c.inbox;
+    T* inv = (T*)c.tinv;
+    const Symbolic& S = c.host_sym;
+    for (const TailNode& t : c.tail) {
+        T* P = L + t.loff;
+        const int r = t.r, w = t.w, o = r - w;
+        tail_gather<T><<<(r + 7) / 8, 256, 0, c.stream>>>(P, r, c.sym.irow_ptr + t.r0, c.sym.inbox_tgt, inbox);
+        c.launches++;
+        for (int kb = 0; kb < w; kb += TB) {
+            const int nb = std::min(TB, w - kb);
+            tail_diag<T><<<1, 256, 0, c.stream>>>(P, r, kb, nb, t.c0, D, c.sym.sign, c.sn_maxd + t.J, c.bumps, c.err,
+                                                  c.delta_s, c.delta_d);
+            c.launches++;
+            const int below = r - kb - nb;
+            if (below > 0) {
+                tail_trsm<T><<<(below + 127) / 128, 128, trsm_smem<T>(), c.stream>>>(P, r, kb, nb, kb + nb,
+                                                                                   D + t.c0 + kb);
+                c.launches++;
+            }
+            const int Mr = r - kb - nb, Nc = w - kb - nb;
+            if (Nc > 0) {
+                const T* A = P + (int64_t)kb * r + kb + nb;
+                dim3 g((Mr + GB - 1) / GB, (Nc + GB - 1) / GB);
+                tail_gemm<T, 0><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0 + kb, Mr, Nc, nb, 0,
+                                                         P + (int64_t)(kb + nb) * r + kb + nb, r, nullptr, nullptr);
+                c.launches++;
+            }
+        }
+        tail_inv<T><<<t.nbd, TB, 0, c.stream>>>(P, r, w, inv + t.inv_off);
+        c.launches++;
+        if (o > 0) {
+            const T* A = P + w;
+            dim3 g((o + GB - 1) / GB, (o + GB - 1) / GB);
+            tail_gemm<T, 1><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
+                                                     c.sym.push_pos + S.cb_off[t.J], inbox);
+            c.launches++;
+        }
+        tail_finish<<<1, 1, 0, c.stream>>>(c.sn_maxd, c.fac_count, t.J, t.parent);
+        c.launches++;
+    }
+}
+
+TailSolveArgs tail_args(Ctx& c, const TailNode& t, int which, int act0, int act1) {
+    TailSolveArgs a;
+    a.c0 = t.c0;
+    a.w = t.w;
+    a.r = t.r;
+    a.nbd = t.nbd;
+    a.dim = c.dim;
+    a.nv = c.sym.nv;
+    a.cvo = c.host_sym.cv_off[t.J];
+    a.rows = c.sym.sn_rows + t.r0;
+    a.vcol_ptr = c.sym.vcol_ptr;
+    a.vpush_pos = c.sym.vpush_pos;
+    a.flags = c.tflags + t.flag_off + (which ? t.nbd : 0);
+    a.ticket = c.tflags + t.flag_off + 2 * t.nbd + which;
+    a.done = c.bwd_done + t.J;
+    a.act0 = act0;
+    a.act1 = act1;
+    return a;
+}
+
+template <typename T>
+void tail_forward_t(Ctx& c, T* x, int act0, int act1) {
+    for (const TailNode& t : c.tail) {
+        const int blocks = t.nbd + (t.r - t.w + TB - 1) / TB;
+        tail_fwd<T><<<blocks, 256, 0, c.stream>>>(tail_args(c, t, 0, act0, act1), (const T*)c.lval + t.loff,
+                                                  (const T*)c.tinv + t.inv_off, x, (T*)c.vin);
+        c.launches++;
+    }
+}
+
+template <typename T>
+void tail_backward_t(Ctx& c, T* x, int act0, int act1) {
+    for (auto it = c.tail.rbegin(); it != c.tail.rend(); ++it) {
+        const TailNode& t = *it;
+        tail_bwd<T><<<t.nbd, 256, 0, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
+                                                 (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x);
+        c.launches++;
+    }
+}
+
+}  // namespace
+
+void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total) {
+    const Symbolic& S = c.host_sym;
+    c.tail.clear();
+    int64_t io = 0, fo = 0;
+    for (int32_t k = S.n_main; k < S.nsuper; ++k) {
+        const int32_t J = S.order[k];
+        TailNode t;
+        t.J = J;
+        t.c0 = S.sn_col[J];
+        t.w = S.sn_col[J + 1] - S.sn_col[J];
+        t.r0 = S.sn_rptr[J];
+        t.r = (int)(S.sn_rptr[J + 1] - S.sn_rptr[J]);
+        t.loff = S.sn_loff[J];
+        t.parent = S.sn_parent[J];
+        t.nbd = (t.w + TB - 1) / TB;
+        t.inv_off = io;
+        t.flag_off = fo;
+        io += (int64_t)t.nbd * TB * TB;
+        fo += 2 * t.nbd + 2;
+        c.tail.push_back(t);
+    }
+    c.tflag_total = fo;
+    *inv_total = io;
+    *flag_total = fo;
+}
+
+void k_tail_factor(Ctx& c) {
+    if (c.tail.empty()) return;
+    if (c.precision == CIPM_FULL) tail_factor_t<double>(c);
+    else tail_factor_t<float>(c);
+}
+
+void k_tail_forward(Ctx& c, void* x, int act0, int act1) {
+    if (c.tail.empty()) return;
+    if (c.precision == CIPM_FULL) tail_forward_t<double>(c, (double*)x, act0, act1);
+    else tail_forward_t<float>(c, (float*)x, act0, act1);
+}
+
+void k_tail_backward(Ctx& c, void* x, int act0, int act1) {
+    if (c.tail.empty()) return;
+    if (c.precision == CIPM_FULL) tail_backward_t<double>(c, (double*)x, act0, act1);
+    else tail_backward_t<float>(c, (float*)x, act0, act1);
+}
+
+}  // namespace cipm

@@ -27,12 +27,6 @@ namespace cipm {
 
 namespace {
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) {
     return __ldcg(p);
@@ -115,7 +109,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
         const int J = a.order[t];
         if (tid == 0) {
             const int need = a.sn_nchild[J];
-            while (ld_acquire(a.count + J) < need) __nanosleep(64);
+            wait_ge(a.count + J, need);
             s_runmax = __ldcg(a.maxd + J);
         }
         __syncthreads();
@@ -240,6 +234,15 @@ struct SolveArgs {
 };
 
 template <typename T>
+__device__ __forceinline__ T vgather(const T* vq, const int64_t* vcol_ptr, int col) {
+    T acc = (T)0;
+    for (int64_t e = vcol_ptr[col]; e < vcol_ptr[col + 1]; ++e) acc += __ldcg(vq + e);
+    return acc;
+}
+
+// forward sweep L y = b: warp per supernode, columns in registers (lane owns
+// columns lane and lane+32; non-tail supernodes are narrower than 64)
+template <typename T>
 __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -248,10 +251,7 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.nsuper) return;
         const int J = a.order[t];
-        if (lane == 0) {
-            const int need = a.sn_nchild[J];
-            while (ld_acquire(a.count + J) < need) __nanosleep(32);
-        }
+        if (lane == 0) wait_ge(a.count + J, a.sn_nchild[J]);
         __syncwarp();
         const int c0 = a.sn_col[J];
         const int w = a.sn_col[J + 1] - c0;
@@ -263,47 +263,29 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xJ = x + (int64_t)q * a.dim + c0;
             T* vq = vin + (int64_t)q * a.nv;
-            if (w <= 32) {
-                T xr = (T)0;
-                if (lane < w) {
-                    T acc = (T)0;
-                    for (int64_t e = a.vcol_ptr[c0 + lane]; e < a.vcol_ptr[c0 + lane + 1]; ++e) acc += __ldcg(vq + e);
-                    xr = xJ[lane] - acc;
-                }
-                for (int j = 0; j < w; ++j) {
-                    const T xj = __shfl_sync(0xffffffffu, xr, j);
-                    if (lane > j && lane < w) xr -= L[(int64_t)j * r + lane] * xj;
-                }
-                if (lane < w) xJ[lane] = xr;
-                for (int i0 = w; i0 < r; i0 += 32) {
-                    const int i = i0 + lane;
-                    T acc = (T)0;
-                    for (int k = 0; k < w; ++k) {
-                        const T xk = __shfl_sync(0xffffffffu, xr, k);
-                        if (i < r) acc += L[(int64_t)k * r + i] * xk;
-                    }
-                    if (i < r) vq[a.vpush_pos[cvo + i - w]] = acc;
-                }
-            } else {
-                for (int j = lane; j < w; j += 32) {
-                    T acc = (T)0;
-                    for (int64_t e = a.vcol_ptr[c0 + j]; e < a.vcol_ptr[c0 + j + 1]; ++e) acc += __ldcg(vq + e);
-                    xJ[j] -= acc;
-                }
-                __syncwarp();
-                for (int j = 0; j < w; ++j) {
-                    const T xj = xJ[j];
-                    __syncwarp();
-                    for (int i = j + 1 + lane; i < w; i += 32) xJ[i] -= L[(int64_t)j * r + i] * xj;
-                    __syncwarp();
-                }
-                for (int i = w + lane; i < r; i += 32) {
-                    T acc = (T)0;
-                    for (int k = 0; k < w; ++k) acc += L[(int64_t)k * r + i] * xJ[k];
-                    vq[a.vpush_pos[cvo + i - w]] = acc;
-                }
+            T x0 = (T)0, x1 = (T)0;
+            if (lane < w) x0 = xJ[lane] - vgather(vq, a.vcol_ptr, c0 + lane);
+            if (lane + 32 < w) x1 = xJ[lane + 32] - vgather(vq, a.vcol_ptr, c0 + lane + 32);
+#pragma unroll 4
+            for (int j = 0; j < w; ++j) {
+                const T l0 = (lane > j && lane < w) ? L[(int64_t)j * r + lane] : (T)0;
+                const T l1 = (lane + 32 > j && lane + 32 < w) ? L[(int64_t)j * r + lane + 32] : (T)0;
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+                x0 -= l0 * xj;
+                x1 -= l1 * xj;
             }
-            __syncwarp();
+            if (lane < w) xJ[lane] = x0;
+            if (lane + 32 < w) xJ[lane + 32] = x1;
+            for (int i0 = w; i0 < r; i0 += 32) {
+                const int i = i0 + lane;
+                T acc = (T)0;
+#pragma unroll 4
+                for (int k = 0; k < w; ++k) {
+                    const T xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+                    if (i < r) acc += L[(int64_t)k * r + i] * xk;
+                }
+                if (i < r) vq[a.vpush_pos[cvo + i - w]] = acc;
+            }
         }
         __threadfence();
         __syncwarp();
@@ -314,6 +296,7 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
     }
 }
 
+// backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
 template <typename T>
 __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __restrict__ lval,
                                                        const T* __restrict__ dvec, T* x) {
@@ -325,8 +308,7 @@ __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __r
         if (t >= a.nsuper) return;
         const int J = a.order[a.nsuper - 1 - t];
         const int P = a.sn_parent[J];
-        if (lane == 0 && P >= 0)
-            while (ld_acquire(a.count + P) == 0) __nanosleep(32);
+        if (lane == 0 && P >= 0) wait_ge(a.count + P, 1);
         __syncwarp();
         const int c0 = a.sn_col[J];
         const int w = a.sn_col[J + 1] - c0;
@@ -334,45 +316,32 @@ __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __r
         const int r = (int)(a.sn_rptr[J + 1] - r0);
         const int32_t* rowsJ = a.sn_rows + r0;
         const T* L = lval + a.sn_loff[J];
+        const T* L0 = L + (int64_t)lane * r;
+        const T* L1 = L + (int64_t)(lane + 32) * r;
+        const bool o0 = lane < w, o1 = lane + 32 < w;
         for (int q = 0; q < 2; ++q) {
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xv = x + (int64_t)q * a.dim;
             T* xJ = xv + c0;
-            if (w <= 32) {
-                T xr = lane < w ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
-                for (int i = w; i < r; ++i) {
-                    const T xi = __ldcg(xv + rowsJ[i]);
-                    if (lane < w) xr -= L[(int64_t)lane * r + i] * xi;
-                }
-                for (int j = w - 1; j >= 0; --j) {
-                    const T xj = __shfl_sync(0xffffffffu, xr, j);
-                    if (lane < j) xr -= L[(int64_t)lane * r + j] * xj;
-                }
-                if (lane < w) xJ[lane] = xr;
-            } else {
-                for (int j = lane; j < w; j += 32) xJ[j] = xJ[j] / dvec[c0 + j];
-                __syncwarp();
-                for (int j = 0; j < w; ++j) {
-                    const T* Lj = L + (int64_t)j * r;
-                    T acc = (T)0;
-                    for (int i = w + lane; i < r; i += 32) acc += Lj[i] * __ldcg(xv + rowsJ[i]);
-                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-                    if (lane == 0) xJ[j] -= acc;
-                }
-                __syncwarp();
-                for (int j = w - 1; j >= 0; --j) {
-                    const T* Lj = L + (int64_t)j * r;
-                    T acc = (T)0;
-                    for (int i = j + 1 + lane; i < w; i += 32) acc += Lj[i] * xJ[i];
-                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-                    if (lane == 0) xJ[j] -= acc;
-                    __syncwarp();
-                }
+            T x0 = o0 ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
+            T x1 = o1 ? xJ[lane + 32] / dvec[c0 + lane + 32] : (T)0;
+#pragma unroll 4
+            for (int i = w; i < r; ++i) {
+                const T xi = __ldcg(xv + rowsJ[i]);
+                if (o0) x0 -= L0[i] * xi;
+                if (o1) x1 -= L1[i] * xi;
             }
+            for (int j = w - 1; j >= 0; --j) {
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+                if (lane < j) x0 -= L0[j] * xj;
+                if (lane + 32 < j) x1 -= L1[j] * xj;
+            }
+            if (o0) xJ[lane] = x0;
+            if (o1) xJ[lane + 32] = x1;
         }
         __threadfence();
         __syncwarp();
-        if (lane == 0) atomicExch(a.count + J, 1);
+        if (lane == 0) st_release(a.count + J, 1);
     }
 }
 
@@ -402,7 +371,7 @@ __global__ void scatter_add_perm(double* __restrict__ x, const T* __restrict__ t
 
 SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1) {
     SolveArgs a;
-    a.nsuper = c.sym.nsuper;
+    a.nsuper = c.host_sym.n_main;
     a.dim = c.dim;
     a.nv = c.sym.nv;
     a.order = c.sym.order;
@@ -441,7 +410,7 @@ void build_base_t(Ctx& c) {
 template <typename T>
 int factor_t(Ctx& c) {
     FactorArgs a;
-    a.nsuper = c.sym.nsuper;
+    a.nsuper = c.host_sym.n_main;
     a.order = c.sym.order;
     a.sn_col = c.sym.sn_col;
     a.sn_rptr = c.sym.sn_rptr;
@@ -470,12 +439,15 @@ int factor_t(Ctx& c) {
         e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
-    factor_kernel<T><<<c.factor_blocks, 256, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+    if (a.nsuper > 0) {
+        factor_kernel<T><<<c.factor_blocks, 256, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+        c.launches++;
+    }
+    k_tail_factor(c);
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_factor.emplace_back(e0, e0 + 1);
     }
-    c.launches++;
     return CIPM_OK;
 }
 
@@ -486,15 +458,18 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
+    if (c.tflag_total) cudaMemsetAsync(c.tflags, 0, sizeof(int32_t) * c.tflag_total, c.stream);
     int e0 = 0;
     if (c.profile) {
         e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
     SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
-    forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    if (f.nsuper > 0) forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    k_tail_forward(c, t, act0, act1);
+    k_tail_backward(c, t, act0, act1);
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
-    backward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+    if (b.nsuper > 0) backward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_solve.emplace_back(e0, e0 + 1);
@@ -542,7 +517,7 @@ static int sm_count() {
 int factor_grid(Ctx& c) {
     // dynamic shared memory: the largest panel below 96 KiB; bigger panels run in place
     const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
-    int64_t cap = c.host_sym.max_panel * es;
+    int64_t cap = c.host_sym.max_panel_main * es;
     if (cap > 96 * 1024) cap = 96 * 1024;
     if (cap < 1024) cap = 1024;
     c.factor_smem = (int)cap;
@@ -556,7 +531,7 @@ int factor_grid(Ctx& c) {
     }
     if (per < 1) per = 1;
     int64_t g = (int64_t)sm_count() * per;
-    if (g > c.sym.nsuper) g = c.sym.nsuper;
+    if (g > c.host_sym.n_main) g = c.host_sym.n_main;
     return (int)(g < 1 ? 1 : g);
 }
 
@@ -568,7 +543,7 @@ int solve_grid(Ctx& c) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<float>, 256, 0);
     if (per < 1) per = 1;
     int64_t g = (int64_t)sm_count() * per;
-    int64_t need = (c.sym.nsuper + 7) / 8;
+    int64_t need = (c.host_sym.n_main + 7) / 8;
     if (g > need) g = need;
     return (int)(g < 1 ? 1 : g);
 }

@@ -505,10 +505,31 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         if (S.sn_parent[J] != -1) S.level[S.sn_parent[J]] = std::max(S.level[S.sn_parent[J]], S.level[J] + 1);
     S.height = 0;
     for (int32_t J = 0; J < ns; ++J) S.height = std::max(S.height, S.level[J] + 1);
+    // dense tail: supernodes whose panel or contribution block is large enough
+    // for the multi-CTA tensor-core path (dense.cu), plus all their ancestors.
+    // The complement is closed under descendants, so the persistent kernels
+    // finish it before the tail starts.
+    S.is_tail.assign(ns, 0);
+    for (int32_t J = 0; J < ns; ++J) {
+        int64_t w = S.sn_col[J + 1] - S.sn_col[J];
+        int64_t o = (S.sn_rptr[J + 1] - S.sn_rptr[J]) - w;
+        if (w >= opt.tail_width || o >= opt.tail_offrows) S.is_tail[J] = 1;
+    }
+    for (int32_t J = 0; J < ns; ++J)       // parents have larger indices (postorder)
+        if (S.is_tail[J] && S.sn_parent[J] >= 0) S.is_tail[S.sn_parent[J]] = 1;
     S.order.resize(ns);
     std::iota(S.order.begin(), S.order.end(), 0);
-    std::stable_sort(S.order.begin(), S.order.end(),
-                     [&](int32_t a, int32_t b) { return S.level[a] < S.level[b]; });
+    std::stable_sort(S.order.begin(), S.order.end(), [&](int32_t a, int32_t b) {
+        if (S.is_tail[a] != S.is_tail[b]) return S.is_tail[a] < S.is_tail[b];
+        return S.level[a] < S.level[b];
+    });
+    S.n_main = 0;
+    for (int32_t J = 0; J < ns; ++J) S.n_main += S.is_tail[J] ? 0 : 1;
+    S.max_panel_main = 0;
+    for (int32_t J = 0; J < ns; ++J)
+        if (!S.is_tail[J])
+            S.max_panel_main = std::max<int64_t>(S.max_panel_main,
+                                                 (S.sn_col[J + 1] - S.sn_col[J]) * (S.sn_rptr[J + 1] - S.sn_rptr[J]));
 
     // scatter maps: K(i,j) (original indices) -> panel position
     auto pos = [&](int64_t i, int64_t j) -> int64_t {

@@ -21,6 +21,8 @@ struct SymbolicOptions {
     double relax_mid_frac = 0.3;
     int relax_big = 64;        // ... up to this width if zero fraction <= relax_big_frac
     double relax_big_frac = 0.05;
+    int tail_width = 64;       // supernodes at least this wide go to the dense tail path
+    int tail_offrows = 512;    // ... or with at least this many off-diagonal rows
 };
 
 struct Symbolic {
@@ -57,9 +59,12 @@ struct Symbolic {
     std::vector<int64_t> vpush_pos;        // cv_off[nsuper]
     std::vector<int64_t> vcol_ptr;         // dim+1
     // schedule
-    std::vector<int32_t> order;            // topological order (leaves first, by level)
+    std::vector<int32_t> order;            // topological order: non-tail by level, then tail by level
     std::vector<int32_t> level;            // per supernode, 0 = leaf
     int32_t height = 0;
+    std::vector<int8_t> is_tail;           // dense tail supernode (multi-CTA path, dense.cu)
+    int32_t n_main = 0;                    // order[0 .. n_main) are the non-tail supernodes
+    int64_t max_panel_main = 0;            // largest non-tail panel (shared-memory sizing)
     // scatter maps into the panel value array (int64 positions)
     std::vector<int64_t> map_p;            // P CSR nnz; -1 for strictly-lower entries
     std::vector<int64_t> map_a;            // A CSR nnz (entry (n+r, j) of K stored at L(col j? ...))

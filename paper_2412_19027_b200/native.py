@@ -93,6 +93,14 @@ _SIGS = {
     "cipm_profile": ([c_void_p, ctypes.c_int], ctypes.c_int),
     "cipm_kernel_stats": ([c_void_p, P_DBL], ctypes.c_int),
     "cipm_timer": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
+    "cipm_batch_create": ([ctypes.POINTER(ProblemDesc), ctypes.c_int, ctypes.POINTER(Settings), c_dbl, c_dbl,
+                           ctypes.c_int, ctypes.POINTER(c_void_p)], ctypes.c_int),
+    "cipm_batch_info": ([c_void_p, P_I64], ctypes.c_int),
+    "cipm_batch_set_values": ([c_void_p, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_batch_solve": ([c_void_p, P_DBL], ctypes.c_int),
+    "cipm_batch_results": ([c_void_p, ctypes.POINTER(ctypes.c_int32), P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_batch_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),
+    "cipm_batch_destroy": ([c_void_p], None),
 }
 
 _lib = None

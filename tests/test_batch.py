@@ -1,0 +1,109 @@
+"""Batched same-pattern instances (C5b): host equilibration (CPU) and the
+one-CTA-per-instance device IPM against the oracle (GPU)."""
+import numpy as np
+import pytest
+
+from oracle import OracleSolver
+from paper_2412_19027_b200 import generators as G
+from paper_2412_19027_b200 import model
+from paper_2412_19027_b200.batch import equilibrate_batch
+from paper_2412_19027_b200.settings import SolverSettings
+
+
+def _mpc(k):
+    return [G.gen_mpc(seed=s) for s in range(k)]
+
+
+def test_equilibrate_batch_bitwise_matches_per_instance():
+    probs = _mpc(6)
+    reo = [model.reorder_cones(p)[0] for p in probs]
+    P, A = reo[0].P, reo[0].A
+    pv = np.stack([r.P.values for r in reo])
+    av = np.stack([r.A.values for r in reo])
+    q = np.stack([r.q for r in reo])
+    b = np.stack([r.b for r in reo])
+    pv_s, av_s, q_s, b_s, d_row, d_col, c_obj = equilibrate_batch(P, A, pv, av, q, b)
+    for k, r in enumerate(reo):
+        s, e = model.equilibrate(r)
+        np.testing.assert_array_equal(pv_s[k], s.P.values)
+        np.testing.assert_array_equal(av_s[k], s.A.values)
+        np.testing.assert_array_equal(q_s[k], s.q)
+        np.testing.assert_array_equal(b_s[k], s.b)
+        np.testing.assert_array_equal(d_row[k], e.d_row)
+        np.testing.assert_array_equal(d_col[k], e.d_col)
+        assert c_obj[k] == e.c_obj
+
+
+def test_mpc_instances_share_one_pattern():
+    probs = _mpc(4)
+    for p in probs[1:]:
+        np.testing.assert_array_equal(p.A.rowptr, probs[0].A.rowptr)
+        np.testing.assert_array_equal(p.A.colidx, probs[0].A.colidx)
+    assert probs[0].n == 118 and probs[0].m == 324
+
+
+def _check(res, ref):
+    assert res.status == ref.status, (res.status, ref.status)
+    assert abs(res.iterations - ref.iterations) <= 1, (res.iterations, ref.iterations)
+    if ref.status in ("optimal", "almost_optimal"):
+        tol = 1e-6 * max(1.0, abs(ref.obj_primal))
+        assert abs(res.obj_primal - ref.obj_primal) <= tol
+        assert abs(res.obj_dual - ref.obj_dual) <= 1e-6 * max(1.0, abs(ref.obj_dual))
+        np.testing.assert_allclose(res.x, ref.x, atol=1e-5 * max(1.0, np.max(np.abs(ref.x))))
+
+
+@pytest.mark.gpu
+def test_gpu_batch_mpc_matches_oracle(gpu):
+    from paper_2412_19027_b200.batch import BatchSolver
+    probs = _mpc(24)
+    cfg = SolverSettings(eps_feas=1e-8)
+    bs = BatchSolver(probs, cfg)
+    out = bs.solve()
+    bs.close()
+    for p, r in zip(probs, out):
+        _check(r, OracleSolver(p, cfg).solve())
+
+
+@pytest.mark.gpu
+def test_gpu_batch_lp_family_and_update(gpu):
+    from paper_2412_19027_b200.batch import BatchSolver
+    base = G.gen_lp(40, 80, seed=3)
+    rng = np.random.default_rng(0)
+    probs = []
+    for k in range(8):
+        p = base.copy()
+        p.q = base.q * (1.0 + 0.1 * rng.standard_normal(base.n))
+        probs.append(p)
+    cfg = SolverSettings(eps_feas=1e-8)
+    bs = BatchSolver(probs, cfg)
+    out = bs.solve()
+    for p, r in zip(probs, out):
+        _check(r, OracleSolver(p, cfg).solve())
+    # parametric: new q for every instance, same device pattern
+    q2 = np.stack([p.q * 1.05 for p in probs])
+    bs.update_data(q=q2)
+    out2 = bs.solve()
+    bs.close()
+    for k, r in enumerate(out2):
+        p = probs[k].copy()
+        p.q = q2[k]
+        _check(r, OracleSolver(p, cfg).solve())
+
+
+@pytest.mark.gpu
+def test_gpu_batch_infeasible_instances(gpu):
+    from golden_io import load_instance, problem_from_doc
+    from paper_2412_19027_b200.batch import BatchSolver
+    for name in ("primal_infeasible_lp", "dual_infeasible_lp"):
+        doc = load_instance(name)
+        p = problem_from_doc(doc)
+        s = doc["settings"]
+        cfg = SolverSettings(eps_feas=s["eps_feas"], max_iter=s["max_iter"])
+        bs = BatchSolver([p, p.copy()], cfg)
+        out = bs.solve()
+        bs.close()
+        for r in out:
+            assert r.status == doc["result"]["status"]
+            assert abs(r.iterations - doc["result"]["iterations"]) <= 1
+            if doc["result"]["certificate"] is not None:
+                np.testing.assert_allclose(r.certificate, doc["result"]["certificate"], atol=1e-6)
