@@ -815,6 +815,23 @@ int cipm_timer(cipm_ctx* h, int op, double* ms) {
     return CIPM_OK;
 }
 
+int cipm_trace(cipm_ctx* h, int enable, int64_t* out) {
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    const int64_t cnt = 6 * (int64_t)c.sym.nsuper;
+    if (enable) {
+        if (!c.trace) {
+            CIPM_CUDA(cudaMalloc(&c.trace, sizeof(int64_t) * cnt));
+            c.allocations.push_back(c.trace);
+        }
+        CIPM_CUDA(cudaMemset(c.trace, 0, sizeof(int64_t) * cnt));
+        return CIPM_OK;
+    }
+    if (c.trace && out) CIPM_CUDA(cudaMemcpy(out, c.trace, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+    c.trace = nullptr;   // stays allocated until destroy
+    return CIPM_OK;
+}
+
 int cipm_kernel_times(cipm_ctx* h, double* factor_ms, double* solve_ms) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));

@@ -122,6 +122,8 @@ struct Ctx {
     void* inbox = nullptr;           // factor contribution inbox (T)
     void* vin = nullptr;             // solve contribution inbox, 2 x nv (T)
     int factor_blocks = 0, solve_blocks = 0, factor_smem = 0;
+    int64_t factor_slice = 0;        // per-warp panel slice (elements) of the factor kernel
+    int factor_cta_smem = 0, factor_cta_blocks = 0;   // mid-tier CTA kernel
     // dense tail (dense.cu)
     std::vector<TailNode> tail;
     void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)
@@ -155,6 +157,8 @@ struct Ctx {
     int64_t solve_rhs = 0;            // right-hand sides processed by the profiled solve launches
     cudaEvent_t t_start = nullptr, t_stop = nullptr;
     float factor_ms = 0.f, solve_ms = 0.f;
+
+    int64_t* trace = nullptr;        // cipm_trace: [forward | factor] x nsuper x 3 timestamps
 
     std::vector<void*> allocations;
 };

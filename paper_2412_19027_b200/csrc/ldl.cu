@@ -18,6 +18,8 @@
 // earlier pivots; δd = eps² makes the term negligible — DESIGN.md).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -26,6 +28,12 @@
 namespace cipm {
 
 namespace {
+
+__device__ __forceinline__ int64_t gtimer() {
+    int64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) {
@@ -67,7 +75,8 @@ __global__ void add_static_reg(T* base, const int64_t* map_diag, int64_t n, int6
 // ---------------------------------------------------------------------------
 
 struct FactorArgs {
-    int32_t nsuper;
+    int32_t nsuper;      // tickets t in [t_begin, nsuper) of `order`
+    int32_t t_begin;
     const int32_t* order;
     const int32_t* sn_col;
     const int64_t* sn_rptr;
@@ -86,31 +95,184 @@ struct FactorArgs {
     int* err;
     double delta_s, delta_d;
     int64_t smem_cap;    // panel elements that fit the dynamic shared memory
+    int64_t* trace;      // optional per-task timeline (cipm_trace)
 };
 
 __device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
 }
 
+// Warp-cooperative segmented gather: entries [lo, hi) sorted so that equal
+// targets are contiguous; P[tgt] -= sum of their values (fixed order: a warp
+// Hillis-Steele scan per 32-entry chunk, carries across chunks).
 template <typename T>
-__global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
-                                                     T* __restrict__ inbox) {
+__device__ __forceinline__ void warp_gather_sub(T* P, const int32_t* __restrict__ tgt, const T* vals, int64_t lo,
+                                                int64_t hi) {
+    const int lane = threadIdx.x & 31;
+    int carry_t = -1;
+    T carry = (T)0;
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t e = base + lane;
+        const bool valid = e < hi;
+        const int tg = valid ? tgt[e] : -(lane + 2);
+        T v = valid ? __ldcg(vals + e) : (T)0;
+        const int t0 = __shfl_sync(0xffffffffu, tg, 0);
+        if (carry_t >= 0 && t0 != carry_t) {
+            if (lane == 0) P[carry_t] -= carry;
+            carry_t = -1;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int tp = __shfl_up_sync(0xffffffffu, tg, off);
+            const T vp = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off && tp == tg) v += vp;
+        }
+        const int tn = __shfl_down_sync(0xffffffffu, tg, 1);
+        const bool is_end = lane == 31 || tn != tg;
+        const bool more = base + 32 < hi;
+        T tot = v;
+        if (valid && is_end && tg == carry_t) tot += carry;
+        if (valid && is_end && !(lane == 31 && more)) P[tg] -= tot;
+        const int t31 = __shfl_sync(0xffffffffu, tg, 31);
+        const T v31 = __shfl_sync(0xffffffffu, tot, 31);
+        if (more) {
+            carry_t = t31;
+            carry = v31;
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+}
+
+constexpr int FW = 8;   // warps per factor CTA
+
+// Task J (one warp): wait until its children are done; stage its panel in the
+// warp's shared-memory slice (in place in HBM when it does not fit); gather its
+// inbox (every contribution entry of every descendant that lands in J, sorted
+// by target, fixed-order segmented sums); factor the dense panel; write L and
+// D; then compute its packed contribution block C_J = L_off D L_off' and
+// scatter it into the ancestors' inboxes.  No floating-point atomics.
+template <typename T>
+__global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+                                                         T* __restrict__ inbox) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ T sD[FW][64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* sp = reinterpret_cast<T*>(smem_raw) + (int64_t)wid * a.smem_cap;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = a.t_begin + atomicAdd(a.ticket, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.nsuper) return;
+        const int J = a.order[t];
+        double runmax = 0.0;
+        if (lane == 0) {
+            if (a.trace) a.trace[3 * t] = gtimer();
+            wait_ge(a.count + J, a.sn_nchild[J]);
+            runmax = __ldcg(a.maxd + J);
+            if (a.trace) a.trace[3 * t + 1] = gtimer();
+        }
+        runmax = __shfl_sync(0xffffffffu, runmax, 0);
+        const int c0 = a.sn_col[J];
+        const int w = a.sn_col[J + 1] - c0;
+        const int64_t r0 = a.sn_rptr[J];
+        const int r = (int)(a.sn_rptr[J + 1] - r0);
+        const int o = r - w;
+        T* L = lval + a.sn_loff[J];
+        const int psize = r * w;
+        const bool in_smem = psize <= a.smem_cap;
+        T* P = in_smem ? sp : L;
+        if (in_smem)
+            for (int i = lane; i < psize; i += 32) sp[i] = L[i];
+        __syncwarp();
+
+        // 1. gather the inbox of all r rows (one contiguous, target-sorted range)
+        warp_gather_sub(P, a.inbox_tgt, inbox, a.irow_ptr[r0], a.irow_ptr[r0 + r]);
+
+        // 2. dense LDL' of the panel (right-looking, lanes over rows)
+        for (int j = 0; j < w; ++j) {
+            T* Pj = P + j * r;
+            double d = (double)Pj[j];
+            const double bound = a.delta_s + a.delta_d * runmax;
+            const bool bump = fabs(d) < bound;
+            if (bump) d = a.sign[c0 + j] > 0 ? bound : -bound;
+            const T dt = (T)d;
+            runmax = fmax(runmax, fabs(d));
+            __syncwarp();
+            if (lane == 0) {
+                if (bump) atomicAdd(a.bumps, 1);
+                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+                dvec[c0 + j] = dt;
+                sD[wid][j] = dt;
+                Pj[j] = (T)1;
+            }
+            for (int i = j + 1 + lane; i < r; i += 32) Pj[i] = Pj[i] / dt;
+            __syncwarp();
+            for (int c = j + 1; c < w; ++c) {
+                const T pjc = Pj[c];
+                T* Pc = P + c * r;
+                for (int i = c + lane; i < r; i += 32) Pc[i] -= Pj[i] * dt * pjc;
+            }
+            __syncwarp();
+        }
+
+        // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
+        if (in_smem)
+            for (int i = lane; i < psize; i += 32) L[i] = sp[i];
+        if (o > 0) {
+            const int64_t base = a.cb_off[J];
+            const T* Dj = sD[wid];
+            int64_t tb = 0;   // packed offset of column bb
+            for (int bb = 0; bb < o; ++bb) {
+                const T* Pb = P + w + bb;
+                for (int aa = bb + lane; aa < o; aa += 32) {
+                    T acc = (T)0;
+                    for (int k = 0; k < w; ++k) acc += P[k * r + w + aa] * Dj[k] * Pb[k * r];
+                    inbox[a.push_pos[base + tb + (aa - bb)]] = acc;
+                }
+                tb += o - bb;
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            const int Pn = a.sn_parent[J];
+            if (Pn >= 0) {
+                atomic_max_pos(a.maxd + Pn, runmax);
+                __threadfence();
+                atomicAdd(a.count + Pn, 1);
+            }
+            if (a.trace) a.trace[3 * t + 2] = gtimer();
+        }
+    }
+}
+
+
+// Mid tier (one CTA per supernode): the same task for panels too large for one
+// warp — the inbox gather is split by rows over the CTA's warps, the dense
+// panel LDL' uses all threads, the contribution block is computed by all
+// threads.  Launched after the warp tier, before the dense tail.
+template <typename T>
+__global__ void __launch_bounds__(256) factor_cta_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+                                                         T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sp = reinterpret_cast<T*>(smem_raw);
     __shared__ int s_task;
     __shared__ double s_piv;
     __shared__ double s_runmax;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ T sD[64];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
     for (;;) {
-        if (tid == 0) s_task = atomicAdd(a.ticket, 1);
+        if (tid == 0) s_task = a.t_begin + atomicAdd(a.ticket, 1);
         __syncthreads();
         const int t = s_task;
         if (t >= a.nsuper) return;
         const int J = a.order[t];
         if (tid == 0) {
-            const int need = a.sn_nchild[J];
-            wait_ge(a.count + J, need);
+            if (a.trace) a.trace[3 * t] = gtimer();
+            wait_ge(a.count + J, a.sn_nchild[J]);
             s_runmax = __ldcg(a.maxd + J);
+            if (a.trace) a.trace[3 * t + 1] = gtimer();
         }
         __syncthreads();
         const int c0 = a.sn_col[J];
@@ -125,27 +287,13 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
         if (in_smem)
             for (int64_t i = tid; i < psize; i += nt) sp[i] = L[i];
         __syncthreads();
-
-        // 1. gather the inbox: thread per panel row, register runs per target column
-        for (int tr = tid; tr < r; tr += nt) {
-            const int64_t lo = a.irow_ptr[r0 + tr], hi = a.irow_ptr[r0 + tr + 1];
-            int cur = -1;
-            T acc = (T)0;
-            for (int64_t e = lo; e < hi; ++e) {
-                const int tg = a.inbox_tgt[e];
-                const T v = __ldcg(inbox + e);
-                if (tg != cur) {
-                    if (cur >= 0) P[cur] -= acc;
-                    cur = tg;
-                    acc = v;
-                } else {
-                    acc += v;
-                }
-            }
-            if (cur >= 0) P[cur] -= acc;
+        // 1. inbox gather, rows split over the warps (targets are unique per row)
+        {
+            const int rs = (int)((int64_t)r * wid / nw), re = (int)((int64_t)r * (wid + 1) / nw);
+            if (re > rs) warp_gather_sub(P, a.inbox_tgt, inbox, a.irow_ptr[r0 + rs], a.irow_ptr[r0 + re]);
+            (void)lane;
         }
         __syncthreads();
-
         // 2. dense LDL' of the panel (right-looking inside the panel)
         for (int j = 0; j < w; ++j) {
             if (tid == 0) {
@@ -158,6 +306,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
                 const T dt = (T)d;
                 if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
                 dvec[c0 + j] = dt;
+                sD[j] = dt;
                 P[(int64_t)j * r + j] = (T)1;
                 s_piv = (double)dt;
                 s_runmax = fmax(s_runmax, fabs(d));
@@ -180,19 +329,17 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
             }
             __syncthreads();
         }
-
-        // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
+        // 3. write back, push C_J = L_off D L_off'
         if (in_smem)
             for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
         if (o > 0) {
-            const T* Dj = dvec + c0;
             const int64_t base = a.cb_off[J];
             const int64_t tot = (int64_t)o * o;
             for (int64_t idx = tid; idx < tot; idx += nt) {
                 const int aa = (int)(idx % o), bb = (int)(idx / o);
                 if (aa < bb) continue;
                 T acc = (T)0;
-                for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * Dj[k] * P[(int64_t)k * r + w + bb];
+                for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * sD[k] * P[(int64_t)k * r + w + bb];
                 const int64_t tpk = (int64_t)bb * o - (int64_t)bb * (bb - 1) / 2 + (aa - bb);
                 inbox[a.push_pos[base + tpk]] = acc;
             }
@@ -206,6 +353,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorArgs a, T* __restrict
                 __threadfence();
                 atomicAdd(a.count + Pn, 1);
             }
+            if (a.trace) a.trace[3 * t + 2] = gtimer();
         }
     }
 }
@@ -231,19 +379,57 @@ struct SolveArgs {
     int32_t* count;      // forward: children done; backward: done flags
     int32_t* ticket;
     int act0, act1;      // active right-hand sides
+    int64_t* trace;      // optional per-task timeline (cipm_trace): ticket / ready / done (ns)
 };
 
+
+// warp-cooperative sums of the vector inbox of columns c0 .. c0+w-1 (one
+// contiguous range grouped by column): colsum[j] = sum of column c0+j's entries
 template <typename T>
-__device__ __forceinline__ T vgather(const T* vq, const int64_t* vcol_ptr, int col) {
-    T acc = (T)0;
-    for (int64_t e = vcol_ptr[col]; e < vcol_ptr[col + 1]; ++e) acc += __ldcg(vq + e);
-    return acc;
+__device__ __forceinline__ void vgather_warp(const T* vq, const int64_t* __restrict__ gptr, int c0, int w,
+                                             T* colsum, int64_t* vcol_ptr) {
+    const int lane = threadIdx.x & 31;
+    for (int j = lane; j < w; j += 32) colsum[j] = (T)0;
+    for (int j = lane; j <= w; j += 32) vcol_ptr[j] = gptr[c0 + j];   // window, re-based at c0
+    __syncwarp();
+    c0 = 0;
+    const int64_t lo = vcol_ptr[0], hi = vcol_ptr[w];
+    if (hi > lo) {
+        // entry -> column: binary search in the (small) column pointer window
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t e = base + lane;
+            const bool valid = e < hi;
+            int col = -(lane + 2);
+            T v = (T)0;
+            if (valid) {
+                int lo_c = 0, hi_c = w - 1;
+                while (lo_c < hi_c) {
+                    const int mid = (lo_c + hi_c + 1) >> 1;
+                    if (vcol_ptr[c0 + mid] <= e) lo_c = mid; else hi_c = mid - 1;
+                }
+                col = lo_c;
+                v = __ldcg(vq + e);
+            }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int cp = __shfl_up_sync(0xffffffffu, col, off);
+                const T vp = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off && cp == col) v += vp;
+            }
+            const int cn = __shfl_down_sync(0xffffffffu, col, 1);
+            if (valid && (lane == 31 || cn != col)) colsum[col] += v;
+            __syncwarp();
+        }
+    }
+    __syncwarp();
 }
 
 // forward sweep L y = b: warp per supernode, columns in registers (lane owns
 // columns lane and lane+32; non-tail supernodes are narrower than 64)
 template <typename T>
 __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
+    __shared__ T colsum[8][64];
+    __shared__ int64_t vwin[8][65];
     const int lane = threadIdx.x & 31;
     for (;;) {
         int t = 0;
@@ -251,8 +437,10 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.nsuper) return;
         const int J = a.order[t];
+        if (a.trace && lane == 0) a.trace[3 * t] = gtimer();
         if (lane == 0) wait_ge(a.count + J, a.sn_nchild[J]);
         __syncwarp();
+        if (a.trace && lane == 0) a.trace[3 * t + 1] = gtimer();
         const int c0 = a.sn_col[J];
         const int w = a.sn_col[J + 1] - c0;
         const int64_t r0 = a.sn_rptr[J];
@@ -263,9 +451,11 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xJ = x + (int64_t)q * a.dim + c0;
             T* vq = vin + (int64_t)q * a.nv;
+            T* cs = colsum[threadIdx.x >> 5];
+            vgather_warp(vq, a.vcol_ptr, c0, w, cs, vwin[threadIdx.x >> 5]);
             T x0 = (T)0, x1 = (T)0;
-            if (lane < w) x0 = xJ[lane] - vgather(vq, a.vcol_ptr, c0 + lane);
-            if (lane + 32 < w) x1 = xJ[lane + 32] - vgather(vq, a.vcol_ptr, c0 + lane + 32);
+            if (lane < w) x0 = xJ[lane] - cs[lane];
+            if (lane + 32 < w) x1 = xJ[lane + 32] - cs[lane + 32];
 #pragma unroll 4
             for (int j = 0; j < w; ++j) {
                 const T l0 = (lane > j && lane < w) ? L[(int64_t)j * r + lane] : (T)0;
@@ -292,6 +482,7 @@ __global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __re
         if (lane == 0) {
             const int P = a.sn_parent[J];
             if (P >= 0) atomicAdd(a.count + P, 1);
+            if (a.trace) a.trace[3 * t + 2] = gtimer();
         }
     }
 }
@@ -388,6 +579,7 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.ticket = ticket;
     a.act0 = act0;
     a.act1 = act1;
+    a.trace = nullptr;
     return a;
 }
 
@@ -429,7 +621,8 @@ int factor_t(Ctx& c) {
     a.err = c.err;
     a.delta_s = c.delta_s;
     a.delta_d = c.delta_d;
-    a.smem_cap = c.factor_smem / (int64_t)sizeof(T);
+    a.smem_cap = c.factor_slice;
+    a.trace = c.trace ? c.trace + 3 * (int64_t)c.sym.nsuper : nullptr;
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.sn_maxd, 0, sizeof(double) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
@@ -439,8 +632,23 @@ int factor_t(Ctx& c) {
         e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
-    if (a.nsuper > 0) {
-        factor_kernel<T><<<c.factor_blocks, 256, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+    const int n_warp = c.host_sym.n_warp, n_main = c.host_sym.n_main;
+    if (n_warp > 0) {
+        a.t_begin = 0;
+        a.nsuper = n_warp;
+        a.ticket = c.tickets;
+        a.smem_cap = c.factor_slice;
+        factor_kernel<T><<<c.factor_blocks, FW * 32, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec,
+                                                                                (T*)c.inbox);
+        c.launches++;
+    }
+    if (n_main > n_warp) {
+        a.t_begin = n_warp;
+        a.nsuper = n_main;
+        a.ticket = c.tickets + 3;
+        a.smem_cap = c.factor_cta_smem / (int64_t)sizeof(T);
+        factor_cta_kernel<T><<<c.factor_cta_blocks, 256, c.factor_cta_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec,
+                                                                                       (T*)c.inbox);
         c.launches++;
     }
     k_tail_factor(c);
@@ -465,6 +673,7 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
     SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
+    f.trace = c.trace;
     if (f.nsuper > 0) forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     k_tail_forward(c, t, act0, act1);
     k_tail_backward(c, t, act0, act1);
@@ -515,23 +724,45 @@ static int sm_count() {
 }
 
 int factor_grid(Ctx& c) {
-    // dynamic shared memory: the largest panel below 96 KiB; bigger panels run in place
+    // per-warp shared-memory panel slice: the largest non-tail panel, capped at
+    // 6 KiB so four 8-warp CTAs fit per SM; bigger panels are factored in place
     const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
-    int64_t cap = c.host_sym.max_panel_main * es;
-    if (cap > 96 * 1024) cap = 96 * 1024;
-    if (cap < 1024) cap = 1024;
-    c.factor_smem = (int)cap;
+    int64_t slice = std::min<int64_t>(c.host_sym.max_panel_warp, 6144 / es);
+    if (slice < 64) slice = 64;
+    c.factor_slice = slice;
+    c.factor_smem = (int)(slice * es * FW);
     int per = 0;
     if (c.precision == CIPM_FULL) {
         cudaFuncSetAttribute(factor_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.factor_smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<double>, 256, c.factor_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<double>, FW * 32, c.factor_smem);
     } else {
         cudaFuncSetAttribute(factor_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, c.factor_smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<float>, 256, c.factor_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, factor_kernel<float>, FW * 32, c.factor_smem);
     }
     if (per < 1) per = 1;
     int64_t g = (int64_t)sm_count() * per;
-    if (g > c.host_sym.n_main) g = c.host_sym.n_main;
+    const int64_t need = (c.host_sym.n_warp + FW - 1) / FW;
+    if (g > need) g = need;
+    if (const char* e = getenv("CIPM_FACTOR_BLOCKS")) g = std::min<int64_t>(g, atoll(e));   // experiments
+    // mid tier: one CTA per supernode, panel in dynamic shared memory up to 96 KiB
+    {
+        int64_t cap = std::min<int64_t>(c.host_sym.max_panel_main * es, 96 * 1024);
+        if (cap < 1024) cap = 1024;
+        c.factor_cta_smem = (int)cap;
+        int pc = 0;
+        if (c.precision == CIPM_FULL) {
+            cudaFuncSetAttribute(factor_cta_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pc, factor_cta_kernel<double>, 256, (int)cap);
+        } else {
+            cudaFuncSetAttribute(factor_cta_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pc, factor_cta_kernel<float>, 256, (int)cap);
+        }
+        if (pc < 1) pc = 1;
+        int64_t gc = (int64_t)sm_count() * pc;
+        const int64_t nmid = c.host_sym.n_main - c.host_sym.n_warp;
+        if (gc > nmid) gc = nmid;
+        c.factor_cta_blocks = (int)(gc < 1 ? 1 : gc);
+    }
     return (int)(g < 1 ? 1 : g);
 }
 
@@ -545,6 +776,7 @@ int solve_grid(Ctx& c) {
     int64_t g = (int64_t)sm_count() * per;
     int64_t need = (c.host_sym.n_main + 7) / 8;
     if (g > need) g = need;
+    if (const char* e = getenv("CIPM_SOLVE_BLOCKS")) g = std::min<int64_t>(g, atoll(e));     // experiments
     return (int)(g < 1 ? 1 : g);
 }
 

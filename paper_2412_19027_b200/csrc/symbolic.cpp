@@ -510,21 +510,43 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     // The complement is closed under descendants, so the persistent kernels
     // finish it before the tail starts.
     S.is_tail.assign(ns, 0);
+    const int64_t tail_w = std::min<int64_t>(opt.tail_width, 64);   // the persistent kernels hold w < 64 columns
     for (int32_t J = 0; J < ns; ++J) {
         int64_t w = S.sn_col[J + 1] - S.sn_col[J];
         int64_t o = (S.sn_rptr[J + 1] - S.sn_rptr[J]) - w;
-        if (w >= opt.tail_width || o >= opt.tail_offrows) S.is_tail[J] = 1;
+        if (w >= tail_w || o >= opt.tail_offrows) S.is_tail[J] = 1;
     }
     for (int32_t J = 0; J < ns; ++J)       // parents have larger indices (postorder)
         if (S.is_tail[J] && S.sn_parent[J] >= 0) S.is_tail[S.sn_parent[J]] = 1;
+    // mid tier: large panels / inboxes and all their (non-tail) ancestors
+    S.is_mid.assign(ns, 0);
+    for (int32_t J = 0; J < ns; ++J) {
+        if (S.is_tail[J]) continue;
+        const int64_t w = S.sn_col[J + 1] - S.sn_col[J];
+        const int64_t r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+        const int64_t inbox = S.irow_ptr[S.sn_rptr[J + 1]] - S.irow_ptr[S.sn_rptr[J]];
+        if (w * r >= opt.mid_panel || inbox >= 2 * (int64_t)opt.mid_panel) S.is_mid[J] = 1;
+    }
+    for (int32_t J = 0; J < ns; ++J)
+        if (S.is_mid[J] && S.sn_parent[J] >= 0 && !S.is_tail[S.sn_parent[J]]) S.is_mid[S.sn_parent[J]] = 1;
+    auto tier = [&](int32_t J) { return S.is_tail[J] ? 2 : (S.is_mid[J] ? 1 : 0); };
     S.order.resize(ns);
     std::iota(S.order.begin(), S.order.end(), 0);
     std::stable_sort(S.order.begin(), S.order.end(), [&](int32_t a, int32_t b) {
-        if (S.is_tail[a] != S.is_tail[b]) return S.is_tail[a] < S.is_tail[b];
+        if (tier(a) != tier(b)) return tier(a) < tier(b);
         return S.level[a] < S.level[b];
     });
     S.n_main = 0;
-    for (int32_t J = 0; J < ns; ++J) S.n_main += S.is_tail[J] ? 0 : 1;
+    S.n_warp = 0;
+    for (int32_t J = 0; J < ns; ++J) {
+        S.n_main += S.is_tail[J] ? 0 : 1;
+        S.n_warp += tier(J) == 0 ? 1 : 0;
+    }
+    S.max_panel_warp = 0;
+    for (int32_t J = 0; J < ns; ++J)
+        if (tier(J) == 0)
+            S.max_panel_warp = std::max<int64_t>(S.max_panel_warp,
+                                                 (S.sn_col[J + 1] - S.sn_col[J]) * (S.sn_rptr[J + 1] - S.sn_rptr[J]));
     S.max_panel_main = 0;
     for (int32_t J = 0; J < ns; ++J)
         if (!S.is_tail[J])

@@ -23,6 +23,8 @@ struct SymbolicOptions {
     double relax_big_frac = 0.05;
     int tail_width = 64;       // supernodes at least this wide go to the dense tail path
     int tail_offrows = 512;    // ... or with at least this many off-diagonal rows
+    int mid_panel = 512;       // panels (w*r) at least this large, or inboxes of 2x this, and
+                               // their ancestors are factored by whole CTAs (mid tier)
 };
 
 struct Symbolic {
@@ -63,8 +65,11 @@ struct Symbolic {
     std::vector<int32_t> level;            // per supernode, 0 = leaf
     int32_t height = 0;
     std::vector<int8_t> is_tail;           // dense tail supernode (multi-CTA path, dense.cu)
+    std::vector<int8_t> is_mid;            // mid tier: one CTA per supernode in the factorisation
     int32_t n_main = 0;                    // order[0 .. n_main) are the non-tail supernodes
+    int32_t n_warp = 0;                    // order[0 .. n_warp) are the warp-tier supernodes
     int64_t max_panel_main = 0;            // largest non-tail panel (shared-memory sizing)
+    int64_t max_panel_warp = 0;            // largest warp-tier panel
     // scatter maps into the panel value array (int64 positions)
     std::vector<int64_t> map_p;            // P CSR nnz; -1 for strictly-lower entries
     std::vector<int64_t> map_a;            // A CSR nnz (entry (n+r, j) of K stored at L(col j? ...))

@@ -93,6 +93,7 @@ _SIGS = {
     "cipm_profile": ([c_void_p, ctypes.c_int], ctypes.c_int),
     "cipm_kernel_stats": ([c_void_p, P_DBL], ctypes.c_int),
     "cipm_timer": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
+    "cipm_trace": ([c_void_p, ctypes.c_int, P_I64], ctypes.c_int),
     "cipm_batch_create": ([ctypes.POINTER(ProblemDesc), ctypes.c_int, ctypes.POINTER(Settings), c_dbl, c_dbl,
                            ctypes.c_int, ctypes.POINTER(c_void_p)], ctypes.c_int),
     "cipm_batch_info": ([c_void_p, P_I64], ctypes.c_int),
