@@ -818,7 +818,7 @@ int cipm_timer(cipm_ctx* h, int op, double* ms) {
 int cipm_trace(cipm_ctx* h, int enable, int64_t* out) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t cnt = 6 * (int64_t)c.sym.nsuper;
+    const int64_t cnt = 9 * (int64_t)c.sym.nsuper;
     if (enable) {
         if (!c.trace) {
             CIPM_CUDA(cudaMalloc(&c.trace, sizeof(int64_t) * cnt));

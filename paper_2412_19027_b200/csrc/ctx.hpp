@@ -124,6 +124,7 @@ struct Ctx {
     int factor_blocks = 0, solve_blocks = 0, factor_smem = 0;
     int64_t factor_slice = 0;        // per-warp panel slice (elements) of the factor kernel
     int factor_cta_smem = 0, factor_cta_blocks = 0;   // mid-tier CTA kernel
+    int64_t solve_slice = 0;         // per-warp panel slice (elements) of the solve kernels
     // dense tail (dense.cu)
     std::vector<TailNode> tail;
     void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)

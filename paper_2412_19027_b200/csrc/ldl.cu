@@ -380,118 +380,161 @@ struct SolveArgs {
     int32_t* ticket;
     int act0, act1;      // active right-hand sides
     int64_t* trace;      // optional per-task timeline (cipm_trace): ticket / ready / done (ns)
+    int slice;           // per-warp shared-memory panel slice (elements)
 };
 
 
 // warp-cooperative sums of the vector inbox of columns c0 .. c0+w-1 (one
-// contiguous range grouped by column): colsum[j] = sum of column c0+j's entries
+// contiguous range grouped by column): colsum[j] = sum of column c0+j's entries.
+// Four 32-entry chunks are loaded before they are reduced (memory parallelism).
 template <typename T>
 __device__ __forceinline__ void vgather_warp(const T* vq, const int64_t* __restrict__ gptr, int c0, int w,
-                                             T* colsum, int64_t* vcol_ptr) {
+                                             T* colsum, int64_t* win) {
     const int lane = threadIdx.x & 31;
     for (int j = lane; j < w; j += 32) colsum[j] = (T)0;
-    for (int j = lane; j <= w; j += 32) vcol_ptr[j] = gptr[c0 + j];   // window, re-based at c0
+    for (int j = lane; j <= w; j += 32) win[j] = gptr[c0 + j];   // column-pointer window
     __syncwarp();
-    c0 = 0;
-    const int64_t lo = vcol_ptr[0], hi = vcol_ptr[w];
-    if (hi > lo) {
-        // entry -> column: binary search in the (small) column pointer window
-        for (int64_t base = lo; base < hi; base += 32) {
-            const int64_t e = base + lane;
-            const bool valid = e < hi;
-            int col = -(lane + 2);
-            T v = (T)0;
-            if (valid) {
-                int lo_c = 0, hi_c = w - 1;
-                while (lo_c < hi_c) {
-                    const int mid = (lo_c + hi_c + 1) >> 1;
-                    if (vcol_ptr[c0 + mid] <= e) lo_c = mid; else hi_c = mid - 1;
+    const int64_t lo = win[0], hi = win[w];
+    for (int64_t base = lo; base < hi; base += 128) {
+        T v[4];
+        int col[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t e = base + 32 * u + lane;
+            v[u] = e < hi ? __ldcg(vq + e) : (T)0;
+            col[u] = -(lane + 2);
+            if (e < hi) {
+                int lc = 0, hc = w - 1;
+                while (lc < hc) {
+                    const int mid = (lc + hc + 1) >> 1;
+                    if (win[mid] <= e) lc = mid; else hc = mid - 1;
                 }
-                col = lo_c;
-                v = __ldcg(vq + e);
+                col[u] = lc;
             }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            T x = v[u];
+            const int cu = col[u];
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const int cp = __shfl_up_sync(0xffffffffu, col, off);
-                const T vp = __shfl_up_sync(0xffffffffu, v, off);
-                if (lane >= off && cp == col) v += vp;
+                const int cp = __shfl_up_sync(0xffffffffu, cu, off);
+                const T vp = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off && cp == cu) x += vp;
             }
-            const int cn = __shfl_down_sync(0xffffffffu, col, 1);
-            if (valid && (lane == 31 || cn != col)) colsum[col] += v;
+            const int cn = __shfl_down_sync(0xffffffffu, cu, 1);
+            if (cu >= 0 && (lane == 31 || cn != cu)) colsum[cu] += x;
             __syncwarp();
         }
     }
     __syncwarp();
 }
 
-// forward sweep L y = b: warp per supernode, columns in registers (lane owns
-// columns lane and lane+32; non-tail supernodes are narrower than 64)
+// stage a panel (r*w elements, 16-byte aligned in HBM) in the warp's shared-memory
+// slice with one TMA bulk copy when it fits; otherwise read it in place
 template <typename T>
-__global__ void __launch_bounds__(256) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
-    __shared__ T colsum[8][64];
-    __shared__ int64_t vwin[8][65];
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ const T* stage_panel(const T* L, int psize, T* slice, int cap, uint64_t* bar,
+                                                uint32_t& phase) {
+    const uint32_t bytes = ((uint32_t)psize * (uint32_t)sizeof(T) + 15u) & ~15u;
+    if (bytes > (uint32_t)cap * (uint32_t)sizeof(T)) return L;
+    fence_proxy_async_smem();     // every lane's earlier generic reads of the slice precede the async write
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) bulk_g2s(slice, L, bytes, bar);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    return slice;
+}
+
+constexpr int SW = 8;   // warps per solve CTA
+
+// forward sweep L y = b: warp per supernode, columns in registers (lane owns
+// columns lane and lane+32; non-tail supernodes are narrower than 64), panel
+// staged in shared memory
+template <typename T>
+__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    __shared__ T colsum[SW][64];
+    __shared__ int64_t vwin[SW][65];
+    __shared__ uint64_t bars[SW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
+    if (lane == 0) mbar_init(&bars[wid], 1);
+    __syncwarp();
+    uint32_t phase = 0;
     for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(a.ticket, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.nsuper) return;
         const int J = a.order[t];
-        if (a.trace && lane == 0) a.trace[3 * t] = gtimer();
-        if (lane == 0) wait_ge(a.count + J, a.sn_nchild[J]);
+        if (a.trace && lane == 0) a.trace[6 * t] = gtimer();
+        if (lane == 0) {
+            const int need = a.sn_nchild[J];
+            if (need > 0) wait_ge(a.count + J, need);
+        }
         __syncwarp();
-        if (a.trace && lane == 0) a.trace[3 * t + 1] = gtimer();
+        if (a.trace && lane == 0) a.trace[6 * t + 1] = gtimer();
         const int c0 = a.sn_col[J];
         const int w = a.sn_col[J + 1] - c0;
         const int64_t r0 = a.sn_rptr[J];
         const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const T* L = lval + a.sn_loff[J];
         const int64_t cvo = a.cv_off[J];
+        const T* L = stage_panel(lval + a.sn_loff[J], r * w, slice, a.slice, &bars[wid], phase);
         for (int q = 0; q < 2; ++q) {
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xJ = x + (int64_t)q * a.dim + c0;
             T* vq = vin + (int64_t)q * a.nv;
-            T* cs = colsum[threadIdx.x >> 5];
-            vgather_warp(vq, a.vcol_ptr, c0, w, cs, vwin[threadIdx.x >> 5]);
+            T* cs = colsum[wid];
+            vgather_warp(vq, a.vcol_ptr, c0, w, cs, vwin[wid]);
+            if (a.trace && lane == 0) a.trace[6 * t + 2] = gtimer();
             T x0 = (T)0, x1 = (T)0;
             if (lane < w) x0 = xJ[lane] - cs[lane];
             if (lane + 32 < w) x1 = xJ[lane + 32] - cs[lane + 32];
-#pragma unroll 4
             for (int j = 0; j < w; ++j) {
-                const T l0 = (lane > j && lane < w) ? L[(int64_t)j * r + lane] : (T)0;
-                const T l1 = (lane + 32 > j && lane + 32 < w) ? L[(int64_t)j * r + lane + 32] : (T)0;
+                const T l0 = (lane > j && lane < w) ? L[j * r + lane] : (T)0;
+                const T l1 = (lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
                 const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
                 x0 -= l0 * xj;
                 x1 -= l1 * xj;
             }
             if (lane < w) xJ[lane] = x0;
             if (lane + 32 < w) xJ[lane + 32] = x1;
+            if (a.trace && lane == 0) a.trace[6 * t + 3] = gtimer();
             for (int i0 = w; i0 < r; i0 += 32) {
                 const int i = i0 + lane;
+                const bool ok = i < r;
+                const int ii = ok ? i : r - 1;
                 T acc = (T)0;
-#pragma unroll 4
                 for (int k = 0; k < w; ++k) {
                     const T xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-                    if (i < r) acc += L[(int64_t)k * r + i] * xk;
+                    acc += L[k * r + ii] * xk;
                 }
-                if (i < r) vq[a.vpush_pos[cvo + i - w]] = acc;
+                if (ok) vq[a.vpush_pos[cvo + i - w]] = acc;
             }
+            if (a.trace && lane == 0) a.trace[6 * t + 4] = gtimer();
         }
         __threadfence();
         __syncwarp();
         if (lane == 0) {
             const int P = a.sn_parent[J];
             if (P >= 0) atomicAdd(a.count + P, 1);
-            if (a.trace) a.trace[3 * t + 2] = gtimer();
+            if (a.trace) a.trace[6 * t + 5] = gtimer();
         }
     }
 }
 
 // backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
 template <typename T>
-__global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __restrict__ lval,
-                                                       const T* __restrict__ dvec, T* x) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T* __restrict__ lval,
+                                                           const T* __restrict__ dvec, T* x) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    __shared__ T xs[SW][2][64];
+    __shared__ uint64_t bars[SW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
+    if (lane == 0) mbar_init(&bars[wid], 1);
+    __syncwarp();
+    uint32_t phase = 0;
     for (;;) {
         int t = 0;
         if (lane == 0) t = atomicAdd(a.ticket, 1);
@@ -505,10 +548,11 @@ __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __r
         const int w = a.sn_col[J + 1] - c0;
         const int64_t r0 = a.sn_rptr[J];
         const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const int32_t* rowsJ = a.sn_rows + r0;
-        const T* L = lval + a.sn_loff[J];
-        const T* L0 = L + (int64_t)lane * r;
-        const T* L1 = L + (int64_t)(lane + 32) * r;
+        const int o = r - w;
+        const int32_t* rowsJ = a.sn_rows + r0 + w;
+        const T* L = stage_panel(lval + a.sn_loff[J], r * w, slice, a.slice, &bars[wid], phase);
+        const T* L0 = L + lane * r;
+        const T* L1 = L + (lane + 32) * r;
         const bool o0 = lane < w, o1 = lane + 32 < w;
         for (int q = 0; q < 2; ++q) {
             if (!(q == 0 ? a.act0 : a.act1)) continue;
@@ -516,11 +560,19 @@ __global__ void __launch_bounds__(256) backward_kernel(SolveArgs a, const T* __r
             T* xJ = xv + c0;
             T x0 = o0 ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
             T x1 = o1 ? xJ[lane + 32] / dvec[c0 + lane + 32] : (T)0;
-#pragma unroll 4
-            for (int i = w; i < r; ++i) {
-                const T xi = __ldcg(xv + rowsJ[i]);
-                if (o0) x0 -= L0[i] * xi;
-                if (o1) x1 -= L1[i] * xi;
+            // ancestors' values at the off rows: gathered once (coalesced over lanes)
+            for (int i0 = 0; i0 < o; i0 += 64) {
+                T* xo = xs[wid][0];
+                const int n = min(64, o - i0);
+                if (lane < n) xo[lane] = __ldcg(xv + rowsJ[i0 + lane]);
+                if (lane + 32 < n) xo[lane + 32] = __ldcg(xv + rowsJ[i0 + lane + 32]);
+                __syncwarp();
+                for (int k = 0; k < n; ++k) {
+                    const T xi = xo[k];
+                    if (o0) x0 -= L0[w + i0 + k] * xi;
+                    if (o1) x1 -= L1[w + i0 + k] * xi;
+                }
+                __syncwarp();
             }
             for (int j = w - 1; j >= 0; --j) {
                 const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
@@ -580,6 +632,7 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.act0 = act0;
     a.act1 = act1;
     a.trace = nullptr;
+    a.slice = (int)c.solve_slice;
     return a;
 }
 
@@ -622,7 +675,7 @@ int factor_t(Ctx& c) {
     a.delta_s = c.delta_s;
     a.delta_d = c.delta_d;
     a.smem_cap = c.factor_slice;
-    a.trace = c.trace ? c.trace + 3 * (int64_t)c.sym.nsuper : nullptr;
+    a.trace = c.trace ? c.trace + 6 * (int64_t)c.sym.nsuper : nullptr;
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.sn_maxd, 0, sizeof(double) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
@@ -674,11 +727,13 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     }
     SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
     f.trace = c.trace;
-    if (f.nsuper > 0) forward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    const size_t ssm = sizeof(T) * (size_t)c.solve_slice * SW;
+    if (f.nsuper > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     k_tail_forward(c, t, act0, act1);
     k_tail_backward(c, t, act0, act1);
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
-    if (b.nsuper > 0) backward_kernel<T><<<c.solve_blocks, 256, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+    if (b.nsuper > 0)
+        backward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_solve.emplace_back(e0, e0 + 1);
@@ -767,14 +822,27 @@ int factor_grid(Ctx& c) {
 }
 
 int solve_grid(Ctx& c) {
-    int per = 0;
-    if (c.precision == CIPM_FULL)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<double>, 256, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<float>, 256, 0);
+    // per-warp panel slice: 6 KiB (four 8-warp CTAs per SM); larger panels are read from L2/HBM
+    const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
+    c.solve_slice = std::max<int64_t>(64, std::min<int64_t>((c.host_sym.max_panel_main + 3) & ~int64_t(3), 6144 / es));
+    if (const char* e = getenv("CIPM_SOLVE_SLICE")) c.solve_slice = std::max<int64_t>(4, atoll(e) & ~int64_t(3));   // experiments
+    const int ssm = (int)(es * c.solve_slice * SW);
+    int per = 0, per2 = 0;
+    if (c.precision == CIPM_FULL) {
+        cudaFuncSetAttribute(forward_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+        cudaFuncSetAttribute(backward_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<double>, SW * 32, ssm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, backward_kernel<double>, SW * 32, ssm);
+    } else {
+        cudaFuncSetAttribute(forward_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+        cudaFuncSetAttribute(backward_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, forward_kernel<float>, SW * 32, ssm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, backward_kernel<float>, SW * 32, ssm);
+    }
+    per = std::min(per, per2);
     if (per < 1) per = 1;
     int64_t g = (int64_t)sm_count() * per;
-    int64_t need = (c.host_sym.n_main + 7) / 8;
+    int64_t need = (c.host_sym.n_main + SW - 1) / SW;
     if (g > need) g = need;
     if (const char* e = getenv("CIPM_SOLVE_BLOCKS")) g = std::min<int64_t>(g, atoll(e));     // experiments
     return (int)(g < 1 ? 1 : g);

@@ -357,12 +357,12 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     for (int32_t J = 0; J < ns; ++J) {
         int64_t w = S.sn_col[J + 1] - S.sn_col[J];
         int64_t r = S.sn_rptr[J + 1] - S.sn_rptr[J];
-        S.sn_loff[J + 1] = S.sn_loff[J] + w * r;
+        S.sn_loff[J + 1] = S.sn_loff[J] + ((w * r + 3) & ~int64_t(3));   // 16-byte aligned panels (TMA bulk)
         S.max_width = std::max(S.max_width, w);
         S.max_rows = std::max(S.max_rows, r);
         S.max_panel = std::max(S.max_panel, w * r);
     }
-    S.nnz_storage = S.sn_loff[ns];
+    S.nnz_storage = S.sn_loff[ns] + 4;   // bulk copies may read up to 16 bytes past a panel
     S.sn_parent.assign(ns, -1);
     S.sn_nchild.assign(ns, 0);
     for (int32_t J = 0; J < ns; ++J) {
