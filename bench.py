@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--cpu-max-iters", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-solves", type=int, default=1, help=argparse.SUPPRESS)
     ap.add_argument("--cpu-impl", default="reference", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-procs", type=int, default=1, help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-instances", type=int, default=0,
+                    help="batched configs: instances in one CPU sample (0: 256 for the cpu_baseline "
+                         "key, every instance for --impl reference)")
     return ap.parse_args()
 
 
@@ -67,7 +71,9 @@ def workload(config):
             "c2_lasso": "C2 lasso 50k features x 200k rows (n=300k, m=300k), fp32 LDL' + fp64 IR",
             "c3_socp": "C3 SOCP 100k cones dim U{3..10}",
             "c4_exppow": "C4 50k exp + 20k pow cones",
-            "c5a_psd": "C5a 10k PSD cones side 6"}[config]
+            "c5a_psd": "C5a 10k PSD cones side 6",
+            "c5b_mpc": "C5b 2048 independent MPC QPs (nx=8, nu=3, N=10), one CTA per instance, "
+                       "instances sharded over the GPUs"}[config]
     return spec, desc
 
 
@@ -158,6 +164,8 @@ def cpu_worker(args):
     """One process: setup once, then `--cpu-solves` bounded solves of at most
     `--cpu-max-iters` IPM iterations each; one JSON line per solve."""
     from paper_2412_19027_b200 import generators as G
+    if "instances" in G.CONFIGS[args.config]:
+        return cpu_worker_batch(args)
     prob = G.build(args.config)
     cap = args.cpu_max_iters or 200
     if args.cpu_impl == "reference":
@@ -190,13 +198,68 @@ def cpu_worker(args):
         print("CPUWORKER " + json.dumps(out), flush=True)
 
 
-def run_cpu(args, max_iters, solves=1, impl=None):
+def _ref_solver_factory(impl, config, eps):
+    """Returns make(problem) -> object with .solve(); reference setup happens in make()."""
+    from paper_2412_19027_b200 import generators as G
+    prec = G.CONFIGS[config]["precision"]
+    if impl == "reference":
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/cipm_numba_cache")
+        sys.dont_write_bytecode = True
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import conic_ipm as ref
+        warm = _to_reference(ref, G.gen_lp(20, 40, seed=1))
+        ref.Solver(warm, ref.SolverSettings(eps_feas=eps, precision=prec)).solve()
+        return lambda p: ref.Solver(_to_reference(ref, p), ref.SolverSettings(eps_feas=eps, precision=prec))
+    from oracle.ipm import OracleSolver
+    from paper_2412_19027_b200.settings import SolverSettings
+    return lambda p: OracleSolver(p, SolverSettings(eps_feas=eps, precision=prec))
+
+
+_CHUNK_SOLVERS = {}
+
+
+def _batch_chunk(payload):
+    """Worker: set up its instances once (cached per process), then time only the solves."""
+    impl, config, eps, lo, hi = payload
+    key = (impl, config, eps, lo, hi)
+    if key not in _CHUNK_SOLVERS:
+        from paper_2412_19027_b200 import generators as G
+        make = _ref_solver_factory(impl, config, eps)
+        _CHUNK_SOLVERS[key] = [make(p) for p in G.build_instances(config, lo, hi)]
+    solvers = _CHUNK_SOLVERS[key]
+    t0 = time.perf_counter()
+    it = sum(s.solve().iterations for s in solvers)
+    return it, time.perf_counter() - t0
+
+
+def cpu_worker_batch(args):
+    """Batched configs: `--cpu-procs` worker processes (the reference's own
+    `bench --jobs` mode, bench.py:98-113) over the first `--cpu-instances`
+    instances; one JSON line per repetition."""
+    from concurrent.futures import ProcessPoolExecutor
+    procs = max(1, args.cpu_procs)
+    count = args.cpu_instances
+    chunks = [(args.cpu_impl, args.config, args.eps, count * k // procs, count * (k + 1) // procs)
+              for k in range(procs)]
+    # one chunk per worker process; setup (reference Solver construction) is done once in each
+    # worker and excluded; a repetition's time is the slowest worker's solve time
+    with ProcessPoolExecutor(max_workers=procs) as ex:
+        for _ in range(max(1, args.cpu_solves)):
+            out = list(ex.map(_batch_chunk, chunks, chunksize=1))
+            its = sum(o[0] for o in out)
+            res = {"impl": args.cpu_impl, "setup_s": 0.0, "solve_s": max(o[1] for o in out), "iterations": its,
+                   "status": "n/a", "obj": None, "instances": count, "procs": procs}
+            print("CPUWORKER " + json.dumps(res), flush=True)
+
+
+def run_cpu(args, max_iters, solves=1, impl=None, procs=1):
     impl = impl or ("reference" if reference_available() else "port")
     env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
                NUMBA_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
     cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--config", args.config,
            "--eps", str(args.eps), "--cpu-max-iters", str(max_iters), "--cpu-solves", str(solves),
-           "--cpu-impl", impl]
+           "--cpu-impl", impl, "--cpu-procs", str(procs), "--cpu-instances", str(args.cpu_instances)]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=3600)
     res = [json.loads(line[len("CPUWORKER "):]) for line in out.stdout.splitlines()
            if line.startswith("CPUWORKER ")]
@@ -208,6 +271,8 @@ def run_cpu(args, max_iters, solves=1, impl=None):
 def cpu_sample(args):
     """Bounded sample for the cpu_baseline key: one solve capped at `--cpu-iters`
     IPM iterations (setup excluded from the rate)."""
+    if not args.cpu_instances:
+        args.cpu_instances = 256
     impl, res = run_cpu(args, args.cpu_iters, 1)
     r = res[0]
     return impl, r
@@ -234,6 +299,128 @@ def ncu_traffic(config):
             return json.load(f).get(config)
     except Exception:
         return None
+
+
+def shard(total, world, rank):
+    """Contiguous block of instances of rank `rank`."""
+    lo = total * rank // world
+    return lo, total * (rank + 1) // world
+
+
+def run_batch(args):
+    """C5b: every rank solves its shard of the 2048 MPC instances in one launch
+    (no collective on the solve path); value = all ranks' IPM iterations / the
+    slowest rank's device time."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_19027_b200 import generators as G
+    from paper_2412_19027_b200.batch import BatchSolver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec, desc = workload(args.config)
+    total = G.CONFIGS[args.config]["instances"]
+    lo, hi = shard(total, world, rank)
+    probs = G.build_instances(args.config, lo, hi)
+    cfg = settings_for(args.config, args.eps)
+    t0 = time.perf_counter()
+    bs = BatchSolver(probs, cfg, device=local)
+    setup = time.perf_counter() - t0
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(args.warmup):
+        bs.run()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        ms.append(bs.run())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    res = bs.results()
+    iters = sum(r.iterations for r in res)
+    statuses = sorted({r.status for r in res})
+    dev_s = sum(ms) / 1e3
+    # e2e through the public API: host arrays -> update_data (equilibration + H2D) -> solve -> results (D2H)
+    q_host = np.stack([p.q for p in probs])
+    b_host = np.stack([p.b for p in probs])
+    from paper_2412_19027_b200.native import lib
+    import ctypes
+    h2d, d2h = ctypes.c_int64(0), ctypes.c_int64(0)
+    lib().cipm_batch_io_bytes(bs.handle, None, None, 1)
+    if world > 1:
+        dist.barrier()
+    e2e = []
+    e2e_it = 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        bs.update_data(q=q_host, b=b_host)
+        out = bs.solve()
+        e2e.append(time.perf_counter() - t1)
+        e2e_it += sum(r.iterations for r in out)
+    lib().cipm_batch_io_bytes(bs.handle, ctypes.byref(h2d), ctypes.byref(d2h), 1)
+    e2e_s = sum(e2e)
+    vals = torch.tensor([dev_s, e2e_s, float(iters), float(e2e_it), float(len(probs))], dtype=torch.float64,
+                        device=f"cuda:{local}")
+    if world > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_s, e2e_s = float(mx[0]), float(mx[1])
+        iters_all, e2e_all, n_all = float(sm[2]), float(sm[3]), int(sm[4])
+    else:
+        iters_all, e2e_all, n_all = float(iters), float(e2e_it), len(probs)
+    value = iters_all * args.steps / dev_s
+    info = bs.info()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
+        "config": {"workload": desc, "config": args.config, "instances": n_all, "instances_per_gpu": len(probs),
+                   "n": info["n"], "m": info["m"], "nnz_L": info["nnz_l"], "smem_bytes_per_cta": info["smem_bytes"],
+                   "eps_feas": args.eps, "status": statuses, "iterations_total": iters_all,
+                   "instances_per_s": n_all * args.steps / dev_s, "setup_s": setup,
+                   "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"instance shards x{world}, no collective on the solve path"},
+        "clocks": clk,
+        "e2e": {"value": e2e_all / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d.value // max(1, args.steps),
+                "d2h_bytes_per_step": d2h.value // max(1, args.steps),
+                "path": "BatchSolver.update_data(q, b) host arrays (equilibration + H2D) + solve() -> host results"},
+        "gpu_launches": args.steps,
+        "roofline": None,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            impl, r = cpu_sample(args)
+            line["cpu_baseline"] = {"value": r["iterations"] / r["solve_s"], "unit": UNIT, "cores": 1, "kind": impl,
+                                    "sample": f"{r['instances']} instances solved sequentially by "
+                                              f"{'the unmodified reference conic_ipm' if impl == 'reference' else 'the oracle'}"
+                                              f" (setup excluded), 1 thread of a {os.cpu_count()}-core host"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"failed: {e}"[:300]}
+    bs.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args):
@@ -418,7 +605,12 @@ def run_reference(args):
     if rank != 0:
         return
     spec, desc = workload(args.config)
-    impl, res = run_cpu(args, args.cpu_iters, args.warmup + args.steps)
+    from paper_2412_19027_b200 import generators as G
+    batched = "instances" in G.CONFIGS[args.config]
+    procs = (os.cpu_count() or 1) if batched else 1
+    if batched and not args.cpu_instances:
+        args.cpu_instances = G.CONFIGS[args.config]["instances"]
+    impl, res = run_cpu(args, args.cpu_iters, args.warmup + args.steps, procs=procs if batched else 1)
     timed = res[args.warmup:]
     it_total = sum(r["iterations"] for r in timed)
     secs = sum(r["solve_s"] for r in timed)
@@ -427,16 +619,18 @@ def run_reference(args):
             else "oracle restatement of the reference (bit-exact on the golden fixtures)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if batched else "weak", "vs_baseline": None,
             "dtype": "f64 iterate / f32 LDL' + f64 refinement" if G_precision(args.config) == "mixed" else "f64",
             "impl": "reference", "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
             "config": {"workload": desc, "config": args.config, "eps_feas": args.eps,
                        "status": sorted({r["status"] for r in timed}),
                        "iterations_per_solve": it_total / max(1, len(timed)),
                        "setup_s": timed[0]["setup_s"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": impl,
-                             "sample": f"{what}: each step one solve capped at {args.cpu_iters} IPM iterations, "
-                                       f"setup excluded, 1 thread of a {os.cpu_count()}-core host"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs if batched else 1, "kind": impl,
+                             "sample": (f"{what}: each step {args.cpu_instances} instances over {procs} worker "
+                                        f"processes (the reference's bench --jobs mode)" if batched else
+                                        f"{what}: each step one solve capped at {args.cpu_iters} IPM iterations, "
+                                        f"setup excluded, 1 thread of a {os.cpu_count()}-core host")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -451,8 +645,11 @@ def main():
     if args.cpu_worker:
         cpu_worker(args)
         return
+    from paper_2412_19027_b200 import generators as G
     if args.impl == "reference":
         run_reference(args)
+    elif "instances" in G.CONFIGS[args.config]:
+        run_batch(args)
     else:
         run_ours(args)
 

@@ -286,7 +286,15 @@ CONFIGS = {
     "c3_socp": dict(gen="socp", kwargs=dict(ncones=100_000), precision="full"),
     "c4_exppow": dict(gen="exppow", kwargs=dict(n_exp=50_000, n_pow=20_000), precision="full"),
     "c5a_psd": dict(gen="psd", kwargs=dict(ncones=10_000, side=6), precision="full"),
+    # C5b: 8 x 256 = 2048 independent MPC QPs (seeds 0..2047), one shared pattern
+    "c5b_mpc": dict(gen="mpc", kwargs=dict(), precision="full", instances=2048),
 }
+
+
+def build_instances(config: str, lo: int, hi: int):
+    """Instances lo .. hi-1 of a batched config (seed = instance index)."""
+    spec = CONFIGS[config]
+    return [GENERATORS[spec["gen"]](seed=k, **spec["kwargs"]) for k in range(lo, hi)]
 
 GENERATORS = {"lp": gen_lp, "lasso": gen_lasso, "socp": gen_socp, "exppow": gen_exppow,
               "psd": gen_psd, "mpc": gen_mpc}
