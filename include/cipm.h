@@ -164,9 +164,9 @@ int cipm_kernel_stats(cipm_ctx *ctx, double *out);
  * returns the elapsed milliseconds */
 int cipm_timer(cipm_ctx *ctx, int op, double *ms);
 /* per-task timeline of the persistent kernels (profiling seam): enable=1 arms it;
- * enable=0 copies out[9*nsuper] = forward {ticket, ready, gathered, triangle, pushed, done} ns
- * per ticket of the last forward sweep, then factor {ticket, ready, done} per ticket of the
- * last factorisation */
+ * enable=0 copies out[12*nsuper] = per supernode: forward {start, start, gathered, triangle,
+ * pushed, done} ns of the last forward sweep, then factor {start, start, staged, gathered,
+ * factored, done} of the last factorisation */
 int cipm_trace(cipm_ctx *ctx, int enable, int64_t *out);
 /* CUDA-event time (ms) of the last numeric factorisation and last triangular solve */
 int cipm_kernel_times(cipm_ctx *ctx, double *factor_ms, double *solve_ms);

@@ -415,6 +415,15 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(upload(c, &c.sym.cv_off, S.cv_off.data(), S.nsuper + 1));
     TRY(upload(c, &c.sym.vpush_pos, S.vpush_pos.data(), (int64_t)S.vpush_pos.size()));
     TRY(upload(c, &c.sym.vcol_ptr, S.vcol_ptr.data(), (int64_t)S.vcol_ptr.size()));
+    TRY(upload(c, &c.sym.desc32, S.desc32.data(), (int64_t)S.desc32.size()));
+    TRY(upload(c, &c.sym.desc64, S.desc64.data(), (int64_t)S.desc64.size()));
+    TRY(upload(c, &c.sym.need, S.need.data(), (int64_t)S.need.size()));
+    TRY(upload(c, &c.sym.start_solve, S.start_solve.data(), (int64_t)S.start_solve.size()));
+    TRY(upload(c, &c.sym.start_fac_warp, S.start_fac_warp.data(), (int64_t)S.start_fac_warp.size()));
+    TRY(upload(c, &c.sym.start_fac_cta, S.start_fac_cta.data(), (int64_t)S.start_fac_cta.size()));
+    TRY(upload(c, &c.sym.vin_col, S.vin_col.data(), (int64_t)S.vin_col.size()));
+    TRY(upload(c, &c.sym.tiny, S.tiny.data(), (int64_t)S.tiny.size()));
+    TRY(upload(c, &c.sym.bwd_order, S.bwd_order.data(), (int64_t)S.bwd_order.size()));
     c.sym.ninbox = S.cb_off[S.nsuper];
     c.sym.nv = S.cv_off[S.nsuper];
     if ((int64_t)S.map_hblk.size() != c.hblk_total) {
@@ -456,7 +465,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     }
     TRY(dalloc(c, &c.fac_count, S.nsuper));
     TRY(dalloc(c, &c.bwd_done, S.nsuper));
-    TRY(dalloc(c, &c.tickets, 4));
+    TRY(dalloc(c, &c.tickets, 8));
     TRY(dalloc(c, &c.sn_maxd, S.nsuper));
     TRY(dalloc(c, &c.bumps, 1));
     TRY(dalloc(c, &c.rb, 2 * c.dim));
@@ -818,7 +827,7 @@ int cipm_timer(cipm_ctx* h, int op, double* ms) {
 int cipm_trace(cipm_ctx* h, int enable, int64_t* out) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    const int64_t cnt = 9 * (int64_t)c.sym.nsuper;
+    const int64_t cnt = 12 * (int64_t)c.sym.nsuper;
     if (enable) {
         if (!c.trace) {
             CIPM_CUDA(cudaMalloc(&c.trace, sizeof(int64_t) * cnt));

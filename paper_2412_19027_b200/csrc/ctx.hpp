@@ -44,6 +44,15 @@ struct DevSymbolic {
     int64_t* cv_off = nullptr;
     int64_t* vpush_pos = nullptr;
     int64_t* vcol_ptr = nullptr;
+    int32_t* desc32 = nullptr;
+    int64_t* desc64 = nullptr;
+    int32_t* need = nullptr;
+    int32_t* start_solve = nullptr;
+    int32_t* start_fac_warp = nullptr;
+    int32_t* start_fac_cta = nullptr;
+    uint8_t* vin_col = nullptr;
+    int32_t* tiny = nullptr;
+    int32_t* bwd_order = nullptr;
     int64_t nnz_storage = 0;
     int64_t ninbox = 0, nv = 0;
 };

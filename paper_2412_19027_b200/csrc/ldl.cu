@@ -1,17 +1,21 @@
 // Supernodal quasi-definite LDL' on sm_100a: numeric refactorisation and
 // triangular solves (replaces kkt/ldl.py:37-104 and kkt/system.py:246-271).
 //
-// Scheduling: one persistent launch per phase.  Tasks (supernodes) are handed
-// out by an atomic ticket in a fixed topological order (leaves first), and a
-// task spins on per-supernode dependency counters until its inputs are final.
-// A task only ever waits on tasks with smaller tickets, which are already held
-// by running CTAs/warps, so the scheme cannot deadlock; there is one launch per
-// factorisation / solve instead of one per elimination-tree level.
+// Scheduling — continuation, not polling.  Every persistent launch starts from
+// a list of seed supernodes (those without children in its tier).  A task
+// (warp or CTA) processes its supernode, publishes its outputs, fences, and
+// increments its parent's same-tier child counter; the task whose increment
+// completes the count continues directly with the parent.  Nothing spins,
+// every supernode is processed exactly once, and the critical path of the
+// elimination tree is walked by one task without hand-offs.  The backward
+// sweep (root first) hands supernodes out by ticket in reverse topological
+// order and waits on the parent's done flag.
 //
-// Numerics: left-looking (fan-in).  Supernode J gathers the updates of every
-// descendant K listed in its update list in a fixed order, then factors its
-// dense panel.  No atomics touch floating-point data, so factors and solutions
-// are bitwise reproducible run to run (SPEC kkt-solver "Determinism").
+// Numerics: push/pull inboxes.  A finished supernode K computes its
+// contribution block C_K = L_off D L_off' and scatters it to the inbox slots
+// of its ancestors; supernode J sums its inbox with fixed-order segmented
+// scans.  No atomics touch floating-point data, so factors and solutions are
+// bitwise reproducible run to run (SPEC kkt-solver "Determinism").
 // Dynamic regularisation (ldl.py:79-87): a pivot with |d| < δs + δd·runmax is
 // replaced by ±bound with the sign of its block; runmax is the largest |D| in
 // the supernode's subtree computed so far (the sequential reference uses all
@@ -33,11 +37,6 @@ __device__ __forceinline__ int64_t gtimer() {
     int64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
-}
-
-template <typename T>
-__device__ __forceinline__ T ldcg(const T* p) {
-    return __ldcg(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -62,41 +61,35 @@ __global__ void add_static_reg(T* base, const int64_t* map_diag, int64_t n, int6
 }
 
 // ---------------------------------------------------------------------------
-// numeric factorisation (push/pull inbox scheme)
-//
-// Task J (one CTA): wait until its children are done; copy its panel to shared
-// memory; gather its inbox — every contribution block entry of every descendant
-// that lands in J, pre-sorted by (row, column, source) so each thread owns one
-// panel row and accumulates runs in registers (no atomics, no barriers, fixed
-// order); factor the dense panel; write L and D; then compute its own packed
-// contribution block C_J = L_off D L_off' and scatter it into the ancestors'
-// inboxes.  The expensive dot products therefore run in the producer, spread
-// over many CTAs, instead of serially in the consumer.
+// shared pieces
 // ---------------------------------------------------------------------------
 
-struct FactorArgs {
-    int32_t nsuper;      // tickets t in [t_begin, nsuper) of `order`
-    int32_t t_begin;
-    const int32_t* order;
-    const int32_t* sn_col;
-    const int64_t* sn_rptr;
-    const int64_t* sn_loff;
-    const int32_t* sn_parent;
-    const int32_t* sn_nchild;
-    const int64_t* cb_off;
-    const int64_t* push_pos;
-    const int64_t* irow_ptr;
-    const int32_t* inbox_tgt;
-    const int8_t* sign;
-    int32_t* count;
-    int32_t* ticket;
-    double* maxd;        // max |D| over the subtree, accumulated by the children (atomic max)
-    int32_t* bumps;
-    int* err;
-    double delta_s, delta_d;
-    int64_t smem_cap;    // panel elements that fit the dynamic shared memory
-    int64_t* trace;      // optional per-task timeline (cipm_trace)
+// per-supernode descriptor (symbolic.hpp desc32 / desc64), loaded by lanes 0..15 in one round trip
+struct Desc {
+    int c0, w, r, parent, tier;
+    int64_t loff, cvo, vlo, vhi, ilo, ihi, cb, rptr;
 };
+
+__device__ __forceinline__ Desc load_desc(const int32_t* __restrict__ d32, const int64_t* __restrict__ d64, int J) {
+    const int lane = threadIdx.x & 31;
+    const int v32 = lane < 8 ? __ldg(d32 + (int64_t)J * 8 + lane) : 0;
+    const int64_t v64 = (lane >= 8 && lane < 16) ? __ldg(d64 + (int64_t)J * 8 + (lane - 8)) : 0;
+    Desc d;
+    d.c0 = __shfl_sync(0xffffffffu, v32, 0);
+    d.w = __shfl_sync(0xffffffffu, v32, 1);
+    d.r = __shfl_sync(0xffffffffu, v32, 2);
+    d.parent = __shfl_sync(0xffffffffu, v32, 3);
+    d.tier = __shfl_sync(0xffffffffu, v32, 6);
+    d.loff = __shfl_sync(0xffffffffu, v64, 8);
+    d.cvo = __shfl_sync(0xffffffffu, v64, 9);
+    d.vlo = __shfl_sync(0xffffffffu, v64, 10);
+    d.vhi = __shfl_sync(0xffffffffu, v64, 11);
+    d.ilo = __shfl_sync(0xffffffffu, v64, 12);
+    d.ihi = __shfl_sync(0xffffffffu, v64, 13);
+    d.cb = __shfl_sync(0xffffffffu, v64, 14);
+    d.rptr = __shfl_sync(0xffffffffu, v64, 15);
+    return d;
+}
 
 __device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
@@ -104,316 +97,534 @@ __device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
 
 // Warp-cooperative segmented gather: entries [lo, hi) sorted so that equal
 // targets are contiguous; P[tgt] -= sum of their values (fixed order: a warp
-// Hillis-Steele scan per 32-entry chunk, carries across chunks).
+// Hillis-Steele scan per 32-entry chunk, carries across chunks).  Four chunks
+// are loaded before they are reduced.
 template <typename T>
 __device__ __forceinline__ void warp_gather_sub(T* P, const int32_t* __restrict__ tgt, const T* vals, int64_t lo,
                                                 int64_t hi) {
     const int lane = threadIdx.x & 31;
     int carry_t = -1;
     T carry = (T)0;
-    for (int64_t base = lo; base < hi; base += 32) {
-        const int64_t e = base + lane;
-        const bool valid = e < hi;
-        const int tg = valid ? tgt[e] : -(lane + 2);
-        T v = valid ? __ldcg(vals + e) : (T)0;
-        const int t0 = __shfl_sync(0xffffffffu, tg, 0);
-        if (carry_t >= 0 && t0 != carry_t) {
-            if (lane == 0) P[carry_t] -= carry;
-            carry_t = -1;
+    for (int64_t base0 = lo; base0 < hi; base0 += 128) {
+        T vv[4];
+        int tt[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t e = base0 + 32 * u + lane;
+            const bool valid = e < hi;
+            tt[u] = valid ? tgt[e] : -(lane + 2);
+            vv[u] = valid ? __ldcg(vals + e) : (T)0;
         }
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int tp = __shfl_up_sync(0xffffffffu, tg, off);
-            const T vp = __shfl_up_sync(0xffffffffu, v, off);
-            if (lane >= off && tp == tg) v += vp;
+        for (int u = 0; u < 4; ++u) {
+            const int64_t base = base0 + 32 * u;
+            if (base >= hi) break;
+            const int tg = tt[u];
+            T v = vv[u];
+            const bool valid = base + lane < hi;
+            const int t0 = __shfl_sync(0xffffffffu, tg, 0);
+            if (carry_t >= 0 && t0 != carry_t) {
+                if (lane == 0) P[carry_t] -= carry;
+                carry_t = -1;
+            }
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int tp = __shfl_up_sync(0xffffffffu, tg, off);
+                const T vp = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off && tp == tg) v += vp;
+            }
+            const int tn = __shfl_down_sync(0xffffffffu, tg, 1);
+            const bool is_end = lane == 31 || tn != tg;
+            const bool more = base + 32 < hi;
+            T tot = v;
+            if (valid && is_end && tg == carry_t) tot += carry;
+            if (valid && is_end && !(lane == 31 && more)) P[tg] -= tot;
+            const int t31 = __shfl_sync(0xffffffffu, tg, 31);
+            const T v31 = __shfl_sync(0xffffffffu, tot, 31);
+            if (more) {
+                carry_t = t31;
+                carry = v31;
+            }
+            __syncwarp();
         }
-        const int tn = __shfl_down_sync(0xffffffffu, tg, 1);
-        const bool is_end = lane == 31 || tn != tg;
-        const bool more = base + 32 < hi;
-        T tot = v;
-        if (valid && is_end && tg == carry_t) tot += carry;
-        if (valid && is_end && !(lane == 31 && more)) P[tg] -= tot;
-        const int t31 = __shfl_sync(0xffffffffu, tg, 31);
-        const T v31 = __shfl_sync(0xffffffffu, tot, 31);
-        if (more) {
-            carry_t = t31;
-            carry = v31;
-        }
-        __syncwarp();
     }
     __syncwarp();
 }
 
-constexpr int FW = 8;   // warps per factor CTA
+// stage a panel (r*w elements, 16-byte aligned in HBM) in the warp's shared-memory
+// slice with one TMA bulk copy when it fits; otherwise read it in place
+template <typename T>
+__device__ __forceinline__ T* stage_panel(T* L, int psize, T* slice, int cap, uint64_t* bar, uint32_t& phase) {
+    const uint32_t bytes = ((uint32_t)psize * (uint32_t)sizeof(T) + 15u) & ~15u;
+    if (bytes > (uint32_t)cap * (uint32_t)sizeof(T)) return L;
+    fence_proxy_async_smem();     // every lane's earlier generic reads of the slice precede the async write
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) bulk_g2s(slice, L, bytes, bar);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    return slice;
+}
 
-// Task J (one warp): wait until its children are done; stage its panel in the
-// warp's shared-memory slice (in place in HBM when it does not fit); gather its
-// inbox (every contribution entry of every descendant that lands in J, sorted
-// by target, fixed-order segmented sums); factor the dense panel; write L and
-// D; then compute its packed contribution block C_J = L_off D L_off' and
-// scatter it into the ancestors' inboxes.  No floating-point atomics.
+// ---------------------------------------------------------------------------
+// numeric factorisation
+// ---------------------------------------------------------------------------
+
+struct FactorArgs {
+    int32_t nstart;      // seeds of this tier
+    const int32_t* start;
+    int32_t ntiny;       // tiny leaves (warp tier only; one lane each)
+    const int32_t* tiny;
+    int32_t* ticket_tiny;
+    int tier;
+    const int32_t* desc32;
+    const int64_t* desc64;
+    const int32_t* need;
+    const int64_t* push_pos;
+    const int32_t* inbox_tgt;
+    const int64_t* irow_ptr;
+    const int8_t* sign;
+    int32_t* count;
+    int32_t* ticket;
+    double* maxd;        // max |D| over the subtree, accumulated by the children (atomic max)
+    int32_t* bumps;
+    int* err;
+    double delta_s, delta_d;
+    int64_t smem_cap;    // panel elements per warp slice (warp tier) / per CTA (CTA tier)
+    int64_t* trace;      // optional per-task timeline (cipm_trace)
+};
+
+
+// warp-tier task body: gather, panel LDL', write-back, contribution push.
+// Forced inline so P keeps its address space at each call site.
+template <typename T>
+__device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const Desc& d, int c0, int w, int r, int o,
+                                               double& runmax, T* sDw, const int8_t* sSgw, const FactorArgs& a,
+                                               T* __restrict__ dvec, T* __restrict__ inbox, int J) {
+    const int lane = threadIdx.x & 31;
+    const int psize = r * w;
+    // 1. gather the inbox of all r rows (one contiguous, target-sorted range)
+    warp_gather_sub(P, a.inbox_tgt, inbox, d.ilo, d.ihi);
+    if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
+    // 2. dense LDL' of the panel (right-looking, lanes over rows)
+    for (int j = 0; j < w; ++j) {
+        T* Pj = P + j * r;
+        double dd = (double)Pj[j];
+        const double bound = a.delta_s + a.delta_d * runmax;
+        const bool bump = fabs(dd) < bound;
+        if (bump) dd = sSgw[j] > 0 ? bound : -bound;
+        const T dt = (T)dd;
+        runmax = fmax(runmax, fabs(dd));
+        __syncwarp();
+        if (lane == 0) {
+            if (bump) atomicAdd(a.bumps, 1);
+            if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+            dvec[c0 + j] = dt;
+            sDw[j] = dt;
+            Pj[j] = (T)1;
+        }
+        for (int i = j + 1 + lane; i < r; i += 32) Pj[i] = Pj[i] / dt;
+        __syncwarp();
+        for (int c = j + 1; c < w; ++c) {
+            const T pjc = Pj[c];
+            T* Pc = P + c * r;
+            for (int i = c + lane; i < r; i += 32) Pc[i] -= Pj[i] * dt * pjc;
+        }
+        __syncwarp();
+    }
+    if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
+    // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
+    if (in_smem)
+        for (int i = lane; i < psize; i += 32) L[i] = P[i];
+    if (o > 0) {
+        int64_t tb = 0;   // packed offset of column bb
+        for (int bb = 0; bb < o; ++bb) {
+            const T* Pb = P + w + bb;
+            for (int aa = bb + lane; aa < o; aa += 32) {
+                T acc = (T)0;
+                for (int k = 0; k < w; ++k) acc += P[k * r + w + aa] * sDw[k] * Pb[k * r];
+                inbox[a.push_pos[d.cb + tb + (aa - bb)]] = acc;
+            }
+            tb += o - bb;
+        }
+    }
+}
+
+constexpr int FW = 8;   // warps per factor CTA (warp tier)
+
+// Warp tier: one warp per supernode.  Stage the panel in the warp's shared
+// slice (in place in HBM when it does not fit); gather its inbox; factor the
+// dense panel (right-looking, lanes over rows); write L and D; compute and
+// scatter C_J = L_off D L_off'; signal the parent and continue with it if
+// this was its last child.
+// tiny leaf (w <= 4, r <= 16, no inbox): the whole task in one lane's registers,
+// specialised on the width W so the register arrays are statically indexed.
+// Returns the parent if this leaf completed its parent's child count.
+template <typename T, int W>
+__device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, int64_t loff, int64_t cb,
+                                             const FactorArgs& a, T* __restrict__ lval, T* __restrict__ dvec,
+                                             T* __restrict__ inbox) {
+    T* L = lval + loff;
+    T p[W][16];
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[j][i] = i < r ? L[j * r + i] : (T)0;
+    double runmax = 0.0;        // a leaf has no subtree below it
+    T dv[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        double dd = (double)p[j][j];
+        const double bound = a.delta_s + a.delta_d * runmax;
+        if (fabs(dd) < bound) {
+            dd = a.sign[c0 + j] > 0 ? bound : -bound;
+            atomicAdd(a.bumps, 1);
+        }
+        const T dt = (T)dd;
+        if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+        runmax = fmax(runmax, fabs(dd));
+        dv[j] = dt;
+        dvec[c0 + j] = dt;
+#pragma unroll
+        for (int i = j + 1; i < 16; ++i) p[j][i] = p[j][i] / dt;
+#pragma unroll
+        for (int c = j + 1; c < W; ++c)
+#pragma unroll
+            for (int i = c; i < 16; ++i) p[c][i] -= p[j][i] * dt * p[j][c];
+        p[j][j] = (T)1;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (i < r) L[j * r + i] = p[j][i];
+    // contribution block: packed column-major lower over the off rows W..r-1
+    const int o = r - W;
+    int64_t tb = 0;
+#pragma unroll
+    for (int b = 0; b < 16 - W; ++b) {
+        if (b >= o) break;
+#pragma unroll
+        for (int aa = b; aa < 16 - W; ++aa) {
+            if (aa >= o) break;
+            T acc = (T)0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc += p[k][W + aa] * dv[k] * p[k][W + b];
+            inbox[a.push_pos[cb + tb + (aa - b)]] = acc;
+        }
+        tb += o - b;
+    }
+    __threadfence();
+    if (parent < 0) return -1;
+    atomic_max_pos(a.maxd + parent, runmax);
+    if (a.desc32[(int64_t)parent * 8 + 6] != 0) return -1;     // parent factored by another tier
+    __threadfence();
+    const int old = atomicAdd(a.count + parent, 1);
+    return old == a.need[2 * parent + 1] - 1 ? parent : -1;
+}
+
+template <typename T>
+__device__ __forceinline__ int factor_tiny_lane(int J, const FactorArgs& a, T* __restrict__ lval, T* __restrict__ dvec,
+                                                T* __restrict__ inbox) {
+    const int32_t* d32 = a.desc32 + (int64_t)J * 8;
+    const int c0 = d32[0], w = d32[1], r = d32[2], parent = d32[3];
+    const int64_t loff = a.desc64[(int64_t)J * 8], cb = a.desc64[(int64_t)J * 8 + 6];
+    switch (w) {
+        case 1: return factor_tiny_w<T, 1>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
+        case 2: return factor_tiny_w<T, 2>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
+        case 3: return factor_tiny_w<T, 3>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
+        default: return factor_tiny_w<T, 4>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
+    }
+}
+
+// one warp-tier supernode task and its continuation chain up the tree
+template <typename T>
+__device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T* __restrict__ lval,
+                                                  T* __restrict__ dvec, T* __restrict__ inbox, T* sp, T* sDw,
+                                                  int8_t* sSgw, uint64_t* bar, uint32_t& phase) {
+    const int lane = threadIdx.x & 31;
+    while (J >= 0) {
+        if (a.trace && lane == 0) a.trace[6 * J] = a.trace[6 * J + 1] = gtimer();
+        const Desc d = load_desc(a.desc32, a.desc64, J);
+        const int c0 = d.c0, w = d.w, r = d.r, o = r - w;
+        int needP = 0, tierP = -1;
+        if (lane == 0 && d.parent >= 0) {
+            needP = a.need[2 * d.parent + 1];
+            tierP = a.desc32[(int64_t)d.parent * 8 + 6];
+        }
+        double runmax = lane == 0 ? __ldcg(a.maxd + J) : 0.0;
+        runmax = __shfl_sync(0xffffffffu, runmax, 0);
+        if (lane < w) sSgw[lane] = a.sign[c0 + lane];
+        if (lane + 32 < w) sSgw[lane + 32] = a.sign[c0 + lane + 32];
+        T* L = lval + d.loff;
+        const int psize = r * w;
+        T* P = stage_panel(L, psize, sp, (int)a.smem_cap, bar, phase);
+        if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
+        if (P != L) warp_task_body(sp, L, true, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
+        else warp_task_body(L, L, false, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
+        __threadfence();
+        __syncwarp();
+        int cont = -1;
+        if (lane == 0) {
+            if (d.parent >= 0) {
+                atomic_max_pos(a.maxd + d.parent, runmax);
+                if (tierP == a.tier) {
+                    __threadfence();
+                    const int old = atomicAdd(a.count + d.parent, 1);
+                    if (old == needP - 1) cont = d.parent;
+                }
+            }
+            if (a.trace) a.trace[6 * J + 5] = gtimer();
+        }
+        J = __shfl_sync(0xffffffffu, cont, 0);
+        if (J >= 0) __threadfence();
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                          T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ T sD[FW][64];
+    __shared__ int8_t sSg[FW][64];
+    __shared__ uint64_t bars[FW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T* sp = reinterpret_cast<T*>(smem_raw) + (int64_t)wid * a.smem_cap;
+    if (lane == 0) mbar_init(&bars[wid], 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    // phase 1: tiny leaves, 32 per warp (one per lane); completed parents continue as warp tasks
     for (;;) {
-        int t = 0;
-        if (lane == 0) t = a.t_begin + atomicAdd(a.ticket, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.nsuper) return;
-        const int J = a.order[t];
-        double runmax = 0.0;
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if ((int64_t)chunk * 32 >= a.ntiny) break;
+        const int idx = chunk * 32 + lane;
+        const int J = idx < a.ntiny ? a.tiny[idx] : -1;
+        const int ready = J >= 0 ? factor_tiny_lane(J, a, lval, dvec, inbox) : -1;
+        unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
+        if (m) __threadfence();
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int P = __shfl_sync(0xffffffffu, ready, l);
+            factor_warp_chain(P, a, lval, dvec, inbox, sp, sD[wid], sSg[wid], &bars[wid], phase);
+        }
+    }
+    // phase 2: the other seeds of the tier, by ticket
+    for (;;) {
+        int J = -1;
         if (lane == 0) {
-            if (a.trace) a.trace[3 * t] = gtimer();
-            wait_ge(a.count + J, a.sn_nchild[J]);
-            runmax = __ldcg(a.maxd + J);
-            if (a.trace) a.trace[3 * t + 1] = gtimer();
+            const int t = atomicAdd(a.ticket, 1);
+            J = t < a.nstart ? a.start[t] : -1;
         }
-        runmax = __shfl_sync(0xffffffffu, runmax, 0);
-        const int c0 = a.sn_col[J];
-        const int w = a.sn_col[J + 1] - c0;
-        const int64_t r0 = a.sn_rptr[J];
-        const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const int o = r - w;
-        T* L = lval + a.sn_loff[J];
-        const int psize = r * w;
-        const bool in_smem = psize <= a.smem_cap;
-        T* P = in_smem ? sp : L;
-        if (in_smem)
-            for (int i = lane; i < psize; i += 32) sp[i] = L[i];
-        __syncwarp();
+        J = __shfl_sync(0xffffffffu, J, 0);
+        if (J < 0) return;
+        factor_warp_chain(J, a, lval, dvec, inbox, sp, sD[wid], sSg[wid], &bars[wid], phase);
+    }
+}
 
-        // 1. gather the inbox of all r rows (one contiguous, target-sorted range)
-        warp_gather_sub(P, a.inbox_tgt, inbox, a.irow_ptr[r0], a.irow_ptr[r0 + r]);
-
-        // 2. dense LDL' of the panel (right-looking, lanes over rows)
-        for (int j = 0; j < w; ++j) {
-            T* Pj = P + j * r;
-            double d = (double)Pj[j];
-            const double bound = a.delta_s + a.delta_d * runmax;
-            const bool bump = fabs(d) < bound;
-            if (bump) d = a.sign[c0 + j] > 0 ? bound : -bound;
-            const T dt = (T)d;
-            runmax = fmax(runmax, fabs(d));
-            __syncwarp();
-            if (lane == 0) {
-                if (bump) atomicAdd(a.bumps, 1);
-                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                dvec[c0 + j] = dt;
-                sD[wid][j] = dt;
-                Pj[j] = (T)1;
-            }
-            for (int i = j + 1 + lane; i < r; i += 32) Pj[i] = Pj[i] / dt;
-            __syncwarp();
-            for (int c = j + 1; c < w; ++c) {
-                const T pjc = Pj[c];
-                T* Pc = P + c * r;
-                for (int i = c + lane; i < r; i += 32) Pc[i] -= Pj[i] * dt * pjc;
-            }
-            __syncwarp();
+// CTA-tier dense panel LDL' (see factor_cta_kernel); forced inline so the
+// panel pointer keeps its address space (shared -> LDS/STS) at each call site
+template <typename T>
+__device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
+                                              const FactorArgs& a, T* __restrict__ dvec) {
+    const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5, nw = nt >> 5, lane = tid & 31;
+    double runmax = s_runmax;
+    for (int j = 0; j < w; ++j) {
+        const T* Pj = P + (int64_t)j * r;
+        double dd = (double)Pj[j];
+        const double bound = a.delta_s + a.delta_d * runmax;
+        const bool bump = fabs(dd) < bound;
+        if (bump) dd = sSg[j] > 0 ? bound : -bound;
+        const T dt = (T)dd;
+        runmax = fmax(runmax, fabs(dd));
+        if (tid == 0) {
+            if (bump) atomicAdd(a.bumps, 1);
+            if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+            sD[j] = dt;
         }
-
-        // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
-        if (in_smem)
-            for (int i = lane; i < psize; i += 32) L[i] = sp[i];
-        if (o > 0) {
-            const int64_t base = a.cb_off[J];
-            const T* Dj = sD[wid];
-            int64_t tb = 0;   // packed offset of column bb
-            for (int bb = 0; bb < o; ++bb) {
-                const T* Pb = P + w + bb;
-                for (int aa = bb + lane; aa < o; aa += 32) {
-                    T acc = (T)0;
-                    for (int k = 0; k < w; ++k) acc += P[k * r + w + aa] * Dj[k] * Pb[k * r];
-                    inbox[a.push_pos[base + tb + (aa - bb)]] = acc;
-                }
-                tb += o - bb;
-            }
+        const T inv = (T)1 / dt;
+        // warps over columns c > j, lanes over rows i >= c
+        for (int c = j + 1 + wid; c < w; c += nw) {
+            const T f = Pj[c] * inv;
+            T* Pc = P + (int64_t)c * r;
+            for (int i = c + lane; i < r; i += 32) Pc[i] -= Pj[i] * f;
         }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-            const int Pn = a.sn_parent[J];
-            if (Pn >= 0) {
-                atomic_max_pos(a.maxd + Pn, runmax);
-                __threadfence();
-                atomicAdd(a.count + Pn, 1);
-            }
-            if (a.trace) a.trace[3 * t + 2] = gtimer();
+        __syncthreads();
+    }
+    for (int j = wid; j < w; j += nw) {
+        const T inv = (T)1 / sD[j];
+        T* Pj = P + (int64_t)j * r;
+        for (int i = j + 1 + lane; i < r; i += 32) Pj[i] = Pj[i] * inv;
+        if (lane == 0) Pj[j] = (T)1;
+    }
+    for (int j = tid; j < w; j += nt) dvec[c0 + j] = sD[j];
+    if (tid == 0) s_runmax = runmax;
+    __syncthreads();
+}
+
+
+// CTA-tier contribution block C = L_off D L_off' scattered to the ancestors' inboxes
+template <typename T>
+__device__ __forceinline__ void cta_push(const T* P, int r, int w, int o, int64_t base, const T* sD,
+                                         const FactorArgs& a, T* __restrict__ inbox) {
+    const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
+    for (int bb = wid; bb < o; bb += nw) {
+        const int64_t tb = (int64_t)bb * o - (int64_t)bb * (bb - 1) / 2;
+        const T* Pb = P + w + bb;
+        for (int aa = bb + (tid & 31); aa < o; aa += 32) {
+            T acc = (T)0;
+#pragma unroll 4
+            for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * sD[k] * Pb[(int64_t)k * r];
+            inbox[a.push_pos[base + tb + (aa - bb)]] = acc;
         }
     }
 }
 
-
-// Mid tier (one CTA per supernode): the same task for panels too large for one
-// warp — the inbox gather is split by rows over the CTA's warps, the dense
-// panel LDL' uses all threads, the contribution block is computed by all
-// threads.  Launched after the warp tier, before the dense tail.
+// CTA tier (one CTA per supernode): panels too large for one warp — the inbox
+// gather is split by rows over the CTA's warps, the dense panel LDL' and the
+// contribution block use all threads.  Same continuation protocol.
 template <typename T>
 __global__ void __launch_bounds__(256) factor_cta_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                          T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sp = reinterpret_cast<T*>(smem_raw);
-    __shared__ int s_task;
-    __shared__ double s_piv;
+    __shared__ int s_J, s_needP, s_tierP, s_next;
     __shared__ double s_runmax;
     __shared__ T sD[64];
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    __shared__ int8_t sSg[64];
+    __shared__ int32_t s_d32[8];
+    __shared__ int64_t s_d64[8];
+    const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5, nw = nt >> 5;
+    if (tid == 0) s_next = -1;
+    __syncthreads();
     for (;;) {
-        if (tid == 0) s_task = a.t_begin + atomicAdd(a.ticket, 1);
-        __syncthreads();
-        const int t = s_task;
-        if (t >= a.nsuper) return;
-        const int J = a.order[t];
         if (tid == 0) {
-            if (a.trace) a.trace[3 * t] = gtimer();
-            wait_ge(a.count + J, a.sn_nchild[J]);
-            s_runmax = __ldcg(a.maxd + J);
-            if (a.trace) a.trace[3 * t + 1] = gtimer();
+            int J = s_next;
+            if (J < 0) {
+                const int t = atomicAdd(a.ticket, 1);
+                J = t < a.nstart ? a.start[t] : -1;
+            }
+            s_J = J;
         }
         __syncthreads();
-        const int c0 = a.sn_col[J];
-        const int w = a.sn_col[J + 1] - c0;
-        const int64_t r0 = a.sn_rptr[J];
-        const int r = (int)(a.sn_rptr[J + 1] - r0);
+        const int J = s_J;
+        if (J < 0) return;
+        if (tid < 8) s_d32[tid] = a.desc32[(int64_t)J * 8 + tid];
+        else if (tid < 16) s_d64[tid - 8] = a.desc64[(int64_t)J * 8 + tid - 8];
+        if (tid == 0) {
+            if (a.trace) a.trace[6 * J] = a.trace[6 * J + 1] = gtimer();
+            s_runmax = __ldcg(a.maxd + J);
+        }
+        __syncthreads();
+        const int c0 = s_d32[0], w = s_d32[1], r = s_d32[2], parent = s_d32[3];
         const int o = r - w;
-        T* L = lval + a.sn_loff[J];
+        const int64_t r0 = s_d64[7];
+        if (tid == 0) {
+            s_needP = parent >= 0 ? a.need[2 * parent + 1] : 0;
+            s_tierP = parent >= 0 ? a.desc32[(int64_t)parent * 8 + 6] : -1;
+        }
+        T* L = lval + s_d64[0];
         const int64_t psize = (int64_t)r * w;
         const bool in_smem = psize <= a.smem_cap;
-        T* P = in_smem ? sp : L;
         if (in_smem)
             for (int64_t i = tid; i < psize; i += nt) sp[i] = L[i];
+        if (tid < w) sSg[tid] = a.sign[c0 + tid];
         __syncthreads();
+        if (a.trace && tid == 0) a.trace[6 * J + 2] = gtimer();
         // 1. inbox gather, rows split over the warps (targets are unique per row)
         {
             const int rs = (int)((int64_t)r * wid / nw), re = (int)((int64_t)r * (wid + 1) / nw);
-            if (re > rs) warp_gather_sub(P, a.inbox_tgt, inbox, a.irow_ptr[r0 + rs], a.irow_ptr[r0 + re]);
-            (void)lane;
+            if (re > rs) {
+                if (in_smem) warp_gather_sub(sp, a.inbox_tgt, inbox, a.irow_ptr[r0 + rs], a.irow_ptr[r0 + re]);
+                else warp_gather_sub(L, a.inbox_tgt, inbox, a.irow_ptr[r0 + rs], a.irow_ptr[r0 + re]);
+            }
         }
         __syncthreads();
-        // 2. dense LDL' of the panel (right-looking inside the panel)
-        for (int j = 0; j < w; ++j) {
-            if (tid == 0) {
-                double d = (double)P[(int64_t)j * r + j];
-                const double bound = a.delta_s + a.delta_d * s_runmax;
-                if (fabs(d) < bound) {
-                    d = a.sign[c0 + j] > 0 ? bound : -bound;
-                    atomicAdd(a.bumps, 1);
-                }
-                const T dt = (T)d;
-                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                dvec[c0 + j] = dt;
-                sD[j] = dt;
-                P[(int64_t)j * r + j] = (T)1;
-                s_piv = (double)dt;
-                s_runmax = fmax(s_runmax, fabs(d));
-            }
-            __syncthreads();
-            const T d = (T)s_piv;
-            T* Pj = P + (int64_t)j * r;
-            for (int i = j + 1 + tid; i < r; i += nt) Pj[i] = Pj[i] / d;
-            __syncthreads();
-            const int rem_c = w - j - 1;
-            if (rem_c > 0) {
-                const int rows = r - j - 1;
-                const int64_t total = (int64_t)rem_c * rows;
-                for (int64_t idx = tid; idx < total; idx += nt) {
-                    const int i = j + 1 + (int)(idx % rows);
-                    const int c = j + 1 + (int)(idx / rows);
-                    if (i < c) continue;
-                    P[(int64_t)c * r + i] -= Pj[i] * d * Pj[c];
-                }
-            }
-            __syncthreads();
-        }
+        if (a.trace && tid == 0) a.trace[6 * J + 3] = gtimer();
+        // 2. dense LDL' of the panel: right-looking on the unscaled columns
+        //    (A_ci -= A_ij A_cj / d_j), one barrier per column, pivots computed
+        //    redundantly by every thread, columns scaled by 1/d at the end
+        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec);
+        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec);
+        if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
         // 3. write back, push C_J = L_off D L_off'
         if (in_smem)
             for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
         if (o > 0) {
-            const int64_t base = a.cb_off[J];
-            const int64_t tot = (int64_t)o * o;
-            for (int64_t idx = tid; idx < tot; idx += nt) {
-                const int aa = (int)(idx % o), bb = (int)(idx / o);
-                if (aa < bb) continue;
-                T acc = (T)0;
-                for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * sD[k] * P[(int64_t)k * r + w + bb];
-                const int64_t tpk = (int64_t)bb * o - (int64_t)bb * (bb - 1) / 2 + (aa - bb);
-                inbox[a.push_pos[base + tpk]] = acc;
-            }
+            if (in_smem) cta_push(sp, r, w, o, s_d64[6], sD, a, inbox);
+            else cta_push(L, r, w, o, s_d64[6], sD, a, inbox);
         }
         __threadfence();
         __syncthreads();
         if (tid == 0) {
-            const int Pn = a.sn_parent[J];
-            if (Pn >= 0) {
-                atomic_max_pos(a.maxd + Pn, s_runmax);
-                __threadfence();
-                atomicAdd(a.count + Pn, 1);
+            int cont = -1;
+            if (parent >= 0) {
+                atomic_max_pos(a.maxd + parent, s_runmax);
+                if (s_tierP == a.tier) {
+                    __threadfence();
+                    const int old = atomicAdd(a.count + parent, 1);
+                    if (old == s_needP - 1) cont = parent;
+                }
             }
-            if (a.trace) a.trace[3 * t + 2] = gtimer();
+            if (a.trace) a.trace[6 * J + 5] = gtimer();
+            if (cont >= 0) __threadfence();
+            s_next = cont;
         }
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-// triangular solves, one warp per supernode task (push/pull for the forward sweep)
+// triangular solves
 // ---------------------------------------------------------------------------
 
 struct SolveArgs {
-    int32_t nsuper;
+    int32_t nstart;      // forward seeds
+    const int32_t* start;
+    int32_t n_main;      // backward: tickets over order[0 .. n_main) reversed
+    const int32_t* order;
+    int32_t ntiny;       // tiny leaves (one lane each)
+    const int32_t* tiny;
+    int32_t* ticket_tiny;
+    const int32_t* bwd_done;   // forward tiny-leaf path: unused; backward: parents' done flags
+    const int32_t* desc32;
+    const int64_t* desc64;
+    const int32_t* need;
     int64_t dim;
     int64_t nv;          // vector inbox length per right-hand side
-    const int32_t* order;
-    const int32_t* sn_col;
-    const int64_t* sn_rptr;
     const int32_t* sn_rows;
-    const int64_t* sn_loff;
-    const int32_t* sn_parent;
-    const int32_t* sn_nchild;
-    const int64_t* cv_off;
     const int64_t* vpush_pos;
-    const int64_t* vcol_ptr;
+    const uint8_t* vin_col;
     int32_t* count;      // forward: children done; backward: done flags
     int32_t* ticket;
     int act0, act1;      // active right-hand sides
-    int64_t* trace;      // optional per-task timeline (cipm_trace): ticket / ready / done (ns)
+    int64_t* trace;      // optional per-task timeline (cipm_trace)
     int slice;           // per-warp shared-memory panel slice (elements)
 };
 
-
-// warp-cooperative sums of the vector inbox of columns c0 .. c0+w-1 (one
-// contiguous range grouped by column): colsum[j] = sum of column c0+j's entries.
-// Four 32-entry chunks are loaded before they are reduced (memory parallelism).
+// warp-cooperative sums of the vector inbox of one supernode's columns (entries
+// [lo, hi), grouped by column, local column ids in vin_col): colsum[j] = sum of
+// column j's entries.  Four 32-entry chunks are loaded before they are reduced.
 template <typename T>
-__device__ __forceinline__ void vgather_warp(const T* vq, const int64_t* __restrict__ gptr, int c0, int w,
-                                             T* colsum, int64_t* win) {
+__device__ __forceinline__ void vgather_warp(const T* vq, const uint8_t* __restrict__ vin_col, int64_t lo,
+                                             int64_t hi, int w, T* colsum) {
     const int lane = threadIdx.x & 31;
     for (int j = lane; j < w; j += 32) colsum[j] = (T)0;
-    for (int j = lane; j <= w; j += 32) win[j] = gptr[c0 + j];   // column-pointer window
     __syncwarp();
-    const int64_t lo = win[0], hi = win[w];
-    for (int64_t base = lo; base < hi; base += 128) {
-        T v[4];
-        int col[4];
+    for (int64_t base = lo; base < hi; base += 256) {
+        T v[8];
+        int col[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
             const int64_t e = base + 32 * u + lane;
-            v[u] = e < hi ? __ldcg(vq + e) : (T)0;
-            col[u] = -(lane + 2);
-            if (e < hi) {
-                int lc = 0, hc = w - 1;
-                while (lc < hc) {
-                    const int mid = (lc + hc + 1) >> 1;
-                    if (win[mid] <= e) lc = mid; else hc = mid - 1;
-                }
-                col[u] = lc;
-            }
+            const bool ok = e < hi;
+            v[u] = ok ? __ldcg(vq + e) : (T)0;
+            col[u] = ok ? (int)__ldg(vin_col + e) : -(lane + 2);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
+            if (base + 32 * u >= hi) break;
             T x = v[u];
             const int cu = col[u];
 #pragma unroll
@@ -430,127 +641,61 @@ __device__ __forceinline__ void vgather_warp(const T* vq, const int64_t* __restr
     __syncwarp();
 }
 
-// stage a panel (r*w elements, 16-byte aligned in HBM) in the warp's shared-memory
-// slice with one TMA bulk copy when it fits; otherwise read it in place
+// forward task, compute part: triangle and off-row push for each active RHS.
+// Forced inline so L keeps its address space (staged panel -> LDS).
 template <typename T>
-__device__ __forceinline__ const T* stage_panel(const T* L, int psize, T* slice, int cap, uint64_t* bar,
-                                                uint32_t& phase) {
-    const uint32_t bytes = ((uint32_t)psize * (uint32_t)sizeof(T) + 15u) & ~15u;
-    if (bytes > (uint32_t)cap * (uint32_t)sizeof(T)) return L;
-    fence_proxy_async_smem();     // every lane's earlier generic reads of the slice precede the async write
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) bulk_g2s(slice, L, bytes, bar);
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    return slice;
-}
-
-constexpr int SW = 8;   // warps per solve CTA
-
-// forward sweep L y = b: warp per supernode, columns in registers (lane owns
-// columns lane and lane+32; non-tail supernodes are narrower than 64), panel
-// staged in shared memory
-template <typename T>
-__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
-    extern __shared__ __align__(16) unsigned char sraw[];
-    __shared__ T colsum[SW][64];
-    __shared__ int64_t vwin[SW][65];
-    __shared__ uint64_t bars[SW];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
-    if (lane == 0) mbar_init(&bars[wid], 1);
-    __syncwarp();
-    uint32_t phase = 0;
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(a.ticket, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.nsuper) return;
-        const int J = a.order[t];
-        if (a.trace && lane == 0) a.trace[6 * t] = gtimer();
-        if (lane == 0) {
-            const int need = a.sn_nchild[J];
-            if (need > 0) wait_ge(a.count + J, need);
-        }
-        __syncwarp();
-        if (a.trace && lane == 0) a.trace[6 * t + 1] = gtimer();
-        const int c0 = a.sn_col[J];
-        const int w = a.sn_col[J + 1] - c0;
-        const int64_t r0 = a.sn_rptr[J];
-        const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const int64_t cvo = a.cv_off[J];
-        const T* L = stage_panel(lval + a.sn_loff[J], r * w, slice, a.slice, &bars[wid], phase);
-        for (int q = 0; q < 2; ++q) {
-            if (!(q == 0 ? a.act0 : a.act1)) continue;
-            T* xJ = x + (int64_t)q * a.dim + c0;
-            T* vq = vin + (int64_t)q * a.nv;
-            T* cs = colsum[wid];
-            vgather_warp(vq, a.vcol_ptr, c0, w, cs, vwin[wid]);
-            if (a.trace && lane == 0) a.trace[6 * t + 2] = gtimer();
-            T x0 = (T)0, x1 = (T)0;
-            if (lane < w) x0 = xJ[lane] - cs[lane];
-            if (lane + 32 < w) x1 = xJ[lane + 32] - cs[lane + 32];
-            for (int j = 0; j < w; ++j) {
-                const T l0 = (lane > j && lane < w) ? L[j * r + lane] : (T)0;
-                const T l1 = (lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
+__device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* x, T* vin,
+                                            const T (&xa)[2], const T (&xb)[2], T (*cs)[64], int J) {
+    const int lane = threadIdx.x & 31;
+    const int c0 = d.c0, w = d.w, r = d.r;
+    for (int q = 0; q < 2; ++q) {
+        if (!(q == 0 ? a.act0 : a.act1)) continue;
+        T* xJ = x + (int64_t)q * a.dim + c0;
+        T* vq = vin + (int64_t)q * a.nv;
+        T x0 = (T)0, x1 = (T)0;
+        if (lane < w) x0 = xa[q] - cs[q][lane];
+        if (lane + 32 < w) x1 = xb[q] - cs[q][lane + 32];
+        for (int j0 = 0; j0 < w; j0 += 8) {
+            T l0[8], l1[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {           // issue the block's loads before the dependent chain
+                const int j = j0 + k;
+                l0[k] = (j < w && lane > j && lane < w) ? L[j * r + lane] : (T)0;
+                l1[k] = (j < w && lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int j = j0 + k;
+                if (j >= w) break;
                 const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-                x0 -= l0 * xj;
-                x1 -= l1 * xj;
+                x0 -= l0[k] * xj;
+                x1 -= l1[k] * xj;
             }
-            if (lane < w) xJ[lane] = x0;
-            if (lane + 32 < w) xJ[lane + 32] = x1;
-            if (a.trace && lane == 0) a.trace[6 * t + 3] = gtimer();
-            for (int i0 = w; i0 < r; i0 += 32) {
-                const int i = i0 + lane;
-                const bool ok = i < r;
-                const int ii = ok ? i : r - 1;
-                T acc = (T)0;
-                for (int k = 0; k < w; ++k) {
-                    const T xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-                    acc += L[k * r + ii] * xk;
-                }
-                if (ok) vq[a.vpush_pos[cvo + i - w]] = acc;
+        }
+        if (lane < w) xJ[lane] = x0;
+        if (lane + 32 < w) xJ[lane + 32] = x1;
+        if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
+        for (int i0 = w; i0 < r; i0 += 32) {
+            const int i = i0 + lane;
+            const bool ok = i < r;
+            const int ii = ok ? i : r - 1;
+            const int64_t pos = ok ? a.vpush_pos[d.cvo + i - w] : 0;
+            T acc = (T)0;
+#pragma unroll 8
+            for (int k = 0; k < w; ++k) {
+                const T xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+                acc += L[k * r + ii] * xk;
             }
-            if (a.trace && lane == 0) a.trace[6 * t + 4] = gtimer();
+            if (ok) vq[pos] = acc;
         }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-            const int P = a.sn_parent[J];
-            if (P >= 0) atomicAdd(a.count + P, 1);
-            if (a.trace) a.trace[6 * t + 5] = gtimer();
-        }
+        if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
     }
 }
 
-// backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
 template <typename T>
-__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T* __restrict__ lval,
-                                                           const T* __restrict__ dvec, T* x) {
-    extern __shared__ __align__(16) unsigned char sraw[];
-    __shared__ T xs[SW][2][64];
-    __shared__ uint64_t bars[SW];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
-    if (lane == 0) mbar_init(&bars[wid], 1);
-    __syncwarp();
-    uint32_t phase = 0;
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(a.ticket, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.nsuper) return;
-        const int J = a.order[a.nsuper - 1 - t];
-        const int P = a.sn_parent[J];
-        if (lane == 0 && P >= 0) wait_ge(a.count + P, 1);
-        __syncwarp();
-        const int c0 = a.sn_col[J];
-        const int w = a.sn_col[J + 1] - c0;
-        const int64_t r0 = a.sn_rptr[J];
-        const int r = (int)(a.sn_rptr[J + 1] - r0);
-        const int o = r - w;
-        const int32_t* rowsJ = a.sn_rows + r0 + w;
-        const T* L = stage_panel(lval + a.sn_loff[J], r * w, slice, a.slice, &bars[wid], phase);
+__device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
+                                         const int32_t* rowsJ, const T* __restrict__ dvec, T* x, T* xo) {
+    const int lane = threadIdx.x & 31;
         const T* L0 = L + lane * r;
         const T* L1 = L + (lane + 32) * r;
         const bool o0 = lane < w, o1 = lane + 32 < w;
@@ -560,13 +705,13 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T*
             T* xJ = xv + c0;
             T x0 = o0 ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
             T x1 = o1 ? xJ[lane + 32] / dvec[c0 + lane + 32] : (T)0;
-            // ancestors' values at the off rows: gathered once (coalesced over lanes)
+            // ancestors' values at the off rows, gathered 64 at a time (coalesced over lanes)
             for (int i0 = 0; i0 < o; i0 += 64) {
-                T* xo = xs[wid][0];
                 const int n = min(64, o - i0);
                 if (lane < n) xo[lane] = __ldcg(xv + rowsJ[i0 + lane]);
                 if (lane + 32 < n) xo[lane + 32] = __ldcg(xv + rowsJ[i0 + lane + 32]);
                 __syncwarp();
+#pragma unroll 8
                 for (int k = 0; k < n; ++k) {
                     const T xi = xo[k];
                     if (o0) x0 -= L0[w + i0 + k] * xi;
@@ -574,17 +719,286 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T*
                 }
                 __syncwarp();
             }
-            for (int j = w - 1; j >= 0; --j) {
-                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-                if (lane < j) x0 -= L0[j] * xj;
-                if (lane + 32 < j) x1 -= L1[j] * xj;
+            for (int j1 = w - 1; j1 >= 0; j1 -= 8) {
+                T l0[8], l1[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {           // loads first, then the dependent chain
+                    const int j = j1 - k;
+                    l0[k] = (j >= 0 && lane < j) ? L0[j] : (T)0;
+                    l1[k] = (j >= 0 && lane + 32 < j) ? L1[j] : (T)0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int j = j1 - k;
+                    if (j < 0) break;
+                    const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
+                    x0 -= l0[k] * xj;
+                    x1 -= l1[k] * xj;
+                }
             }
             if (o0) xJ[lane] = x0;
             if (o1) xJ[lane + 32] = x1;
         }
+}
+
+constexpr int SW = 8;   // warps per solve CTA
+
+// forward sweep L y = b: warp per supernode, columns in registers (lane owns
+// columns lane and lane+32; non-tail supernodes are narrower than 64), panel
+// staged in shared memory by one bulk copy, continuation to the parent
+// tiny leaf, forward: x_J = L11^-1 b_J (no inbox below a leaf), push L_off x_J
+template <typename T, int W>
+__device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+                                          T* x, T* vin) {
+    const int c0 = d32[0], r = d32[2], parent = d32[3];
+    const int64_t loff = a.desc64[(int64_t)J * 8], cvo = a.desc64[(int64_t)J * 8 + 1];
+    const T* L = lval + loff;
+    T p[W][16];
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[j][i] = (i < r && i > j) ? L[j * r + i] : (T)0;
+    const int needP = parent >= 0 ? a.need[2 * parent] : 0;
+    for (int q = 0; q < 2; ++q) {
+        if (!(q == 0 ? a.act0 : a.act1)) continue;
+        T* xJ = x + (int64_t)q * a.dim + c0;
+        T xv[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) xv[j] = xJ[j];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+#pragma unroll
+            for (int i = j + 1; i < W; ++i) xv[i] -= p[j][i] * xv[j];
+#pragma unroll
+        for (int j = 0; j < W; ++j) xJ[j] = xv[j];
+        T* vq = vin + (int64_t)q * a.nv;
+#pragma unroll
+        for (int i = W; i < 16; ++i) {
+            if (i >= r) break;
+            T acc = (T)0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc += p[k][i] * xv[k];
+            vq[a.vpush_pos[cvo + i - W]] = acc;
+        }
+    }
+    __threadfence();
+    if (parent < 0) return -1;
+    const int old = atomicAdd(a.count + parent, 1);
+    return old == needP - 1 ? parent : -1;
+}
+
+template <typename T>
+__device__ __forceinline__ int fwd_tiny_lane(int J, const SolveArgs& a, const T* __restrict__ lval, T* x, T* vin) {
+    const int32_t* d32 = a.desc32 + (int64_t)J * 8;
+    switch (d32[1]) {
+        case 1: return fwd_tiny_w<T, 1>(J, d32, a, lval, x, vin);
+        case 2: return fwd_tiny_w<T, 2>(J, d32, a, lval, x, vin);
+        case 3: return fwd_tiny_w<T, 3>(J, d32, a, lval, x, vin);
+        default: return fwd_tiny_w<T, 4>(J, d32, a, lval, x, vin);
+    }
+}
+
+// one forward task and its continuation chain
+template <typename T>
+__device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __restrict__ lval, T* x, T* vin,
+                                          T* slice, T (*cs)[64], uint64_t* bar, uint32_t& phase) {
+    const int lane = threadIdx.x & 31;
+    bool have_dn = false;
+    Desc dn;                       // descriptor of the parent, prefetched for a continuation
+    while (J >= 0) {
+        if (a.trace && lane == 0) a.trace[6 * J] = a.trace[6 * J + 1] = gtimer();
+        const Desc d = have_dn ? dn : load_desc(a.desc32, a.desc64, J);
+        const int w = d.w, r = d.r;
+        const T* Lg = lval + d.loff;
+        // 1. issue the panel's TMA bulk copy; it lands while the inputs are gathered
+        const uint32_t bytes = ((uint32_t)(r * w) * (uint32_t)sizeof(T) + 15u) & ~15u;
+        const bool staged = bytes <= (uint32_t)a.slice * (uint32_t)sizeof(T);
+        if (staged) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) bulk_g2s(slice, Lg, bytes, bar);
+        }
+        const int needP = (lane == 0 && d.parent >= 0) ? a.need[2 * d.parent] : 0;
+        dn = load_desc(a.desc32, a.desc64, d.parent >= 0 ? d.parent : J);
+        // 2. own right-hand-side values and the vector inbox of the supernode's columns
+        T xa[2] = {(T)0, (T)0}, xb[2] = {(T)0, (T)0};
+        for (int q = 0; q < 2; ++q) {
+            if (!(q == 0 ? a.act0 : a.act1)) continue;
+            const T* xJ = x + (int64_t)q * a.dim + d.c0;
+            xa[q] = lane < w ? xJ[lane] : (T)0;
+            xb[q] = lane + 32 < w ? xJ[lane + 32] : (T)0;
+            vgather_warp(vin + (int64_t)q * a.nv, a.vin_col, d.vlo, d.vhi, w, cs[q]);
+        }
+        if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
+        // 3. triangle + push, from shared memory when staged
+        if (staged) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            fwd_compute<T>(slice, a, d, x, vin, xa, xb, cs, J);
+        } else {
+            fwd_compute<T>(Lg, a, d, x, vin, xa, xb, cs, J);
+        }
+        __threadfence();
+        __syncwarp();
+        int cont = -1;
+        if (lane == 0) {
+            if (d.parent >= 0) {
+                const int old = atomicAdd(a.count + d.parent, 1);
+                if (old == needP - 1) cont = d.parent;
+            }
+            if (a.trace) a.trace[6 * J + 5] = gtimer();
+        }
+        J = __shfl_sync(0xffffffffu, cont, 0);
+        have_dn = true;
+        if (J >= 0) __threadfence();
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    __shared__ T colsum[SW][2][64];
+    __shared__ uint64_t bars[SW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
+    if (lane == 0) mbar_init(&bars[wid], 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    // phase 1: tiny leaves, one per lane; completed parents continue as warp tasks
+    for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if ((int64_t)chunk * 32 >= a.ntiny) break;
+        const int idx = chunk * 32 + lane;
+        const int J = idx < a.ntiny ? a.tiny[idx] : -1;
+        const int ready = J >= 0 ? fwd_tiny_lane(J, a, lval, x, vin) : -1;
+        unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
+        if (m) __threadfence();
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            fwd_chain(__shfl_sync(0xffffffffu, ready, l), a, lval, x, vin, slice, colsum[wid], &bars[wid], phase);
+        }
+    }
+    // phase 2: remaining seeds by ticket
+    for (;;) {
+        int J = -1;
+        if (lane == 0) {
+            const int t = atomicAdd(a.ticket, 1);
+            J = t < a.nstart ? a.start[t] : -1;
+        }
+        J = __shfl_sync(0xffffffffu, J, 0);
+        if (J < 0) return;
+        fwd_chain(J, a, lval, x, vin, slice, colsum[wid], &bars[wid], phase);
+    }
+}
+
+// backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
+// tiny leaf, backward: x_J = L11^-T (D^-1 x_J - L_off' x_off) once the parent is final
+template <typename T, int W>
+__device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+                                           const T* __restrict__ dvec, T* x) {
+    const int c0 = d32[0], r = d32[2], parent = d32[3];
+    const int64_t loff = a.desc64[(int64_t)J * 8], rptr = a.desc64[(int64_t)J * 8 + 7];
+    const T* L = lval + loff;
+    T p[W][16];
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) p[j][i] = (i < r && i > j) ? L[j * r + i] : (T)0;
+    int rows[16];
+#pragma unroll
+    for (int i = W; i < 16; ++i) rows[i] = i < r ? a.sn_rows[rptr + i] : 0;
+    T dinv[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) dinv[j] = dvec[c0 + j];
+    if (parent >= 0) {
+        while (ld_relaxed(a.count + parent) == 0) __nanosleep(32);
+        __threadfence();
+    }
+    for (int q = 0; q < 2; ++q) {
+        if (!(q == 0 ? a.act0 : a.act1)) continue;
+        T* xv = x + (int64_t)q * a.dim;
+        T xr[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) xr[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
+#pragma unroll
+        for (int i = W; i < 16; ++i) {
+            if (i >= r) break;
+            const T xi = __ldcg(xv + rows[i]);
+#pragma unroll
+            for (int j = 0; j < W; ++j) xr[j] -= p[j][i] * xi;
+        }
+#pragma unroll
+        for (int j = W - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = j + 1; i < W; ++i) xr[j] -= p[j][i] * xr[i];
+#pragma unroll
+        for (int j = 0; j < W; ++j) xv[c0 + j] = xr[j];
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T* __restrict__ lval,
+                                                           const T* __restrict__ dvec, T* x) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    __shared__ T xs[SW][64];
+    __shared__ uint64_t bars[SW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
+    if (lane == 0) mbar_init(&bars[wid], 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= a.n_main) break;
+        const int J = a.order[a.n_main - 1 - t];     // a.order = bwd_order here
+        const Desc d = load_desc(a.desc32, a.desc64, J);
+        const int c0 = d.c0, w = d.w, r = d.r;
+        const int o = r - w;
+        const int32_t* rowsJ = a.sn_rows + d.rptr + w;
+        const T* Lg = lval + d.loff;
+        // the panel is static: start its bulk copy before waiting for the parent
+        const uint32_t bytes = ((uint32_t)(r * w) * (uint32_t)sizeof(T) + 15u) & ~15u;
+        const bool staged = bytes <= (uint32_t)a.slice * (uint32_t)sizeof(T);
+        if (staged) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) bulk_g2s(slice, Lg, bytes, &bars[wid]);
+        }
+        if (lane == 0 && d.parent >= 0) wait_ge(a.count + d.parent, 1);
+        __syncwarp();
+        if (staged) {
+            mbar_wait(&bars[wid], phase);
+            phase ^= 1u;
+            bwd_body<T>(slice, a, c0, w, r, o, rowsJ, dvec, x, xs[wid]);
+        } else {
+            bwd_body<T>(Lg, a, c0, w, r, o, rowsJ, dvec, x, xs[wid]);
+        }
         __threadfence();
         __syncwarp();
         if (lane == 0) st_release(a.count + J, 1);
+    }
+    // phase 2: tiny leaves, one per lane (nobody waits on a leaf)
+    for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if ((int64_t)chunk * 32 >= a.ntiny) return;
+        const int idx = chunk * 32 + lane;
+        if (idx < a.ntiny) {
+            const int J = a.tiny[idx];
+            const int32_t* d32 = a.desc32 + (int64_t)J * 8;
+            switch (d32[1]) {
+                case 1: bwd_tiny_w<T, 1>(J, d32, a, lval, dvec, x); break;
+                case 2: bwd_tiny_w<T, 2>(J, d32, a, lval, dvec, x); break;
+                case 3: bwd_tiny_w<T, 3>(J, d32, a, lval, dvec, x); break;
+                default: bwd_tiny_w<T, 4>(J, d32, a, lval, dvec, x); break;
+            }
+        }
     }
 }
 
@@ -614,19 +1028,22 @@ __global__ void scatter_add_perm(double* __restrict__ x, const T* __restrict__ t
 
 SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1) {
     SolveArgs a;
-    a.nsuper = c.host_sym.n_main;
+    a.nstart = (int32_t)c.host_sym.start_solve.size();
+    a.start = c.sym.start_solve;
+    a.n_main = (int32_t)c.host_sym.bwd_order.size();
+    a.order = c.sym.bwd_order;
+    a.ntiny = (int32_t)c.host_sym.tiny.size();
+    a.tiny = c.sym.tiny;
+    a.ticket_tiny = nullptr;
+    a.bwd_done = nullptr;
+    a.desc32 = c.sym.desc32;
+    a.desc64 = c.sym.desc64;
+    a.need = c.sym.need;
     a.dim = c.dim;
     a.nv = c.sym.nv;
-    a.order = c.sym.order;
-    a.sn_col = c.sym.sn_col;
-    a.sn_rptr = c.sym.sn_rptr;
     a.sn_rows = c.sym.sn_rows;
-    a.sn_loff = c.sym.sn_loff;
-    a.sn_parent = c.sym.sn_parent;
-    a.sn_nchild = c.sym.sn_nchild;
-    a.cv_off = c.sym.cv_off;
     a.vpush_pos = c.sym.vpush_pos;
-    a.vcol_ptr = c.sym.vcol_ptr;
+    a.vin_col = c.sym.vin_col;
     a.count = count;
     a.ticket = ticket;
     a.act0 = act0;
@@ -655,49 +1072,49 @@ void build_base_t(Ctx& c) {
 template <typename T>
 int factor_t(Ctx& c) {
     FactorArgs a;
-    a.nsuper = c.host_sym.n_main;
-    a.order = c.sym.order;
-    a.sn_col = c.sym.sn_col;
-    a.sn_rptr = c.sym.sn_rptr;
-    a.sn_loff = c.sym.sn_loff;
-    a.sn_parent = c.sym.sn_parent;
-    a.sn_nchild = c.sym.sn_nchild;
-    a.cb_off = c.sym.cb_off;
+    a.desc32 = c.sym.desc32;
+    a.desc64 = c.sym.desc64;
+    a.need = c.sym.need;
     a.push_pos = c.sym.push_pos;
-    a.irow_ptr = c.sym.irow_ptr;
     a.inbox_tgt = c.sym.inbox_tgt;
+    a.irow_ptr = c.sym.irow_ptr;
     a.sign = c.sym.sign;
     a.count = c.fac_count;
-    a.ticket = c.tickets;
     a.maxd = c.sn_maxd;
     a.bumps = c.bumps;
     a.err = c.err;
     a.delta_s = c.delta_s;
     a.delta_d = c.delta_d;
-    a.smem_cap = c.factor_slice;
     a.trace = c.trace ? c.trace + 6 * (int64_t)c.sym.nsuper : nullptr;
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.sn_maxd, 0, sizeof(double) * c.sym.nsuper, c.stream);
-    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
+    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 8, c.stream);
     cudaMemsetAsync(c.bumps, 0, sizeof(int32_t), c.stream);
     int e0 = 0;
     if (c.profile) {
         e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
-    const int n_warp = c.host_sym.n_warp, n_main = c.host_sym.n_main;
-    if (n_warp > 0) {
-        a.t_begin = 0;
-        a.nsuper = n_warp;
+    const int ns_warp = (int)c.host_sym.start_fac_warp.size(), ns_cta = (int)c.host_sym.start_fac_cta.size();
+    const int ntiny = (int)c.host_sym.tiny.size();
+    if (ns_warp + ntiny > 0) {
+        a.tier = 0;
+        a.nstart = ns_warp;
+        a.start = c.sym.start_fac_warp;
+        a.ntiny = ntiny;
+        a.tiny = c.sym.tiny;
+        a.ticket_tiny = c.tickets + 4;
         a.ticket = c.tickets;
         a.smem_cap = c.factor_slice;
         factor_kernel<T><<<c.factor_blocks, FW * 32, c.factor_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec,
                                                                                 (T*)c.inbox);
         c.launches++;
     }
-    if (n_main > n_warp) {
-        a.t_begin = n_warp;
-        a.nsuper = n_main;
+    if (ns_cta > 0) {
+        a.ntiny = 0;
+        a.tier = 1;
+        a.nstart = ns_cta;
+        a.start = c.sym.start_fac_cta;
         a.ticket = c.tickets + 3;
         a.smem_cap = c.factor_cta_smem / (int64_t)sizeof(T);
         factor_cta_kernel<T><<<c.factor_cta_blocks, 256, c.factor_cta_smem, c.stream>>>(a, (T*)c.lval, (T*)c.dvec,
@@ -718,7 +1135,7 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1);
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
-    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 4, c.stream);
+    cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 8, c.stream);
     if (c.tflag_total) cudaMemsetAsync(c.tflags, 0, sizeof(int32_t) * c.tflag_total, c.stream);
     int e0 = 0;
     if (c.profile) {
@@ -726,13 +1143,15 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         cudaEventRecord(pooled_event(c, e0), c.stream);
     }
     SolveArgs f = solve_args(c, c.fac_count, c.tickets + 1, act0, act1);
+    f.ticket_tiny = c.tickets + 5;
     f.trace = c.trace;
     const size_t ssm = sizeof(T) * (size_t)c.solve_slice * SW;
-    if (f.nsuper > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    if (f.nstart + f.ntiny > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     k_tail_forward(c, t, act0, act1);
     k_tail_backward(c, t, act0, act1);
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
-    if (b.nsuper > 0)
+    b.ticket_tiny = c.tickets + 6;
+    if (b.n_main + b.ntiny > 0)
         backward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
@@ -782,7 +1201,7 @@ int factor_grid(Ctx& c) {
     // per-warp shared-memory panel slice: the largest non-tail panel, capped at
     // 6 KiB so four 8-warp CTAs fit per SM; bigger panels are factored in place
     const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
-    int64_t slice = std::min<int64_t>(c.host_sym.max_panel_warp, 6144 / es);
+    int64_t slice = std::min<int64_t>((c.host_sym.max_panel_warp + 3) & ~int64_t(3), 6144 / es);   // 16-byte multiple (TMA)
     if (slice < 64) slice = 64;
     c.factor_slice = slice;
     c.factor_smem = (int)(slice * es * FW);

@@ -577,6 +577,73 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         for (int64_t rl = 0; rl < bdim[b]; ++rl)
             for (int64_t cl = rl; cl < bdim[b]; ++cl)
                 S.map_hblk.push_back(pos(n + boff[b] + rl, n + boff[b] + cl));
+    // continuation scheduling (ldl.cu): per-supernode descriptors, same-tier child
+    // counts, start lists (supernodes without same-tier children), inbox column ids
+    {
+        const int32_t BIG = 0x3fffffff;
+        S.tier.assign(ns, 0);
+        for (int32_t J = 0; J < ns; ++J) S.tier[J] = S.is_tail[J] ? 2 : (S.is_mid[J] ? 1 : 0);
+        std::vector<int32_t> need_fac(ns, 0), need_solve(ns, 0);
+        for (int32_t J = 0; J < ns; ++J) {
+            const int32_t P = S.sn_parent[J];
+            if (P < 0) continue;
+            if (S.tier[P] != 2) need_solve[P]++;
+            if (S.tier[P] == S.tier[J] && S.tier[P] != 2) need_fac[P]++;
+        }
+        S.desc32.assign((size_t)ns * 8, 0);
+        S.desc64.assign((size_t)ns * 8, 0);
+        for (int32_t J = 0; J < ns; ++J) {
+            int32_t* d = &S.desc32[(size_t)J * 8];
+            d[0] = S.sn_col[J];
+            d[1] = S.sn_col[J + 1] - S.sn_col[J];
+            d[2] = (int32_t)(S.sn_rptr[J + 1] - S.sn_rptr[J]);
+            d[3] = S.sn_parent[J];
+            d[4] = S.tier[J] == 2 ? BIG : need_solve[J];
+            d[5] = S.tier[J] == 2 ? BIG : need_fac[J];
+            d[6] = S.tier[J];
+            int64_t* e = &S.desc64[(size_t)J * 8];
+            e[0] = S.sn_loff[J];
+            e[1] = S.cv_off[J];
+            e[2] = S.vcol_ptr[S.sn_col[J]];
+            e[3] = S.vcol_ptr[S.sn_col[J + 1]];
+            e[4] = S.irow_ptr[S.sn_rptr[J]];
+            e[5] = S.irow_ptr[S.sn_rptr[J + 1]];
+            e[6] = S.cb_off[J];
+            e[7] = S.sn_rptr[J];
+        }
+        S.need.assign((size_t)ns * 2, 0);
+        for (int32_t J = 0; J < ns; ++J) {
+            S.need[2 * (size_t)J] = S.desc32[(size_t)J * 8 + 4];
+            S.need[2 * (size_t)J + 1] = S.desc32[(size_t)J * 8 + 5];
+        }
+        // tiny leaves (no children, w <= 4, r <= 16) are processed one per lane
+        std::vector<char> tiny(ns, 0);
+        S.tiny.clear();
+        for (int32_t J = 0; J < ns; ++J) {
+            const int64_t w = S.sn_col[J + 1] - S.sn_col[J], r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+            if (S.tier[J] == 0 && S.sn_nchild[J] == 0 && w <= 4 && r <= 16) {
+                tiny[J] = 1;
+                S.tiny.push_back(J);
+            }
+        }
+        S.start_solve.clear();
+        S.start_fac_warp.clear();
+        S.start_fac_cta.clear();
+        for (int32_t J = 0; J < ns; ++J) {
+            if (S.tier[J] == 2 || tiny[J]) continue;
+            if (need_solve[J] == 0) S.start_solve.push_back(J);
+            if (need_fac[J] == 0) (S.tier[J] == 0 ? S.start_fac_warp : S.start_fac_cta).push_back(J);
+        }
+        // backward sweep order: non-tail, non-tiny supernodes, topological (children first)
+        S.bwd_order.clear();
+        for (int32_t k = 0; k < S.n_main; ++k)
+            if (!tiny[S.order[k]]) S.bwd_order.push_back(S.order[k]);
+        S.vin_col.assign((size_t)S.vcol_ptr[dim], 0);
+        for (int64_t j = 0; j < dim; ++j) {
+            const int32_t J = S.col2sn[j];
+            for (int64_t e = S.vcol_ptr[j]; e < S.vcol_ptr[j + 1]; ++e) S.vin_col[e] = (uint8_t)(j - S.sn_col[J]);
+        }
+    }
     (void)lin;
     return 0;
 }

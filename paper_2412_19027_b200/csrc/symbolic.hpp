@@ -70,6 +70,18 @@ struct Symbolic {
     int32_t n_warp = 0;                    // order[0 .. n_warp) are the warp-tier supernodes
     int64_t max_panel_main = 0;            // largest non-tail panel (shared-memory sizing)
     int64_t max_panel_warp = 0;            // largest warp-tier panel
+    // continuation scheduling: a task finishing supernode K increments its parent's
+    // same-tier counter; the task that completes it continues with the parent
+    std::vector<int8_t> tier;              // 0 warp, 1 CTA, 2 dense tail
+    std::vector<int32_t> desc32;           // 8 per supernode: c0, w, r, parent, need_solve, need_fac, tier, -
+    std::vector<int64_t> desc64;           // 8 per supernode: loff, cv_off, vlo, vhi, ilo, ihi, cb_off, rptr
+    std::vector<int32_t> need;             // 2 per supernode: need_solve, need_fac
+    std::vector<int32_t> start_solve;      // non-tail supernodes with no children (forward sweep seeds)
+    std::vector<int32_t> start_fac_warp;   // warp-tier supernodes with no warp-tier children
+    std::vector<int32_t> start_fac_cta;    // CTA-tier supernodes with no CTA-tier children
+    std::vector<uint8_t> vin_col;          // vector-inbox entry -> local column in its supernode
+    std::vector<int32_t> tiny;             // leaves with w <= 4, r <= 16: one lane each (factor, solves)
+    std::vector<int32_t> bwd_order;        // backward tickets (reversed): non-tail, non-tiny, topological
     // scatter maps into the panel value array (int64 positions)
     std::vector<int64_t> map_p;            // P CSR nnz; -1 for strictly-lower entries
     std::vector<int64_t> map_a;            // A CSR nnz (entry (n+r, j) of K stored at L(col j? ...))

@@ -69,11 +69,11 @@ def trace_main():
     ctx.call("cipm_factor")
     ctx.call("cipm_kkt_solve", pdbl(rhs), pdbl(x), ctypes.byref(steps), ctypes.byref(res))
     ns = s.symbolic.info()["nsuper"]
-    out = np.zeros(9 * ns, dtype=np.int64)
+    out = np.zeros(12 * ns, dtype=np.int64)
     ctx.call("cipm_trace", 0, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.savez(os.path.join(ROOT, "gpurun_out", f"trace_{cfg}.npz"), fwd=out[:6 * ns].reshape(ns, 6),
-             fac=out[6 * ns:].reshape(ns, 3),
+             fac=out[6 * ns:].reshape(ns, 6),
              order=s.symbolic.array("order"), sn_col=s.symbolic.array("sn_col"),
              sn_rptr=s.symbolic.array("sn_rptr"), sn_parent=s.symbolic.array("sn_parent"))
     print("trace written", ns)
