@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -79,8 +80,65 @@ int read_sc(Ctx& c) {
     return *c.h_err;
 }
 
-// refined solve of rb[q], q < nrhs; result in rbest[q]
+// refined solve of rb[q], q < nrhs; result in rbest[q] (kkt/system.py:279-314).
+// Default: the whole refinement loop (t_max steps) is one CUDA graph per
+// right-hand-side count; convergence / stall flags live on the device and the
+// kernels of a finished right-hand side return immediately, so the host reads
+// the state once at the end.  With profiling or tracing on, the eager loop
+// below runs instead (per-step host decisions, per-launch events).
+int refine_graph(Ctx& c, int nrhs, int* steps_out) {
+    if (!c.refine_graph[nrhs]) {
+        // graph = one WHILE conditional node; its body is one refinement step
+        // (solve + residual + controller for every right-hand side) followed by
+        // a 1-thread kernel that sets the loop condition from the device state
+        cudaGraph_t g = nullptr;
+        CIPM_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CIPM_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CIPM_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        const int64_t l0 = c.launches;
+        CIPM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        int active[2] = {1, nrhs > 1 ? 1 : 0};
+        k_refine_step(c, nrhs, active);
+        for (int q = 0; q < nrhs; ++q) k_kkt_residual_one(c, q);
+        k_refine_continue(c, h, nrhs);
+        cudaGraph_t captured = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c.stream, &captured);
+        if (e != cudaSuccess) {
+            fprintf(stderr, "[cipm] refinement graph capture failed: %s\n", cudaGetErrorString(e));
+            cudaGraphDestroy(g);
+            return CIPM_E_CUDA;
+        }
+        CIPM_CUDA(cudaGraphInstantiate(&c.refine_graph[nrhs], g, 0));
+        cudaGraphDestroy(g);
+        c.refine_graph_launches[nrhs] = c.launches - l0;
+        c.launches = l0;
+    }
+    for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
+    CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
+    c.d2h_bytes += sizeof(double) * 16 + sizeof(int);
+    CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (*c.h_err) return *c.h_err;
+    int steps = (int)c.h_rstate[6];
+    if (nrhs > 1) steps = std::max(steps, (int)c.h_rstate[14]);
+    c.launches += c.refine_graph_launches[nrhs] * steps;
+    if (steps_out) *steps_out = steps;
+    c.h_sc[CIPM_SC_REFINE_STEPS] = steps;
+    return CIPM_OK;
+}
+
 int refine(Ctx& c, int nrhs, int* steps_out) {
+    if (c.use_graphs && !c.profile && !c.trace) return refine_graph(c, nrhs, steps_out);
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
     int active[2] = {1, nrhs > 1 ? 1 : 0};
     int steps = 0;
@@ -254,6 +312,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     c.refine_abs = st->refine_abs;
     c.refine_rel = st->refine_rel;
     c.refine_max = st->refine_max;
+    if (const char* e = getenv("CIPM_NO_GRAPHS")) c.use_graphs = atoi(e) == 0;
     c.zero_dim = d->zero_dim;
     c.nonneg_dim = d->nonneg_dim;
     c.lin = d->zero_dim + d->nonneg_dim;
@@ -466,6 +525,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(dalloc(c, &c.fac_count, S.nsuper));
     TRY(dalloc(c, &c.bwd_done, S.nsuper));
     TRY(dalloc(c, &c.tickets, 8));
+    TRY(dalloc(c, &c.refine_iter, 1));
     TRY(dalloc(c, &c.sn_maxd, S.nsuper));
     TRY(dalloc(c, &c.bumps, 1));
     TRY(dalloc(c, &c.rb, 2 * c.dim));
@@ -528,6 +588,8 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     for (int i = 0; i < 4; ++i)
         if (c.ev[i]) cudaEventDestroy(c.ev[i]);
     for (auto e : c.ev_pool) cudaEventDestroy(e);
+    for (auto& g : c.refine_graph)
+        if (g) cudaGraphExecDestroy(g);
     if (c.t_start) cudaEventDestroy(c.t_start);
     if (c.t_stop) cudaEventDestroy(c.t_stop);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);

@@ -50,13 +50,24 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
     return v;
 }
 
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void wait_ge(const int* p, int need) {
     if (ld_relaxed(p) < need) {
         do {
             __nanosleep(32);
         } while (ld_relaxed(p) < need);
     }
-    __threadfence();
+    fence_acq_rel_gpu();
+}
+
+// counter increment that publishes this thread's (and, after a warp/CTA barrier,
+// its group's) earlier writes and acquires the writes published by earlier
+// increments — one RMW instead of fence + atomic + fence
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 // ---------------------------------------------------------------------------

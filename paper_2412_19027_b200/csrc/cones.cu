@@ -63,9 +63,9 @@ __global__ void blk_scatter(T* lval, const int64_t* map_hblk, const double* hv, 
 
 // out = alpha*u + beta*(H v) on zero + nonneg rows (H = 0 on zero rows)
 __global__ void nn_apply_h(const double* h, const double* v, double* out, double alpha, const double* u,
-                           double beta, int64_t zero_dim, int64_t lin) {
+                           double beta, int64_t zero_dim, int64_t lin, const double* skip) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= lin) return;
+    if (i >= lin || (skip && *skip != 0.0)) return;
     double hv = i < zero_dim ? 0.0 : h[i - zero_dim] * v[i];
     double base = u ? alpha * u[i] : 0.0;
     out[i] = base + beta * hv;
@@ -180,10 +180,10 @@ __global__ void soc_scaling(SocArgs a, const double* s, const double* z, double*
 
 // out = alpha*u + beta*H v on SOC rows
 __global__ void soc_apply_h(SocArgs a, const double* W, const double* ETA, const double* v, double* out,
-                            double alpha, const double* u, double beta) {
+                            double alpha, const double* u, double beta, const double* skip) {
     const int lane = threadIdx.x & 31;
     const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
+    if (c >= a.nsoc || (skip && *skip != 0.0)) return;
     const int off = a.off[c], d = a.dim[c];
     const double* w = W + (off - a.base);
     const double* vv = v + off;
@@ -425,9 +425,9 @@ __global__ void nsym_scaling(NsymArgs a, const double* s, const double* z, const
 }
 
 __global__ void nsym_apply_h(NsymArgs a, const double* H, const double* v, double* out, double alpha,
-                             const double* u, double beta) {
+                             const double* u, double beta, const double* skip) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.nsym) return;
+    if (c >= a.nsym || (skip && *skip != 0.0)) return;
     int off, kind;
     double al;
     nsym_cone(a, c, &off, &kind, &al);
@@ -578,9 +578,9 @@ __global__ void psd_scaling(PsdArgs a, const double* s, const double* z, double*
 
 template <int MS>
 __global__ void psd_apply_h(PsdArgs a, const double* Q, const double* v, double* out, double alpha,
-                            const double* u, double beta) {
+                            const double* u, double beta, const double* skip) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
+    if (c >= a.npsd || (skip && *skip != 0.0)) return;
     const int n = a.side[c], off = a.off[c];
     if (n > MS) return;
     double q[MS * MS], X[MS * MS], T[MS * MS], Y[MS * MS], hv[MS * (MS + 1) / 2];
@@ -770,21 +770,23 @@ void k_scatter_h(Ctx& c) {
     }
 }
 
-void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta) {
+void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta,
+               const double* skip) {
     if (c.lin) {
-        nn_apply_h<<<grid_for(c.lin), kThreads, 0, c.stream>>>(c.nn_h, v, out, alpha, u, beta, c.zero_dim, c.lin);
+        nn_apply_h<<<grid_for(c.lin), kThreads, 0, c.stream>>>(c.nn_h, v, out, alpha, u, beta, c.zero_dim, c.lin,
+                                                               skip);
         c.launches++;
     }
     if (c.nsoc) {
         soc_apply_h<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.soc_w, c.soc_eta, v, out, alpha, u,
-                                                                  beta);
+                                                                  beta, skip);
         c.launches++;
     }
     if (c.nsym) {
-        nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta);
+        nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta, skip);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_apply_h, psd_args(c), c.psd_q, v, out, alpha, u, beta);
+    if (c.npsd) PSD_DISPATCH(psd_apply_h, psd_args(c), c.psd_q, v, out, alpha, u, beta, skip);
 }
 
 void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a) {

@@ -168,7 +168,12 @@ struct Ctx {
     cudaEvent_t t_start = nullptr, t_stop = nullptr;
     float factor_ms = 0.f, solve_ms = 0.f;
 
-    int64_t* trace = nullptr;        // cipm_trace: [forward | factor] x nsuper x 3 timestamps
+    int64_t* trace = nullptr;        // cipm_trace: per-supernode timelines
+    // refinement as one CUDA graph per right-hand-side count (device-side convergence flags)
+    cudaGraphExec_t refine_graph[3] = {nullptr, nullptr, nullptr};
+    int64_t refine_graph_launches[3] = {0, 0, 0};
+    int* refine_iter = nullptr;      // steps taken by the graph-driven refinement loop
+    bool use_graphs = true;
 
     std::vector<void*> allocations;
 };
@@ -196,10 +201,12 @@ void k_step_init(Ctx& c, int which);         // α bound from τ/κ
 void k_step_finish(Ctx& c, int which);       // α check + σ
 void k_kkt_residual(Ctx& c, int nrhs, const int* active_host);
 void k_mu_candidates(Ctx& c, int k0, int nk);
+void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs);
 // cones.cu
 void k_update_scaling(Ctx& c);
 void k_scatter_h(Ctx& c);
-void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta);
+void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta,
+               const double* skip = nullptr);
 void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a);
 void k_step_bound(Ctx& c, const double* dz, const double* ds);
 void k_nsym_feasible_mask(Ctx& c, const double* dz, const double* ds, int k0);

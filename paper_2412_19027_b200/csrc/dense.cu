@@ -324,12 +324,19 @@ struct TailSolveArgs {
     int* ticket;
     int* done;                 // backward: solve-done flag of the supernode (persistent-kernel protocol)
     int act0, act1;
+    const double* rstate;      // refinement state: skip converged right-hand sides
 };
 
 // forward: CTA per row block (diag blocks 0..nbd-1, then off-row blocks)
 template <typename T>
-__global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a, const T* __restrict__ L, const T* __restrict__ inv,
+__global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
                                                 T* x, T* vin) {
+    TailSolveArgs a = a0;
+    if (a.rstate) {
+        a.act0 = a.act0 && a.rstate[4] == 0.0;
+        a.act1 = a.act1 && a.rstate[12] == 0.0;
+    }
+    if (!a.act0 && !a.act1) return;
     __shared__ int s_b;
     __shared__ T acc[2][TB];
     __shared__ T xs[2][TB];
@@ -411,8 +418,14 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a, const T* __rest
 
 // backward: CTA per column block, last block first
 template <typename T>
-__global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a, const T* __restrict__ L, const T* __restrict__ inv,
+__global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
                                                 const T* __restrict__ dvec, T* x) {
+    TailSolveArgs a = a0;
+    if (a.rstate) {
+        a.act0 = a.act0 && a.rstate[4] == 0.0;
+        a.act1 = a.act1 && a.rstate[12] == 0.0;
+    }
+    if (!a.act0 && !a.act1) return;
     __shared__ int s_b;
     __shared__ T acc[2][TB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -558,6 +571,7 @@ TailSolveArgs tail_args(Ctx& c, const TailNode& t, int which, int act0, int act1
     a.done = c.bwd_done + t.J;
     a.act0 = act0;
     a.act1 = act1;
+    a.rstate = c.rstate;
     return a;
 }
 

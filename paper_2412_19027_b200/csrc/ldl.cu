@@ -39,6 +39,14 @@ __device__ __forceinline__ int64_t gtimer() {
     return t;
 }
 
+// device-side refinement state: a right-hand side is active while its done flag is 0
+__device__ __forceinline__ void resolve_act(const double* rstate, int& act0, int& act1) {
+    if (rstate) {
+        act0 = act0 && rstate[4] == 0.0;
+        act1 = act1 && rstate[12] == 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // base image / assembly
 // ---------------------------------------------------------------------------
@@ -70,10 +78,7 @@ struct Desc {
     int64_t loff, cvo, vlo, vhi, ilo, ihi, cb, rptr;
 };
 
-__device__ __forceinline__ Desc load_desc(const int32_t* __restrict__ d32, const int64_t* __restrict__ d64, int J) {
-    const int lane = threadIdx.x & 31;
-    const int v32 = lane < 8 ? __ldg(d32 + (int64_t)J * 8 + lane) : 0;
-    const int64_t v64 = (lane >= 8 && lane < 16) ? __ldg(d64 + (int64_t)J * 8 + (lane - 8)) : 0;
+__device__ __forceinline__ Desc desc_from_regs(int v32, int64_t v64) {
     Desc d;
     d.c0 = __shfl_sync(0xffffffffu, v32, 0);
     d.w = __shfl_sync(0xffffffffu, v32, 1);
@@ -89,6 +94,13 @@ __device__ __forceinline__ Desc load_desc(const int32_t* __restrict__ d32, const
     d.cb = __shfl_sync(0xffffffffu, v64, 14);
     d.rptr = __shfl_sync(0xffffffffu, v64, 15);
     return d;
+}
+
+__device__ __forceinline__ Desc load_desc(const int32_t* __restrict__ d32, const int64_t* __restrict__ d64, int J) {
+    const int lane = threadIdx.x & 31;
+    const int v32 = lane < 8 ? __ldg(d32 + (int64_t)J * 8 + lane) : 0;
+    const int64_t v64 = (lane >= 8 && lane < 16) ? __ldg(d64 + (int64_t)J * 8 + (lane - 8)) : 0;
+    return desc_from_regs(v32, v64);
 }
 
 __device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
@@ -313,12 +325,10 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
         }
         tb += o - b;
     }
-    __threadfence();
     if (parent < 0) return -1;
     atomic_max_pos(a.maxd + parent, runmax);
     if (a.desc32[(int64_t)parent * 8 + 6] != 0) return -1;     // parent factored by another tier
-    __threadfence();
-    const int old = atomicAdd(a.count + parent, 1);
+    const int old = atomic_add_acq_rel(a.count + parent, 1);
     return old == a.need[2 * parent + 1] - 1 ? parent : -1;
 }
 
@@ -361,22 +371,20 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
         if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
         if (P != L) warp_task_body(sp, L, true, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
         else warp_task_body(L, L, false, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
-        __threadfence();
         __syncwarp();
         int cont = -1;
         if (lane == 0) {
             if (d.parent >= 0) {
                 atomic_max_pos(a.maxd + d.parent, runmax);
                 if (tierP == a.tier) {
-                    __threadfence();
-                    const int old = atomicAdd(a.count + d.parent, 1);
+                    const int old = atomic_add_acq_rel(a.count + d.parent, 1);
                     if (old == needP - 1) cont = d.parent;
                 }
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
         }
         J = __shfl_sync(0xffffffffu, cont, 0);
-        if (J >= 0) __threadfence();
+        __syncwarp();
     }
 }
 
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
         const int J = idx < a.ntiny ? a.tiny[idx] : -1;
         const int ready = J >= 0 ? factor_tiny_lane(J, a, lval, dvec, inbox) : -1;
         unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
-        if (m) __threadfence();
+        __syncwarp();
         while (m) {
             const int l = __ffs(m) - 1;
             m &= m - 1;
@@ -555,20 +563,17 @@ __global__ void __launch_bounds__(256) factor_cta_kernel(FactorArgs a, T* __rest
             if (in_smem) cta_push(sp, r, w, o, s_d64[6], sD, a, inbox);
             else cta_push(L, r, w, o, s_d64[6], sD, a, inbox);
         }
-        __threadfence();
         __syncthreads();
         if (tid == 0) {
             int cont = -1;
             if (parent >= 0) {
                 atomic_max_pos(a.maxd + parent, s_runmax);
                 if (s_tierP == a.tier) {
-                    __threadfence();
-                    const int old = atomicAdd(a.count + parent, 1);
+                    const int old = atomic_add_acq_rel(a.count + parent, 1);
                     if (old == s_needP - 1) cont = parent;
                 }
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
-            if (cont >= 0) __threadfence();
             s_next = cont;
         }
         __syncthreads();
@@ -601,6 +606,7 @@ struct SolveArgs {
     int act0, act1;      // active right-hand sides
     int64_t* trace;      // optional per-task timeline (cipm_trace)
     int slice;           // per-warp shared-memory panel slice (elements)
+    const double* rstate;   // refinement state: skip right-hand sides that have converged
 };
 
 // warp-cooperative sums of the vector inbox of one supernode's columns (entries
@@ -781,9 +787,8 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
             vq[a.vpush_pos[cvo + i - W]] = acc;
         }
     }
-    __threadfence();
     if (parent < 0) return -1;
-    const int old = atomicAdd(a.count + parent, 1);
+    const int old = atomic_add_acq_rel(a.count + parent, 1);
     return old == needP - 1 ? parent : -1;
 }
 
@@ -819,7 +824,10 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
             if (lane == 0) bulk_g2s(slice, Lg, bytes, bar);
         }
         const int needP = (lane == 0 && d.parent >= 0) ? a.need[2 * d.parent] : 0;
-        dn = load_desc(a.desc32, a.desc64, d.parent >= 0 ? d.parent : J);
+        // parent descriptor: raw loads now, shuffled after the compute (off the critical path)
+        const int Jn = d.parent >= 0 ? d.parent : J;
+        const int pv32 = lane < 8 ? __ldg(a.desc32 + (int64_t)Jn * 8 + lane) : 0;
+        const int64_t pv64 = (lane >= 8 && lane < 16) ? __ldg(a.desc64 + (int64_t)Jn * 8 + (lane - 8)) : 0;
         // 2. own right-hand-side values and the vector inbox of the supernode's columns
         T xa[2] = {(T)0, (T)0}, xb[2] = {(T)0, (T)0};
         for (int q = 0; q < 2; ++q) {
@@ -838,24 +846,27 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         } else {
             fwd_compute<T>(Lg, a, d, x, vin, xa, xb, cs, J);
         }
-        __threadfence();
+        dn = desc_from_regs(pv32, pv64);
         __syncwarp();
         int cont = -1;
         if (lane == 0) {
             if (d.parent >= 0) {
-                const int old = atomicAdd(a.count + d.parent, 1);
+                const int old = atomic_add_acq_rel(a.count + d.parent, 1);
                 if (old == needP - 1) cont = d.parent;
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
         }
         J = __shfl_sync(0xffffffffu, cont, 0);
         have_dn = true;
-        if (J >= 0) __threadfence();
+        __syncwarp();
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a, const T* __restrict__ lval, T* x, T* vin) {
+__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
+    SolveArgs a = a0;
+    resolve_act(a.rstate, a.act0, a.act1);
+    if (!a.act0 && !a.act1) return;
     extern __shared__ __align__(16) unsigned char sraw[];
     __shared__ T colsum[SW][2][64];
     __shared__ uint64_t bars[SW];
@@ -874,7 +885,7 @@ __global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a, const T* 
         const int J = idx < a.ntiny ? a.tiny[idx] : -1;
         const int ready = J >= 0 ? fwd_tiny_lane(J, a, lval, x, vin) : -1;
         unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
-        if (m) __threadfence();
+        __syncwarp();
         while (m) {
             const int l = __ffs(m) - 1;
             m &= m - 1;
@@ -913,10 +924,7 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
     T dinv[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) dinv[j] = dvec[c0 + j];
-    if (parent >= 0) {
-        while (ld_relaxed(a.count + parent) == 0) __nanosleep(32);
-        __threadfence();
-    }
+    if (parent >= 0) wait_ge(a.count + parent, 1);
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xv = x + (int64_t)q * a.dim;
@@ -940,8 +948,11 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T* __restrict__ lval,
+__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a0, const T* __restrict__ lval,
                                                            const T* __restrict__ dvec, T* x) {
+    SolveArgs a = a0;
+    resolve_act(a.rstate, a.act0, a.act1);
+    if (!a.act0 && !a.act1) return;
     extern __shared__ __align__(16) unsigned char sraw[];
     __shared__ T xs[SW][64];
     __shared__ uint64_t bars[SW];
@@ -978,7 +989,6 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T*
         } else {
             bwd_body<T>(Lg, a, c0, w, r, o, rowsJ, dvec, x, xs[wid]);
         }
-        __threadfence();
         __syncwarp();
         if (lane == 0) st_release(a.count + J, 1);
     }
@@ -1008,8 +1018,9 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a, const T*
 
 template <typename T>
 __global__ void gather_perm(const double* __restrict__ r, T* __restrict__ t, const int32_t* __restrict__ perm,
-                            int64_t dim, int act0, int act1) {
+                            int64_t dim, int act0, int act1, const double* rstate) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    resolve_act(rstate, act0, act1);
     if (k >= dim) return;
     const int32_t p = perm[k];
     if (act0) t[k] = (T)r[p];
@@ -1018,8 +1029,9 @@ __global__ void gather_perm(const double* __restrict__ r, T* __restrict__ t, con
 
 template <typename T>
 __global__ void scatter_add_perm(double* __restrict__ x, const T* __restrict__ t, const int32_t* __restrict__ perm,
-                                 int64_t dim, int act0, int act1) {
+                                 int64_t dim, int act0, int act1, const double* rstate) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    resolve_act(rstate, act0, act1);
     if (k >= dim) return;
     const int32_t p = perm[k];
     if (act0) x[p] = x[p] + (double)t[k];
@@ -1050,6 +1062,7 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.act1 = act1;
     a.trace = nullptr;
     a.slice = (int)c.solve_slice;
+    a.rstate = c.rstate;
     return a;
 }
 
@@ -1132,7 +1145,7 @@ int factor_t(Ctx& c) {
 template <typename T>
 void refine_solve_t(Ctx& c, int act0, int act1) {
     T* t = (T*)c.rt;
-    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1);
+    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1, c.rstate);
     cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 8, c.stream);
@@ -1157,7 +1170,8 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_solve.emplace_back(e0, e0 + 1);
     }
-    scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1);
+    scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1,
+                                                                    c.rstate);
     c.launches += 4;
 }
 

@@ -412,23 +412,24 @@ __global__ void take_step_scalars(double* sc, double scale, int* err) {
 // r1 = b1 - (P x1 + A' x2)
 __global__ void kkt_res_n(const int64_t* prp, const int64_t* pci, const double* pv, const int64_t* atrp,
                           const int64_t* atci, const double* atv, const double* xv, const double* bv, double* rv,
-                          int64_t n) {
+                          int64_t n, const double* st) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || st[4] != 0.0) return;
     const double kx = csr_row(prp, pci, pv, xv, i) + csr_row(atrp, atci, atv, xv + n, i);
     rv[i] = bv[i] - kx;
 }
 
 // t2 = b2 - A x1   (H x2 is added by the cone kernels)
 __global__ void kkt_res_m(const int64_t* arp, const int64_t* aci, const double* av, const double* xv,
-                          const double* bv, double* rv, int64_t n, int64_t m) {
+                          const double* bv, double* rv, int64_t n, int64_t m, const double* st) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= m) return;
+    if (i >= m || st[4] != 0.0) return;
     rv[n + i] = bv[n + i] - csr_row(arp, aci, av, xv, i);
 }
 
 // ‖r‖∞ and the refinement controller of system.py:298-314 for one rhs
 __global__ void refine_control(const double* rv, int64_t dim, double* st, double* partials, unsigned int* counter) {
+    if (st[4] != 0.0) return;      // this right-hand side already finished (graph-driven refinement)
     double v[1] = {0.0};
     const int ops[1] = {RED_MAX};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
@@ -452,8 +453,16 @@ __global__ void refine_control(const double* rv, int64_t dim, double* st, double
     }
 }
 
+// loop condition of the graph-driven refinement: continue while a right-hand side
+// is active and fewer than t_max steps were taken
+__global__ void refine_continue(cudaGraphConditionalHandle h, const double* st, int nrhs, int* iter, int max_steps) {
+    const int it = ++(*iter);
+    const bool any = st[4] == 0.0 || (nrhs > 1 && st[12] == 0.0);
+    cudaGraphSetConditional(h, (any && it < max_steps) ? 1u : 0u);
+}
+
 __global__ void copy_if_improved(const double* src, double* dst, const double* st, int64_t n) {
-    if (st[5] == 0.0) return;
+    if (st[5] == 0.0) return;      // cleared by refine_control on every active step
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[i];
 }
@@ -597,15 +606,21 @@ void k_kkt_residual_one(Ctx& c, int q) {
     const double* xv = c.rx + (int64_t)q * c.dim;
     const double* bv = c.rb + (int64_t)q * c.dim;
     double* rv = c.rr + (int64_t)q * c.dim;
+    const double* st = c.rstate + 8 * q;
     kkt_res_n<<<grid_for(c.n), kThreads, 0, c.stream>>>(c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, xv, bv, rv,
-                                                        c.n);
-    kkt_res_m<<<grid_for(c.m), kThreads, 0, c.stream>>>(c.a_rp, c.a_ci, c.a_v, xv, bv, rv, c.n, c.m);
+                                                        c.n, st);
+    kkt_res_m<<<grid_for(c.m), kThreads, 0, c.stream>>>(c.a_rp, c.a_ci, c.a_v, xv, bv, rv, c.n, c.m, st);
     c.launches += 2;
-    k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0);
+    k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0, st + 4);
     refine_control<<<red_grid(c.dim), kThreads, 0, c.stream>>>(rv, c.dim, c.rstate + 8 * q, c.partials, c.counter);
     copy_if_improved<<<grid_for(c.dim), kThreads, 0, c.stream>>>(xv, c.rbest + (int64_t)q * c.dim, c.rstate + 8 * q,
                                                                  c.dim);
     c.launches += 2;
+}
+
+void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs) {
+    refine_continue<<<1, 1, 0, c.stream>>>(h, c.rstate, nrhs, c.refine_iter, c.refine_max);
+    c.launches++;
 }
 
 void k_refine_init_one(Ctx& c, int q) {
