@@ -590,6 +590,7 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     for (auto e : c.ev_pool) cudaEventDestroy(e);
     for (auto& g : c.refine_graph)
         if (g) cudaGraphExecDestroy(g);
+    if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
     if (c.t_start) cudaEventDestroy(c.t_start);
     if (c.t_stop) cudaEventDestroy(c.t_stop);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
@@ -637,8 +638,27 @@ int cipm_update_scaling(cipm_ctx* h) {
 
 int cipm_factor(cipm_ctx* h) {
     Ctx& c = h->c;
-    k_assemble(c);
-    return k_factor(c);
+    // the whole factorisation (assembly, persistent tiers, dense tail) is a static
+    // launch sequence: after one eager run it is captured once and replayed as a graph
+    if (!c.use_graphs || c.profile || c.trace || c.factor_runs++ == 0) {
+        k_assemble(c);
+        return k_factor(c);
+    }
+    if (!c.factor_graph) {
+        cudaGraph_t g = nullptr;
+        const int64_t l0 = c.launches;
+        CIPM_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        k_assemble(c);
+        k_factor(c);
+        CIPM_CUDA(cudaStreamEndCapture(c.stream, &g));
+        CIPM_CUDA(cudaGraphInstantiate(&c.factor_graph, g, 0));
+        cudaGraphDestroy(g);
+        c.factor_graph_launches = c.launches - l0;
+        c.launches = l0;
+    }
+    CIPM_CUDA(cudaGraphLaunch(c.factor_graph, c.stream));
+    c.launches += c.factor_graph_launches;
+    return CIPM_OK;
 }
 
 int cipm_solve_affine(cipm_ctx* h, int* steps) {

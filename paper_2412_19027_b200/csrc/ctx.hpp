@@ -173,6 +173,9 @@ struct Ctx {
     cudaGraphExec_t refine_graph[3] = {nullptr, nullptr, nullptr};
     int64_t refine_graph_launches[3] = {0, 0, 0};
     int* refine_iter = nullptr;      // steps taken by the graph-driven refinement loop
+    cudaGraphExec_t factor_graph = nullptr;
+    int64_t factor_graph_launches = 0;
+    int64_t factor_runs = 0;
     bool use_graphs = true;
 
     std::vector<void*> allocations;

@@ -11,11 +11,11 @@
 //   tail_gather   inbox -> panel (warp per row, fixed-order segmented sums)
 //   for each 64-column block kb:
 //     tail_diag   64x64 diagonal block: unblocked LDL' with the reference's
-//                 dynamic-regularisation rule (ldl.py:79-87), one CTA
-//     tail_trsm   rows below: L21 = A21 L11^-T D^-1 (thread per row)
+//                 dynamic-regularisation rule (ldl.py:79-87), one CTA, and the
+//                 explicit inverse of its unit-lower factor
+//     tail_gemm   rows below: L21 = A21 L11^-T D^-1 as a GEMM with that inverse
 //     tail_gemm   trailing panel columns -= L21 D L21'   (FP64: DMMA
 //                 mma.sync.m8n8k4 tensor-core tiles; FP32: FFMA tiles)
-//   tail_inv      explicit inverses of the unit-lower diagonal blocks (solves)
 //   tail_gemm     contribution block C = L_off D L_off' pushed to the ancestors'
 //                 inboxes (same GEMM, scatter epilogue)
 //
@@ -83,97 +83,166 @@ __global__ void __launch_bounds__(256) tail_gather(T* __restrict__ L, int r, con
 }
 
 // ---------------------------------------------------------------------------
-// diagonal block: unblocked LDL' of the nb x nb block at (kb, kb)
+// diagonal block: unblocked LDL' of the nb x nb block at (kb, kb), right-looking
+// on the unscaled columns (one barrier per column, pivots with the reference's
+// bump rule computed by every thread), then the explicit inverse of the unit
+// lower factor — row-major for the solves, column-major as the B operand of the
+// TRSM-as-GEMM (L21 = A21 L11^-T D^-1).
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int kb, int nb, int c0,
                                                  T* __restrict__ dvec, const int8_t* __restrict__ sign,
                                                  double* maxd, int32_t* bumps, int* err, double delta_s,
-                                                 double delta_d) {
-    __shared__ T S[TB][TB + 1];      // S[i][j], i >= j
-    __shared__ double s_piv, s_runmax;
-    const int tid = threadIdx.x, nt = blockDim.x;
+                                                 double delta_d, T* __restrict__ inv_rm, T* __restrict__ inv_cm) {
+    // blocked in 16-column sub-panels: (a) one warp factors the 16x16 sub-diagonal
+    // block with its rows in registers, (b) one thread per row below solves
+    // against it, (c) all threads apply the rank-16 update; 2 barriers per sub-panel
+    constexpr int SB = 16;
+    constexpr int LD = TB + 1;
+    extern __shared__ __align__(16) unsigned char dsm_raw[];
+    T* S = reinterpret_cast<T*>(dsm_raw);          // S[i * LD + j], i >= j
+    T* I = S + TB * LD;                            // inverse, I[i * LD + j]
+    __shared__ T sD[TB];
+    __shared__ int8_t sSg[TB];
+    __shared__ double s_runmax;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
     T* B = L + (int64_t)kb * r + kb;
     for (int idx = tid; idx < nb * nb; idx += nt) {
         const int i = idx % nb, j = idx / nb;
-        if (i >= j) S[i][j] = B[(int64_t)j * r + i];
+        if (i >= j) S[i * LD + j] = B[(int64_t)j * r + i];
     }
+    if (tid < nb) sSg[tid] = sign[c0 + kb + tid];
     if (tid == 0) s_runmax = *maxd;
     __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-        if (tid == 0) {
-            double d = (double)S[j][j];
-            const double bound = delta_s + delta_d * s_runmax;
-            if (fabs(d) < bound) {
-                d = sign[c0 + kb + j] > 0 ? bound : -bound;
-                atomicAdd(bumps, 1);
+    for (int k0 = 0; k0 < nb; k0 += SB) {
+        const int nbk = min(SB, nb - k0);
+        // (a) sub-diagonal block, lanes 0..15 own rows k0 + lane (unscaled right-looking)
+        if (wid == 0) {
+            double runmax = s_runmax;
+            T row[SB];
+#pragma unroll
+            for (int c = 0; c < SB; ++c)
+                row[c] = (lane < nbk && c <= lane && c < nbk) ? S[(k0 + lane) * LD + k0 + c] : (T)0;
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                if (j >= nbk) break;
+                double dd = (double)__shfl_sync(0xffffffffu, row[j], j);
+                const double bound = delta_s + delta_d * runmax;
+                const bool bump = fabs(dd) < bound;
+                if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
+                const T dt = (T)dd;
+                runmax = fmax(runmax, fabs(dd));
+                if (lane == 0) {
+                    if (bump) atomicAdd(bumps, 1);
+                    if (dt == (T)0) set_error(err, CIPM_E_FACTOR);
+                    sD[k0 + j] = dt;
+                    dvec[c0 + kb + k0 + j] = dt;
+                }
+                const T inv_d = (T)1 / dt;
+                const T lij = row[j] * inv_d;           // l_ij (valid on lanes i > j)
+#pragma unroll
+                for (int c = j + 1; c < SB; ++c) {
+                    const T acj = __shfl_sync(0xffffffffu, row[j], c);   // unscaled A(c, j)
+                    if (lane >= c) row[c] -= lij * acj;
+                }
+                if (lane > j) row[j] = lij;
+                else if (lane == j) row[j] = (T)1;
             }
-            const T dt = (T)d;
-            if (dt == (T)0) set_error(err, CIPM_E_FACTOR);
-            dvec[c0 + kb + j] = dt;
-            S[j][j] = (T)1;
-            s_piv = (double)dt;
-            s_runmax = fmax(s_runmax, fabs(d));
+#pragma unroll
+            for (int c = 0; c < SB; ++c)
+                if (lane < nbk && c <= lane && c < nbk) S[(k0 + lane) * LD + k0 + c] = row[c];
+            if (lane == 0) s_runmax = runmax;
         }
         __syncthreads();
-        const T d = (T)s_piv;
-        for (int i = j + 1 + tid; i < nb; i += nt) S[i][j] = S[i][j] / d;
-        __syncthreads();
-        const int rem = nb - j - 1;
-        const int tot = rem * rem;
-        for (int idx = tid; idx < tot; idx += nt) {
-            const int i = j + 1 + idx % rem, c = j + 1 + idx / rem;
-            if (i >= c) S[i][c] -= S[i][j] * d * S[c][j];
+        const int rest = nb - k0 - nbk;
+        if (rest > 0) {
+            // (b) rows below the sub-panel: l_ij = (a_ij - sum_{k<j} l_ik d_k l_jk) / d_j
+            for (int i = k0 + nbk + tid; i < nb; i += nt) {
+                T* Si = S + i * LD + k0;
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                    if (j >= nbk) break;
+                    T v = Si[j];
+                    const T* Sj = S + (k0 + j) * LD + k0;
+#pragma unroll
+                    for (int k = 0; k < j; ++k) v -= Si[k] * sD[k0 + k] * Sj[k];
+                    Si[j] = v / sD[k0 + j];
+                }
+            }
+            __syncthreads();
+            // (c) rank-nbk update of the trailing block: A(i,c) -= sum_k l_ik d_k l_ck
+            const int c1 = k0 + nbk;
+            const int tot = rest * rest;
+            for (int idx = tid; idx < tot; idx += nt) {
+                const int i = c1 + idx % rest, c = c1 + idx / rest;
+                if (i < c) continue;
+                const T* Si = S + i * LD + k0;
+                const T* Sc = S + c * LD + k0;
+                T acc = (T)0;
+#pragma unroll
+                for (int k = 0; k < SB; ++k)
+                    if (k < nbk) acc += Si[k] * sD[k0 + k] * Sc[k];
+                S[i * LD + c] -= acc;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     for (int idx = tid; idx < nb * nb; idx += nt) {
         const int i = idx % nb, j = idx / nb;
-        if (i >= j) B[(int64_t)j * r + i] = S[i][j];
+        if (i >= j) B[(int64_t)j * r + i] = S[i * LD + j];
+    }
+    // inverse of the unit lower block by recursive doubling (padded to 64 with the identity):
+    // 16x16 diagonal blocks by 4 warps, then [A 0; C B]^-1 = [Ai 0; -Bi C Ai Bi] for 16 and 32
+    T* Tm = I + TB * LD;                            // 32 x (32+1) scratch
+    auto Lp = [&](int i, int j) -> T {
+        if (i < nb && j < nb) return i > j ? S[i * LD + j] : (i == j ? (T)1 : (T)0);
+        return i == j ? (T)1 : (T)0;
+    };
+    for (int idx = tid; idx < TB * LD; idx += nt) I[idx] = (T)0;
+    __syncthreads();
+    if (wid < TB / SB && lane < SB) {
+        const int bb = wid * SB, col = bb + lane;
+        I[col * LD + col] = (T)1;
+        for (int i = lane + 1; i < SB; ++i) {
+            T v = (T)0;
+            for (int k = lane; k < i; ++k) v -= Lp(bb + i, bb + k) * I[(bb + k) * LD + col];
+            I[(bb + i) * LD + col] = v;
+        }
+    }
+    __syncthreads();
+    for (int sz = SB; sz < TB; sz *= 2) {
+        const int npair = TB / (2 * sz);
+        // Tm = C * Ai for every pair (C = L[bb+sz.., bb..], Ai = I[bb.., bb..])
+        for (int idx = tid; idx < npair * sz * sz; idx += nt) {
+            const int pr = idx / (sz * sz), e = idx % (sz * sz), i = e / sz, j = e % sz;
+            const int bb = pr * 2 * sz;
+            T acc = (T)0;
+            for (int k = j; k < sz; ++k) acc += Lp(bb + sz + i, bb + k) * I[(bb + k) * LD + bb + j];
+            Tm[(pr * sz + i) * (TB / 2 + 1) + j] = acc;
+        }
+        __syncthreads();
+        // lower-left block = -Bi * Tm (Bi = I[bb+sz.., bb+sz..], unit lower)
+        for (int idx = tid; idx < npair * sz * sz; idx += nt) {
+            const int pr = idx / (sz * sz), e = idx % (sz * sz), i = e / sz, j = e % sz;
+            const int bb = pr * 2 * sz;
+            T acc = (T)0;
+            for (int k = 0; k <= i; ++k) acc += I[(bb + sz + i) * LD + bb + sz + k] * Tm[(pr * sz + k) * (TB / 2 + 1) + j];
+            I[(bb + sz + i) * LD + bb + j] = -acc;
+        }
+        __syncthreads();
+    }
+    for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int i = idx / TB, j = idx % TB;
+        const T v = (i < nb && j <= i) ? I[i * LD + j] : (T)0;
+        inv_rm[idx] = v;                 // row-major: inv(i, j)
+        inv_cm[j * TB + i] = v;          // column-major copy
     }
     if (tid == 0) *maxd = s_runmax;
 }
 
-// ---------------------------------------------------------------------------
-// rows below the diagonal block: l_i = a_i L11^-T D^-1 (thread per row)
-// ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(128) tail_trsm(T* __restrict__ L, int r, int kb, int nb, int row_begin,
-                                                 const T* __restrict__ dblk) {
-    // dynamic smem: U[k][j] = d_k * L11[j][k] (k < j), then the CTA's rows As[t][j]
-    extern __shared__ __align__(16) unsigned char tsm_raw[];
-    T* U = reinterpret_cast<T*>(tsm_raw);                 // TB x (TB+1)
-    T* As = U + TB * (TB + 1);                            // 128 x (TB+1)
-    __shared__ T dinv[TB];
-    const T* B = L + (int64_t)kb * r + kb;
-    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
-        const int j = idx % TB, k = idx / TB;
-        U[k * (TB + 1) + j] = (j > k && j < nb) ? dblk[k] * B[(int64_t)k * r + j] : (T)0;
-    }
-    for (int k = threadIdx.x; k < TB; k += blockDim.x) dinv[k] = k < nb ? (T)1 / dblk[k] : (T)0;
-    const int i0 = row_begin + blockIdx.x * blockDim.x;
-    const int nrows = min((int)blockDim.x, r - i0);
-    // coalesced load of the 128 x nb row block (column-major in global)
-    for (int idx = threadIdx.x; idx < nrows * nb; idx += blockDim.x) {
-        const int t = idx % nrows, j = idx / nrows;
-        As[t * (TB + 1) + j] = L[(int64_t)(kb + j) * r + i0 + t];
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < nrows) {
-        T* a = As + t * (TB + 1);
-        for (int j = 0; j < nb; ++j) {
-            T v = a[j];
-            const T* Uj = U + j;
-            for (int k = 0; k < j; ++k) v -= a[k] * Uj[k * (TB + 1)];
-            a[j] = v * dinv[j];
-        }
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nrows * nb; idx += blockDim.x) {
-        const int tt = idx % nrows, j = idx / nrows;
-        L[(int64_t)(kb + j) * r + i0 + tt] = As[tt * (TB + 1) + j];
-    }
+constexpr int diag_smem() {
+    return (int)sizeof(T) * (2 * TB * (TB + 1) + (TB / 2) * (TB / 2 + 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -191,10 +260,10 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(128) tail_gemm(const T* __restrict__ A, int lda, const T* __restrict__ Bm, int ldb,
+__global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* __restrict__ Bm, int ldb,
                                                  const T* __restrict__ d, int M, int N, int K, int diag_off,
-                                                 T* __restrict__ C, int ldc, const int64_t* __restrict__ push_pos,
-                                                 T* __restrict__ inbox) {
+                                                 T* C, int ldc, const int64_t* __restrict__ push_pos,
+                                                 T* __restrict__ inbox, const T* __restrict__ dscale) {
     const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
     if (m0 + GB - 1 + diag_off < n0) return;      // tile strictly above the diagonal
     __shared__ __align__(16) T As[GK][GP];
@@ -215,7 +284,7 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* __restrict__ A, int ld
             T av = (T)0, bv = (T)0;
             if (gk < K) {
                 if (m0 + li < M) av = A[(int64_t)gk * lda + m0 + li];
-                if (n0 + li < N) bv = Bm[(int64_t)gk * ldb + n0 + li] * d[gk];
+                if (n0 + li < N) bv = d ? Bm[(int64_t)gk * ldb + n0 + li] * d[gk] : Bm[(int64_t)gk * ldb + n0 + li];
             }
             As[k][li] = av;
             Bs[k][li] = bv;
@@ -269,38 +338,13 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* __restrict__ A, int ld
                 if (MODE == 0) {
                     T* p = C + (int64_t)j * ldc + i;
                     *p = *p - (T)acc[a][b][e];
+                } else if (MODE == 2) {
+                    C[(int64_t)j * ldc + i] = (T)acc[a][b][e] / dscale[j];
                 } else {
                     const int64_t tpk = (int64_t)j * M - (int64_t)j * (j - 1) / 2 + (i - j);
                     inbox[push_pos[tpk]] = (T)acc[a][b][e];
                 }
             }
-}
-
-// explicit inverse of each unit-lower diagonal block (row-major, lower incl. diagonal);
-// thread t owns column t of the inverse and builds it in the output buffer
-template <typename T>
-__global__ void __launch_bounds__(TB) tail_inv(const T* __restrict__ L, int r, int w, T* __restrict__ inv) {
-    __shared__ T Ls[TB][TB + 1];
-    const int b = blockIdx.x;
-    const int kb = b * TB;
-    const int nb = min(TB, w - kb);
-    const T* B = L + (int64_t)kb * r + kb;
-    T* out = inv + (int64_t)b * TB * TB;
-    for (int idx = threadIdx.x; idx < TB * TB; idx += blockDim.x) {
-        const int i = idx % TB, j = idx / TB;
-        Ls[i][j] = (i > j && i < nb) ? B[(int64_t)j * r + i] : (T)0;
-        out[idx] = (T)0;
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < nb) {
-        out[t * TB + t] = (T)1;
-        for (int i = t + 1; i < nb; ++i) {
-            T v = (T)0;
-            for (int k = t; k < i; ++k) v -= Ls[i][k] * out[k * TB + t];
-            out[i * TB + t] = v;
-        }
-    }
 }
 
 __global__ void tail_finish(double* maxd, int32_t* count, int J, int parent) {
@@ -499,15 +543,10 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
 }
 
 template <typename T>
-constexpr int trsm_smem() {
-    return (int)sizeof(T) * (TB + 128) * (TB + 1);
-}
-
-template <typename T>
 void tail_factor_t(Ctx& c) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tail_trsm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem<T>());
+        cudaFuncSetAttribute(tail_diag<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<T>());
         attr = true;
     }
     T* L = (T*)c.lval;
@@ -522,13 +561,19 @@ void tail_factor_t(Ctx& c) {
         c.launches++;
         for (int kb = 0; kb < w; kb += TB) {
             const int nb = std::min(TB, w - kb);
-            tail_diag<T><<<1, 256, 0, c.stream>>>(P, r, kb, nb, t.c0, D, c.sym.sign, c.sn_maxd + t.J, c.bumps, c.err,
-                                                  c.delta_s, c.delta_d);
+            const int b = kb / TB;
+            T* inv_rm = inv + t.inv_off + (int64_t)b * TB * TB;
+            T* inv_cm = inv + t.inv_off + (int64_t)(t.nbd + b) * TB * TB;
+            tail_diag<T><<<1, 256, diag_smem<T>(), c.stream>>>(P, r, kb, nb, t.c0, D, c.sym.sign, c.sn_maxd + t.J,
+                                                              c.bumps, c.err, c.delta_s, c.delta_d, inv_rm, inv_cm);
             c.launches++;
             const int below = r - kb - nb;
             if (below > 0) {
-                tail_trsm<T><<<(below + 127) / 128, 128, trsm_smem<T>(), c.stream>>>(P, r, kb, nb, kb + nb,
-                                                                                   D + t.c0 + kb);
+                // L21 = A21 L11^-T D^-1 as a GEMM with the column-major inverse (DMMA in FP64)
+                T* A21 = P + (int64_t)kb * r + kb + nb;
+                dim3 g((below + GB - 1) / GB, 1);
+                tail_gemm<T, 2><<<g, 128, 0, c.stream>>>(A21, r, inv_cm, TB, nullptr, below, nb, nb, 1 << 30, A21, r,
+                                                         nullptr, nullptr, D + t.c0 + kb);
                 c.launches++;
             }
             const int Mr = r - kb - nb, Nc = w - kb - nb;
@@ -536,17 +581,16 @@ void tail_factor_t(Ctx& c) {
                 const T* A = P + (int64_t)kb * r + kb + nb;
                 dim3 g((Mr + GB - 1) / GB, (Nc + GB - 1) / GB);
                 tail_gemm<T, 0><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0 + kb, Mr, Nc, nb, 0,
-                                                         P + (int64_t)(kb + nb) * r + kb + nb, r, nullptr, nullptr);
+                                                         P + (int64_t)(kb + nb) * r + kb + nb, r, nullptr, nullptr,
+                                                         nullptr);
                 c.launches++;
             }
         }
-        tail_inv<T><<<t.nbd, TB, 0, c.stream>>>(P, r, w, inv + t.inv_off);
-        c.launches++;
         if (o > 0) {
             const T* A = P + w;
             dim3 g((o + GB - 1) / GB, (o + GB - 1) / GB);
             tail_gemm<T, 1><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
-                                                     c.sym.push_pos + S.cb_off[t.J], inbox);
+                                                     c.sym.push_pos + S.cb_off[t.J], inbox, nullptr);
             c.launches++;
         }
         tail_finish<<<1, 1, 0, c.stream>>>(c.sn_maxd, c.fac_count, t.J, t.parent);
@@ -614,7 +658,7 @@ void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total) {
         t.nbd = (t.w + TB - 1) / TB;
         t.inv_off = io;
         t.flag_off = fo;
-        io += (int64_t)t.nbd * TB * TB;
+        io += 2 * (int64_t)t.nbd * TB * TB;     // row-major (solves) + column-major (TRSM GEMM) inverses
         fo += 2 * t.nbd + 2;
         c.tail.push_back(t);
     }

@@ -618,18 +618,18 @@ __device__ __forceinline__ void vgather_warp(const T* vq, const uint8_t* __restr
     const int lane = threadIdx.x & 31;
     for (int j = lane; j < w; j += 32) colsum[j] = (T)0;
     __syncwarp();
-    for (int64_t base = lo; base < hi; base += 256) {
-        T v[8];
-        int col[8];
+    for (int64_t base = lo; base < hi; base += 512) {
+        T v[16];
+        int col[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {             // one round trip for up to 512 entries
             const int64_t e = base + 32 * u + lane;
             const bool ok = e < hi;
             v[u] = ok ? __ldcg(vq + e) : (T)0;
             col[u] = ok ? (int)__ldg(vin_col + e) : -(lane + 2);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
             if (base + 32 * u >= hi) break;
             T x = v[u];
             const int cu = col[u];
@@ -651,7 +651,8 @@ __device__ __forceinline__ void vgather_warp(const T* vq, const uint8_t* __restr
 // Forced inline so L keeps its address space (staged panel -> LDS).
 template <typename T>
 __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* x, T* vin,
-                                            const T (&xa)[2], const T (&xb)[2], T (*cs)[64], int J) {
+                                            const T (&xa)[2], const T (&xb)[2], T (*cs)[64], int J,
+                                            const int64_t (&pos_pf)[2]) {
     const int lane = threadIdx.x & 31;
     const int c0 = d.c0, w = d.w, r = d.r;
     for (int q = 0; q < 2; ++q) {
@@ -685,7 +686,8 @@ __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, cons
             const int i = i0 + lane;
             const bool ok = i < r;
             const int ii = ok ? i : r - 1;
-            const int64_t pos = ok ? a.vpush_pos[d.cvo + i - w] : 0;
+            const int pass = (i0 - w) >> 5;
+            const int64_t pos = pass < 2 ? pos_pf[pass] : (ok ? a.vpush_pos[d.cvo + i - w] : 0);
             T acc = (T)0;
 #pragma unroll 8
             for (int k = 0; k < w; ++k) {
@@ -700,7 +702,8 @@ __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, cons
 
 template <typename T>
 __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
-                                         const int32_t* rowsJ, const T* __restrict__ dvec, T* x, T* xo) {
+                                         const int32_t* rowsJ, const T* __restrict__ dvec, T* x, T* xo,
+                                         const int (&rows_pf)[2], const T (&d_pf)[2]) {
     const int lane = threadIdx.x & 31;
         const T* L0 = L + lane * r;
         const T* L1 = L + (lane + 32) * r;
@@ -709,13 +712,15 @@ __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0,
             if (!(q == 0 ? a.act0 : a.act1)) continue;
             T* xv = x + (int64_t)q * a.dim;
             T* xJ = xv + c0;
-            T x0 = o0 ? xJ[lane] / dvec[c0 + lane] : (T)0;      // D solve (ldl.py:101-102)
-            T x1 = o1 ? xJ[lane + 32] / dvec[c0 + lane + 32] : (T)0;
+            T x0 = o0 ? xJ[lane] / d_pf[0] : (T)0;      // D solve (ldl.py:101-102)
+            T x1 = o1 ? xJ[lane + 32] / d_pf[1] : (T)0;
             // ancestors' values at the off rows, gathered 64 at a time (coalesced over lanes)
             for (int i0 = 0; i0 < o; i0 += 64) {
                 const int n = min(64, o - i0);
-                if (lane < n) xo[lane] = __ldcg(xv + rowsJ[i0 + lane]);
-                if (lane + 32 < n) xo[lane + 32] = __ldcg(xv + rowsJ[i0 + lane + 32]);
+                const int ra = i0 == 0 ? rows_pf[0] : (lane < n ? rowsJ[i0 + lane] : 0);
+                const int rb = i0 == 0 ? rows_pf[1] : (lane + 32 < n ? rowsJ[i0 + lane + 32] : 0);
+                if (lane < n) xo[lane] = __ldcg(xv + ra);
+                if (lane + 32 < n) xo[lane + 32] = __ldcg(xv + rb);
                 __syncwarp();
 #pragma unroll 8
                 for (int k = 0; k < n; ++k) {
@@ -828,6 +833,10 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         const int Jn = d.parent >= 0 ? d.parent : J;
         const int pv32 = lane < 8 ? __ldg(a.desc32 + (int64_t)Jn * 8 + lane) : 0;
         const int64_t pv64 = (lane >= 8 && lane < 16) ? __ldg(a.desc64 + (int64_t)Jn * 8 + (lane - 8)) : 0;
+        // push positions of the first 64 off rows (static: prefetched with the inputs)
+        int64_t pos_pf[2];
+        pos_pf[0] = lane < r - w ? __ldg(a.vpush_pos + d.cvo + lane) : 0;
+        pos_pf[1] = lane + 32 < r - w ? __ldg(a.vpush_pos + d.cvo + 32 + lane) : 0;
         // 2. own right-hand-side values and the vector inbox of the supernode's columns
         T xa[2] = {(T)0, (T)0}, xb[2] = {(T)0, (T)0};
         for (int q = 0; q < 2; ++q) {
@@ -842,9 +851,9 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         if (staged) {
             mbar_wait(bar, phase);
             phase ^= 1u;
-            fwd_compute<T>(slice, a, d, x, vin, xa, xb, cs, J);
+            fwd_compute<T>(slice, a, d, x, vin, xa, xb, cs, J, pos_pf);
         } else {
-            fwd_compute<T>(Lg, a, d, x, vin, xa, xb, cs, J);
+            fwd_compute<T>(Lg, a, d, x, vin, xa, xb, cs, J, pos_pf);
         }
         dn = desc_from_regs(pv32, pv64);
         __syncwarp();
@@ -980,14 +989,17 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a0, const T
             __syncwarp();
             if (lane == 0) bulk_g2s(slice, Lg, bytes, &bars[wid]);
         }
+        // static inputs fetched before waiting for the parent
+        const int rows_pf[2] = {lane < o ? __ldg(rowsJ + lane) : 0, lane + 32 < o ? __ldg(rowsJ + 32 + lane) : 0};
+        const T d_pf[2] = {lane < w ? dvec[c0 + lane] : (T)1, lane + 32 < w ? dvec[c0 + lane + 32] : (T)1};
         if (lane == 0 && d.parent >= 0) wait_ge(a.count + d.parent, 1);
         __syncwarp();
         if (staged) {
             mbar_wait(&bars[wid], phase);
             phase ^= 1u;
-            bwd_body<T>(slice, a, c0, w, r, o, rowsJ, dvec, x, xs[wid]);
+            bwd_body<T>(slice, a, c0, w, r, o, rowsJ, dvec, x, xs[wid], rows_pf, d_pf);
         } else {
-            bwd_body<T>(Lg, a, c0, w, r, o, rowsJ, dvec, x, xs[wid]);
+            bwd_body<T>(Lg, a, c0, w, r, o, rowsJ, dvec, x, xs[wid], rows_pf, d_pf);
         }
         __syncwarp();
         if (lane == 0) st_release(a.count + J, 1);

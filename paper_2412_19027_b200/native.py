@@ -252,8 +252,20 @@ class DeviceContext:
         self.m = sym._desc.m
         self.sc = np.zeros(SC_COUNT)
 
+    # CIPM_HOST_PROFILE=1: synchronise after every call and accumulate wall time per entry point
+    host_profile = os.environ.get("CIPM_HOST_PROFILE", "0") != "0"
+
     def call(self, name, *args, where=None):
-        rc = getattr(lib(), name)(self.handle, *args)
+        if self.host_profile:
+            import time
+            t0 = time.perf_counter()
+            rc = getattr(lib(), name)(self.handle, *args)
+            lib().cipm_sync(self.handle)
+            prof = self.__dict__.setdefault("profile", {})
+            tot, cnt = prof.get(name, (0.0, 0))
+            prof[name] = (tot + time.perf_counter() - t0, cnt + 1)
+        else:
+            rc = getattr(lib(), name)(self.handle, *args)
         if rc is not None and rc < 0:
             raise_for_status(rc, where or name)
         return rc

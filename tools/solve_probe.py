@@ -79,6 +79,32 @@ def trace_main():
     print("trace written", ns)
 
 
+def host_main():
+    """python tools/solve_probe.py --host c2_lasso: per-entry-point wall time of one solve
+    (CIPM_HOST_PROFILE=1 synchronises after every C call)."""
+    os.environ["CIPM_HOST_PROFILE"] = "1"
+    from paper_2412_19027_b200 import native
+    native.DeviceContext.host_profile = True
+    cfg = sys.argv[2]
+    prob = G.build(cfg)
+    s = Solver(prob, SolverSettings(eps_feas=1e-8, precision=G.CONFIGS[cfg]["precision"]))
+    s.solve()
+    s._ctx.profile = {}
+    t0 = time.perf_counter()
+    r = s.solve()
+    wall = time.perf_counter() - t0
+    prof = s._ctx.profile
+    tot = sum(v[0] for v in prof.values())
+    print(f"{cfg}: wall {wall*1e3:.2f} ms, in C calls {tot*1e3:.2f} ms, iterations {r.iterations}")
+    for k, (t, n) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        print(f"  {k:24s} {n:4d} calls {t*1e3:9.3f} ms  {t*1e3/max(1,n):8.3f} ms/call")
+    s.close()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--host":
+    host_main()
+    sys.exit(0)
+
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "--trace":
     trace_main()
     sys.exit(0)
