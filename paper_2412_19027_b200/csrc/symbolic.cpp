@@ -10,6 +10,7 @@
 #include "symbolic.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <queue>
@@ -223,7 +224,15 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                 for (int32_t i = ci[p]; fl[i] != j; i = parent[i]) { cnt0[i]++; fl[i] = (int32_t)j; }
         }
     }
-    std::vector<int32_t> post = postorder(parent, cnt0, dim);
+    // postorder weight: subtree height first (the critical-path child is numbered
+    // immediately before its parent, so the top chain is contiguous and can be
+    // merged), column count second (a dense tail's continuation joins its supernode)
+    std::vector<int64_t> height_col(dim, 1);
+    for (int64_t j = 0; j < dim; ++j)
+        if (parent[j] != -1) height_col[parent[j]] = std::max(height_col[parent[j]], height_col[j] + 1);
+    std::vector<int64_t> pweight(dim);
+    for (int64_t j = 0; j < dim; ++j) pweight[j] = (height_col[j] << 32) + cnt0[j];
+    std::vector<int32_t> post = postorder(parent, pweight, dim);
     {
         std::vector<int32_t> p2(dim);
         for (int64_t k = 0; k < dim; ++k) p2[k] = perm[post[k]];
@@ -314,6 +323,42 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         first[P] = first[s];
         width[P] = w;
         truenz[P] += truenz[s];
+    }
+    // top-chain merge: the single-child chain hanging below each root is one long
+    // sequential path through the elimination tree (one dependency hop per
+    // supernode in every factorisation and triangular sweep).  Merged into one
+    // dense supernode it becomes a dense-tail node (multi-CTA blocked kernels).
+    int64_t chain_max = opt.chain_merge_max;
+    if (const char* e = getenv("CIPM_CHAIN_MERGE")) chain_max = atoll(e);   // experiments
+    if (chain_max > 0) {
+        // the child adjacent in postorder (numbered immediately before its parent) is
+        // the heaviest one: the critical-path continuation
+        std::vector<int32_t> adj(nf, -1);
+        for (int64_t s = 0; s < nf; ++s) {
+            if (find((int32_t)s) != s || fparent[s] == -1) continue;
+            const int32_t P = find(fparent[s]);
+            if (first[s] + width[s] == first[P]) adj[P] = (int32_t)s;
+        }
+        for (int64_t R = 0; R < nf; ++R) {
+            if (find((int32_t)R) != R || fparent[R] != -1) continue;
+            std::vector<int32_t> chain;
+            int32_t cur = (int32_t)R;
+            int64_t wsum = width[R];
+            while (adj[cur] >= 0) {
+                const int32_t ch = adj[cur];
+                if (wsum + width[ch] > chain_max) break;
+                chain.push_back(ch);
+                wsum += width[ch];
+                cur = ch;
+            }
+            if (chain.size() < 2 || wsum < opt.tail_width) continue;
+            for (int32_t ch : chain) {
+                rep[ch] = (int32_t)R;
+                first[R] = first[ch];
+                truenz[R] += truenz[ch];
+            }
+            width[R] = wsum;
+        }
     }
     // final supernodes in column order
     std::vector<int32_t> sid(nf, -1);

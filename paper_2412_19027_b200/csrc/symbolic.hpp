@@ -25,6 +25,8 @@ struct SymbolicOptions {
     int tail_offrows = 512;    // ... or with at least this many off-diagonal rows
     int mid_panel = 512;       // panels (w*r) at least this large, or inboxes of 2x this, and
                                // their ancestors are factored by whole CTAs (mid tier)
+    int chain_merge_max = 256;    // merge the single-child chain below a root into one dense
+                                  // supernode of at most this many columns (0: off)
 };
 
 struct Symbolic {
