@@ -117,6 +117,16 @@ int cipm_ctx_create(const cipm_problem_desc *desc, const cipm_symbolic *sym,
 int cipm_ctx_set_values(cipm_ctx *ctx, const double *p_values, const double *a_values,
                         const double *q, const double *b, const double *d_row,
                         const double *d_col, double c_obj);
+/* device-side problem setup (replaces the host reorder_cones + equilibrate, problem.py:177-284,
+ * for the parametric re-solve path ipm.py:187-221): row_perm[i] = user row of reordered row i,
+ * a_src[k] = user A-value index of reordered A nonzero k (set once) */
+int cipm_ctx_set_reorder(cipm_ctx *ctx, const int64_t *row_perm, const int64_t *a_src);
+/* raw USER-order values (P full symmetric values, A values, q, b) -> H2D, reorder, 10 Ruiz
+ * rounds (bitwise the reference's arithmetic) when equilibrate != 0, factor base image */
+int cipm_ctx_set_problem(cipm_ctx *ctx, const double *p_values, const double *a_values,
+                         const double *q, const double *b, int equilibrate);
+/* the equilibration of the last set_problem: d_row (m), d_col (n), c_obj */
+int cipm_ctx_get_equilibration(cipm_ctx *ctx, double *d_row, double *d_col, double *c_obj);
 void cipm_ctx_destroy(cipm_ctx *ctx);
 int cipm_sync(cipm_ctx *ctx);
 int cipm_device_bytes(const cipm_ctx *ctx, int64_t *bytes);

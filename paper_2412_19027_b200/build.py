@@ -21,9 +21,9 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libcipm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["capi.cu", "ldl.cu", "dense.cu", "cones.cu", "vec.cu", "batch.cu"]
+CU_SOURCES = ["capi.cu", "ldl.cu", "dense.cu", "cones.cu", "vec.cu", "batch.cu", "setup.cu"]
 CPP_SOURCES = ["symbolic.cpp"]
-NO_FMAD = {"cones.cu", "batch.cu"}
+NO_FMAD = {"cones.cu", "batch.cu", "setup.cu"}
 
 
 def _headers():

@@ -400,6 +400,22 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     }
     TRY(dalloc(c, &c.q, c.n));
     TRY(dalloc(c, &c.b, c.m));
+    TRY(dalloc(c, &c.a_user, c.a_nnz));
+    TRY(dalloc(c, &c.b_user, c.m));
+    TRY(dalloc(c, &c.a_src, c.a_nnz));
+    TRY(dalloc(c, &c.b_src, c.m));
+    TRY(dalloc(c, &c.eq_cnorm, c.n));
+    TRY(dalloc(c, &c.eq_rnorm, c.m));
+    TRY(dalloc(c, &c.eq_cstep, c.n));
+    TRY(dalloc(c, &c.eq_rstep, c.m));
+    TRY(dalloc(c, &c.eq_cobj, 1));
+    {
+        std::vector<int64_t> bo, bd;
+        blocks_of(d, bo, bd);
+        c.eq_nblocks = (int64_t)bo.size();
+        TRY(upload(c, &c.eq_boff, bo.data(), c.eq_nblocks));
+        TRY(upload(c, &c.eq_bdim, bd.data(), c.eq_nblocks));
+    }
     TRY(dalloc(c, &c.dr, c.m));
     TRY(dalloc(c, &c.dc, c.n));
 
@@ -573,6 +589,47 @@ int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const d
     c.h2d_bytes += (int64_t)sizeof(double) * (c.p_nnz + 2 * c.a_nnz + 2 * c.n + 2 * c.m);
     k_build_base(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    return CIPM_OK;
+}
+
+int cipm_ctx_set_reorder(cipm_ctx* h, const int64_t* row_perm, const int64_t* a_src) {
+    if (!h || (h->c.m && !row_perm) || (h->c.a_nnz && !a_src)) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    if (c.m) CIPM_CUDA(cudaMemcpy(c.b_src, row_perm, sizeof(int64_t) * c.m, cudaMemcpyHostToDevice));
+    if (c.a_nnz) CIPM_CUDA(cudaMemcpy(c.a_src, a_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyHostToDevice));
+    c.have_reorder = true;
+    return CIPM_OK;
+}
+
+int cipm_ctx_set_problem(cipm_ctx* h, const double* p_values, const double* a_values, const double* q,
+                         const double* b, int equilibrate) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    if (!c.have_reorder) return CIPM_E_ARG;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    if (c.p_nnz) CIPM_CUDA(cudaMemcpyAsync(c.p_v, p_values, sizeof(double) * c.p_nnz, cudaMemcpyHostToDevice, c.stream));
+    if (c.a_nnz)
+        CIPM_CUDA(cudaMemcpyAsync(c.a_user, a_values, sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.q, q, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemcpyAsync(c.b_user, b, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+    c.h2d_bytes += (int64_t)sizeof(double) * (c.p_nnz + c.a_nnz + c.n + c.m);
+    int rc = k_set_problem(c, equilibrate != 0);
+    if (rc) return rc;
+    CIPM_CUDA(cudaMemcpyAsync(&c.c_obj, c.eq_cobj, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(cudaGetLastError());
+    return CIPM_OK;
+}
+
+int cipm_ctx_get_equilibration(cipm_ctx* h, double* d_row, double* d_col, double* c_obj) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (d_row && c.m) CIPM_CUDA(cudaMemcpy(d_row, c.dr, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (d_col && c.n) CIPM_CUDA(cudaMemcpy(d_col, c.dc, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (c_obj) *c_obj = c.c_obj;
+    c.d2h_bytes += (int64_t)sizeof(double) * ((d_row ? c.m : 0) + (d_col ? c.n : 0));
     return CIPM_OK;
 }
 

@@ -98,6 +98,14 @@ struct Ctx {
     int64_t *at_rp = nullptr, *at_ci = nullptr, *at_src = nullptr;
     double* at_v = nullptr;
     double *q = nullptr, *b = nullptr, *dr = nullptr, *dc = nullptr;
+    // device-side setup (setup.cu): user-order raw values, reorder maps, Ruiz work
+    double *a_user = nullptr, *b_user = nullptr;
+    int64_t *a_src = nullptr, *b_src = nullptr;
+    bool have_reorder = false;
+    double *eq_cnorm = nullptr, *eq_rnorm = nullptr, *eq_cstep = nullptr, *eq_rstep = nullptr, *eq_cobj = nullptr;
+    int32_t *eq_boff = nullptr, *eq_bdim = nullptr;
+    int64_t eq_nblocks = 0;
+    double one = 1.0;
 
     // iterate and work vectors
     double *x = nullptr, *z = nullptr, *s = nullptr;
@@ -222,6 +230,8 @@ void k_build_base(Ctx& c);
 void k_assemble(Ctx& c);
 int k_factor(Ctx& c);
 void k_refine_step(Ctx& c, int nrhs, const int* active_host);
+// setup.cu
+int k_set_problem(Ctx& c, bool equilibrate);
 // dense.cu
 void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total);
 void k_tail_factor(Ctx& c);

@@ -66,6 +66,9 @@ _SIGS = {
                          ctypes.POINTER(c_void_p)], ctypes.c_int),
     "cipm_ctx_set_values": ([c_void_p, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, c_dbl], ctypes.c_int),
     "cipm_ctx_destroy": ([c_void_p], None),
+    "cipm_ctx_set_reorder": ([c_void_p, P_I64, P_I64], ctypes.c_int),
+    "cipm_ctx_set_problem": ([c_void_p, P_DBL, P_DBL, P_DBL, P_DBL, ctypes.c_int], ctypes.c_int),
+    "cipm_ctx_get_equilibration": ([c_void_p, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_sync": ([c_void_p], ctypes.c_int),
     "cipm_device_bytes": ([c_void_p, P_I64], ctypes.c_int),
     "cipm_init_iterate": ([c_void_p], ctypes.c_int),

@@ -20,8 +20,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from .exceptions import ConicError, PatternMismatch
-from .model import Equilibration, ProblemData, equilibrate, reorder_cones, unscale_solution, validate
-from .native import SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, require_device
+from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, unscale_solution, validate,
+                    validate_values)
+from .native import P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, require_device
 from .settings import (ALMOST_OPTIMAL_FACTOR, FULL, MIXED, STALL_IMPROVEMENT, STALL_WINDOW, SolveResult,
                        SolverSettings, Status, default_dynamic_reg, default_static_reg)
 
@@ -110,12 +111,11 @@ class Solver:
         self._original = problem.copy()
         reordered, perm = reorder_cones(problem)
         self._perm = perm
-        self._reordered = reordered
-        self._equilibrate(reordered)
-        self.layout = Layout(self._scaled.cones)
+        self._reordered = reordered          # pattern of the reordered problem (values: user order on the device)
+        self.layout = Layout(reordered.cones)
         self.nu = self.layout.degree
-        self.n, self.m = self._scaled.n, self._scaled.m
-        self.symbolic = SymbolicAnalysis(self._scaled.P, self._scaled.A, self.layout, ordering=ordering)
+        self.n, self.m = reordered.n, reordered.m
+        self.symbolic = SymbolicAnalysis(reordered.P, reordered.A, self.layout, ordering=ordering)
         st = self.settings
         prec = st.precision
         cs = Settings()
@@ -133,6 +133,10 @@ class Solver:
         cs.stream = None
         torch.cuda.set_device(device)
         self._ctx = DeviceContext(self.symbolic, cs)
+        # reorder maps once: reordered row i <- user row perm[i]; reordered A nonzero k <- user nonzero
+        self._row_perm = np.ascontiguousarray(perm, dtype=np.int64)
+        self._a_src = np.ascontiguousarray(csr_row_gather_src(problem.A, perm), dtype=np.int64)
+        self._ctx.call("cipm_ctx_set_reorder", pi64(self._row_perm) or P_I64(), pi64(self._a_src) or P_I64())
         self._upload_values()
         self.num_symbolic = 1
         self.setup_seconds = time.perf_counter() - t0
@@ -141,46 +145,41 @@ class Solver:
 
     # -- data plumbing --------------------------------------------------------
 
-    def _equilibrate(self, reordered):
-        if self.settings.do_equilibrate:
-            self._scaled, self._equil = equilibrate(reordered)
-        else:
-            self._scaled, self._equil = reordered.copy(), Equilibration.identity(reordered.m, reordered.n)
-        qr, br = reordered.q, reordered.b
-        self._norm_q = float(np.max(np.abs(qr))) if qr.size else 0.0
-        self._norm_b = float(np.max(np.abs(br))) if br.size else 0.0
-
     def _upload_values(self):
-        sp_, e = self._scaled, self._equil
-        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in
-                      (sp_.P.values, sp_.A.values, sp_.q, sp_.b, e.d_row, e.d_col)]
+        """Raw user-order values to the device; cone reordering and Ruiz equilibration
+        run there (setup.cu, bitwise the reference's problem.py:177-284 arithmetic)."""
+        prob = self._original
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (prob.P.values, prob.A.values, prob.q, prob.b)]
         k = self._keep
-        self._ctx.call("cipm_ctx_set_values", pdbl(k[0]), pdbl(k[1]), pdbl(k[2]), pdbl(k[3]), pdbl(k[4]),
-                       pdbl(k[5]), float(e.c_obj))
+        self._ctx.call("cipm_ctx_set_problem", pdbl(k[0]), pdbl(k[1]), pdbl(k[2]), pdbl(k[3]),
+                       1 if self.settings.do_equilibrate else 0)
+        d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
+        self._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
+        self._equil = Equilibration(d_row, d_col, float(c_obj.value))
+        # termination norms use the reordered unscaled data (ipm.py:184-185); max is order-free
+        self._norm_q = float(np.max(np.abs(prob.q))) if prob.q.size else 0.0
+        self._norm_b = float(np.max(np.abs(prob.b))) if prob.b.size else 0.0
 
     def update_data(self, P=None, A=None, q=None, b=None) -> None:
         """Parametric re-solve (reference ipm.py:187-221): same patterns, fresh
-        equilibration, value-only upload; the symbolic analysis is reused."""
+        equilibration, value-only upload; the symbolic analysis is reused.  Only
+        the changed arrays are re-validated (the patterns are checked equal)."""
         prob = self._original
         if P is not None:
             if not (np.array_equal(P.rowptr, prob.P.rowptr) and np.array_equal(P.colidx, prob.P.colidx)):
                 raise PatternMismatch("P pattern differs from the setup pattern")
-            prob.P = P.copy()
         if A is not None:
             if not (np.array_equal(A.rowptr, prob.A.rowptr) and np.array_equal(A.colidx, prob.A.colidx)):
                 raise PatternMismatch("A pattern differs from the setup pattern")
-            prob.A = A.copy()
-        if q is not None:
-            if len(q) != prob.n:
-                raise PatternMismatch("q length changed")
-            prob.q = np.asarray(q, dtype=np.float64).copy()
-        if b is not None:
-            if len(b) != prob.m:
-                raise PatternMismatch("b length changed")
-            prob.b = np.asarray(b, dtype=np.float64).copy()
-        validate(prob)
-        self._reordered, _ = reorder_cones(prob)
-        self._equilibrate(self._reordered)
+        if q is not None and len(q) != prob.n:
+            raise PatternMismatch("q length changed")
+        if b is not None and len(b) != prob.m:
+            raise PatternMismatch("b length changed")
+        new = ProblemData(P.copy() if P is not None else prob.P, A.copy() if A is not None else prob.A,
+                          np.asarray(q, dtype=np.float64).copy() if q is not None else prob.q,
+                          np.asarray(b, dtype=np.float64).copy() if b is not None else prob.b, prob.cones)
+        validate_values(new, P is not None, A is not None, q is not None, b is not None)
+        self._original = new
         self._upload_values()
 
     def _block_list(self):

@@ -56,3 +56,25 @@ def test_kkt_solve_residual_all_tiers(gpu):
         ctx.call("cipm_kkt_solve", pdbl(rhs), pdbl(x), ctypes.byref(steps), ctypes.byref(res))
         assert res.value <= 1e-9 * max(1.0, np.max(np.abs(rhs))), (res.value, steps.value)
     s.close()
+
+
+@pytest.mark.parametrize("name", ["lp_150x300", "socp_40", "psd_6x4", "exppow_20_8", "lasso_10x40"])
+def test_device_equilibration_bitwise(gpu, name):
+    """setup.cu reorders and Ruiz-equilibrates on the device with the reference's
+    arithmetic: D_r, D_c and c equal the host routine (problem.py:222-284) bit for bit."""
+    import ctypes
+
+    from golden_io import load_instance, problem_from_doc
+    from paper_2412_19027_b200 import model
+    from paper_2412_19027_b200.native import pdbl
+    from paper_2412_19027_b200.solver import Solver
+    prob = problem_from_doc(load_instance(name))
+    s = Solver(prob, SolverSettings(eps_feas=1e-8))
+    d_row, d_col, c = np.empty(s.m), np.empty(s.n), ctypes.c_double(0)
+    s._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c))
+    s.close()
+    r, _ = model.reorder_cones(prob)
+    _, e = model.equilibrate(r)
+    np.testing.assert_array_equal(d_row, e.d_row)
+    np.testing.assert_array_equal(d_col, e.d_col)
+    assert c.value == e.c_obj
