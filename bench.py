@@ -402,7 +402,7 @@ def run_batch(args):
         "clocks": clk,
         "e2e": {"value": e2e_all / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d.value // max(1, args.steps),
                 "d2h_bytes_per_step": d2h.value // max(1, args.steps),
-                "path": "BatchSolver.update_data(q, b) host arrays (equilibration + H2D) + solve() -> host results"},
+                "path": "BatchSolver.update_data(q, b) raw host arrays (H2D; reorder + Ruiz per instance on the device) + solve() -> host results"},
         "gpu_launches": args.steps,
         "roofline": None,
     }

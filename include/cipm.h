@@ -196,6 +196,14 @@ int cipm_batch_info(const cipm_batch *b, int64_t *info);
 int cipm_batch_set_values(cipm_batch *b, const double *V, const double *q, const double *bvec,
                           const double *d_row, const double *d_col, const double *c_obj,
                           const double *norm_q, const double *norm_b);
+/* device-side setup per instance (replaces the host reorder + equilibration): the
+ * reorder maps once (row_perm[i] = user row of reordered row i, a_src[k] = user A-value
+ * index of reordered nonzero k), then raw USER-order values per solve: V = [P | A] (user
+ * order), q, b.  Results then come back unscaled, divided by tau (not for infeasibility
+ * certificates) and in the user's row order. */
+int cipm_batch_set_reorder(cipm_batch *b, const int64_t *row_perm, const int64_t *a_src);
+int cipm_batch_set_raw_values(cipm_batch *b, const double *V, const double *q, const double *bvec,
+                              int equilibrate);
 /* run every instance to termination; *ms = CUDA-event time of the launch */
 int cipm_batch_solve(cipm_batch *b, double *ms);
 /* status[count] (0 optimal, 1 primal_inf, 2 dual_inf, 3 almost_optimal, 4 max_iterations,

@@ -24,7 +24,7 @@ import numpy as np
 
 from .exceptions import ConicError, PatternMismatch, raise_for_status
 from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, reorder_cones, validate
-from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, require_device
+from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, pi64, require_device
 from .settings import FULL, SolveResult, SolverSettings, Status, default_dynamic_reg, default_static_reg
 
 RUIZ_ITERS = 10
@@ -121,21 +121,35 @@ class BatchSolver:
         self.last_kernel_ms = 0.0
 
     def _upload(self):
+        """Raw user-order arrays to the device; each instance's CTA reorders and
+        Ruiz-equilibrates its own data (batch.cu, the reference's arithmetic)."""
+        if not getattr(self, "_reorder_set", False):
+            perm = np.ascontiguousarray(self._perm, dtype=np.int64)
+            a_src = np.ascontiguousarray(_take_rows_src(self.problems[0].A, self._perm), dtype=np.int64)
+            raise_for_status(lib().cipm_batch_set_reorder(self.handle, pi64(perm), pi64(a_src)), "batch reorder")
+            self._reorder_set = True
+        V = np.concatenate([np.stack([p.P.values for p in self.problems]),
+                            np.stack([p.A.values for p in self.problems])], axis=1)
+        self._host = [np.ascontiguousarray(a) for a in
+                      (V, np.stack([p.q for p in self.problems]), np.stack([p.b for p in self.problems]))]
+        rc = lib().cipm_batch_set_raw_values(self.handle, *[pdbl(a) for a in self._host],
+                                             1 if self.settings.do_equilibrate else 0)
+        raise_for_status(rc, "batch upload")
+
+    def _upload_host_equilibrated(self):
+        """Alternative path: host reorder + vectorised Ruiz (equilibrate_batch), scaled upload."""
         perm = self._perm
         P, A = self._pattern.P, self._pattern.A
-        # rows of A are permuted identically in every instance: gather the values once per instance
-        a_src = self._a_src = _take_rows_src(self.problems[0].A, perm)
+        a_src = _take_rows_src(self.problems[0].A, perm)
         pv = np.stack([p.P.values for p in self.problems])
         av = np.stack([p.A.values[a_src] for p in self.problems])
         q = np.stack([p.q for p in self.problems])
         b = np.stack([p.b[perm] for p in self.problems])
-        self._norm_q = np.max(np.abs(q), axis=1) if self.n else np.zeros(self.count)
-        self._norm_b = np.max(np.abs(b), axis=1) if self.m else np.zeros(self.count)
+        norm_q = np.max(np.abs(q), axis=1) if self.n else np.zeros(self.count)
+        norm_b = np.max(np.abs(b), axis=1) if self.m else np.zeros(self.count)
         pv_s, av_s, q_s, b_s, d_row, d_col, c_obj = equilibrate_batch(P, A, pv, av, q, b)
-        self._d_row, self._d_col, self._c_obj = d_row, d_col, c_obj
         self._host = [np.ascontiguousarray(a) for a in
-                      (np.concatenate([pv_s, av_s], axis=1), q_s, b_s, d_row, d_col, c_obj, self._norm_q,
-                       self._norm_b)]
+                      (np.concatenate([pv_s, av_s], axis=1), q_s, b_s, d_row, d_col, c_obj, norm_q, norm_b)]
         rc = lib().cipm_batch_set_values(self.handle, *[pdbl(a) for a in self._host])
         raise_for_status(rc, "batch upload")
 
@@ -169,22 +183,16 @@ class BatchSolver:
                                                   pdbl(res), pdbl(x), pdbl(z), pdbl(s)), "batch results")
         secs = self.last_kernel_ms / 1e3 if secs is None else secs
         out = []
-        inv = self._perm
         for k in range(c):
             st = _STATUS[int(status[k])]
             g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = res[k]
-            x_u = self._d_col[k] * x[k]
-            z_u = self._d_row[k] * z[k] / self._c_obj[k]
-            s_u = s[k] / self._d_row[k]
+            # the device returned unscaled, user-row-order iterates (divided by tau unless a certificate)
+            x_o, z_o, s_o = x[k], z[k], s[k]
             cert = None
-            if st in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
-                x_o, z_o, s_o = x_u, _user_rows(z_u, inv), _user_rows(s_u, inv)
-                if st == Status.PRIMAL_INFEASIBLE:
-                    cert = z_o / abs(float(self.problems[k].b @ z_o))
-                else:
-                    cert = x_o / abs(float(self.problems[k].q @ x_o))
-            else:
-                x_o, z_o, s_o = x_u / tau, _user_rows(z_u / tau, inv), _user_rows(s_u / tau, inv)
+            if st == Status.PRIMAL_INFEASIBLE:
+                cert = z_o / abs(float(self.problems[k].b @ z_o))
+            elif st == Status.DUAL_INFEASIBLE:
+                cert = x_o / abs(float(self.problems[k].q @ x_o))
             out.append(SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=float(g_p),
                                    obj_dual=float(g_d), iterations=int(iters), setup_seconds=self.setup_seconds,
                                    solve_seconds=secs, norm_rp=float(rp), norm_rd=float(rd),

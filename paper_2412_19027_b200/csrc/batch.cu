@@ -72,7 +72,7 @@ __device__ __forceinline__ void breduce(double (&v)[K], unsigned maxmask, double
 struct Inst {
     // shared-memory (or workspace) vectors
     double *x, *z, *s, *dx[2], *dz[2], *ds[2], *gx, *gz, *col2, *sol, *rb, *rx, *rr, *rbest, *t, *dsc, *h, *w, *lam,
-        *V, *lx, *d, *y;
+        *V, *lx, *d, *y, *qs, *bs;
 };
 
 __device__ __forceinline__ double csr_dot(const int32_t* rp, const int32_t* ci, const double* v, const double* x,
@@ -102,6 +102,7 @@ __device__ void carve(const BatchPattern& pt, double* base, Inst& I) {
     I.dsc = take(m); I.h = take(m); I.w = take(m); I.lam = take(m);
     I.V = take(pt.nnz_p + pt.nnz_a);
     I.lx = take(pt.nnz_l); I.d = take(dim); I.y = take(dim);
+    I.qs = take(n); I.bs = take(m);
 }
 
 // ------------------------- factorisation (thread 0) -------------------------
@@ -187,19 +188,104 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
     Inst I;
     carve(pt, bd.use_smem ? bsm : bd.workspace + (int64_t)inst * bd.ws_stride, I);
     const double* gV = bd.V + (int64_t)inst * (pt.nnz_p + pt.nnz_a);
-    const double* q = bd.q + (int64_t)inst * n;
-    const double* b = bd.b + (int64_t)inst * m;
-    const double* dr = bd.dr + (int64_t)inst * m;
-    const double* dc = bd.dc + (int64_t)inst * n;
-    const double cobj = bd.c_obj[inst], norm_q = bd.norm_q[inst], norm_b = bd.norm_b[inst];
+    const double* q_in = bd.q + (int64_t)inst * n;
+    const double* b_in = bd.b + (int64_t)inst * m;
+    double* dr = bd.dr + (int64_t)inst * m;
+    double* dc = bd.dc + (int64_t)inst * n;
     double* bx = bd.best_x + (int64_t)inst * n;
     double* bz_ = bd.best_z + (int64_t)inst * m;
     double* bs = bd.best_s + (int64_t)inst * m;
     const double* Va = I.V + pt.nnz_p;
+    double* Vw = I.V + pt.nnz_p;
     const double nu1 = (double)nnd + 1.0;
     const double eps_feas = bd.eps_feas, eps_inf = bd.eps_inf;
+    double* q = I.qs;
+    double* b = I.bs;
+    double cobj, norm_q, norm_b;
 
-    for (int k = tid; k < pt.nnz_p + pt.nnz_a; k += BT) I.V[k] = gV[k];
+    if (bd.device_setup) {
+        // raw user-order data: cone reordering + Ruiz equilibration in the CTA
+        // (problem.py:177-284, the reference's elementwise arithmetic, no FMA contraction)
+        for (int k = tid; k < pt.nnz_p; k += BT) I.V[k] = gV[k];
+        for (int k = tid; k < pt.nnz_a; k += BT) Vw[k] = gV[pt.nnz_p + pt.a_src[k]];
+        for (int k = tid; k < n; k += BT) q[k] = q_in[k];
+        for (int k = tid; k < m; k += BT) b[k] = b_in[pt.b_src[k]];
+        double nq[2] = {0.0, 0.0};
+        for (int k = tid; k < n; k += BT) nq[0] = fmax(nq[0], fabs(q_in[k]));
+        for (int k = tid; k < m; k += BT) nq[1] = fmax(nq[1], fabs(b_in[k]));
+        breduce<2>(nq, 3u, sred);
+        norm_q = n ? nq[0] : 0.0;
+        norm_b = m ? nq[1] : 0.0;
+        double* cnorm = I.rb;            // scratch (the refinement vectors are free before the loop)
+        double* rnorm = I.rb + n;
+        double* cstep = I.rx;
+        double* rstep = I.rx + n;
+        double* dcol = I.rr;
+        double* drow = I.rr + n;
+        for (int k = tid; k < n; k += BT) dcol[k] = 1.0;
+        for (int k = tid; k < m; k += BT) drow[k] = 1.0;
+        __syncthreads();
+        if (bd.equilibrate) {
+            for (int it = 0; it < 10; ++it) {
+                for (int j = tid; j < n; j += BT) {
+                    double c = 0.0;
+                    for (int p = pt.p_rp[j]; p < pt.p_rp[j + 1]; ++p) c = fmax(c, fabs(I.V[p]));
+                    for (int p = pt.at_rp[j]; p < pt.at_rp[j + 1]; ++p) c = fmax(c, fabs(Vw[pt.at_src[p]]));
+                    cnorm[j] = c;
+                }
+                for (int r = tid; r < m; r += BT) {
+                    double c = 0.0;
+                    for (int p = pt.a_rp[r]; p < pt.a_rp[r + 1]; ++p) c = fmax(c, fabs(Vw[p]));
+                    rnorm[r] = c;
+                }
+                __syncthreads();
+                for (int j = tid; j < n; j += BT) {
+                    const double st = cnorm[j] > 0.0 ? 1.0 / sqrt(cnorm[j]) : 1.0;
+                    const double nd = fmin(fmax(dcol[j] * st, 1e-4), 1e4);
+                    cstep[j] = nd / dcol[j];
+                    dcol[j] = nd;
+                }
+                for (int r = tid; r < m; r += BT) {
+                    const double st = rnorm[r] > 0.0 ? 1.0 / sqrt(rnorm[r]) : 1.0;
+                    const double nd = fmin(fmax(drow[r] * st, 1e-4), 1e4);
+                    rstep[r] = nd / drow[r];
+                    drow[r] = nd;
+                }
+                __syncthreads();
+                for (int j = tid; j < n; j += BT) {
+                    const double cj = cstep[j];
+                    for (int p = pt.p_rp[j]; p < pt.p_rp[j + 1]; ++p) I.V[p] = (cj * I.V[p]) * cstep[pt.p_ci[p]];
+                    q[j] *= cj;
+                }
+                for (int r = tid; r < m; r += BT) {
+                    const double ri = rstep[r];
+                    for (int p = pt.a_rp[r]; p < pt.a_rp[r + 1]; ++p) Vw[p] = (ri * Vw[p]) * cstep[pt.a_ci[p]];
+                    b[r] *= ri;
+                }
+                __syncthreads();
+            }
+            double qm[1] = {0.0};
+            for (int k = tid; k < n; k += BT) qm[0] = fmax(qm[0], fabs(q[k]));
+            breduce<1>(qm, 1u, sred);
+            const double qmax = n ? qm[0] : 0.0;
+            cobj = qmax == 0.0 ? 1.0 : fmin(fmax(1.0 / qmax, 1e-4), 1e4);
+            for (int k = tid; k < pt.nnz_p; k += BT) I.V[k] = I.V[k] * cobj;
+            for (int k = tid; k < n; k += BT) q[k] = q[k] * cobj;
+        } else {
+            cobj = 1.0;
+        }
+        for (int k = tid; k < n; k += BT) dc[k] = dcol[k];
+        for (int k = tid; k < m; k += BT) dr[k] = drow[k];
+        if (tid == 0) bd.out_cobj[inst] = cobj;
+    } else {
+        for (int k = tid; k < pt.nnz_p + pt.nnz_a; k += BT) I.V[k] = gV[k];
+        for (int k = tid; k < n; k += BT) q[k] = q_in[k];
+        for (int k = tid; k < m; k += BT) b[k] = b_in[k];
+        cobj = bd.c_obj[inst];
+        norm_q = bd.norm_q[inst];
+        norm_b = bd.norm_b[inst];
+    }
+    __syncthreads();
     // unit start (set.py:91-112): x = 0, zero block 0, nonneg 1
     for (int k = tid; k < n; k += BT) I.x[k] = 0.0;
     for (int k = tid; k < m; k += BT) {
@@ -531,8 +617,25 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
     double* ox = bd.out_x + (int64_t)inst * n;
     double* oz = bd.out_z + (int64_t)inst * m;
     double* os = bd.out_s + (int64_t)inst * m;
-    for (int k = tid; k < n; k += BT) ox[k] = px[k];
-    for (int k = tid; k < m; k += BT) { oz[k] = pz[k]; os[k] = ps[k]; }
+    if (bd.device_setup) {
+        // recovery on the device (ipm.py:383-407): unscale x = Dc x, z = Dr z / c, s = s / Dr,
+        // divide by tau unless an infeasibility certificate, back to the user's row order
+        const bool cert = final_status == BS_PRIMAL_INF || final_status == BS_DUAL_INF;
+        const double tau_f = res[4];
+        for (int k = tid; k < n; k += BT) {
+            const double v = dc[k] * px[k];
+            ox[k] = cert ? v : v / tau_f;
+        }
+        for (int k = tid; k < m; k += BT) {
+            const double zu = dr[k] * pz[k] / cobj, su = ps[k] / dr[k];
+            const int u = pt.b_src[k];
+            oz[u] = cert ? zu : zu / tau_f;
+            os[u] = cert ? su : su / tau_f;
+        }
+    } else {
+        for (int k = tid; k < n; k += BT) ox[k] = px[k];
+        for (int k = tid; k < m; k += BT) { oz[k] = pz[k]; os[k] = ps[k]; }
+    }
     if (tid == 0) {
         bd.out_status[inst] = final_status;
         for (int k = 0; k < 9; ++k) bd.out_res[(int64_t)inst * 9 + k] = res[k];
@@ -544,7 +647,7 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
 size_t batch_smem_doubles(const BatchPattern& pt) {
     const int64_t n = pt.n, m = pt.m, dim = n + m;
     auto r2 = [](int64_t c) { return (c + 1) & ~int64_t(1); };
-    return (size_t)(r2(n) * 4 + r2(m) * 12 + r2(dim) * 7 + r2(pt.nnz_p + pt.nnz_a) + r2(pt.nnz_l) + r2(dim) * 2);
+    return (size_t)(r2(n) * 5 + r2(m) * 13 + r2(dim) * 7 + r2(pt.nnz_p + pt.nnz_a) + r2(pt.nnz_l) + r2(dim) * 2);
 }
 
 int batch_launch(const BatchPattern& pt, const BatchData& bd, int count, cudaStream_t stream, int smem_bytes) {
@@ -782,11 +885,12 @@ int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings
     BTRY(balloc(h, &tmp, count * nv)); bd.V = tmp;
     BTRY(balloc(h, &tmp, count * n)); bd.q = tmp;
     BTRY(balloc(h, &tmp, count * m)); bd.b = tmp;
-    BTRY(balloc(h, &tmp, count * m)); bd.dr = tmp;
-    BTRY(balloc(h, &tmp, count * n)); bd.dc = tmp;
+    BTRY(balloc(h, &bd.dr, count * m));
+    BTRY(balloc(h, &bd.dc, count * n));
     BTRY(balloc(h, &tmp, count)); bd.c_obj = tmp;
     BTRY(balloc(h, &tmp, count)); bd.norm_q = tmp;
     BTRY(balloc(h, &tmp, count)); bd.norm_b = tmp;
+    BTRY(balloc(h, &bd.out_cobj, count));
     BTRY(balloc(h, &bd.best_x, count * n));
     BTRY(balloc(h, &bd.best_z, count * m));
     BTRY(balloc(h, &bd.best_s, count * m));
@@ -853,7 +957,31 @@ int cipm_batch_set_values(cipm_batch* h, const double* V, const double* q, const
     if (!rc) rc = cp(h->bd.c_obj, c_obj, c);
     if (!rc) rc = cp(h->bd.norm_q, norm_q, c);
     if (!rc) rc = cp(h->bd.norm_b, norm_b, c);
+    h->bd.device_setup = 0;
     return rc;
+}
+
+int cipm_batch_set_reorder(cipm_batch* h, const int64_t* row_perm, const int64_t* a_src) {
+    using namespace cipm;
+    if (!h) return CIPM_E_ARG;
+    const int64_t m = h->pt.m, nnza = h->pt.nnz_a;
+    std::vector<int32_t> bs(row_perm, row_perm + m), as(a_src, a_src + nnza);
+    int rc = bup(h, &h->pt.b_src, bs);
+    if (!rc) rc = bup(h, &h->pt.a_src, as);
+    return rc;
+}
+
+int cipm_batch_set_raw_values(cipm_batch* h, const double* V, const double* q, const double* b, int equilibrate) {
+    if (!h || !h->pt.b_src) return CIPM_E_ARG;
+    const int64_t c = h->count, n = h->pt.n, m = h->pt.m, nv = (int64_t)h->pt.nnz_p + h->pt.nnz_a;
+    CIPM_CUDA(cudaSetDevice(h->device));
+    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.V, V, sizeof(double) * c * nv, cudaMemcpyHostToDevice, h->stream));
+    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.q, q, sizeof(double) * c * n, cudaMemcpyHostToDevice, h->stream));
+    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.b, b, sizeof(double) * c * m, cudaMemcpyHostToDevice, h->stream));
+    h->h2d += (int64_t)sizeof(double) * c * (nv + n + m);
+    h->bd.device_setup = 1;
+    h->bd.equilibrate = equilibrate ? 1 : 0;
+    return CIPM_OK;
 }
 
 int cipm_batch_solve(cipm_batch* h, double* ms) {

@@ -22,12 +22,16 @@ struct BatchPattern {
     const int32_t* perm = nullptr;                           // permuted position -> KKT index
     const int32_t *lp = nullptr, *li = nullptr;              // L column pointers / rows
     const int32_t *up_ptr = nullptr, *up_i = nullptr, *up_p2 = nullptr;   // up-looking schedule
+    const int32_t *a_src = nullptr, *b_src = nullptr;        // user -> reordered A values / rows
 };
 
 // Per-instance data (device pointers, instance-major) and settings.
 struct BatchData {
-    const double *V = nullptr, *q = nullptr, *b = nullptr, *dr = nullptr, *dc = nullptr;
+    const double *V = nullptr, *q = nullptr, *b = nullptr;
+    double *dr = nullptr, *dc = nullptr;      // device_setup: written by the kernel
     const double *c_obj = nullptr, *norm_q = nullptr, *norm_b = nullptr;
+    double* out_cobj = nullptr;
+    int device_setup = 0, equilibrate = 1;
     double *best_x = nullptr, *best_z = nullptr, *best_s = nullptr;
     double *out_x = nullptr, *out_z = nullptr, *out_s = nullptr, *out_res = nullptr;
     int32_t* out_status = nullptr;

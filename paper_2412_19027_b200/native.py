@@ -102,6 +102,8 @@ _SIGS = {
     "cipm_batch_info": ([c_void_p, P_I64], ctypes.c_int),
     "cipm_batch_set_values": ([c_void_p, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_batch_solve": ([c_void_p, P_DBL], ctypes.c_int),
+    "cipm_batch_set_reorder": ([c_void_p, P_I64, P_I64], ctypes.c_int),
+    "cipm_batch_set_raw_values": ([c_void_p, P_DBL, P_DBL, P_DBL, ctypes.c_int], ctypes.c_int),
     "cipm_batch_results": ([c_void_p, ctypes.POINTER(ctypes.c_int32), P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_batch_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_batch_destroy": ([c_void_p], None),
