@@ -325,11 +325,8 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
         }
         tb += o - b;
     }
-    if (parent < 0) return -1;
-    atomic_max_pos(a.maxd + parent, runmax);
-    if (a.desc32[(int64_t)parent * 8 + 6] != 0) return -1;     // parent factored by another tier
-    const int old = atomic_add_acq_rel(a.count + parent, 1);
-    return old == a.need[2 * parent + 1] - 1 ? parent : -1;
+    if (parent >= 0) atomic_max_pos(a.maxd + parent, runmax);
+    return -1;     // tiny leaves are excluded from the child counts (separate launch)
 }
 
 template <typename T>
@@ -388,6 +385,14 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
     }
 }
 
+// tiny leaves: one thread each (launched before the warp tier)
+template <typename T>
+__global__ void __launch_bounds__(128) factor_tiny_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+                                                          T* __restrict__ inbox) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < a.ntiny) factor_tiny_lane(a.tiny[k], a, lval, dvec, inbox);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                          T* __restrict__ inbox) {
@@ -400,24 +405,6 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
     if (lane == 0) mbar_init(&bars[wid], 1);
     __syncwarp();
     uint32_t phase = 0;
-    // phase 1: tiny leaves, 32 per warp (one per lane); completed parents continue as warp tasks
-    for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        if ((int64_t)chunk * 32 >= a.ntiny) break;
-        const int idx = chunk * 32 + lane;
-        const int J = idx < a.ntiny ? a.tiny[idx] : -1;
-        const int ready = J >= 0 ? factor_tiny_lane(J, a, lval, dvec, inbox) : -1;
-        unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
-        __syncwarp();
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            const int P = __shfl_sync(0xffffffffu, ready, l);
-            factor_warp_chain(P, a, lval, dvec, inbox, sp, sD[wid], sSg[wid], &bars[wid], phase);
-        }
-    }
     // phase 2: the other seeds of the tier, by ticket
     for (;;) {
         int J = -1;
@@ -769,7 +756,8 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
     for (int j = 0; j < W; ++j)
 #pragma unroll
         for (int i = 0; i < 16; ++i) p[j][i] = (i < r && i > j) ? L[j * r + i] : (T)0;
-    const int needP = parent >= 0 ? a.need[2 * parent] : 0;
+    const int needP = 0;
+    (void)parent;
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xJ = x + (int64_t)q * a.dim + c0;
@@ -792,9 +780,8 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
             vq[a.vpush_pos[cvo + i - W]] = acc;
         }
     }
-    if (parent < 0) return -1;
-    const int old = atomic_add_acq_rel(a.count + parent, 1);
-    return old == needP - 1 ? parent : -1;
+    (void)needP;
+    return -1;     // tiny leaves are excluded from the child counts (separate launch)
 }
 
 template <typename T>
@@ -871,8 +858,18 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
     }
 }
 
+// tiny leaves, forward: one thread each (launched before the persistent sweep)
 template <typename T>
-__global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
+__global__ void __launch_bounds__(128) fwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
+    SolveArgs a = a0;
+    resolve_act(a.rstate, a.act0, a.act1);
+    if (!a.act0 && !a.act1) return;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < a.ntiny) fwd_tiny_lane(a.tiny[k], a, lval, x, vin);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SW * 32, 3) forward_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
     SolveArgs a = a0;
     resolve_act(a.rstate, a.act0, a.act1);
     if (!a.act0 && !a.act1) return;
@@ -884,23 +881,6 @@ __global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a0, const T*
     if (lane == 0) mbar_init(&bars[wid], 1);
     __syncwarp();
     uint32_t phase = 0;
-    // phase 1: tiny leaves, one per lane; completed parents continue as warp tasks
-    for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        if ((int64_t)chunk * 32 >= a.ntiny) break;
-        const int idx = chunk * 32 + lane;
-        const int J = idx < a.ntiny ? a.tiny[idx] : -1;
-        const int ready = J >= 0 ? fwd_tiny_lane(J, a, lval, x, vin) : -1;
-        unsigned m = __ballot_sync(0xffffffffu, ready >= 0);
-        __syncwarp();
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            fwd_chain(__shfl_sync(0xffffffffu, ready, l), a, lval, x, vin, slice, colsum[wid], &bars[wid], phase);
-        }
-    }
     // phase 2: remaining seeds by ticket
     for (;;) {
         int J = -1;
@@ -915,6 +895,29 @@ __global__ void __launch_bounds__(SW * 32) forward_kernel(SolveArgs a0, const T*
 }
 
 // backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
+// tiny leaves, backward: one thread each, launched after the persistent sweep
+template <typename T, int W>
+__device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+                                           const T* __restrict__ dvec, T* x);
+
+template <typename T>
+__global__ void __launch_bounds__(128) bwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval,
+                                                       const T* __restrict__ dvec, T* x) {
+    SolveArgs a = a0;
+    resolve_act(a.rstate, a.act0, a.act1);
+    if (!a.act0 && !a.act1) return;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= a.ntiny) return;
+    const int J = a.tiny[k];
+    const int32_t* d32 = a.desc32 + (int64_t)J * 8;
+    switch (d32[1]) {
+        case 1: bwd_tiny_w<T, 1>(J, d32, a, lval, dvec, x); break;
+        case 2: bwd_tiny_w<T, 2>(J, d32, a, lval, dvec, x); break;
+        case 3: bwd_tiny_w<T, 3>(J, d32, a, lval, dvec, x); break;
+        default: bwd_tiny_w<T, 4>(J, d32, a, lval, dvec, x); break;
+    }
+}
+
 // tiny leaf, backward: x_J = L11^-T (D^-1 x_J - L_off' x_off) once the parent is final
 template <typename T, int W>
 __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
@@ -933,7 +936,7 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
     T dinv[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) dinv[j] = dvec[c0 + j];
-    if (parent >= 0) wait_ge(a.count + parent, 1);
+    (void)parent;      // the persistent backward sweep finished before this launch
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xv = x + (int64_t)q * a.dim;
@@ -957,7 +960,7 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
 }
 
 template <typename T>
-__global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a0, const T* __restrict__ lval,
+__global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, const T* __restrict__ lval,
                                                            const T* __restrict__ dvec, T* x) {
     SolveArgs a = a0;
     resolve_act(a.rstate, a.act0, a.act1);
@@ -974,7 +977,7 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a0, const T
         int t = 0;
         if (lane == 0) t = atomicAdd(a.ticket, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.n_main) break;
+        if (t >= a.n_main) return;
         const int J = a.order[a.n_main - 1 - t];     // a.order = bwd_order here
         const Desc d = load_desc(a.desc32, a.desc64, J);
         const int c0 = d.c0, w = d.w, r = d.r;
@@ -1003,24 +1006,6 @@ __global__ void __launch_bounds__(SW * 32) backward_kernel(SolveArgs a0, const T
         }
         __syncwarp();
         if (lane == 0) st_release(a.count + J, 1);
-    }
-    // phase 2: tiny leaves, one per lane (nobody waits on a leaf)
-    for (;;) {
-        int chunk = 0;
-        if (lane == 0) chunk = atomicAdd(a.ticket_tiny, 1);
-        chunk = __shfl_sync(0xffffffffu, chunk, 0);
-        if ((int64_t)chunk * 32 >= a.ntiny) return;
-        const int idx = chunk * 32 + lane;
-        if (idx < a.ntiny) {
-            const int J = a.tiny[idx];
-            const int32_t* d32 = a.desc32 + (int64_t)J * 8;
-            switch (d32[1]) {
-                case 1: bwd_tiny_w<T, 1>(J, d32, a, lval, dvec, x); break;
-                case 2: bwd_tiny_w<T, 2>(J, d32, a, lval, dvec, x); break;
-                case 3: bwd_tiny_w<T, 3>(J, d32, a, lval, dvec, x); break;
-                default: bwd_tiny_w<T, 4>(J, d32, a, lval, dvec, x); break;
-            }
-        }
     }
 }
 
@@ -1122,12 +1107,17 @@ int factor_t(Ctx& c) {
     }
     const int ns_warp = (int)c.host_sym.start_fac_warp.size(), ns_cta = (int)c.host_sym.start_fac_cta.size();
     const int ntiny = (int)c.host_sym.tiny.size();
-    if (ns_warp + ntiny > 0) {
+    if (ntiny > 0) {
+        a.ntiny = ntiny;
+        a.tiny = c.sym.tiny;
+        factor_tiny_kernel<T><<<grid_for(ntiny, 128), 128, 0, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+        c.launches++;
+    }
+    if (ns_warp > 0) {
         a.tier = 0;
         a.nstart = ns_warp;
         a.start = c.sym.start_fac_warp;
-        a.ntiny = ntiny;
-        a.tiny = c.sym.tiny;
+        a.ntiny = 0;
         a.ticket_tiny = c.tickets + 4;
         a.ticket = c.tickets;
         a.smem_cap = c.factor_slice;
@@ -1171,13 +1161,22 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     f.ticket_tiny = c.tickets + 5;
     f.trace = c.trace;
     const size_t ssm = sizeof(T) * (size_t)c.solve_slice * SW;
-    if (f.nstart + f.ntiny > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    if (f.ntiny > 0) {
+        fwd_tiny_kernel<T><<<grid_for(f.ntiny, 128), 128, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+        c.launches++;
+    }
+    f.ntiny = 0;
+    if (f.nstart > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     k_tail_forward(c, t, act0, act1);
     k_tail_backward(c, t, act0, act1);
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
     b.ticket_tiny = c.tickets + 6;
-    if (b.n_main + b.ntiny > 0)
+    if (b.n_main > 0)
         backward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+    if (b.ntiny > 0) {
+        bwd_tiny_kernel<T><<<grid_for(b.ntiny, 128), 128, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+        c.launches++;
+    }
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_solve.emplace_back(e0, e0 + 1);

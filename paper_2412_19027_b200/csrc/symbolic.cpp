@@ -628,10 +628,22 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         const int32_t BIG = 0x3fffffff;
         S.tier.assign(ns, 0);
         for (int32_t J = 0; J < ns; ++J) S.tier[J] = S.is_tail[J] ? 2 : (S.is_mid[J] ? 1 : 0);
+        // tiny leaves (no children, w <= 4, r <= 16): one thread each, in separate
+        // launches before (factor, forward) / after (backward) the persistent kernels,
+        // so they are excluded from the continuation child counts
+        std::vector<char> tiny(ns, 0);
+        S.tiny.clear();
+        for (int32_t J = 0; J < ns; ++J) {
+            const int64_t w = S.sn_col[J + 1] - S.sn_col[J], r = S.sn_rptr[J + 1] - S.sn_rptr[J];
+            if (S.tier[J] == 0 && S.sn_nchild[J] == 0 && w <= 4 && r <= 16) {
+                tiny[J] = 1;
+                S.tiny.push_back(J);
+            }
+        }
         std::vector<int32_t> need_fac(ns, 0), need_solve(ns, 0);
         for (int32_t J = 0; J < ns; ++J) {
             const int32_t P = S.sn_parent[J];
-            if (P < 0) continue;
+            if (P < 0 || tiny[J]) continue;
             if (S.tier[P] != 2) need_solve[P]++;
             if (S.tier[P] == S.tier[J] && S.tier[P] != 2) need_fac[P]++;
         }
@@ -660,16 +672,6 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         for (int32_t J = 0; J < ns; ++J) {
             S.need[2 * (size_t)J] = S.desc32[(size_t)J * 8 + 4];
             S.need[2 * (size_t)J + 1] = S.desc32[(size_t)J * 8 + 5];
-        }
-        // tiny leaves (no children, w <= 4, r <= 16) are processed one per lane
-        std::vector<char> tiny(ns, 0);
-        S.tiny.clear();
-        for (int32_t J = 0; J < ns; ++J) {
-            const int64_t w = S.sn_col[J + 1] - S.sn_col[J], r = S.sn_rptr[J + 1] - S.sn_rptr[J];
-            if (S.tier[J] == 0 && S.sn_nchild[J] == 0 && w <= 4 && r <= 16) {
-                tiny[J] = 1;
-                S.tiny.push_back(J);
-            }
         }
         S.start_solve.clear();
         S.start_fac_warp.clear();
