@@ -273,6 +273,10 @@ int cipm_symbolic_array(const cipm_symbolic* sym, const char* name, void* dst, i
     ARR("cv_off", s.cv_off)
     ARR("vpush_pos", s.vpush_pos)
     ARR("vcol_ptr", s.vcol_ptr)
+    ARR("tier", s.tier)
+    ARR("level", s.level)
+    ARR("desc32", s.desc32)
+    ARR("tiny", s.tiny)
 #undef ARR
     if (!es) return CIPM_E_ARG;
     if (count) *count = cnt;

@@ -83,166 +83,183 @@ __global__ void __launch_bounds__(256) tail_gather(T* __restrict__ L, int r, con
 }
 
 // ---------------------------------------------------------------------------
-// diagonal block: unblocked LDL' of the nb x nb block at (kb, kb), right-looking
-// on the unscaled columns (one barrier per column, pivots with the reference's
-// bump rule computed by every thread), then the explicit inverse of the unit
-// lower factor — row-major for the solves, column-major as the B operand of the
-// TRSM-as-GEMM (L21 = A21 L11^-T D^-1).
+// diagonal block: LDL' of the nb x nb block at (kb, kb) with the reference's
+// dynamic-regularisation rule (ldl.py:79-87), then the explicit inverse of its
+// unit lower factor — row-major for the solves, column-major as the B operand
+// of the TRSM-as-GEMM (L21 = A21 L11^-T D^-1).
+//
+// The block sits column-major in shared memory (ld 64, zero outside the lower
+// nb x nb triangle).  Blocked by 16 columns: (a) warp 0 factors the 16 x 16
+// diagonal sub-block with lane i holding row i in registers (shuffles, no
+// barriers), publishing L11' and 1/d; (b) one thread per row below applies the
+// same right-looking elimination in registers; (c) rank-16 update of the
+// trailing sub-matrix.  The inverse: one thread per column j of L^-1 holds that
+// column in registers and eliminates right-looking down the 64 rows (column k
+// of L is a contiguous, broadcast shared-memory read).
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int kb, int nb, int c0,
                                                  T* __restrict__ dvec, const int8_t* __restrict__ sign,
                                                  double* maxd, int32_t* bumps, int* err, double delta_s,
                                                  double delta_d, T* __restrict__ inv_rm, T* __restrict__ inv_cm) {
-    // blocked in 16-column sub-panels: (a) one warp factors the 16x16 sub-diagonal
-    // block with its rows in registers, (b) one thread per row below solves
-    // against it, (c) all threads apply the rank-16 update; 2 barriers per sub-panel
     constexpr int SB = 16;
-    constexpr int LD = TB + 1;
     extern __shared__ __align__(16) unsigned char dsm_raw[];
-    T* S = reinterpret_cast<T*>(dsm_raw);          // S[i * LD + j], i >= j
-    T* I = S + TB * LD;                            // inverse, I[i * LD + j]
+    T* S = reinterpret_cast<T*>(dsm_raw);          // S[j * TB + i]: column-major block
+    T* DL = S + TB * TB;                           // (TB - SB) x SB: d_k l_ck of the trailing columns
     __shared__ T sD[TB];
+    __shared__ T sInv[SB];
+    __shared__ __align__(16) T sLt[SB * SB];
     __shared__ int8_t sSg[TB];
     __shared__ double s_runmax;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
     T* B = L + (int64_t)kb * r + kb;
-    for (int idx = tid; idx < nb * nb; idx += nt) {
-        const int i = idx % nb, j = idx / nb;
-        if (i >= j) S[i * LD + j] = B[(int64_t)j * r + i];
+    for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int i = idx & (TB - 1), j = idx >> 6;
+        S[idx] = (i < nb && j < nb && i >= j) ? B[(int64_t)j * r + i] : (T)0;
     }
     if (tid < nb) sSg[tid] = sign[c0 + kb + tid];
     if (tid == 0) s_runmax = *maxd;
     __syncthreads();
     for (int k0 = 0; k0 < nb; k0 += SB) {
         const int nbk = min(SB, nb - k0);
-        // (a) sub-diagonal block, lanes 0..15 own rows k0 + lane (unscaled right-looking)
+        T* Sk = S + k0 * TB;                       // column k0
+        // (a) diagonal sub-block, lane i owns row k0 + i
         if (wid == 0) {
             double runmax = s_runmax;
-            T row[SB];
+            T x[SB];
 #pragma unroll
-            for (int c = 0; c < SB; ++c)
-                row[c] = (lane < nbk && c <= lane && c < nbk) ? S[(k0 + lane) * LD + k0 + c] : (T)0;
+            for (int c = 0; c < SB; ++c) x[c] = (lane < nbk && c <= lane) ? Sk[c * TB + k0 + lane] : (T)0;
 #pragma unroll
             for (int j = 0; j < SB; ++j) {
-                if (j >= nbk) break;
-                double dd = (double)__shfl_sync(0xffffffffu, row[j], j);
-                const double bound = delta_s + delta_d * runmax;
-                const bool bump = fabs(dd) < bound;
-                if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
-                const T dt = (T)dd;
-                runmax = fmax(runmax, fabs(dd));
-                if (lane == 0) {
-                    if (bump) atomicAdd(bumps, 1);
-                    if (dt == (T)0) set_error(err, CIPM_E_FACTOR);
-                    sD[k0 + j] = dt;
-                    dvec[c0 + kb + k0 + j] = dt;
-                }
-                const T inv_d = (T)1 / dt;
-                const T lij = row[j] * inv_d;           // l_ij (valid on lanes i > j)
+                if (j < nbk) {
+                    double dd = (double)__shfl_sync(0xffffffffu, x[j], j);
+                    const double bound = delta_s + delta_d * runmax;
+                    const bool bump = fabs(dd) < bound;
+                    if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
+                    const T dt = (T)dd;
+                    runmax = fmax(runmax, fabs(dd));
+                    const T inv = (T)1 / dt;
+                    if (lane == 0) {
+                        if (bump) atomicAdd(bumps, 1);
+                        if (dt == (T)0) set_error(err, CIPM_E_FACTOR);
+                        sD[k0 + j] = dt;
+                        sInv[j] = inv;
+                        dvec[c0 + kb + k0 + j] = dt;
+                    }
+                    const T xj = x[j];
 #pragma unroll
-                for (int c = j + 1; c < SB; ++c) {
-                    const T acj = __shfl_sync(0xffffffffu, row[j], c);   // unscaled A(c, j)
-                    if (lane >= c) row[c] -= lij * acj;
+                    for (int c = j + 1; c < SB; ++c) {
+                        const T acj = __shfl_sync(0xffffffffu, xj, c);
+                        if (lane >= c) x[c] -= xj * (acj * inv);
+                    }
+                    x[j] = lane > j ? xj * inv : (lane == j ? (T)1 : x[j]);
+                } else if (lane == 0) {
+                    sInv[j] = (T)0;
                 }
-                if (lane > j) row[j] = lij;
-                else if (lane == j) row[j] = (T)1;
             }
+            int row = k0 + lane;
+            asm volatile("" : "+r"(row));
 #pragma unroll
-            for (int c = 0; c < SB; ++c)
-                if (lane < nbk && c <= lane && c < nbk) S[(k0 + lane) * LD + k0 + c] = row[c];
+            for (int c = 0; c < SB; ++c) {
+                if (lane < nbk && c <= lane) Sk[c * TB + row] = x[c];
+                if (lane < SB) sLt[c * SB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;
+            }
             if (lane == 0) s_runmax = runmax;
         }
         __syncthreads();
-        const int rest = nb - k0 - nbk;
-        if (rest > 0) {
-            // (b) rows below the sub-panel: l_ij = (a_ij - sum_{k<j} l_ik d_k l_jk) / d_j
-            for (int i = k0 + nbk + tid; i < nb; i += nt) {
-                T* Si = S + i * LD + k0;
+        const int c1 = k0 + nbk, rest = nb - c1;
+        if (rest <= 0) break;
+        // (b) rows below the sub-block
+        for (int i = c1 + tid; i < nb; i += nt) {
+            T x[SB];
 #pragma unroll
-                for (int j = 0; j < SB; ++j) {
-                    if (j >= nbk) break;
-                    T v = Si[j];
-                    const T* Sj = S + (k0 + j) * LD + k0;
+            for (int c = 0; c < SB; ++c) x[c] = Sk[c * TB + i];
 #pragma unroll
-                    for (int k = 0; k < j; ++k) v -= Si[k] * sD[k0 + k] * Sj[k];
-                    Si[j] = v / sD[k0 + j];
-                }
+            for (int j = 0; j < SB; ++j) {
+                const T xj = x[j];
+#pragma unroll
+                for (int c = j + 1; c < SB; ++c) x[c] -= xj * sLt[j * SB + c];
+                x[j] = xj * sInv[j];
             }
-            __syncthreads();
-            // (c) rank-nbk update of the trailing block: A(i,c) -= sum_k l_ik d_k l_ck
-            const int c1 = k0 + nbk;
-            const int tot = rest * rest;
-            for (int idx = tid; idx < tot; idx += nt) {
-                const int i = c1 + idx % rest, c = c1 + idx / rest;
-                if (i < c) continue;
-                const T* Si = S + i * LD + k0;
-                const T* Sc = S + c * LD + k0;
+            int is = i;
+            asm volatile("" : "+r"(is));
+#pragma unroll
+            for (int c = 0; c < SB; ++c) Sk[c * TB + is] = x[c];
+        }
+        // d_k l_ck of the trailing columns (reads the rows just finished: own thread only)
+        __syncthreads();
+        for (int idx = tid; idx < rest * SB; idx += nt) {
+            const int cc = idx / SB, k = idx - cc * SB;
+            DL[idx] = sD[k0 + k] * Sk[k * TB + c1 + cc];
+        }
+        __syncthreads();
+        // (c) trailing columns c >= c1, rows i >= c: A(i,c) -= sum_k l_ik d_k l_ck
+        for (int c = c1 + wid; c < nb; c += nw) {
+            const T* dl = DL + (c - c1) * SB;
+            for (int i = c + lane; i < nb; i += 32) {
                 T acc = (T)0;
 #pragma unroll
-                for (int k = 0; k < SB; ++k)
-                    if (k < nbk) acc += Si[k] * sD[k0 + k] * Sc[k];
-                S[i * LD + c] -= acc;
+                for (int k = 0; k < SB; ++k) acc += Sk[k * TB + i] * dl[k];
+                S[c * TB + i] -= acc;
             }
-            __syncthreads();
         }
+        __syncthreads();
     }
     for (int idx = tid; idx < nb * nb; idx += nt) {
         const int i = idx % nb, j = idx / nb;
-        if (i >= j) B[(int64_t)j * r + i] = S[i * LD + j];
+        if (i >= j) B[(int64_t)j * r + i] = S[j * TB + i];
     }
-    // inverse of the unit lower block by recursive doubling (padded to 64 with the identity):
-    // 16x16 diagonal blocks by 4 warps, then [A 0; C B]^-1 = [Ai 0; -Bi C Ai Bi] for 16 and 32
-    T* Tm = I + TB * LD;                            // 32 x (32+1) scratch
-    auto Lp = [&](int i, int j) -> T {
-        if (i < nb && j < nb) return i > j ? S[i * LD + j] : (i == j ? (T)1 : (T)0);
-        return i == j ? (T)1 : (T)0;
-    };
-    for (int idx = tid; idx < TB * LD; idx += nt) I[idx] = (T)0;
-    __syncthreads();
-    if (wid < TB / SB && lane < SB) {
-        const int bb = wid * SB, col = bb + lane;
-        I[col * LD + col] = (T)1;
-        for (int i = lane + 1; i < SB; ++i) {
-            T v = (T)0;
-            for (int k = lane; k < i; ++k) v -= Lp(bb + i, bb + k) * I[(bb + k) * LD + col];
-            I[(bb + i) * LD + col] = v;
+    if (tid == 0) *maxd = s_runmax;
+    // inverse of the unit lower block by 16 x 16 blocks: X_ii = L_ii^-1 (thread per
+    // column, registers), then block rows bi = 1..3: X_ij = -X_ii sum_{k=j}^{bi-1} L_ik X_kj.
+    // Compact loops: this kernel runs once per diagonal block, from a cold i-cache.
+    constexpr int XL = TB + 1;
+    T* X = DL + (TB - SB) * SB;                    // X[col * XL + row]
+    T* Tm = X + TB * XL;                           // 3 x 16 x 16 scratch
+    if (tid < TB) {
+        const int base = tid & ~(SB - 1), jj = tid & (SB - 1);
+        T x[SB];
+#pragma unroll
+        for (int rr = 0; rr < SB; ++rr) x[rr] = rr == jj ? (T)1 : (T)0;
+#pragma unroll
+        for (int k = 0; k < SB - 1; ++k) {
+            const T xk = x[k];
+#pragma unroll
+            for (int rr = k + 1; rr < SB; ++rr) x[rr] -= S[(base + k) * TB + base + rr] * xk;
         }
+#pragma unroll
+        for (int rr = 0; rr < SB; ++rr) X[(base + jj) * XL + base + rr] = x[rr];
     }
     __syncthreads();
-    for (int sz = SB; sz < TB; sz *= 2) {
-        const int npair = TB / (2 * sz);
-        // Tm = C * Ai for every pair (C = L[bb+sz.., bb..], Ai = I[bb.., bb..])
-        for (int idx = tid; idx < npair * sz * sz; idx += nt) {
-            const int pr = idx / (sz * sz), e = idx % (sz * sz), i = e / sz, j = e % sz;
-            const int bb = pr * 2 * sz;
+    for (int bi = 1; bi < TB / SB; ++bi) {
+        for (int e = tid; e < bi * SB * SB; e += nt) {
+            const int bj = e >> 8, rr = e & (SB - 1), cc = (e >> 4) & (SB - 1);
             T acc = (T)0;
-            for (int k = j; k < sz; ++k) acc += Lp(bb + sz + i, bb + k) * I[(bb + k) * LD + bb + j];
-            Tm[(pr * sz + i) * (TB / 2 + 1) + j] = acc;
+            for (int k = bj * SB; k < bi * SB; ++k) acc += S[k * TB + bi * SB + rr] * X[(bj * SB + cc) * XL + k];
+            Tm[e] = acc;                           // Tm[bj](rr, cc)
         }
         __syncthreads();
-        // lower-left block = -Bi * Tm (Bi = I[bb+sz.., bb+sz..], unit lower)
-        for (int idx = tid; idx < npair * sz * sz; idx += nt) {
-            const int pr = idx / (sz * sz), e = idx % (sz * sz), i = e / sz, j = e % sz;
-            const int bb = pr * 2 * sz;
+        for (int e = tid; e < bi * SB * SB; e += nt) {
+            const int bj = e >> 8, rr = e & (SB - 1), cc = (e >> 4) & (SB - 1);
+            const T* Tb = Tm + bj * SB * SB + cc * SB;
             T acc = (T)0;
-            for (int k = 0; k <= i; ++k) acc += I[(bb + sz + i) * LD + bb + sz + k] * Tm[(pr * sz + k) * (TB / 2 + 1) + j];
-            I[(bb + sz + i) * LD + bb + j] = -acc;
+#pragma unroll 4
+            for (int m = 0; m < SB; ++m) acc += X[(bi * SB + m) * XL + bi * SB + rr] * Tb[m];
+            X[(bj * SB + cc) * XL + bi * SB + rr] = -acc;
         }
         __syncthreads();
     }
     for (int idx = tid; idx < TB * TB; idx += nt) {
-        const int i = idx / TB, j = idx % TB;
-        const T v = (i < nb && j <= i) ? I[i * LD + j] : (T)0;
-        inv_rm[idx] = v;                 // row-major: inv(i, j)
-        inv_cm[j * TB + i] = v;          // column-major copy
+        const int hi = idx >> 6, lo = idx & (TB - 1);
+        // column-major copy: (row lo, column hi); row-major: (row hi, column lo)
+        inv_cm[idx] = (lo < nb && (lo >> 4) >= (hi >> 4)) ? X[hi * XL + lo] : (T)0;
+        inv_rm[idx] = (hi < nb && (hi >> 4) >= (lo >> 4)) ? X[lo * XL + hi] : (T)0;
     }
-    if (tid == 0) *maxd = s_runmax;
 }
 
 template <typename T>
 constexpr int diag_smem() {
-    return (int)sizeof(T) * (2 * TB * (TB + 1) + (TB / 2) * (TB / 2 + 1));
+    return (int)sizeof(T) * (TB * TB + (TB - 16) * 16 + TB * (TB + 1) + 3 * 16 * 16);
 }
 
 // ---------------------------------------------------------------------------

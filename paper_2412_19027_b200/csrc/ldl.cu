@@ -420,42 +420,134 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
 
 // CTA-tier dense panel LDL' (see factor_cta_kernel); forced inline so the
 // panel pointer keeps its address space (shared -> LDS/STS) at each call site
+//
+// Blocked by 32 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
+// diagonal block with lane i holding row i in registers (warp-synchronous
+// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
+// per row below holds its nbk entries in registers and applies the same
+// right-looking elimination against L11 (broadcast shared-memory reads);
+// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
+// instead of one per column.
+template <typename T, int NB>
+__device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, const int8_t* sSg, T* sD,
+                                               double& s_runmax, const FactorArgs& a, T* sLt, T* sInv) {
+    const int lane = threadIdx.x & 31;
+    double runmax = s_runmax;
+    T x[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+        x[c] = (lane < nbk && c < nbk && c <= lane) ? Pk[c * r + k0 + lane] : (T)0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        if (j < nbk) {
+            double dd = (double)__shfl_sync(0xffffffffu, x[j], j);
+            const double bound = a.delta_s + a.delta_d * runmax;
+            const bool bump = fabs(dd) < bound;
+            if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
+            const T dt = (T)dd;
+            runmax = fmax(runmax, fabs(dd));
+            const T inv = (T)1 / dt;
+            if (lane == 0) {
+                if (bump) atomicAdd(a.bumps, 1);
+                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+                sD[k0 + j] = dt;
+                sInv[j] = inv;
+            }
+            const T xj = x[j];                   // unscaled a_ij (lanes i > j)
+#pragma unroll
+            for (int c = j + 1; c < NB; ++c) {
+                const T acj = __shfl_sync(0xffffffffu, xj, c);   // unscaled a_cj
+                if (lane >= c) x[c] -= xj * (acj * inv);
+            }
+            x[j] = lane > j ? xj * inv : (lane == j ? (T)1 : x[j]);
+        } else if (lane == 0) {
+            sInv[j] = (T)0;
+        }
+    }
+    int row = k0 + lane;
+    asm volatile("" : "+r"(row));            // recompute the store addresses (no 32 live pointers)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+        if (lane < nbk && c < nbk && c <= lane) Pk[c * r + row] = x[c];
+        if (lane < NB) sLt[c * NB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;   // Lt[j][i] = l_ij
+    }
+    if (lane == 0) s_runmax = runmax;
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void cta_below_rows(T* Pk, int r, int i0, int nbk, const T* sLt, const T* sInv) {
+#pragma unroll 1
+    for (int i = i0 + threadIdx.x; i < r; i += blockDim.x) {
+        T x[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) x[c] = c < nbk ? Pk[c * r + i] : (T)0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const T xj = x[j];
+#pragma unroll
+            for (int c = j + 1; c < NB; ++c) x[c] -= xj * sLt[j * NB + c];
+            x[j] = xj * sInv[j];
+            asm volatile("" ::: "memory");      // L11 row loads per step (register budget)
+        }
+        int is = i;
+        asm volatile("" : "+r"(is));         // recompute the store addresses (no 32 live pointers)
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+            if (c < nbk) Pk[c * r + is] = x[c];
+    }
+}
+
+//
+// Blocked by 16 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
+// diagonal block with lane i holding row i in registers (warp-synchronous
+// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
+// per row below holds its nbk entries in registers and applies the same
+// right-looking elimination against L11 (broadcast shared-memory reads);
+// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
+// instead of one per column.
 template <typename T>
 __device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
-                                              const FactorArgs& a, T* __restrict__ dvec) {
-    const int tid = threadIdx.x, nt = blockDim.x, wid = tid >> 5, nw = nt >> 5, lane = tid & 31;
-    double runmax = s_runmax;
-    for (int j = 0; j < w; ++j) {
-        const T* Pj = P + (int64_t)j * r;
-        double dd = (double)Pj[j];
-        const double bound = a.delta_s + a.delta_d * runmax;
-        const bool bump = fabs(dd) < bound;
-        if (bump) dd = sSg[j] > 0 ? bound : -bound;
-        const T dt = (T)dd;
-        runmax = fmax(runmax, fabs(dd));
-        if (tid == 0) {
-            if (bump) atomicAdd(a.bumps, 1);
-            if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-            sD[j] = dt;
-        }
-        const T inv = (T)1 / dt;
-        // warps over columns c > j, lanes over rows i >= c
-        for (int c = j + 1 + wid; c < w; c += nw) {
-            const T f = Pj[c] * inv;
-            T* Pc = P + (int64_t)c * r;
-            for (int i = c + lane; i < r; i += 32) Pc[i] -= Pj[i] * f;
+                                              const FactorArgs& a, T* __restrict__ dvec, T* sLt, T* sInv) {
+    // block width 16: a row of the block in registers, 2 CTAs / SM without spills
+    constexpr int KB = 16;
+    const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
+    for (int k0 = 0; k0 < w; k0 += KB) {
+        const int nbk = min(KB, w - k0);
+        T* Pk = P + k0 * r;               // column k0 of the panel
+        if (wid == 0) {
+            if (nbk <= 8) cta_diag_block<T, 8>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
+            else cta_diag_block<T, KB>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
         }
         __syncthreads();
+        // (b) rows below the diagonal block
+        if (nbk <= 8) cta_below_rows<T, 8>(Pk, r, k0 + nbk, nbk, sLt, sInv);
+        else cta_below_rows<T, KB>(Pk, r, k0 + nbk, nbk, sLt, sInv);
+        __syncthreads();
+        // (c) trailing columns c >= k0 + nbk, rows i >= c: A(i,c) -= sum_k l_ik d_k l_ck
+        //     (only reached with a full block, nbk == KB)
+        const int c1 = k0 + nbk;
+        if (c1 < w) {
+            // d_k l_ck for the trailing columns, into the (now free) L11' buffer
+            for (int idx = tid; idx < (w - c1) * KB; idx += blockDim.x) {
+                const int cc = idx / KB, k = idx - cc * KB;
+                sLt[idx] = sD[k0 + k] * Pk[k * r + c1 + cc];
+            }
+            __syncthreads();
+            for (int c = c1 + wid; c < w; c += nw) {
+                const T* dl = sLt + (c - c1) * KB;
+                T* Pc = P + c * r;
+#pragma unroll 1
+                for (int i = c + (tid & 31); i < r; i += 32) {
+                    T acc = (T)0;
+#pragma unroll 8
+                    for (int k = 0; k < KB; ++k) acc += Pk[k * r + i] * dl[k];
+                    Pc[i] -= acc;
+                }
+            }
+            __syncthreads();
+        }
     }
-    for (int j = wid; j < w; j += nw) {
-        const T inv = (T)1 / sD[j];
-        T* Pj = P + (int64_t)j * r;
-        for (int i = j + 1 + lane; i < r; i += 32) Pj[i] = Pj[i] * inv;
-        if (lane == 0) Pj[j] = (T)1;
-    }
-    for (int j = tid; j < w; j += nt) dvec[c0 + j] = sD[j];
-    if (tid == 0) s_runmax = runmax;
-    __syncthreads();
+    for (int j = tid; j < w; j += blockDim.x) dvec[c0 + j] = sD[j];
 }
 
 
@@ -480,13 +572,15 @@ __device__ __forceinline__ void cta_push(const T* P, int r, int w, int o, int64_
 // gather is split by rows over the CTA's warps, the dense panel LDL' and the
 // contribution block use all threads.  Same continuation protocol.
 template <typename T>
-__global__ void __launch_bounds__(256) factor_cta_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+__global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                          T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sp = reinterpret_cast<T*>(smem_raw);
     __shared__ int s_J, s_needP, s_tierP, s_next;
     __shared__ double s_runmax;
     __shared__ T sD[64];
+    __shared__ __align__(16) T sLt[64 * 16];    // L11' of a 16-column block / d_k l_ck of the trailing columns
+    __shared__ T sInv[16];
     __shared__ int8_t sSg[64];
     __shared__ int32_t s_d32[8];
     __shared__ int64_t s_d64[8];
@@ -540,8 +634,8 @@ __global__ void __launch_bounds__(256) factor_cta_kernel(FactorArgs a, T* __rest
         // 2. dense LDL' of the panel: right-looking on the unscaled columns
         //    (A_ci -= A_ij A_cj / d_j), one barrier per column, pivots computed
         //    redundantly by every thread, columns scaled by 1/d at the end
-        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec);
-        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec);
+        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
+        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
         if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
         // 3. write back, push C_J = L_off D L_off'
         if (in_smem)
