@@ -691,146 +691,193 @@ struct SolveArgs {
 };
 
 // warp-cooperative sums of the vector inbox of one supernode's columns (entries
-// [lo, hi), grouped by column, local column ids in vin_col): colsum[j] = sum of
-// column j's entries.  Four 32-entry chunks are loaded before they are reduced.
-template <typename T>
-__device__ __forceinline__ void vgather_warp(const T* vq, const uint8_t* __restrict__ vin_col, int64_t lo,
-                                             int64_t hi, int w, T* colsum) {
+// [lo, hi), grouped by column, local column ids in vin_col), for NQ right-hand
+// sides at once: cs[q][j] = sum of column j's entries of RHS q.  The entries of
+// every RHS (32 * CH per round trip) are loaded before any is reduced, and the
+// segmented scan shares its column-id shuffles across the RHS.
+template <typename T, int NQ>
+__device__ __forceinline__ void vgather_q(T* const (&vq)[NQ], const uint8_t* __restrict__ vin_col, int64_t lo,
+                                          int64_t hi, int w, T (*cs)[64]) {
+    constexpr int CH = 8 / NQ;
     const int lane = threadIdx.x & 31;
-    for (int j = lane; j < w; j += 32) colsum[j] = (T)0;
-    __syncwarp();
-    for (int64_t base = lo; base < hi; base += 512) {
-        T v[16];
-        int col[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {             // one round trip for up to 512 entries
+    for (int q = 0; q < NQ; ++q)
+        for (int j = lane; j < w; j += 32) cs[q][j] = (T)0;
+    __syncwarp();
+    for (int64_t base = lo; base < hi; base += 32 * CH) {
+        T v[NQ][CH];
+        int col[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {             // one round trip for every RHS
             const int64_t e = base + 32 * u + lane;
             const bool ok = e < hi;
-            v[u] = ok ? __ldcg(vq + e) : (T)0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) v[q][u] = ok ? __ldcg(vq[q] + e) : (T)0;
             col[u] = ok ? (int)__ldg(vin_col + e) : -(lane + 2);
         }
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < CH; ++u) {
             if (base + 32 * u >= hi) break;
-            T x = v[u];
             const int cu = col[u];
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const int cp = __shfl_up_sync(0xffffffffu, cu, off);
-                const T vp = __shfl_up_sync(0xffffffffu, x, off);
-                if (lane >= off && cp == cu) x += vp;
+                const bool take = lane >= off && cp == cu;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const T vp = __shfl_up_sync(0xffffffffu, v[q][u], off);
+                    if (take) v[q][u] += vp;
+                }
             }
             const int cn = __shfl_down_sync(0xffffffffu, cu, 1);
-            if (cu >= 0 && (lane == 31 || cn != cu)) colsum[cu] += x;
+            if (cu >= 0 && (lane == 31 || cn != cu)) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) cs[q][cu] += v[q][u];
+            }
             __syncwarp();
         }
     }
     __syncwarp();
 }
 
-// forward task, compute part: triangle and off-row push for each active RHS.
-// Forced inline so L keeps its address space (staged panel -> LDS).
-template <typename T>
-__device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* x, T* vin,
-                                            const T (&xa)[2], const T (&xb)[2], T (*cs)[64], int J,
-                                            const int64_t (&pos_pf)[2]) {
+// forward task, compute part: triangle and off-row push for NQ right-hand sides
+// together (each L element is read once for all of them).  Forced inline so L
+// keeps its address space (staged panel -> LDS).
+template <typename T, int NQ>
+__device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* const (&xq)[NQ],
+                                            T* const (&vq)[NQ], const T (&xa)[NQ], const T (&xb)[NQ],
+                                            T (*cs)[64], int J, const int64_t (&pos_pf)[2]) {
     const int lane = threadIdx.x & 31;
     const int c0 = d.c0, w = d.w, r = d.r;
-    for (int q = 0; q < 2; ++q) {
-        if (!(q == 0 ? a.act0 : a.act1)) continue;
-        T* xJ = x + (int64_t)q * a.dim + c0;
-        T* vq = vin + (int64_t)q * a.nv;
-        T x0 = (T)0, x1 = (T)0;
-        if (lane < w) x0 = xa[q] - cs[q][lane];
-        if (lane + 32 < w) x1 = xb[q] - cs[q][lane + 32];
-        for (int j0 = 0; j0 < w; j0 += 8) {
-            T l0[8], l1[8];
+    T x0[NQ], x1[NQ];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {           // issue the block's loads before the dependent chain
-                const int j = j0 + k;
-                l0[k] = (j < w && lane > j && lane < w) ? L[j * r + lane] : (T)0;
-                l1[k] = (j < w && lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int j = j0 + k;
-                if (j >= w) break;
-                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-                x0 -= l0[k] * xj;
-                x1 -= l1[k] * xj;
-            }
-        }
-        if (lane < w) xJ[lane] = x0;
-        if (lane + 32 < w) xJ[lane + 32] = x1;
-        if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
-        for (int i0 = w; i0 < r; i0 += 32) {
-            const int i = i0 + lane;
-            const bool ok = i < r;
-            const int ii = ok ? i : r - 1;
-            const int pass = (i0 - w) >> 5;
-            const int64_t pos = pass < 2 ? pos_pf[pass] : (ok ? a.vpush_pos[d.cvo + i - w] : 0);
-            T acc = (T)0;
-#pragma unroll 8
-            for (int k = 0; k < w; ++k) {
-                const T xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-                acc += L[k * r + ii] * xk;
-            }
-            if (ok) vq[pos] = acc;
-        }
-        if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
+    for (int q = 0; q < NQ; ++q) {
+        x0[q] = lane < w ? xa[q] - cs[q][lane] : (T)0;
+        x1[q] = lane + 32 < w ? xb[q] - cs[q][lane + 32] : (T)0;
     }
+    constexpr int KB = 8 / NQ;                  // columns whose loads are issued together
+    for (int j0 = 0; j0 < w; j0 += KB) {
+        T l0[KB], l1[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {          // issue the block's loads before the dependent chain
+            const int j = j0 + k;
+            l0[k] = (j < w && lane > j && lane < w) ? L[j * r + lane] : (T)0;
+            l1[k] = (j < w && lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
+        }
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const int j = j0 + k;
+            if (j >= w) break;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
+                x0[q] -= l0[k] * xj;
+                x1[q] -= l1[k] * xj;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (lane < w) xq[q][c0 + lane] = x0[q];
+        if (lane + 32 < w) xq[q][c0 + lane + 32] = x1[q];
+    }
+    if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
+    for (int i0 = w; i0 < r; i0 += 32) {
+        const int i = i0 + lane;
+        const bool ok = i < r;
+        const int ii = ok ? i : r - 1;
+        const int pass = (i0 - w) >> 5;
+        const int64_t pos = pass < 2 ? pos_pf[pass] : (ok ? a.vpush_pos[d.cvo + i - w] : 0);
+        T acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = (T)0;
+#pragma unroll 8
+        for (int k = 0; k < w; ++k) {
+            const T lk = L[k * r + ii];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[q] += lk * __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+        }
+        if (ok) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) vq[q][pos] = acc[q];
+        }
+    }
+    if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
 }
 
-template <typename T>
+// backward task body for NQ right-hand sides: own values (xa/xb, loaded before
+// the parent wait) D-solved, the ancestors' values at the off rows gathered for
+// every RHS in one round trip (64 rows at a time), then the transposed triangle.
+template <typename T, int NQ>
 __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
-                                         const int32_t* rowsJ, const T* __restrict__ dvec, T* x, T* xo,
-                                         const int (&rows_pf)[2], const T (&d_pf)[2]) {
+                                         const int32_t* rowsJ, T* const (&xq)[NQ], T (*xo)[64],
+                                         const int (&rows_pf)[2], const T (&d_pf)[2], const T (&xa)[NQ],
+                                         const T (&xb)[NQ]) {
     const int lane = threadIdx.x & 31;
-        const T* L0 = L + lane * r;
-        const T* L1 = L + (lane + 32) * r;
-        const bool o0 = lane < w, o1 = lane + 32 < w;
-        for (int q = 0; q < 2; ++q) {
-            if (!(q == 0 ? a.act0 : a.act1)) continue;
-            T* xv = x + (int64_t)q * a.dim;
-            T* xJ = xv + c0;
-            T x0 = o0 ? xJ[lane] / d_pf[0] : (T)0;      // D solve (ldl.py:101-102)
-            T x1 = o1 ? xJ[lane + 32] / d_pf[1] : (T)0;
-            // ancestors' values at the off rows, gathered 64 at a time (coalesced over lanes)
-            for (int i0 = 0; i0 < o; i0 += 64) {
-                const int n = min(64, o - i0);
-                const int ra = i0 == 0 ? rows_pf[0] : (lane < n ? rowsJ[i0 + lane] : 0);
-                const int rb = i0 == 0 ? rows_pf[1] : (lane + 32 < n ? rowsJ[i0 + lane + 32] : 0);
-                if (lane < n) xo[lane] = __ldcg(xv + ra);
-                if (lane + 32 < n) xo[lane + 32] = __ldcg(xv + rb);
-                __syncwarp();
-#pragma unroll 8
-                for (int k = 0; k < n; ++k) {
-                    const T xi = xo[k];
-                    if (o0) x0 -= L0[w + i0 + k] * xi;
-                    if (o1) x1 -= L1[w + i0 + k] * xi;
-                }
-                __syncwarp();
-            }
-            for (int j1 = w - 1; j1 >= 0; j1 -= 8) {
-                T l0[8], l1[8];
+    const T* L0 = L + lane * r;
+    const T* L1 = L + (lane + 32) * r;
+    const bool o0 = lane < w, o1 = lane + 32 < w;
+    T x0[NQ], x1[NQ];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {           // loads first, then the dependent chain
-                    const int j = j1 - k;
-                    l0[k] = (j >= 0 && lane < j) ? L0[j] : (T)0;
-                    l1[k] = (j >= 0 && lane + 32 < j) ? L1[j] : (T)0;
-                }
+    for (int q = 0; q < NQ; ++q) {
+        x0[q] = o0 ? xa[q] / d_pf[0] : (T)0;      // D solve (ldl.py:101-102)
+        x1[q] = o1 ? xb[q] / d_pf[1] : (T)0;
+    }
+    for (int i0 = 0; i0 < o; i0 += 64) {
+        const int n = min(64, o - i0);
+        const int ra = i0 == 0 ? rows_pf[0] : (lane < n ? rowsJ[i0 + lane] : 0);
+        const int rb = i0 == 0 ? rows_pf[1] : (lane + 32 < n ? rowsJ[i0 + lane + 32] : 0);
+        T va[NQ], vb[NQ];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int j = j1 - k;
-                    if (j < 0) break;
-                    const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0 : x1, j & 31);
-                    x0 -= l0[k] * xj;
-                    x1 -= l1[k] * xj;
-                }
-            }
-            if (o0) xJ[lane] = x0;
-            if (o1) xJ[lane + 32] = x1;
+        for (int q = 0; q < NQ; ++q) {
+            va[q] = lane < n ? __ldcg(xq[q] + ra) : (T)0;
+            vb[q] = lane + 32 < n ? __ldcg(xq[q] + rb) : (T)0;
         }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            xo[q][lane] = va[q];
+            xo[q][lane + 32] = vb[q];
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int k = 0; k < n; ++k) {
+            const T la = o0 ? L0[w + i0 + k] : (T)0;
+            const T lb = o1 ? L1[w + i0 + k] : (T)0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xi = xo[q][k];
+                x0[q] -= la * xi;
+                x1[q] -= lb * xi;
+            }
+        }
+        __syncwarp();
+    }
+    constexpr int KB = 8 / NQ;
+    for (int j1 = w - 1; j1 >= 0; j1 -= KB) {
+        T l0[KB], l1[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {          // loads first, then the dependent chain
+            const int j = j1 - k;
+            l0[k] = (j >= 0 && lane < j) ? L0[j] : (T)0;
+            l1[k] = (j >= 0 && lane + 32 < j) ? L1[j] : (T)0;
+        }
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const int j = j1 - k;
+            if (j < 0) break;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
+                x0[q] -= l0[k] * xj;
+                x1[q] -= l1[k] * xj;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (o0) xq[q][c0 + lane] = x0[q];
+        if (o1) xq[q][c0 + lane + 32] = x1[q];
+    }
 }
 
 constexpr int SW = 8;   // warps per solve CTA
@@ -890,9 +937,10 @@ __device__ __forceinline__ int fwd_tiny_lane(int J, const SolveArgs& a, const T*
 }
 
 // one forward task and its continuation chain
-template <typename T>
-__device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __restrict__ lval, T* x, T* vin,
-                                          T* slice, T (*cs)[64], uint64_t* bar, uint32_t& phase) {
+template <typename T, int NQ>
+__device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __restrict__ lval, T* const (&xq)[NQ],
+                                          T* const (&vq)[NQ], T* slice, T (*cs)[64], uint64_t* bar,
+                                          uint32_t& phase) {
     const int lane = threadIdx.x & 31;
     bool have_dn = false;
     Desc dn;                       // descriptor of the parent, prefetched for a continuation
@@ -919,22 +967,21 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         pos_pf[0] = lane < r - w ? __ldg(a.vpush_pos + d.cvo + lane) : 0;
         pos_pf[1] = lane + 32 < r - w ? __ldg(a.vpush_pos + d.cvo + 32 + lane) : 0;
         // 2. own right-hand-side values and the vector inbox of the supernode's columns
-        T xa[2] = {(T)0, (T)0}, xb[2] = {(T)0, (T)0};
-        for (int q = 0; q < 2; ++q) {
-            if (!(q == 0 ? a.act0 : a.act1)) continue;
-            const T* xJ = x + (int64_t)q * a.dim + d.c0;
-            xa[q] = lane < w ? xJ[lane] : (T)0;
-            xb[q] = lane + 32 < w ? xJ[lane + 32] : (T)0;
-            vgather_warp(vin + (int64_t)q * a.nv, a.vin_col, d.vlo, d.vhi, w, cs[q]);
+        T xa[NQ], xb[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            xa[q] = lane < w ? xq[q][d.c0 + lane] : (T)0;
+            xb[q] = lane + 32 < w ? xq[q][d.c0 + lane + 32] : (T)0;
         }
+        vgather_q<T, NQ>(vq, a.vin_col, d.vlo, d.vhi, w, cs);
         if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
         // 3. triangle + push, from shared memory when staged
         if (staged) {
             mbar_wait(bar, phase);
             phase ^= 1u;
-            fwd_compute<T>(slice, a, d, x, vin, xa, xb, cs, J, pos_pf);
+            fwd_compute<T, NQ>(slice, a, d, xq, vq, xa, xb, cs, J, pos_pf);
         } else {
-            fwd_compute<T>(Lg, a, d, x, vin, xa, xb, cs, J, pos_pf);
+            fwd_compute<T, NQ>(Lg, a, d, xq, vq, xa, xb, cs, J, pos_pf);
         }
         dn = desc_from_regs(pv32, pv64);
         __syncwarp();
@@ -984,7 +1031,16 @@ __global__ void __launch_bounds__(SW * 32, 3) forward_kernel(SolveArgs a0, const
         }
         J = __shfl_sync(0xffffffffu, J, 0);
         if (J < 0) return;
-        fwd_chain(J, a, lval, x, vin, slice, colsum[wid], &bars[wid], phase);
+        if (a.act0 && a.act1) {
+            T* const xq[2] = {x, x + a.dim};
+            T* const vq[2] = {vin, vin + a.nv};
+            fwd_chain<T, 2>(J, a, lval, xq, vq, slice, colsum[wid], &bars[wid], phase);
+        } else {
+            const int64_t q = a.act0 ? 0 : 1;
+            T* const xq[1] = {x + q * a.dim};
+            T* const vq[1] = {vin + q * a.nv};
+            fwd_chain<T, 1>(J, a, lval, xq, vq, slice, colsum[wid], &bars[wid], phase);
+        }
     }
 }
 
@@ -1060,7 +1116,7 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
     resolve_act(a.rstate, a.act0, a.act1);
     if (!a.act0 && !a.act1) return;
     extern __shared__ __align__(16) unsigned char sraw[];
-    __shared__ T xs[SW][64];
+    __shared__ T xs[SW][2][64];
     __shared__ uint64_t bars[SW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T* slice = reinterpret_cast<T*>(sraw) + (int64_t)wid * a.slice;
@@ -1089,14 +1145,34 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
         // static inputs fetched before waiting for the parent
         const int rows_pf[2] = {lane < o ? __ldg(rowsJ + lane) : 0, lane + 32 < o ? __ldg(rowsJ + 32 + lane) : 0};
         const T d_pf[2] = {lane < w ? dvec[c0 + lane] : (T)1, lane + 32 < w ? dvec[c0 + lane + 32] : (T)1};
-        if (lane == 0 && d.parent >= 0) wait_ge(a.count + d.parent, 1);
-        __syncwarp();
-        if (staged) {
-            mbar_wait(&bars[wid], phase);
-            phase ^= 1u;
-            bwd_body<T>(slice, a, c0, w, r, o, rowsJ, dvec, x, xs[wid], rows_pf, d_pf);
+        // own values: final since the forward sweep, loaded before the wait too
+        if (a.act0 && a.act1) {
+            T* const xq[2] = {x, x + a.dim};
+            const T xa[2] = {lane < w ? xq[0][c0 + lane] : (T)0, lane < w ? xq[1][c0 + lane] : (T)0};
+            const T xb[2] = {lane + 32 < w ? xq[0][c0 + lane + 32] : (T)0,
+                             lane + 32 < w ? xq[1][c0 + lane + 32] : (T)0};
+            if (lane == 0 && d.parent >= 0) wait_ge(a.count + d.parent, 1);
+            __syncwarp();
+            if (staged) {
+                mbar_wait(&bars[wid], phase);
+                phase ^= 1u;
+                bwd_body<T, 2>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+            } else {
+                bwd_body<T, 2>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+            }
         } else {
-            bwd_body<T>(Lg, a, c0, w, r, o, rowsJ, dvec, x, xs[wid], rows_pf, d_pf);
+            T* const xq[1] = {x + (a.act0 ? 0 : a.dim)};
+            const T xa[1] = {lane < w ? xq[0][c0 + lane] : (T)0};
+            const T xb[1] = {lane + 32 < w ? xq[0][c0 + lane + 32] : (T)0};
+            if (lane == 0 && d.parent >= 0) wait_ge(a.count + d.parent, 1);
+            __syncwarp();
+            if (staged) {
+                mbar_wait(&bars[wid], phase);
+                phase ^= 1u;
+                bwd_body<T, 1>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+            } else {
+                bwd_body<T, 1>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+            }
         }
         __syncwarp();
         if (lane == 0) st_release(a.count + J, 1);
