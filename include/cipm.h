@@ -96,12 +96,18 @@ typedef struct {
 typedef struct {
     int64_t dim, nsuper, nnz_l, nnz_storage, n_updates, max_width, max_rows, height;
     double flops;
+    int64_t ordering;              /* ordering used: 0 minimum degree (reference), 1 natural, 2 nested dissection */
 } cipm_symbolic_info;
 
 int cipm_version(void);
 
 /* --- symbolic analysis (replaces kkt/system.py:87-148 + :188-240, ordering.py:15-53) --- */
+/* ordering: 0 = the reference's exact minimum degree (ordering.py:15-53), 1 = natural,
+ * 2 = nested dissection, 3 = auto (MD below 20k rows, else ND when its fill and flops
+ * stay within 1.25x / 1.5x of MD's) */
 int cipm_symbolic_create(const cipm_problem_desc *desc, int ordering, cipm_symbolic **out);
+/* same, with the nested-dissection leaf size (parts up to nd_leaf rows are ordered by MD; 0 = default 256) */
+int cipm_symbolic_create_ex(const cipm_problem_desc *desc, int ordering, int64_t nd_leaf, cipm_symbolic **out);
 int cipm_symbolic_info_get(const cipm_symbolic *sym, cipm_symbolic_info *info);
 /* copy a named symbolic array ("perm", "sn_col", "sn_rptr", "sn_rows", "sn_loff", "sn_parent",
  * "upd_ptr", "upd_src", "upd_p0", "upd_p1", "order", "map_p", "map_a", "map_diag", "map_hblk") */

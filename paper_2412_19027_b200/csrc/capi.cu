@@ -210,12 +210,17 @@ static void blocks_of(const cipm_problem_desc* d, std::vector<int64_t>& off, std
 }
 
 int cipm_symbolic_create(const cipm_problem_desc* d, int ordering, cipm_symbolic** out) {
-    if (!d || !out) return CIPM_E_ARG;
+    return cipm_symbolic_create_ex(d, ordering, 0, out);
+}
+
+int cipm_symbolic_create_ex(const cipm_problem_desc* d, int ordering, int64_t nd_leaf, cipm_symbolic** out) {
+    if (!d || !out || ordering < 0 || ordering > 3 || nd_leaf < 0) return CIPM_E_ARG;
     auto* h = new cipm_symbolic();
     std::vector<int64_t> off, dim;
     blocks_of(d, off, dim);
     SymbolicOptions opt;
     opt.ordering = ordering;
+    if (nd_leaf > 0) opt.nd_leaf = nd_leaf;
     int rc = analyze(d->n, d->m, d->p_rowptr, d->p_colidx, d->a_rowptr, d->a_colidx, d->zero_dim + d->nonneg_dim,
                      (int64_t)off.size(), off.data(), dim.data(), opt, h->s);
     if (rc) {
@@ -238,6 +243,7 @@ int cipm_symbolic_info_get(const cipm_symbolic* sym, cipm_symbolic_info* info) {
     info->max_rows = s.max_rows;
     info->height = s.height;
     info->flops = s.flops;
+    info->ordering = s.ordering_used;
     return CIPM_OK;
 }
 

@@ -10,10 +10,13 @@
 #include "symbolic.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <queue>
+#include <thread>
 #include <utility>
 
 namespace cipm {
@@ -118,6 +121,188 @@ std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim) {
     return perm;
 }
 
+// Nested dissection by BFS level-structure vertex separators (ordering = 2).
+// Each part: a pseudo-peripheral start (repeated BFS), BFS levels, the level
+// nearest the weighted middle with the fewest nodes inside a balance window as
+// the separator, trimmed to the nodes adjacent to the far side; parts at most
+// `leaf` nodes are ordered by the exact minimum degree above on their induced
+// subgraph.  Separators are numbered after both halves, so the elimination
+// tree's height is O(log n) separators instead of MD's long chains on banded
+// problems (FP64 results are ordering-independent; the solution-
+// level parity contract allows it).
+struct NdWork {
+    const Graph& g;
+    std::vector<int32_t> part;     // part id per node (-1 = already ordered)
+    std::vector<int32_t> level;
+    std::vector<int32_t> queue;
+    std::vector<int32_t> loc;      // node -> local index (leaf subgraph)
+    std::vector<int32_t> out;      // the order, separators last within a part
+    int32_t next_id = 1;
+    int64_t leaf;
+    explicit NdWork(const Graph& gg, int64_t dim, int64_t lf)
+        : g(gg), part(dim, 0), level(dim, -1), queue(dim), loc(dim, -1), leaf(lf) {}
+
+    // BFS from s inside part id; fills queue[0..cnt), level[]; returns cnt, sets last level
+    int64_t bfs(int32_t s, int32_t id, int32_t& maxlev) {
+        int64_t head = 0, tail = 0;
+        queue[tail++] = s;
+        level[s] = 0;
+        maxlev = 0;
+        while (head < tail) {
+            int32_t v = queue[head++];
+            for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
+                int32_t u = g.idx[p];
+                if (part[u] == id && level[u] < 0) {
+                    level[u] = level[v] + 1;
+                    maxlev = std::max(maxlev, level[u]);
+                    queue[tail++] = u;
+                }
+            }
+        }
+        return tail;
+    }
+    void clear_levels(int64_t cnt) {
+        for (int64_t k = 0; k < cnt; ++k) level[queue[k]] = -1;
+    }
+
+    void order_leaf(const std::vector<int32_t>& nodes) {
+        const int64_t k = (int64_t)nodes.size();
+        for (int64_t i = 0; i < k; ++i) loc[nodes[i]] = (int32_t)i;
+        const int32_t id = part[nodes[0]];
+        Graph sg;
+        sg.ptr.assign(k + 1, 0);
+        for (int64_t i = 0; i < k; ++i) {
+            int32_t v = nodes[i];
+            for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p)
+                if (part[g.idx[p]] == id) sg.idx.push_back(loc[g.idx[p]]);
+            sg.ptr[i + 1] = (int64_t)sg.idx.size();
+        }
+        std::vector<int32_t> pl = minimum_degree(sg, k);
+        for (int32_t i : pl) out.push_back(nodes[i]);
+        for (int32_t v : nodes) { part[v] = -1; loc[v] = -1; }
+    }
+
+    // order the part `id` whose nodes are `nodes` (appends to out)
+    void dissect(std::vector<int32_t> nodes) {
+        struct Item { std::vector<int32_t> nodes; int stage; std::vector<int32_t> sep; };
+        std::vector<Item> stack;
+        stack.push_back({std::move(nodes), 0, {}});
+        while (!stack.empty()) {
+            Item& it = stack.back();
+            if (it.stage == 1) {            // both halves ordered: the separator goes last
+                for (int32_t v : it.sep) { out.push_back(v); part[v] = -1; }
+                stack.pop_back();
+                continue;
+            }
+            std::vector<int32_t> cur = std::move(it.nodes);
+            const int32_t id = part[cur[0]];
+            if ((int64_t)cur.size() <= leaf) {
+                stack.pop_back();
+                order_leaf(cur);
+                continue;
+            }
+            // connected components, all found in one pass; each is ordered on its own
+            int32_t s = cur[0], maxlev = 0;
+            int64_t cnt = bfs(s, id, maxlev);
+            if (cnt < (int64_t)cur.size()) {
+                std::vector<std::vector<int32_t>> comps;
+                comps.emplace_back(queue.begin(), queue.begin() + cnt);
+                for (int32_t v : cur) {
+                    if (level[v] >= 0) continue;
+                    int32_t ml = 0;
+                    const int64_t c2 = bfs(v, id, ml);
+                    comps.emplace_back(queue.begin(), queue.begin() + c2);
+                }
+                for (int32_t v : cur) level[v] = -1;
+                stack.pop_back();
+                for (auto& comp : comps) {
+                    const int32_t nid = next_id++;
+                    for (int32_t v : comp) part[v] = nid;
+                    stack.push_back({std::move(comp), 0, {}});
+                }
+                continue;
+            }
+            for (int sweep = 0; sweep < 3; ++sweep) {
+                int32_t best = -1;
+                int64_t bdeg = INT64_MAX;
+                for (int64_t k = cnt - 1; k >= 0 && level[queue[k]] == maxlev; --k) {
+                    int32_t v = queue[k];
+                    int64_t dg = g.ptr[v + 1] - g.ptr[v];
+                    if (dg < bdeg) { bdeg = dg; best = v; }
+                }
+                clear_levels(cnt);
+                int32_t ml2 = 0;
+                cnt = bfs(best, id, ml2);
+                if (ml2 <= maxlev) { maxlev = ml2; s = best; break; }
+                maxlev = ml2;
+                s = best;
+            }
+            // level sizes; separator level: fewest nodes within the balance window
+            std::vector<int64_t> lsz(maxlev + 2, 0);
+            for (int64_t k = 0; k < cnt; ++k) lsz[level[queue[k]]]++;
+            int64_t below = 0, bestsz = INT64_MAX;
+            int32_t sl = -1;
+            const int64_t tot = cnt;
+            for (int32_t l = 1; l < maxlev; ++l) {
+                below += lsz[l - 1];
+                const int64_t above = tot - below - lsz[l];
+                const double bal = (double)std::min(below, above) / (double)tot;
+                if (bal < 0.3) continue;
+                if (lsz[l] < bestsz) { bestsz = lsz[l]; sl = l; }
+            }
+            if (sl < 0) {
+                // no balanced level (e.g. a star): fall back to the middle level
+                below = 0;
+                for (int32_t l = 0; l <= maxlev; ++l) {
+                    if (below + lsz[l] >= tot / 2) { sl = l; break; }
+                    below += lsz[l];
+                }
+                if (sl <= 0 || sl >= maxlev) {
+                    clear_levels(cnt);
+                    stack.pop_back();
+                    order_leaf(cur);       // cannot split: minimum degree on the whole part
+                    continue;
+                }
+            }
+            // separator: level-sl nodes adjacent to level sl+1 (the rest join the low side)
+            const int32_t lo = next_id++, hi = next_id++;
+            std::vector<int32_t> A, B, S;
+            for (int64_t k = 0; k < cnt; ++k) {
+                int32_t v = queue[k];
+                int32_t lv = level[v];
+                if (lv < sl) A.push_back(v);
+                else if (lv > sl) B.push_back(v);
+                else {
+                    bool touches = false;
+                    for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
+                        int32_t u = g.idx[p];
+                        if (part[u] == id && level[u] == sl + 1) { touches = true; break; }
+                    }
+                    (touches ? S : A).push_back(v);
+                }
+            }
+            clear_levels(cnt);
+            const int32_t sid = next_id++;
+            for (int32_t v : A) part[v] = lo;
+            for (int32_t v : B) part[v] = hi;
+            for (int32_t v : S) part[v] = sid;
+            it.stage = 1;
+            it.sep = std::move(S);
+            if (!B.empty()) stack.push_back({std::move(B), 0, {}});
+            if (!A.empty()) stack.push_back({std::move(A), 0, {}});
+        }
+    }
+};
+
+std::vector<int32_t> nested_dissection(const Graph& g, int64_t dim, int64_t leaf) {
+    NdWork w(g, dim, leaf);
+    std::vector<int32_t> all(dim);
+    std::iota(all.begin(), all.end(), 0);
+    w.out.reserve(dim);
+    if (dim > 0) w.dissect(std::move(all));
+    return w.out;
+}
+
 // upper CSC of the permuted pattern: column c holds rows r < c
 void permuted_upper(const Graph& g, const std::vector<int32_t>& iperm, int64_t dim,
                     std::vector<int64_t>& cp, std::vector<int32_t>& ci) {
@@ -189,6 +374,55 @@ std::vector<int32_t> postorder(const std::vector<int32_t>& parent, const std::ve
     return post;
 }
 
+
+// nnz(L) and 2*sum c_j^2 of an ordering (etree + path-walk column counts),
+// abandoned (returns false) once nnz exceeds `budget`
+bool fill_stats(const Graph& g, const std::vector<int32_t>& perm, int64_t dim, int64_t budget, int64_t& nnz,
+                double& flops) {
+    std::vector<int32_t> iperm(dim);
+    for (int64_t k = 0; k < dim; ++k) iperm[perm[k]] = (int32_t)k;
+    std::vector<int64_t> cp;
+    std::vector<int32_t> ci;
+    permuted_upper(g, iperm, dim, cp, ci);
+    std::vector<int32_t> parent = etree(cp, ci, dim);
+    std::vector<int64_t> cnt(dim, 0);
+    std::vector<int32_t> fl(dim, -1);
+    nnz = 0;
+    for (int64_t j = 0; j < dim; ++j) {
+        fl[j] = (int32_t)j;
+        for (int64_t p = cp[j]; p < cp[j + 1]; ++p)
+            for (int32_t i = ci[p]; fl[i] != j; i = parent[i]) { cnt[i]++; fl[i] = (int32_t)j; nnz++; }
+        if (nnz > budget) return false;
+    }
+    flops = 0.0;
+    for (int64_t j = 0; j < dim; ++j) flops += 2.0 * (double)cnt[j] * (double)cnt[j];
+    return true;
+}
+
+// ordering 3 (auto): the reference's minimum degree for small systems; for
+// large ones minimum degree and nested dissection are computed concurrently
+// and nested dissection is kept when its fill and flops stay close to MD's
+// (banded problems: same fill, a 4x shallower elimination tree)
+std::vector<int32_t> auto_order(const Graph& g, int64_t dim, const SymbolicOptions& opt, int* chosen) {
+    if (dim < opt.auto_min_dim) {
+        *chosen = 0;
+        return minimum_degree(g, dim);
+    }
+    std::vector<int32_t> md, nd;
+    std::thread t([&] { nd = nested_dissection(g, dim, opt.nd_leaf); });
+    md = minimum_degree(g, dim);
+    t.join();
+    int64_t nnz_md = 0, nnz_nd = 0;
+    double fl_md = 0, fl_nd = 0;
+    fill_stats(g, md, dim, INT64_MAX, nnz_md, fl_md);
+    const bool ok = fill_stats(g, nd, dim, (int64_t)(opt.nd_max_fill * (double)nnz_md), nnz_nd, fl_nd);
+    if (ok && fl_nd <= opt.nd_max_flops * fl_md) {
+        *chosen = 2;
+        return nd;
+    }
+    *chosen = 0;
+    return md;
+}
 }  // namespace
 
 int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const int64_t* arp,
@@ -201,9 +435,16 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     Graph g = kkt_graph(n, m, prp, pci, arp, aci, nblocks, boff, bdim);
 
     std::vector<int32_t> perm;
+    S.ordering_used = opt.ordering == 3 ? 0 : opt.ordering;
     if (opt.ordering == 1) {
         perm.resize(dim);
         std::iota(perm.begin(), perm.end(), 0);
+    } else if (opt.ordering == 2) {
+        perm = nested_dissection(g, dim, opt.nd_leaf);
+    } else if (opt.ordering == 3) {
+        int chosen = 0;
+        perm = auto_order(g, dim, opt, &chosen);
+        S.ordering_used = chosen;
     } else {
         perm = minimum_degree(g, dim);
     }

@@ -15,7 +15,12 @@
 namespace cipm {
 
 struct SymbolicOptions {
-    int ordering = 0;          // 0 = exact minimum degree (reference order), 1 = natural
+    int ordering = 0;          // 0 = exact minimum degree (reference order), 1 = natural,
+                               // 2 = nested dissection (level-structure separators, MD leaves)
+    int64_t nd_leaf = 256;     // nested dissection: parts up to this size are ordered by MD
+    int64_t auto_min_dim = 20000;   // ordering 3 (auto): below this, the reference's MD
+    double nd_max_fill = 1.25;      // ... above it ND if nnz(L) <= this x MD's
+    double nd_max_flops = 1.5;      // ... and factor flops <= this x MD's
     int relax_small = 8;       // always merge a child into its parent up to this width
     int relax_mid = 32;        // ... up to this width if zero fraction <= relax_mid_frac
     double relax_mid_frac = 0.3;
@@ -33,7 +38,8 @@ struct Symbolic {
     int64_t n = 0, m = 0, dim = 0;
     // permutation: position k of the factor holds original KKT index perm[k]
     std::vector<int32_t> perm, iperm;
-    std::vector<int32_t> md_perm;          // raw minimum-degree order (before postordering)
+    std::vector<int32_t> md_perm;          // raw fill-reducing order (before postordering)
+    int ordering_used = 0;                 // 0 MD, 1 natural, 2 nested dissection
     std::vector<int8_t> sign;              // +1 x rows, -1 z rows (permuted order)
     // supernodes
     int32_t nsuper = 0;

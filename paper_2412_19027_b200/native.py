@@ -51,13 +51,15 @@ class Settings(ctypes.Structure):
 class SymInfo(ctypes.Structure):
     _fields_ = [("dim", c_i64), ("nsuper", c_i64), ("nnz_l", c_i64), ("nnz_storage", c_i64),
                 ("n_updates", c_i64), ("max_width", c_i64), ("max_rows", c_i64), ("height", c_i64),
-                ("flops", c_dbl)]
+                ("flops", c_dbl), ("ordering", c_i64)]
 
 
 # every exported symbol of include/cipm.h with its signature
 _SIGS = {
     "cipm_version": ([], ctypes.c_int),
     "cipm_symbolic_create": ([ctypes.POINTER(ProblemDesc), ctypes.c_int, ctypes.POINTER(c_void_p)], ctypes.c_int),
+    "cipm_symbolic_create_ex": ([ctypes.POINTER(ProblemDesc), ctypes.c_int, c_i64, ctypes.POINTER(c_void_p)],
+                                ctypes.c_int),
     "cipm_symbolic_info_get": ([c_void_p, ctypes.POINTER(SymInfo)], ctypes.c_int),
     "cipm_symbolic_array": ([c_void_p, ctypes.c_char_p, c_void_p, P_I64], ctypes.c_int),
     "cipm_symbolic_destroy": ([c_void_p], None),
@@ -198,10 +200,15 @@ def make_desc(P, A, lay: Layout):
 class SymbolicAnalysis:
     """Host symbolic analysis handle (ordering, etree, supernodes, scatter maps)."""
 
-    def __init__(self, P, A, lay: Layout, ordering: int = 0):
+    ORDERINGS = {"md": 0, "natural": 1, "nd": 2, "auto": 3}
+
+    def __init__(self, P, A, lay: Layout, ordering: int = 0, nd_leaf: int = 0):
+        """ordering: 0 the reference's exact minimum degree, 1 natural, 2 nested
+        dissection (parts up to nd_leaf rows ordered by MD), 3 auto (MD below 20k
+        rows, else ND when its fill stays close to MD's)."""
         self._desc, self._keep = make_desc(P, A, lay)
         h = c_void_p()
-        rc = lib().cipm_symbolic_create(ctypes.byref(self._desc), ordering, ctypes.byref(h))
+        rc = lib().cipm_symbolic_create_ex(ctypes.byref(self._desc), int(ordering), int(nd_leaf), ctypes.byref(h))
         raise_for_status(rc, "symbolic analysis")
         self.handle = h
 

@@ -102,7 +102,7 @@ class Solver:
     """One problem instance: setup once on the host + GPU, solve and re-solve."""
 
     def __init__(self, problem: ProblemData, settings: SolverSettings | None = None, device: int = 0,
-                 ordering: int = 0):
+                 ordering: int = 3, nd_leaf: int = 0):
         self.settings = settings or SolverSettings()
         torch = require_device()
         self.device = device
@@ -115,7 +115,8 @@ class Solver:
         self.layout = Layout(reordered.cones)
         self.nu = self.layout.degree
         self.n, self.m = reordered.n, reordered.m
-        self.symbolic = SymbolicAnalysis(reordered.P, reordered.A, self.layout, ordering=ordering)
+        # ordering (not a reference setting): 3 = auto, see native.SymbolicAnalysis
+        self.symbolic = SymbolicAnalysis(reordered.P, reordered.A, self.layout, ordering=ordering, nd_leaf=nd_leaf)
         st = self.settings
         prec = st.precision
         cs = Settings()

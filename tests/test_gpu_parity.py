@@ -82,3 +82,20 @@ def test_gpu_update_data_reuses_symbolic(gpu):
         assert rel(r.obj_primal, o.obj_primal) <= 1e-6
     assert s.num_symbolic == 1
     s.close()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_nested_dissection_matches_reference_golden(name, gpu):
+    """Same parity contract with the nested-dissection ordering forced (small
+    leaves so the golden instances are actually dissected): the ordering is a
+    solver-internal choice and must not change the outcome."""
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance(name)
+    s = Solver(problem_from_doc(doc), settings_of(doc), ordering=2, nd_leaf=16)
+    assert s.symbolic.info()["ordering"] == 2
+    res = s.solve()
+    s.close()
+    check_parity(res, doc["result"])
+    if res.status == "optimal":
+        x_ref = np.array(doc["result"]["x"])
+        assert np.max(np.abs(res.x - x_ref)) <= 1e-4 * max(1.0, np.max(np.abs(x_ref)))

@@ -47,11 +47,12 @@ def test_min_degree_matches_reference_order(name):
     assert sym.info()["nnz_l"] == o.kkt.nnz_l
 
 
+@pytest.mark.parametrize("ordering", [0, 2])
 @pytest.mark.parametrize("name", ["lp_20x40", "socp_10", "psd_4x3", "exppow_20_8", "mpc_s0", "lasso_40x160"])
-def test_supernodal_structure_reconstructs_kkt(name):
+def test_supernodal_structure_reconstructs_kkt(name, ordering):
     _, s = _scaled(name)
     lay = native.Layout(s.cones)
-    sym = native.SymbolicAnalysis(s.P, s.A, lay)
+    sym = native.SymbolicAnalysis(s.P, s.A, lay, ordering=ordering, nd_leaf=8)
     olay = C.ConeLayout.from_specs(s.cones)
     s0, z0 = C.unit_start(olay)
     sc = C.update_scaling(olay, s0, z0, 1.0)
@@ -117,3 +118,31 @@ def test_min_degree_entry_point_on_arrow():
     m = sp.csr_matrix(a)
     perm = native.min_degree(m.indptr, m.indices)
     assert perm[-1] == 4 or perm[-2] == 4
+
+
+def test_nested_dissection_is_a_shallow_permutation():
+    """ND (ordering 2) is a permutation; on a banded SOCP it keeps MD's fill within
+    the auto rule's bounds and cuts the supernodal tree height; auto picks it."""
+    from paper_2412_19027_b200 import generators as G
+    prob = G.gen_socp(3000, seed=0)
+    r, _ = model.reorder_cones(prob)
+    lay = native.Layout(r.cones)
+    md = native.SymbolicAnalysis(r.P, r.A, lay, ordering=0)
+    nd = native.SymbolicAnalysis(r.P, r.A, lay, ordering=2)
+    auto = native.SymbolicAnalysis(r.P, r.A, lay, ordering=3)
+    dim = r.n + r.m
+    assert np.array_equal(np.sort(nd.array("md_perm")), np.arange(dim))
+    imd, ind = md.info(), nd.info()
+    assert ind["ordering"] == 2 and imd["ordering"] == 0
+    assert ind["nnz_l"] <= 1.25 * imd["nnz_l"]
+    assert ind["height"] < imd["height"]
+    assert auto.info()["ordering"] == 2
+    assert np.array_equal(auto.array("perm"), nd.array("perm"))
+
+
+def test_auto_ordering_keeps_reference_md_when_small_or_fill_heavy():
+    prob, s = _scaled("lp_150x300")
+    sym = native.SymbolicAnalysis(s.P, s.A, native.Layout(s.cones), ordering=3)
+    assert sym.info()["ordering"] == 0
+    o = OracleSolver(prob, SolverSettings())
+    np.testing.assert_array_equal(sym.array("md_perm"), o.kkt.perm)

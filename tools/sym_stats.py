@@ -17,7 +17,7 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2_lasso"
     prob = G.build(cfg)
     rp, _ = reorder_cones(prob)
-    sym = SymbolicAnalysis(rp.P, rp.A, Layout(rp.cones))
+    sym = SymbolicAnalysis(rp.P, rp.A, Layout(rp.cones), ordering=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
     info = sym.info()
     col = sym.array("sn_col")
     rptr = sym.array("sn_rptr")
