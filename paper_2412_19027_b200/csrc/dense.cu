@@ -388,7 +388,11 @@ struct TailSolveArgs {
     const double* rstate;      // refinement state: skip converged right-hand sides
 };
 
-// forward: CTA per row block (diag blocks 0..nbd-1, then off-row blocks)
+// forward: CTA per row block (diag blocks 0..nbd-1, then off-row blocks).
+// Everything static is fetched before the CTA waits: its inverse block into
+// shared memory, and each block's L values into registers before that block's
+// flag is polled, so the critical step after a flag is one load of the 64
+// solved values, a GEMV from registers and (diag) a GEMV from shared memory.
 template <typename T>
 __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
                                                 T* x, T* vin) {
@@ -402,6 +406,7 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
     __shared__ T acc[2][TB];
     __shared__ T xs[2][TB];
     __shared__ T part[4][2][TB];
+    __shared__ __align__(16) T inv_s[TB * TB];
     const int tid = threadIdx.x, ri = tid & 63, kp = tid >> 6;
     if (tid == 0) s_b = atomicAdd(a.ticket, 1);
     __syncthreads();
@@ -411,6 +416,10 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
     const int rend = diag ? min(a.w, row0 + TB) : a.r;
     const int nrow = min(TB, rend - row0);
     const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    if (diag) {
+        const T* I = inv + (int64_t)b * TB * TB;
+        for (int e = tid; e < TB * TB; e += 256) inv_s[e] = I[e];
+    }
     if (kp == 0) {
         for (int q = 0; q < 2; ++q) {
             T v = (T)0;
@@ -423,41 +432,43 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
             acc[q][ri] = v;
         }
     }
-    __syncthreads();
     const int nblk = diag ? b : a.nbd;
     for (int kb = 0; kb < nblk; ++kb) {
+        const int kc = kb * TB, kn = min(TB, a.w - kc);
+        T lv[TB / 4];
+        const T* Lr = L + (int64_t)kc * a.r + row0 + ri;
+#pragma unroll
+        for (int u = 0; u < TB / 4; ++u) {
+            const int k = kp + 4 * u;
+            lv[u] = (ri < nrow && k < kn) ? Lr[(int64_t)k * a.r] : (T)0;
+        }
         if (tid == 0) wait_flag(a.flags + kb);
         __syncthreads();
-        const int kc = kb * TB, kn = min(TB, a.w - kc);
         if (tid < 2 * TB) {
             const int q = tid >> 6, k = tid & 63;
             xs[q][k] = (act[q] && k < kn) ? __ldcg(x + q * a.dim + a.c0 + kc + k) : (T)0;
         }
         __syncthreads();
         T p0 = (T)0, p1 = (T)0;
-        if (ri < nrow) {
-            const T* Lr = L + (int64_t)kc * a.r + row0 + ri;
-            for (int k = kp; k < kn; k += 4) {
-                const T l = Lr[(int64_t)k * a.r];
-                p0 += l * xs[0][k];
-                p1 += l * xs[1][k];
-            }
+#pragma unroll
+        for (int u = 0; u < TB / 4; ++u) {
+            p0 += lv[u] * xs[0][kp + 4 * u];
+            p1 += lv[u] * xs[1][kp + 4 * u];
         }
         part[kp][0][ri] = p0;
         part[kp][1][ri] = p1;
         __syncthreads();
-        if (kp == 0)
+        if (kp == 0)          // acc row ri is only touched by this thread: no barrier after it
             for (int q = 0; q < 2; ++q)
                 acc[q][ri] -= ((part[0][q][ri] + part[1][q][ri]) + part[2][q][ri]) + part[3][q][ri];
-        __syncthreads();
     }
+    __syncthreads();
     if (diag) {
-        // x_b = inv(L_bb) * acc (row-major lower inverse)
-        const T* I = inv + (int64_t)b * TB * TB;
+        // x_b = inv(L_bb) * acc (row-major lower inverse, staged in shared memory)
         T p0 = (T)0, p1 = (T)0;
         if (ri < nrow)
             for (int t = kp; t <= ri; t += 4) {
-                const T iv = I[ri * TB + t];
+                const T iv = inv_s[ri * TB + t];
                 p0 += iv * acc[0][t];
                 p1 += iv * acc[1][t];
             }
@@ -477,7 +488,10 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
     }
 }
 
-// backward: CTA per column block, last block first
+// backward: CTA per column block, last block first.  Warp w owns columns
+// j = w, w+8, ... (lanes over rows: coalesced column reads); each warp polls the
+// flags itself, with that block's L values already in registers, so there is
+// no CTA barrier per block; the inverse block is staged in shared memory.
 template <typename T>
 __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
                                                 const T* __restrict__ dvec, T* x) {
@@ -489,6 +503,7 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
     if (!a.act0 && !a.act1) return;
     __shared__ int s_b;
     __shared__ T acc[2][TB];
+    __shared__ __align__(16) T inv_s[TB * TB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_b = a.nbd - 1 - atomicAdd(a.ticket, 1);
     __syncthreads();
@@ -496,6 +511,10 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
     const int col0 = b * TB;
     const int ncol = min(TB, a.w - col0);
     const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    {
+        const T* I = inv + (int64_t)b * TB * TB;
+        for (int e = tid; e < TB * TB; e += 256) inv_s[e] = I[e];
+    }
     // off rows (ancestors' x is final)
     for (int j = warp; j < ncol; j += 8) {
         const T* Lc = L + (int64_t)(col0 + j) * a.r;
@@ -517,37 +536,53 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
             acc[1][j] = act[1] ? __ldcg(x + a.dim + gc) / dj - s1 : (T)0;
         }
     }
-    // later own blocks
+    // later own blocks, last first
     for (int kb = a.nbd - 1; kb > b; --kb) {
-        if (tid == 0) wait_flag(a.flags + kb);
-        __syncthreads();
         const int r0 = kb * TB, rn = min(TB, a.w - r0);
-        for (int j = warp; j < ncol; j += 8) {
+        T l0[TB / 8], l1[TB / 8];
+#pragma unroll
+        for (int c = 0; c < TB / 8; ++c) {
+            const int j = warp + 8 * c;
             const T* Lc = L + (int64_t)(col0 + j) * a.r + r0;
-            T s0 = (T)0, s1 = (T)0;
-            for (int i = lane; i < rn; i += 32) {
-                const T l = Lc[i];
-                if (act[0]) s0 += l * __ldcg(x + a.c0 + r0 + i);
-                if (act[1]) s1 += l * __ldcg(x + a.dim + a.c0 + r0 + i);
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                s0 += __shfl_down_sync(0xffffffffu, s0, o);
-                s1 += __shfl_down_sync(0xffffffffu, s1, o);
-            }
-            if (lane == 0) {
-                acc[0][j] -= s0;
-                acc[1][j] -= s1;
-            }
+            l0[c] = (j < ncol && lane < rn) ? Lc[lane] : (T)0;
+            l1[c] = (j < ncol && lane + 32 < rn) ? Lc[lane + 32] : (T)0;
         }
+        if (lane == 0) wait_flag(a.flags + kb);
+        __syncwarp();
+        T xa[2], xb[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            xa[q] = (act[q] && lane < rn) ? __ldcg(x + q * a.dim + a.c0 + r0 + lane) : (T)0;
+            xb[q] = (act[q] && lane + 32 < rn) ? __ldcg(x + q * a.dim + a.c0 + r0 + lane + 32) : (T)0;
+        }
+        T s[TB / 8][2];
+#pragma unroll
+        for (int c = 0; c < TB / 8; ++c)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) s[c][q] = l0[c] * xa[q] + l1[c] * xb[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int c = 0; c < TB / 8; ++c)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) s[c][q] += __shfl_down_sync(0xffffffffu, s[c][q], o);
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < TB / 8; ++c) {
+                const int j = warp + 8 * c;
+                if (j < ncol) {
+                    acc[0][j] -= s[c][0];
+                    acc[1][j] -= s[c][1];
+                }
+            }
     }
     __syncthreads();
     // x_b = inv(L_bb)' * acc
     if (tid < 2 * TB) {
         const int q = tid >> 6, j = tid & 63;
         if (act[q] && j < ncol) {
-            const T* I = inv + (int64_t)b * TB * TB;
             T v = (T)0;
-            for (int t = j; t < ncol; ++t) v += I[t * TB + j] * acc[q][t];
+            for (int t = j; t < ncol; ++t) v += inv_s[t * TB + j] * acc[q][t];
             x[q * a.dim + a.c0 + col0 + j] = v;
         }
     }
