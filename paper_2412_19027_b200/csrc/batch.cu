@@ -691,7 +691,10 @@ int bup(cipm_batch* h, const T** dst, const std::vector<T>& v) {
     void* p = nullptr;
     CIPM_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(v.size(), 1)));
     h->allocs.push_back(p);
-    if (!v.empty()) CIPM_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    if (!v.empty()) {
+        CIPM_CUDA(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, h->stream));
+        CIPM_CUDA(cudaStreamSynchronize(h->stream));
+    }
     *dst = (const T*)p;
     return CIPM_OK;
 }
@@ -1006,11 +1009,12 @@ int cipm_batch_results(cipm_batch* h, int32_t* status, double* res, double* x, d
     const int64_t c = h->count, n = h->pt.n, m = h->pt.m;
     CIPM_CUDA(cudaSetDevice(h->device));
     CIPM_CUDA(cudaStreamSynchronize(h->stream));
-    if (status) CIPM_CUDA(cudaMemcpy(status, h->bd.out_status, sizeof(int32_t) * c, cudaMemcpyDeviceToHost));
-    if (res) CIPM_CUDA(cudaMemcpy(res, h->bd.out_res, sizeof(double) * c * 9, cudaMemcpyDeviceToHost));
-    if (x) CIPM_CUDA(cudaMemcpy(x, h->bd.out_x, sizeof(double) * c * n, cudaMemcpyDeviceToHost));
-    if (z) CIPM_CUDA(cudaMemcpy(z, h->bd.out_z, sizeof(double) * c * m, cudaMemcpyDeviceToHost));
-    if (s) CIPM_CUDA(cudaMemcpy(s, h->bd.out_s, sizeof(double) * c * m, cudaMemcpyDeviceToHost));
+    if (status) CIPM_CUDA(cudaMemcpyAsync(status, h->bd.out_status, sizeof(int32_t) * c, cudaMemcpyDeviceToHost, h->stream));
+    if (res) CIPM_CUDA(cudaMemcpyAsync(res, h->bd.out_res, sizeof(double) * c * 9, cudaMemcpyDeviceToHost, h->stream));
+    if (x) CIPM_CUDA(cudaMemcpyAsync(x, h->bd.out_x, sizeof(double) * c * n, cudaMemcpyDeviceToHost, h->stream));
+    if (z) CIPM_CUDA(cudaMemcpyAsync(z, h->bd.out_z, sizeof(double) * c * m, cudaMemcpyDeviceToHost, h->stream));
+    if (s) CIPM_CUDA(cudaMemcpyAsync(s, h->bd.out_s, sizeof(double) * c * m, cudaMemcpyDeviceToHost, h->stream));
+    CIPM_CUDA(cudaStreamSynchronize(h->stream));     // results land in the caller's buffers before return
     h->d2h += (int64_t)(status ? 4 * c : 0) + (int64_t)sizeof(double) * ((res ? 9 * c : 0) + (x ? c * n : 0) +
                                                                          (z ? c * m : 0) + (s ? c * m : 0));
     return CIPM_OK;

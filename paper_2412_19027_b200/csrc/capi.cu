@@ -39,6 +39,15 @@ struct cipm_ctx {
 
 namespace {
 
+// every host<->device copy goes through the context's stream: the stream is
+// non-blocking, so a legacy-default-stream cudaMemcpy is NOT ordered after the
+// allocation memsets / kernels queued on it (and could be zeroed by a later memset)
+cudaError_t copy_sync(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c.stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(c.stream);
+}
+
 template <typename T>
 int dalloc(Ctx& c, T** p, int64_t count) {
     *p = nullptr;
@@ -60,14 +69,14 @@ int upload(Ctx& c, T** p, const S* host, int64_t count) {
     if (count <= 0) return CIPM_OK;
     std::vector<T> tmp((size_t)count);
     for (int64_t i = 0; i < count; ++i) tmp[i] = (T)host[i];
-    CIPM_CUDA(cudaMemcpy(*p, tmp.data(), sizeof(T) * count, cudaMemcpyHostToDevice));
+    CIPM_CUDA(copy_sync(c, *p, tmp.data(), sizeof(T) * count, cudaMemcpyHostToDevice));
     return CIPM_OK;
 }
 
 int sync_err(Ctx& c) {
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
     CIPM_CUDA(cudaGetLastError());
-    CIPM_CUDA(cudaMemcpy(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost));
+    CIPM_CUDA(copy_sync(c, c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost));
     return *c.h_err;
 }
 
@@ -586,10 +595,10 @@ int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const d
     if (c.a_nnz) {
         CIPM_CUDA(cudaMemcpyAsync(c.a_v, av, sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice, c.stream));
         std::vector<int64_t> src(c.a_nnz);
-        CIPM_CUDA(cudaMemcpy(src.data(), c.at_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyDeviceToHost));
+        CIPM_CUDA(copy_sync(c, src.data(), c.at_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyDeviceToHost));
         std::vector<double> tv(c.a_nnz);
         for (int64_t t = 0; t < c.a_nnz; ++t) tv[t] = av[src[t]];
-        CIPM_CUDA(cudaMemcpy(c.at_v, tv.data(), sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice));
+        CIPM_CUDA(copy_sync(c, c.at_v, tv.data(), sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice));
     }
     CIPM_CUDA(cudaMemcpyAsync(c.q, q, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
     CIPM_CUDA(cudaMemcpyAsync(c.b, b, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
@@ -606,8 +615,8 @@ int cipm_ctx_set_reorder(cipm_ctx* h, const int64_t* row_perm, const int64_t* a_
     if (!h || (h->c.m && !row_perm) || (h->c.a_nnz && !a_src)) return CIPM_E_ARG;
     Ctx& c = h->c;
     CIPM_CUDA(cudaSetDevice(c.device));
-    if (c.m) CIPM_CUDA(cudaMemcpy(c.b_src, row_perm, sizeof(int64_t) * c.m, cudaMemcpyHostToDevice));
-    if (c.a_nnz) CIPM_CUDA(cudaMemcpy(c.a_src, a_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyHostToDevice));
+    if (c.m) CIPM_CUDA(copy_sync(c, c.b_src, row_perm, sizeof(int64_t) * c.m, cudaMemcpyHostToDevice));
+    if (c.a_nnz) CIPM_CUDA(copy_sync(c, c.a_src, a_src, sizeof(int64_t) * c.a_nnz, cudaMemcpyHostToDevice));
     c.have_reorder = true;
     return CIPM_OK;
 }
@@ -636,8 +645,8 @@ int cipm_ctx_get_equilibration(cipm_ctx* h, double* d_row, double* d_col, double
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    if (d_row && c.m) CIPM_CUDA(cudaMemcpy(d_row, c.dr, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
-    if (d_col && c.n) CIPM_CUDA(cudaMemcpy(d_col, c.dc, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (d_row && c.m) CIPM_CUDA(copy_sync(c, d_row, c.dr, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (d_col && c.n) CIPM_CUDA(copy_sync(c, d_col, c.dc, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
     if (c_obj) *c_obj = c.c_obj;
     c.d2h_bytes += (int64_t)sizeof(double) * ((d_row ? c.m : 0) + (d_col ? c.n : 0));
     return CIPM_OK;
@@ -789,11 +798,11 @@ int cipm_get_iterate(cipm_ctx* h, int which, double* x, double* z, double* s, do
     const double* px = which ? c.bx : c.x;
     const double* pz = which ? c.bz : c.z;
     const double* ps = which ? c.bs : c.s;
-    if (x) CIPM_CUDA(cudaMemcpy(x, px, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
-    if (z) CIPM_CUDA(cudaMemcpy(z, pz, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
-    if (s) CIPM_CUDA(cudaMemcpy(s, ps, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (x) CIPM_CUDA(copy_sync(c, x, px, sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (z) CIPM_CUDA(copy_sync(c, z, pz, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (s) CIPM_CUDA(copy_sync(c, s, ps, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
     if (tkm) {
-        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        CIPM_CUDA(copy_sync(c, c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
         tkm[0] = c.h_sc[CIPM_SC_TAU];
         tkm[1] = c.h_sc[CIPM_SC_KAPPA];
         tkm[2] = c.h_sc[CIPM_SC_MU];
@@ -804,15 +813,15 @@ int cipm_get_iterate(cipm_ctx* h, int which, double* x, double* z, double* s, do
 int cipm_set_iterate(cipm_ctx* h, const double* x, const double* z, const double* s, const double* tkm) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    if (x) CIPM_CUDA(cudaMemcpy(c.x, x, sizeof(double) * c.n, cudaMemcpyHostToDevice));
-    if (z) CIPM_CUDA(cudaMemcpy(c.z, z, sizeof(double) * c.m, cudaMemcpyHostToDevice));
-    if (s) CIPM_CUDA(cudaMemcpy(c.s, s, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (x) CIPM_CUDA(copy_sync(c, c.x, x, sizeof(double) * c.n, cudaMemcpyHostToDevice));
+    if (z) CIPM_CUDA(copy_sync(c, c.z, z, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (s) CIPM_CUDA(copy_sync(c, c.s, s, sizeof(double) * c.m, cudaMemcpyHostToDevice));
     if (tkm) {
-        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        CIPM_CUDA(copy_sync(c, c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
         c.h_sc[CIPM_SC_TAU] = tkm[0];
         c.h_sc[CIPM_SC_KAPPA] = tkm[1];
         c.h_sc[CIPM_SC_MU] = tkm[2];
-        CIPM_CUDA(cudaMemcpy(c.sc, c.h_sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyHostToDevice));
+        CIPM_CUDA(copy_sync(c, c.sc, c.h_sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyHostToDevice));
     }
     return CIPM_OK;
 }
@@ -823,7 +832,7 @@ int cipm_kkt_solve(cipm_ctx* h, const double* rhs, double* x, int* steps, double
     int e = refine(c, 1, steps);
     if (e) return e;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    CIPM_CUDA(cudaMemcpy(x, c.rbest, sizeof(double) * c.dim, cudaMemcpyDeviceToHost));
+    CIPM_CUDA(copy_sync(c, x, c.rbest, sizeof(double) * c.dim, cudaMemcpyDeviceToHost));
     if (residual) *residual = c.h_rstate[7];
     return CIPM_OK;
 }
@@ -833,10 +842,10 @@ int cipm_apply_h(cipm_ctx* h, const double* v, double* out) {
     double *dv = nullptr, *dout = nullptr;
     CIPM_CUDA(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(c.m, 1)));
     CIPM_CUDA(cudaMalloc(&dout, sizeof(double) * std::max<int64_t>(c.m, 1)));
-    CIPM_CUDA(cudaMemcpy(dv, v, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    CIPM_CUDA(copy_sync(c, dv, v, sizeof(double) * c.m, cudaMemcpyHostToDevice));
     k_apply_h(c, dv, dout, 0.0, nullptr, 1.0);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    CIPM_CUDA(cudaMemcpy(out, dout, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    CIPM_CUDA(copy_sync(c, out, dout, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
     cudaFree(dv);
     cudaFree(dout);
     return *c.h_err;
@@ -848,11 +857,11 @@ int cipm_scaling_values(cipm_ctx* h, double* diag, double* blocks) {
     if (diag) {
         std::vector<double> tmp(c.lin, 0.0);
         if (c.nonneg_dim)
-            CIPM_CUDA(cudaMemcpy(tmp.data() + c.zero_dim, c.nn_h, sizeof(double) * c.nonneg_dim,
+            CIPM_CUDA(copy_sync(c, tmp.data() + c.zero_dim, c.nn_h, sizeof(double) * c.nonneg_dim,
                                  cudaMemcpyDeviceToHost));
         memcpy(diag, tmp.data(), sizeof(double) * c.lin);
     }
-    if (blocks && c.hblk_total) CIPM_CUDA(cudaMemcpy(blocks, c.hv, sizeof(double) * c.hblk_total, cudaMemcpyDeviceToHost));
+    if (blocks && c.hblk_total) CIPM_CUDA(copy_sync(c, blocks, c.hv, sizeof(double) * c.hblk_total, cudaMemcpyDeviceToHost));
     return sync_err(c);
 }
 
@@ -860,11 +869,11 @@ int cipm_get_direction(cipm_ctx* h, int combined, double* dx, double* dz, double
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
     const int w = combined ? 1 : 0;
-    if (dx) CIPM_CUDA(cudaMemcpy(dx, c.dx[w], sizeof(double) * c.n, cudaMemcpyDeviceToHost));
-    if (dz) CIPM_CUDA(cudaMemcpy(dz, c.dz[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
-    if (ds) CIPM_CUDA(cudaMemcpy(ds, c.ds[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (dx) CIPM_CUDA(copy_sync(c, dx, c.dx[w], sizeof(double) * c.n, cudaMemcpyDeviceToHost));
+    if (dz) CIPM_CUDA(copy_sync(c, dz, c.dz[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    if (ds) CIPM_CUDA(copy_sync(c, ds, c.ds[w], sizeof(double) * c.m, cudaMemcpyDeviceToHost));
     if (dtk) {
-        CIPM_CUDA(cudaMemcpy(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        CIPM_CUDA(copy_sync(c, c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
         dtk[0] = c.h_sc[w ? CIPM_SC_DTAU_C : CIPM_SC_DTAU_A];
         dtk[1] = c.h_sc[w ? CIPM_SC_DKAPPA_C : CIPM_SC_DKAPPA_A];
     }
@@ -889,7 +898,7 @@ int cipm_get_vector(cipm_ctx* h, const char* name, double* out, int64_t* count) 
     else return CIPM_E_ARG;
     if (count) *count = cnt;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    if (out && cnt) CIPM_CUDA(cudaMemcpy(out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
+    if (out && cnt) CIPM_CUDA(copy_sync(c, out, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost));
     return CIPM_OK;
 }
 
@@ -898,10 +907,10 @@ int cipm_soc_residuals(cipm_ctx* h, const double* x, double* out) {
     double *dx = nullptr, *dout = nullptr;
     CIPM_CUDA(cudaMalloc(&dx, sizeof(double) * std::max<int64_t>(c.m, 1)));
     CIPM_CUDA(cudaMalloc(&dout, sizeof(double) * std::max<int64_t>(c.nsoc, 1)));
-    CIPM_CUDA(cudaMemcpy(dx, x, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    CIPM_CUDA(copy_sync(c, dx, x, sizeof(double) * c.m, cudaMemcpyHostToDevice));
     k_soc_residuals(c, dx, dout);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
-    if (c.nsoc) CIPM_CUDA(cudaMemcpy(out, dout, sizeof(double) * c.nsoc, cudaMemcpyDeviceToHost));
+    if (c.nsoc) CIPM_CUDA(copy_sync(c, out, dout, sizeof(double) * c.nsoc, cudaMemcpyDeviceToHost));
     cudaFree(dx);
     cudaFree(dout);
     return CIPM_OK;
@@ -982,10 +991,10 @@ int cipm_trace(cipm_ctx* h, int enable, int64_t* out) {
             CIPM_CUDA(cudaMalloc(&c.trace, sizeof(int64_t) * cnt));
             c.allocations.push_back(c.trace);
         }
-        CIPM_CUDA(cudaMemset(c.trace, 0, sizeof(int64_t) * cnt));
+        CIPM_CUDA(cudaMemsetAsync(c.trace, 0, sizeof(int64_t) * cnt, c.stream));
         return CIPM_OK;
     }
-    if (c.trace && out) CIPM_CUDA(cudaMemcpy(out, c.trace, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
+    if (c.trace && out) CIPM_CUDA(copy_sync(c, out, c.trace, sizeof(int64_t) * cnt, cudaMemcpyDeviceToHost));
     c.trace = nullptr;   // stays allocated until destroy
     return CIPM_OK;
 }

@@ -265,16 +265,42 @@ constexpr int diag_smem() {
 // ---------------------------------------------------------------------------
 // C (M x N, lower: i + diag_off >= j) op= A (M x K) * diag(d) * B (N x K)'
 // A, B column-major with leading dimensions lda / ldb.  MODE 0: C -= acc in
-// place (ld = ldc).  MODE 1: inbox[push_pos[i,j packed]] = acc.
-// 64x64 CTA tile, 4 warps of 32x32, BK = 16; FP64 uses DMMA m8n8k4.
+// place (ld = ldc).  MODE 1: inbox[push_pos[i,j packed]] = acc.  MODE 2:
+// C = acc / dscale[j] (the rows-below solve with a block inverse, in place).
+// 64x64 CTA tile, 4 warps of 32x32, K staged in 16-deep slices through a
+// 4-stage cp.async ring (all of a K = 64 update is in flight at once); the MODE 0
+// tile of C is loaded (negated) into the accumulators before the K loop, so its
+// read overlaps the operand loads.  FP64 uses DMMA m8n8k4; FP32 FFMA tiles.
 // ---------------------------------------------------------------------------
-constexpr int GB = 64, GK = 16, GP = GB + 4;
+constexpr int GB = 64, GK = 16, GP = GB + 4, GST = 4;
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool ok) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <typename T>
+struct GemmSmem {
+    T A[GST][GK][GP];
+    T B[GST][GK][GP];
+    T D[GST][GK];
+};
+
+template <typename T>
+constexpr int gemm_smem() { return (int)sizeof(GemmSmem<T>); }
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* __restrict__ Bm, int ldb,
@@ -283,38 +309,63 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
                                                  T* __restrict__ inbox, const T* __restrict__ dscale) {
     const int m0 = blockIdx.x * GB, n0 = blockIdx.y * GB;
     if (m0 + GB - 1 + diag_off < n0) return;      // tile strictly above the diagonal
-    __shared__ __align__(16) T As[GK][GP];
-    __shared__ __align__(16) T Bs[GK][GP];
+    extern __shared__ __align__(16) unsigned char gsm_raw[];
+    GemmSmem<T>& sm = *reinterpret_cast<GemmSmem<T>*>(gsm_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
+    const int nk = (K + GK - 1) / GK;
+    auto load_stage = [&](int kt) {
+        const int slot = kt % GST, k0 = kt * GK;
+#pragma unroll
+        for (int u = 0; u < GK * GB / 128; ++u) {
+            const int e = tid + 128 * u, k = e >> 6, mi = e & 63;
+            const int gk = k0 + k;
+            const bool kok = gk < K;
+            const bool aok = kok && m0 + mi < M, bok = kok && n0 + mi < N;
+            cp_async_elem(&sm.A[slot][k][mi], aok ? A + (int64_t)gk * lda + m0 + mi : A, aok);
+            cp_async_elem(&sm.B[slot][k][mi], bok ? Bm + (int64_t)gk * ldb + n0 + mi : Bm, bok);
+        }
+        if (tid < GK) {
+            const bool ok = d != nullptr && k0 + tid < K;
+            cp_async_elem(&sm.D[slot][tid], ok ? d + k0 + tid : Bm, ok);
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < GST - 1; ++s) {
+        if (s < nk) load_stage(s);
+        cp_async_commit();
+    }
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    const int li = tid & 63, lk = tid >> 6;   // loader: row li, k = lk + 2t
-    for (int k0 = 0; k0 < K; k0 += GK) {
+        for (int b = 0; b < 4; ++b)
 #pragma unroll
-        for (int t = 0; t < GK / 2; ++t) {
-            const int k = lk + 2 * t;
-            const int gk = k0 + k;
-            T av = (T)0, bv = (T)0;
-            if (gk < K) {
-                if (m0 + li < M) av = A[(int64_t)gk * lda + m0 + li];
-                if (n0 + li < N) bv = d ? Bm[(int64_t)gk * ldb + n0 + li] * d[gk] : Bm[(int64_t)gk * ldb + n0 + li];
+            for (int e = 0; e < 2; ++e) {
+                double v = 0.0;
+                if (MODE == 0) {
+                    const int i = m0 + wm * 32 + a * 8 + (lane >> 2);
+                    const int j = n0 + wn * 32 + b * 8 + (lane & 3) * 2 + e;
+                    if (i < M && j < N && i + diag_off >= j) v = -(double)C[(int64_t)j * ldc + i];
+                }
+                acc[a][b][e] = v;
             }
-            As[k][li] = av;
-            Bs[k][li] = bv;
-        }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<GST - 2>();
         __syncthreads();
+        if (kt + GST - 1 < nk) load_stage(kt + GST - 1);
+        cp_async_commit();
+        const int slot = kt % GST;
         if constexpr (std::is_same<T, double>::value) {
 #pragma unroll
             for (int kk = 0; kk < GK; kk += 4) {
+                const int kr = kk + (lane & 3);
+                const double dk = d ? sm.D[slot][kr] : 1.0;
                 double af[4], bf[4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) af[a] = As[kk + (lane & 3)][wm * 32 + a * 8 + (lane >> 2)];
+                for (int a = 0; a < 4; ++a) af[a] = sm.A[slot][kr][wm * 32 + a * 8 + (lane >> 2)];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) bf[b] = Bs[kk + (lane & 3)][wn * 32 + b * 8 + (lane >> 2)];
+                for (int b = 0; b < 4; ++b) bf[b] = sm.B[slot][kr][wn * 32 + b * 8 + (lane >> 2)] * dk;
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -324,13 +375,14 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
             // FP32 (mixed mode): same fragment ownership, FFMA accumulation
 #pragma unroll 4
             for (int k = 0; k < GK; ++k) {
+                const float dk = d ? sm.D[slot][k] : 1.0f;
                 float af[4], bf[4][2];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) af[a] = As[k][wm * 32 + a * 8 + (lane >> 2)];
+                for (int a = 0; a < 4; ++a) af[a] = sm.A[slot][k][wm * 32 + a * 8 + (lane >> 2)];
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    bf[b][0] = Bs[k][wn * 32 + b * 8 + (lane & 3) * 2];
-                    bf[b][1] = Bs[k][wn * 32 + b * 8 + (lane & 3) * 2 + 1];
+                    bf[b][0] = sm.B[slot][k][wn * 32 + b * 8 + (lane & 3) * 2] * dk;
+                    bf[b][1] = sm.B[slot][k][wn * 32 + b * 8 + (lane & 3) * 2 + 1] * dk;
                 }
 #pragma unroll
                 for (int a = 0; a < 4; ++a)
@@ -341,8 +393,8 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
                     }
             }
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -353,8 +405,7 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
                 const int j = n0 + wn * 32 + b * 8 + (lane & 3) * 2 + e;
                 if (i >= M || j >= N || i + diag_off < j) continue;
                 if (MODE == 0) {
-                    T* p = C + (int64_t)j * ldc + i;
-                    *p = *p - (T)acc[a][b][e];
+                    C[(int64_t)j * ldc + i] = (T)(-acc[a][b][e]);
                 } else if (MODE == 2) {
                     C[(int64_t)j * ldc + i] = (T)acc[a][b][e] / dscale[j];
                 } else {
@@ -599,6 +650,9 @@ void tail_factor_t(Ctx& c) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tail_diag<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<T>());
+        cudaFuncSetAttribute(tail_gemm<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<T>());
+        cudaFuncSetAttribute(tail_gemm<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<T>());
+        cudaFuncSetAttribute(tail_gemm<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem<T>());
         attr = true;
     }
     T* L = (T*)c.lval;
@@ -624,7 +678,7 @@ void tail_factor_t(Ctx& c) {
                 // L21 = A21 L11^-T D^-1 as a GEMM with the column-major inverse (DMMA in FP64)
                 T* A21 = P + (int64_t)kb * r + kb + nb;
                 dim3 g((below + GB - 1) / GB, 1);
-                tail_gemm<T, 2><<<g, 128, 0, c.stream>>>(A21, r, inv_cm, TB, nullptr, below, nb, nb, 1 << 30, A21, r,
+                tail_gemm<T, 2><<<g, 128, gemm_smem<T>(), c.stream>>>(A21, r, inv_cm, TB, nullptr, below, nb, nb, 1 << 30, A21, r,
                                                          nullptr, nullptr, D + t.c0 + kb);
                 c.launches++;
             }
@@ -632,7 +686,7 @@ void tail_factor_t(Ctx& c) {
             if (Nc > 0) {
                 const T* A = P + (int64_t)kb * r + kb + nb;
                 dim3 g((Mr + GB - 1) / GB, (Nc + GB - 1) / GB);
-                tail_gemm<T, 0><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0 + kb, Mr, Nc, nb, 0,
+                tail_gemm<T, 0><<<g, 128, gemm_smem<T>(), c.stream>>>(A, r, A, r, D + t.c0 + kb, Mr, Nc, nb, 0,
                                                          P + (int64_t)(kb + nb) * r + kb + nb, r, nullptr, nullptr,
                                                          nullptr);
                 c.launches++;
@@ -641,7 +695,7 @@ void tail_factor_t(Ctx& c) {
         if (o > 0) {
             const T* A = P + w;
             dim3 g((o + GB - 1) / GB, (o + GB - 1) / GB);
-            tail_gemm<T, 1><<<g, 128, 0, c.stream>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
+            tail_gemm<T, 1><<<g, 128, gemm_smem<T>(), c.stream>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
                                                      c.sym.push_pos + S.cb_off[t.J], inbox, nullptr);
             c.launches++;
         }

@@ -15,7 +15,7 @@ import numpy as np
 from .exceptions import ConicError, raise_for_status
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libcipm.so")
+LIB_PATH = os.environ.get("CIPM_LIB") or os.path.join(PKG, "lib", "libcipm.so")   # override: debugging builds only
 
 c_i64 = ctypes.c_int64
 c_dbl = ctypes.c_double

@@ -99,3 +99,20 @@ def test_gpu_nested_dissection_matches_reference_golden(name, gpu):
     if res.status == "optimal":
         x_ref = np.array(doc["result"]["x"])
         assert np.max(np.abs(res.x - x_ref)) <= 1e-4 * max(1.0, np.max(np.abs(x_ref)))
+
+
+def test_gpu_fresh_solvers_bitwise_identical(gpu):
+    """Independent Solver instances of one problem give bitwise identical results
+    (guards the setup path: every host<->device copy is ordered on the context's
+    stream, after the allocation memsets queued there)."""
+    from paper_2412_19027_b200 import generators as G
+    from paper_2412_19027_b200.solver import Solver
+    prob = G.gen_socp(2000, seed=3)
+    out = set()
+    for _ in range(6):
+        s = Solver(prob, SolverSettings(eps_feas=1e-8))
+        r = s.solve()
+        s.close()
+        assert r.status == "optimal"
+        out.add((r.iterations, r.obj_primal.hex(), r.x.tobytes()))
+    assert len(out) == 1

@@ -13,5 +13,7 @@ cap c3_soc "soc_" 10 6 python bench.py --config c3_socp --steps 1 --warmup 0 --n
 cap c5a_psd "psd_" 10 6 python bench.py --config c5a_psd --steps 1 --warmup 0 --no-cpu-baseline
 cap c4_nsym "nsym_" 10 6 python tools/c4_check.py fifth
 cap c1_gemm "tail_gemm|tail_diag" 30 6 python tools/solve_probe.py c1_lp 2
+cap c1_tailsolve "tail_fwd|tail_bwd" 40 6 python tools/solve_probe.py c1_lp 2
+cap c3_solve "forward_kernel|backward_kernel|factor_cta_kernel" 4 3 python tools/solve_probe.py c3_socp 3
 cap c5b_batch "batch_ipm" 0 1 python bench.py --config c5b_mpc --steps 1 --warmup 0 --no-cpu-baseline
 du -sh gpurun_out/ncu
