@@ -509,6 +509,12 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(upload(c, &c.sym.cv_off, S.cv_off.data(), S.nsuper + 1));
     TRY(upload(c, &c.sym.vpush_pos, S.vpush_pos.data(), (int64_t)S.vpush_pos.size()));
     TRY(upload(c, &c.sym.vcol_ptr, S.vcol_ptr.data(), (int64_t)S.vcol_ptr.size()));
+    TRY(upload(c, &c.sym.vt_lo, S.vt_lo.data(), (int64_t)S.vt_lo.size()));
+    TRY(upload(c, &c.sym.vt_hi, S.vt_hi.data(), (int64_t)S.vt_hi.size()));
+    TRY(upload(c, &c.sym.vn_lo, S.vn_lo.data(), (int64_t)S.vn_lo.size()));
+    TRY(upload(c, &c.sym.vn_hi, S.vn_hi.data(), (int64_t)S.vn_hi.size()));
+    TRY(upload(c, &c.sym.tfold_cols, S.tfold_cols.data(), (int64_t)S.tfold_cols.size()));
+    c.sym.ntfold = (int64_t)S.tfold_cols.size();
     TRY(upload(c, &c.sym.desc32, S.desc32.data(), (int64_t)S.desc32.size()));
     TRY(upload(c, &c.sym.desc64, S.desc64.data(), (int64_t)S.desc64.size()));
     TRY(upload(c, &c.sym.need, S.need.data(), (int64_t)S.need.size()));

@@ -44,6 +44,9 @@ struct DevSymbolic {
     int64_t* cv_off = nullptr;
     int64_t* vpush_pos = nullptr;
     int64_t* vcol_ptr = nullptr;
+    int64_t *vt_lo = nullptr, *vt_hi = nullptr, *vn_lo = nullptr, *vn_hi = nullptr;
+    int32_t* tfold_cols = nullptr;
+    int64_t ntfold = 0;
     int32_t* desc32 = nullptr;
     int64_t* desc64 = nullptr;
     int32_t* need = nullptr;

@@ -430,7 +430,8 @@ struct TailSolveArgs {
     int c0, w, r, nbd;
     int64_t dim, nv, cvo;
     const int32_t* rows;       // sn_rows + r0 (permuted row indices)
-    const int64_t* vcol_ptr;
+    const int64_t* vn_lo;      // non-tiny vector-inbox entries of each column (tiny ones are folded)
+    const int64_t* vn_hi;
     const int64_t* vpush_pos;
     int* flags;                // nbd flags
     int* ticket;
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
                 const int col = a.c0 + row0 + ri;
                 v = x[q * a.dim + col];
                 const T* vq = vin + q * a.nv;
-                for (int64_t e = a.vcol_ptr[col]; e < a.vcol_ptr[col + 1]; ++e) v -= __ldcg(vq + e);
+                for (int64_t e = a.vn_lo[col]; e < a.vn_hi[col]; ++e) v -= __ldcg(vq + e);
             }
             acc[q][ri] = v;
         }
@@ -714,7 +715,8 @@ TailSolveArgs tail_args(Ctx& c, const TailNode& t, int which, int act0, int act1
     a.nv = c.sym.nv;
     a.cvo = c.host_sym.cv_off[t.J];
     a.rows = c.sym.sn_rows + t.r0;
-    a.vcol_ptr = c.sym.vcol_ptr;
+    a.vn_lo = c.sym.vn_lo;
+    a.vn_hi = c.sym.vn_hi;
     a.vpush_pos = c.sym.vpush_pos;
     a.flags = c.tflags + t.flag_off + (which ? t.nbd : 0);
     a.ticket = c.tflags + t.flag_off + 2 * t.nbd + which;

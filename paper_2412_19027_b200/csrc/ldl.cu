@@ -999,6 +999,28 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
     }
 }
 
+// after the tiny leaves: fold their vector-inbox entries into the right-hand side,
+// one thread per receiving column, entries in ascending order (deterministic);
+// the persistent sweep then gathers only the entries of non-tiny children
+template <typename T>
+__global__ void __launch_bounds__(256) tiny_fold_kernel(SolveArgs a0, const int32_t* __restrict__ cols, int64_t ncols,
+                                                        const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+                                                        T* x, const T* __restrict__ vin) {
+    SolveArgs a = a0;
+    resolve_act(a.rstate, a.act0, a.act1);
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= ncols) return;
+    const int32_t j = cols[k];
+    const int64_t e0 = lo[j], e1 = hi[j];
+    for (int q = 0; q < 2; ++q) {
+        if (!(q == 0 ? a.act0 : a.act1)) continue;
+        const T* vq = vin + (int64_t)q * a.nv;
+        T s = (T)0;
+        for (int64_t e = e0; e < e1; ++e) s += vq[e];
+        x[(int64_t)q * a.dim + j] -= s;
+    }
+}
+
 // tiny leaves, forward: one thread each (launched before the persistent sweep)
 template <typename T>
 __global__ void __launch_bounds__(128) fwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
@@ -1336,6 +1358,12 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         c.launches++;
     }
     f.ntiny = 0;
+    if (c.sym.ntfold > 0) {
+        tiny_fold_kernel<T><<<grid_for(c.sym.ntfold, 256), 256, 0, c.stream>>>(f, c.sym.tfold_cols, c.sym.ntfold,
+                                                                               c.sym.vt_lo, c.sym.vt_hi, t,
+                                                                               (const T*)c.vin);
+        c.launches++;
+    }
     if (f.nstart > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     k_tail_forward(c, t, act0, act1);
     k_tail_backward(c, t, act0, act1);

@@ -881,6 +881,43 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                 S.tiny.push_back(J);
             }
         }
+        // vector inbox re-laid per target supernode: tiny sources first, then the rest
+        {
+            std::vector<int64_t> tc(dim, 0), nc(dim, 0);
+            for (int32_t K = 0; K < ns; ++K) {
+                const int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+                for (int64_t p = S.sn_rptr[K] + w; p < S.sn_rptr[K + 1]; ++p) (tiny[K] ? tc : nc)[S.sn_rows[p]]++;
+            }
+            S.vt_lo.assign(dim, 0);
+            S.vt_hi.assign(dim, 0);
+            S.vn_lo.assign(dim, 0);
+            S.vn_hi.assign(dim, 0);
+            S.tfold_cols.clear();
+            for (int32_t J = 0; J < ns; ++J) {
+                const int64_t c0 = S.sn_col[J], c1 = S.sn_col[J + 1];
+                int64_t t = S.vcol_ptr[c0], tot_t = 0;
+                for (int64_t j = c0; j < c1; ++j) tot_t += tc[j];
+                int64_t u = S.vcol_ptr[c0] + tot_t;
+                for (int64_t j = c0; j < c1; ++j) {
+                    S.vt_lo[j] = t;
+                    t += tc[j];
+                    S.vt_hi[j] = t;
+                    S.vn_lo[j] = u;
+                    u += nc[j];
+                    S.vn_hi[j] = u;
+                    if (tc[j] > 0) S.tfold_cols.push_back((int32_t)j);
+                }
+            }
+            std::vector<int64_t> tf(S.vt_lo), nf(S.vn_lo);
+            for (int32_t K = 0; K < ns; ++K) {
+                const int64_t w = S.sn_col[K + 1] - S.sn_col[K];
+                int64_t a = 0;
+                for (int64_t p = S.sn_rptr[K] + w; p < S.sn_rptr[K + 1]; ++p, ++a) {
+                    const int32_t j = S.sn_rows[p];
+                    S.vpush_pos[S.cv_off[K] + a] = tiny[K] ? tf[j]++ : nf[j]++;
+                }
+            }
+        }
         std::vector<int32_t> need_fac(ns, 0), need_solve(ns, 0);
         for (int32_t J = 0; J < ns; ++J) {
             const int32_t P = S.sn_parent[J];
@@ -902,7 +939,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
             int64_t* e = &S.desc64[(size_t)J * 8];
             e[0] = S.sn_loff[J];
             e[1] = S.cv_off[J];
-            e[2] = S.vcol_ptr[S.sn_col[J]];
+            e[2] = S.vn_lo[S.sn_col[J]];            // non-tiny part of the vector inbox
             e[3] = S.vcol_ptr[S.sn_col[J + 1]];
             e[4] = S.irow_ptr[S.sn_rptr[J]];
             e[5] = S.irow_ptr[S.sn_rptr[J + 1]];
@@ -929,7 +966,8 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         S.vin_col.assign((size_t)S.vcol_ptr[dim], 0);
         for (int64_t j = 0; j < dim; ++j) {
             const int32_t J = S.col2sn[j];
-            for (int64_t e = S.vcol_ptr[j]; e < S.vcol_ptr[j + 1]; ++e) S.vin_col[e] = (uint8_t)(j - S.sn_col[J]);
+            for (int64_t e = S.vt_lo[j]; e < S.vt_hi[j]; ++e) S.vin_col[e] = (uint8_t)(j - S.sn_col[J]);
+            for (int64_t e = S.vn_lo[j]; e < S.vn_hi[j]; ++e) S.vin_col[e] = (uint8_t)(j - S.sn_col[J]);
         }
     }
     (void)lin;

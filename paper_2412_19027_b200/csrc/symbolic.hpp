@@ -88,6 +88,14 @@ struct Symbolic {
     std::vector<int32_t> start_fac_warp;   // warp-tier supernodes with no warp-tier children
     std::vector<int32_t> start_fac_cta;    // CTA-tier supernodes with no CTA-tier children
     std::vector<uint8_t> vin_col;          // vector-inbox entry -> local column in its supernode
+    // Within each target supernode's inbox region, the entries pushed by tiny
+    // leaves come first (grouped by column), then the rest (grouped by column):
+    // column j's tiny entries are [vt_lo[j], vt_hi[j]), its other entries
+    // [vn_lo[j], vn_hi[j]).  The forward sweep folds the tiny entries into the
+    // right-hand side in one parallel pass (tfold_cols: columns with any), so the
+    // persistent kernel gathers only [desc64 vlo, vhi) = the non-tiny part.
+    std::vector<int64_t> vt_lo, vt_hi, vn_lo, vn_hi;   // dim
+    std::vector<int32_t> tfold_cols;
     std::vector<int32_t> tiny;             // leaves with w <= 4, r <= 16: one lane each (factor, solves)
     std::vector<int32_t> bwd_order;        // backward tickets (reversed): non-tail, non-tiny, topological
     // scatter maps into the panel value array (int64 positions)
