@@ -1207,8 +1207,13 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
 
 template <typename T>
 __global__ void gather_perm(const double* __restrict__ r, T* __restrict__ t, const int32_t* __restrict__ perm,
-                            int64_t dim, int act0, int act1, const double* rstate) {
+                            int64_t dim, int act0, int act1, const double* rstate, int32_t* __restrict__ z0,
+                            int64_t n0, int32_t* __restrict__ z1, int64_t n1, int32_t* __restrict__ z2, int64_t n2) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // the sweeps' dependency counters / done flags / tail flags, reset in the same pass
+    for (int64_t i = k; i < n0; i += (int64_t)gridDim.x * blockDim.x) z0[i] = 0;
+    for (int64_t i = k; i < n1; i += (int64_t)gridDim.x * blockDim.x) z1[i] = 0;
+    for (int64_t i = k; i < n2; i += (int64_t)gridDim.x * blockDim.x) z2[i] = 0;
     resolve_act(rstate, act0, act1);
     if (k >= dim) return;
     const int32_t p = perm[k];
@@ -1336,14 +1341,46 @@ int factor_t(Ctx& c) {
     return CIPM_OK;
 }
 
+// CIPM_PHASES=1 (probes only): per-launch warm timings of one sweep pair, on stderr
+struct PhaseTimer {
+    Ctx& c;
+    bool on;
+    std::vector<std::pair<const char*, cudaEvent_t>> ev;
+    explicit PhaseTimer(Ctx& cc) : c(cc), on(false) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(c.stream, &st);
+        on = getenv("CIPM_PHASES") != nullptr && st == cudaStreamCaptureStatusNone;
+        mark("start");
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, c.stream);
+        ev.emplace_back(name, e);
+    }
+    ~PhaseTimer() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back().second);
+        fprintf(stderr, "[phases]");
+        for (size_t k = 1; k < ev.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[k - 1].second, ev[k].second);
+            fprintf(stderr, " %s=%.1f", ev[k].first, ms * 1000.f);
+        }
+        fprintf(stderr, " us\n");
+        for (auto& p : ev) cudaEventDestroy(p.second);
+    }
+};
+
 template <typename T>
 void refine_solve_t(Ctx& c, int act0, int act1) {
+    PhaseTimer pt(c);
     T* t = (T*)c.rt;
-    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1, c.rstate);
-    cudaMemsetAsync(c.fac_count, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
-    cudaMemsetAsync(c.bwd_done, 0, sizeof(int32_t) * c.sym.nsuper, c.stream);
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 8, c.stream);
-    if (c.tflag_total) cudaMemsetAsync(c.tflags, 0, sizeof(int32_t) * c.tflag_total, c.stream);
+    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1, c.rstate,
+                                                               c.fac_count, c.sym.nsuper, c.bwd_done, c.sym.nsuper,
+                                                               c.tflags, c.tflag_total);
     int e0 = 0;
     if (c.profile) {
         e0 = (int)(2 * (c.ev_factor.size() + c.ev_solve.size()));
@@ -1357,6 +1394,7 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         fwd_tiny_kernel<T><<<grid_for(f.ntiny, 128), 128, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
         c.launches++;
     }
+    pt.mark("gather+fwd_tiny");
     f.ntiny = 0;
     if (c.sym.ntfold > 0) {
         tiny_fold_kernel<T><<<grid_for(c.sym.ntfold, 256), 256, 0, c.stream>>>(f, c.sym.tfold_cols, c.sym.ntfold,
@@ -1364,13 +1402,18 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
                                                                                (const T*)c.vin);
         c.launches++;
     }
+    pt.mark("fold");
     if (f.nstart > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+    pt.mark("forward");
     k_tail_forward(c, t, act0, act1);
+    pt.mark("tail_fwd");
     k_tail_backward(c, t, act0, act1);
+    pt.mark("tail_bwd");
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
     b.ticket_tiny = c.tickets + 6;
     if (b.n_main > 0)
         backward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+    pt.mark("backward");
     if (b.ntiny > 0) {
         bwd_tiny_kernel<T><<<grid_for(b.ntiny, 128), 128, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
         c.launches++;
@@ -1379,8 +1422,10 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_solve.emplace_back(e0, e0 + 1);
     }
+    pt.mark("bwd_tiny");
     scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1,
                                                                     c.rstate);
+    pt.mark("scatter");
     c.launches += 4;
 }
 
