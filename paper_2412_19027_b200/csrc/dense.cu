@@ -51,11 +51,19 @@ __global__ void __launch_bounds__(256) tail_gather(T* __restrict__ L, int r, con
     const int64_t lo = irow[tr], hi = irow[tr + 1];
     int carry_t = -1;
     T carry = (T)0;
+    // next chunk's entries are requested before the current one is scanned
+    int tg_n = lo + lane < hi ? tgt[lo + lane] : -(lane + 2);
+    T v_n = lo + lane < hi ? __ldcg(inbox + lo + lane) : (T)0;
     for (int64_t base = lo; base < hi; base += 32) {
         const int64_t e = base + lane;
         const bool valid = e < hi;
-        const int tg = valid ? tgt[e] : -(lane + 2);
-        T v = valid ? __ldcg(inbox + e) : (T)0;
+        const int tg = tg_n;
+        T v = v_n;
+        {
+            const int64_t en = e + 32;
+            tg_n = en < hi ? tgt[en] : -(lane + 2);
+            v_n = en < hi ? __ldcg(inbox + en) : (T)0;
+        }
         const int t0 = __shfl_sync(0xffffffffu, tg, 0);
         if (carry_t >= 0 && t0 != carry_t) {
             if (lane == 0) L[carry_t] -= carry;
@@ -571,11 +579,28 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
     for (int j = warp; j < ncol; j += 8) {
         const T* Lc = L + (int64_t)(col0 + j) * a.r;
         T s0 = (T)0, s1 = (T)0;
-        for (int i = a.w + lane; i < a.r; i += 32) {
-            const T l = Lc[i];
-            const int gi = a.rows[i];
-            if (act[0]) s0 += l * __ldcg(x + gi);
-            if (act[1]) s1 += l * __ldcg(x + a.dim + gi);
+        // 8 rows per lane in flight: the index -> value gathers are latency-bound
+        // (narrow tail supernodes have thousands of off rows)
+        for (int i0 = a.w + lane; i0 < a.r; i0 += 32 * 8) {
+            int gi[8];
+            T l[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + 32 * u;
+                gi[u] = i < a.r ? a.rows[i] : -1;
+                l[u] = i < a.r ? Lc[i] : (T)0;
+            }
+            T v0[8], v1[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                v0[u] = (act[0] && gi[u] >= 0) ? __ldcg(x + gi[u]) : (T)0;
+                v1[u] = (act[1] && gi[u] >= 0) ? __ldcg(x + a.dim + gi[u]) : (T)0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                s0 += l[u] * v0[u];
+                s1 += l[u] * v1[u];
+            }
         }
         for (int o = 16; o > 0; o >>= 1) {
             s0 += __shfl_down_sync(0xffffffffu, s0, o);
