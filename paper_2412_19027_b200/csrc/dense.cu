@@ -121,9 +121,16 @@ __global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int k
     __shared__ double s_runmax;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
     T* B = L + (int64_t)kb * r + kb;
-    for (int idx = tid; idx < TB * TB; idx += nt) {
-        const int i = idx & (TB - 1), j = idx >> 6;
-        S[idx] = (i < nb && j < nb && i >= j) ? B[(int64_t)j * r + i] : (T)0;
+    {
+        // all 16 loads of a thread in flight at once (blockDim = 256)
+        T v[TB * TB / 256];
+#pragma unroll
+        for (int u = 0; u < TB * TB / 256; ++u) {
+            const int idx = tid + 256 * u, i = idx & (TB - 1), j = idx >> 6;
+            v[u] = (i < nb && j < nb && i >= j) ? B[(int64_t)j * r + i] : (T)0;
+        }
+#pragma unroll
+        for (int u = 0; u < TB * TB / 256; ++u) S[tid + 256 * u] = v[u];
     }
     if (tid < nb) sSg[tid] = sign[c0 + kb + tid];
     if (tid == 0) s_runmax = *maxd;
@@ -478,6 +485,7 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
     const bool act[2] = {a.act0 != 0, a.act1 != 0};
     if (diag) {
         const T* I = inv + (int64_t)b * TB * TB;
+#pragma unroll
         for (int e = tid; e < TB * TB; e += 256) inv_s[e] = I[e];
     }
     if (kp == 0) {
@@ -573,6 +581,7 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
     const bool act[2] = {a.act0 != 0, a.act1 != 0};
     {
         const T* I = inv + (int64_t)b * TB * TB;
+#pragma unroll
         for (int e = tid; e < TB * TB; e += 256) inv_s[e] = I[e];
     }
     // off rows (ancestors' x is final)
