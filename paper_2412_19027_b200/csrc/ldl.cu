@@ -617,7 +617,14 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         const int64_t psize = (int64_t)r * w;
         const bool in_smem = psize <= a.smem_cap;
         if (in_smem)
-            for (int64_t i = tid; i < psize; i += nt) sp[i] = L[i];
+            for (int64_t i0 = tid; i0 < psize; i0 += (int64_t)nt * 8) {   // 8 loads per thread in flight
+                T v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = i0 + nt * u < psize ? L[i0 + nt * u] : (T)0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i0 + nt * u < psize) sp[i0 + nt * u] = v[u];
+            }
         if (tid < w) sSg[tid] = a.sign[c0 + tid];
         __syncthreads();
         if (a.trace && tid == 0) a.trace[6 * J + 2] = gtimer();
