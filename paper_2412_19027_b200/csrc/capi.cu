@@ -288,6 +288,11 @@ int cipm_symbolic_array(const cipm_symbolic* sym, const char* name, void* dst, i
     ARR("cv_off", s.cv_off)
     ARR("vpush_pos", s.vpush_pos)
     ARR("vcol_ptr", s.vcol_ptr)
+    ARR("vt_lo", s.vt_lo)
+    ARR("vt_hi", s.vt_hi)
+    ARR("vn_lo", s.vn_lo)
+    ARR("vn_hi", s.vn_hi)
+    ARR("tfold_cols", s.tfold_cols)
     ARR("tier", s.tier)
     ARR("level", s.level)
     ARR("desc32", s.desc32)

@@ -221,7 +221,8 @@ class SymbolicAnalysis:
         cnt = c_i64(0)
         raise_for_status(lib().cipm_symbolic_array(self.handle, name.encode(), None, ctypes.byref(cnt)))
         dt = np.int32 if name in ("perm", "md_perm", "sn_col", "sn_rows", "sn_parent", "upd_src", "upd_p0",
-                                  "upd_p1", "order", "inbox_tgt", "level", "desc32", "tiny") else (
+                                  "upd_p1", "order", "inbox_tgt", "level", "desc32", "tiny",
+                                  "tfold_cols") else (
             np.int8 if name == "tier" else np.int64)
         out = np.empty(cnt.value, dtype=dt)
         if cnt.value:

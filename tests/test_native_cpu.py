@@ -146,3 +146,34 @@ def test_auto_ordering_keeps_reference_md_when_small_or_fill_heavy():
     assert sym.info()["ordering"] == 0
     o = OracleSolver(prob, SolverSettings())
     np.testing.assert_array_equal(sym.array("md_perm"), o.kkt.perm)
+
+
+@pytest.mark.parametrize("name", ["lasso_40x160", "lp_150x300", "socp_10", "mpc_s0"])
+def test_vector_inbox_tiny_first_layout(name):
+    """Each supernode's vector inbox holds the tiny leaves' entries first, then the
+    rest, both grouped by column; every push position is used exactly once and a
+    tiny source lands in its column's tiny range (the fold pass sums exactly those)."""
+    _, s = _scaled(name)
+    sym = native.SymbolicAnalysis(s.P, s.A, native.Layout(s.cones))
+    col, rptr, rows = sym.array("sn_col"), sym.array("sn_rptr"), sym.array("sn_rows")
+    vcp, cvo, vpp = sym.array("vcol_ptr"), sym.array("cv_off"), sym.array("vpush_pos")
+    tlo, thi, nlo, nhi = (sym.array(k) for k in ("vt_lo", "vt_hi", "vn_lo", "vn_hi"))
+    tiny = set(sym.array("tiny").tolist())
+    ns = len(col) - 1
+    assert np.array_equal(np.sort(vpp), np.arange(vcp[-1]))          # a permutation of the inbox slots
+    for J in range(ns):
+        c0, c1 = col[J], col[J + 1]
+        lo, hi = vcp[c0], vcp[c1]
+        t_tot = int(np.sum(thi[c0:c1] - tlo[c0:c1]))
+        assert tlo[c0] == lo and nlo[c0] == lo + t_tot and nhi[c1 - 1] == hi
+        assert np.all(tlo[c0 + 1:c1] == thi[c0:c1 - 1]) and np.all(nlo[c0 + 1:c1] == nhi[c0:c1 - 1])
+    fold = set(sym.array("tfold_cols").tolist())
+    assert fold == {j for j in range(len(tlo)) if thi[j] > tlo[j]}
+    for K in range(ns):
+        w = col[K + 1] - col[K]
+        for a, p in enumerate(range(rptr[K] + w, rptr[K + 1])):
+            j, pos = rows[p], vpp[cvo[K] + a]
+            if K in tiny:
+                assert tlo[j] <= pos < thi[j]
+            else:
+                assert nlo[j] <= pos < nhi[j]
