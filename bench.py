@@ -282,6 +282,25 @@ def cpu_sample(args):
 # our arm
 # ---------------------------------------------------------------------------
 
+def fp64_peak_tflops(device):
+    """FP64 tensor-pipe reference peak of this GPU: cuBLAS DGEMM 8192^3 (best of 5)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=device)
+    b = torch.randn(n, n, dtype=torch.float64, device=device)
+    torch.matmul(a, b)
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize(device)
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b
+    return 2.0 * n ** 3 / best / 1e12
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -556,6 +575,14 @@ def run_ours(args):
             "traffic": ncu_traffic(args.config), "peak_source": peak_kind, "dominant": dom,
             "factor_ms_avg": fac_ms / fac_n if fac_n else None,
             "solve_ms_avg_per_pair": sol_ms / sol_n if sol_n else None}
+    if "tflops" in dom and cfg.precision == "full":
+        # factorisation-dominated (dense tail on the FP64 tensor pipe): the tensor roofline,
+        # against a DGEMM measured here (MEASURED_PEAKS.json has no FP64 figure)
+        f64 = fp64_peak_tflops(f"cuda:{local}")
+        roof.update({"bound": "tensor", "achieved": dom["tflops"], "peak": f64, "unit": "TFLOP/s",
+                     "frac": dom["tflops"] / f64, "traffic": None,
+                     "peak_source": "measured here: cuBLAS DGEMM (torch.matmul float64 8192^3, best of 5)",
+                     "hbm_view": {"achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm}})
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

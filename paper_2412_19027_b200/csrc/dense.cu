@@ -495,7 +495,14 @@ __global__ void __launch_bounds__(256) tail_fwd(TailSolveArgs a0, const T* __res
                 const int col = a.c0 + row0 + ri;
                 v = x[q * a.dim + col];
                 const T* vq = vin + q * a.nv;
-                for (int64_t e = a.vn_lo[col]; e < a.vn_hi[col]; ++e) v -= __ldcg(vq + e);
+                const int64_t e1 = a.vn_hi[col];
+                for (int64_t e0 = a.vn_lo[col]; e0 < e1; e0 += 4) {      // 4 entries in flight, fixed order
+                    T u[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) u[k] = e0 + k < e1 ? __ldcg(vq + e0 + k) : (T)0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v -= u[k];
+                }
             }
             acc[q][ri] = v;
         }
