@@ -128,7 +128,9 @@ int cipm_ctx_set_values(cipm_ctx *ctx, const double *p_values, const double *a_v
  * a_src[k] = user A-value index of reordered A nonzero k (set once) */
 int cipm_ctx_set_reorder(cipm_ctx *ctx, const int64_t *row_perm, const int64_t *a_src);
 /* raw USER-order values (P full symmetric values, A values, q, b) -> H2D, reorder, 10 Ruiz
- * rounds (bitwise the reference's arithmetic) when equilibrate != 0, factor base image */
+ * rounds (bitwise the reference's arithmetic) when equilibrate != 0, factor base image.
+ * After the first call a NULL array keeps the device's previous raw values (update_data
+ * with only q / b changed sends only q / b). */
 int cipm_ctx_set_problem(cipm_ctx *ctx, const double *p_values, const double *a_values,
                          const double *q, const double *b, int equilibrate);
 /* the equilibration of the last set_problem: d_row (m), d_col (n), c_obj */

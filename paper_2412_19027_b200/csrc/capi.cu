@@ -426,6 +426,8 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(dalloc(c, &c.b, c.m));
     TRY(dalloc(c, &c.a_user, c.a_nnz));
     TRY(dalloc(c, &c.b_user, c.m));
+    TRY(dalloc(c, &c.p_user, c.p_nnz));
+    TRY(dalloc(c, &c.q_user, c.n));
     TRY(dalloc(c, &c.a_src, c.a_nnz));
     TRY(dalloc(c, &c.b_src, c.m));
     TRY(dalloc(c, &c.eq_cnorm, c.n));
@@ -638,12 +640,31 @@ int cipm_ctx_set_problem(cipm_ctx* h, const double* p_values, const double* a_va
     Ctx& c = h->c;
     if (!c.have_reorder) return CIPM_E_ARG;
     CIPM_CUDA(cudaSetDevice(c.device));
-    if (c.p_nnz) CIPM_CUDA(cudaMemcpyAsync(c.p_v, p_values, sizeof(double) * c.p_nnz, cudaMemcpyHostToDevice, c.stream));
-    if (c.a_nnz)
+    // a NULL array keeps the raw values of the previous call (parametric re-solve:
+    // only the changed arrays cross PCIe); the first call must pass all four
+    const bool have = c.have_user_values;
+    if (!have && ((!p_values && c.p_nnz) || (!a_values && c.a_nnz) || (!q && c.n) || (!b && c.m)))
+        return CIPM_E_ARG;
+    if (p_values && c.p_nnz) {
+        CIPM_CUDA(cudaMemcpyAsync(c.p_user, p_values, sizeof(double) * c.p_nnz, cudaMemcpyHostToDevice, c.stream));
+        c.h2d_bytes += (int64_t)sizeof(double) * c.p_nnz;
+    }
+    if (a_values && c.a_nnz) {
         CIPM_CUDA(cudaMemcpyAsync(c.a_user, a_values, sizeof(double) * c.a_nnz, cudaMemcpyHostToDevice, c.stream));
-    CIPM_CUDA(cudaMemcpyAsync(c.q, q, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
-    CIPM_CUDA(cudaMemcpyAsync(c.b_user, b, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
-    c.h2d_bytes += (int64_t)sizeof(double) * (c.p_nnz + c.a_nnz + c.n + c.m);
+        c.h2d_bytes += (int64_t)sizeof(double) * c.a_nnz;
+    }
+    if (q && c.n) {
+        CIPM_CUDA(cudaMemcpyAsync(c.q_user, q, sizeof(double) * c.n, cudaMemcpyHostToDevice, c.stream));
+        c.h2d_bytes += (int64_t)sizeof(double) * c.n;
+    }
+    if (b && c.m) {
+        CIPM_CUDA(cudaMemcpyAsync(c.b_user, b, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+        c.h2d_bytes += (int64_t)sizeof(double) * c.m;
+    }
+    c.have_user_values = true;
+    if (c.p_nnz)
+        CIPM_CUDA(cudaMemcpyAsync(c.p_v, c.p_user, sizeof(double) * c.p_nnz, cudaMemcpyDeviceToDevice, c.stream));
+    if (c.n) CIPM_CUDA(cudaMemcpyAsync(c.q, c.q_user, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
     int rc = k_set_problem(c, equilibrate != 0);
     if (rc) return rc;
     CIPM_CUDA(cudaMemcpyAsync(&c.c_obj, c.eq_cobj, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

@@ -103,6 +103,8 @@ struct Ctx {
     double *q = nullptr, *b = nullptr, *dr = nullptr, *dc = nullptr;
     // device-side setup (setup.cu): user-order raw values, reorder maps, Ruiz work
     double *a_user = nullptr, *b_user = nullptr;
+    double *p_user = nullptr, *q_user = nullptr;   // raw user values (P, q are scaled in place)
+    bool have_user_values = false;
     int64_t *a_src = nullptr, *b_src = nullptr;
     bool have_reorder = false;
     double *eq_cnorm = nullptr, *eq_rnorm = nullptr, *eq_cstep = nullptr, *eq_rstep = nullptr, *eq_cobj = nullptr;

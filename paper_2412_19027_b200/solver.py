@@ -146,13 +146,15 @@ class Solver:
 
     # -- data plumbing --------------------------------------------------------
 
-    def _upload_values(self):
+    def _upload_values(self, changed=(True, True, True, True)):
         """Raw user-order values to the device; cone reordering and Ruiz equilibration
-        run there (setup.cu, bitwise the reference's problem.py:177-284 arithmetic)."""
+        run there (setup.cu, bitwise the reference's problem.py:177-284 arithmetic).
+        Arrays flagged unchanged (P, A, q, b) are not re-sent: the device keeps the
+        previous raw values."""
         prob = self._original
         self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (prob.P.values, prob.A.values, prob.q, prob.b)]
-        k = self._keep
-        self._ctx.call("cipm_ctx_set_problem", pdbl(k[0]), pdbl(k[1]), pdbl(k[2]), pdbl(k[3]),
+        k = [pdbl(a) if ch else None for a, ch in zip(self._keep, changed)]
+        self._ctx.call("cipm_ctx_set_problem", k[0], k[1], k[2], k[3],
                        1 if self.settings.do_equilibrate else 0)
         d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
         self._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
@@ -181,7 +183,7 @@ class Solver:
                           np.asarray(b, dtype=np.float64).copy() if b is not None else prob.b, prob.cones)
         validate_values(new, P is not None, A is not None, q is not None, b is not None)
         self._original = new
-        self._upload_values()
+        self._upload_values((P is not None, A is not None, q is not None, b is not None))
 
     def _block_list(self):
         lay = self.layout
