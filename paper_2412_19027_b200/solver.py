@@ -156,9 +156,11 @@ class Solver:
         k = [pdbl(a) if ch else None for a, ch in zip(self._keep, changed)]
         self._ctx.call("cipm_ctx_set_problem", k[0], k[1], k[2], k[3],
                        1 if self.settings.do_equilibrate else 0)
-        d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
-        self._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
-        self._equil = Equilibration(d_row, d_col, float(c_obj.value))
+        # only the scalar c is needed per iteration; D_r / D_c are fetched when a
+        # result is recovered (_scaling), not on every parametric update
+        c_obj = ctypes.c_double(1.0)
+        self._ctx.call("cipm_ctx_get_equilibration", None, None, ctypes.byref(c_obj))
+        self._equil = Equilibration(None, None, float(c_obj.value))
         # termination norms use the reordered unscaled data (ipm.py:184-185); max is order-free
         self._norm_q = float(np.max(np.abs(prob.q))) if prob.q.size else 0.0
         self._norm_b = float(np.max(np.abs(prob.b))) if prob.b.size else 0.0
@@ -255,6 +257,10 @@ class Solver:
         st = self._state(which)
         if tkm is not None:
             st.tau, st.kappa, st.mu = tkm
+        if self._equil.d_row is None:
+            d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
+            self._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
+            self._equil = Equilibration(d_row, d_col, float(c_obj.value))
         x_u, z_u, s_u = unscale_solution(st.x, st.z, st.s, self._equil)
         cert = None
         if status not in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
