@@ -210,6 +210,7 @@ int cipm_batch_set_values(cipm_batch *b, const double *V, const double *q, const
  * order), q, b.  Results then come back unscaled, divided by tau (not for infeasibility
  * certificates) and in the user's row order. */
 int cipm_batch_set_reorder(cipm_batch *b, const int64_t *row_perm, const int64_t *a_src);
+/* NULL V / q / bvec (after the first call) keep the device's previous raw arrays */
 int cipm_batch_set_raw_values(cipm_batch *b, const double *V, const double *q, const double *bvec,
                               int equilibrate);
 /* run every instance to termination; *ms = CUDA-event time of the launch */

@@ -154,13 +154,27 @@ class BatchSolver:
         raise_for_status(rc, "batch upload")
 
     def update_data(self, q=None, b=None):
-        """Parametric re-solve of every instance (same patterns): q, b as (count, n) / (count, m)."""
-        for k, p in enumerate(self.problems):
-            if q is not None:
-                p.q = np.asarray(q[k], dtype=np.float64).copy()
-            if b is not None:
-                p.b = np.asarray(b[k], dtype=np.float64).copy()
-        self._upload()
+        """Parametric re-solve of every instance (same patterns): q, b as (count, n) / (count, m).
+        Only the given arrays are sent; the device keeps the raw P / A values."""
+        qs = np.array(q, dtype=np.float64, order="C") if q is not None else None
+        bs = np.array(b, dtype=np.float64, order="C") if b is not None else None
+        if qs is not None and qs.shape != (self.count, self.n):
+            raise ValueError(f"q must be ({self.count}, {self.n})")
+        if bs is not None and bs.shape != (self.count, self.m):
+            raise ValueError(f"b must be ({self.count}, {self.m})")
+        for k, p in enumerate(self.problems):          # per-instance views (certificates, results)
+            if qs is not None:
+                p.q = qs[k]
+            if bs is not None:
+                p.b = bs[k]
+        if qs is not None:
+            self._host[1] = qs
+        if bs is not None:
+            self._host[2] = bs
+        rc = lib().cipm_batch_set_raw_values(self.handle, None, pdbl(qs) if qs is not None else None,
+                                             pdbl(bs) if bs is not None else None,
+                                             1 if self.settings.do_equilibrate else 0)
+        raise_for_status(rc, "batch upload")
 
     def info(self) -> dict:
         out = np.zeros(6, dtype=np.int64)

@@ -677,6 +677,7 @@ struct cipm_batch {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    bool have_raw = false;        // raw V / q / b uploaded once (NULL keeps them)
     int smem_bytes = 0;
     std::vector<void*> allocs;
     std::vector<int32_t> h_perm;
@@ -978,10 +979,22 @@ int cipm_batch_set_raw_values(cipm_batch* h, const double* V, const double* q, c
     if (!h || !h->pt.b_src) return CIPM_E_ARG;
     const int64_t c = h->count, n = h->pt.n, m = h->pt.m, nv = (int64_t)h->pt.nnz_p + h->pt.nnz_a;
     CIPM_CUDA(cudaSetDevice(h->device));
-    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.V, V, sizeof(double) * c * nv, cudaMemcpyHostToDevice, h->stream));
-    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.q, q, sizeof(double) * c * n, cudaMemcpyHostToDevice, h->stream));
-    CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.b, b, sizeof(double) * c * m, cudaMemcpyHostToDevice, h->stream));
-    h->h2d += (int64_t)sizeof(double) * c * (nv + n + m);
+    // NULL keeps the previous raw array (the kernel reads them, never writes them):
+    // a parametric update of q / b sends only q / b
+    if ((!V && nv && !h->have_raw) || (!q && n && !h->have_raw) || (!b && m && !h->have_raw)) return CIPM_E_ARG;
+    if (V && nv) {
+        CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.V, V, sizeof(double) * c * nv, cudaMemcpyHostToDevice, h->stream));
+        h->h2d += (int64_t)sizeof(double) * c * nv;
+    }
+    if (q && n) {
+        CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.q, q, sizeof(double) * c * n, cudaMemcpyHostToDevice, h->stream));
+        h->h2d += (int64_t)sizeof(double) * c * n;
+    }
+    if (b && m) {
+        CIPM_CUDA(cudaMemcpyAsync((void*)h->bd.b, b, sizeof(double) * c * m, cudaMemcpyHostToDevice, h->stream));
+        h->h2d += (int64_t)sizeof(double) * c * m;
+    }
+    h->have_raw = true;
     h->bd.device_setup = 1;
     h->bd.equilibrate = equilibrate ? 1 : 0;
     return CIPM_OK;
