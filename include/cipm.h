@@ -169,6 +169,27 @@ int cipm_get_direction(cipm_ctx *ctx, int combined, double *dx, double *dz, doub
 int cipm_get_vector(cipm_ctx *ctx, const char *name, double *out, int64_t *count);
 /* per-cone batched SOC residuals t^2 - |u|^2 with the reference's fixed order (steps.py:136-175) */
 int cipm_soc_residuals(cipm_ctx *ctx, const double *x, double *out);
+/* ---- kernel-level seams: the reference's L1 cone functions one call at a time
+ * (tests/test_gpu_seams.py checks them against tests/golden/kernels.json) ---- */
+/* set direction `which` (0 affine, 1 combined): dx (n), dz (m), ds (m), dtk = {dtau, dkappa};
+ * NULL arrays are left unchanged */
+int cipm_set_direction(cipm_ctx *ctx, int which, const double *dx, const double *dz, const double *ds,
+                       const double *dtk);
+/* step_length (cones/steps.py:79-116) of direction `which` at the current iterate
+ * (tau, kappa from cipm_set_iterate); CIPM_E_STEP below 1e-11 */
+int cipm_step_length(cipm_ctx *ctx, int which, double *alpha);
+/* combined_ds (cones/scaling.py:277-320) at the current scaling (cipm_update_scaling):
+ * out (m) from the affine dz_a, ds_a, sigma, mu */
+int cipm_combined_ds(cipm_ctx *ctx, const double *dz_a, const double *ds_a, double sigma, double mu,
+                     double *out);
+/* neighborhood_ok (cones/scaling.py:364-401) of the current s, z at the given mu, beta; ok = 0 / 1 */
+int cipm_neighborhood_ok(cipm_ctx *ctx, double mu, double beta, int *ok);
+/* is_in_cone(s) / is_in_dual_cone(z), strict (cones/set.py:166-207); overwrites the iterate */
+int cipm_membership(cipm_ctx *ctx, const double *s, const double *z, int *in_cone, int *in_dual);
+/* KKTSystem counters (kkt/system.py:78-79,261-262): out[0] = numeric factorisations
+ * since the context was created (num_numeric), out[1] = pivots bumped by the dynamic
+ * regularisation in the last factorisation (last_bumped_pivots) */
+int cipm_kkt_counters(cipm_ctx *ctx, int64_t *out);
 /* host<->device bytes moved by the API since the last reset (bench e2e accounting) */
 int cipm_io_bytes(cipm_ctx *ctx, int64_t *h2d, int64_t *d2h, int reset);
 /* kernel launches issued since the last reset (bench accounting) */

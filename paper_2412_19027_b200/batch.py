@@ -22,7 +22,7 @@ import time
 
 import numpy as np
 
-from .exceptions import ConicError, PatternMismatch, raise_for_status
+from .exceptions import ConicError, NonFiniteData, PatternMismatch, raise_for_status
 from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, reorder_cones, validate
 from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, pi64, require_device
 from .settings import FULL, SolveResult, SolverSettings, Status, default_dynamic_reg, default_static_reg
@@ -135,6 +135,7 @@ class BatchSolver:
         rc = lib().cipm_batch_set_raw_values(self.handle, *[pdbl(a) for a in self._host],
                                              1 if self.settings.do_equilibrate else 0)
         raise_for_status(rc, "batch upload")
+        self._raw_on_device = True
 
     def _upload_host_equilibrated(self):
         """Alternative path: host reorder + vectorised Ruiz (equilibrate_batch), scaled upload."""
@@ -152,6 +153,7 @@ class BatchSolver:
                       (np.concatenate([pv_s, av_s], axis=1), q_s, b_s, d_row, d_col, c_obj, norm_q, norm_b)]
         rc = lib().cipm_batch_set_values(self.handle, *[pdbl(a) for a in self._host])
         raise_for_status(rc, "batch upload")
+        self._raw_on_device = False
 
     def update_data(self, q=None, b=None):
         """Parametric re-solve of every instance (same patterns): q, b as (count, n) / (count, m).
@@ -162,6 +164,11 @@ class BatchSolver:
             raise ValueError(f"q must be ({self.count}, {self.n})")
         if bs is not None and bs.shape != (self.count, self.m):
             raise ValueError(f"b must be ({self.count}, {self.m})")
+        # the reference's update_data re-validates (problem.py:149-174): non-finite data raises
+        if qs is not None and not np.all(np.isfinite(qs)):
+            raise NonFiniteData("q")
+        if bs is not None and not np.all(np.isfinite(bs)):
+            raise NonFiniteData("b")
         for k, p in enumerate(self.problems):          # per-instance views (certificates, results)
             if qs is not None:
                 p.q = qs[k]
@@ -171,6 +178,9 @@ class BatchSolver:
             self._host[1] = qs
         if bs is not None:
             self._host[2] = bs
+        if not getattr(self, "_raw_on_device", True):
+            self._upload()                  # after a host-equilibrated upload: re-send the raw arrays
+            return
         rc = lib().cipm_batch_set_raw_values(self.handle, None, pdbl(qs) if qs is not None else None,
                                              pdbl(bs) if bs is not None else None,
                                              1 if self.settings.do_equilibrate else 0)

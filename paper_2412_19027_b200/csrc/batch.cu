@@ -962,6 +962,9 @@ int cipm_batch_set_values(cipm_batch* h, const double* V, const double* q, const
     if (!rc) rc = cp(h->bd.norm_q, norm_q, c);
     if (!rc) rc = cp(h->bd.norm_b, norm_b, c);
     h->bd.device_setup = 0;
+    // bd.V / q / b now hold reordered, scaled values: a later raw update must
+    // re-send every array (a NULL would reuse them as raw user-order data)
+    h->have_raw = false;
     return rc;
 }
 

@@ -746,6 +746,7 @@ int cipm_update_scaling(cipm_ctx* h) {
 
 int cipm_factor(cipm_ctx* h) {
     Ctx& c = h->c;
+    c.num_numeric++;
     // the whole factorisation (assembly, persistent tiers, dense tail) is a static
     // launch sequence: after one eager run it is captured once and replayed as a graph
     if (!c.use_graphs || c.profile || c.trace || c.factor_runs++ == 0) {
@@ -945,6 +946,104 @@ int cipm_soc_residuals(cipm_ctx* h, const double* x, double* out) {
     if (c.nsoc) CIPM_CUDA(copy_sync(c, out, dout, sizeof(double) * c.nsoc, cudaMemcpyDeviceToHost));
     cudaFree(dx);
     cudaFree(dout);
+    return CIPM_OK;
+}
+
+// ---- kernel-level seams (tests: the reference's L1 functions one at a time) ----
+
+int cipm_set_direction(cipm_ctx* h, int which, const double* dx, const double* dz, const double* ds,
+                       const double* dtk) {
+    if (!h || which < 0 || which > 1) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    if (dx && c.n) CIPM_CUDA(copy_sync(c, c.dx[which], dx, sizeof(double) * c.n, cudaMemcpyHostToDevice));
+    if (dz && c.m) CIPM_CUDA(copy_sync(c, c.dz[which], dz, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (ds && c.m) CIPM_CUDA(copy_sync(c, c.ds[which], ds, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    if (dtk) {
+        CIPM_CUDA(copy_sync(c, c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+        c.h_sc[which ? CIPM_SC_DTAU_C : CIPM_SC_DTAU_A] = dtk[0];
+        c.h_sc[which ? CIPM_SC_DKAPPA_C : CIPM_SC_DKAPPA_A] = dtk[1];
+        CIPM_CUDA(copy_sync(c, c.sc, c.h_sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyHostToDevice));
+    }
+    return CIPM_OK;
+}
+
+int cipm_step_length(cipm_ctx* h, int which, double* alpha) {
+    if (!h || which < 0 || which > 1) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    int e = step_length(c, which);
+    if (e) return e;
+    e = read_sc(c);
+    if (alpha) *alpha = c.h_sc[which ? CIPM_SC_ALPHA_C : CIPM_SC_ALPHA_A];
+    return e;
+}
+
+int cipm_combined_ds(cipm_ctx* h, const double* dz_a, const double* ds_a, double sigma, double mu, double* out) {
+    if (!h || !dz_a || !ds_a || !out) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    CIPM_CUDA(copy_sync(c, c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost));
+    c.h_sc[CIPM_SC_SIGMA] = sigma;
+    c.h_sc[CIPM_SC_MU] = mu;
+    CIPM_CUDA(copy_sync(c, c.sc, c.h_sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyHostToDevice));
+    if (c.m) {
+        CIPM_CUDA(copy_sync(c, c.dz[0], dz_a, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+        CIPM_CUDA(copy_sync(c, c.ds[0], ds_a, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+    }
+    k_combined_ds(c, c.dz[0], c.ds[0]);
+    int e = sync_err(c);
+    if (c.m) CIPM_CUDA(copy_sync(c, out, c.dsc, sizeof(double) * c.m, cudaMemcpyDeviceToHost));
+    return e;
+}
+
+int cipm_neighborhood_ok(cipm_ctx* h, double mu, double beta, int* ok) {
+    if (!h || !ok || !(mu > 0.0)) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    if (c.m) {
+        CIPM_CUDA(cudaMemsetAsync(c.dz[1], 0, sizeof(double) * c.m, c.stream));
+        CIPM_CUDA(cudaMemsetAsync(c.ds[1], 0, sizeof(double) * c.m, c.stream));
+    }
+    const double beta0 = c.beta;
+    c.beta = beta;
+    k_mu_candidates(c, 0, 1, mu);
+    k_neighborhood_mask(c, 0, 1);
+    c.beta = beta0;
+    unsigned int bits = 0;
+    CIPM_CUDA(cudaMemcpyAsync(&bits, c.mask, sizeof(unsigned int), cudaMemcpyDeviceToHost, c.stream));
+    int e = sync_err(c);
+    *ok = (bits & 1u) ? 1 : 0;
+    return e;
+}
+
+int cipm_membership(cipm_ctx* h, const double* s, const double* z, int* in_cone, int* in_dual) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    for (int side = 0; side < 2; ++side) {
+        const double* v = side == 0 ? s : z;
+        int* flag = side == 0 ? in_cone : in_dual;
+        if (!v || !flag) continue;
+        // the other side is the unit point (interior of both the cone and its dual)
+        CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+        k_init_iterate(c);
+        if (c.m) CIPM_CUDA(copy_sync(c, side == 0 ? c.s : c.z, v, sizeof(double) * c.m, cudaMemcpyHostToDevice));
+        k_membership(c);
+        int e = sync_err(c);
+        if (e != CIPM_OK && e != CIPM_E_INTERIOR) return e;
+        *flag = e == CIPM_OK ? 1 : 0;
+    }
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    return sync_err(c);
+}
+
+int cipm_kkt_counters(cipm_ctx* h, int64_t* out) {
+    if (!h || !out) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    int32_t bumps = 0;
+    CIPM_CUDA(copy_sync(c, &bumps, c.bumps, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    out[0] = c.num_numeric;
+    out[1] = bumps;
     return CIPM_OK;
 }
 

@@ -189,6 +189,7 @@ struct Ctx {
     cudaGraphExec_t factor_graph = nullptr;
     int64_t factor_graph_launches = 0;
     int64_t factor_runs = 0;
+    int64_t num_numeric = 0;         // numeric factorisations (KKTSystem.num_numeric, system.py:261)
     bool use_graphs = true;
 
     std::vector<void*> allocations;
@@ -216,7 +217,7 @@ void k_take_step(Ctx& c);
 void k_step_init(Ctx& c, int which);         // α bound from τ/κ
 void k_step_finish(Ctx& c, int which);       // α check + σ
 void k_kkt_residual(Ctx& c, int nrhs, const int* active_host);
-void k_mu_candidates(Ctx& c, int k0, int nk);
+void k_mu_candidates(Ctx& c, int k0, int nk, double mu_fixed = -1.0);
 void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs);
 // cones.cu
 void k_update_scaling(Ctx& c);

@@ -326,6 +326,7 @@ struct MuCand {
     int64_t m, nn0, nnd;
     double nu1, beta, bt, scale;
     int nk, g0;       // candidates in this batch, global index of the first
+    double mu_fixed;  // > 0: use this μ for every candidate (neighborhood_ok seam) instead of μ(trial)
 };
 
 __global__ void mu_candidates(MuCand a, double* sc, double* nb, unsigned int* mask, int* err, double* partials,
@@ -362,7 +363,7 @@ __global__ void mu_candidates(MuCand a, double* sc, double* nb, unsigned int* ma
             const double step = a.scale * alk;
             const double tt = sc[CIPM_SC_TAU] + step * sc[CIPM_SC_DTAU_C];
             const double kt = sc[CIPM_SC_KAPPA] + step * sc[CIPM_SC_DKAPPA_C];
-            const double mu_t = (out[k] + tt * kt) / a.nu1;
+            const double mu_t = a.mu_fixed > 0.0 ? a.mu_fixed : (out[k] + tt * kt) / a.nu1;
             nb[k] = mu_t;
             nb[16 + k] = step;
             nb[32 + k] = alk;
@@ -578,9 +579,9 @@ void k_step_store(Ctx& c, int which) {
     c.launches++;
 }
 
-void k_mu_candidates(Ctx& c, int g0, int nk) {
+void k_mu_candidates(Ctx& c, int g0, int nk, double mu_fixed) {
     MuCand a{c.s, c.z, c.ds[1], c.dz[1], c.m, c.zero_dim, c.nonneg_dim, c.nu + 1.0, c.beta, c.backtrack,
-             c.step_scale, nk, g0};
+             c.step_scale, nk, g0, mu_fixed};
     mu_candidates<<<red_grid(c.m), kThreads, 0, c.stream>>>(a, c.sc, c.nb, c.mask, c.err, c.partials, c.counter);
     c.launches++;
 }

@@ -92,6 +92,13 @@ _SIGS = {
     "cipm_get_direction": ([c_void_p, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_get_vector": ([c_void_p, ctypes.c_char_p, P_DBL, P_I64], ctypes.c_int),
     "cipm_soc_residuals": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_set_direction": ([c_void_p, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_step_length": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
+    "cipm_combined_ds": ([c_void_p, P_DBL, P_DBL, c_dbl, c_dbl, P_DBL], ctypes.c_int),
+    "cipm_neighborhood_ok": ([c_void_p, c_dbl, c_dbl, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "cipm_membership": ([c_void_p, P_DBL, P_DBL, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
+                        ctypes.c_int),
+    "cipm_kkt_counters": ([c_void_p, P_I64], ctypes.c_int),
     "cipm_launch_count": ([c_void_p, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_kernel_times": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .exceptions import ConicError, PatternMismatch
+from .exceptions import ConicError, DeviceError, PatternMismatch
 from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, unscale_solution, validate,
                     validate_values)
 from .native import P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, require_device
@@ -29,7 +29,9 @@ from .settings import (ALMOST_OPTIMAL_FACTOR, FULL, MIXED, STALL_IMPROVEMENT, ST
 
 @dataclass
 class Residuals:
-    """Unscaled residual summary (reference ipm.py:98-114, norms only)."""
+    """Unscaled residuals, objectives and norms (reference ipm.py:98-114).  The loop
+    only needs the norms (fused device reductions); r_p / r_d are filled by
+    Solver.compute_residuals, which fetches the residual vectors."""
 
     g_p: float
     g_d: float
@@ -38,6 +40,8 @@ class Residuals:
     norm_xbar: float
     norm_sbar: float
     norm_zbar: float
+    r_p: np.ndarray | None = None
+    r_d: np.ndarray | None = None
 
     @property
     def gap(self) -> float:
@@ -98,6 +102,34 @@ class DeviceScaling:
         return h
 
 
+class DeviceKKT:
+    """Counters of the device KKT system (reference KKTSystem, kkt/system.py:78-79,
+    239, 261-262).  num_symbolic counts host symbolic analyses of this Solver (one:
+    update_data reuses it); num_numeric and last_bumped_pivots come from the device."""
+
+    def __init__(self, solver: "Solver"):
+        self._solver = solver
+        self.num_symbolic = 0
+        self.precision = solver.settings.precision
+
+    def _counters(self):
+        out = np.zeros(2, dtype=np.int64)
+        self._solver._ctx.call("cipm_kkt_counters", pi64(out))
+        return out
+
+    @property
+    def num_numeric(self) -> int:
+        return int(self._counters()[0])
+
+    @property
+    def last_bumped_pivots(self) -> int:
+        return int(self._counters()[1])
+
+    @property
+    def dim(self) -> int:
+        return self._solver.n + self._solver.m
+
+
 class Solver:
     """One problem instance: setup once on the host + GPU, solve and re-solve."""
 
@@ -117,6 +149,8 @@ class Solver:
         self.n, self.m = reordered.n, reordered.m
         # ordering (not a reference setting): 3 = auto, see native.SymbolicAnalysis
         self.symbolic = SymbolicAnalysis(reordered.P, reordered.A, self.layout, ordering=ordering, nd_leaf=nd_leaf)
+        self.kkt = DeviceKKT(self)
+        self.kkt.num_symbolic += 1          # the only symbolic analysis of this Solver (system.py:239)
         st = self.settings
         prec = st.precision
         cs = Settings()
@@ -139,7 +173,6 @@ class Solver:
         self._a_src = np.ascontiguousarray(csr_row_gather_src(problem.A, perm), dtype=np.int64)
         self._ctx.call("cipm_ctx_set_reorder", pi64(self._row_perm) or P_I64(), pi64(self._a_src) or P_I64())
         self._upload_values()
-        self.num_symbolic = 1
         self.setup_seconds = time.perf_counter() - t0
         self._sc = np.zeros(64)
         self.last_refine_steps = []
@@ -225,6 +258,34 @@ class Solver:
                          norm_rp=sc[SC["NRM_GZ"]] / tau, norm_rd=sc[SC["NRM_GX"]] / (c * tau),
                          norm_xbar=sc[SC["NRM_XU"]] / tau, norm_sbar=sc[SC["NRM_SU"]] / tau,
                          norm_zbar=sc[SC["NRM_ZU"]] / (c * tau))
+
+    @property
+    def num_symbolic(self) -> int:
+        return self.kkt.num_symbolic
+
+    def compute_residuals(self, state: IterateState | None = None) -> Residuals:
+        """Residuals and objectives of the normalised iterate on the unscaled,
+        reordered data (reference ipm.py:233-251), with the r_p / r_d vectors (rows
+        in the reordered order, as the reference's).  state=None evaluates the
+        device iterate; a given (scaled) state is uploaded into the device iterate
+        first.  Not on the hot path: the loop uses the fused norms only."""
+        ctx = self._ctx
+        if state is not None:
+            ctx.call("cipm_set_iterate", pdbl(state.x), pdbl(state.z), pdbl(state.s),
+                     pdbl(np.array([state.tau, state.kappa, state.mu])))
+        sc = np.zeros(64)
+        ctx.call("cipm_residuals", pdbl(sc))
+        res = self._residuals(sc)
+        if self._equil.d_row is None:
+            d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
+            ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
+            self._equil = Equilibration(d_row, d_col, float(c_obj.value))
+        tau, c = float(sc[SC["TAU"]]), self._equil.c_obj
+        # g_z = s + A x - b tau and g_x = -(P x + A'z + q tau) in the scaled space:
+        # r_p = -g_z / (D_r tau), r_d = -g_x / (D_c c tau)
+        res.r_p = -self._vector("gz") / (self._equil.d_row * tau)
+        res.r_d = -self._vector("gx") / (self._equil.d_col * c * tau)
+        return res
 
     def _ratios(self, r: Residuals):
         return (r.norm_rp / max(1.0, self._norm_b + r.norm_xbar + r.norm_sbar),
@@ -348,6 +409,8 @@ class Solver:
                     observer(self._observer_doc(it, state_before))
                 ctx.call("cipm_take_step")
                 iterations = it + 1
+        except DeviceError:
+            raise                    # CUDA / ABI faults are infrastructure errors, not a solver status
         except (ConicError, np.linalg.LinAlgError) as err:
             if cfg.verbose:
                 print(f"numerical error: {err}")

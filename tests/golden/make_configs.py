@@ -1,7 +1,8 @@
 """Config-shape golden results from the UNMODIFIED reference solver.
 
-The BASELINE configs at reduced scale (the full C2-C5a sizes take the
-reference's Python setup minutes to hours): status, iterations, objectives and
+The BASELINE configs at full size (C1, C2, C3, C5a) and reduced scale (C2,
+C3, C5a at 1/10; C4 at 1/5 -- its full size takes the reference's Python setup
+hours): status, iterations, objectives and
 final residual norms of ``conic_ipm.solve`` on the same seeded generator
 instances the bench uses.  Run in the build container (``/root/reference`` is
 not on the GPU box):
@@ -27,6 +28,12 @@ CASES = {
     "c3_socp_tenth": ("socp", dict(ncones=10_000), "full"),
     "c4_exppow_fifth": ("exppow", dict(n_exp=10_000, n_pow=4_000), "full"),
     "c5a_psd_tenth": ("psd", dict(ncones=1_000, side=6), "full"),
+    # the BASELINE sizes themselves (reference setup + solve: minutes each); C4 at
+    # full size is not here: the reference's pure-Python minimum degree on its
+    # 415k-row KKT pattern runs for hours
+    "c2_lasso_full": ("lasso", dict(nf=50_000, mr=200_000), "mixed"),
+    "c3_socp_full": ("socp", dict(ncones=100_000), "full"),
+    "c5a_psd_full": ("psd", dict(ncones=10_000, side=6), "full"),
 }
 
 

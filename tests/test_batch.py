@@ -107,3 +107,92 @@ def test_gpu_batch_infeasible_instances(gpu):
             assert abs(r.iterations - doc["result"]["iterations"]) <= 1
             if doc["result"]["certificate"] is not None:
                 np.testing.assert_allclose(r.certificate, doc["result"]["certificate"], atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_gpu_batch_partial_updates_match_fresh(gpu):
+    """update_data(b=) alone, then q and b together, then after a host-equilibrated
+    upload: each equals a fresh BatchSolver on the same data bit for bit."""
+    from paper_2412_19027_b200.batch import BatchSolver
+    base = G.gen_mpc(seed=5)
+    probs = [G.gen_mpc(seed=5 + k) for k in range(6)]
+    cfg = SolverSettings(eps_feas=1e-8)
+    rng = np.random.default_rng(1)
+    bs = BatchSolver(probs, cfg)
+    bs.solve()
+
+    def fresh(qs, bsv):
+        ps = []
+        for k, p in enumerate(probs):
+            c = p.copy()
+            c.q, c.b = qs[k].copy(), bsv[k].copy()
+            ps.append(c)
+        f = BatchSolver(ps, cfg)
+        out = f.solve()
+        f.close()
+        return out
+
+    def same(a, b):
+        for ra, rb in zip(a, b):
+            assert ra.status == rb.status and ra.iterations == rb.iterations
+            np.testing.assert_array_equal(ra.x, rb.x)
+            np.testing.assert_array_equal(ra.z, rb.z)
+
+    q0 = np.stack([p.q for p in probs])
+    b1 = np.stack([p.b for p in probs]) * (1.0 + 0.05 * rng.standard_normal((len(probs), base.m)))
+    bs.update_data(b=b1)
+    same(bs.solve(), fresh(q0, b1))
+    q2 = q0 * 1.1
+    b2 = b1 * 0.9
+    bs.update_data(q=q2, b=b2)
+    same(bs.solve(), fresh(q2, b2))
+    bs._upload_host_equilibrated()
+    q3 = q2 * 0.95
+    bs.update_data(q=q3)                 # must re-send raw P / A / b, not reuse the scaled arrays
+    out3 = bs.solve()
+    bs.close()
+    ref3 = fresh(q3, b2)
+    for ra, rb in zip(out3, ref3):
+        assert ra.status == rb.status
+        assert abs(ra.obj_primal - rb.obj_primal) <= 1e-9 * max(1.0, abs(rb.obj_primal))
+
+
+def test_batch_update_rejects_non_finite():
+    """BatchSolver.update_data re-validates like the reference's update_data (problem.py:149-174)."""
+    from paper_2412_19027_b200.batch import BatchSolver
+    from paper_2412_19027_b200.exceptions import NonFiniteData
+    bs = BatchSolver.__new__(BatchSolver)
+    bs.count, bs.n, bs.m = 2, 3, 4
+    q = np.ones((2, 3))
+    q[1, 2] = np.nan
+    with pytest.raises(NonFiniteData):
+        bs.update_data(q=q)
+    b = np.ones((2, 4))
+    b[0, 0] = np.inf
+    with pytest.raises(NonFiniteData):
+        bs.update_data(b=b)
+
+
+@pytest.mark.gpu
+def test_gpu_batch_c5b_all_2048_match_reference(gpu):
+    """The whole C5b batch (2048 MPC QPs, seeds 0..2047) against the unmodified
+    reference's per-instance results (tests/golden/mpc2048.json, written by
+    tests/golden/make_mpc.py): same status, iterations within 1, objectives
+    within 1e-6 relative, for every instance."""
+    import json
+    import os
+    from paper_2412_19027_b200.batch import BatchSolver
+    doc = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mpc2048.json")))
+    probs = G.build_instances("c5b_mpc", 0, len(doc["status"]))
+    bs = BatchSolver(probs, SolverSettings(eps_feas=doc["eps_feas"]))
+    out = bs.solve()
+    bs.close()
+    bad = []
+    for k, r in enumerate(out):
+        ok = (r.status == doc["status"][k] and abs(r.iterations - doc["iterations"][k]) <= 1
+              and abs(r.obj_primal - doc["obj_primal"][k]) <= 1e-6 * max(1.0, abs(doc["obj_primal"][k]))
+              and abs(r.obj_dual - doc["obj_dual"][k]) <= 1e-6 * max(1.0, abs(doc["obj_dual"][k])))
+        if not ok:
+            bad.append((k, r.status, r.iterations, r.obj_primal, doc["status"][k], doc["iterations"][k]))
+    assert not bad, bad[:10]
+    assert sum(r.iterations for r in out) == pytest.approx(sum(doc["iterations"]), abs=len(out) // 100)

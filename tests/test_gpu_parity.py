@@ -69,19 +69,48 @@ def test_gpu_update_data_reuses_symbolic(gpu):
     prob = problem_from_doc(doc)
     cfg = settings_of(doc)
     s = Solver(prob, cfg)
+    handle = s.symbolic.handle.value
+    assert s.kkt.num_symbolic == 1 and s.kkt.num_numeric == 0
     rng = np.random.default_rng(3)
+    factors = 0
     for k in range(3):
         q = prob.q * (1.0 + 0.05 * rng.standard_normal(prob.n))
         s.update_data(q=q)
         r = s.solve()
+        factors += r.iterations          # one numeric factorisation per IPM iteration (ipm.py:441)
+        assert s.kkt.num_numeric == factors
+        assert s.kkt.last_bumped_pivots >= 0
         p2 = prob.copy()
         p2.q = q
         o = OracleSolver(p2, cfg).solve()
         assert r.status == o.status
         assert abs(r.iterations - o.iterations) <= 1
         assert rel(r.obj_primal, o.obj_primal) <= 1e-6
-    assert s.num_symbolic == 1
+    # the symbolic analysis ran once and its handle was never replaced
+    assert s.kkt.num_symbolic == 1 and s.symbolic.handle.value == handle
     s.close()
+
+
+def test_gpu_compute_residuals_vectors(gpu):
+    """Solver.compute_residuals (ipm.py:233-251): r_p = b - A x̄ - s̄ and
+    r_d = P x̄ + A'z̄ + q on the reordered data, consistent with the returned
+    solution and with the fused device norms."""
+    from paper_2412_19027_b200.model import reorder_cones
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance("socp_40")
+    prob = problem_from_doc(doc)
+    s = Solver(prob, settings_of(doc))
+    r = s.solve()
+    res = s.compute_residuals()
+    s.close()
+    rp, _ = reorder_cones(prob)
+    perm = s._perm
+    xb, zb, sb = r.x, r.z[perm], r.s[perm]
+    A, P = rp.A.to_scipy(), rp.P.to_scipy()
+    np.testing.assert_allclose(res.r_p, rp.b - A @ xb - sb, rtol=0, atol=1e-9 * max(1.0, np.abs(rp.b).max()))
+    np.testing.assert_allclose(res.r_d, P @ xb + A.T @ zb + rp.q, rtol=0, atol=1e-9 * max(1.0, np.abs(rp.q).max()))
+    assert np.max(np.abs(res.r_p)) == pytest.approx(res.norm_rp, rel=1e-12, abs=1e-300)
+    assert np.max(np.abs(res.r_d)) == pytest.approx(res.norm_rd, rel=1e-12, abs=1e-300)
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -147,5 +176,5 @@ def test_gpu_partial_updates_match_fresh_solver(gpu):
         f.close()
         assert r.status == rf.status and r.iterations == rf.iterations
         assert r.obj_primal == rf.obj_primal and np.array_equal(r.x, rf.x)
-    assert s.num_symbolic == 1
+    assert s.kkt.num_symbolic == 1
     s.close()

@@ -25,7 +25,7 @@ for k in range(reps):
     import hashlib
     hp = hashlib.md5(s.symbolic.array("perm").tobytes()).hexdigest()[:8]
     he = hashlib.md5(s._equil.d_row.tobytes() + s._equil.d_col.tobytes()).hexdigest()[:8] \
-        if hasattr(s._equil, "d_row") else "?"
+        if s._equil.d_row is not None else "?"
     print(name, k, r1.status, r1.iterations, r1.obj_primal.hex(), "| same solver again:", r2.status, r2.iterations,
           "perm", hp, "equil", he, flush=True)
     s.close()
