@@ -147,6 +147,9 @@ struct Ctx {
     int64_t factor_slice = 0;        // per-warp panel slice (elements) of the factor kernel
     int factor_cta_smem = 0, factor_cta_blocks = 0;   // mid-tier CTA kernel
     int64_t solve_slice = 0;         // per-warp panel slice (elements) of the solve kernels
+    int64_t solve_form_slice = 0;    // per-warp panel slice of the solve-form pass
+    int solve_form_blocks = 1;
+    int solve_form_inv = 0;          // per-warp Linv buffer (max non-tail width squared)
     // dense tail (dense.cu)
     std::vector<TailNode> tail;
     void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)

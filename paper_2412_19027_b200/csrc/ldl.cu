@@ -244,9 +244,7 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
         __syncwarp();
     }
     if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
-    // 3. write the factor back, then push C_J = L_off D L_off' into the ancestors' inboxes
-    if (in_smem)
-        for (int i = lane; i < psize; i += 32) L[i] = P[i];
+    // 3. push C_J = L_off D L_off' into the ancestors' inboxes, then write the factor back
     if (o > 0) {
         int64_t tb = 0;   // packed offset of column bb
         for (int bb = 0; bb < o; ++bb) {
@@ -259,6 +257,9 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
             tb += o - bb;
         }
     }
+    __syncwarp();
+    if (in_smem)
+        for (int i = lane; i < psize; i += 32) L[i] = P[i];
 }
 
 constexpr int FW = 8;   // warps per factor CTA (warp tier)
@@ -304,11 +305,6 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
             for (int i = c; i < 16; ++i) p[c][i] -= p[j][i] * dt * p[j][c];
         p[j][j] = (T)1;
     }
-#pragma unroll
-    for (int j = 0; j < W; ++j)
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (i < r) L[j * r + i] = p[j][i];
     // contribution block: packed column-major lower over the off rows W..r-1
     const int o = r - W;
     int64_t tb = 0;
@@ -325,6 +321,36 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
         }
         tb += o - b;
     }
+    // solve form (see warp_panel_to_solve_form): p[j][i] = M[i][j]
+#pragma unroll
+    for (int j = W - 2; j >= 0; --j)
+#pragma unroll
+        for (int i = W - 1; i > j; --i) {          // descending i: p[j][k], k < i, still hold L
+            T acc = p[j][i];
+#pragma unroll
+            for (int k = j + 1; k < i; ++k) acc += p[k][i] * p[j][k];
+            p[j][i] = -acc;
+        }
+#pragma unroll
+    for (int j = 1; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < j; ++i) p[j][i] = (T)0;
+#pragma unroll
+    for (int i = W; i < 16; ++i) {
+        if (i >= r) break;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            T acc = p[j][i];
+#pragma unroll
+            for (int k = j + 1; k < W; ++k) acc += p[k][i] * p[j][k];
+            p[j][i] = acc;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (i < r) L[j * r + i] = p[j][i];
     if (parent >= 0) atomic_max_pos(a.maxd + parent, runmax);
     return -1;     // tiny leaves are excluded from the child counts (separate launch)
 }
@@ -349,6 +375,7 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
                                                   T* __restrict__ dvec, T* __restrict__ inbox, T* sp, T* sDw,
                                                   int8_t* sSgw, uint64_t* bar, uint32_t& phase) {
     const int lane = threadIdx.x & 31;
+    double carry_max = 0.0;      // the child's runmax when continuing (its atomic max may still be in flight)
     while (J >= 0) {
         if (a.trace && lane == 0) a.trace[6 * J] = a.trace[6 * J + 1] = gtimer();
         const Desc d = load_desc(a.desc32, a.desc64, J);
@@ -358,7 +385,7 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
             needP = a.need[2 * d.parent + 1];
             tierP = a.desc32[(int64_t)d.parent * 8 + 6];
         }
-        double runmax = lane == 0 ? __ldcg(a.maxd + J) : 0.0;
+        double runmax = lane == 0 ? fmax(__ldcg(a.maxd + J), carry_max) : 0.0;
         runmax = __shfl_sync(0xffffffffu, runmax, 0);
         if (lane < w) sSgw[lane] = a.sign[c0 + lane];
         if (lane + 32 < w) sSgw[lane + 32] = a.sign[c0 + lane + 32];
@@ -374,13 +401,14 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
             if (d.parent >= 0) {
                 atomic_max_pos(a.maxd + d.parent, runmax);
                 if (tierP == a.tier) {
-                    const int old = atomic_add_acq_rel(a.count + d.parent, 1);
-                    if (old == needP - 1) cont = d.parent;
+                    if (needP == 1) cont = d.parent;        // sole same-tier child: no counter round trip
+                    else if (atomic_add_acq_rel(a.count + d.parent, 1) == needP - 1) cont = d.parent;
                 }
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
         }
         J = __shfl_sync(0xffffffffu, cont, 0);
+        carry_max = runmax;
         __syncwarp();
     }
 }
@@ -577,7 +605,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sp = reinterpret_cast<T*>(smem_raw);
     __shared__ int s_J, s_needP, s_tierP, s_next;
-    __shared__ double s_runmax;
+    __shared__ double s_runmax, s_carry;
     __shared__ T sD[64];
     __shared__ __align__(16) T sLt[64 * 16];    // L11' of a 16-column block / d_k l_ck of the trailing columns
     __shared__ T sInv[16];
@@ -593,6 +621,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
             if (J < 0) {
                 const int t = atomicAdd(a.ticket, 1);
                 J = t < a.nstart ? a.start[t] : -1;
+                s_carry = 0.0;
             }
             s_J = J;
         }
@@ -603,7 +632,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         else if (tid < 16) s_d64[tid - 8] = a.desc64[(int64_t)J * 8 + tid - 8];
         if (tid == 0) {
             if (a.trace) a.trace[6 * J] = a.trace[6 * J + 1] = gtimer();
-            s_runmax = __ldcg(a.maxd + J);
+            s_runmax = fmax(__ldcg(a.maxd + J), s_carry);
         }
         __syncthreads();
         const int c0 = s_d32[0], w = s_d32[1], r = s_d32[2], parent = s_d32[3];
@@ -644,27 +673,105 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
         else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
         if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
-        // 3. write back, push C_J = L_off D L_off'
-        if (in_smem)
-            for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
+        // 3. push C_J = L_off D L_off', write the factor back
         if (o > 0) {
             if (in_smem) cta_push(sp, r, w, o, s_d64[6], sD, a, inbox);
             else cta_push(L, r, w, o, s_d64[6], sD, a, inbox);
         }
+        if (in_smem)
+            for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
         __syncthreads();
         if (tid == 0) {
             int cont = -1;
             if (parent >= 0) {
                 atomic_max_pos(a.maxd + parent, s_runmax);
                 if (s_tierP == a.tier) {
-                    const int old = atomic_add_acq_rel(a.count + parent, 1);
-                    if (old == s_needP - 1) cont = parent;
+                    if (s_needP == 1) cont = parent;        // sole same-tier child: no counter round trip
+                    else if (atomic_add_acq_rel(a.count + parent, 1) == s_needP - 1) cont = parent;
                 }
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
             s_next = cont;
+            s_carry = s_runmax;
         }
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solve form: after the factorisation, every warp / CTA-tier panel
+// P = [L11; L21] (r x w, column-major, unit lower L11) is rewritten in place as
+// M = [L11^-1; L21 L11^-1] (strict upper triangle of the top block zeroed), so
+// each supernode of the triangular sweeps is one dense GEMV with independent
+// dot products: forward [y_J; push] = M b_J, backward x_J = M' [y_J / D; -x_off]
+// (the same L, D solves as ldl.py:91-104).  One warp per supernode, all
+// supernodes in parallel, off the factorisation's critical path (tiny leaves do
+// the same in registers inside factor_tiny_kernel; the dense tail keeps its own
+// blocked inverses).
+//   (i)  Linv, lanes over columns j (j + 32): x_i = -sum_{k<i} L[i][k] x_k with
+//        x_j = 1 and x_k = 0 for k < j — the same trip count on every lane;
+//   (ii) rows below, lanes over rows: m_i[j] = sum_{k>=j} l_i[k] Linv[k][j],
+//        j ascending, in place.
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void solve_form_body(T* P, int r, int w, T* inv) {
+    const int lane = threadIdx.x & 31;
+    // (i) Linv row-major in inv[i * w + j] (lane j writes column j: conflict-free)
+    for (int i = 0; i < w; ++i) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            if (j < w) {
+                T acc = (T)0;
+                for (int k = j; k < i; ++k) acc += P[(int64_t)k * r + i] * inv[k * w + j];
+                inv[i * w + j] = i == j ? (T)1 : (i < j ? (T)0 : -acc);
+            }
+        }
+        __syncwarp();
+    }
+    // (ii) rows below
+    for (int i = w + lane; i < r; i += 32)
+        for (int j = 0; j < w; ++j) {
+            T acc = P[(int64_t)j * r + i];
+#pragma unroll 4
+            for (int k = j + 1; k < w; ++k) acc += P[(int64_t)k * r + i] * inv[k * w + j];
+            P[(int64_t)j * r + i] = acc;
+        }
+    // top block <- Linv (column-major, zeros above the diagonal)
+    for (int e = lane; e < w * w; e += 32) {
+        const int j = e / w, i = e - j * w;
+        P[(int64_t)j * r + i] = inv[i * w + j];
+    }
+    __syncwarp();
+}
+
+constexpr int SFW = 4;   // warps per solve-form CTA
+
+template <typename T>
+__global__ void __launch_bounds__(SFW * 32) solve_form_kernel(const int32_t* __restrict__ list, int32_t n,
+                                                              const int32_t* __restrict__ d32,
+                                                              const int64_t* __restrict__ d64, T* lval, int slice,
+                                                              int inv_cap) {
+    extern __shared__ __align__(16) unsigned char sraw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T* inv = reinterpret_cast<T*>(sraw) + (int64_t)wid * (inv_cap + slice);
+    T* sp = inv + inv_cap;
+    for (int64_t t = blockIdx.x * (int64_t)SFW + wid; t < n; t += (int64_t)gridDim.x * SFW) {
+        const int J = list[t];
+        const int w = __ldg(d32 + (int64_t)J * 8 + 1), r = __ldg(d32 + (int64_t)J * 8 + 2);
+        T* L = lval + __ldg(d64 + (int64_t)J * 8);
+        const int psize = r * w;
+        if (w < 1) continue;
+        if (psize <= slice) {
+            for (int e = lane; e < psize; e += 32) sp[e] = L[e];
+            __syncwarp();
+            solve_form_body(sp, r, w, inv);
+            for (int e = lane; e < psize; e += 32) L[e] = sp[e];
+        } else {
+            solve_form_body(L, r, w, inv);
+        }
+        __syncwarp();
     }
 }
 
@@ -747,48 +854,44 @@ __device__ __forceinline__ void vgather_q(T* const (&vq)[NQ], const uint8_t* __r
     __syncwarp();
 }
 
-// forward task, compute part: triangle and off-row push for NQ right-hand sides
-// together (each L element is read once for all of them).  Forced inline so L
-// keeps its address space (staged panel -> LDS).
+// forward task, compute part, for NQ right-hand sides together: the panel is in
+// solve form (M = [L11^-1; L21 L11^-1]), so y_J = M_top b_J and the off-row push
+// M_off b_J are one GEMV with independent row dot products (lanes over rows; b_J
+// broadcast from shared memory).  Forced inline so L keeps its address space
+// (staged panel -> LDS).
 template <typename T, int NQ>
 __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* const (&xq)[NQ],
                                             T* const (&vq)[NQ], const T (&xa)[NQ], const T (&xb)[NQ],
                                             T (*cs)[64], int J, const int64_t (&pos_pf)[2]) {
     const int lane = threadIdx.x & 31;
     const int c0 = d.c0, w = d.w, r = d.r;
-    T x0[NQ], x1[NQ];
+    // b_J = own values - inbox sums, into the shared column buffer
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        x0[q] = lane < w ? xa[q] - cs[q][lane] : (T)0;
-        x1[q] = lane + 32 < w ? xb[q] - cs[q][lane + 32] : (T)0;
+        if (lane < w) cs[q][lane] = xa[q] - cs[q][lane];
+        if (lane + 32 < w) cs[q][lane + 32] = xb[q] - cs[q][lane + 32];
     }
-    constexpr int KB = 8 / NQ;                  // columns whose loads are issued together
-    for (int j0 = 0; j0 < w; j0 += KB) {
-        T l0[KB], l1[KB];
+    __syncwarp();
+    // top rows: y_J (M_top is unit lower: the diagonal term is b_i itself)
+    for (int i0 = 0; i0 < w; i0 += 32) {
+        const int i = i0 + lane;
+        const int ii = i < w ? i : w - 1;
+        T acc[NQ];
 #pragma unroll
-        for (int k = 0; k < KB; ++k) {          // issue the block's loads before the dependent chain
-            const int j = j0 + k;
-            l0[k] = (j < w && lane > j && lane < w) ? L[j * r + lane] : (T)0;
-            l1[k] = (j < w && lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
+        for (int q = 0; q < NQ; ++q) acc[q] = cs[q][ii];
+#pragma unroll 8
+        for (int k = 0; k < ii; ++k) {
+            const T mk = L[k * r + ii];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[q] += mk * cs[q][k];
         }
+        if (i < w) {
 #pragma unroll
-        for (int k = 0; k < KB; ++k) {
-            const int j = j0 + k;
-            if (j >= w) break;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
-                x0[q] -= l0[k] * xj;
-                x1[q] -= l1[k] * xj;
-            }
+            for (int q = 0; q < NQ; ++q) xq[q][c0 + i] = acc[q];
         }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        if (lane < w) xq[q][c0 + lane] = x0[q];
-        if (lane + 32 < w) xq[q][c0 + lane + 32] = x1[q];
     }
     if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
+    // off rows: push M_off b_J into the ancestors' vector inboxes
     for (int i0 = w; i0 < r; i0 += 32) {
         const int i = i0 + lane;
         const bool ok = i < r;
@@ -800,9 +903,9 @@ __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, cons
         for (int q = 0; q < NQ; ++q) acc[q] = (T)0;
 #pragma unroll 8
         for (int k = 0; k < w; ++k) {
-            const T lk = L[k * r + ii];
+            const T mk = L[k * r + ii];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) acc[q] += lk * __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+            for (int q = 0; q < NQ; ++q) acc[q] += mk * cs[q][k];
         }
         if (ok) {
 #pragma unroll
@@ -812,9 +915,11 @@ __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, cons
     if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
 }
 
-// backward task body for NQ right-hand sides: own values (xa/xb, loaded before
-// the parent wait) D-solved, the ancestors' values at the off rows gathered for
-// every RHS in one round trip (64 rows at a time), then the transposed triangle.
+// backward task body for NQ right-hand sides, panel in solve form:
+// x_J = M' v with v = [y_J / D; -x_off] — lane j owns columns j and j + 32 and
+// accumulates independent products over the rows (no dependent chain).  Own
+// values (xa / xb) were loaded before the parent wait; the ancestors' values at
+// the off rows are gathered for every RHS in one round trip (64 rows at a time).
 template <typename T, int NQ>
 __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
                                          const int32_t* rowsJ, T* const (&xq)[NQ], T (*xo)[64],
@@ -825,11 +930,33 @@ __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0,
     const T* L1 = L + (lane + 32) * r;
     const bool o0 = lane < w, o1 = lane + 32 < w;
     T x0[NQ], x1[NQ];
+    // top rows: v = y_J / D (ldl.py:101-102) through the shared buffer; M_top' is unit upper
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        x0[q] = o0 ? xa[q] / d_pf[0] : (T)0;      // D solve (ldl.py:101-102)
-        x1[q] = o1 ? xb[q] / d_pf[1] : (T)0;
+        const T v0 = o0 ? xa[q] / d_pf[0] : (T)0;
+        const T v1 = o1 ? xb[q] / d_pf[1] : (T)0;
+        x0[q] = v0;
+        x1[q] = v1;
+        xo[q][lane] = v0;
+        xo[q][lane + 32] = v1;
     }
+    __syncwarp();
+    {
+        const int j0 = o0 ? lane : w, j1 = o1 ? lane + 32 : w;
+#pragma unroll 4
+        for (int i = j0 + 1; i < w; ++i) {
+            const T m = L0[i];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) x0[q] += m * xo[q][i];
+        }
+#pragma unroll 4
+        for (int i = j1 + 1; i < w; ++i) {
+            const T m = L1[i];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) x1[q] += m * xo[q][i];
+        }
+    }
+    __syncwarp();
     for (int i0 = 0; i0 < o; i0 += 64) {
         const int n = min(64, o - i0);
         const int ra = i0 == 0 ? rows_pf[0] : (lane < n ? rowsJ[i0 + lane] : 0);
@@ -858,27 +985,6 @@ __device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0,
             }
         }
         __syncwarp();
-    }
-    constexpr int KB = 8 / NQ;
-    for (int j1 = w - 1; j1 >= 0; j1 -= KB) {
-        T l0[KB], l1[KB];
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {          // loads first, then the dependent chain
-            const int j = j1 - k;
-            l0[k] = (j >= 0 && lane < j) ? L0[j] : (T)0;
-            l1[k] = (j >= 0 && lane + 32 < j) ? L1[j] : (T)0;
-        }
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {
-            const int j = j1 - k;
-            if (j < 0) break;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
-                x0[q] -= l0[k] * xj;
-                x1[q] -= l1[k] * xj;
-            }
-        }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -909,22 +1015,24 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xJ = x + (int64_t)q * a.dim + c0;
-        T xv[W];
+        T bv[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) xv[j] = xJ[j];
+        for (int j = 0; j < W; ++j) bv[j] = xJ[j];
+        // solve form: [y_J; push] = M b_J (p[k][i] = M[i][k], M_top = L11^-1 unit lower)
 #pragma unroll
-        for (int j = 0; j < W; ++j)
+        for (int i = 0; i < W; ++i) {
+            T acc = bv[i];
 #pragma unroll
-            for (int i = j + 1; i < W; ++i) xv[i] -= p[j][i] * xv[j];
-#pragma unroll
-        for (int j = 0; j < W; ++j) xJ[j] = xv[j];
+            for (int k = 0; k < i; ++k) acc += p[k][i] * bv[k];
+            xJ[i] = acc;
+        }
         T* vq = vin + (int64_t)q * a.nv;
 #pragma unroll
         for (int i = W; i < 16; ++i) {
             if (i >= r) break;
             T acc = (T)0;
 #pragma unroll
-            for (int k = 0; k < W; ++k) acc += p[k][i] * xv[k];
+            for (int k = 0; k < W; ++k) acc += p[k][i] * bv[k];
             vq[a.vpush_pos[cvo + i - W]] = acc;
         }
     }
@@ -995,8 +1103,11 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         int cont = -1;
         if (lane == 0) {
             if (d.parent >= 0) {
-                const int old = atomic_add_acq_rel(a.count + d.parent, 1);
-                if (old == needP - 1) cont = d.parent;
+                // a sole (non-tiny) child continues without the counter round trip: this
+                // warp's writes are ordered before its own later reads, and before other
+                // tasks' reads by the release of the chain's next counted increment
+                if (needP == 1) cont = d.parent;
+                else if (atomic_add_acq_rel(a.count + d.parent, 1) == needP - 1) cont = d.parent;
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
         }
@@ -1119,9 +1230,17 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xv = x + (int64_t)q * a.dim;
-        T xr[W];
+        T vt[W], xr[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) xr[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
+        for (int j = 0; j < W; ++j) vt[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
+        // solve form: x_J = M_top' (y_J / D) - M_off' x_off
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            T acc = vt[j];
+#pragma unroll
+            for (int i = j + 1; i < W; ++i) acc += p[j][i] * vt[i];
+            xr[j] = acc;
+        }
 #pragma unroll
         for (int i = W; i < 16; ++i) {
             if (i >= r) break;
@@ -1129,10 +1248,6 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
 #pragma unroll
             for (int j = 0; j < W; ++j) xr[j] -= p[j][i] * xi;
         }
-#pragma unroll
-        for (int j = W - 1; j >= 0; --j)
-#pragma unroll
-            for (int i = j + 1; i < W; ++i) xr[j] -= p[j][i] * xr[i];
 #pragma unroll
         for (int j = 0; j < W; ++j) xv[c0 + j] = xr[j];
     }
@@ -1341,6 +1456,15 @@ int factor_t(Ctx& c) {
         c.launches++;
     }
     k_tail_factor(c);
+    const int nsf = (int)c.host_sym.bwd_order.size();
+    if (nsf > 0) {
+        const int slice = (int)c.solve_form_slice;
+        const size_t smem = sizeof(T) * (size_t)(c.solve_form_inv + slice) * SFW;
+        solve_form_kernel<T><<<c.solve_form_blocks, SFW * 32, smem, c.stream>>>(c.sym.bwd_order, nsf, c.sym.desc32,
+                                                                                c.sym.desc64, (T*)c.lval, slice,
+                                                                                c.solve_form_inv);
+        c.launches++;
+    }
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
         c.ev_factor.emplace_back(e0, e0 + 1);
@@ -1516,9 +1640,9 @@ int factor_grid(Ctx& c) {
 }
 
 int solve_grid(Ctx& c) {
-    // per-warp panel slice: 6 KiB (four 8-warp CTAs per SM); larger panels are read from L2/HBM
+    // per-warp panel slice: up to 8 KiB (three 8-warp CTAs per SM); larger panels are read from L2/HBM
     const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
-    c.solve_slice = std::max<int64_t>(64, std::min<int64_t>((c.host_sym.max_panel_main + 3) & ~int64_t(3), 6144 / es));
+    c.solve_slice = std::max<int64_t>(64, std::min<int64_t>((c.host_sym.max_panel_main + 3) & ~int64_t(3), 8192 / es));
     if (const char* e = getenv("CIPM_SOLVE_SLICE")) c.solve_slice = std::max<int64_t>(4, atoll(e) & ~int64_t(3));   // experiments
     const int ssm = (int)(es * c.solve_slice * SW);
     int per = 0, per2 = 0;
@@ -1535,6 +1659,27 @@ int solve_grid(Ctx& c) {
     }
     per = std::min(per, per2);
     if (per < 1) per = 1;
+    {
+        // solve-form pass: one warp per supernode, Linv (64 x 64) + a panel slice of up to 16 KiB per warp
+        c.solve_form_slice = std::max<int64_t>(64, std::min<int64_t>((c.host_sym.max_panel_main + 3) & ~int64_t(3),
+                                                                     16384 / es));
+        int64_t maxw = 1;
+        for (int32_t J : c.host_sym.bwd_order)
+            maxw = std::max<int64_t>(maxw, c.host_sym.sn_col[J + 1] - c.host_sym.sn_col[J]);
+        c.solve_form_inv = (int)((maxw * maxw + 3) & ~int64_t(3));
+        const int sfm = (int)(es * (c.solve_form_inv + c.solve_form_slice) * SFW);
+        int pf = 0;
+        if (c.precision == CIPM_FULL) {
+            cudaFuncSetAttribute(solve_form_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, solve_form_kernel<double>, SFW * 32, sfm);
+        } else {
+            cudaFuncSetAttribute(solve_form_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sfm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, solve_form_kernel<float>, SFW * 32, sfm);
+        }
+        if (pf < 1) pf = 1;
+        const int64_t nsf = (int64_t)c.host_sym.bwd_order.size();
+        c.solve_form_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * pf, (nsf + SFW - 1) / SFW));
+    }
     int64_t g = (int64_t)sm_count() * per;
     int64_t need = (c.host_sym.n_main + SW - 1) / SW;
     if (g > need) g = need;
