@@ -570,6 +570,8 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         c.tinv = p;
         TRY(dalloc(c, &c.tflags, flag_total));
     }
+    TRY(dalloc(c, &c.sf_flag, S.nsuper));    // zero: tiny leaves / tail never use the solve form
+    if (const char* e = getenv("CIPM_SF_TAU")) c.sf_tau = atof(e);
     TRY(dalloc(c, &c.fac_count, S.nsuper));
     TRY(dalloc(c, &c.bwd_done, S.nsuper));
     TRY(dalloc(c, &c.tickets, 8));

@@ -206,6 +206,18 @@ struct FactorArgs {
 };
 
 
+// packed column-major lower index e of an o x o block -> (column bb, row aa >= bb);
+// column bb starts at tb(bb) = bb*o - bb*(bb-1)/2
+__device__ __forceinline__ void unpack_lower(int e, int o, int& bb, int& aa) {
+    const double t = 2.0 * o + 1.0;
+    int b = (int)((t - sqrt(t * t - 8.0 * (double)e)) * 0.5);
+    b = max(0, min(b, o - 1));
+    while (b > 0 && b * o - b * (b - 1) / 2 > e) --b;
+    while (b + 1 < o && (b + 1) * o - (b + 1) * b / 2 <= e) ++b;
+    bb = b;
+    aa = b + (e - (b * o - b * (b - 1) / 2));
+}
+
 // warp-tier task body: gather, panel LDL', write-back, contribution push.
 // Forced inline so P keeps its address space at each call site.
 template <typename T>
@@ -218,6 +230,7 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
     warp_gather_sub(P, a.inbox_tgt, inbox, d.ilo, d.ihi);
     if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
     // 2. dense LDL' of the panel (right-looking, lanes over rows)
+    int nbump = 0;
     for (int j = 0; j < w; ++j) {
         T* Pj = P + j * r;
         double dd = (double)Pj[j];
@@ -227,8 +240,8 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
         const T dt = (T)dd;
         runmax = fmax(runmax, fabs(dd));
         __syncwarp();
+        nbump += bump ? 1 : 0;
         if (lane == 0) {
-            if (bump) atomicAdd(a.bumps, 1);
             if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
             dvec[c0 + j] = dt;
             sDw[j] = dt;
@@ -243,23 +256,26 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
         }
         __syncwarp();
     }
+    if (lane == 0 && nbump) atomicAdd(a.bumps, nbump);
     if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
     // 3. push C_J = L_off D L_off' into the ancestors' inboxes, then write the factor back
     if (o > 0) {
-        int64_t tb = 0;   // packed offset of column bb
-        for (int bb = 0; bb < o; ++bb) {
-            const T* Pb = P + w + bb;
-            for (int aa = bb + lane; aa < o; aa += 32) {
-                T acc = (T)0;
-                for (int k = 0; k < w; ++k) acc += P[k * r + w + aa] * sDw[k] * Pb[k * r];
-                inbox[a.push_pos[d.cb + tb + (aa - bb)]] = acc;
-            }
-            tb += o - bb;
+        // C_J entries flattened over the lanes (packed column-major lower), push
+        // positions loaded coalesced
+        const int ne = o * (o + 1) / 2;
+        for (int e = lane; e < ne; e += 32) {
+            const int64_t pos = __ldg(a.push_pos + d.cb + e);
+            int bb, aa;
+            unpack_lower(e, o, bb, aa);
+            T acc = (T)0;
+            for (int k = 0; k < w; ++k) acc += P[k * r + w + aa] * (sDw[k] * P[k * r + w + bb]);
+            inbox[pos] = acc;
         }
     }
     __syncwarp();
-    if (in_smem)
-        for (int i = lane; i < psize; i += 32) L[i] = P[i];
+    (void)in_smem;
+    (void)psize;
+    (void)L;
 }
 
 constexpr int FW = 8;   // warps per factor CTA (warp tier)
@@ -320,31 +336,6 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
             inbox[a.push_pos[cb + tb + (aa - b)]] = acc;
         }
         tb += o - b;
-    }
-    // solve form (see warp_panel_to_solve_form): p[j][i] = M[i][j]
-#pragma unroll
-    for (int j = W - 2; j >= 0; --j)
-#pragma unroll
-        for (int i = W - 1; i > j; --i) {          // descending i: p[j][k], k < i, still hold L
-            T acc = p[j][i];
-#pragma unroll
-            for (int k = j + 1; k < i; ++k) acc += p[k][i] * p[j][k];
-            p[j][i] = -acc;
-        }
-#pragma unroll
-    for (int j = 1; j < W; ++j)
-#pragma unroll
-        for (int i = 0; i < j; ++i) p[j][i] = (T)0;
-#pragma unroll
-    for (int i = W; i < 16; ++i) {
-        if (i >= r) break;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            T acc = p[j][i];
-#pragma unroll
-            for (int k = j + 1; k < W; ++k) acc += p[k][i] * p[j][k];
-            p[j][i] = acc;
-        }
     }
 #pragma unroll
     for (int j = 0; j < W; ++j)
@@ -407,6 +398,9 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
             }
             if (a.trace) a.trace[6 * J + 5] = gtimer();
         }
+        // the factor is written back after the signal (the ancestors only read the inbox)
+        if (P != L)
+            for (int i = lane; i < psize; i += 32) L[i] = sp[i];
         J = __shfl_sync(0xffffffffu, cont, 0);
         carry_max = runmax;
         __syncwarp();
@@ -446,153 +440,143 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
     }
 }
 
-// CTA-tier dense panel LDL' (see factor_cta_kernel); forced inline so the
-// panel pointer keeps its address space (shared -> LDS/STS) at each call site
-//
-// Blocked by 32 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
-// diagonal block with lane i holding row i in registers (warp-synchronous
-// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
-// per row below holds its nbk entries in registers and applies the same
-// right-looking elimination against L11 (broadcast shared-memory reads);
-// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
-// instead of one per column.
+// CTA-tier dense panel LDL' (replaces the column loop of ldl.py:62-88 for one
+// supernode): right-looking on the UNSCALED columns, one row per thread (rows
+// tid, tid + nthr, ...), the j loop kept rolled so the code stays a few hundred
+// instructions — the unrolled register / blocked variants were several hundred
+// KiB of SASS, and instruction-cache misses made every pivot step ~0.4 us on the
+// C2 critical path.  Step j: every participating thread reads the final pivot
+// a_jj, applies the dynamic regularisation (ldl.py:79-87) redundantly, and
+// updates its own rows a_ic -= a_ij a_cj / d_j for j < c <= i (a_cj is read
+// unscaled: its owner does not touch column j during the step); one named
+// barrier per step.  Columns are scaled by 1 / d_j in a final pass.
+// Narrow panels (w <= NB, r <= 64): the same right-looking elimination with each
+// thread's row in registers, one row per thread (warp 0 rows 0..31, warp 1 rows
+// 32..63), the j loop rolled and the row ROTATED one column per step so every
+// register index is static (current column = x[0]).  Per step warp 0, which
+// holds the pivot row, publishes 1/d_j and the scaled column l_cj (rows c < w)
+// in a double-buffered shared array; one 64-thread named barrier; every row
+// applies a_ic -= a_ij l_cj.  ~1/3 of the per-step latency of the shared-memory
+// read-modify-write loop, and a compact body (instruction-cache resident).
 template <typename T, int NB>
-__device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, const int8_t* sSg, T* sD,
-                                               double& s_runmax, const FactorArgs& a, T* sLt, T* sInv) {
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void rot_panel_ldl(T* P, int r, int w, const int8_t* sSg, T* sD, double& s_runmax,
+                                              const FactorArgs& a, T (*scol)[2 * NB + 1]) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool two = r > 32;
+    const bool have = tid < r;
     double runmax = s_runmax;
+    int nbump = 0;
     T x[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c)
-        x[c] = (lane < nbk && c < nbk && c <= lane) ? Pk[c * r + k0 + lane] : (T)0;
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-        if (j < nbk) {
-            double dd = (double)__shfl_sync(0xffffffffu, x[j], j);
+    for (int c = 0; c < NB; ++c) x[c] = (c < w && have) ? P[c * r + tid] : (T)0;
+    if (tid < 2 * NB + 1) { scol[0][tid] = (T)0; scol[1][tid] = (T)0; }   // columns >= w read as 0
+    if (two) asm volatile("bar.sync 1, 64;" ::: "memory");
+    else __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < w; ++j) {
+        T* col = scol[j & 1];
+        if (tid < 32) {
+            double dd = (double)__shfl_sync(0xffffffffu, x[0], j);
             const double bound = a.delta_s + a.delta_d * runmax;
             const bool bump = fabs(dd) < bound;
-            if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
+            if (bump) dd = sSg[j] > 0 ? bound : -bound;
+            const T dt = (T)dd;
+            runmax = fmax(runmax, fabs(dd));
+            nbump += bump ? 1 : 0;
+            const T inv = (T)1 / dt;
+            if (lane == 0) {
+                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
+                sD[j] = dt;
+                col[2 * NB] = inv;
+            }
+            // l_cj of rows c in (j, w) at col[c - j]; col[0] unused; stale entries of
+            // step j - 2 beyond w - j zeroed (disjoint from the writes above)
+            if (lane > j && lane < w) col[lane - j] = x[0] * inv;
+            if (lane >= w - j && lane < NB) col[lane] = (T)0;
+        }
+        if (two) asm volatile("bar.sync 1, 64;" ::: "memory");
+        else __syncwarp();
+        const T inv = col[2 * NB];
+        const T aij = x[0];
+        if (have && tid >= j) P[j * r + tid] = tid > j ? aij * inv : (T)1;
+#pragma unroll
+        for (int c = 1; c < NB; ++c) x[c - 1] = x[c] - aij * col[c];
+        x[NB - 1] = (T)0;
+    }
+    if (tid == 0) {
+        s_runmax = runmax;
+        if (nbump) atomicAdd(a.bumps, nbump);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
+                                              const FactorArgs& a, T* __restrict__ dvec) {
+    const int tid = threadIdx.x;
+    const int nthr = min((int)blockDim.x, (r + 31) & ~31);
+    if (tid < nthr) {
+        double runmax = s_runmax;
+        int nbump = 0;
+        for (int j = 0; j < w; ++j) {
+            T* Pj = P + (int64_t)j * r;
+            double dd = (double)Pj[j];
+            const double bound = a.delta_s + a.delta_d * runmax;
+            const bool bump = fabs(dd) < bound;
+            if (bump) dd = sSg[j] > 0 ? bound : -bound;
             const T dt = (T)dd;
             runmax = fmax(runmax, fabs(dd));
             const T inv = (T)1 / dt;
-            if (lane == 0) {
-                if (bump) atomicAdd(a.bumps, 1);
+            nbump += bump ? 1 : 0;
+            if (tid == 0) {
                 if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                sD[k0 + j] = dt;
-                sInv[j] = inv;
+                sD[j] = dt;
             }
-            const T xj = x[j];                   // unscaled a_ij (lanes i > j)
-#pragma unroll
-            for (int c = j + 1; c < NB; ++c) {
-                const T acj = __shfl_sync(0xffffffffu, xj, c);   // unscaled a_cj
-                if (lane >= c) x[c] -= xj * (acj * inv);
+            for (int i = j + 1 + tid; i < r; i += nthr) {
+                const T aij = Pj[i] * inv;
+                const int cend = min(i, w - 1);
+#pragma unroll 4
+                for (int c = j + 1; c <= cend; ++c) P[(int64_t)c * r + i] -= aij * Pj[c];
             }
-            x[j] = lane > j ? xj * inv : (lane == j ? (T)1 : x[j]);
-        } else if (lane == 0) {
-            sInv[j] = (T)0;
+            if (nthr > 32) asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+            else __syncwarp();
+        }
+        if (tid == 0) {
+            s_runmax = runmax;
+            if (nbump) atomicAdd(a.bumps, nbump);
         }
     }
-    int row = k0 + lane;
-    asm volatile("" : "+r"(row));            // recompute the store addresses (no 32 live pointers)
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-        if (lane < nbk && c < nbk && c <= lane) Pk[c * r + row] = x[c];
-        if (lane < NB) sLt[c * NB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;   // Lt[j][i] = l_ij
-    }
-    if (lane == 0) s_runmax = runmax;
-}
-
-template <typename T, int NB>
-__device__ __forceinline__ void cta_below_rows(T* Pk, int r, int i0, int nbk, const T* sLt, const T* sInv) {
-#pragma unroll 1
-    for (int i = i0 + threadIdx.x; i < r; i += blockDim.x) {
-        T x[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) x[c] = c < nbk ? Pk[c * r + i] : (T)0;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-            const T xj = x[j];
-#pragma unroll
-            for (int c = j + 1; c < NB; ++c) x[c] -= xj * sLt[j * NB + c];
-            x[j] = xj * sInv[j];
-            asm volatile("" ::: "memory");      // L11 row loads per step (register budget)
-        }
-        int is = i;
-        asm volatile("" : "+r"(is));         // recompute the store addresses (no 32 live pointers)
-#pragma unroll
-        for (int c = 0; c < NB; ++c)
-            if (c < nbk) Pk[c * r + is] = x[c];
-    }
-}
-
-//
-// Blocked by 16 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
-// diagonal block with lane i holding row i in registers (warp-synchronous
-// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
-// per row below holds its nbk entries in registers and applies the same
-// right-looking elimination against L11 (broadcast shared-memory reads);
-// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
-// instead of one per column.
-template <typename T>
-__device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
-                                              const FactorArgs& a, T* __restrict__ dvec, T* sLt, T* sInv) {
-    // block width 16: a row of the block in registers, 2 CTAs / SM without spills
-    constexpr int KB = 16;
-    const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
-    for (int k0 = 0; k0 < w; k0 += KB) {
-        const int nbk = min(KB, w - k0);
-        T* Pk = P + k0 * r;               // column k0 of the panel
-        if (wid == 0) {
-            if (nbk <= 8) cta_diag_block<T, 8>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
-            else cta_diag_block<T, KB>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
-        }
-        __syncthreads();
-        // (b) rows below the diagonal block
-        if (nbk <= 8) cta_below_rows<T, 8>(Pk, r, k0 + nbk, nbk, sLt, sInv);
-        else cta_below_rows<T, KB>(Pk, r, k0 + nbk, nbk, sLt, sInv);
-        __syncthreads();
-        // (c) trailing columns c >= k0 + nbk, rows i >= c: A(i,c) -= sum_k l_ik d_k l_ck
-        //     (only reached with a full block, nbk == KB)
-        const int c1 = k0 + nbk;
-        if (c1 < w) {
-            // d_k l_ck for the trailing columns, into the (now free) L11' buffer
-            for (int idx = tid; idx < (w - c1) * KB; idx += blockDim.x) {
-                const int cc = idx / KB, k = idx - cc * KB;
-                sLt[idx] = sD[k0 + k] * Pk[k * r + c1 + cc];
-            }
-            __syncthreads();
-            for (int c = c1 + wid; c < w; c += nw) {
-                const T* dl = sLt + (c - c1) * KB;
-                T* Pc = P + c * r;
-#pragma unroll 1
-                for (int i = c + (tid & 31); i < r; i += 32) {
-                    T acc = (T)0;
-#pragma unroll 8
-                    for (int k = 0; k < KB; ++k) acc += Pk[k * r + i] * dl[k];
-                    Pc[i] -= acc;
-                }
-            }
-            __syncthreads();
-        }
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        T* Pj = P + (int64_t)j * r;
+        const T inv = (T)1 / sD[j];
+        for (int i = j + 1 + tid; i < r; i += blockDim.x) Pj[i] = Pj[i] * inv;
+        if (tid == 0) Pj[j] = (T)1;
     }
     for (int j = tid; j < w; j += blockDim.x) dvec[c0 + j] = sD[j];
+    __syncthreads();
 }
 
-
-// CTA-tier contribution block C = L_off D L_off' scattered to the ancestors' inboxes
+// CTA-tier contribution block C = L_off D L_off' scattered to the ancestors'
+// inboxes: entries (packed column-major lower) flattened over all threads, push
+// positions loaded coalesced
 template <typename T>
 __device__ __forceinline__ void cta_push(const T* P, int r, int w, int o, int64_t base, const T* sD,
                                          const FactorArgs& a, T* __restrict__ inbox) {
-    const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
-    for (int bb = wid; bb < o; bb += nw) {
-        const int64_t tb = (int64_t)bb * o - (int64_t)bb * (bb - 1) / 2;
+    const int ne = o * (o + 1) / 2;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        const int64_t pos = __ldg(a.push_pos + base + e);
+        int bb, aa;
+        unpack_lower(e, o, bb, aa);
+        const T* Pa = P + w + aa;
         const T* Pb = P + w + bb;
-        for (int aa = bb + (tid & 31); aa < o; aa += 32) {
-            T acc = (T)0;
-#pragma unroll 4
-            for (int k = 0; k < w; ++k) acc += P[(int64_t)k * r + w + aa] * sD[k] * Pb[(int64_t)k * r];
-            inbox[a.push_pos[base + tb + (aa - bb)]] = acc;
+        T acc0 = (T)0, acc1 = (T)0;
+        int k = 0;
+        for (; k + 1 < w; k += 2) {
+            acc0 += Pa[(int64_t)k * r] * (sD[k] * Pb[(int64_t)k * r]);
+            acc1 += Pa[(int64_t)(k + 1) * r] * (sD[k + 1] * Pb[(int64_t)(k + 1) * r]);
         }
+        if (k < w) acc0 += Pa[(int64_t)k * r] * (sD[k] * Pb[(int64_t)k * r]);
+        inbox[pos] = acc0 + acc1;
     }
 }
 
@@ -607,8 +591,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
     __shared__ int s_J, s_needP, s_tierP, s_next;
     __shared__ double s_runmax, s_carry;
     __shared__ T sD[64];
-    __shared__ __align__(16) T sLt[64 * 16];    // L11' of a 16-column block / d_k l_ck of the trailing columns
-    __shared__ T sInv[16];
+    __shared__ T s_col[2][65];
     __shared__ int8_t sSg[64];
     __shared__ int32_t s_d32[8];
     __shared__ int64_t s_d64[8];
@@ -667,19 +650,24 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         }
         __syncthreads();
         if (a.trace && tid == 0) a.trace[6 * J + 3] = gtimer();
-        // 2. dense LDL' of the panel: right-looking on the unscaled columns
-        //    (A_ci -= A_ij A_cj / d_j), one barrier per column, pivots computed
-        //    redundantly by every thread, columns scaled by 1/d at the end
-        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
-        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
+        // 2. dense LDL' of the panel
+        constexpr int NBR = sizeof(T) == 4 ? 32 : 16;
+        if (in_smem && w <= NBR && r <= 64) {
+            if (wid < 2) rot_panel_ldl<T, NBR>(sp, r, w, sSg, sD, s_runmax, a, (T(*)[2 * NBR + 1])s_col);
+            __syncthreads();
+            for (int j = tid; j < w; j += nt) dvec[c0 + j] = sD[j];
+        } else if (in_smem) {
+            cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec);
+        } else {
+            cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec);
+        }
         if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
-        // 3. push C_J = L_off D L_off', write the factor back
+        // 3. push C_J = L_off D L_off' (the factor is written back after the signal:
+        //    the ancestors only read the inbox, so the release does not wait for it)
         if (o > 0) {
             if (in_smem) cta_push(sp, r, w, o, s_d64[6], sD, a, inbox);
             else cta_push(L, r, w, o, s_d64[6], sD, a, inbox);
         }
-        if (in_smem)
-            for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
         __syncthreads();
         if (tid == 0) {
             int cont = -1;
@@ -694,6 +682,8 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
             s_next = cont;
             s_carry = s_runmax;
         }
+        if (in_smem)
+            for (int64_t i = tid; i < psize; i += nt) L[i] = sp[i];
         __syncthreads();
     }
 }
@@ -715,7 +705,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
 // ---------------------------------------------------------------------------
 
 template <typename T>
-__device__ __forceinline__ void solve_form_body(T* P, int r, int w, T* inv) {
+__device__ __forceinline__ bool solve_form_body(T* P, int r, int w, T* inv, double tau) {
     const int lane = threadIdx.x & 31;
     // (i) Linv row-major in inv[i * w + j] (lane j writes column j: conflict-free)
     for (int i = 0; i < w; ++i) {
@@ -730,6 +720,13 @@ __device__ __forceinline__ void solve_form_body(T* P, int r, int w, T* inv) {
         }
         __syncwarp();
     }
+    // growth test: the explicit inverse is used only when max |Linv| <= tau (an
+    // inverse-based solve loses at most that factor against substitution); larger
+    // panels keep L and the sweeps use substitution for them
+    double g = 0.0;
+    for (int e = lane; e < w * w; e += 32) g = fmax(g, fabs((double)inv[e]));
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if (!(g <= tau)) return false;
     // (ii) rows below
     for (int i = w + lane; i < r; i += 32)
         for (int j = 0; j < w; ++j) {
@@ -744,6 +741,7 @@ __device__ __forceinline__ void solve_form_body(T* P, int r, int w, T* inv) {
         P[(int64_t)j * r + i] = inv[i * w + j];
     }
     __syncwarp();
+    return true;
 }
 
 constexpr int SFW = 4;   // warps per solve-form CTA
@@ -752,7 +750,7 @@ template <typename T>
 __global__ void __launch_bounds__(SFW * 32) solve_form_kernel(const int32_t* __restrict__ list, int32_t n,
                                                               const int32_t* __restrict__ d32,
                                                               const int64_t* __restrict__ d64, T* lval, int slice,
-                                                              int inv_cap) {
+                                                              int inv_cap, double tau, int8_t* sf) {
     extern __shared__ __align__(16) unsigned char sraw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T* inv = reinterpret_cast<T*>(sraw) + (int64_t)wid * (inv_cap + slice);
@@ -763,14 +761,17 @@ __global__ void __launch_bounds__(SFW * 32) solve_form_kernel(const int32_t* __r
         T* L = lval + __ldg(d64 + (int64_t)J * 8);
         const int psize = r * w;
         if (w < 1) continue;
+        bool ok;
         if (psize <= slice) {
             for (int e = lane; e < psize; e += 32) sp[e] = L[e];
             __syncwarp();
-            solve_form_body(sp, r, w, inv);
-            for (int e = lane; e < psize; e += 32) L[e] = sp[e];
+            ok = solve_form_body(sp, r, w, inv, tau);
+            if (ok)
+                for (int e = lane; e < psize; e += 32) L[e] = sp[e];
         } else {
-            solve_form_body(L, r, w, inv);
+            ok = solve_form_body(L, r, w, inv, tau);
         }
+        if (lane == 0) sf[J] = ok ? 1 : 0;
         __syncwarp();
     }
 }
@@ -802,6 +803,7 @@ struct SolveArgs {
     int64_t* trace;      // optional per-task timeline (cipm_trace)
     int slice;           // per-warp shared-memory panel slice (elements)
     const double* rstate;   // refinement state: skip right-hand sides that have converged
+    const int8_t* sf;       // per supernode: 1 = panel in solve form (M), 0 = plain L (solve_form_kernel)
 };
 
 // warp-cooperative sums of the vector inbox of one supernode's columns (entries
@@ -854,13 +856,78 @@ __device__ __forceinline__ void vgather_q(T* const (&vq)[NQ], const uint8_t* __r
     __syncwarp();
 }
 
+// forward task, compute part: triangle and off-row push for NQ right-hand sides
+// together (each L element is read once for all of them).  Forced inline so L
+// keeps its address space (staged panel -> LDS).
+template <typename T, int NQ>
+__device__ __forceinline__ void fwd_compute_tri(const T* L, const SolveArgs& a, const Desc& d, T* const (&xq)[NQ],
+                                            T* const (&vq)[NQ], const T (&xa)[NQ], const T (&xb)[NQ],
+                                            T (*cs)[64], int J, const int64_t (&pos_pf)[2]) {
+    const int lane = threadIdx.x & 31;
+    const int c0 = d.c0, w = d.w, r = d.r;
+    T x0[NQ], x1[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        x0[q] = lane < w ? xa[q] - cs[q][lane] : (T)0;
+        x1[q] = lane + 32 < w ? xb[q] - cs[q][lane + 32] : (T)0;
+    }
+    constexpr int KB = 8 / NQ;                  // columns whose loads are issued together
+    for (int j0 = 0; j0 < w; j0 += KB) {
+        T l0[KB], l1[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {          // issue the block's loads before the dependent chain
+            const int j = j0 + k;
+            l0[k] = (j < w && lane > j && lane < w) ? L[j * r + lane] : (T)0;
+            l1[k] = (j < w && lane + 32 > j && lane + 32 < w) ? L[j * r + lane + 32] : (T)0;
+        }
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const int j = j0 + k;
+            if (j >= w) break;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
+                x0[q] -= l0[k] * xj;
+                x1[q] -= l1[k] * xj;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (lane < w) xq[q][c0 + lane] = x0[q];
+        if (lane + 32 < w) xq[q][c0 + lane + 32] = x1[q];
+    }
+    if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
+    for (int i0 = w; i0 < r; i0 += 32) {
+        const int i = i0 + lane;
+        const bool ok = i < r;
+        const int ii = ok ? i : r - 1;
+        const int pass = (i0 - w) >> 5;
+        const int64_t pos = pass < 2 ? pos_pf[pass] : (ok ? a.vpush_pos[d.cvo + i - w] : 0);
+        T acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = (T)0;
+#pragma unroll 8
+        for (int k = 0; k < w; ++k) {
+            const T lk = L[k * r + ii];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc[q] += lk * __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+        }
+        if (ok) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) vq[q][pos] = acc[q];
+        }
+    }
+    if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
+}
+
 // forward task, compute part, for NQ right-hand sides together: the panel is in
 // solve form (M = [L11^-1; L21 L11^-1]), so y_J = M_top b_J and the off-row push
 // M_off b_J are one GEMV with independent row dot products (lanes over rows; b_J
 // broadcast from shared memory).  Forced inline so L keeps its address space
 // (staged panel -> LDS).
 template <typename T, int NQ>
-__device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, const Desc& d, T* const (&xq)[NQ],
+__device__ __forceinline__ void fwd_compute_sf(const T* L, const SolveArgs& a, const Desc& d, T* const (&xq)[NQ],
                                             T* const (&vq)[NQ], const T (&xa)[NQ], const T (&xb)[NQ],
                                             T (*cs)[64], int J, const int64_t (&pos_pf)[2]) {
     const int lane = threadIdx.x & 31;
@@ -915,13 +982,88 @@ __device__ __forceinline__ void fwd_compute(const T* L, const SolveArgs& a, cons
     if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
 }
 
+// backward task body for NQ right-hand sides: own values (xa/xb, loaded before
+// the parent wait) D-solved, the ancestors' values at the off rows gathered for
+// every RHS in one round trip (64 rows at a time), then the transposed triangle.
+template <typename T, int NQ>
+__device__ __forceinline__ void bwd_body_tri(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
+                                         const int32_t* rowsJ, T* const (&xq)[NQ], T (*xo)[64],
+                                         const int (&rows_pf)[2], const T (&d_pf)[2], const T (&xa)[NQ],
+                                         const T (&xb)[NQ]) {
+    const int lane = threadIdx.x & 31;
+    const T* L0 = L + lane * r;
+    const T* L1 = L + (lane + 32) * r;
+    const bool o0 = lane < w, o1 = lane + 32 < w;
+    T x0[NQ], x1[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        x0[q] = o0 ? xa[q] / d_pf[0] : (T)0;      // D solve (ldl.py:101-102)
+        x1[q] = o1 ? xb[q] / d_pf[1] : (T)0;
+    }
+    for (int i0 = 0; i0 < o; i0 += 64) {
+        const int n = min(64, o - i0);
+        const int ra = i0 == 0 ? rows_pf[0] : (lane < n ? rowsJ[i0 + lane] : 0);
+        const int rb = i0 == 0 ? rows_pf[1] : (lane + 32 < n ? rowsJ[i0 + lane + 32] : 0);
+        T va[NQ], vb[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            va[q] = lane < n ? __ldcg(xq[q] + ra) : (T)0;
+            vb[q] = lane + 32 < n ? __ldcg(xq[q] + rb) : (T)0;
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            xo[q][lane] = va[q];
+            xo[q][lane + 32] = vb[q];
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int k = 0; k < n; ++k) {
+            const T la = o0 ? L0[w + i0 + k] : (T)0;
+            const T lb = o1 ? L1[w + i0 + k] : (T)0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xi = xo[q][k];
+                x0[q] -= la * xi;
+                x1[q] -= lb * xi;
+            }
+        }
+        __syncwarp();
+    }
+    constexpr int KB = 8 / NQ;
+    for (int j1 = w - 1; j1 >= 0; j1 -= KB) {
+        T l0[KB], l1[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {          // loads first, then the dependent chain
+            const int j = j1 - k;
+            l0[k] = (j >= 0 && lane < j) ? L0[j] : (T)0;
+            l1[k] = (j >= 0 && lane + 32 < j) ? L1[j] : (T)0;
+        }
+#pragma unroll
+        for (int k = 0; k < KB; ++k) {
+            const int j = j1 - k;
+            if (j < 0) break;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const T xj = __shfl_sync(0xffffffffu, j < 32 ? x0[q] : x1[q], j & 31);
+                x0[q] -= l0[k] * xj;
+                x1[q] -= l1[k] * xj;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (o0) xq[q][c0 + lane] = x0[q];
+        if (o1) xq[q][c0 + lane + 32] = x1[q];
+    }
+}
+
 // backward task body for NQ right-hand sides, panel in solve form:
 // x_J = M' v with v = [y_J / D; -x_off] — lane j owns columns j and j + 32 and
 // accumulates independent products over the rows (no dependent chain).  Own
 // values (xa / xb) were loaded before the parent wait; the ancestors' values at
 // the off rows are gathered for every RHS in one round trip (64 rows at a time).
 template <typename T, int NQ>
-__device__ __forceinline__ void bwd_body(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
+__device__ __forceinline__ void bwd_body_sf(const T* L, const SolveArgs& a, int c0, int w, int r, int o,
                                          const int32_t* rowsJ, T* const (&xq)[NQ], T (*xo)[64],
                                          const int (&rows_pf)[2], const T (&d_pf)[2], const T (&xa)[NQ],
                                          const T (&xb)[NQ]) {
@@ -1015,24 +1157,22 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xJ = x + (int64_t)q * a.dim + c0;
-        T bv[W];
+        T xv[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) bv[j] = xJ[j];
-        // solve form: [y_J; push] = M b_J (p[k][i] = M[i][k], M_top = L11^-1 unit lower)
+        for (int j = 0; j < W; ++j) xv[j] = xJ[j];
 #pragma unroll
-        for (int i = 0; i < W; ++i) {
-            T acc = bv[i];
+        for (int j = 0; j < W; ++j)
 #pragma unroll
-            for (int k = 0; k < i; ++k) acc += p[k][i] * bv[k];
-            xJ[i] = acc;
-        }
+            for (int i = j + 1; i < W; ++i) xv[i] -= p[j][i] * xv[j];
+#pragma unroll
+        for (int j = 0; j < W; ++j) xJ[j] = xv[j];
         T* vq = vin + (int64_t)q * a.nv;
 #pragma unroll
         for (int i = W; i < 16; ++i) {
             if (i >= r) break;
             T acc = (T)0;
 #pragma unroll
-            for (int k = 0; k < W; ++k) acc += p[k][i] * bv[k];
+            for (int k = 0; k < W; ++k) acc += p[k][i] * xv[k];
             vq[a.vpush_pos[cvo + i - W]] = acc;
         }
     }
@@ -1073,6 +1213,7 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
             if (lane == 0) bulk_g2s(slice, Lg, bytes, bar);
         }
         const int needP = (lane == 0 && d.parent >= 0) ? a.need[2 * d.parent] : 0;
+        const bool sfJ = __ldg(a.sf + J) != 0;
         // parent descriptor: raw loads now, shuffled after the compute (off the critical path)
         const int Jn = d.parent >= 0 ? d.parent : J;
         const int pv32 = lane < 8 ? __ldg(a.desc32 + (int64_t)Jn * 8 + lane) : 0;
@@ -1090,13 +1231,15 @@ __device__ __forceinline__ void fwd_chain(int J, const SolveArgs& a, const T* __
         }
         vgather_q<T, NQ>(vq, a.vin_col, d.vlo, d.vhi, w, cs);
         if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
-        // 3. triangle + push, from shared memory when staged
+        // 3. GEMV (solve form) or triangle + push, from shared memory when staged
         if (staged) {
             mbar_wait(bar, phase);
             phase ^= 1u;
-            fwd_compute<T, NQ>(slice, a, d, xq, vq, xa, xb, cs, J, pos_pf);
+            if (sfJ) fwd_compute_sf<T, NQ>(slice, a, d, xq, vq, xa, xb, cs, J, pos_pf);
+            else fwd_compute_tri<T, NQ>(slice, a, d, xq, vq, xa, xb, cs, J, pos_pf);
         } else {
-            fwd_compute<T, NQ>(Lg, a, d, xq, vq, xa, xb, cs, J, pos_pf);
+            if (sfJ) fwd_compute_sf<T, NQ>(Lg, a, d, xq, vq, xa, xb, cs, J, pos_pf);
+            else fwd_compute_tri<T, NQ>(Lg, a, d, xq, vq, xa, xb, cs, J, pos_pf);
         }
         dn = desc_from_regs(pv32, pv64);
         __syncwarp();
@@ -1230,17 +1373,9 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xv = x + (int64_t)q * a.dim;
-        T vt[W], xr[W];
+        T xr[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) vt[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
-        // solve form: x_J = M_top' (y_J / D) - M_off' x_off
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            T acc = vt[j];
-#pragma unroll
-            for (int i = j + 1; i < W; ++i) acc += p[j][i] * vt[i];
-            xr[j] = acc;
-        }
+        for (int j = 0; j < W; ++j) xr[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
 #pragma unroll
         for (int i = W; i < 16; ++i) {
             if (i >= r) break;
@@ -1248,6 +1383,10 @@ __device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const Solv
 #pragma unroll
             for (int j = 0; j < W; ++j) xr[j] -= p[j][i] * xi;
         }
+#pragma unroll
+        for (int j = W - 1; j >= 0; --j)
+#pragma unroll
+            for (int i = j + 1; i < W; ++i) xr[j] -= p[j][i] * xr[i];
 #pragma unroll
         for (int j = 0; j < W; ++j) xv[c0 + j] = xr[j];
     }
@@ -1287,6 +1426,7 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
             if (lane == 0) bulk_g2s(slice, Lg, bytes, &bars[wid]);
         }
         // static inputs fetched before waiting for the parent
+        const bool sfJ = __ldg(a.sf + J) != 0;
         const int rows_pf[2] = {lane < o ? __ldg(rowsJ + lane) : 0, lane + 32 < o ? __ldg(rowsJ + 32 + lane) : 0};
         const T d_pf[2] = {lane < w ? dvec[c0 + lane] : (T)1, lane + 32 < w ? dvec[c0 + lane + 32] : (T)1};
         // own values: final since the forward sweep, loaded before the wait too
@@ -1300,9 +1440,11 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
             if (staged) {
                 mbar_wait(&bars[wid], phase);
                 phase ^= 1u;
-                bwd_body<T, 2>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                { if (sfJ) bwd_body_sf<T, 2>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                  else bwd_body_tri<T, 2>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb); }
             } else {
-                bwd_body<T, 2>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                { if (sfJ) bwd_body_sf<T, 2>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                  else bwd_body_tri<T, 2>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb); }
             }
         } else {
             T* const xq[1] = {x + (a.act0 ? 0 : a.dim)};
@@ -1313,9 +1455,11 @@ __global__ void __launch_bounds__(SW * 32, 3) backward_kernel(SolveArgs a0, cons
             if (staged) {
                 mbar_wait(&bars[wid], phase);
                 phase ^= 1u;
-                bwd_body<T, 1>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                { if (sfJ) bwd_body_sf<T, 1>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                  else bwd_body_tri<T, 1>(slice, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb); }
             } else {
-                bwd_body<T, 1>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                { if (sfJ) bwd_body_sf<T, 1>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb);
+                  else bwd_body_tri<T, 1>(Lg, a, c0, w, r, o, rowsJ, xq, xs[wid], rows_pf, d_pf, xa, xb); }
             }
         }
         __syncwarp();
@@ -1379,6 +1523,7 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.trace = nullptr;
     a.slice = (int)c.solve_slice;
     a.rstate = c.rstate;
+    a.sf = c.sf_flag;
     return a;
 }
 
@@ -1462,7 +1607,7 @@ int factor_t(Ctx& c) {
         const size_t smem = sizeof(T) * (size_t)(c.solve_form_inv + slice) * SFW;
         solve_form_kernel<T><<<c.solve_form_blocks, SFW * 32, smem, c.stream>>>(c.sym.bwd_order, nsf, c.sym.desc32,
                                                                                 c.sym.desc64, (T*)c.lval, slice,
-                                                                                c.solve_form_inv);
+                                                                                c.solve_form_inv, c.sf_tau, c.sf_flag);
         c.launches++;
     }
     if (c.profile) {

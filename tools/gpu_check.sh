@@ -17,3 +17,5 @@ PY
 CIPM_PHASES=1 timeout 300 python tools/solve_probe.py c2_lasso 3 2>&1 | grep phases | tail -1
 timeout 300 python tools/solve_probe.py --trace c2_lasso > $O/trace.log 2>&1; mv gpurun_out/trace_c2_lasso.npz $O/ 2>/dev/null
 timeout 300 python tools/solve_probe.py --host c2_lasso 2>&1 | head -5
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_probe.csv python tools/solve_probe.py c2_lasso 2 > /dev/null 2>&1
+python tools/launch_summary.py $O/launches_probe.csv 25 > $O/launches_probe.txt 2>&1; head -30 $O/launches_probe.txt
