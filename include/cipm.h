@@ -220,7 +220,8 @@ int cipm_kernel_times(cipm_ctx *ctx, double *factor_ms, double *solve_ms);
  * ‖q‖∞, ‖b‖∞ of the reordered unscaled data, ipm.py:184-185). --- */
 int cipm_batch_create(const cipm_problem_desc *desc, int count, const cipm_settings *settings,
                       double eps_feas, double eps_inf, int max_iter, cipm_batch **out);
-/* info[6] = {count, n, m, nnz(L), shared bytes per instance CTA, in shared memory (1) or workspace (0)} */
+/* info[9] = {count, n, m, nnz(L), shared bytes per instance CTA, in shared memory (1) or workspace (0),
+ *           CTA-parallel factorisation (1) or sequential (0), dense root width, leaf groups} */
 int cipm_batch_info(const cipm_batch *b, int64_t *info);
 int cipm_batch_set_values(cipm_batch *b, const double *V, const double *q, const double *bvec,
                           const double *d_row, const double *d_col, const double *c_obj,

@@ -187,9 +187,10 @@ class BatchSolver:
         raise_for_status(rc, "batch upload")
 
     def info(self) -> dict:
-        out = np.zeros(6, dtype=np.int64)
+        out = np.zeros(9, dtype=np.int64)
         raise_for_status(lib().cipm_batch_info(self.handle, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
-        return dict(zip(("count", "n", "m", "nnz_l", "smem_bytes", "in_smem"), (int(v) for v in out)))
+        return dict(zip(("count", "n", "m", "nnz_l", "smem_bytes", "in_smem", "cta_factor", "root_width", "groups"),
+                        (int(v) for v in out)))
 
     def run(self) -> float:
         """Device solve of every instance; returns the CUDA-event time (ms)."""

@@ -101,7 +101,7 @@ __device__ void carve(const BatchPattern& pt, double* base, Inst& I) {
     I.rb = take(dim); I.rx = take(dim); I.rr = take(dim); I.rbest = take(dim); I.t = take(dim);
     I.dsc = take(m); I.h = take(m); I.w = take(m); I.lam = take(m);
     I.V = take(pt.nnz_p + pt.nnz_a);
-    I.lx = take(pt.nnz_l); I.d = take(dim); I.y = take(dim);
+    I.lx = take(pt.use_groups ? pt.panel_total + pt.inbox_total : pt.nnz_l); I.d = take(dim); I.y = take(dim);
     I.qs = take(n); I.bs = take(m);
 }
 
@@ -165,6 +165,287 @@ __device__ void ldl_solve_add(const BatchPattern& pt, Inst& I, const double* r, 
     for (int k = 0; k < dim; ++k) x[pt.perm[k]] += t[k];
 }
 
+// ------------------- CTA-parallel factorisation (use_groups) -------------------
+// The same L D L' as kkt/ldl.py:37-88 (same elimination order: the groups are
+// independent subtrees, so eliminating them first or interleaved gives the same
+// factor up to rounding), computed by all threads of the instance's CTA:
+//   1. base values of every group panel and of the dense root block scattered from
+//      V / -h with the static regularisation on the diagonal (system.py:253);
+//   2. one thread per group: dense right-looking LDL' of its panel (w <= 16),
+//      its contribution block L_off D L_off' into private inbox slots;
+//   3. root entries gather their inbox slots (fixed order, no atomics);
+//   4. root: blocked right-looking LDL' with 32-column blocks — warp 0 factors the
+//      diagonal block in registers (shuffles), one thread per row below solves
+//      against it, the trailing update is parallel over entries;
+//   5. every diagonal block is replaced by its unit-lower inverse (solve form:
+//      the blocked triangular solves become GEMVs).
+// Dynamic regularisation (ldl.py:79-87): groups use their own running max, the
+// root starts from the max over all group pivots (delta_d * runmax is O(eps^2)).
+constexpr int RB = 32;             // root block width
+
+__device__ __forceinline__ double root_bump(double dd, double ds, double dd_coef, double runmax, int8_t sg,
+                                            int& bumped) {
+    const double bound = ds + dd_coef * runmax;
+    if (fabs(dd) < bound) {
+        ++bumped;
+        return sg > 0 ? bound : -bound;
+    }
+    return dd;
+}
+
+__device__ int group_ldl(const BatchPattern& pt, double* P, int r, int w, const int32_t* cols, double* d,
+                         double ds, double ddc, double& runmax) {
+    int bumped = 0;
+    for (int j = 0; j < w; ++j) {
+        double dj = root_bump(P[j * r + j], ds, ddc, runmax, pt.sign[cols[j]], bumped);
+        if (dj == 0.0) return -1;
+        d[cols[j]] = dj;
+        runmax = fmax(runmax, fabs(dj));
+        const double inv = 1.0 / dj;
+        for (int i = j + 1; i < r; ++i) {
+            const double lij = P[j * r + i] * inv;          // a_ij unscaled -> l_ij
+            const int cend = i < w - 1 ? i : w - 1;
+            for (int c = j + 1; c <= cend; ++c) P[c * r + i] -= lij * P[j * r + c];
+        }
+        for (int i = j + 1; i < r; ++i) P[j * r + i] *= inv;
+        P[j * r + j] = 1.0;
+    }
+    return bumped;
+}
+
+// all threads; returns (in *s_err) 1 on a zero pivot
+__device__ void bfactor_cta(const BatchPattern& pt, Inst& I, double ds, double ddc, double* sblk, int* s_err,
+                            double* sred) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = pt.W, s0 = pt.s;
+    double* PS = I.lx;                       // group panels, then the root block (col-major W x W)
+    double* R = PS + pt.root_off;
+    double* inbox = PS + pt.panel_total;
+    for (int k = tid; k < pt.panel_total; k += BT) PS[k] = 0.0;
+    __syncthreads();
+    for (int k = tid; k < pt.nbsc; k += BT) {
+        const int src = pt.bsc_src[k];
+        PS[pt.bsc_slot[k]] = src >= 0 ? I.V[src] : -I.h[-src - 2];
+    }
+    __syncthreads();
+    for (int k = tid; k < pt.nbdg; k += BT) {
+        const int slot = pt.bdg_slot[k];
+        PS[slot] = PS[slot] + (pt.sign[pt.bdg_col[k]] > 0 ? ds : -ds);
+    }
+    __syncthreads();
+    // 2. groups
+    double gmax[1] = {0.0};
+    for (int g = tid; g < pt.ngroups; g += BT) {
+        const int32_t* gi = pt.g_info + 8 * g;
+        const int w = gi[1], r = gi[2], o = r - w;
+        double* P = PS + gi[3];
+        double runmax = 0.0;
+        if (group_ldl(pt, P, r, w, pt.g_cols + gi[0], I.d, ds, ddc, runmax) < 0) *s_err = 1;
+        gmax[0] = fmax(gmax[0], runmax);
+        double* ib = inbox + gi[4];
+        int tb = 0;
+        for (int b = 0; b < o; ++b) {
+            for (int a = b; a < o; ++a) {
+                double acc = 0.0;
+                for (int k = 0; k < w; ++k) acc += P[k * r + w + a] * I.d[pt.g_cols[gi[0] + k]] * P[k * r + w + b];
+                ib[tb + (a - b)] = acc;
+            }
+            tb += o - b;
+        }
+    }
+    breduce<1>(gmax, 1u, sred);
+    // 3. root assembly: R(e) -= sum of its inbox slots
+    for (int k = tid; k < pt.nrg; k += BT) {
+        double acc = 0.0;
+        for (int p = pt.rg_ptr[k]; p < pt.rg_ptr[k + 1]; ++p) acc += inbox[pt.rg_idx[p]];
+        R[pt.rg_tgt[k]] -= acc;
+    }
+    __syncthreads();
+    // 4. root blocked LDL'
+    double runmax = gmax[0];
+    int bumped = 0;
+    for (int k0 = 0; k0 < W; k0 += RB) {
+        const int nbk = min(RB, W - k0), k1 = k0 + nbk;
+        if (warp == 0) {
+            double x[RB];
+#pragma unroll
+            for (int c = 0; c < RB; ++c) x[c] = (c < nbk && lane < nbk && c <= lane) ? R[(k0 + c) * W + k0 + lane] : 0.0;
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                if (j < nbk) {
+                    double dj = __shfl_sync(0xffffffffu, x[j], j);
+                    dj = root_bump(dj, ds, ddc, runmax, pt.sign[s0 + k0 + j], bumped);
+                    if (dj == 0.0 && lane == 0) *s_err = 1;
+                    runmax = fmax(runmax, fabs(dj));
+                    const double inv = 1.0 / dj;
+                    if (lane == 0) {
+                        I.d[s0 + k0 + j] = dj;
+                        sblk[RB * RB + j] = inv;
+                    }
+                    const double xj = x[j];
+#pragma unroll
+                    for (int c = j + 1; c < RB; ++c) {
+                        const double acj = __shfl_sync(0xffffffffu, xj, c) * inv;
+                        if (lane >= c) x[c] -= xj * acj;
+                    }
+                    x[j] = lane > j ? xj * inv : (lane == j ? 1.0 : 0.0);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < RB; ++c) {
+                if (c < nbk && lane < nbk && c <= lane) R[(k0 + c) * W + k0 + lane] = x[c];
+                sblk[c * RB + lane] = (c < lane && lane < nbk) ? x[c] : 0.0;   // sblk[c][i] = l_ic
+            }
+        }
+        __syncthreads();
+        // rows below the diagonal block: x_i L11' = a_i (right-looking on the row)
+        for (int i = k1 + tid; i < W; i += BT) {
+            double x[RB];
+#pragma unroll
+            for (int c = 0; c < RB; ++c) x[c] = c < nbk ? R[(k0 + c) * W + i] : 0.0;
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                const double xj = x[j];
+#pragma unroll
+                for (int c = j + 1; c < RB; ++c) x[c] -= xj * sblk[j * RB + c];
+                x[j] = xj * sblk[RB * RB + j];
+            }
+#pragma unroll
+            for (int c = 0; c < RB; ++c)
+                if (c < nbk) R[(k0 + c) * W + i] = x[c];
+        }
+        __syncthreads();
+        // trailing update of the lower triangle
+        for (int c = k1 + warp; c < W; c += NW) {
+            for (int i = c + lane; i < W; i += 32) {
+                double acc = 0.0;
+                for (int k = 0; k < nbk; ++k) {
+                    const double* Ck = R + (k0 + k) * W;
+                    acc += Ck[i] * (I.d[s0 + k0 + k] * Ck[c]);
+                }
+                R[c * W + i] -= acc;
+            }
+        }
+        __syncthreads();
+    }
+    // 5. diagonal blocks -> unit-lower inverses (column-parallel substitution, lane j = column j)
+    for (int kb = warp; kb * RB < W; kb += NW) {
+        const int k0 = kb * RB, nbk = min(RB, W - k0);
+        double v[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            if (i < nbk)
+                for (int k = 0; k < i; ++k) acc += R[(k0 + k) * W + k0 + i] * v[k];
+            v[i] = (i < nbk && lane < nbk) ? (i == lane ? 1.0 : (i < lane ? 0.0 : -acc)) : 0.0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+            if (lane < nbk && i < nbk) R[(k0 + lane) * W + k0 + i] = v[i];   // column lane, zeros above the diagonal
+        __syncwarp();
+    }
+    __syncthreads();
+    (void)bumped;
+}
+
+// x += solve(r) (permuted, groups + blocked root, kkt/ldl.py:91-104); all threads
+__device__ void bsolve_cta(const BatchPattern& pt, Inst& I, const double* r, double* x, double* sblk) {
+    const int tid = threadIdx.x;
+    const int dim = pt.n + pt.m, W = pt.W, s0 = pt.s;
+    double* t = I.t;
+    double* PS = I.lx;
+    const double* R = PS + pt.root_off;
+    double* vin = PS + pt.panel_total;       // the factor inbox is free during solves
+    for (int k = tid; k < dim; k += BT) t[k] = r[pt.perm[k]];
+    __syncthreads();
+    // groups, forward
+    for (int g = tid; g < pt.ngroups; g += BT) {
+        const int32_t* gi = pt.g_info + 8 * g;
+        const int w = gi[1], rr = gi[2], o = rr - w;
+        const double* P = PS + gi[3];
+        const int32_t* cols = pt.g_cols + gi[0];
+        double y[16];
+        for (int c = 0; c < w; ++c) {
+            double acc = t[cols[c]];
+            for (int k = 0; k < c; ++k) acc -= P[k * rr + c] * y[k];
+            y[c] = acc;
+            t[cols[c]] = acc;
+        }
+        for (int a = 0; a < o; ++a) {
+            double acc = 0.0;
+            for (int k = 0; k < w; ++k) acc += P[k * rr + w + a] * y[k];
+            vin[gi[5] + a] = acc;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < W; i += BT) {
+        double acc = 0.0;
+        for (int p = pt.rv_ptr[i]; p < pt.rv_ptr[i + 1]; ++p) acc += vin[pt.rv_idx[p]];
+        t[s0 + i] -= acc;
+    }
+    __syncthreads();
+    // root, forward: y_b = inv(L_bb) (t_b - sum_{k<b} L_bk y_k)
+    for (int k0 = 0; k0 < W; k0 += RB) {
+        const int nbk = min(RB, W - k0), k1 = k0 + nbk;
+        if (tid < nbk) {
+            double acc = 0.0;
+            for (int k = 0; k <= tid; ++k) acc += R[(k0 + k) * W + k0 + tid] * t[s0 + k0 + k];
+            sblk[tid] = acc;
+        }
+        __syncthreads();
+        if (tid < nbk) t[s0 + k0 + tid] = sblk[tid];
+        __syncthreads();
+        for (int i = k1 + tid; i < W; i += BT) {
+            double acc = 0.0;
+            for (int k = 0; k < nbk; ++k) acc += R[(k0 + k) * W + i] * t[s0 + k0 + k];
+            t[s0 + i] -= acc;
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < W; i += BT) t[s0 + i] /= I.d[s0 + i];
+    __syncthreads();
+    // root, backward: x_b = inv(L_bb)' (t_b - sum_{i>=k1} L_ib' x_i), last block first
+    const int nb = (W + RB - 1) / RB;
+    for (int kb = nb - 1; kb >= 0; --kb) {
+        const int k0 = kb * RB, nbk = min(RB, W - k0), k1 = k0 + nbk;
+        if (tid < nbk) {
+            const double* Ck = R + (k0 + tid) * W;
+            double acc = 0.0;
+            for (int i = k1; i < W; ++i) acc += Ck[i] * t[s0 + i];
+            sblk[tid] = t[s0 + k0 + tid] - acc;
+        }
+        __syncthreads();
+        if (tid < nbk) {
+            const double* Cj = R + (k0 + tid) * W + k0;     // column tid of the inverse block
+            double acc = 0.0;
+            for (int i = tid; i < nbk; ++i) acc += Cj[i] * sblk[i];
+            t[s0 + k0 + tid] = acc;
+        }
+        __syncthreads();
+    }
+    // groups, backward: x_c = y_c / d_c - L_off' x_R - sum_{k>c} l_kc x_k
+    for (int g = tid; g < pt.ngroups; g += BT) {
+        const int32_t* gi = pt.g_info + 8 * g;
+        const int w = gi[1], rr = gi[2], o = rr - w;
+        const double* P = PS + gi[3];
+        const int32_t* cols = pt.g_cols + gi[0];
+        const int32_t* rows = pt.g_rows + gi[6];
+        double xv[16];
+        for (int c = w - 1; c >= 0; --c) {
+            double acc = t[cols[c]] / I.d[cols[c]];
+            for (int a = 0; a < o; ++a) acc -= P[c * rr + w + a] * t[s0 + rows[a]];
+            for (int k = c + 1; k < w; ++k) acc -= P[c * rr + k] * xv[k];
+            xv[c] = acc;
+            t[cols[c]] = acc;
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < dim; k += BT) x[pt.perm[k]] += t[k];
+    __syncthreads();
+}
+
 struct Ctl {
     double tau, kappa, mu, gtau, sigma;
     double dtau[2], dkappa[2];
@@ -180,6 +461,7 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
     __shared__ double sred[NW * 16];
     __shared__ Ctl C;
     __shared__ double sv[8];
+    __shared__ double sblk[RB * RB + RB];   // root: L11 of the current block + 1/d (factor), block vector (solve)
     const int inst = blockIdx.x;
     if (inst >= count) return;
     const int tid = threadIdx.x;
@@ -400,7 +682,9 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
         __syncthreads();
         if (C.err) { status = BS_NUMERICAL; break; }
         // ---- numeric factorisation ----
-        if (tid == 0) {
+        if (pt.use_groups) {
+            bfactor_cta(pt, I, bd.delta_s, bd.delta_d, sblk, &C.err, sred);
+        } else if (tid == 0) {
             const int bumped = factor_seq(pt, I, bd.delta_s, bd.delta_d);
             if (bumped < 0) C.err = 1;
         }
@@ -421,7 +705,8 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
             double best = INFINITY, prev = INFINITY;
             int ups = 0;
             for (int step = 1; step <= bd.refine_max; ++step) {
-                if (tid == 0) ldl_solve_add(pt, I, I.rr, I.rx);
+                if (pt.use_groups) bsolve_cta(pt, I, I.rr, I.rx, sblk);
+                else if (tid == 0) ldl_solve_add(pt, I, I.rr, I.rx);
                 __syncthreads();
                 double rn[1] = {-INFINITY};
                 for (int i = tid; i < n; i += BT) {
@@ -647,7 +932,8 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
 size_t batch_smem_doubles(const BatchPattern& pt) {
     const int64_t n = pt.n, m = pt.m, dim = n + m;
     auto r2 = [](int64_t c) { return (c + 1) & ~int64_t(1); };
-    return (size_t)(r2(n) * 5 + r2(m) * 13 + r2(dim) * 7 + r2(pt.nnz_p + pt.nnz_a) + r2(pt.nnz_l) + r2(dim) * 2);
+    const int64_t nl = pt.use_groups ? (int64_t)pt.panel_total + pt.inbox_total : pt.nnz_l;
+    return (size_t)(r2(n) * 5 + r2(m) * 13 + r2(dim) * 7 + r2(pt.nnz_p + pt.nnz_a) + r2(nl) + r2(dim) * 2);
 }
 
 int batch_launch(const BatchPattern& pt, const BatchData& bd, int count, cudaStream_t stream, int smem_bytes) {
@@ -665,6 +951,7 @@ int batch_launch(const BatchPattern& pt, const BatchData& bd, int count, cudaStr
 // host side: pattern analysis (once) + the C ABI (include/cipm.h cipm_batch_*)
 // ===========================================================================
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -832,6 +1119,164 @@ int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings
         }
         upp[j + 1] = (int32_t)upi.size();
     }
+    // ---- CTA-parallel factorisation plan (BatchPattern::use_groups) ----
+    // Groups = maximal subtrees of the elimination tree with <= 16 columns and <= 48
+    // panel rows (independent: no K or L entries between disjoint subtrees); every
+    // other column joins the dense root block (<= 128 columns), the Schur complement
+    // of the groups.  The elimination order becomes [groups..., root] (the same L D L'
+    // up to rounding: each group is closed under descendants), so the root is the
+    // contiguous range [s, dim) of the new order.
+    std::vector<int32_t> g_info, g_cols, g_rows, bsc_slot, bsc_src, bdg_slot, bdg_col, rg_tgt, rg_ptr, rg_idx,
+        rv_ptr, rv_idx, perm_g, sign_g_i;
+    std::vector<int8_t> sign_g;
+    int64_t plan_s = dim, plan_W = 0, plan_ng = 0, panel_total = 0, root_off = 0, inbox_total = 0;
+    bool plan_ok = false;
+    if (!getenv("CIPM_BATCH_SEQ") && dim > 0) {
+        std::vector<std::vector<int32_t>> kids(dim);
+        std::vector<int32_t> ssize(dim, 1);
+        for (int64_t j = 0; j < dim; ++j)
+            if (parent[j] >= 0) kids[parent[j]].push_back((int32_t)j);
+        for (int64_t j = 0; j < dim; ++j)
+            if (parent[j] >= 0) ssize[parent[j]] += ssize[j];     // children precede parents
+        std::vector<int32_t> gid(dim, -1);
+        std::vector<std::vector<int32_t>> gcols, groots_old;
+        std::vector<int32_t> rootc;
+        std::vector<int32_t> stack;
+        for (int64_t j = dim - 1; j >= 0; --j)
+            if (parent[j] < 0) stack.push_back((int32_t)j);
+        while (!stack.empty()) {
+            const int32_t j = stack.back();
+            stack.pop_back();
+            bool grp = false;
+            if (ssize[j] <= 16) {
+                std::vector<int32_t> cols, sub{j}, offr;
+                while (!sub.empty()) {
+                    const int32_t u = sub.back();
+                    sub.pop_back();
+                    cols.push_back(u);
+                    for (int32_t k : kids[u]) sub.push_back(k);
+                }
+                std::sort(cols.begin(), cols.end());
+                for (int32_t u : cols)
+                    for (int32_t p = lp[u]; p < lp[u + 1]; ++p)
+                        if (!std::binary_search(cols.begin(), cols.end(), li[p])) offr.push_back(li[p]);
+                std::sort(offr.begin(), offr.end());
+                offr.erase(std::unique(offr.begin(), offr.end()), offr.end());
+                if (cols.size() + offr.size() <= 48) {
+                    grp = true;
+                    for (int32_t u : cols) gid[u] = (int32_t)gcols.size();
+                    gcols.push_back(cols);
+                    groots_old.push_back(offr);
+                }
+            }
+            if (!grp) {
+                rootc.push_back(j);
+                for (int32_t k : kids[j]) stack.push_back(k);
+            }
+        }
+        std::sort(rootc.begin(), rootc.end());
+        const int64_t W = (int64_t)rootc.size(), ng = (int64_t)gcols.size();
+        bool ok = W <= 128;
+        for (int64_t g = 0; g < ng && ok; ++g)
+            for (int32_t r : groots_old[g])
+                if (gid[r] >= 0) ok = false;                      // off rows must be root columns
+        if (ok) {
+            // new elimination order: groups (ascending old index inside), then the root
+            std::vector<int32_t> sigma, inv(dim);
+            for (auto& cols : gcols)
+                for (int32_t u : cols) sigma.push_back(u);
+            const int64_t s0 = (int64_t)sigma.size();
+            for (int32_t u : rootc) sigma.push_back(u);
+            for (int64_t k = 0; k < dim; ++k) inv[sigma[k]] = (int32_t)k;
+            perm_g.resize(dim);
+            sign_g.resize(dim);
+            for (int64_t k = 0; k < dim; ++k) { perm_g[k] = perm[sigma[k]]; sign_g[k] = sign[sigma[k]]; }
+            std::vector<std::vector<int32_t>> groots(ng);     // root-local off rows, ascending
+            for (int64_t g = 0; g < ng; ++g) {
+                for (int32_t r : groots_old[g]) groots[g].push_back(inv[r] - (int32_t)s0);
+                std::sort(groots[g].begin(), groots[g].end());
+            }
+            std::vector<int32_t> lrow(dim, -1);                // new index -> local row in its group panel
+            int64_t off = 0, ib = 0, vb = 0;
+            g_info.assign((size_t)ng * 8, 0);
+            for (int64_t g = 0; g < ng; ++g) {
+                const int64_t w = (int64_t)gcols[g].size(), o = (int64_t)groots[g].size(), r = w + o;
+                int32_t* gi = &g_info[(size_t)g * 8];
+                gi[0] = (int32_t)g_cols.size();
+                gi[1] = (int32_t)w;
+                gi[2] = (int32_t)r;
+                gi[3] = (int32_t)off;
+                gi[4] = (int32_t)ib;
+                gi[5] = (int32_t)vb;
+                gi[6] = (int32_t)g_rows.size();
+                for (int64_t c = 0; c < w; ++c) {
+                    const int32_t nc = inv[gcols[g][c]];
+                    g_cols.push_back(nc);
+                    lrow[nc] = (int32_t)c;
+                }
+                for (int32_t rr : groots[g]) g_rows.push_back(rr);
+                off += r * w;
+                ib += o * (o + 1) / 2;
+                vb += o;
+            }
+            root_off = off;
+            panel_total = off + W * W;
+            inbox_total = std::max<int64_t>(ib, vb);
+            // base scatter: K entry (old i <= old j) is the lower entry (max, min) of the new order
+            for (int64_t j = 0; j < dim; ++j)
+                for (int32_t p = cp[j]; p < cp[j + 1]; ++p) {
+                    const int64_t a0 = inv[ci[p]], b0 = inv[j];
+                    const int64_t row = std::max(a0, b0), col = std::min(a0, b0);
+                    int64_t slot;
+                    if (col >= s0) {
+                        slot = root_off + (col - s0) * W + (row - s0);
+                    } else {
+                        const int64_t g = gid[sigma[col]];
+                        const int32_t* gi = &g_info[(size_t)g * 8];
+                        const int64_t r = gi[2], w = gi[1];
+                        int64_t lr;
+                        if (row < s0) lr = lrow[row];
+                        else lr = w + (std::lower_bound(groots[g].begin(), groots[g].end(), (int32_t)(row - s0)) -
+                                       groots[g].begin());
+                        slot = gi[3] + (int64_t)lrow[col] * r + lr;
+                    }
+                    if (csrc[p] != -1) { bsc_slot.push_back((int32_t)slot); bsc_src.push_back(csrc[p]); }
+                    if (a0 == b0) { bdg_slot.push_back((int32_t)slot); bdg_col.push_back((int32_t)col); }
+                }
+            // root gather of the contribution inboxes, and of the solve's vector inbox per root row
+            std::vector<std::pair<int32_t, int32_t>> tg;
+            std::vector<std::vector<int32_t>> vrows(W);
+            for (int64_t g = 0; g < ng; ++g) {
+                const int32_t* gi = &g_info[(size_t)g * 8];
+                const int64_t o = (int64_t)groots[g].size();
+                int64_t tb = 0;
+                for (int64_t b = 0; b < o; ++b) {
+                    for (int64_t a = b; a < o; ++a)
+                        tg.emplace_back((int32_t)(groots[g][b] * W + groots[g][a]), (int32_t)(gi[4] + tb + (a - b)));
+                    tb += o - b;
+                }
+                for (int64_t a = 0; a < o; ++a) vrows[groots[g][a]].push_back((int32_t)(gi[5] + a));
+            }
+            std::stable_sort(tg.begin(), tg.end(), [](auto& x, auto& y) { return x.first < y.first; });
+            for (size_t e = 0; e < tg.size(); ++e) {
+                if (e == 0 || tg[e].first != tg[e - 1].first) { rg_tgt.push_back(tg[e].first); rg_ptr.push_back((int32_t)e); }
+                rg_idx.push_back(tg[e].second);
+            }
+            rg_ptr.push_back((int32_t)tg.size());
+            rv_ptr.push_back(0);
+            for (int64_t i = 0; i < W; ++i) {
+                for (int32_t v : vrows[i]) rv_idx.push_back(v);
+                rv_ptr.push_back((int32_t)rv_idx.size());
+            }
+            plan_s = s0;
+            plan_W = W;
+            plan_ng = ng;
+            plan_ok = true;
+        }
+        if (getenv("CIPM_BATCH_DEBUG"))
+            fprintf(stderr, "[cipm] batch plan: dim %lld root W %lld groups %lld ok %d\n", (long long)dim, (long long)W,
+                    (long long)ng, (int)ok);
+    }
     // CSR / transposed patterns (int32)
     std::vector<int32_t> prp(d->p_rowptr, d->p_rowptr + n + 1), pci(d->p_colidx, d->p_colidx + nnzp);
     std::vector<int32_t> arp(d->a_rowptr, d->a_rowptr + m + 1), aci(d->a_colidx, d->a_colidx + nnza);
@@ -882,6 +1327,38 @@ int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings
     BTRY(bup(h, &pt.up_i, upi));
     BTRY(bup(h, &pt.up_p2, up2));
     h->h_perm = perm;
+    if (plan_ok) {
+        pt.s = (int)plan_s;
+        pt.W = (int)plan_W;
+        pt.ngroups = (int)plan_ng;
+        pt.panel_total = (int)panel_total;
+        pt.root_off = (int)root_off;
+        pt.inbox_total = (int)inbox_total;
+        pt.nbsc = (int)bsc_slot.size();
+        pt.nbdg = (int)bdg_slot.size();
+        pt.nrg = (int)rg_tgt.size();
+        BTRY(bup(h, &pt.g_info, g_info));
+        BTRY(bup(h, &pt.g_cols, g_cols));
+        BTRY(bup(h, &pt.g_rows, g_rows));
+        BTRY(bup(h, &pt.bsc_slot, bsc_slot));
+        BTRY(bup(h, &pt.bsc_src, bsc_src));
+        BTRY(bup(h, &pt.bdg_slot, bdg_slot));
+        BTRY(bup(h, &pt.bdg_col, bdg_col));
+        BTRY(bup(h, &pt.rg_tgt, rg_tgt));
+        BTRY(bup(h, &pt.rg_ptr, rg_ptr));
+        BTRY(bup(h, &pt.rg_idx, rg_idx));
+        BTRY(bup(h, &pt.rv_ptr, rv_ptr));
+        BTRY(bup(h, &pt.rv_idx, rv_idx));
+        pt.use_groups = 1;
+        if (batch_smem_doubles(pt) * sizeof(double) > 220 * 1024) {
+            pt.use_groups = 0;                    // too large for one CTA: keep the sequential path
+        } else {
+            // the new elimination order: permutation and signs of the groups-then-root order
+            BTRY(bup(h, &pt.perm, perm_g));
+            BTRY(bup(h, &pt.sign, sign_g));
+            h->h_perm = perm_g;
+        }
+    }
     // per-instance buffers
     BatchData& bd = h->bd;
     const int64_t nv = nnzp + nnza;
@@ -905,7 +1382,7 @@ int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings
     BTRY(balloc(h, &bd.out_status, count));
     const size_t nd = batch_smem_doubles(pt);
     const size_t bytes = nd * sizeof(double);
-    if (bytes <= 200 * 1024) {
+    if (bytes <= 220 * 1024) {
         bd.use_smem = 1;
         h->smem_bytes = (int)bytes;
     } else {
@@ -940,6 +1417,9 @@ int cipm_batch_info(const cipm_batch* h, int64_t* info) {
     info[3] = h->pt.nnz_l;
     info[4] = h->smem_bytes;
     info[5] = h->bd.use_smem;
+    info[6] = h->pt.use_groups;
+    info[7] = h->pt.W;
+    info[8] = h->pt.ngroups;
     return CIPM_OK;
 }
 

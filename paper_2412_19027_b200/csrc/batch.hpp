@@ -23,6 +23,23 @@ struct BatchPattern {
     const int32_t *lp = nullptr, *li = nullptr;              // L column pointers / rows
     const int32_t *up_ptr = nullptr, *up_i = nullptr, *up_p2 = nullptr;   // up-looking schedule
     const int32_t *a_src = nullptr, *b_src = nullptr;        // user -> reordered A values / rows
+    // ---- CTA-parallel factorisation (use_groups): the elimination order splits into
+    // independent leaf groups (subtrees below the top chain) and one dense root block of
+    // the last W columns (rows / columns >= s).  Groups: thread per group, dense panel;
+    // root: blocked right-looking LDL' by the CTA, diagonal blocks kept as inverses.
+    int use_groups = 0;
+    int s = 0, W = 0, ngroups = 0;
+    int panel_total = 0, root_off = 0, inbox_total = 0;
+    const int32_t* g_info = nullptr;    // per group 8 ints: cols_off, w, r, panel_off, inbox_off, vin_off, rows_off, 0
+    const int32_t* g_cols = nullptr;    // group columns (permuted indices, ascending)
+    const int32_t* g_rows = nullptr;    // root-local indices of each group's off rows (ascending)
+    int nbsc = 0;
+    const int32_t *bsc_slot = nullptr, *bsc_src = nullptr;   // K value -> panel slot (src coded as csrc)
+    int nbdg = 0;
+    const int32_t *bdg_slot = nullptr, *bdg_col = nullptr;   // diagonal slots (static regularisation)
+    int nrg = 0;
+    const int32_t *rg_tgt = nullptr, *rg_ptr = nullptr, *rg_idx = nullptr;   // root entry <- inbox slots
+    const int32_t *rv_ptr = nullptr, *rv_idx = nullptr;      // root row <- vector-inbox slots (W + 1)
 };
 
 // Per-instance data (device pointers, instance-major) and settings.
