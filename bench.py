@@ -77,6 +77,18 @@ def workload(config):
     return spec, desc
 
 
+def common_config(config, eps, prob=None):
+    """The config keys both arms report (same workload, same generator, same sizes)."""
+    from paper_2412_19027_b200 import generators as G
+    spec, desc = workload(config)
+    prob = prob if prob is not None else (G.build_instances(config, 0, 1)[0] if "instances" in spec else G.build(config))
+    out = {"workload": desc, "config": config, "generator": f"generators.{spec['gen']}(seed, **{spec['kwargs']})",
+           "n": prob.n, "m": prob.m, "nnz_A": prob.A.nnz, "precision": spec["precision"], "eps_feas": eps}
+    if "instances" in spec:
+        out["instances"] = spec["instances"]
+    return out
+
+
 def settings_for(config, eps):
     from paper_2412_19027_b200 import generators as G
     from paper_2412_19027_b200.settings import SolverSettings
@@ -311,11 +323,13 @@ def peaks():
 
 
 def ncu_traffic(config):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    """DRAM bytes per sweep pair of the dominant kernel class from the committed ncu
+    capture (profiles/ncu_traffic.json, tools/ncu_sweeps.sh + tools/ncu_traffic.py), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(config)
+            v = json.load(f).get(config)
+        return v if isinstance(v, dict) else None
     except Exception:
         return None
 
@@ -412,9 +426,11 @@ def run_batch(args):
         "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
-        "config": {"workload": desc, "config": args.config, "instances": n_all, "instances_per_gpu": len(probs),
-                   "n": info["n"], "m": info["m"], "nnz_L": info["nnz_l"], "smem_bytes_per_cta": info["smem_bytes"],
-                   "eps_feas": args.eps, "status": statuses, "iterations_total": iters_all,
+        "config": {**common_config(args.config, args.eps, probs[0]), "instances": n_all,
+                   "instances_per_gpu": len(probs), "nnz_L": info["nnz_l"],
+                   "smem_bytes_per_cta": info["smem_bytes"], "cta_factorisation": bool(info["cta_factor"]),
+                   "root_width": info["root_width"], "leaf_groups": info["groups"],
+                   "status": statuses, "iterations_total": iters_all,
                    "instances_per_s": n_all * args.steps / dev_s, "setup_s": setup,
                    "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"instance shards x{world}, no collective on the solve path"},
@@ -427,11 +443,23 @@ def run_batch(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            impl, r = cpu_sample(args)
-            line["cpu_baseline"] = {"value": r["iterations"] / r["solve_s"], "unit": UNIT, "cores": 1, "kind": impl,
-                                    "sample": f"{r['instances']} instances solved sequentially by "
-                                              f"{'the unmodified reference conic_ipm' if impl == 'reference' else 'the oracle'}"
-                                              f" (setup excluded), 1 thread of a {os.cpu_count()}-core host"}
+            # the reference's own bench --jobs mode (bench.py:98-113): one worker process per
+            # host core over a bounded sample of the instances; the single-core rate beside it
+            procs = os.cpu_count() or 1
+            if not args.cpu_instances:
+                args.cpu_instances = 32 * procs
+            impl, res = run_cpu(args, args.cpu_iters, 1, procs=procs)
+            rj = res[0]
+            args.cpu_instances = 64
+            _, res1 = run_cpu(args, args.cpu_iters, 1, procs=1)
+            r1 = res1[0]
+            who = 'the unmodified reference conic_ipm' if impl == 'reference' else 'the oracle'
+            line["cpu_baseline"] = {"value": rj["iterations"] / rj["solve_s"], "unit": UNIT, "cores": procs,
+                                    "kind": impl,
+                                    "sample": f"{rj['instances']} instances over {procs} worker processes "
+                                              f"(the reference's bench --jobs mode) by {who}, setup excluded",
+                                    "single_core": {"value": r1["iterations"] / r1["solve_s"], "cores": 1,
+                                                    "sample": f"{r1['instances']} instances, 1 process"}}
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"failed: {e}"[:300]}
@@ -509,6 +537,10 @@ def run_ours(args):
     ctx.call("cipm_kernel_stats", pdbl(kst))
     ctx.call("cipm_profile", 0)
     kst_iters = max(1, prof_res.iterations)
+    # the other kernel classes of the north star (fused residual SpMV, KKT matvec, cone
+    # scaling per family) timed at the final iterate with CUDA events on the solver stream
+    kcls = np.zeros(12)
+    ctx.call("cipm_kernel_classes", 20, pdbl(kcls))
 
     total_s = sum(step_ms) / 1e3
     total_it = sum(iters)
@@ -571,10 +603,22 @@ def run_ours(args):
                "avg_ms": fac_ms / fac_n, "bytes_per_launch": bytes_fac,
                "share_of_step": fac_ms / (sum(step_ms) / len(step_ms) or 1),
                "tflops": info["flops"] / (fac_ms / fac_n / 1e3) / 1e12}
+    kernels = {}
+    for k, name in enumerate(("residual_spmv (resid_n + resid_m)", "kkt_matvec (kkt_res_n + kkt_res_m + apply_H)",
+                              "scaling_nonneg (nn_scaling)", "scaling_soc (soc_scaling)",
+                              "scaling_exp_pow (nsym_scaling)", "scaling_psd (psd_scaling)")):
+        ms_k, by_k = kcls[2 * k], kcls[2 * k + 1]
+        if ms_k > 0:
+            gbs = by_k / (ms_k / 1e3) / 1e9
+            kernels[name] = {"us": ms_k * 1e3, "bytes": by_k, "achieved_gbs": gbs, "frac": gbs / hbm}
+    traffic = ncu_traffic(args.config)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic(args.config), "peak_source": peak_kind, "dominant": dom,
+            "traffic": (traffic or {}).get("bytes") if isinstance(traffic, dict) else traffic,
+            "traffic_source": (traffic or {}).get("source") if isinstance(traffic, dict) else None,
+            "peak_source": peak_kind, "dominant": dom,
             "factor_ms_avg": fac_ms / fac_n if fac_n else None,
-            "solve_ms_avg_per_pair": sol_ms / sol_n if sol_n else None}
+            "solve_ms_avg_per_pair": sol_ms / sol_n if sol_n else None,
+            "kernels": kernels}
     if "tflops" in dom and cfg.precision == "full":
         # factorisation-dominated (dense tail on the FP64 tensor pipe): the tensor roofline,
         # against a DGEMM measured here (MEASURED_PEAKS.json has no FP64 figure)
@@ -590,8 +634,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 iterate / f32 LDL' + f64 refinement" if cfg.precision == "mixed" else "f64",
         "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
-        "config": {"workload": desc, "config": args.config, "n": prob.n, "m": prob.m, "nnz_A": prob.A.nnz,
-                   "precision": cfg.precision, "eps_feas": args.eps, "status": sorted(statuses),
+        "config": {**common_config(args.config, args.eps, prob), "status": sorted(statuses),
                    "iterations_per_solve": total_it / max(1, args.steps),
                    "solve_time_s": sum(step_ms) / 1e3 / args.steps,
                    "setup_s": solver.setup_seconds, "nnz_L": nnz_l, "supernodes": info["nsuper"],
@@ -655,8 +698,7 @@ def run_reference(args):
             "scaling": "strong" if batched else "weak", "vs_baseline": None,
             "dtype": "f64 iterate / f32 LDL' + f64 refinement" if G_precision(args.config) == "mixed" else "f64",
             "impl": "reference", "data": "synthetic (seeded generator, paper_2412_19027_b200/generators.py)",
-            "config": {"workload": desc, "config": args.config, "eps_feas": args.eps,
-                       "status": sorted({r["status"] for r in timed}),
+            "config": {**common_config(args.config, args.eps), "status": sorted({r["status"] for r in timed}),
                        "iterations_per_solve": it_total / max(1, len(timed)),
                        "setup_s": timed[0]["setup_s"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs if batched else 1, "kind": impl,

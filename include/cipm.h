@@ -190,6 +190,10 @@ int cipm_membership(cipm_ctx *ctx, const double *s, const double *z, int *in_con
  * since the context was created (num_numeric), out[1] = pivots bumped by the dynamic
  * regularisation in the last factorisation (last_bumped_pivots) */
 int cipm_kkt_counters(cipm_ctx *ctx, int64_t *out);
+/* bench roofline: per-launch time (ms) and algorithmic bytes of the kernel classes
+ * at the current iterate, out[12] = {residual SpMV, KKT matvec, scaling nonneg, SOC,
+ * exp+pow, PSD} x {ms, bytes}; reps timed launches each (CUDA events, context stream) */
+int cipm_kernel_classes(cipm_ctx *ctx, int reps, double *out);
 /* host<->device bytes moved by the API since the last reset (bench e2e accounting) */
 int cipm_io_bytes(cipm_ctx *ctx, int64_t *h2d, int64_t *d2h, int reset);
 /* kernel launches issued since the last reset (bench accounting) */

@@ -21,6 +21,7 @@ void k_nsym_resolve(Ctx& c);
 void k_step_store(Ctx& c, int which);
 void k_nb_resolve(Ctx& c, int g0, int nk);
 void k_kkt_residual_one(Ctx& c, int q);
+void k_kkt_matvec_only(Ctx& c, int q);
 void k_refine_init_one(Ctx& c, int q);
 void k_copy(Ctx& c, const double* src, double* dst, int64_t n);
 int factor_grid(Ctx& c);
@@ -384,6 +385,8 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         psd_deg += (double)sd;
     }
     c.hblk_total = hp;
+    for (int64_t i = 0; i < c.nsoc; ++i) c.host_blocks.emplace_back(0, (int)d->soc_dim[i]);
+    for (int64_t i = 0; i < c.npsd; ++i) c.host_blocks.emplace_back(3, (int)d->psd_side[i]);
     c.psd_mat_total = mp;
     c.psd_lam_total = lp;
     c.nu = (double)c.nonneg_dim + (double)c.nsoc + 3.0 * (double)c.nsym + psd_deg;
@@ -530,6 +533,27 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(upload(c, &c.sym.start_fac_cta, S.start_fac_cta.data(), (int64_t)S.start_fac_cta.size()));
     TRY(upload(c, &c.sym.vin_col, S.vin_col.data(), (int64_t)S.vin_col.size()));
     TRY(upload(c, &c.sym.tiny, S.tiny.data(), (int64_t)S.tiny.size()));
+    {
+        const int64_t nt = (int64_t)S.tiny.size();
+        std::vector<int32_t> td((size_t)std::max<int64_t>(nt, 1) * 4), tr((size_t)std::max<int64_t>(nt, 1));
+        for (int64_t k = 0; k < nt; ++k) {
+            const int32_t J = S.tiny[k];
+            const int32_t w = S.sn_col[J + 1] - S.sn_col[J], r = (int32_t)(S.sn_rptr[J + 1] - S.sn_rptr[J]);
+            if (S.sn_loff[J] > INT32_MAX || S.cv_off[J] > INT32_MAX) {
+                cipm_ctx_destroy(h);
+                return CIPM_E_DIM;
+            }
+            td[4 * k] = S.sn_col[J];
+            td[4 * k + 1] = (int32_t)S.sn_loff[J];
+            td[4 * k + 2] = (int32_t)S.cv_off[J];
+            td[4 * k + 3] = w | (r << 8);
+            tr[k] = (int32_t)S.sn_rptr[J];
+        }
+        int32_t* tdp = nullptr;
+        TRY(upload(c, &tdp, td.data(), (int64_t)td.size()));
+        c.sym.tdesc = reinterpret_cast<int4*>(tdp);
+        TRY(upload(c, &c.sym.trptr, tr.data(), (int64_t)tr.size()));
+    }
     TRY(upload(c, &c.sym.bwd_order, S.bwd_order.data(), (int64_t)S.bwd_order.size()));
     c.sym.ninbox = S.cb_off[S.nsuper];
     c.sym.nv = S.cv_off[S.nsuper];
@@ -1047,6 +1071,60 @@ int cipm_kkt_counters(cipm_ctx* h, int64_t* out) {
     out[0] = c.num_numeric;
     out[1] = bumps;
     return CIPM_OK;
+}
+
+// Kernel-class timing at the current iterate (bench roofline): CUDA events on the
+// context stream around `reps` back-to-back launches of each class; out[2k] = ms
+// per launch, out[2k+1] = algorithmic bytes per launch (SURVEY.md §8d formulas,
+// 8-byte values, 4-byte indices).  Classes: 0 fused residual SpMV (resid_n +
+// resid_m), 1 KKT refinement matvec r = b - K x (one right-hand side), 2-5 the
+// scaling update of the nonneg / SOC / exp+pow / PSD family.
+int cipm_kernel_classes(cipm_ctx* h, int reps, double* out) {
+    if (!h || !out || reps < 1) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    cudaEvent_t e0, e1;
+    CIPM_CUDA(cudaEventCreate(&e0));
+    CIPM_CUDA(cudaEventCreate(&e1));
+    auto timed = [&](auto&& fn) -> double {
+        fn();                                             // warm
+        cudaEventRecord(e0, c.stream);
+        for (int r = 0; r < reps; ++r) fn();
+        cudaEventRecord(e1, c.stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        return (double)ms / reps;
+    };
+    const double n = (double)c.n, m = (double)c.m, dim = (double)c.dim;
+    const double nnzp = (double)c.p_nnz, nnza = (double)c.a_nnz;
+    for (int k = 0; k < 12; ++k) out[k] = 0.0;
+    out[0] = timed([&] { k_residuals(c); });
+    out[1] = 12.0 * (nnzp + 2.0 * nnza) + 8.0 * (3.0 * n + 4.0 * m);
+    // one refinement matvec on right-hand side 0 (rstate forced active for the timing)
+    CIPM_CUDA(cudaMemsetAsync(c.rstate, 0, sizeof(double) * 8, c.stream));
+    out[2] = timed([&] { k_kkt_matvec_only(c, 0); });
+    out[3] = 12.0 * (nnzp + 2.0 * nnza) + 8.0 * (double)c.hblk_total + 8.0 * (double)c.nonneg_dim + 24.0 * dim;
+    // scaling families
+    double soc_bytes = 0.0, psd_bytes = 0.0;
+    {
+        for (size_t i = 0; i < c.host_blocks.size(); ++i) {
+            const double d = (double)c.host_blocks[i].second;
+            const int kind = c.host_blocks[i].first;
+            if (kind == 0) soc_bytes += 2 * 8 * d + 2 * 8 * d + 8 + 8 * d * (d + 1) / 2;
+            if (kind == 3) {
+                const double sd = d;                      // side
+                const double sv = sd * (sd + 1) / 2;
+                psd_bytes += 2 * 8 * sv + 3 * 8 * sd * sd + 8 * sd + 8 * sv * (sv + 1) / 2;
+            }
+        }
+    }
+    if (c.nonneg_dim) { out[4] = timed([&] { k_update_scaling_family(c, 0); }); out[5] = 40.0 * (double)c.nonneg_dim; }
+    if (c.nsoc) { out[6] = timed([&] { k_update_scaling_family(c, 1); }); out[7] = soc_bytes; }
+    if (c.nsym) { out[8] = timed([&] { k_update_scaling_family(c, 2); }); out[9] = 288.0 * (double)c.nsym; }
+    if (c.npsd) { out[10] = timed([&] { k_update_scaling_family(c, 3); }); out[11] = psd_bytes; }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return sync_err(c);
 }
 
 int cipm_io_bytes(cipm_ctx* h, int64_t* h2d, int64_t* d2h, int reset) {

@@ -724,6 +724,26 @@ inline int warp_grid(int64_t nwarps) { return grid_for(nwarps * 32); }
 
 // ---------------------------------------------------------------------------
 
+// one family's scaling update (bench / profiling: per-family timing); fam 0 nonneg, 1 SOC, 2 exp/pow, 3 PSD
+void k_update_scaling_family(Ctx& c, int fam) {
+    if (fam == 0 && c.nonneg_dim) {
+        nn_scaling<<<grid_for(c.nonneg_dim), kThreads, 0, c.stream>>>(c.s, c.z, c.nn_h, c.nn_w, c.nn_lam,
+                                                                      c.zero_dim, c.nonneg_dim, c.err);
+        c.launches++;
+    }
+    if (fam == 1 && c.nsoc) {
+        soc_scaling<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.s, c.z, c.soc_w, c.soc_lam,
+                                                                  c.soc_eta, c.hv, c.err);
+        c.launches++;
+    }
+    if (fam == 2 && c.nsym) {
+        nsym_scaling<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.sc, c.ns_h, c.ns_grad,
+                                                                  c.ns_hess, c.ns_zt, c.hv, c.err);
+        c.launches++;
+    }
+    if (fam == 3 && c.npsd) PSD_DISPATCH(psd_scaling, psd_args(c), c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+}
+
 void k_update_scaling(Ctx& c) {
     if (c.nonneg_dim) {
         nn_scaling<<<grid_for(c.nonneg_dim), kThreads, 0, c.stream>>>(c.s, c.z, c.nn_h, c.nn_w, c.nn_lam,

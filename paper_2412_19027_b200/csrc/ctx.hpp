@@ -42,7 +42,7 @@ struct DevSymbolic {
     int64_t* irow_ptr = nullptr;
     int32_t* inbox_tgt = nullptr;
     int64_t* cv_off = nullptr;
-    int64_t* vpush_pos = nullptr;
+    int32_t* vpush_pos = nullptr;    // int32 on the device (half the push-position traffic)
     int64_t* vcol_ptr = nullptr;
     int64_t *vt_lo = nullptr, *vt_hi = nullptr, *vn_lo = nullptr, *vn_hi = nullptr;
     int32_t* tfold_cols = nullptr;
@@ -55,6 +55,8 @@ struct DevSymbolic {
     int32_t* start_fac_cta = nullptr;
     uint8_t* vin_col = nullptr;
     int32_t* tiny = nullptr;
+    int4* tdesc = nullptr;           // tiny leaves {c0, loff, cvo, w | r << 8}
+    int32_t* trptr = nullptr;        // tiny leaves: sn_rptr
     int32_t* bwd_order = nullptr;
     int64_t nnz_storage = 0;
     int64_t ninbox = 0, nv = 0;
@@ -198,6 +200,7 @@ struct Ctx {
     bool use_graphs = true;
 
     std::vector<void*> allocations;
+    std::vector<std::pair<int, int>> host_blocks;   // (kind 0 SOC dim / 3 PSD side) for bench byte counts
 };
 
 inline cudaEvent_t pooled_event(Ctx& c, size_t idx) {
@@ -226,6 +229,7 @@ void k_mu_candidates(Ctx& c, int k0, int nk, double mu_fixed = -1.0);
 void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs);
 // cones.cu
 void k_update_scaling(Ctx& c);
+void k_update_scaling_family(Ctx& c, int fam);
 void k_scatter_h(Ctx& c);
 void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta,
                const double* skip = nullptr);

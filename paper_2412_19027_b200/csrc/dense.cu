@@ -447,7 +447,7 @@ struct TailSolveArgs {
     const int32_t* rows;       // sn_rows + r0 (permuted row indices)
     const int64_t* vn_lo;      // non-tiny vector-inbox entries of each column (tiny ones are folded)
     const int64_t* vn_hi;
-    const int64_t* vpush_pos;
+    const int32_t* vpush_pos;
     int* flags;                // nbd flags
     int* ticket;
     int* done;                 // backward: solve-done flag of the supernode (persistent-kernel protocol)

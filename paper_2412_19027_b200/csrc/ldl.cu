@@ -795,7 +795,7 @@ struct SolveArgs {
     int64_t dim;
     int64_t nv;          // vector inbox length per right-hand side
     const int32_t* sn_rows;
-    const int64_t* vpush_pos;
+    const int32_t* vpush_pos;
     const uint8_t* vin_col;
     int32_t* count;      // forward: children done; backward: done flags
     int32_t* ticket;
@@ -804,6 +804,8 @@ struct SolveArgs {
     int slice;           // per-warp shared-memory panel slice (elements)
     const double* rstate;   // refinement state: skip right-hand sides that have converged
     const int8_t* sf;       // per supernode: 1 = panel in solve form (M), 0 = plain L (solve_form_kernel)
+    const int4* tdesc;      // tiny leaves, compact: {c0, loff, cvo, w | r << 8}
+    const int32_t* trptr;   // tiny leaves: offset of the row list in sn_rows
 };
 
 // warp-cooperative sums of the vector inbox of one supernode's columns (entries
@@ -1142,10 +1144,11 @@ constexpr int SW = 8;   // warps per solve CTA
 // staged in shared memory by one bulk copy, continuation to the parent
 // tiny leaf, forward: x_J = L11^-1 b_J (no inbox below a leaf), push L_off x_J
 template <typename T, int W>
-__device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+__device__ __forceinline__ int fwd_tiny_w(const int4 td, const SolveArgs& a, const T* __restrict__ lval,
                                           T* x, T* vin) {
-    const int c0 = d32[0], r = d32[2], parent = d32[3];
-    const int64_t loff = a.desc64[(int64_t)J * 8], cvo = a.desc64[(int64_t)J * 8 + 1];
+    // compact tiny-leaf descriptor {c0, loff, cvo, w | r << 8} (16 bytes instead of 96)
+    const int c0 = td.x, r = (td.w >> 8) & 0xff, parent = -1;
+    const int64_t loff = (uint32_t)td.y, cvo = (uint32_t)td.z;
     const T* L = lval + loff;
     T p[W][16];
 #pragma unroll
@@ -1181,13 +1184,13 @@ __device__ __forceinline__ int fwd_tiny_w(int J, const int32_t* d32, const Solve
 }
 
 template <typename T>
-__device__ __forceinline__ int fwd_tiny_lane(int J, const SolveArgs& a, const T* __restrict__ lval, T* x, T* vin) {
-    const int32_t* d32 = a.desc32 + (int64_t)J * 8;
-    switch (d32[1]) {
-        case 1: return fwd_tiny_w<T, 1>(J, d32, a, lval, x, vin);
-        case 2: return fwd_tiny_w<T, 2>(J, d32, a, lval, x, vin);
-        case 3: return fwd_tiny_w<T, 3>(J, d32, a, lval, x, vin);
-        default: return fwd_tiny_w<T, 4>(J, d32, a, lval, x, vin);
+__device__ __forceinline__ int fwd_tiny_lane(int64_t k, const SolveArgs& a, const T* __restrict__ lval, T* x, T* vin) {
+    const int4 td = __ldg(a.tdesc + k);
+    switch (td.w & 0xff) {
+        case 1: return fwd_tiny_w<T, 1>(td, a, lval, x, vin);
+        case 2: return fwd_tiny_w<T, 2>(td, a, lval, x, vin);
+        case 3: return fwd_tiny_w<T, 3>(td, a, lval, x, vin);
+        default: return fwd_tiny_w<T, 4>(td, a, lval, x, vin);
     }
 }
 
@@ -1289,7 +1292,7 @@ __global__ void __launch_bounds__(128) fwd_tiny_kernel(SolveArgs a0, const T* __
     resolve_act(a.rstate, a.act0, a.act1);
     if (!a.act0 && !a.act1) return;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < a.ntiny) fwd_tiny_lane(a.tiny[k], a, lval, x, vin);
+    if (k < a.ntiny) fwd_tiny_lane(k, a, lval, x, vin);
 }
 
 template <typename T>
@@ -1330,7 +1333,7 @@ __global__ void __launch_bounds__(SW * 32, 3) forward_kernel(SolveArgs a0, const
 // backward sweep L' x = D^-1 y: warp per supernode, reverse topological order
 // tiny leaves, backward: one thread each, launched after the persistent sweep
 template <typename T, int W>
-__device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+__device__ __forceinline__ void bwd_tiny_w(const int4 td, int64_t rptr, const SolveArgs& a, const T* __restrict__ lval,
                                            const T* __restrict__ dvec, T* x);
 
 template <typename T>
@@ -1341,22 +1344,22 @@ __global__ void __launch_bounds__(128) bwd_tiny_kernel(SolveArgs a0, const T* __
     if (!a.act0 && !a.act1) return;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= a.ntiny) return;
-    const int J = a.tiny[k];
-    const int32_t* d32 = a.desc32 + (int64_t)J * 8;
-    switch (d32[1]) {
-        case 1: bwd_tiny_w<T, 1>(J, d32, a, lval, dvec, x); break;
-        case 2: bwd_tiny_w<T, 2>(J, d32, a, lval, dvec, x); break;
-        case 3: bwd_tiny_w<T, 3>(J, d32, a, lval, dvec, x); break;
-        default: bwd_tiny_w<T, 4>(J, d32, a, lval, dvec, x); break;
+    const int4 td = __ldg(a.tdesc + k);
+    const int64_t rptr = (uint32_t)__ldg(a.trptr + k);
+    switch (td.w & 0xff) {
+        case 1: bwd_tiny_w<T, 1>(td, rptr, a, lval, dvec, x); break;
+        case 2: bwd_tiny_w<T, 2>(td, rptr, a, lval, dvec, x); break;
+        case 3: bwd_tiny_w<T, 3>(td, rptr, a, lval, dvec, x); break;
+        default: bwd_tiny_w<T, 4>(td, rptr, a, lval, dvec, x); break;
     }
 }
 
 // tiny leaf, backward: x_J = L11^-T (D^-1 x_J - L_off' x_off) once the parent is final
 template <typename T, int W>
-__device__ __forceinline__ void bwd_tiny_w(int J, const int32_t* d32, const SolveArgs& a, const T* __restrict__ lval,
+__device__ __forceinline__ void bwd_tiny_w(const int4 td, int64_t rptr, const SolveArgs& a, const T* __restrict__ lval,
                                            const T* __restrict__ dvec, T* x) {
-    const int c0 = d32[0], r = d32[2], parent = d32[3];
-    const int64_t loff = a.desc64[(int64_t)J * 8], rptr = a.desc64[(int64_t)J * 8 + 7];
+    const int c0 = td.x, r = (td.w >> 8) & 0xff, parent = -1;
+    const int64_t loff = (uint32_t)td.y;
     const T* L = lval + loff;
     T p[W][16];
 #pragma unroll
@@ -1524,6 +1527,8 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     a.slice = (int)c.solve_slice;
     a.rstate = c.rstate;
     a.sf = c.sf_flag;
+    a.tdesc = c.sym.tdesc;
+    a.trptr = c.sym.trptr;
     return a;
 }
 

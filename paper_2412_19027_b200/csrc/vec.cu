@@ -619,6 +619,19 @@ void k_kkt_residual_one(Ctx& c, int q) {
     c.launches += 2;
 }
 
+// the matvec part of k_kkt_residual_one only (bench timing: no controller state change)
+void k_kkt_matvec_only(Ctx& c, int q) {
+    const double* xv = c.rx + (int64_t)q * c.dim;
+    const double* bv = c.rb + (int64_t)q * c.dim;
+    double* rv = c.rr + (int64_t)q * c.dim;
+    const double* st = c.rstate + 8 * q;
+    kkt_res_n<<<grid_for(c.n), kThreads, 0, c.stream>>>(c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, xv, bv, rv,
+                                                        c.n, st);
+    kkt_res_m<<<grid_for(c.m), kThreads, 0, c.stream>>>(c.a_rp, c.a_ci, c.a_v, xv, bv, rv, c.n, c.m, st);
+    c.launches += 2;
+    k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0, st + 4);
+}
+
 void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs) {
     refine_continue<<<1, 1, 0, c.stream>>>(h, c.rstate, nrhs, c.refine_iter, c.refine_max);
     c.launches++;

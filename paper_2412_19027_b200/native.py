@@ -99,6 +99,7 @@ _SIGS = {
     "cipm_membership": ([c_void_p, P_DBL, P_DBL, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
                         ctypes.c_int),
     "cipm_kkt_counters": ([c_void_p, P_I64], ctypes.c_int),
+    "cipm_kernel_classes": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
     "cipm_launch_count": ([c_void_p, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_kernel_times": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
