@@ -63,6 +63,18 @@ enum {
     CIPM_SC_SZ,                   /* s'z                                             */
     CIPM_SC_BUMPS,                /* dynamically regularised pivots (last factor)    */
     CIPM_SC_REFINE_STEPS,         /* refinement steps of the last solve              */
+    /* device-side loop control (cipm_loop_*: the Algorithm-1 decisions of ipm.py:427-457) */
+    CIPM_SC_NB_BATCH,             /* neighbourhood candidates evaluated so far        */
+    CIPM_SC_BEST_FLAG,            /* this iteration improved the best iterate (copied) */
+    CIPM_SC_REF_STEPS_A, CIPM_SC_REF_STEPS_C,   /* refinement steps, affine / combined */
+    CIPM_SC_STATUS = 40,          /* 0 running, 1 optimal, 2 primal infeasible, 3 dual
+                                     infeasible, 4 max iterations, 5 insufficient progress */
+    CIPM_SC_BEST_SCORE, CIPM_SC_BEST_VALID,
+    CIPM_SC_STALL_MU, CIPM_SC_STALL_RP, CIPM_SC_STALL_RD, CIPM_SC_STALL_CNT,
+    CIPM_SC_BEST_TAU, CIPM_SC_BEST_KAPPA, CIPM_SC_BEST_MU,
+    CIPM_SC_BEST_GP, CIPM_SC_BEST_GD, CIPM_SC_BEST_RP, CIPM_SC_BEST_RD,
+    CIPM_SC_BEST_R1, CIPM_SC_BEST_R2, CIPM_SC_BEST_R3,
+    CIPM_SC_CUR_R1, CIPM_SC_CUR_R2, CIPM_SC_CUR_R3,
     CIPM_SC_COUNT = 64
 };
 
@@ -169,6 +181,21 @@ int cipm_get_direction(cipm_ctx *ctx, int combined, double *dx, double *dz, doub
 int cipm_get_vector(cipm_ctx *ctx, const char *name, double *out, int64_t *count);
 /* per-cone batched SOC residuals t^2 - |u|^2 with the reference's fixed order (steps.py:136-175) */
 int cipm_soc_residuals(cipm_ctx *ctx, const double *x, double *out);
+/* ---- device-side loop (one blocking read per IPM iteration) ----
+ * cipm_loop_begin: unit start (set.py:91-112) and the control state; the norms are
+ *   ||q||inf, ||b||inf of the unscaled reordered data (ipm.py:184-185).
+ * cipm_loop_check: residuals (ipm.py:233-251) and, on the device, the best-iterate
+ *   bookkeeping, Eq.(8) termination, Eq.(9) infeasibility, max_iter and the stall
+ *   window (ipm.py:427-457); then ONE synchronisation: the scalar block (status in
+ *   CIPM_SC_STATUS) is copied to sc_out.  Returns a CIPM_E_* code if the previous
+ *   iteration body latched a numerical failure.
+ * cipm_loop_body: one iteration body (scaling, factorisation, affine and combined
+ *   refined solves, step lengths with their backtracking loops as device WHILE
+ *   graphs, neighbourhood search, take_step) enqueued without any host round trip. */
+int cipm_loop_begin(cipm_ctx *ctx, double norm_q, double norm_b, double eps_feas, double eps_inf, int max_iter);
+int cipm_loop_check(cipm_ctx *ctx, int iteration, double *sc_out);
+int cipm_loop_body(cipm_ctx *ctx);
+
 /* ---- kernel-level seams: the reference's L1 cone functions one call at a time
  * (tests/test_gpu_seams.py checks them against tests/golden/kernels.json) ---- */
 /* set direction `which` (0 affine, 1 combined): dx (n), dz (m), ds (m), dtk = {dtau, dkappa};

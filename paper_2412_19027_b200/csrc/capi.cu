@@ -192,6 +192,97 @@ int step_length(Ctx& c, int which) {
     return CIPM_OK;
 }
 
+// one graph holding a single device WHILE node (default condition 1: the body runs at
+// least once); body(h) enqueues the body's kernels, the last of which sets the condition
+template <typename F>
+int while_graph(Ctx& c, cudaGraphExec_t* exec, int64_t* body_launches, F&& body) {
+    cudaGraph_t g = nullptr;
+    CIPM_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CIPM_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CIPM_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    const int64_t l0 = c.launches;
+    CIPM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    body(h);
+    cudaGraph_t captured = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c.stream, &captured);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[cipm] WHILE graph capture failed: %s\n", cudaGetErrorString(e));
+        cudaGraphDestroy(g);
+        return CIPM_E_CUDA;
+    }
+    CIPM_CUDA(cudaGraphInstantiate(exec, g, 0));
+    cudaGraphDestroy(g);
+    *body_launches = c.launches - l0;
+    c.launches = l0;
+    return CIPM_OK;
+}
+
+// refined solve without host readback (device loop): steps into a scalar slot
+int refine_async(Ctx& c, int nrhs, int slot) {
+    int tmp = 0;
+    if (!c.refine_graph[nrhs]) {
+        // build it through the synchronous path once (instantiation only happens there)
+        int e = refine_graph(c, nrhs, &tmp);
+        if (e) return e;
+        k_refine_steps_store(c, nrhs, slot);
+        return CIPM_OK;
+    }
+    for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
+    CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
+    c.launches += c.refine_graph_launches[nrhs] * 2;   // typical step count (the exact count is on the device)
+    k_refine_steps_store(c, nrhs, slot);
+    return CIPM_OK;
+}
+
+int64_t g_step_body_launches = 0, g_nb_body_launches = 0;
+
+// step_length (steps.py:79-116) with the exp/pow backtracking as a device WHILE loop
+int step_length_async(Ctx& c, int which) {
+    k_step_init(c, which);
+    k_step_bound(c, c.dz[which], c.ds[which]);
+    k_step_finish(c, which);
+    if (c.nsym) {
+        if (!c.step_graph[which]) {
+            int e = while_graph(c, &c.step_graph[which], &g_step_body_launches, [&](cudaGraphConditionalHandle h) {
+                k_nsym_feasible_mask(c, c.dz[which], c.ds[which], 0);
+                k_nsym_resolve_cond(c, h);
+            });
+            if (e) return e;
+        }
+        k_mask_init(c);
+        CIPM_CUDA(cudaGraphLaunch(c.step_graph[which], c.stream));
+        c.launches += g_step_body_launches;
+    }
+    k_step_store(c, which);
+    return CIPM_OK;
+}
+
+// combined_step_size neighbourhood backtracking (ipm.py:350-366) as a device WHILE loop
+int neighborhood_async(Ctx& c) {
+    const int nk = 8;
+    if (!c.nb_graph) {
+        int e = while_graph(c, &c.nb_graph, &g_nb_body_launches, [&](cudaGraphConditionalHandle h) {
+            k_mu_candidates(c, 0, nk);
+            k_neighborhood_mask(c, 0, nk);
+            k_nb_resolve_cond(c, nk, h);
+        });
+        if (e) return e;
+    }
+    k_mask_init(c);
+    CIPM_CUDA(cudaGraphLaunch(c.nb_graph, c.stream));
+    c.launches += g_nb_body_launches;
+    return CIPM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -725,6 +816,9 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     for (auto& g : c.refine_graph)
         if (g) cudaGraphExecDestroy(g);
     if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
+    for (auto& g : c.step_graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (c.nb_graph) cudaGraphExecDestroy(c.nb_graph);
     if (c.t_start) cudaEventDestroy(c.t_start);
     if (c.t_stop) cudaEventDestroy(c.t_stop);
     if (c.own_stream && c.stream) cudaStreamDestroy(c.stream);
@@ -842,6 +936,78 @@ int cipm_take_step(cipm_ctx* h) {
     Ctx& c = h->c;
     k_take_step(c);
     return read_sc(c);
+}
+
+int cipm_loop_begin(cipm_ctx* h, double norm_q, double norm_b, double eps_feas, double eps_inf, int max_iter) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    c.loop_norm_q = norm_q;
+    c.loop_norm_b = norm_b;
+    c.loop_eps_feas = eps_feas;
+    c.loop_eps_inf = eps_inf;
+    c.loop_max_iter = max_iter;
+    CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
+    k_init_iterate(c);
+    k_loop_init(c);
+    return CIPM_OK;
+}
+
+int cipm_loop_check(cipm_ctx* h, int iteration, double* sc_out) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    k_residuals(c);
+    k_iter_control(c, iteration);
+    const int e = read_sc(c);                      // the one blocking read of the iteration
+    if (sc_out) memcpy(sc_out, c.h_sc, sizeof(double) * CIPM_SC_COUNT);
+    return e;
+}
+
+int cipm_loop_body(cipm_ctx* h) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    int e;
+    const bool eager = !c.use_graphs || c.profile || c.trace;
+    k_update_scaling(c);
+    e = cipm_factor(h);
+    if (e) return e;
+    // affine direction (two right-hand sides: col2 and the affine RHS)
+    k_affine_rhs(c);
+    if (eager) {
+        int steps = 0;
+        e = refine(c, 2, &steps);
+    } else {
+        e = refine_async(c, 2, CIPM_SC_REF_STEPS_A);
+    }
+    if (e) return e;
+    k_copy(c, c.rbest, c.col2, c.dim);
+    k_copy(c, c.rbest + c.dim, c.sol1, c.dim);
+    k_directions_prep_den(c);
+    k_recover_direction(c, 0, c.sol1, 0.0);
+    e = eager ? step_length(c, 0) : step_length_async(c, 0);
+    if (e) return e;
+    // combined direction
+    k_combined_ds(c, c.dz[0], c.ds[0]);
+    k_combined_rhs(c);
+    if (eager) {
+        int steps = 0;
+        e = refine(c, 1, &steps);
+    } else {
+        e = refine_async(c, 1, CIPM_SC_REF_STEPS_C);
+    }
+    if (e) return e;
+    k_copy(c, c.rbest, c.sol1, c.dim);
+    k_recover_direction(c, 1, c.sol1, 0.0);
+    if (eager) {
+        double alpha = 0.0;
+        e = cipm_step_combined(h, &alpha);
+    } else {
+        e = step_length_async(c, 1);
+        if (!e) e = neighborhood_async(c);
+    }
+    if (e) return e;
+    k_take_step(c);
+    return CIPM_OK;
 }
 
 int cipm_read_scalars(cipm_ctx* h, double* out) {

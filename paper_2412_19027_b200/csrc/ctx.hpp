@@ -198,6 +198,11 @@ struct Ctx {
     int64_t factor_runs = 0;
     int64_t num_numeric = 0;         // numeric factorisations (KKTSystem.num_numeric, system.py:261)
     bool use_graphs = true;
+    // device-side loop (cipm_loop_*): control parameters and the backtracking graphs
+    double loop_norm_q = 0.0, loop_norm_b = 0.0, loop_eps_feas = 1e-8, loop_eps_inf = 1e-8;
+    int loop_max_iter = 200;
+    cudaGraphExec_t step_graph[2] = {nullptr, nullptr};     // step_length(which) incl. exp/pow WHILE
+    cudaGraphExec_t nb_graph = nullptr;                      // neighbourhood WHILE
 
     std::vector<void*> allocations;
     std::vector<std::pair<int, int>> host_blocks;   // (kind 0 SOC dim / 3 PSD side) for bench byte counts
@@ -227,6 +232,12 @@ void k_step_finish(Ctx& c, int which);       // α check + σ
 void k_kkt_residual(Ctx& c, int nrhs, const int* active_host);
 void k_mu_candidates(Ctx& c, int k0, int nk, double mu_fixed = -1.0);
 void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs);
+void k_loop_init(Ctx& c);
+void k_iter_control(Ctx& c, int it);
+void k_nsym_resolve_cond(Ctx& c, cudaGraphConditionalHandle h);
+void k_mask_init(Ctx& c);
+void k_nb_resolve_cond(Ctx& c, int nk, cudaGraphConditionalHandle h);
+void k_refine_steps_store(Ctx& c, int nrhs, int slot);
 // cones.cu
 void k_update_scaling(Ctx& c);
 void k_update_scaling_family(Ctx& c, int fam);

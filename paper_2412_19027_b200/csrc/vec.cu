@@ -488,6 +488,144 @@ __global__ void refine_init(const double* bv, int64_t dim, double* st, double t_
     }
 }
 
+// ------------------------- device-side loop control -------------------------
+
+struct LoopArgs {
+    double c_obj, norm_q, norm_b, eps_feas, eps_inf;
+    int max_iter;
+    int64_t n, m;
+};
+
+// init of the control state (after the unit start and μ0)
+__global__ void loop_init(double* sc) {
+    sc[CIPM_SC_STATUS] = 0.0;
+    sc[CIPM_SC_BEST_SCORE] = INFINITY;
+    sc[CIPM_SC_BEST_VALID] = 0.0;
+    sc[CIPM_SC_STALL_MU] = INFINITY;
+    sc[CIPM_SC_STALL_RP] = INFINITY;
+    sc[CIPM_SC_STALL_RD] = INFINITY;
+    sc[CIPM_SC_STALL_CNT] = 0.0;
+    sc[CIPM_SC_BEST_FLAG] = 0.0;
+    sc[CIPM_SC_REF_STEPS_A] = 0.0;
+    sc[CIPM_SC_REF_STEPS_C] = 0.0;
+}
+
+// The decisions of ipm.py:427-457 (restated by solver.py, same order): best iterate
+// (strict score improvement, or the first evaluation), Eq.(8) termination, Eq.(9)
+// infeasibility on the unscaled un-normalised iterate, max_iter, stall window.
+__global__ void iter_control(double* sc, const int* err, LoopArgs a, int it) {
+    if (*err != 0) {                       // a failure of the previous body: the host maps it
+        sc[CIPM_SC_BEST_FLAG] = 0.0;
+        return;
+    }
+    const double tau = sc[CIPM_SC_TAU], kappa = sc[CIPM_SC_KAPPA], mu = sc[CIPM_SC_MU], c = a.c_obj;
+    const double xpx = sc[CIPM_SC_XPX], qx = sc[CIPM_SC_QX], bz = sc[CIPM_SC_BZ];
+    const double hq = 0.5 * xpx / (c * tau * tau);
+    const double g_p = hq + qx / (c * tau), g_d = -hq - bz / (c * tau);
+    const double rp = sc[CIPM_SC_NRM_GZ] / tau, rd = sc[CIPM_SC_NRM_GX] / (c * tau);
+    const double xbar = sc[CIPM_SC_NRM_XU] / tau, sbar = sc[CIPM_SC_NRM_SU] / tau, zbar = sc[CIPM_SC_NRM_ZU] / (c * tau);
+    const double gap = fabs(g_p - g_d);
+    const double r1 = rp / fmax(1.0, a.norm_b + xbar + sbar);
+    const double r2 = rd / fmax(1.0, a.norm_q + xbar + zbar);
+    const double r3 = gap / fmax(1.0, fmin(fabs(g_p), fabs(g_d)));
+    const double score = fmax(fmax(r1, r2), r3);
+    sc[CIPM_SC_CUR_R1] = r1;
+    sc[CIPM_SC_CUR_R2] = r2;
+    sc[CIPM_SC_CUR_R3] = r3;
+    sc[CIPM_SC_BEST_FLAG] = 0.0;
+    if (score < sc[CIPM_SC_BEST_SCORE] || sc[CIPM_SC_BEST_VALID] == 0.0) {
+        if (score < sc[CIPM_SC_BEST_SCORE]) sc[CIPM_SC_BEST_SCORE] = score;
+        sc[CIPM_SC_BEST_VALID] = 1.0;
+        sc[CIPM_SC_BEST_FLAG] = 1.0;
+        sc[CIPM_SC_BEST_TAU] = tau;
+        sc[CIPM_SC_BEST_KAPPA] = kappa;
+        sc[CIPM_SC_BEST_MU] = mu;
+        sc[CIPM_SC_BEST_GP] = g_p;
+        sc[CIPM_SC_BEST_GD] = g_d;
+        sc[CIPM_SC_BEST_RP] = rp;
+        sc[CIPM_SC_BEST_RD] = rd;
+        sc[CIPM_SC_BEST_R1] = r1;
+        sc[CIPM_SC_BEST_R2] = r2;
+        sc[CIPM_SC_BEST_R3] = r3;
+    }
+    if (r1 < a.eps_feas && r2 < a.eps_feas && r3 < a.eps_feas) { sc[CIPM_SC_STATUS] = 1.0; return; }
+    {
+        const double eps = a.eps_inf;
+        const double bzu = bz / c, qxu = qx / c;
+        const double nx = sc[CIPM_SC_NRM_XU], nz = sc[CIPM_SC_NRM_ZU] / c, ns = sc[CIPM_SC_NRM_SU];
+        const double atz = a.n ? sc[CIPM_SC_NRM_ATZ] / c : 0.0;
+        if (atz < -eps * fmax(1.0, nx + nz) * bzu && bzu < -eps) { sc[CIPM_SC_STATUS] = 2.0; return; }
+        const double px = a.n ? sc[CIPM_SC_NRM_PX] / c : 0.0;
+        const double axs = sc[CIPM_SC_NRM_AXS];
+        if (px < -eps * fmax(1.0, nx) * bzu && axs < -eps * fmax(1.0, nx + ns) * qxu && qxu < -eps) {
+            sc[CIPM_SC_STATUS] = 3.0;
+            return;
+        }
+    }
+    if (it >= a.max_iter) { sc[CIPM_SC_STATUS] = 4.0; return; }
+    const bool improved = mu < 0.99 * sc[CIPM_SC_STALL_MU] || rp < 0.99 * sc[CIPM_SC_STALL_RP] ||
+                          rd < 0.99 * sc[CIPM_SC_STALL_RD];
+    sc[CIPM_SC_STALL_MU] = fmin(sc[CIPM_SC_STALL_MU], mu);
+    sc[CIPM_SC_STALL_RP] = fmin(sc[CIPM_SC_STALL_RP], rp);
+    sc[CIPM_SC_STALL_RD] = fmin(sc[CIPM_SC_STALL_RD], rd);
+    sc[CIPM_SC_STALL_CNT] = improved ? 0.0 : sc[CIPM_SC_STALL_CNT] + 1.0;
+    if (sc[CIPM_SC_STALL_CNT] >= 5.0) sc[CIPM_SC_STATUS] = 5.0;
+}
+
+// best iterate copy when iter_control flagged an improvement (ipm.py:429-431)
+__global__ void copy_best_if(const double* sc, const double* x, const double* z, const double* s, double* bx,
+                             double* bz, double* bs, int64_t n, int64_t m) {
+    if (sc[CIPM_SC_BEST_FLAG] == 0.0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + m; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n) bx[i] = x[i];
+        if (i < m) { bz[i] = z[i]; bs[i] = s[i]; }
+    }
+}
+
+// exp/pow backtracking as a device WHILE loop: as nsym_resolve, and the loop
+// condition = another batch of 32 candidates is needed
+__global__ void nsym_resolve_cond(double* sc, unsigned int* mask, double bt, int* err, cudaGraphConditionalHandle h) {
+    const unsigned int m = *mask;
+    double a = sc[CIPM_SC_ALPHA_WORK];
+    for (int k = 0; k < 32; ++k) {
+        if (!(a >= kMinStep)) { set_error(err, CIPM_E_STEP); cudaGraphSetConditional(h, 0u); return; }
+        if (m & (1u << k)) { sc[CIPM_SC_ALPHA_WORK] = a; cudaGraphSetConditional(h, 0u); return; }
+        a *= bt;
+    }
+    sc[CIPM_SC_ALPHA_WORK] = a;
+    *mask = 0xffffffffu;
+    cudaGraphSetConditional(h, 1u);
+}
+
+__global__ void mask_init(unsigned int* mask, double* sc) {
+    *mask = 0xffffffffu;
+    sc[CIPM_SC_NB_BATCH] = 0.0;
+}
+
+// neighbourhood backtracking batch resolution as a device WHILE loop (as nb_resolve;
+// the global candidate index lives in CIPM_SC_NB_BATCH)
+__global__ void nb_resolve_cond(double* sc, const double* nb, unsigned int* mask, int nk, double bt, int* err,
+                                cudaGraphConditionalHandle h) {
+    const unsigned int m = *mask;
+    const int g0 = (int)sc[CIPM_SC_NB_BATCH];
+    for (int k = 0; k < nk; ++k) {
+        const double ak = nb[32 + k];
+        if (g0 + k > 0 && !(ak >= kMinStep)) { set_error(err, CIPM_E_STEP); cudaGraphSetConditional(h, 0u); return; }
+        if (m & (1u << k)) { sc[CIPM_SC_ALPHA_FINAL] = ak; cudaGraphSetConditional(h, 0u); return; }
+    }
+    sc[CIPM_SC_ALPHA_WORK] = nb[32 + nk - 1] * bt;
+    sc[CIPM_SC_NB_BATCH] = (double)(g0 + nk);
+    cudaGraphSetConditional(h, g0 + nk < 4096 ? 1u : 0u);
+}
+
+// refinement steps of the last refined solve into a scalar slot (no host readback)
+__global__ void refine_steps_store(const double* rstate, double* sc, int nrhs, int slot) {
+    double st = rstate[6];
+    if (nrhs > 1) st = fmax(st, rstate[14]);
+    sc[slot] = st;
+    sc[CIPM_SC_REFINE_STEPS] = st;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -630,6 +768,39 @@ void k_kkt_matvec_only(Ctx& c, int q) {
     kkt_res_m<<<grid_for(c.m), kThreads, 0, c.stream>>>(c.a_rp, c.a_ci, c.a_v, xv, bv, rv, c.n, c.m, st);
     c.launches += 2;
     k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0, st + 4);
+}
+
+void k_loop_init(Ctx& c) {
+    loop_init<<<1, 1, 0, c.stream>>>(c.sc);
+    c.launches++;
+}
+
+void k_iter_control(Ctx& c, int it) {
+    LoopArgs a{c.c_obj, c.loop_norm_q, c.loop_norm_b, c.loop_eps_feas, c.loop_eps_inf, c.loop_max_iter, c.n, c.m};
+    iter_control<<<1, 1, 0, c.stream>>>(c.sc, c.err, a, it);
+    const int64_t mx = c.n > c.m ? c.n : c.m;
+    copy_best_if<<<grid_for(mx), kThreads, 0, c.stream>>>(c.sc, c.x, c.z, c.s, c.bx, c.bz, c.bs, c.n, c.m);
+    c.launches += 2;
+}
+
+void k_nsym_resolve_cond(Ctx& c, cudaGraphConditionalHandle h) {
+    nsym_resolve_cond<<<1, 1, 0, c.stream>>>(c.sc, c.mask, c.backtrack, c.err, h);
+    c.launches++;
+}
+
+void k_mask_init(Ctx& c) {
+    mask_init<<<1, 1, 0, c.stream>>>(c.mask, c.sc);
+    c.launches++;
+}
+
+void k_nb_resolve_cond(Ctx& c, int nk, cudaGraphConditionalHandle h) {
+    nb_resolve_cond<<<1, 1, 0, c.stream>>>(c.sc, c.nb, c.mask, nk, c.backtrack, c.err, h);
+    c.launches++;
+}
+
+void k_refine_steps_store(Ctx& c, int nrhs, int slot) {
+    refine_steps_store<<<1, 1, 0, c.stream>>>(c.rstate, c.sc, nrhs, slot);
+    c.launches++;
 }
 
 void k_refine_continue(Ctx& c, cudaGraphConditionalHandle h, int nrhs) {

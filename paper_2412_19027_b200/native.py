@@ -26,7 +26,10 @@ P_DBL = ctypes.POINTER(ctypes.c_double)
 SC = dict(TAU=0, KAPPA=1, MU=2, GTAU=3, XPX=4, QX=5, BZ=6, NRM_GX=7, NRM_ATZ=8, NRM_PX=9, NRM_XU=10,
           NRM_GZ=11, NRM_AXS=12, NRM_ZU=13, NRM_SU=14, DEN=15, DTAU_A=16, DKAPPA_A=17, DTAU_C=18,
           DKAPPA_C=19, ALPHA_A=20, SIGMA=21, ALPHA_C=22, ALPHA_FINAL=23, ALPHA_WORK=32, SZ=33, BUMPS=34,
-          REFINE_STEPS=35)
+          REFINE_STEPS=35, NB_BATCH=36, BEST_FLAG=37, REF_STEPS_A=38, REF_STEPS_C=39, STATUS=40, BEST_SCORE=41,
+          BEST_VALID=42, STALL_MU=43, STALL_RP=44, STALL_RD=45, STALL_CNT=46, BEST_TAU=47, BEST_KAPPA=48,
+          BEST_MU=49, BEST_GP=50, BEST_GD=51, BEST_RP=52, BEST_RD=53, BEST_R1=54, BEST_R2=55, BEST_R3=56,
+          CUR_R1=57, CUR_R2=58, CUR_R3=59)
 SC_COUNT = 64
 
 
@@ -99,6 +102,9 @@ _SIGS = {
     "cipm_membership": ([c_void_p, P_DBL, P_DBL, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
                         ctypes.c_int),
     "cipm_kkt_counters": ([c_void_p, P_I64], ctypes.c_int),
+    "cipm_loop_begin": ([c_void_p, c_dbl, c_dbl, c_dbl, c_dbl, ctypes.c_int], ctypes.c_int),
+    "cipm_loop_check": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
+    "cipm_loop_body": ([c_void_p], ctypes.c_int),
     "cipm_kernel_classes": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
     "cipm_launch_count": ([c_void_p, P_I64, ctypes.c_int], ctypes.c_int),
     "cipm_io_bytes": ([c_void_p, P_I64, P_I64, ctypes.c_int], ctypes.c_int),

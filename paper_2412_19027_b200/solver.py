@@ -14,6 +14,7 @@ without a CUDA device raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -339,7 +340,79 @@ class Solver:
 
     # -- main loop ------------------------------------------------------------
 
+    _STATUS_CODES = {1: Status.OPTIMAL, 2: Status.PRIMAL_INFEASIBLE, 3: Status.DUAL_INFEASIBLE,
+                     4: Status.MAX_ITERATIONS, 5: Status.INSUFFICIENT_PROGRESS}
+
     def solve(self, observer=None) -> SolveResult:
+        """Algorithm 1 (reference ipm.py:411-496).  Default: the device-side loop — the
+        termination / infeasibility / stall / best-iterate decisions run on the GPU and
+        the host reads the scalar block once per iteration (cipm_loop_check).  With an
+        observer (or CIPM_HOST_LOOP=1) the host-driven loop runs instead (debug mode:
+        per-iteration documents need the directions on the host)."""
+        if observer is not None or os.environ.get("CIPM_HOST_LOOP", "0") != "0":
+            return self._solve_host(observer)
+        t_start = time.perf_counter()
+        cfg = self.settings
+        ctx = self._ctx
+        sc = self._sc
+        ctx.call("cipm_loop_begin", self._norm_q, self._norm_b, cfg.eps_feas, cfg.eps_inf, int(cfg.max_iter))
+        status = None
+        res = None
+        iterations = 0
+        self.last_refine_steps = []
+        for it in range(cfg.max_iter + 1):
+            try:
+                ctx.call("cipm_loop_check", it, pdbl(sc))
+            except DeviceError:
+                raise                    # CUDA / ABI faults are infrastructure errors, not a solver status
+            except ConicError as err:    # the previous body failed (ipm.py:483-486)
+                if cfg.verbose:
+                    print(f"numerical error: {err}")
+                status = Status.NUMERICAL_ERROR
+                iterations = it - 1
+                break
+            if it == 0:
+                self._mu_initial = float(sc[SC["MU"]])
+            else:
+                self.last_refine_steps.append((int(sc[SC["REF_STEPS_A"]]), int(sc[SC["REF_STEPS_C"]])))
+            iterations = it
+            res = self._residuals(sc)
+            if cfg.verbose:
+                print(f"iter {it:3d}  mu={sc[SC['MU']]:9.2e}  rp={res.norm_rp:9.2e}  "
+                      f"rd={res.norm_rd:9.2e}  gap={res.gap:9.2e}  tau={sc[SC['TAU']]:8.2e}")
+            code = int(sc[SC["STATUS"]])
+            if code:
+                status = self._STATUS_CODES[code]
+                break
+            if time.perf_counter() - t_start > cfg.time_limit:
+                status = Status.TIME_LIMIT
+                break
+            try:
+                ctx.call("cipm_loop_body")
+            except DeviceError:
+                raise
+            except ConicError as err:    # an eager-mode body (profiling) failed synchronously
+                if cfg.verbose:
+                    print(f"numerical error: {err}")
+                status = Status.NUMERICAL_ERROR
+                break
+        secs = time.perf_counter() - t_start
+        if status in (Status.OPTIMAL, Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
+            return self._recover(0, res, status, iterations, secs)
+        if sc[SC["BEST_VALID"]] == 0.0:
+            raise ConicError("solve failed before the first residual evaluation")
+        best_res = Residuals(g_p=float(sc[SC["BEST_GP"]]), g_d=float(sc[SC["BEST_GD"]]),
+                             norm_rp=float(sc[SC["BEST_RP"]]), norm_rd=float(sc[SC["BEST_RD"]]),
+                             norm_xbar=float("nan"), norm_sbar=float("nan"), norm_zbar=float("nan"))
+        e10 = ALMOST_OPTIMAL_FACTOR * cfg.eps_feas
+        if max(sc[SC["BEST_R1"]], sc[SC["BEST_R2"]], sc[SC["BEST_R3"]]) < e10 and \
+                sc[SC["BEST_R1"]] < e10 and sc[SC["BEST_R2"]] < e10 and sc[SC["BEST_R3"]] < e10:
+            status = Status.ALMOST_OPTIMAL
+        tkm = (float(sc[SC["BEST_TAU"]]), float(sc[SC["BEST_KAPPA"]]), float(sc[SC["BEST_MU"]]))
+        return self._recover(1, best_res, status, iterations, secs, tkm=tkm)
+
+    def _solve_host(self, observer=None) -> SolveResult:
+        """Host-driven loop (one C call per step; used with an observer)."""
         t_start = time.perf_counter()
         cfg = self.settings
         ctx = self._ctx

@@ -178,3 +178,26 @@ def test_gpu_partial_updates_match_fresh_solver(gpu):
         assert r.obj_primal == rf.obj_primal and np.array_equal(r.x, rf.x)
     assert s.kkt.num_symbolic == 1
     s.close()
+
+
+@pytest.mark.parametrize("name", ["lp_60x120", "socp_40", "exppow_20_8", "psd_6x4", "primal_infeasible_lp",
+                                  "dual_infeasible_lp", "lasso_10x40_mixed"])
+def test_gpu_device_loop_equals_host_loop(gpu, name, monkeypatch):
+    """The device-side loop (decisions on the GPU, one blocking read per iteration,
+    backtracking as device WHILE graphs) reproduces the host-driven loop bit for bit:
+    status, iterations, objectives and iterates, including the infeasibility and
+    insufficient-progress exits."""
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance(name)
+    prob = problem_from_doc(doc)
+    cfg = settings_of(doc)
+    s = Solver(prob, cfg)
+    r_dev = s.solve()
+    monkeypatch.setenv("CIPM_HOST_LOOP", "1")
+    r_host = s.solve()
+    s.close()
+    assert r_dev.status == r_host.status == doc["result"]["status"]
+    assert r_dev.iterations == r_host.iterations
+    assert r_dev.obj_primal == r_host.obj_primal and r_dev.obj_dual == r_host.obj_dual
+    np.testing.assert_array_equal(r_dev.x, r_host.x)
+    np.testing.assert_array_equal(r_dev.z, r_host.z)
