@@ -315,7 +315,7 @@ int cipm_symbolic_create(const cipm_problem_desc* d, int ordering, cipm_symbolic
 }
 
 int cipm_symbolic_create_ex(const cipm_problem_desc* d, int ordering, int64_t nd_leaf, cipm_symbolic** out) {
-    if (!d || !out || ordering < 0 || ordering > 3 || nd_leaf < 0) return CIPM_E_ARG;
+    if (!d || !out || ordering < 0 || ordering > 4 || nd_leaf < 0) return CIPM_E_ARG;
     auto* h = new cipm_symbolic();
     std::vector<int64_t> off, dim;
     blocks_of(d, off, dim);

@@ -17,6 +17,8 @@
 #include <numeric>
 #include <queue>
 #include <thread>
+#include <chrono>
+#include <cstdio>
 #include <utility>
 
 namespace cipm {
@@ -66,8 +68,12 @@ Graph kkt_graph(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, co
     return g;
 }
 
-std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim) {
+// exact minimum degree (the reference's order); `budget` > 0 caps the elimination-
+// graph work (adjacency entries touched): past it the order is abandoned and an
+// empty vector returned (the caller switches to the quotient-graph AMD below)
+std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim, int64_t budget = 0) {
     std::vector<std::vector<int32_t>> adj(dim);
+    int64_t work = 0;
     for (int64_t i = 0; i < dim; ++i) adj[i].assign(g.idx.begin() + g.ptr[i], g.idx.begin() + g.ptr[i + 1]);
     std::vector<char> alive(dim, 1);
     std::vector<int64_t> mark(dim, -1);
@@ -103,6 +109,11 @@ std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim) {
             for (size_t t = 0; t < au.size(); ++t)
                 if (au[t] == v) { au[t] = au.back(); au.pop_back(); break; }
         }
+        if (budget > 0) {
+            work += (int64_t)nbrs.size() * (int64_t)nbrs.size();
+            for (int32_t u : nbrs) work += (int64_t)adj[u].size();
+            if (work > budget) return {};
+        }
         for (size_t a = 0; a < nbrs.size(); ++a) {
             int32_t u = nbrs[a];
             ++stamp;
@@ -119,6 +130,143 @@ std::vector<int32_t> minimum_degree(const Graph& g, int64_t dim) {
         std::vector<int32_t>().swap(adj[v]);
     }
     return perm;
+}
+
+// Approximate minimum degree on the quotient graph (ordering = 4, and the
+// fallback of the exact order when its elimination graph grows too large — e.g.
+// C4's block-simplex rows: the exact order forms every fill clique explicitly).
+// Eliminated variables become elements; a variable keeps its element list and
+// its remaining variable neighbours, so the work is bounded by the quotient
+// graph instead of the filled graph.  Per pivot p (the classic scheme):
+//  * L_p = A_p  U  (U_{e in E_p} L_e) \ {p}; the elements of E_p are absorbed;
+//  * |L_e \ L_p| for every element touching L_p (weights by supervariable size),
+//    elements with L_e subset of L_p absorbed as well (aggressive absorption);
+//  * approximate external degree of i in L_p:
+//      min(d_i + |L_p \ i|, |A_i| + |L_p \ i| + sum_{e in E_i \ p} |L_e \ L_p|, n_left);
+//  * indistinguishable variables (same E_i, same A_i) merged into supervariables,
+//    eliminated together.
+std::vector<int32_t> approx_min_degree(const Graph& g, int64_t dim) {
+    std::vector<std::vector<int32_t>> vars(dim), elems(dim), Le(dim);
+    std::vector<int32_t> nv(dim, 1), snext(dim, -1), stail(dim);
+    std::vector<int8_t> state(dim, 0);             // 0 variable, 1 element, 2 absorbed element
+    std::vector<int64_t> deg(dim), w(dim, 0), wmark(dim, 0), mark(dim, 0);
+    std::iota(stail.begin(), stail.end(), 0);
+    using Item = std::pair<int64_t, int32_t>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int64_t i = 0; i < dim; ++i) {
+        vars[i].assign(g.idx.begin() + g.ptr[i], g.idx.begin() + g.ptr[i + 1]);
+        deg[i] = (int64_t)vars[i].size();
+        heap.emplace(deg[i], (int32_t)i);
+    }
+    std::vector<int32_t> order, Lp;
+    order.reserve(dim);
+    int64_t nel = 0, tag = 0, wtag = 0;
+    while (nel < dim && !heap.empty()) {
+        const Item it = heap.top();
+        heap.pop();
+        const int32_t p = it.second;
+        if (state[p] != 0 || nv[p] == 0 || it.first != deg[p]) continue;
+        // L_p
+        ++tag;
+        mark[p] = tag;
+        Lp.clear();
+        for (int32_t v : vars[p])
+            if (state[v] == 0 && nv[v] > 0 && mark[v] != tag) { mark[v] = tag; Lp.push_back(v); }
+        for (int32_t e : elems[p]) {
+            if (state[e] != 1) continue;
+            for (int32_t v : Le[e])
+                if (state[v] == 0 && nv[v] > 0 && mark[v] != tag) { mark[v] = tag; Lp.push_back(v); }
+            state[e] = 2;
+            std::vector<int32_t>().swap(Le[e]);
+        }
+        for (int32_t v = p; v >= 0; v = snext[v]) order.push_back(v);
+        nel += nv[p];
+        state[p] = 1;
+        std::vector<int32_t>().swap(vars[p]);
+        std::vector<int32_t>().swap(elems[p]);
+        int64_t dLp = 0;
+        for (int32_t v : Lp) dLp += nv[v];
+        Le[p] = Lp;
+        // |L_e \ L_p| of the other elements touching L_p
+        ++wtag;
+        for (int32_t i : Lp)
+            for (int32_t e : elems[i]) {
+                if (state[e] != 1 || e == p) continue;
+                if (wmark[e] != wtag) {
+                    wmark[e] = wtag;
+                    int64_t sz = 0;
+                    auto& L = Le[e];
+                    size_t k = 0;
+                    for (int32_t v : L)
+                        if (state[v] == 0 && nv[v] > 0) { L[k++] = v; sz += nv[v]; }
+                    L.resize(k);
+                    w[e] = sz;
+                }
+                w[e] -= nv[i];
+            }
+        for (int32_t i : Lp)          // aggressive absorption: L_e inside L_p
+            for (int32_t e : elems[i])
+                if (state[e] == 1 && e != p && wmark[e] == wtag && w[e] <= 0) {
+                    state[e] = 2;
+                    std::vector<int32_t>().swap(Le[e]);
+                }
+        // update the variables of L_p
+        const int64_t left = dim - nel;
+        for (int32_t i : Lp) {
+            auto& E = elems[i];
+            size_t k = 0;
+            int64_t ext = 0;
+            for (int32_t e : E)
+                if (state[e] == 1 && e != p) { E[k++] = e; ext += std::max<int64_t>(w[e], 0); }
+            E.resize(k);
+            E.push_back(p);
+            auto& A = vars[i];
+            k = 0;
+            int64_t a = 0;
+            for (int32_t v : A)
+                if (state[v] == 0 && nv[v] > 0 && mark[v] != tag) { A[k++] = v; a += nv[v]; }
+            A.resize(k);
+            const int64_t lp_ext = dLp - nv[i];
+            int64_t d = std::min(deg[i] + lp_ext, a + lp_ext + ext);
+            deg[i] = std::max<int64_t>(0, std::min(d, left - nv[i]));
+        }
+        // supervariables: identical (E_i, A_i) among L_p
+        std::vector<std::pair<uint64_t, int32_t>> hs;
+        hs.reserve(Lp.size());
+        for (int32_t i : Lp) {
+            uint64_t h = 1469598103934665603ull;
+            std::sort(elems[i].begin(), elems[i].end());
+            std::sort(vars[i].begin(), vars[i].end());
+            for (int32_t e : elems[i]) h = (h ^ (uint64_t)(e + 1)) * 1099511628211ull;
+            h = (h ^ 0x9e3779b97f4a7c15ull) * 1099511628211ull;
+            for (int32_t v : vars[i]) h = (h ^ (uint64_t)(v + 1)) * 1099511628211ull;
+            hs.emplace_back(h, i);
+        }
+        std::sort(hs.begin(), hs.end());
+        for (size_t a = 0; a < hs.size();) {
+            size_t b = a;
+            while (b < hs.size() && hs[b].first == hs[a].first) ++b;
+            for (size_t x = a; x < b; ++x) {
+                const int32_t i = hs[x].second;
+                if (nv[i] == 0) continue;
+                for (size_t y = x + 1; y < b; ++y) {
+                    const int32_t j = hs[y].second;
+                    if (nv[j] == 0 || elems[i] != elems[j] || vars[i] != vars[j]) continue;
+                    nv[i] += nv[j];
+                    deg[i] = std::max<int64_t>(0, deg[i] - nv[j]);
+                    nv[j] = 0;
+                    snext[stail[i]] = j;
+                    stail[i] = stail[j];
+                    std::vector<int32_t>().swap(vars[j]);
+                    std::vector<int32_t>().swap(elems[j]);
+                }
+            }
+            a = b;
+        }
+        for (int32_t i : Lp)
+            if (nv[i] > 0) heap.emplace(deg[i], i);
+    }
+    return order;
 }
 
 // Nested dissection by BFS level-structure vertex separators (ordering = 2).
@@ -410,7 +558,10 @@ std::vector<int32_t> auto_order(const Graph& g, int64_t dim, const SymbolicOptio
     }
     std::vector<int32_t> md, nd;
     std::thread t([&] { nd = nested_dissection(g, dim, opt.nd_leaf); });
-    md = minimum_degree(g, dim);
+    // the reference's exact order while its elimination graph stays moderate, else AMD
+    md = minimum_degree(g, dim, opt.md_work_budget_per_nnz * (int64_t)(g.ptr[dim] + dim));
+    const bool amd = (int64_t)md.size() != dim;
+    if (amd) md = approx_min_degree(g, dim);
     t.join();
     int64_t nnz_md = 0, nnz_nd = 0;
     double fl_md = 0, fl_nd = 0;
@@ -420,9 +571,22 @@ std::vector<int32_t> auto_order(const Graph& g, int64_t dim, const SymbolicOptio
         *chosen = 2;
         return nd;
     }
-    *chosen = 0;
+    *chosen = amd ? 4 : 0;
     return md;
 }
+}  // namespace
+
+namespace {
+struct SymTimer {
+    bool on = getenv("CIPM_SYM_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[symbolic] %-28s %8.3f s\n", what, std::chrono::duration<double>(t - t0).count());
+        t0 = t;
+    }
+};
 }  // namespace
 
 int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const int64_t* arp,
@@ -434,6 +598,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     S.dim = dim;
     Graph g = kkt_graph(n, m, prp, pci, arp, aci, nblocks, boff, bdim);
 
+    SymTimer T;
     std::vector<int32_t> perm;
     S.ordering_used = opt.ordering == 3 ? 0 : opt.ordering;
     if (opt.ordering == 1) {
@@ -445,10 +610,13 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         int chosen = 0;
         perm = auto_order(g, dim, opt, &chosen);
         S.ordering_used = chosen;
+    } else if (opt.ordering == 4) {
+        perm = approx_min_degree(g, dim);
     } else {
         perm = minimum_degree(g, dim);
     }
     S.md_perm = perm;
+    T.mark("ordering");
     std::vector<int32_t> iperm(dim);
     for (int64_t k = 0; k < dim; ++k) iperm[perm[k]] = (int32_t)k;
 
@@ -487,6 +655,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     S.sign.resize(dim);
     for (int64_t k = 0; k < dim; ++k) S.sign[k] = perm[k] < n ? 1 : -1;
 
+    T.mark("etree + postorder");
     // column structures of L (strict lower), row-by-row reach through the etree
     std::vector<int64_t> cnt(dim, 0);
     std::vector<int32_t> flag(dim, -1);
@@ -511,6 +680,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     S.flops = 0.0;
     for (int64_t j = 0; j < dim; ++j) S.flops += 2.0 * (double)cnt[j] * (double)cnt[j];
 
+    T.mark("column structures");
     // fundamental supernodes
     std::vector<int32_t> nchild(dim, 0);
     for (int64_t j = 0; j < dim; ++j)
@@ -620,6 +790,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     }
     S.sn_col.push_back((int32_t)dim);
     S.nsuper = ns;
+    T.mark("supernodes + amalgamation");
     // row lists: own columns then union of column structures beyond the last column
     S.sn_rptr.assign(ns + 1, 0);
     S.sn_rows.clear();
@@ -659,6 +830,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
             S.sn_nchild[S.sn_parent[J]]++;
         }
     }
+    T.mark("row lists");
     // update lists (K -> J), K ascending inside each J
     std::vector<int64_t> ucount(ns + 1, 0);
     for (int pass = 0; pass < 2; ++pass) {
@@ -692,6 +864,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         }
     }
     S.n_updates = S.upd_ptr[ns];
+    T.mark("update lists");
     // inbox maps for the push/pull factorisation and forward solve
     {
         S.cb_off.assign(ns + 1, 0);
@@ -707,6 +880,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         // pass 1: count entries per (J, tr) bucket (global row slot = sn_rptr[J] + tr)
         std::vector<int64_t> cnt_row(nrow_all + 1, 0);
         std::vector<int32_t> tr_of;   // per K scratch: local row in the target supernode
+        std::vector<int64_t> src_of;  // inbox slot -> contribution record
         for (int pass = 0; pass < 2; ++pass) {
             std::vector<int64_t> fillp;
             if (pass == 1) {
@@ -714,6 +888,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                 for (int64_t t = 0; t < nrow_all; ++t) S.irow_ptr[t + 1] = S.irow_ptr[t] + cnt_row[t];
                 S.push_pos.assign(nrec, 0);
                 S.inbox_tgt.assign(nrec, 0);
+                src_of.assign(nrec, 0);
                 fillp.assign(S.irow_ptr.begin(), S.irow_ptr.end() - 1);
             }
             for (int32_t K = 0; K < ns; ++K) {
@@ -722,18 +897,29 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                 const int64_t o = (S.sn_rptr[K + 1] - r0) - w;
                 if (o == 0) continue;
                 const int32_t* offrows = S.sn_rows.data() + r0 + w;
-                // target supernode and its local row for every off row
+                // target supernode of every off row; the off rows are ascending, so the
+                // targets are too, and each target's local rows of offrows[b..) come from
+                // ONE merge walk per distinct target (not a search per entry)
                 std::vector<int32_t> tJ(o), tloc(o);
                 for (int64_t a = 0; a < o; ++a) tJ[a] = S.col2sn[offrows[a]];
                 int64_t t = 0;
+                int32_t curJ = -1;
                 for (int64_t b = 0; b < o; ++b) {
                     const int32_t J = tJ[b];
                     const int32_t c0 = S.sn_col[J];
                     const int32_t* rowsJ = S.sn_rows.data() + S.sn_rptr[J];
                     const int64_t rJ = S.sn_rptr[J + 1] - S.sn_rptr[J];
+                    if (J != curJ) {
+                        curJ = J;
+                        int64_t q = std::lower_bound(rowsJ, rowsJ + rJ, offrows[b]) - rowsJ;
+                        for (int64_t a = b; a < o; ++a) {
+                            while (q < rJ && rowsJ[q] < offrows[a]) ++q;
+                            tloc[a] = (int32_t)q;
+                        }
+                    }
                     const int32_t tc = offrows[b] - c0;
                     for (int64_t a = b; a < o; ++a, ++t) {
-                        const int32_t tr = (int32_t)(std::lower_bound(rowsJ, rowsJ + rJ, offrows[a]) - rowsJ);
+                        const int32_t tr = tloc[a];
                         const int64_t slot = S.sn_rptr[J] + tr;
                         if (pass == 0) {
                             cnt_row[slot]++;
@@ -741,30 +927,31 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                             const int64_t e = fillp[slot]++;
                             S.push_pos[S.cb_off[K] + t] = e;
                             S.inbox_tgt[e] = (int32_t)(tc * rJ + tr);
+                            src_of[e] = S.cb_off[K] + t;
                         }
                     }
                 }
             }
         }
-        // within each row bucket: order by target column (stable: source K ascending)
+        // within each row bucket: order by target column, ties by arrival (source K
+        // ascending) — one sort of packed (target, arrival) keys per bucket
         {
-            std::vector<int64_t> inv(nrec);
-            for (int64_t p = 0; p < nrec; ++p) inv[S.push_pos[p]] = p;
-            std::vector<int64_t> idx;
-            std::vector<int32_t> tg;
+            std::vector<uint64_t> key;
             std::vector<int64_t> src;
             for (int64_t t = 0; t < nrow_all; ++t) {
                 const int64_t lo = S.irow_ptr[t], hi = S.irow_ptr[t + 1];
                 if (hi - lo < 2) continue;
-                idx.resize(hi - lo);
-                std::iota(idx.begin(), idx.end(), lo);
-                std::stable_sort(idx.begin(), idx.end(),
-                                 [&](int64_t x, int64_t y) { return S.inbox_tgt[x] < S.inbox_tgt[y]; });
-                tg.resize(hi - lo);
-                src.resize(hi - lo);
-                for (int64_t k = 0; k < hi - lo; ++k) { tg[k] = S.inbox_tgt[idx[k]]; src[k] = inv[idx[k]]; }
-                for (int64_t k = 0; k < hi - lo; ++k) {
-                    S.inbox_tgt[lo + k] = tg[k];
+                const int64_t nb = hi - lo;
+                key.resize(nb);
+                for (int64_t k = 0; k < nb; ++k) key[k] = ((uint64_t)(uint32_t)S.inbox_tgt[lo + k] << 32) | (uint64_t)k;
+                bool sorted = true;
+                for (int64_t k = 1; k < nb && sorted; ++k) sorted = key[k - 1] <= key[k];
+                if (sorted) continue;
+                std::sort(key.begin(), key.end());
+                src.resize(nb);
+                for (int64_t k = 0; k < nb; ++k) src[k] = src_of[lo + (int64_t)(key[k] & 0xffffffffu)];
+                for (int64_t k = 0; k < nb; ++k) {
+                    S.inbox_tgt[lo + k] = (int32_t)(key[k] >> 32);
                     S.push_pos[src[k]] = lo + k;
                 }
             }
@@ -785,6 +972,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
                 S.vpush_pos[S.cv_off[K] + a] = vf[S.sn_rows[p]]++;
         }
     }
+    T.mark("inbox maps");
     // levels and topological order
     S.level.assign(ns, 0);
     for (int32_t J = 0; J < ns; ++J)
@@ -839,6 +1027,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
             S.max_panel_main = std::max<int64_t>(S.max_panel_main,
                                                  (S.sn_col[J + 1] - S.sn_col[J]) * (S.sn_rptr[J + 1] - S.sn_rptr[J]));
 
+    T.mark("levels + tiers");
     // scatter maps: K(i,j) (original indices) -> panel position
     auto pos = [&](int64_t i, int64_t j) -> int64_t {
         int32_t a = iperm[i], b = iperm[j];
@@ -863,6 +1052,7 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
         for (int64_t rl = 0; rl < bdim[b]; ++rl)
             for (int64_t cl = rl; cl < bdim[b]; ++cl)
                 S.map_hblk.push_back(pos(n + boff[b] + rl, n + boff[b] + cl));
+    T.mark("scatter maps");
     // continuation scheduling (ldl.cu): per-supernode descriptors, same-tier child
     // counts, start lists (supernodes without same-tier children), inbox column ids
     {

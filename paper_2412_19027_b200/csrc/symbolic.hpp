@@ -21,6 +21,7 @@ struct SymbolicOptions {
     int64_t auto_min_dim = 20000;   // ordering 3 (auto): below this, the reference's MD
     double nd_max_fill = 1.25;      // ... above it ND if nnz(L) <= this x MD's
     double nd_max_flops = 1.5;      // ... and factor flops <= this x MD's
+    int64_t md_work_budget_per_nnz = 50;   // exact MD abandoned for AMD past this work / (nnz + dim)
     int relax_small = 8;       // always merge a child into its parent up to this width
     int relax_mid = 32;        // ... up to this width if zero fraction <= relax_mid_frac
     double relax_mid_frac = 0.3;
@@ -39,7 +40,7 @@ struct Symbolic {
     // permutation: position k of the factor holds original KKT index perm[k]
     std::vector<int32_t> perm, iperm;
     std::vector<int32_t> md_perm;          // raw fill-reducing order (before postordering)
-    int ordering_used = 0;                 // 0 MD, 1 natural, 2 nested dissection
+    int ordering_used = 0;                 // 0 MD (or AMD past the work budget), 1 natural, 2 ND, 4 AMD
     std::vector<int8_t> sign;              // +1 x rows, -1 z rows (permuted order)
     // supernodes
     int32_t nsuper = 0;

@@ -214,10 +214,11 @@ def make_desc(P, A, lay: Layout):
 class SymbolicAnalysis:
     """Host symbolic analysis handle (ordering, etree, supernodes, scatter maps)."""
 
-    ORDERINGS = {"md": 0, "natural": 1, "nd": 2, "auto": 3}
+    ORDERINGS = {"md": 0, "natural": 1, "nd": 2, "auto": 3, "amd": 4}
 
     def __init__(self, P, A, lay: Layout, ordering: int = 0, nd_leaf: int = 0):
-        """ordering: 0 the reference's exact minimum degree, 1 natural, 2 nested
+        """ordering: 0 the reference's exact minimum degree, 1 natural, 4 approximate
+        minimum degree (quotient graph), 2 nested
         dissection (parts up to nd_leaf rows ordered by MD), 3 auto (MD below 20k
         rows, else ND when its fill stays close to MD's)."""
         self._desc, self._keep = make_desc(P, A, lay)
