@@ -18,7 +18,8 @@
 #include "common.cuh"
 #include "ctx.hpp"
 #include "nsym.cuh"
-#include "psd.cuh"
+#include "psd_warp.cuh"
+#include <algorithm>
 
 namespace cipm {
 
@@ -522,6 +523,9 @@ __global__ void nsym_membership(NsymArgs a, const double* s, const double* z, in
 }
 
 // ================================ PSD ======================================
+// one warp per cone (psd_warp.cuh): lane i owns row i of the cone's matrices,
+// which live in the warp's shared-memory slice of PW_MATS matrices (nmax x ld)
+// plus two svec vectors and the eigenvalue vector; side <= 32 (problem.py:36)
 
 struct PsdArgs {
     int64_t npsd;
@@ -530,149 +534,230 @@ struct PsdArgs {
     const int64_t* mptr;    // side^2 prefix
     const int64_t* lptr;    // side prefix
     const int64_t* hptr;    // into hv
+    int nmax, ld;           // largest side, leading dimension of the slice matrices
 };
 
-template <int MS>
-__global__ void psd_scaling(PsdArgs a, const double* s, const double* z, double* R, double* RI, double* Q,
-                            double* LAM, double* hv, int* err) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
-    double r[MS * MS], ri[MS * MS], lam[MS], q[MS * MS];
-    int rc = psd_nt<MS>(s + off, z + off, n, r, ri, lam);
-    if (rc != 0) { set_error(err, CIPM_E_SCALING); return; }
-    mm<MS>(r, r, n, q, 2);   // Q = R R'
-    double* Rc = R + a.mptr[c];
-    double* RIc = RI + a.mptr[c];
-    double* Qc = Q + a.mptr[c];
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            Rc[i * n + j] = r[i * MS + j];
-            RIc[i * n + j] = ri[i * MS + j];
-            Qc[i * n + j] = q[i * MS + j];
+constexpr int PW_MATS = 6;
+
+__device__ __forceinline__ double* pw_slice(const PsdArgs& a, double* smem) {
+    const int w = threadIdx.x >> 5;
+    const int per = PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2;
+    return smem + (int64_t)w * per;
+}
+
+struct PwView {
+    double* M[PW_MATS];
+    double *v0, *v1, *lam;
+};
+
+__device__ __forceinline__ PwView pw_view(const PsdArgs& a, double* base) {
+    PwView v;
+    const int msz = a.nmax * a.ld;
+    for (int k = 0; k < PW_MATS; ++k) v.M[k] = base + k * msz;
+    const int dmax = a.nmax * (a.nmax + 1) / 2;
+    v.v0 = base + PW_MATS * msz;
+    v.v1 = v.v0 + dmax;
+    v.lam = v.v1 + dmax;
+    return v;
+}
+
+// cone index of this warp (grid-stride over cones)
+#define PSD_WARP_LOOP(a)                                                                        \
+    extern __shared__ __align__(16) double psd_smem[];                                          \
+    PwView W = pw_view(a, pw_slice(a, psd_smem));                                               \
+    const int lane = threadIdx.x & 31;                                                          \
+    (void)lane;                                                                                  \
+    for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < a.npsd;         \
+         c += ((int64_t)gridDim.x * blockDim.x) >> 5)
+
+// NT scaling (scaling.py PSD part, psdcone.py:98-117) + congruence block H = Q (x)s Q
+__global__ void psd_scaling_w(PsdArgs a, const double* s, const double* z, double* R, double* RI, double* Q,
+                              double* LAM, double* hv, int* err) {
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c], ld = a.ld;
+        double *W0 = W.M[0], *W1 = W.M[1], *W2 = W.M[2], *W3 = W.M[3], *Rm = W.M[4], *RIm = W.M[5];
+        if (!pw::nt_factor(s + off, z + off, n, ld, W0, W1, W2, W3, Rm, RIm, W.lam)) {
+            if (lane == 0) set_error(err, CIPM_E_SCALING);
+            continue;
         }
-    for (int i = 0; i < n; ++i) LAM[a.lptr[c] + i] = lam[i];
-    // congruence matrix of X -> Q X Q in svec coordinates, upper triangle row-major
-    const int d = n * (n + 1) / 2;
-    int ka[MS * (MS + 1) / 2], kb[MS * (MS + 1) / 2];
-    {
-        int k = 0;
-        for (int j = 0; j < n; ++j)
-            for (int i = j; i < n; ++i) { ka[k] = i; kb[k] = j; ++k; }
-    }
-    double* hb = hv + a.hptr[c];
-    int t = 0;
-    for (int k = 0; k < d; ++k) {
-        const int p = ka[k], qq = kb[k];          // row entry (p, qq), p >= qq
-        const double sk = p == qq ? 1.0 : kSqrt2;
-        for (int l = k; l < d; ++l) {
-            const int i = ka[l], j = kb[l];
-            double mv;
-            if (i == j) mv = q[p * MS + i] * q[qq * MS + i];
-            else mv = (q[p * MS + i] * q[qq * MS + j] + q[p * MS + j] * q[qq * MS + i]) / kSqrt2;
-            hb[t++] = sk * mv;
+        pw::mm(Rm, Rm, n, ld, W0, 2);                 // Q = R R'
+        double* Rc = R + a.mptr[c];
+        double* RIc = RI + a.mptr[c];
+        double* Qc = Q + a.mptr[c];
+        for (int e = lane; e < n * n; e += 32) {
+            const int i = e / n, j = e - i * n;
+            Rc[e] = Rm[i * ld + j];
+            RIc[e] = RIm[i * ld + j];
+            Qc[e] = W0[i * ld + j];
         }
+        for (int i = lane; i < n; i += 32) LAM[a.lptr[c] + i] = W.lam[i];
+        // H(k, l), k <= l over svec indices, upper triangle row-major: row k = (p, q)
+        const int d = n * (n + 1) / 2;
+        double* hb = hv + a.hptr[c];
+        int64_t rowoff = 0;
+        int p = 0, q = 0;                                // svec index k -> (p >= q)
+        for (int k = 0; k < d; ++k) {
+            const double sk = p == q ? 1.0 : pw::kR2;
+            // entries l = k .. d-1, (i, j) of svec index l
+            for (int l = k + lane; l < d; l += 32) {
+                int j = 0, rem = l;
+                while (rem >= n - j) { rem -= n - j; ++j; }
+                const int i = j + rem;
+                double mv;
+                if (i == j) mv = W0[p * ld + i] * W0[q * ld + i];
+                else mv = (W0[p * ld + i] * W0[q * ld + j] + W0[p * ld + j] * W0[q * ld + i]) / pw::kR2;
+                hb[rowoff + (l - k)] = sk * mv;
+            }
+            rowoff += d - k;
+            if (++p == n) { ++q; p = q; }
+        }
+        __syncwarp();
     }
 }
 
-template <int MS>
-__global__ void psd_apply_h(PsdArgs a, const double* Q, const double* v, double* out, double alpha,
-                            const double* u, double beta, const double* skip) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd || (skip && *skip != 0.0)) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
-    double q[MS * MS], X[MS * MS], T[MS * MS], Y[MS * MS], hv[MS * (MS + 1) / 2];
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) q[i * MS + j] = Q[a.mptr[c] + i * n + j];
-    smat<MS>(v + off, n, X);
-    mm<MS>(q, X, n, T, 0);
-    mm<MS>(T, q, n, Y, 0);
-    svec<MS>(Y, n, hv);
-    const int d = n * (n + 1) / 2;
-    for (int k = 0; k < d; ++k) {
-        const double base = u ? alpha * u[off + k] : 0.0;
-        out[off + k] = base + beta * hv[k];
+// out = alpha u + beta svec(Q smat(v) Q)
+__global__ void psd_apply_h_w(PsdArgs a, const double* Q, const double* v, double* out, double alpha,
+                              const double* u, double beta, const double* skip) {
+    if (skip && *skip != 0.0) return;
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c], ld = a.ld;
+        double *Qm = W.M[0], *X = W.M[1], *T = W.M[2];
+        for (int e = lane; e < n * n; e += 32) Qm[(e / n) * ld + e % n] = Q[a.mptr[c] + e];
+        __syncwarp();
+        pw::smat(v + off, n, X, ld);
+        pw::mm(Qm, X, n, ld, T, 0);
+        pw::mm(T, Qm, n, ld, X, 0);
+        pw::svec(X, n, ld, W.v0);
+        const int d = n * (n + 1) / 2;
+        for (int k = lane; k < d; k += 32) {
+            const double base = u ? alpha * u[off + k] : 0.0;
+            out[off + k] = base + beta * W.v0[k];
+        }
+        __syncwarp();
     }
 }
 
-template <int MS>
-__global__ void psd_combined_ds(PsdArgs a, const double* R, const double* RI, const double* LAM,
-                                const double* dz_a, const double* ds_a, const double* sc, double* out) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
+// combined d_s (scaling.py:277-320, PSD part): R (2 (diag lam^2 + sym(A B) - sigma mu I) / (lam_i + lam_j)) R'
+__global__ void psd_combined_ds_w(PsdArgs a, const double* R, const double* RI, const double* LAM,
+                                  const double* dz_a, const double* ds_a, const double* sc, double* out) {
     const double sigma = sc[CIPM_SC_SIGMA], mu = sc[CIPM_SC_MU];
-    double r[MS * MS], ri[MS * MS], lam[MS], X[MS * MS], T[MS * MS], A[MS * MS], B[MS * MS];
-    for (int i = 0; i < n; ++i) {
-        lam[i] = LAM[a.lptr[c] + i];
-        for (int j = 0; j < n; ++j) {
-            r[i * MS + j] = R[a.mptr[c] + i * n + j];
-            ri[i * MS + j] = RI[a.mptr[c] + i * n + j];
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c], ld = a.ld;
+        double *r = W.M[0], *ri = W.M[1], *X = W.M[2], *T = W.M[3], *A = W.M[4], *B = W.M[5];
+        for (int e = lane; e < n * n; e += 32) {
+            r[(e / n) * ld + e % n] = R[a.mptr[c] + e];
+            ri[(e / n) * ld + e % n] = RI[a.mptr[c] + e];
         }
-    }
-    smat<MS>(ds_a + off, n, X);
-    mm<MS>(ri, X, n, T, 0);
-    mm<MS>(T, ri, n, A, 2);          // Rinv ds Rinv'
-    smat<MS>(dz_a + off, n, X);
-    mm<MS>(r, X, n, T, 1);           // R' dz
-    mm<MS>(T, r, n, B, 0);           // R' dz R
-    mm<MS>(A, B, n, X, 0);
-    mm<MS>(B, A, n, T, 0);
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            double e = 0.5 * (X[i * MS + j] + T[i * MS + j]);
-            double rhs = (i == j ? lam[i] * lam[i] : 0.0) + e - (i == j ? sigma * mu : 0.0);
-            A[i * MS + j] = 2.0 * rhs / (lam[i] + lam[j]);
+        for (int i = lane; i < n; i += 32) W.lam[i] = LAM[a.lptr[c] + i];
+        __syncwarp();
+        pw::smat(ds_a + off, n, X, ld);
+        pw::mm(ri, X, n, ld, T, 0);
+        pw::mm(T, ri, n, ld, A, 2);                  // Rinv ds Rinv'
+        pw::smat(dz_a + off, n, X, ld);
+        pw::mm(r, X, n, ld, T, 1);                   // R' dz
+        pw::mm(T, r, n, ld, B, 0);                   // R' dz R
+        pw::mm(A, B, n, ld, X, 0);
+        pw::mm(B, A, n, ld, T, 0);
+        if (lane < n) {
+            const int i = lane;
+            for (int j = 0; j < n; ++j) {
+                const double e = 0.5 * (X[i * ld + j] + T[i * ld + j]);
+                const double rhs = (i == j ? W.lam[i] * W.lam[i] : 0.0) + e - (i == j ? sigma * mu : 0.0);
+                A[i * ld + j] = 2.0 * rhs / (W.lam[i] + W.lam[j]);
+            }
         }
-    mm<MS>(r, A, n, T, 0);
-    mm<MS>(T, r, n, X, 2);           // R U R'
-    svec<MS>(X, n, out + off);
-}
-
-template <int MS>
-__global__ void psd_step_bound(PsdArgs a, const double* z, const double* s, const double* dz, const double* ds,
-                               double* sc, int* err) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
-    double b1 = psd_step<MS>(z + off, dz + off, n);
-    double b2 = psd_step<MS>(s + off, ds + off, n);
-    if (b1 < 0.0 || b2 < 0.0) { set_error(err, CIPM_E_DOMAIN); return; }
-    double b = fmin(b1, b2);
-    if (b < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, b);
-}
-
-template <int MS>
-__global__ void psd_neighborhood(PsdArgs a, const double* s, const double* z, const double* ds, const double* dz,
-                                 const double* nb, int nk, double beta, unsigned int* mask, int* err) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
-    const int d = n * (n + 1) / 2;
-    unsigned int bits = 0u;
-    double st[MS * (MS + 1) / 2], zt[MS * (MS + 1) / 2];
-    for (int k = 0; k < nk; ++k) {
-        const double step = nb[16 + k];
-        for (int i = 0; i < d; ++i) { st[i] = s[off + i] + step * ds[off + i]; zt[i] = z[off + i] + step * dz[off + i]; }
-        double tr;
-        if (!psd_trace_inv<MS>(st, zt, n, &tr)) { set_error(err, CIPM_E_DOMAIN); continue; }
-        if (!((double)n / tr < beta * nb[k])) bits |= 1u << k;
+        __syncwarp();
+        pw::mm(r, A, n, ld, T, 0);
+        pw::mm(T, r, n, ld, X, 2);                   // R U R'
+        pw::svec(X, n, ld, out + off);
     }
-    if (bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
 }
 
-template <int MS>
-__global__ void psd_membership(PsdArgs a, const double* s, const double* z, int* err) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= a.npsd) return;
-    const int n = a.side[c], off = a.off[c];
-    if (n > MS) return;
-    if (!psd_is_pd<MS>(s + off, n) || !psd_is_pd<MS>(z + off, n)) set_error(err, CIPM_E_INTERIOR);
+// sup{alpha >= 0: mat(v) + alpha mat(dv) PSD} (psdcone.py:120-133); < 0 on DomainError
+__device__ __forceinline__ double psd_step_w(const double* v, const double* dv, int n, int ld, const PwView& W) {
+    double *X = W.M[0], *Li = W.M[1], *D = W.M[2], *T = W.M[3];
+    pw::smat(v, n, X, ld);
+    if (!pw::chol(X, n, ld)) return -1.0;
+    pw::tri_inv(X, n, ld, Li);
+    pw::smat(dv, n, D, ld);
+    pw::mm(Li, D, n, ld, T, 0);
+    pw::mm(T, Li, n, ld, X, 2);                      // Li D Li'
+    const double lmin = pw::sym_min_eig(X, n, ld);
+    return lmin >= 0.0 ? INFINITY : -1.0 / lmin;
+}
+
+__global__ void psd_step_bound_w(PsdArgs a, const double* z, const double* s, const double* dz, const double* ds,
+                                 double* sc, int* err) {
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c];
+        const double b1 = psd_step_w(z + off, dz + off, n, a.ld, W);
+        const double b2 = psd_step_w(s + off, ds + off, n, a.ld, W);
+        if (lane == 0) {
+            if (b1 < 0.0 || b2 < 0.0) set_error(err, CIPM_E_DOMAIN);
+            else {
+                const double b = fmin(b1, b2);
+                if (b < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, b);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// tr(S^-1 Z^-1); false if either is not positive definite
+__device__ __forceinline__ bool psd_trace_inv_w(const double* sv, const double* zv, int n, int ld, const PwView& W,
+                                                double* tr) {
+    double *X = W.M[0], *Li = W.M[1], *Si = W.M[2], *Zi = W.M[3];
+    pw::smat(sv, n, X, ld);
+    if (!pw::chol(X, n, ld)) return false;
+    pw::tri_inv(X, n, ld, Li);
+    pw::mm(Li, Li, n, ld, Si, 1);                    // L^-T L^-1 = S^-1
+    pw::smat(zv, n, X, ld);
+    if (!pw::chol(X, n, ld)) return false;
+    pw::tri_inv(X, n, ld, Li);
+    pw::mm(Li, Li, n, ld, Zi, 1);
+    const int i = threadIdx.x & 31;
+    double acc = 0.0;
+    if (i < n)
+        for (int j = 0; j < n; ++j) acc += Si[i * ld + j] * Zi[j * ld + i];
+    *tr = pw::wsum(acc);
+    return true;
+}
+
+__global__ void psd_neighborhood_w(PsdArgs a, const double* s, const double* z, const double* ds, const double* dz,
+                                   const double* nb, int nk, double beta, unsigned int* mask, int* err) {
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c];
+        const int d = n * (n + 1) / 2;
+        unsigned int bits = 0u;
+        for (int k = 0; k < nk; ++k) {
+            const double step = nb[16 + k];
+            for (int e = lane; e < d; e += 32) {
+                W.v0[e] = s[off + e] + step * ds[off + e];
+                W.v1[e] = z[off + e] + step * dz[off + e];
+            }
+            __syncwarp();
+            double tr;
+            if (!psd_trace_inv_w(W.v0, W.v1, n, a.ld, W, &tr)) {
+                if (lane == 0) set_error(err, CIPM_E_DOMAIN);
+                continue;
+            }
+            if (!((double)n / tr < beta * nb[k])) bits |= 1u << k;
+        }
+        if (lane == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
+        __syncwarp();
+    }
+}
+
+__global__ void psd_membership_w(PsdArgs a, const double* s, const double* z, int* err) {
+    PSD_WARP_LOOP(a) {
+        const int n = a.side[c], off = a.off[c];
+        pw::smat(s + off, n, W.M[0], a.ld);
+        const bool ok1 = pw::chol(W.M[0], n, a.ld);
+        pw::smat(z + off, n, W.M[1], a.ld);
+        const bool ok2 = pw::chol(W.M[1], n, a.ld);
+        if (lane == 0 && (!ok1 || !ok2)) set_error(err, CIPM_E_INTERIOR);
+        __syncwarp();
+    }
 }
 
 // ============================== launch glue ================================
@@ -707,17 +792,28 @@ PsdArgs psd_args(Ctx& c) {
     a.mptr = c.psd_mptr;
     a.lptr = c.psd_lptr;
     a.hptr = c.psd_hptr;
+    a.nmax = c.psd_max_side;
+    a.ld = c.psd_max_side | 1;
     return a;
 }
 
 inline int warp_grid(int64_t nwarps) { return grid_for(nwarps * 32); }
 
-#define PSD_DISPATCH(KERNEL, ...)                                                        \
-    do {                                                                                 \
-        if (c.psd_max_side <= 4) KERNEL<4><<<grid_for(c.npsd, 128), 128, 0, c.stream>>>(__VA_ARGS__); \
-        else if (c.psd_max_side <= 8) KERNEL<8><<<grid_for(c.npsd, 64), 64, 0, c.stream>>>(__VA_ARGS__); \
-        else KERNEL<16><<<grid_for(c.npsd, 32), 32, 0, c.stream>>>(__VA_ARGS__);         \
-        c.launches++;                                                                    \
+// warp-per-cone PSD launch: warps per CTA from the slice size (<= 96 KiB per CTA)
+inline size_t psd_slice_bytes(const PsdArgs& a) {
+    return sizeof(double) * (size_t)(PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2);
+}
+
+#define PSD_DISPATCH(KERNEL, ...)                                                                      \
+    do {                                                                                               \
+        const PsdArgs pa_ = psd_args(c);                                                               \
+        const size_t sl_ = psd_slice_bytes(pa_);                                                       \
+        int wpb_ = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / sl_));                   \
+        const size_t smem_ = sl_ * (size_t)wpb_;                                                       \
+        if (smem_ > 48 * 1024) cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_); \
+        const int64_t blocks_ = (c.npsd + wpb_ - 1) / wpb_;                                            \
+        KERNEL<<<(int)std::min<int64_t>(blocks_, 148 * 32), wpb_ * 32, smem_, c.stream>>>(__VA_ARGS__); \
+        c.launches++;                                                                                  \
     } while (0)
 
 }  // namespace
@@ -741,7 +837,7 @@ void k_update_scaling_family(Ctx& c, int fam) {
                                                                   c.ns_hess, c.ns_zt, c.hv, c.err);
         c.launches++;
     }
-    if (fam == 3 && c.npsd) PSD_DISPATCH(psd_scaling, psd_args(c), c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+    if (fam == 3 && c.npsd) PSD_DISPATCH(psd_scaling_w, pa_, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
 }
 
 void k_update_scaling(Ctx& c) {
@@ -760,7 +856,7 @@ void k_update_scaling(Ctx& c) {
                                                                   c.ns_hess, c.ns_zt, c.hv, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_scaling, psd_args(c), c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+    if (c.npsd) PSD_DISPATCH(psd_scaling_w, pa_, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
 }
 
 // hv (upper triangles of all dense blocks) lives in c.wm (sized >= hblk_total)
@@ -806,7 +902,7 @@ void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double*
         nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta, skip);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_apply_h, psd_args(c), c.psd_q, v, out, alpha, u, beta, skip);
+    if (c.npsd) PSD_DISPATCH(psd_apply_h_w, pa_, c.psd_q, v, out, alpha, u, beta, skip);
 }
 
 void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a) {
@@ -825,7 +921,7 @@ void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a) {
                                                                       c.ns_hess, c.sc, c.dsc, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_combined_ds, psd_args(c), c.psd_r, c.psd_rinv, c.psd_lam, dz_a, ds_a, c.sc, c.dsc);
+    if (c.npsd) PSD_DISPATCH(psd_combined_ds_w, pa_, c.psd_r, c.psd_rinv, c.psd_lam, dz_a, ds_a, c.sc, c.dsc);
 }
 
 void k_step_bound(Ctx& c, const double* dz, const double* ds) {
@@ -838,7 +934,7 @@ void k_step_bound(Ctx& c, const double* dz, const double* ds) {
         soc_step_bound<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.z, c.s, dz, ds, c.sc);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_step_bound, psd_args(c), c.z, c.s, dz, ds, c.sc, c.err);
+    if (c.npsd) PSD_DISPATCH(psd_step_bound_w, pa_, c.z, c.s, dz, ds, c.sc, c.err);
 }
 
 void k_nsym_feasible_mask(Ctx& c, const double* dz, const double* ds, int k0) {
@@ -861,7 +957,7 @@ void k_neighborhood_mask(Ctx& c, int k0, int nk) {
                                                                        c.nb, nk, c.beta, c.mask, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_neighborhood, psd_args(c), c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err);
+    if (c.npsd) PSD_DISPATCH(psd_neighborhood_w, pa_, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err);
 }
 
 void k_membership(Ctx& c) {
@@ -877,7 +973,7 @@ void k_membership(Ctx& c) {
         nsym_membership<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_membership, psd_args(c), c.s, c.z, c.err);
+    if (c.npsd) PSD_DISPATCH(psd_membership_w, pa_, c.s, c.z, c.err);
 }
 
 void k_soc_residuals(Ctx& c, const double* x, double* out) {

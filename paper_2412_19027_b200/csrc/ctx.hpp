@@ -154,6 +154,7 @@ struct Ctx {
     int solve_form_inv = 0;          // per-warp Linv buffer (max non-tail width squared)
     int8_t* sf_flag = nullptr;       // per supernode: panel in solve form (1) or plain L (0)
     double sf_tau = 16.0;            // growth bound max |L11^-1| for the solve form (CIPM_SF_TAU)
+    bool solve_form = false;         // panels in solve form (default: mixed precision, CIPM_SOLVE_FORM)
     // dense tail (dense.cu)
     std::vector<TailNode> tail;
     void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)

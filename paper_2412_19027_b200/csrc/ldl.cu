@@ -440,121 +440,138 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
     }
 }
 
-// CTA-tier dense panel LDL' (replaces the column loop of ldl.py:62-88 for one
-// supernode): right-looking on the UNSCALED columns, one row per thread (rows
-// tid, tid + nthr, ...), the j loop kept rolled so the code stays a few hundred
-// instructions — the unrolled register / blocked variants were several hundred
-// KiB of SASS, and instruction-cache misses made every pivot step ~0.4 us on the
-// C2 critical path.  Step j: every participating thread reads the final pivot
-// a_jj, applies the dynamic regularisation (ldl.py:79-87) redundantly, and
-// updates its own rows a_ic -= a_ij a_cj / d_j for j < c <= i (a_cj is read
-// unscaled: its owner does not touch column j during the step); one named
-// barrier per step.  Columns are scaled by 1 / d_j in a final pass.
-// Narrow panels (w <= NB, r <= 64): the same right-looking elimination with each
-// thread's row in registers, one row per thread (warp 0 rows 0..31, warp 1 rows
-// 32..63), the j loop rolled and the row ROTATED one column per step so every
-// register index is static (current column = x[0]).  Per step warp 0, which
-// holds the pivot row, publishes 1/d_j and the scaled column l_cj (rows c < w)
-// in a double-buffered shared array; one 64-thread named barrier; every row
-// applies a_ic -= a_ij l_cj.  ~1/3 of the per-step latency of the shared-memory
-// read-modify-write loop, and a compact body (instruction-cache resident).
+// CTA-tier dense panel LDL' (see factor_cta_kernel); forced inline so the
+// panel pointer keeps its address space (shared -> LDS/STS) at each call site
+//
+// Blocked by 32 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
+// diagonal block with lane i holding row i in registers (warp-synchronous
+// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
+// per row below holds its nbk entries in registers and applies the same
+// right-looking elimination against L11 (broadcast shared-memory reads);
+// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
+// instead of one per column.
 template <typename T, int NB>
-__device__ __forceinline__ void rot_panel_ldl(T* P, int r, int w, const int8_t* sSg, T* sD, double& s_runmax,
-                                              const FactorArgs& a, T (*scol)[2 * NB + 1]) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const bool two = r > 32;
-    const bool have = tid < r;
+__device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, const int8_t* sSg, T* sD,
+                                               double& s_runmax, const FactorArgs& a, T* sLt, T* sInv) {
+    const int lane = threadIdx.x & 31;
     double runmax = s_runmax;
-    int nbump = 0;
     T x[NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) x[c] = (c < w && have) ? P[c * r + tid] : (T)0;
-    if (tid < 2 * NB + 1) { scol[0][tid] = (T)0; scol[1][tid] = (T)0; }   // columns >= w read as 0
-    if (two) asm volatile("bar.sync 1, 64;" ::: "memory");
-    else __syncwarp();
-#pragma unroll 1
-    for (int j = 0; j < w; ++j) {
-        T* col = scol[j & 1];
-        if (tid < 32) {
-            double dd = (double)__shfl_sync(0xffffffffu, x[0], j);
+    for (int c = 0; c < NB; ++c)
+        x[c] = (lane < nbk && c < nbk && c <= lane) ? Pk[c * r + k0 + lane] : (T)0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        if (j < nbk) {
+            double dd = (double)__shfl_sync(0xffffffffu, x[j], j);
             const double bound = a.delta_s + a.delta_d * runmax;
             const bool bump = fabs(dd) < bound;
-            if (bump) dd = sSg[j] > 0 ? bound : -bound;
+            if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
             const T dt = (T)dd;
             runmax = fmax(runmax, fabs(dd));
-            nbump += bump ? 1 : 0;
             const T inv = (T)1 / dt;
             if (lane == 0) {
+                if (bump) atomicAdd(a.bumps, 1);
                 if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                sD[j] = dt;
-                col[2 * NB] = inv;
+                sD[k0 + j] = dt;
+                sInv[j] = inv;
             }
-            // l_cj of rows c in (j, w) at col[c - j]; col[0] unused; stale entries of
-            // step j - 2 beyond w - j zeroed (disjoint from the writes above)
-            if (lane > j && lane < w) col[lane - j] = x[0] * inv;
-            if (lane >= w - j && lane < NB) col[lane] = (T)0;
-        }
-        if (two) asm volatile("bar.sync 1, 64;" ::: "memory");
-        else __syncwarp();
-        const T inv = col[2 * NB];
-        const T aij = x[0];
-        if (have && tid >= j) P[j * r + tid] = tid > j ? aij * inv : (T)1;
+            const T xj = x[j];                   // unscaled a_ij (lanes i > j)
 #pragma unroll
-        for (int c = 1; c < NB; ++c) x[c - 1] = x[c] - aij * col[c];
-        x[NB - 1] = (T)0;
+            for (int c = j + 1; c < NB; ++c) {
+                const T acj = __shfl_sync(0xffffffffu, xj, c);   // unscaled a_cj
+                if (lane >= c) x[c] -= xj * (acj * inv);
+            }
+            x[j] = lane > j ? xj * inv : (lane == j ? (T)1 : x[j]);
+        } else if (lane == 0) {
+            sInv[j] = (T)0;
+        }
     }
-    if (tid == 0) {
-        s_runmax = runmax;
-        if (nbump) atomicAdd(a.bumps, nbump);
+    int row = k0 + lane;
+    asm volatile("" : "+r"(row));            // recompute the store addresses (no 32 live pointers)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+        if (lane < nbk && c < nbk && c <= lane) Pk[c * r + row] = x[c];
+        if (lane < NB) sLt[c * NB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;   // Lt[j][i] = l_ij
+    }
+    if (lane == 0) s_runmax = runmax;
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void cta_below_rows(T* Pk, int r, int i0, int nbk, const T* sLt, const T* sInv) {
+#pragma unroll 1
+    for (int i = i0 + threadIdx.x; i < r; i += blockDim.x) {
+        T x[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) x[c] = c < nbk ? Pk[c * r + i] : (T)0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const T xj = x[j];
+#pragma unroll
+            for (int c = j + 1; c < NB; ++c) x[c] -= xj * sLt[j * NB + c];
+            x[j] = xj * sInv[j];
+            asm volatile("" ::: "memory");      // L11 row loads per step (register budget)
+        }
+        int is = i;
+        asm volatile("" : "+r"(is));         // recompute the store addresses (no 32 live pointers)
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+            if (c < nbk) Pk[c * r + is] = x[c];
     }
 }
 
+//
+// Blocked by 16 columns.  Per block k0: (a) warp 0 factors the nbk x nbk
+// diagonal block with lane i holding row i in registers (warp-synchronous
+// right-looking, shuffles, no barriers), publishing L11' and 1/d; (b) one thread
+// per row below holds its nbk entries in registers and applies the same
+// right-looking elimination against L11 (broadcast shared-memory reads);
+// (c) rank-nbk update of the trailing columns.  Two or three barriers per block
+// instead of one per column.
 template <typename T>
 __device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
-                                              const FactorArgs& a, T* __restrict__ dvec) {
-    const int tid = threadIdx.x;
-    const int nthr = min((int)blockDim.x, (r + 31) & ~31);
-    if (tid < nthr) {
-        double runmax = s_runmax;
-        int nbump = 0;
-        for (int j = 0; j < w; ++j) {
-            T* Pj = P + (int64_t)j * r;
-            double dd = (double)Pj[j];
-            const double bound = a.delta_s + a.delta_d * runmax;
-            const bool bump = fabs(dd) < bound;
-            if (bump) dd = sSg[j] > 0 ? bound : -bound;
-            const T dt = (T)dd;
-            runmax = fmax(runmax, fabs(dd));
-            const T inv = (T)1 / dt;
-            nbump += bump ? 1 : 0;
-            if (tid == 0) {
-                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                sD[j] = dt;
-            }
-            for (int i = j + 1 + tid; i < r; i += nthr) {
-                const T aij = Pj[i] * inv;
-                const int cend = min(i, w - 1);
-#pragma unroll 4
-                for (int c = j + 1; c <= cend; ++c) P[(int64_t)c * r + i] -= aij * Pj[c];
-            }
-            if (nthr > 32) asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
-            else __syncwarp();
+                                              const FactorArgs& a, T* __restrict__ dvec, T* sLt, T* sInv) {
+    // block width 16: a row of the block in registers, 2 CTAs / SM without spills
+    constexpr int KB = 16;
+    const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
+    for (int k0 = 0; k0 < w; k0 += KB) {
+        const int nbk = min(KB, w - k0);
+        T* Pk = P + k0 * r;               // column k0 of the panel
+        if (wid == 0) {
+            if (nbk <= 8) cta_diag_block<T, 8>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
+            else cta_diag_block<T, KB>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
         }
-        if (tid == 0) {
-            s_runmax = runmax;
-            if (nbump) atomicAdd(a.bumps, nbump);
+        __syncthreads();
+        // (b) rows below the diagonal block
+        if (nbk <= 8) cta_below_rows<T, 8>(Pk, r, k0 + nbk, nbk, sLt, sInv);
+        else cta_below_rows<T, KB>(Pk, r, k0 + nbk, nbk, sLt, sInv);
+        __syncthreads();
+        // (c) trailing columns c >= k0 + nbk, rows i >= c: A(i,c) -= sum_k l_ik d_k l_ck
+        //     (only reached with a full block, nbk == KB)
+        const int c1 = k0 + nbk;
+        if (c1 < w) {
+            // d_k l_ck for the trailing columns, into the (now free) L11' buffer
+            for (int idx = tid; idx < (w - c1) * KB; idx += blockDim.x) {
+                const int cc = idx / KB, k = idx - cc * KB;
+                sLt[idx] = sD[k0 + k] * Pk[k * r + c1 + cc];
+            }
+            __syncthreads();
+            for (int c = c1 + wid; c < w; c += nw) {
+                const T* dl = sLt + (c - c1) * KB;
+                T* Pc = P + c * r;
+#pragma unroll 1
+                for (int i = c + (tid & 31); i < r; i += 32) {
+                    T acc = (T)0;
+#pragma unroll 8
+                    for (int k = 0; k < KB; ++k) acc += Pk[k * r + i] * dl[k];
+                    Pc[i] -= acc;
+                }
+            }
+            __syncthreads();
         }
-    }
-    __syncthreads();
-    for (int j = 0; j < w; ++j) {
-        T* Pj = P + (int64_t)j * r;
-        const T inv = (T)1 / sD[j];
-        for (int i = j + 1 + tid; i < r; i += blockDim.x) Pj[i] = Pj[i] * inv;
-        if (tid == 0) Pj[j] = (T)1;
     }
     for (int j = tid; j < w; j += blockDim.x) dvec[c0 + j] = sD[j];
-    __syncthreads();
 }
+
 
 // CTA-tier contribution block C = L_off D L_off' scattered to the ancestors'
 // inboxes: entries (packed column-major lower) flattened over all threads, push
@@ -591,7 +608,8 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
     __shared__ int s_J, s_needP, s_tierP, s_next;
     __shared__ double s_runmax, s_carry;
     __shared__ T sD[64];
-    __shared__ T s_col[2][65];
+    __shared__ __align__(16) T sLt[64 * 16];    // blocked LDL: L11' of a 16-column block / d_k l_ck
+    __shared__ T sInv[16];
     __shared__ int8_t sSg[64];
     __shared__ int32_t s_d32[8];
     __shared__ int64_t s_d64[8];
@@ -650,17 +668,9 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         }
         __syncthreads();
         if (a.trace && tid == 0) a.trace[6 * J + 3] = gtimer();
-        // 2. dense LDL' of the panel
-        constexpr int NBR = sizeof(T) == 4 ? 32 : 16;
-        if (in_smem && w <= NBR && r <= 64) {
-            if (wid < 2) rot_panel_ldl<T, NBR>(sp, r, w, sSg, sD, s_runmax, a, (T(*)[2 * NBR + 1])s_col);
-            __syncthreads();
-            for (int j = tid; j < w; j += nt) dvec[c0 + j] = sD[j];
-        } else if (in_smem) {
-            cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec);
-        } else {
-            cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec);
-        }
+        // 2. dense LDL' of the panel: blocked by 16 columns (cta_panel_ldl)
+        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
+        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
         if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
         // 3. push C_J = L_off D L_off' (the factor is written back after the signal:
         //    the ancestors only read the inbox, so the release does not wait for it)
@@ -1607,7 +1617,7 @@ int factor_t(Ctx& c) {
     }
     k_tail_factor(c);
     const int nsf = (int)c.host_sym.bwd_order.size();
-    if (nsf > 0) {
+    if (nsf > 0 && c.solve_form) {
         const int slice = (int)c.solve_form_slice;
         const size_t smem = sizeof(T) * (size_t)(c.solve_form_inv + slice) * SFW;
         solve_form_kernel<T><<<c.solve_form_blocks, SFW * 32, smem, c.stream>>>(c.sym.bwd_order, nsf, c.sym.desc32,

@@ -78,3 +78,21 @@ def test_device_equilibration_bitwise(gpu, name):
     np.testing.assert_array_equal(d_row, e.d_row)
     np.testing.assert_array_equal(d_col, e.d_col)
     assert c.value == e.c_obj
+
+
+@pytest.mark.parametrize("side,ncones", [(6, 40), (17, 3), (24, 2), (32, 1)])
+def test_gpu_psd_sides_match_oracle(gpu, side, ncones):
+    """Warp-per-cone PSD kernels for every side the reference accepts (<= 32,
+    problem.py:36): same status, iterations within 1 and objectives within 1e-6 of
+    the oracle restatement of the reference."""
+    from paper_2412_19027_b200.solver import Solver
+    prob = G.gen_psd(ncones=ncones, side=side, seed=3)
+    cfg = SolverSettings(eps_feas=1e-8)
+    s = Solver(prob, cfg)
+    r = s.solve()
+    s.close()
+    ref = OracleSolver(prob, cfg).solve()
+    assert r.status == ref.status
+    assert abs(r.iterations - ref.iterations) <= 1
+    assert rel(r.obj_primal, ref.obj_primal) <= 1e-6
+    assert rel(r.obj_dual, ref.obj_dual) <= 1e-6
