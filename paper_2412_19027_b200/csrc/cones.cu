@@ -523,9 +523,10 @@ __global__ void nsym_membership(NsymArgs a, const double* s, const double* z, in
 }
 
 // ================================ PSD ======================================
-// one warp per cone (psd_warp.cuh): lane i owns row i of the cone's matrices,
-// which live in the warp's shared-memory slice of PW_MATS matrices (nmax x ld)
-// plus two svec vectors and the eigenvalue vector; side <= 32 (problem.py:36)
+// a lane group per cone (psd_warp.cuh): G = 8 / 16 / 32 lanes by the largest
+// side, lane i of a group owns row i of the cone's matrices, which live in the
+// group's shared-memory slice of PW_MATS matrices (nmax x ld) plus two svec
+// vectors and the eigenvalue vector; sides up to 32 (problem.py:36)
 
 struct PsdArgs {
     int64_t npsd;
@@ -534,23 +535,23 @@ struct PsdArgs {
     const int64_t* mptr;    // side^2 prefix
     const int64_t* lptr;    // side prefix
     const int64_t* hptr;    // into hv
-    int nmax, ld;           // largest side, leading dimension of the slice matrices
+    int nmax, ld, gw;       // largest side, leading dimension, lanes per cone
 };
 
 constexpr int PW_MATS = 6;
-
-__device__ __forceinline__ double* pw_slice(const PsdArgs& a, double* smem) {
-    const int w = threadIdx.x >> 5;
-    const int per = PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2;
-    return smem + (int64_t)w * per;
-}
 
 struct PwView {
     double* M[PW_MATS];
     double *v0, *v1, *lam;
 };
 
-__device__ __forceinline__ PwView pw_view(const PsdArgs& a, double* base) {
+__device__ __forceinline__ int pw_slice_doubles(const PsdArgs& a) {
+    return PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2;
+}
+
+__device__ __forceinline__ PwView pw_view(const PsdArgs& a, double* smem) {
+    const int grp = threadIdx.x / a.gw;                // group index within the CTA
+    double* base = smem + (int64_t)grp * pw_slice_doubles(a);
     PwView v;
     const int msz = a.nmax * a.ld;
     for (int k = 0; k < PW_MATS; ++k) v.M[k] = base + k * msz;
@@ -561,55 +562,72 @@ __device__ __forceinline__ PwView pw_view(const PsdArgs& a, double* base) {
     return v;
 }
 
-// cone index of this warp (grid-stride over cones)
-#define PSD_WARP_LOOP(a)                                                                        \
-    extern __shared__ __align__(16) double psd_smem[];                                          \
-    PwView W = pw_view(a, pw_slice(a, psd_smem));                                               \
-    const int lane = threadIdx.x & 31;                                                          \
-    (void)lane;                                                                                  \
-    for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c < a.npsd;         \
-         c += ((int64_t)gridDim.x * blockDim.x) >> 5)
+// grid-stride loop over the warp's cone batches (warp-uniform trip count); inside,
+// c is this group's cone (or -1) and G its lane view with the warp-uniform bound
+#define PSD_GROUP_LOOP(a)                                                                           \
+    extern __shared__ __align__(16) double psd_smem[];                                              \
+    PwView W = pw_view(a, psd_smem);                                                                \
+    const int lane = threadIdx.x & 31;                                                              \
+    const int cpw = 32 / a.gw;                                                                      \
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;                      \
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;                                  \
+    for (int64_t base = wid * cpw; base < a.npsd; base += nwarps * cpw)                             \
+        for (int once = 0; once < 1; ++once)                                                        \
+            if (const int64_t c = base + lane / a.gw; true)                                         \
+                if (const pw::Grp G = psd_group(a, c, lane); true)
+
+__device__ __forceinline__ pw::Grp psd_group(const PsdArgs& a, int64_t c, int lane) {
+    pw::Grp G;
+    G.i = lane % a.gw;
+    G.g = a.gw;
+    G.n = c < a.npsd ? a.side[c] : 0;
+    G.nu = __reduce_max_sync(0xffffffffu, (unsigned)G.n);
+    return G;
+}
 
 // NT scaling (scaling.py PSD part, psdcone.py:98-117) + congruence block H = Q (x)s Q
 __global__ void psd_scaling_w(PsdArgs a, const double* s, const double* z, double* R, double* RI, double* Q,
                               double* LAM, double* hv, int* err) {
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c], ld = a.ld;
+    PSD_GROUP_LOOP(a) {
+        const int n = G.n, ld = a.ld, i = G.i;
+        const int off = n ? a.off[c] : 0;
         double *W0 = W.M[0], *W1 = W.M[1], *W2 = W.M[2], *W3 = W.M[3], *Rm = W.M[4], *RIm = W.M[5];
-        if (!pw::nt_factor(s + off, z + off, n, ld, W0, W1, W2, W3, Rm, RIm, W.lam)) {
-            if (lane == 0) set_error(err, CIPM_E_SCALING);
-            continue;
-        }
-        pw::mm(Rm, Rm, n, ld, W0, 2);                 // Q = R R'
-        double* Rc = R + a.mptr[c];
-        double* RIc = RI + a.mptr[c];
-        double* Qc = Q + a.mptr[c];
-        for (int e = lane; e < n * n; e += 32) {
-            const int i = e / n, j = e - i * n;
-            Rc[e] = Rm[i * ld + j];
-            RIc[e] = RIm[i * ld + j];
-            Qc[e] = W0[i * ld + j];
-        }
-        for (int i = lane; i < n; i += 32) LAM[a.lptr[c] + i] = W.lam[i];
-        // H(k, l), k <= l over svec indices, upper triangle row-major: row k = (p, q)
-        const int d = n * (n + 1) / 2;
-        double* hb = hv + a.hptr[c];
-        int64_t rowoff = 0;
-        int p = 0, q = 0;                                // svec index k -> (p >= q)
-        for (int k = 0; k < d; ++k) {
-            const double sk = p == q ? 1.0 : pw::kR2;
-            // entries l = k .. d-1, (i, j) of svec index l
-            for (int l = k + lane; l < d; l += 32) {
-                int j = 0, rem = l;
-                while (rem >= n - j) { rem -= n - j; ++j; }
-                const int i = j + rem;
-                double mv;
-                if (i == j) mv = W0[p * ld + i] * W0[q * ld + i];
-                else mv = (W0[p * ld + i] * W0[q * ld + j] + W0[p * ld + j] * W0[q * ld + i]) / pw::kR2;
-                hb[rowoff + (l - k)] = sk * mv;
+        const bool ok = pw::nt_factor(G, s + off, z + off, ld, W0, W1, W2, W3, Rm, RIm, W.lam);
+        if (n && !ok && i == 0) set_error(err, CIPM_E_SCALING);
+        pw::Grp H = G;
+        if (!ok) H.n = 0;
+        pw::mm(H, Rm, Rm, ld, W0, 2);               // Q = R R'
+        const int nn = H.n;
+        if (nn) {
+            double* Rc = R + a.mptr[c];
+            double* RIc = RI + a.mptr[c];
+            double* Qc = Q + a.mptr[c];
+            for (int e = i; e < nn * nn; e += G.g) {
+                const int r = e / nn, j = e - r * nn;
+                Rc[e] = Rm[r * ld + j];
+                RIc[e] = RIm[r * ld + j];
+                Qc[e] = W0[r * ld + j];
             }
-            rowoff += d - k;
-            if (++p == n) { ++q; p = q; }
+            for (int k = i; k < nn; k += G.g) LAM[a.lptr[c] + k] = W.lam[k];
+            // H(k, l), k <= l over svec indices, upper triangle row-major; row k = (p, q)
+            const int d = nn * (nn + 1) / 2;
+            double* hb = hv + a.hptr[c];
+            int64_t rowoff = 0;
+            int p = 0, q = 0;
+            for (int k = 0; k < d; ++k) {
+                const double sk = p == q ? 1.0 : pw::kR2;
+                for (int l = k + i; l < d; l += G.g) {
+                    int j = 0, rem = l;
+                    while (rem >= nn - j) { rem -= nn - j; ++j; }
+                    const int ii = j + rem;
+                    double mv;
+                    if (ii == j) mv = W0[p * ld + ii] * W0[q * ld + ii];
+                    else mv = (W0[p * ld + ii] * W0[q * ld + j] + W0[p * ld + j] * W0[q * ld + ii]) / pw::kR2;
+                    hb[rowoff + (l - k)] = sk * mv;
+                }
+                rowoff += d - k;
+                if (++p == nn) { ++q; p = q; }
+            }
         }
         __syncwarp();
     }
@@ -619,19 +637,21 @@ __global__ void psd_scaling_w(PsdArgs a, const double* s, const double* z, doubl
 __global__ void psd_apply_h_w(PsdArgs a, const double* Q, const double* v, double* out, double alpha,
                               const double* u, double beta, const double* skip) {
     if (skip && *skip != 0.0) return;
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c], ld = a.ld;
+    PSD_GROUP_LOOP(a) {
+        const int n = G.n, ld = a.ld, i = G.i;
+        const int off = n ? a.off[c] : 0;
         double *Qm = W.M[0], *X = W.M[1], *T = W.M[2];
-        for (int e = lane; e < n * n; e += 32) Qm[(e / n) * ld + e % n] = Q[a.mptr[c] + e];
+        for (int e = i; e < n * n; e += G.g) Qm[(e / n) * ld + e % n] = Q[a.mptr[c] + e];
         __syncwarp();
-        pw::smat(v + off, n, X, ld);
-        pw::mm(Qm, X, n, ld, T, 0);
-        pw::mm(T, Qm, n, ld, X, 0);
-        pw::svec(X, n, ld, W.v0);
+        if (n) pw::smat(G, v + off, X, ld);
+        else __syncwarp();
+        pw::mm(G, Qm, X, ld, T, 0);
+        pw::mm(G, T, Qm, ld, X, 0);
+        pw::svec(G, X, ld, W.v0);
         const int d = n * (n + 1) / 2;
-        for (int k = lane; k < d; k += 32) {
-            const double base = u ? alpha * u[off + k] : 0.0;
-            out[off + k] = base + beta * W.v0[k];
+        for (int k = i; k < d; k += G.g) {
+            const double b0 = u ? alpha * u[off + k] : 0.0;
+            out[off + k] = b0 + beta * W.v0[k];
         }
         __syncwarp();
     }
@@ -641,58 +661,66 @@ __global__ void psd_apply_h_w(PsdArgs a, const double* Q, const double* v, doubl
 __global__ void psd_combined_ds_w(PsdArgs a, const double* R, const double* RI, const double* LAM,
                                   const double* dz_a, const double* ds_a, const double* sc, double* out) {
     const double sigma = sc[CIPM_SC_SIGMA], mu = sc[CIPM_SC_MU];
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c], ld = a.ld;
+    PSD_GROUP_LOOP(a) {
+        const int n = G.n, ld = a.ld, i = G.i;
+        const int off = n ? a.off[c] : 0;
         double *r = W.M[0], *ri = W.M[1], *X = W.M[2], *T = W.M[3], *A = W.M[4], *B = W.M[5];
-        for (int e = lane; e < n * n; e += 32) {
+        for (int e = i; e < n * n; e += G.g) {
             r[(e / n) * ld + e % n] = R[a.mptr[c] + e];
             ri[(e / n) * ld + e % n] = RI[a.mptr[c] + e];
         }
-        for (int i = lane; i < n; i += 32) W.lam[i] = LAM[a.lptr[c] + i];
+        for (int k = i; k < n; k += G.g) W.lam[k] = LAM[a.lptr[c] + k];
         __syncwarp();
-        pw::smat(ds_a + off, n, X, ld);
-        pw::mm(ri, X, n, ld, T, 0);
-        pw::mm(T, ri, n, ld, A, 2);                  // Rinv ds Rinv'
-        pw::smat(dz_a + off, n, X, ld);
-        pw::mm(r, X, n, ld, T, 1);                   // R' dz
-        pw::mm(T, r, n, ld, B, 0);                   // R' dz R
-        pw::mm(A, B, n, ld, X, 0);
-        pw::mm(B, A, n, ld, T, 0);
-        if (lane < n) {
-            const int i = lane;
+        if (n) pw::smat(G, ds_a + off, X, ld);
+        else __syncwarp();
+        pw::mm(G, ri, X, ld, T, 0);
+        pw::mm(G, T, ri, ld, A, 2);                  // Rinv ds Rinv'
+        if (n) pw::smat(G, dz_a + off, X, ld);
+        else __syncwarp();
+        pw::mm(G, r, X, ld, T, 1);                   // R' dz
+        pw::mm(G, T, r, ld, B, 0);                   // R' dz R
+        pw::mm(G, A, B, ld, X, 0);
+        pw::mm(G, B, A, ld, T, 0);
+        if (i < n)
             for (int j = 0; j < n; ++j) {
                 const double e = 0.5 * (X[i * ld + j] + T[i * ld + j]);
                 const double rhs = (i == j ? W.lam[i] * W.lam[i] : 0.0) + e - (i == j ? sigma * mu : 0.0);
                 A[i * ld + j] = 2.0 * rhs / (W.lam[i] + W.lam[j]);
             }
-        }
         __syncwarp();
-        pw::mm(r, A, n, ld, T, 0);
-        pw::mm(T, r, n, ld, X, 2);                   // R U R'
-        pw::svec(X, n, ld, out + off);
+        pw::mm(G, r, A, ld, T, 0);
+        pw::mm(G, T, r, ld, X, 2);                   // R U R'
+        if (n) pw::svec(G, X, ld, out + off);
+        else __syncwarp();
     }
 }
 
 // sup{alpha >= 0: mat(v) + alpha mat(dv) PSD} (psdcone.py:120-133); < 0 on DomainError
-__device__ __forceinline__ double psd_step_w(const double* v, const double* dv, int n, int ld, const PwView& W) {
+__device__ __forceinline__ double psd_step_w(const pw::Grp& G, const double* v, const double* dv, int ld,
+                                             const PwView& W) {
     double *X = W.M[0], *Li = W.M[1], *D = W.M[2], *T = W.M[3];
-    pw::smat(v, n, X, ld);
-    if (!pw::chol(X, n, ld)) return -1.0;
-    pw::tri_inv(X, n, ld, Li);
-    pw::smat(dv, n, D, ld);
-    pw::mm(Li, D, n, ld, T, 0);
-    pw::mm(T, Li, n, ld, X, 2);                      // Li D Li'
-    const double lmin = pw::sym_min_eig(X, n, ld);
+    if (G.n) pw::smat(G, v, X, ld);
+    else __syncwarp();
+    const bool ok = pw::chol(G, X, ld);
+    pw::Grp H = G;
+    if (!ok) H.n = 0;
+    pw::tri_inv(H, X, ld, Li);
+    if (H.n) pw::smat(H, dv, D, ld);
+    else __syncwarp();
+    pw::mm(H, Li, D, ld, T, 0);
+    pw::mm(H, T, Li, ld, X, 2);                      // Li D Li'
+    const double lmin = pw::sym_min_eig(H, X, ld);
+    if (!ok) return -1.0;
     return lmin >= 0.0 ? INFINITY : -1.0 / lmin;
 }
 
 __global__ void psd_step_bound_w(PsdArgs a, const double* z, const double* s, const double* dz, const double* ds,
                                  double* sc, int* err) {
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c];
-        const double b1 = psd_step_w(z + off, dz + off, n, a.ld, W);
-        const double b2 = psd_step_w(s + off, ds + off, n, a.ld, W);
-        if (lane == 0) {
+    PSD_GROUP_LOOP(a) {
+        const int off = G.n ? a.off[c] : 0;
+        const double b1 = psd_step_w(G, z + off, dz + off, a.ld, W);
+        const double b2 = psd_step_w(G, s + off, ds + off, a.ld, W);
+        if (G.n && G.i == 0) {
             if (b1 < 0.0 || b2 < 0.0) set_error(err, CIPM_E_DOMAIN);
             else {
                 const double b = fmin(b1, b2);
@@ -704,58 +732,64 @@ __global__ void psd_step_bound_w(PsdArgs a, const double* z, const double* s, co
 }
 
 // tr(S^-1 Z^-1); false if either is not positive definite
-__device__ __forceinline__ bool psd_trace_inv_w(const double* sv, const double* zv, int n, int ld, const PwView& W,
-                                                double* tr) {
+__device__ __forceinline__ bool psd_trace_inv_w(const pw::Grp& G, const double* sv, const double* zv, int ld,
+                                                const PwView& W, double* tr) {
     double *X = W.M[0], *Li = W.M[1], *Si = W.M[2], *Zi = W.M[3];
-    pw::smat(sv, n, X, ld);
-    if (!pw::chol(X, n, ld)) return false;
-    pw::tri_inv(X, n, ld, Li);
-    pw::mm(Li, Li, n, ld, Si, 1);                    // L^-T L^-1 = S^-1
-    pw::smat(zv, n, X, ld);
-    if (!pw::chol(X, n, ld)) return false;
-    pw::tri_inv(X, n, ld, Li);
-    pw::mm(Li, Li, n, ld, Zi, 1);
-    const int i = threadIdx.x & 31;
+    if (G.n) pw::smat(G, sv, X, ld);
+    else __syncwarp();
+    bool ok = pw::chol(G, X, ld);
+    pw::tri_inv(G, X, ld, Li);
+    pw::mm(G, Li, Li, ld, Si, 1);                    // L^-T L^-1 = S^-1
+    if (G.n) pw::smat(G, zv, X, ld);
+    else __syncwarp();
+    ok = pw::chol(G, X, ld) && ok;
+    pw::tri_inv(G, X, ld, Li);
+    pw::mm(G, Li, Li, ld, Zi, 1);
     double acc = 0.0;
-    if (i < n)
-        for (int j = 0; j < n; ++j) acc += Si[i * ld + j] * Zi[j * ld + i];
-    *tr = pw::wsum(acc);
-    return true;
+    if (G.i < G.n)
+        for (int j = 0; j < G.n; ++j) acc += Si[G.i * ld + j] * Zi[j * ld + G.i];
+    *tr = pw::gsum(acc, G.g);
+    return ok;
 }
 
 __global__ void psd_neighborhood_w(PsdArgs a, const double* s, const double* z, const double* ds, const double* dz,
                                    const double* nb, int nk, double beta, unsigned int* mask, int* err) {
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c];
+    PSD_GROUP_LOOP(a) {
+        const int n = G.n;
+        const int off = n ? a.off[c] : 0;
         const int d = n * (n + 1) / 2;
         unsigned int bits = 0u;
         for (int k = 0; k < nk; ++k) {
             const double step = nb[16 + k];
-            for (int e = lane; e < d; e += 32) {
+            for (int e = G.i; e < d; e += G.g) {
                 W.v0[e] = s[off + e] + step * ds[off + e];
                 W.v1[e] = z[off + e] + step * dz[off + e];
             }
             __syncwarp();
             double tr;
-            if (!psd_trace_inv_w(W.v0, W.v1, n, a.ld, W, &tr)) {
-                if (lane == 0) set_error(err, CIPM_E_DOMAIN);
+            const bool ok = psd_trace_inv_w(G, W.v0, W.v1, a.ld, W, &tr);
+            if (!n) continue;
+            if (!ok) {
+                if (G.i == 0) set_error(err, CIPM_E_DOMAIN);
                 continue;
             }
             if (!((double)n / tr < beta * nb[k])) bits |= 1u << k;
         }
-        if (lane == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
+        if (n && G.i == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
         __syncwarp();
     }
 }
 
 __global__ void psd_membership_w(PsdArgs a, const double* s, const double* z, int* err) {
-    PSD_WARP_LOOP(a) {
-        const int n = a.side[c], off = a.off[c];
-        pw::smat(s + off, n, W.M[0], a.ld);
-        const bool ok1 = pw::chol(W.M[0], n, a.ld);
-        pw::smat(z + off, n, W.M[1], a.ld);
-        const bool ok2 = pw::chol(W.M[1], n, a.ld);
-        if (lane == 0 && (!ok1 || !ok2)) set_error(err, CIPM_E_INTERIOR);
+    PSD_GROUP_LOOP(a) {
+        const int off = G.n ? a.off[c] : 0;
+        if (G.n) pw::smat(G, s + off, W.M[0], a.ld);
+        else __syncwarp();
+        const bool ok1 = pw::chol(G, W.M[0], a.ld);
+        if (G.n) pw::smat(G, z + off, W.M[1], a.ld);
+        else __syncwarp();
+        const bool ok2 = pw::chol(G, W.M[1], a.ld);
+        if (G.n && G.i == 0 && (!ok1 || !ok2)) set_error(err, CIPM_E_INTERIOR);
         __syncwarp();
     }
 }
@@ -794,14 +828,17 @@ PsdArgs psd_args(Ctx& c) {
     a.hptr = c.psd_hptr;
     a.nmax = c.psd_max_side;
     a.ld = c.psd_max_side | 1;
+    a.gw = c.psd_max_side <= 8 ? 8 : (c.psd_max_side <= 16 ? 16 : 32);
     return a;
 }
 
 inline int warp_grid(int64_t nwarps) { return grid_for(nwarps * 32); }
 
-// warp-per-cone PSD launch: warps per CTA from the slice size (<= 96 KiB per CTA)
+// group-per-cone PSD launch: slices per warp = 32 / gw; warps per CTA from the slice
+// size (<= 96 KiB per CTA)
 inline size_t psd_slice_bytes(const PsdArgs& a) {
-    return sizeof(double) * (size_t)(PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2);
+    return sizeof(double) * (size_t)(32 / a.gw) *
+           (size_t)(PW_MATS * a.nmax * a.ld + 2 * (a.nmax * (a.nmax + 1) / 2) + a.nmax + 2);
 }
 
 #define PSD_DISPATCH(KERNEL, ...)                                                                      \
@@ -811,7 +848,7 @@ inline size_t psd_slice_bytes(const PsdArgs& a) {
         int wpb_ = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / sl_));                   \
         const size_t smem_ = sl_ * (size_t)wpb_;                                                       \
         if (smem_ > 48 * 1024) cudaFuncSetAttribute(KERNEL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_); \
-        const int64_t blocks_ = (c.npsd + wpb_ - 1) / wpb_;                                            \
+        const int64_t blocks_ = (c.npsd + (int64_t)wpb_ * (32 / pa_.gw) - 1) / ((int64_t)wpb_ * (32 / pa_.gw)); \
         KERNEL<<<(int)std::min<int64_t>(blocks_, 148 * 32), wpb_ * 32, smem_, c.stream>>>(__VA_ARGS__); \
         c.launches++;                                                                                  \
     } while (0)
