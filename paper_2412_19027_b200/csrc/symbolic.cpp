@@ -330,6 +330,100 @@ struct NdWork {
         for (int32_t v : nodes) { part[v] = -1; loc[v] = -1; }
     }
 
+    // minimum vertex cover of the edges between BFS levels sl and sl+1 of the part
+    // (queue[0..cnt) holds the part's nodes with their levels); cover[k] marks queue[k]
+    void min_cover_between_levels(int64_t cnt, int32_t id, int32_t sl, std::vector<char>& cover) {
+        min_cover_between_levels(queue, cnt, id, sl, cover);
+    }
+    void min_cover_between_levels(const std::vector<int32_t>& q, int64_t cnt, int32_t id, int32_t sl,
+                                  std::vector<char>& cover) {
+        cover.assign(cnt, 0);
+        // U = level sl nodes with an edge to sl+1, V = level sl+1 nodes with an edge to sl
+        std::vector<int32_t> U, V;
+        for (int64_t k = 0; k < cnt; ++k) {
+            const int32_t v = q[k];
+            if (level[v] != sl && level[v] != sl + 1) continue;
+            const int32_t other = level[v] == sl ? sl + 1 : sl;
+            bool touches = false;
+            for (int64_t p = g.ptr[v]; p < g.ptr[v + 1] && !touches; ++p) {
+                const int32_t u = g.idx[p];
+                touches = part[u] == id && level[u] == other;
+            }
+            if (!touches) continue;
+            loc[v] = (int32_t)(level[v] == sl ? U.size() : V.size());
+            (level[v] == sl ? U : V).push_back(v);
+        }
+        const int32_t nu = (int32_t)U.size(), nv = (int32_t)V.size();
+        std::vector<int32_t> mu(nu, -1), mv(nv, -1), dist(nu);
+        auto nbrs = [&](int32_t ui, auto&& f) {
+            const int32_t v = U[ui];
+            for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
+                const int32_t w = g.idx[p];
+                if (part[w] == id && level[w] == sl + 1 && loc[w] >= 0) f(loc[w]);
+            }
+        };
+        // Hopcroft-Karp
+        std::vector<int32_t> bfsq(nu);
+        for (;;) {
+            int64_t h = 0, t = 0;
+            bool found = false;
+            for (int32_t ui = 0; ui < nu; ++ui) {
+                dist[ui] = mu[ui] < 0 ? 0 : -1;
+                if (mu[ui] < 0) bfsq[t++] = ui;
+            }
+            while (h < t) {
+                const int32_t ui = bfsq[h++];
+                nbrs(ui, [&](int32_t vi) {
+                    const int32_t u2 = mv[vi];
+                    if (u2 < 0) found = true;
+                    else if (dist[u2] < 0) { dist[u2] = dist[ui] + 1; bfsq[t++] = u2; }
+                });
+            }
+            if (!found) break;
+            std::function<bool(int32_t)> dfs = [&](int32_t ui) -> bool {
+                const int32_t v = U[ui];
+                for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
+                    const int32_t w = g.idx[p];
+                    if (!(part[w] == id && level[w] == sl + 1 && loc[w] >= 0)) continue;
+                    const int32_t vi = loc[w], u2 = mv[vi];
+                    if (u2 < 0 || (dist[u2] == dist[ui] + 1 && dfs(u2))) {
+                        mu[ui] = vi;
+                        mv[vi] = ui;
+                        return true;
+                    }
+                }
+                dist[ui] = -1;
+                return false;
+            };
+            for (int32_t ui = 0; ui < nu; ++ui)
+                if (mu[ui] < 0) dfs(ui);
+        }
+        // Koenig: Z = reachable from unmatched U by alternating paths; cover = (U \ Z) + (V & Z)
+        std::vector<char> zu(nu, 0), zv(nv, 0);
+        std::vector<int32_t> st;
+        for (int32_t ui = 0; ui < nu; ++ui)
+            if (mu[ui] < 0) { zu[ui] = 1; st.push_back(ui); }
+        while (!st.empty()) {
+            const int32_t ui = st.back();
+            st.pop_back();
+            nbrs(ui, [&](int32_t vi) {
+                if (zv[vi] || mu[ui] == vi) return;
+                zv[vi] = 1;
+                const int32_t u2 = mv[vi];
+                if (u2 >= 0 && !zu[u2]) { zu[u2] = 1; st.push_back(u2); }
+            });
+        }
+        std::vector<char> inS(0);
+        for (int64_t k = 0; k < cnt; ++k) {
+            const int32_t v = q[k];
+            if (loc[v] < 0) continue;
+            if (level[v] == sl) cover[k] = zu[loc[v]] ? 0 : 1;
+            else if (level[v] == sl + 1) cover[k] = zv[loc[v]] ? 1 : 0;
+        }
+        for (int32_t v : U) loc[v] = -1;
+        for (int32_t v : V) loc[v] = -1;
+    }
+
     // order the part `id` whose nodes are `nodes` (appends to out)
     void dissect(std::vector<int32_t> nodes) {
         struct Item { std::vector<int32_t> nodes; int stage; std::vector<int32_t> sep; };
@@ -412,22 +506,21 @@ struct NdWork {
                     continue;
                 }
             }
-            // separator: level-sl nodes adjacent to level sl+1 (the rest join the low side)
+            // separator: a minimum vertex cover of the bipartite graph of the edges
+            // between levels sl and sl+1 (Koenig: maximum matching, then the cover from
+            // the alternating reachability), never larger than the level-sl boundary; the
+            // uncovered level-sl nodes join the low side, the uncovered level-(sl+1) nodes
+            // the high side (BFS levels only touch adjacent levels, so the cover separates)
             const int32_t lo = next_id++, hi = next_id++;
             std::vector<int32_t> A, B, S;
+            std::vector<char> cover;
+            min_cover_between_levels(queue, cnt, id, sl, cover);
             for (int64_t k = 0; k < cnt; ++k) {
                 int32_t v = queue[k];
                 int32_t lv = level[v];
-                if (lv < sl) A.push_back(v);
-                else if (lv > sl) B.push_back(v);
-                else {
-                    bool touches = false;
-                    for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
-                        int32_t u = g.idx[p];
-                        if (part[u] == id && level[u] == sl + 1) { touches = true; break; }
-                    }
-                    (touches ? S : A).push_back(v);
-                }
+                if (cover[k]) S.push_back(v);
+                else if (lv <= sl) A.push_back(v);
+                else B.push_back(v);
             }
             clear_levels(cnt);
             const int32_t sid = next_id++;
@@ -444,10 +537,21 @@ struct NdWork {
 
 std::vector<int32_t> nested_dissection(const Graph& g, int64_t dim, int64_t leaf) {
     NdWork w(g, dim, leaf);
-    std::vector<int32_t> all(dim);
-    std::iota(all.begin(), all.end(), 0);
     w.out.reserve(dim);
-    if (dim > 0) w.dissect(std::move(all));
+    // pendant nodes (degree <= 1: e.g. the lasso's y_i hanging off its zero row) are
+    // eliminated first — no fill — and kept out of the BFS levels, where every
+    // pendant edge would otherwise have to be cut by the separator
+    std::vector<int32_t> rest;
+    rest.reserve(dim);
+    for (int64_t v = 0; v < dim; ++v) {
+        if (g.ptr[v + 1] - g.ptr[v] <= 1) {
+            w.out.push_back((int32_t)v);
+            w.part[v] = -1;
+        } else {
+            rest.push_back((int32_t)v);
+        }
+    }
+    if (!rest.empty()) w.dissect(std::move(rest));
     return w.out;
 }
 
