@@ -264,5 +264,7 @@ void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total);
 void k_tail_factor(Ctx& c);
 void k_tail_forward(Ctx& c, void* x, int act0, int act1);
 void k_tail_backward(Ctx& c, void* x, int act0, int act1);
+bool tail_is_single_root(const Ctx& c);
+void k_root_solve(Ctx& c, void* x, int act0, int act1);   // tail = one dense root: fwd + D + bwd in one CTA
 
 }  // namespace cipm

@@ -25,6 +25,8 @@
 // the diagonal solves are GEMVs with the precomputed block inverses.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <type_traits>
 
 #include "common.cuh"
@@ -687,6 +689,147 @@ __global__ void __launch_bounds__(256) tail_bwd(TailSolveArgs a0, const T* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// single dense ROOT (the whole tail is one supernode with no off rows, w <= 256:
+// C2, C3, C5a): forward, D and backward solve of the root in ONE CTA of 1024
+// threads, right-hand sides in shared memory — replaces the tail_fwd / tail_bwd
+// pair (multi-CTA wavefronts that synchronise through global flags, ~20 us each
+// for a 4-block root) with block GEMVs separated by CTA barriers.
+//   forward  y_b = inv(L_bb) (t_b - sum_{k<b} L_bk y_k)      (inv row-major, per 64-block)
+//   backward x_b = inv(L_bb)' (y_b / D_b - sum_{i>b} L_ib' x_i)
+// Partial sums: 16 threads per row / column, fixed-order combination.
+// ---------------------------------------------------------------------------
+constexpr int RT = 1024, RP = RT / TB;      // threads, partial sums per row (16)
+
+template <typename T>
+__global__ void __launch_bounds__(RT) root_solve(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
+                                                 const T* __restrict__ dvec, T* x, const T* __restrict__ vin) {
+    TailSolveArgs a = a0;
+    if (a.rstate) {
+        a.act0 = a.act0 && a.rstate[4] == 0.0;
+        a.act1 = a.act1 && a.rstate[12] == 0.0;
+    }
+    const int tid = threadIdx.x;
+    const int w = a.w, r = a.r;
+    __shared__ T xs[2][256];
+    __shared__ T acc[2][TB];
+    __shared__ T part[RP][2][TB];
+    if (!a.act0 && !a.act1) {
+        if (tid == 0) st_release(a.done, 1);
+        return;
+    }
+    const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    // 1. right-hand side of the root columns minus the non-tiny vector inbox
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        T v = (T)0;
+        if (act[q]) {
+            const int col = a.c0 + j;
+            v = x[q * a.dim + col];
+            const T* vq = vin + q * a.nv;
+            for (int64_t p = a.vn_lo[col]; p < a.vn_hi[col]; ++p) v -= __ldcg(vq + p);
+        }
+        xs[q][j] = v;
+    }
+    __syncthreads();
+    const int ri = tid & (TB - 1), kp = tid >> 6;       // row / column within the block, partial index
+    // 2. forward, block by block
+    for (int b = 0; b < a.nbd; ++b) {
+        const int row0 = b * TB, nb = min(TB, w - row0);
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nb)
+            for (int k = kp; k < row0; k += RP) {
+                const T l = L[(int64_t)k * r + row0 + ri];
+                p0 += l * xs[0][k];
+                p1 += l * xs[1][k];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, i = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][i];
+            acc[q][i] = i < nb ? xs[q][row0 + i] - s : (T)0;
+        }
+        __syncthreads();
+        const T* Ib = inv + (int64_t)b * TB * TB;           // row-major lower inverse of L_bb
+        p0 = (T)0;
+        p1 = (T)0;
+        if (ri < nb)
+            for (int t = kp; t <= ri; t += RP) {
+                const T iv = Ib[ri * TB + t];
+                p0 += iv * acc[0][t];
+                p1 += iv * acc[1][t];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, i = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][i];
+            if (i < nb) xs[q][row0 + i] = s;
+        }
+        __syncthreads();
+    }
+    // 3. D solve (ldl.py:101-102)
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        xs[q][j] = xs[q][j] / dvec[a.c0 + j];
+    }
+    __syncthreads();
+    // 4. backward, last block first
+    for (int b = a.nbd - 1; b >= 0; --b) {
+        const int col0 = b * TB, nb = min(TB, w - col0), i0 = col0 + nb;
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nb) {
+            const T* Lc = L + (int64_t)(col0 + ri) * r;
+            for (int i = i0 + kp; i < w; i += RP) {
+                const T l = Lc[i];
+                p0 += l * xs[0][i];
+                p1 += l * xs[1][i];
+            }
+        }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, j = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][j];
+            acc[q][j] = j < nb ? xs[q][col0 + j] - s : (T)0;
+        }
+        __syncthreads();
+        const T* Ib = inv + (int64_t)b * TB * TB;
+        p0 = (T)0;
+        p1 = (T)0;
+        if (ri < nb)
+            for (int t = ri + kp; t < nb; t += RP) {          // x_j = sum_{t >= j} inv[t][j] acc_t
+                const T iv = Ib[t * TB + ri];
+                p0 += iv * acc[0][t];
+                p1 += iv * acc[1][t];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, j = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][j];
+            if (j < nb) xs[q][col0 + j] = s;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        if (act[q]) x[q * a.dim + a.c0 + j] = xs[q][j];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(a.done, 1);
+}
+
 template <typename T>
 void tail_factor_t(Ctx& c) {
     static bool attr = false;
@@ -779,6 +922,14 @@ void tail_forward_t(Ctx& c, T* x, int act0, int act1) {
 }
 
 template <typename T>
+void root_solve_t(Ctx& c, T* x, int act0, int act1) {
+    const TailNode& t = c.tail[0];
+    root_solve<T><<<1, RT, 0, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
+                                          (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x, (const T*)c.vin);
+    c.launches++;
+}
+
+template <typename T>
 void tail_backward_t(Ctx& c, T* x, int act0, int act1) {
     for (auto it = c.tail.rbegin(); it != c.tail.rend(); ++it) {
         const TailNode& t = *it;
@@ -826,6 +977,15 @@ void k_tail_forward(Ctx& c, void* x, int act0, int act1) {
     if (c.tail.empty()) return;
     if (c.precision == CIPM_FULL) tail_forward_t<double>(c, (double*)x, act0, act1);
     else tail_forward_t<float>(c, (float*)x, act0, act1);
+}
+
+bool tail_is_single_root(const Ctx& c) {
+    return c.tail.size() == 1 && c.tail[0].r == c.tail[0].w && c.tail[0].w <= 256 && !getenv("CIPM_NO_ROOT_SOLVE");
+}
+
+void k_root_solve(Ctx& c, void* x, int act0, int act1) {
+    if (c.precision == CIPM_FULL) root_solve_t<double>(c, (double*)x, act0, act1);
+    else root_solve_t<float>(c, (float*)x, act0, act1);
 }
 
 void k_tail_backward(Ctx& c, void* x, int act0, int act1) {

@@ -1696,10 +1696,15 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     pt.mark("fold");
     if (f.nstart > 0) forward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
     pt.mark("forward");
-    k_tail_forward(c, t, act0, act1);
-    pt.mark("tail_fwd");
-    k_tail_backward(c, t, act0, act1);
-    pt.mark("tail_bwd");
+    if (tail_is_single_root(c)) {
+        k_root_solve(c, t, act0, act1);
+        pt.mark("root_solve");
+    } else {
+        k_tail_forward(c, t, act0, act1);
+        pt.mark("tail_fwd");
+        k_tail_backward(c, t, act0, act1);
+        pt.mark("tail_bwd");
+    }
     SolveArgs b = solve_args(c, c.bwd_done, c.tickets + 2, act0, act1);
     b.ticket_tiny = c.tickets + 6;
     if (b.n_main > 0)
