@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int k
                 if (lane < nbk && c <= lane) Sk[c * TB + row] = x[c];
                 if (lane < SB) sLt[c * SB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;
             }
+            __syncwarp();
             if (lane == 0) s_runmax = runmax;
         }
         __syncthreads();
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
         if (s < nk) load_stage(s);
         cp_async_commit();
     }
-    double acc[4][4][2];
+    T acc[4][4][2];                                 // FP64: DMMA accumulators; FP32: FFMA (true FP32, as the reference's factor)
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -405,8 +406,8 @@ __global__ void __launch_bounds__(128) tail_gemm(const T* A, int lda, const T* _
                 for (int a = 0; a < 4; ++a)
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        acc[a][b][0] += (double)(af[a] * bf[b][0]);
-                        acc[a][b][1] += (double)(af[a] * bf[b][1]);
+                        acc[a][b][0] = fmaf(af[a], bf[b][0], acc[a][b][0]);
+                        acc[a][b][1] = fmaf(af[a], bf[b][1], acc[a][b][1]);
                     }
             }
         }

@@ -493,6 +493,7 @@ __device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, co
         if (lane < nbk && c < nbk && c <= lane) Pk[c * r + row] = x[c];
         if (lane < NB) sLt[c * NB + lane] = (c < lane && lane < nbk) ? x[c] : (T)0;   // Lt[j][i] = l_ij
     }
+    __syncwarp();                           // every lane read s_runmax before lane 0 updates it
     if (lane == 0) s_runmax = runmax;
 }
 

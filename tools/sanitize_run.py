@@ -19,7 +19,15 @@ cases = {
     "socp": (G.gen_socp(60, seed=1), "full"),
     "psd": (G.gen_psd(40, side=4, seed=1), "full"),
     "exppow": (G.gen_exppow(60, 20, seed=1), "full"),
+    "lasso_nd": (G.gen_lasso(200, 800, seed=1), "mixed"),
+    "psd_side20": (G.gen_psd(2, side=20, seed=1), "full"),
 }
+if which in ("all", "batch"):
+    from paper_2412_19027_b200.batch import BatchSolver
+    bs = BatchSolver(G.build_instances("c5b_mpc", 0, 4), SolverSettings(eps_feas=1e-8))
+    out = bs.solve()
+    bs.close()
+    print("batch", [r.status for r in out], [r.iterations for r in out], flush=True)
 for name, (prob, prec) in cases.items():
     if which != "all" and which != name:
         continue
