@@ -1002,6 +1002,7 @@ extern "C" {
 
 int cipm_batch_create(const cipm_problem_desc* d, int count, const cipm_settings* st, double eps_feas,
                       double eps_inf, int max_iter, cipm_batch** out) {
+    CIPM_NVTX("cipm_batch_create");
     using namespace cipm;
     if (!d || !st || !out || count <= 0) return CIPM_E_ARG;
     if (d->n_soc || d->n_exp || d->n_pow || d->n_psd) {
@@ -1459,6 +1460,7 @@ int cipm_batch_set_reorder(cipm_batch* h, const int64_t* row_perm, const int64_t
 }
 
 int cipm_batch_set_raw_values(cipm_batch* h, const double* V, const double* q, const double* b, int equilibrate) {
+    CIPM_NVTX("cipm_batch_set_raw_values");
     if (!h || !h->pt.b_src) return CIPM_E_ARG;
     const int64_t c = h->count, n = h->pt.n, m = h->pt.m, nv = (int64_t)h->pt.nnz_p + h->pt.nnz_a;
     CIPM_CUDA(cudaSetDevice(h->device));
@@ -1484,6 +1486,7 @@ int cipm_batch_set_raw_values(cipm_batch* h, const double* V, const double* q, c
 }
 
 int cipm_batch_solve(cipm_batch* h, double* ms) {
+    CIPM_NVTX("cipm_batch_solve");
     if (!h) return CIPM_E_ARG;
     CIPM_CUDA(cudaSetDevice(h->device));
     CIPM_CUDA(cudaEventRecord(h->ev0, h->stream));
@@ -1501,6 +1504,7 @@ int cipm_batch_solve(cipm_batch* h, double* ms) {
 }
 
 int cipm_batch_results(cipm_batch* h, int32_t* status, double* res, double* x, double* z, double* s) {
+    CIPM_NVTX("cipm_batch_results");
     if (!h) return CIPM_E_ARG;
     const int64_t c = h->count, n = h->pt.n, m = h->pt.m;
     CIPM_CUDA(cudaSetDevice(h->device));

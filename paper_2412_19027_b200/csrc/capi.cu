@@ -315,6 +315,7 @@ int cipm_symbolic_create(const cipm_problem_desc* d, int ordering, cipm_symbolic
 }
 
 int cipm_symbolic_create_ex(const cipm_problem_desc* d, int ordering, int64_t nd_leaf, cipm_symbolic** out) {
+    CIPM_NVTX("cipm_symbolic_create_ex");
     if (!d || !out || ordering < 0 || ordering > 4 || nd_leaf < 0) return CIPM_E_ARG;
     auto* h = new cipm_symbolic();
     std::vector<int64_t> off, dim;
@@ -399,6 +400,7 @@ int cipm_symbolic_array(const cipm_symbolic* sym, const char* name, void* dst, i
 void cipm_symbolic_destroy(cipm_symbolic* sym) { delete sym; }
 
 int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const cipm_settings* st, cipm_ctx** out) {
+    CIPM_NVTX("cipm_ctx_create");
     if (!d || !symh || !st || !out) return CIPM_E_ARG;
     for (int64_t i = 0; i < d->n_psd; ++i)
         if (d->psd_side[i] > 32) {      // problem.py:36 PSD_MAX_SIDE (one warp per cone, lane = row)
@@ -711,6 +713,9 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     CIPM_CUDA(cudaMallocHost((void**)&c.h_err, sizeof(int)));
     CIPM_CUDA(cudaMallocHost((void**)&c.h_rstate, sizeof(double) * 16));
     for (int i = 0; i < 4; ++i) CIPM_CUDA(cudaEventCreate(&c.ev[i]));
+    CIPM_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    CIPM_CUDA(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
+    CIPM_CUDA(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
     c.factor_blocks = factor_grid(c);
     c.solve_blocks = solve_grid(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
@@ -721,6 +726,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
 
 int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const double* q, const double* b,
                         const double* dr, const double* dc, double c_obj) {
+    CIPM_NVTX("cipm_ctx_set_values");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     CIPM_CUDA(cudaSetDevice(c.device));
@@ -756,6 +762,7 @@ int cipm_ctx_set_reorder(cipm_ctx* h, const int64_t* row_perm, const int64_t* a_
 
 int cipm_ctx_set_problem(cipm_ctx* h, const double* p_values, const double* a_values, const double* q,
                          const double* b, int equilibrate) {
+    CIPM_NVTX("cipm_ctx_set_problem");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     if (!c.have_reorder) return CIPM_E_ARG;
@@ -816,6 +823,9 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     for (int i = 0; i < 4; ++i)
         if (c.ev[i]) cudaEventDestroy(c.ev[i]);
     for (auto e : c.ev_pool) cudaEventDestroy(e);
+    if (c.fork_ev) cudaEventDestroy(c.fork_ev);
+    if (c.join_ev) cudaEventDestroy(c.join_ev);
+    if (c.side) cudaStreamDestroy(c.side);
     for (auto& g : c.refine_graph)
         if (g) cudaGraphExecDestroy(g);
     if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);
@@ -842,6 +852,7 @@ int cipm_device_bytes(const cipm_ctx* h, int64_t* bytes) {
 }
 
 int cipm_init_iterate(cipm_ctx* h) {
+    CIPM_NVTX("cipm_init_iterate");
     Ctx& c = h->c;
     CIPM_CUDA(cudaSetDevice(c.device));
     CIPM_CUDA(cudaMemsetAsync(c.err, 0, sizeof(int), c.stream));
@@ -850,6 +861,7 @@ int cipm_init_iterate(cipm_ctx* h) {
 }
 
 int cipm_residuals(cipm_ctx* h, double* out) {
+    CIPM_NVTX("cipm_residuals");
     Ctx& c = h->c;
     k_residuals(c);
     int e = read_sc(c);
@@ -863,11 +875,13 @@ int cipm_save_best(cipm_ctx* h) {
 }
 
 int cipm_update_scaling(cipm_ctx* h) {
+    CIPM_NVTX("cipm_update_scaling");
     k_update_scaling(h->c);
     return CIPM_OK;
 }
 
 int cipm_factor(cipm_ctx* h) {
+    CIPM_NVTX("cipm_factor");
     Ctx& c = h->c;
     c.num_numeric++;
     // the whole factorisation (assembly, persistent tiers, dense tail) is a static
@@ -894,6 +908,7 @@ int cipm_factor(cipm_ctx* h) {
 }
 
 int cipm_solve_affine(cipm_ctx* h, int* steps) {
+    CIPM_NVTX("cipm_solve_affine");
     Ctx& c = h->c;
     k_affine_rhs(c);
     int e = refine(c, 2, steps);
@@ -908,6 +923,7 @@ int cipm_solve_affine(cipm_ctx* h, int* steps) {
 int cipm_step_affine(cipm_ctx* h) { return step_length(h->c, 0); }
 
 int cipm_solve_combined(cipm_ctx* h, int* steps) {
+    CIPM_NVTX("cipm_solve_combined");
     Ctx& c = h->c;
     k_combined_ds(c, c.dz[0], c.ds[0]);
     k_combined_rhs(c);
@@ -919,6 +935,7 @@ int cipm_solve_combined(cipm_ctx* h, int* steps) {
 }
 
 int cipm_step_combined(cipm_ctx* h, double* alpha) {
+    CIPM_NVTX("cipm_step_combined");
     Ctx& c = h->c;
     int e = step_length(c, 1);
     if (e) return e;
@@ -936,12 +953,14 @@ int cipm_step_combined(cipm_ctx* h, double* alpha) {
 }
 
 int cipm_take_step(cipm_ctx* h) {
+    CIPM_NVTX("cipm_take_step");
     Ctx& c = h->c;
     k_take_step(c);
     return read_sc(c);
 }
 
 int cipm_loop_begin(cipm_ctx* h, double norm_q, double norm_b, double eps_feas, double eps_inf, int max_iter) {
+    CIPM_NVTX("cipm_loop_begin");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     CIPM_CUDA(cudaSetDevice(c.device));
@@ -957,6 +976,7 @@ int cipm_loop_begin(cipm_ctx* h, double norm_q, double norm_b, double eps_feas, 
 }
 
 int cipm_loop_check(cipm_ctx* h, int iteration, double* sc_out) {
+    CIPM_NVTX("cipm_loop_check");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     k_residuals(c);
@@ -967,6 +987,7 @@ int cipm_loop_check(cipm_ctx* h, int iteration, double* sc_out) {
 }
 
 int cipm_loop_body(cipm_ctx* h) {
+    CIPM_NVTX("cipm_loop_body");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     int e;
@@ -1055,6 +1076,7 @@ int cipm_set_iterate(cipm_ctx* h, const double* x, const double* z, const double
 }
 
 int cipm_kkt_solve(cipm_ctx* h, const double* rhs, double* x, int* steps, double* residual) {
+    CIPM_NVTX("cipm_kkt_solve");
     Ctx& c = h->c;
     CIPM_CUDA(cudaMemcpyAsync(c.rb, rhs, sizeof(double) * c.dim, cudaMemcpyHostToDevice, c.stream));
     int e = refine(c, 1, steps);

@@ -4,9 +4,19 @@
 #include <cstdint>
 #include <cstdio>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/cipm.h"
 
 namespace cipm {
+
+// NVTX range around a C-ABI entry point (header-only NVTX v3: no library to
+// link; a no-op unless a profiler injects itself).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define CIPM_NVTX(name) ::cipm::NvtxRange nvtx_range__(name)
 
 constexpr int kThreads = 256;
 constexpr int kMaxRedBlocks = 1184;     // 148 SMs x 8 — fixed grid => deterministic reductions

@@ -71,6 +71,9 @@ struct TailNode {
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // side stream: the solve-form pass runs beside the dense tail factorisation
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool own_stream = false;
     int64_t n = 0, m = 0, dim = 0;
     int precision = CIPM_FULL;

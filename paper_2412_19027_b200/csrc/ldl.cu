@@ -1616,15 +1616,31 @@ int factor_t(Ctx& c) {
                                                                                        (T*)c.inbox);
         c.launches++;
     }
-    k_tail_factor(c);
+    // the solve-form pass only touches warp / CTA-tier panels, which the dense
+    // tail never reads (it consumes their inbox contributions): run it on the
+    // side stream while the tail factorises (fork / join; captured into the
+    // factor graph as two parallel branches)
     const int nsf = (int)c.host_sym.bwd_order.size();
-    if (nsf > 0 && c.solve_form) {
+    const bool sf = nsf > 0 && c.solve_form;
+    static const bool overlap = !getenv("CIPM_SF_SERIAL");
+    cudaStream_t sfs = c.stream;
+    if (sf && overlap) {
+        cudaEventRecord(c.fork_ev, c.stream);
+        cudaStreamWaitEvent(c.side, c.fork_ev, 0);
+        sfs = c.side;
+    }
+    if (sf) {
         const int slice = (int)c.solve_form_slice;
         const size_t smem = sizeof(T) * (size_t)(c.solve_form_inv + slice) * SFW;
-        solve_form_kernel<T><<<c.solve_form_blocks, SFW * 32, smem, c.stream>>>(c.sym.bwd_order, nsf, c.sym.desc32,
-                                                                                c.sym.desc64, (T*)c.lval, slice,
-                                                                                c.solve_form_inv, c.sf_tau, c.sf_flag);
+        solve_form_kernel<T><<<c.solve_form_blocks, SFW * 32, smem, sfs>>>(c.sym.bwd_order, nsf, c.sym.desc32,
+                                                                           c.sym.desc64, (T*)c.lval, slice,
+                                                                           c.solve_form_inv, c.sf_tau, c.sf_flag);
         c.launches++;
+    }
+    k_tail_factor(c);
+    if (sf && overlap) {
+        cudaEventRecord(c.join_ev, c.side);
+        cudaStreamWaitEvent(c.stream, c.join_ev, 0);
     }
     if (c.profile) {
         cudaEventRecord(pooled_event(c, e0 + 1), c.stream);
