@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -21,6 +22,8 @@ void k_nsym_resolve(Ctx& c);
 void k_step_store(Ctx& c, int which);
 void k_nb_resolve(Ctx& c, int g0, int nk);
 void k_kkt_residual_one(Ctx& c, int q);
+void k_kkt_residual(Ctx& c, int nrhs);
+void k_refine_finish(Ctx& c, int nrhs);
 void k_kkt_matvec_only(Ctx& c, int q);
 void k_refine_init_one(Ctx& c, int q);
 void k_copy(Ctx& c, const double* src, double* dst, int64_t n);
@@ -117,7 +120,7 @@ int refine_graph(Ctx& c, int nrhs, int* steps_out) {
         CIPM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         int active[2] = {1, nrhs > 1 ? 1 : 0};
         k_refine_step(c, nrhs, active);
-        for (int q = 0; q < nrhs; ++q) k_kkt_residual_one(c, q);
+        k_kkt_residual(c, nrhs);
         k_refine_continue(c, h, nrhs);
         cudaGraph_t captured = nullptr;
         cudaError_t e = cudaStreamEndCapture(c.stream, &captured);
@@ -134,6 +137,7 @@ int refine_graph(Ctx& c, int nrhs, int* steps_out) {
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
     CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
     CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
+    k_refine_finish(c, nrhs);
     c.d2h_bytes += sizeof(double) * 16 + sizeof(int);
     CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
     CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -154,8 +158,7 @@ int refine(Ctx& c, int nrhs, int* steps_out) {
     int steps = 0;
     for (int step = 1; step <= c.refine_max; ++step) {
         k_refine_step(c, nrhs, active);
-        for (int q = 0; q < nrhs; ++q)
-            if (active[q]) k_kkt_residual_one(c, q);
+        k_kkt_residual(c, nrhs);
         c.d2h_bytes += sizeof(double) * 16 + sizeof(int);
         CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
         CIPM_CUDA(cudaMemcpyAsync(c.h_err, c.err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -169,6 +172,7 @@ int refine(Ctx& c, int nrhs, int* steps_out) {
         }
         if (!any) break;
     }
+    k_refine_finish(c, nrhs);
     if (steps_out) *steps_out = steps;
     c.h_sc[CIPM_SC_REFINE_STEPS] = steps;
     return CIPM_OK;
@@ -238,6 +242,7 @@ int refine_async(Ctx& c, int nrhs, int slot) {
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
     CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
     CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
+    k_refine_finish(c, nrhs);
     c.launches += c.refine_graph_launches[nrhs] * 2;   // typical step count (the exact count is on the device)
     k_refine_steps_store(c, nrhs, slot);
     return CIPM_OK;
@@ -986,15 +991,55 @@ int cipm_loop_check(cipm_ctx* h, int iteration, double* sc_out) {
     return e;
 }
 
+// CIPM_BODY_TIMING=1 (probes only): host enqueue time and device time of each
+// segment of cipm_loop_body, on stderr (one line per iteration)
+struct BodyTimer {
+    Ctx& c;
+    bool on;
+    std::vector<std::pair<const char*, double>> host;
+    std::vector<cudaEvent_t> ev;
+    std::chrono::steady_clock::time_point t0;
+    explicit BodyTimer(Ctx& cc) : c(cc) {
+        static const bool env = getenv("CIPM_BODY_TIMING") != nullptr;
+        on = env;
+        if (on) mark("start");
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        host.emplace_back(name, ev.empty() ? 0.0 : std::chrono::duration<double, std::micro>(t - t0).count());
+        t0 = t;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, c.stream);
+        ev.push_back(e);
+    }
+    ~BodyTimer() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back());
+        fprintf(stderr, "[body]");
+        for (size_t k = 1; k < ev.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[k - 1], ev[k]);
+            fprintf(stderr, " %s=%.0f/%.0f", host[k].first, host[k].second, ms * 1000.f);
+        }
+        fprintf(stderr, " (host/device us)\n");
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 int cipm_loop_body(cipm_ctx* h) {
     CIPM_NVTX("cipm_loop_body");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
     int e;
     const bool eager = !c.use_graphs || c.profile || c.trace;
+    BodyTimer bt(c);
     k_update_scaling(c);
+    bt.mark("scaling");
     e = cipm_factor(h);
     if (e) return e;
+    bt.mark("factor");
     // affine direction (two right-hand sides: col2 and the affine RHS)
     k_affine_rhs(c);
     if (eager) {
@@ -1004,12 +1049,14 @@ int cipm_loop_body(cipm_ctx* h) {
         e = refine_async(c, 2, CIPM_SC_REF_STEPS_A);
     }
     if (e) return e;
+    bt.mark("solve_a");
     k_copy(c, c.rbest, c.col2, c.dim);
     k_copy(c, c.rbest + c.dim, c.sol1, c.dim);
     k_directions_prep_den(c);
     k_recover_direction(c, 0, c.sol1, 0.0);
     e = eager ? step_length(c, 0) : step_length_async(c, 0);
     if (e) return e;
+    bt.mark("step_a");
     // combined direction
     k_combined_ds(c, c.dz[0], c.ds[0]);
     k_combined_rhs(c);
@@ -1020,6 +1067,7 @@ int cipm_loop_body(cipm_ctx* h) {
         e = refine_async(c, 1, CIPM_SC_REF_STEPS_C);
     }
     if (e) return e;
+    bt.mark("solve_c");
     k_copy(c, c.rbest, c.sol1, c.dim);
     k_recover_direction(c, 1, c.sol1, 0.0);
     if (eager) {
@@ -1030,7 +1078,9 @@ int cipm_loop_body(cipm_ctx* h) {
         if (!e) e = neighborhood_async(c);
     }
     if (e) return e;
+    bt.mark("step_c");
     k_take_step(c);
+    bt.mark("take");
     return CIPM_OK;
 }
 

@@ -831,6 +831,170 @@ __global__ void __launch_bounds__(RT) root_solve(TailSolveArgs a0, const T* __re
     if (tid == 0) st_release(a.done, 1);
 }
 
+// root_solve with the root's factor and block inverses staged in shared memory
+// first (cp.async, all in flight at once): every block GEMV of the substitution
+// then reads shared memory instead of a chain of dependent L2 loads.
+constexpr int RIB = TB * (TB + 1) / 2;      // packed lower triangle of one 64 x 64 inverse block
+__device__ __forceinline__ int root_pk(int j, int w) { return j * w - ((j * (j - 1)) >> 1); }
+template <typename T>
+constexpr int root_solve_smem(int w) {
+    return (int)sizeof(T) * (((w * (w + 1) / 2 + 3) & ~3) + ((w + TB - 1) / TB) * RIB);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RT) root_solve_s(TailSolveArgs a0, const T* __restrict__ L, const T* __restrict__ inv,
+                                                 const T* __restrict__ dvec, T* x, const T* __restrict__ vin) {
+    TailSolveArgs a = a0;
+    if (a.rstate) {
+        a.act0 = a.act0 && a.rstate[4] == 0.0;
+        a.act1 = a.act1 && a.rstate[12] == 0.0;
+    }
+    const int tid = threadIdx.x;
+    const int w = a.w, r = a.r;
+    __shared__ T xs[2][256];
+    __shared__ T acc[2][TB];
+    __shared__ T part[RP][2][TB];
+    if (!a.act0 && !a.act1) {
+        if (tid == 0) st_release(a.done, 1);
+        return;
+    }
+    const bool act[2] = {a.act0 != 0, a.act1 != 0};
+    // stage the root's factor (packed lower, Ls[cs[k] + i - k] = L(i, k)) and the
+    // lower triangles of its 64 x 64 diagonal-block inverses (Is, row-major packed)
+    // in shared memory with cp.async; the right-hand side is assembled meanwhile
+    extern __shared__ __align__(16) unsigned char rss_raw[];
+    T* Ls = reinterpret_cast<T*>(rss_raw);
+    T* Is = Ls + ((w * (w + 1) / 2 + 3) & ~3);
+    __shared__ int cs[257];
+    {
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int k = wid; k < w; k += RT / 32) {
+            const int ck = root_pk(k, w) - k;
+            for (int i = k + lane; i < w; i += 32) cp_async_elem(Ls + ck + i, L + (int64_t)k * r + i, true);
+        }
+        for (int row = wid; row < a.nbd * TB; row += RT / 32) {
+            const int bb = row / TB, ri = row - bb * TB;
+            if (bb * TB + ri >= w) continue;
+            T* dst = Is + bb * RIB + ri * (ri + 1) / 2;
+            const T* src = inv + (int64_t)bb * TB * TB + ri * TB;
+            for (int t = lane; t <= ri; t += 32) cp_async_elem(dst + t, src + t, true);
+        }
+        cp_async_commit();
+        for (int j = tid; j <= w; j += RT) cs[j] = root_pk(j, w);
+    }
+    // 1. right-hand side of the root columns minus the non-tiny vector inbox
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        T v = (T)0;
+        if (act[q]) {
+            const int col = a.c0 + j;
+            v = x[q * a.dim + col];
+            const T* vq = vin + q * a.nv;
+            for (int64_t p = a.vn_lo[col]; p < a.vn_hi[col]; ++p) v -= __ldcg(vq + p);
+        }
+        xs[q][j] = v;
+    }
+    __syncthreads();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int ri = tid & (TB - 1), kp = tid >> 6;       // row / column within the block, partial index
+    // 2. forward, block by block
+    for (int b = 0; b < a.nbd; ++b) {
+        const int row0 = b * TB, nb = min(TB, w - row0);
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nb)
+            for (int k = kp; k < row0; k += RP) {
+                const T l = Ls[cs[k] + row0 + ri - k];
+                p0 += l * xs[0][k];
+                p1 += l * xs[1][k];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, i = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][i];
+            acc[q][i] = i < nb ? xs[q][row0 + i] - s : (T)0;
+        }
+        __syncthreads();
+        const T* Ib = Is + b * RIB + ri * (ri + 1) / 2;     // row ri of the lower inverse of L_bb
+        p0 = (T)0;
+        p1 = (T)0;
+        if (ri < nb)
+            for (int t = kp; t <= ri; t += RP) {
+                const T iv = Ib[t];
+                p0 += iv * acc[0][t];
+                p1 += iv * acc[1][t];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, i = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][i];
+            if (i < nb) xs[q][row0 + i] = s;
+        }
+        __syncthreads();
+    }
+    // 3. D solve (ldl.py:101-102)
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        xs[q][j] = xs[q][j] / dvec[a.c0 + j];
+    }
+    __syncthreads();
+    // 4. backward, last block first
+    for (int b = a.nbd - 1; b >= 0; --b) {
+        const int col0 = b * TB, nb = min(TB, w - col0), i0 = col0 + nb;
+        T p0 = (T)0, p1 = (T)0;
+        if (ri < nb) {
+            const T* Lc = Ls + cs[col0 + ri] - (col0 + ri);
+            for (int i = i0 + kp; i < w; i += RP) {
+                const T l = Lc[i];
+                p0 += l * xs[0][i];
+                p1 += l * xs[1][i];
+            }
+        }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, j = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][j];
+            acc[q][j] = j < nb ? xs[q][col0 + j] - s : (T)0;
+        }
+        __syncthreads();
+        const T* Ib = Is + b * RIB;
+        p0 = (T)0;
+        p1 = (T)0;
+        if (ri < nb)
+            for (int t = ri + kp; t < nb; t += RP) {          // x_j = sum_{t >= j} inv[t][j] acc_t
+                const T iv = Ib[t * (t + 1) / 2 + ri];
+                p0 += iv * acc[0][t];
+                p1 += iv * acc[1][t];
+            }
+        part[kp][0][ri] = p0;
+        part[kp][1][ri] = p1;
+        __syncthreads();
+        if (tid < 2 * TB) {
+            const int q = tid >> 6, j = tid & (TB - 1);
+            T s = (T)0;
+            for (int k = 0; k < RP; ++k) s += part[k][q][j];
+            if (j < nb) xs[q][col0 + j] = s;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < 2 * w; e += RT) {
+        const int q = e / w, j = e - q * w;
+        if (act[q]) x[q * a.dim + a.c0 + j] = xs[q][j];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(a.done, 1);
+}
+
 template <typename T>
 void tail_factor_t(Ctx& c) {
     static bool attr = false;
@@ -925,8 +1089,20 @@ void tail_forward_t(Ctx& c, T* x, int act0, int act1) {
 template <typename T>
 void root_solve_t(Ctx& c, T* x, int act0, int act1) {
     const TailNode& t = c.tail[0];
-    root_solve<T><<<1, RT, 0, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
-                                          (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x, (const T*)c.vin);
+    const int sm = root_solve_smem<T>(t.w);
+    static const bool staged_env = !getenv("CIPM_ROOT_UNSTAGED");
+    if (staged_env && sm <= 200 * 1024) {
+        static int attr = 0;
+        if (attr < sm) {
+            cudaFuncSetAttribute(root_solve_s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr = 200 * 1024;
+        }
+        root_solve_s<T><<<1, RT, sm, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
+                                                 (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x, (const T*)c.vin);
+    } else {
+        root_solve<T><<<1, RT, 0, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
+                                              (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x, (const T*)c.vin);
+    }
     c.launches++;
 }
 

@@ -1503,11 +1503,16 @@ __global__ void gather_perm(const double* __restrict__ r, T* __restrict__ t, con
 
 template <typename T>
 __global__ void scatter_add_perm(double* __restrict__ x, const T* __restrict__ t, const int32_t* __restrict__ perm,
-                                 int64_t dim, int act0, int act1, const double* rstate) {
+                                 int64_t dim, int act0, int act1, const double* rstate, double* __restrict__ best) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // the previous step's iterate becomes the best one if its residual improved
+    // (rstate[5], set by the controller; system.py:301-302) — before it is updated
+    const bool imp0 = rstate && rstate[5] != 0.0, imp1 = rstate && act1 && rstate[13] != 0.0;
     resolve_act(rstate, act0, act1);
     if (k >= dim) return;
     const int32_t p = perm[k];
+    if (imp0) best[p] = x[p];
+    if (imp1) best[dim + p] = x[dim + p];
     if (act0) x[p] = x[p] + (double)t[k];
     if (act1) x[dim + p] = x[dim + p] + (double)t[dim + k];
 }
@@ -1737,7 +1742,7 @@ void refine_solve_t(Ctx& c, int act0, int act1) {
     }
     pt.mark("bwd_tiny");
     scatter_add_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx, t, c.sym.perm, c.dim, act0, act1,
-                                                                    c.rstate);
+                                                                    c.rstate, c.rbest);
     pt.mark("scatter");
     c.launches += 4;
 }

@@ -8,6 +8,7 @@
 // A-class passes in the reference.  All reductions are two-level with a fixed
 // grid (bitwise reproducible).
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.hpp"
@@ -428,7 +429,24 @@ __global__ void kkt_res_m(const int64_t* arp, const int64_t* aci, const double* 
     rv[n + i] = bv[n + i] - csr_row(arp, aci, av, xv, i);
 }
 
-// ‖r‖∞ and the refinement controller of system.py:298-314 for one rhs
+// the refinement controller of system.py:298-314 for one rhs, given ‖r‖∞
+// st: 0 best, 1 prev, 2 ups, 3 target, 4 done, 5 improved, 6 steps, 7 resid
+__device__ void refine_update(double rn, double* st) {
+    st[6] += 1.0;
+    st[5] = 0.0;
+    if (rn < st[0]) { st[0] = rn; st[5] = 1.0; }
+    if (rn <= st[3]) { st[4] = 1.0; st[7] = rn; return; }
+    if (rn > st[1]) {
+        st[2] += 1.0;
+        if (st[2] >= 2.0) { st[4] = 2.0; st[7] = st[0]; return; }
+    } else {
+        st[2] = 0.0;
+    }
+    st[1] = rn;
+    st[7] = st[0];
+}
+
+// ‖r‖∞ and the controller for one rhs
 __global__ void refine_control(const double* rv, int64_t dim, double* st, double* partials, unsigned int* counter) {
     if (st[4] != 0.0) return;      // this right-hand side already finished (graph-driven refinement)
     double v[1] = {0.0};
@@ -436,21 +454,80 @@ __global__ void refine_control(const double* rv, int64_t dim, double* st, double
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim; i += (int64_t)gridDim.x * blockDim.x)
         v[0] = fmax(v[0], fabs(rv[i]));
     double out[1];
-    if (grid_reduce<1>(v, ops, partials, counter, out)) {
-        // st: 0 best, 1 prev, 2 ups, 3 target, 4 done, 5 improved, 6 steps, 7 resid
-        const double rn = dim ? out[0] : 0.0;
-        st[6] += 1.0;
-        st[5] = 0.0;
-        if (rn < st[0]) { st[0] = rn; st[5] = 1.0; }
-        if (rn <= st[3]) { st[4] = 1.0; st[7] = rn; return; }
-        if (rn > st[1]) {
-            st[2] += 1.0;
-            if (st[2] >= 2.0) { st[4] = 2.0; st[7] = st[0]; return; }
+    if (grid_reduce<1>(v, ops, partials, counter, out)) refine_update(dim ? out[0] : 0.0, st);
+}
+
+// Zero / nonneg cones only (LP, QP): the whole residual step of the refinement
+// for both right-hand sides in one pass — r = b - K x with K = [P A'; A -H]
+// (H diagonal), ‖r‖∞ per rhs, and the controller in the last block — instead
+// of kkt_res_n + kkt_res_m + nn_apply_h + refine_control per rhs.  The CSR
+// index arrays are read once for both right-hand sides.
+struct Res2Args {
+    const int64_t *prp, *pci;
+    const double* pv;
+    const int64_t *atrp, *atci;
+    const double* atv;
+    const int64_t *arp, *aci;
+    const double* av;
+    const double* h;             // nonneg diagonal of H (rows zero_dim.. of the m block)
+    const double* x;             // [q][dim]
+    const double* b;
+    double* r;
+    double* st;                  // rstate (8 per rhs)
+    int64_t n, m, dim, zero_dim;
+    int nrhs;
+};
+
+__global__ void __launch_bounds__(kThreads) kkt_resid2(Res2Args a, double* partials, unsigned int* counter) {
+    const bool act0 = a.st[4] == 0.0, act1 = a.nrhs > 1 && a.st[12] == 0.0;
+    if (!act0 && !act1) return;          // uniform across the grid: no block enters the reduction
+    const double* x0 = a.x;
+    const double* x1 = a.x + a.dim;
+    double v[2] = {0.0, 0.0};
+    const int ops[2] = {RED_MAX, RED_MAX};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.dim; i += (int64_t)gridDim.x * blockDim.x) {
+        double k0 = 0.0, k1 = 0.0;
+        if (i < a.n) {
+            for (int64_t p = a.prp[i]; p < a.prp[i + 1]; ++p) {
+                const int64_t c = a.pci[p];
+                const double w = a.pv[p];
+                k0 += w * x0[c];
+                if (act1) k1 += w * x1[c];
+            }
+            for (int64_t p = a.atrp[i]; p < a.atrp[i + 1]; ++p) {
+                const int64_t c = a.n + a.atci[p];
+                const double w = a.atv[p];
+                k0 += w * x0[c];
+                if (act1) k1 += w * x1[c];
+            }
         } else {
-            st[2] = 0.0;
+            const int64_t j = i - a.n;
+            for (int64_t p = a.arp[j]; p < a.arp[j + 1]; ++p) {
+                const int64_t c = a.aci[p];
+                const double w = a.av[p];
+                k0 += w * x0[c];
+                if (act1) k1 += w * x1[c];
+            }
+            const double hj = j < a.zero_dim ? 0.0 : a.h[j - a.zero_dim];
+            k0 -= hj * x0[i];
+            if (act1) k1 -= hj * x1[i];
         }
-        st[1] = rn;
-        st[7] = st[0];
+        if (act0) {
+            const double r0 = a.b[i] - k0;
+            a.r[i] = r0;
+            v[0] = fmax(v[0], fabs(r0));
+        }
+        if (act1) {
+            const double r1 = a.b[a.dim + i] - k1;
+            a.r[a.dim + i] = r1;
+            v[1] = fmax(v[1], fabs(r1));
+        }
+    }
+    double out[2];
+    if (grid_reduce<2>(v, ops, partials, counter, out)) {
+        const double nrm0 = a.dim ? out[0] : 0.0, nrm1 = a.dim ? out[1] : 0.0;
+        if (act0) refine_update(nrm0, a.st);
+        if (act1) refine_update(nrm1, a.st + 8);
     }
 }
 
@@ -740,7 +817,7 @@ void k_take_step(Ctx& c) {
     c.launches++;
 }
 
-// r = b - K x for rhs q (K = [P A'; A -H], unregularised, FP64)
+// r = b - K x for rhs q (K = [P A'; A -H], unregularised, FP64) and the controller
 void k_kkt_residual_one(Ctx& c, int q) {
     const double* xv = c.rx + (int64_t)q * c.dim;
     const double* bv = c.rb + (int64_t)q * c.dim;
@@ -752,9 +829,31 @@ void k_kkt_residual_one(Ctx& c, int q) {
     c.launches += 2;
     k_apply_h(c, xv + c.n, rv + c.n, 1.0, rv + c.n, 1.0, st + 4);
     refine_control<<<red_grid(c.dim), kThreads, 0, c.stream>>>(rv, c.dim, c.rstate + 8 * q, c.partials, c.counter);
-    copy_if_improved<<<grid_for(c.dim), kThreads, 0, c.stream>>>(xv, c.rbest + (int64_t)q * c.dim, c.rstate + 8 * q,
-                                                                 c.dim);
-    c.launches += 2;
+    c.launches++;
+}
+
+// the residual step of one refinement step for the active right-hand sides q < nrhs
+// (the improved iterate is copied to rbest by the next step's scatter, or by
+// k_refine_finish after the last step)
+void k_kkt_residual(Ctx& c, int nrhs) {
+    static const bool fused_env = !getenv("CIPM_NO_FUSED_RESID");
+    if (fused_env && c.nsoc == 0 && c.nsym == 0 && c.npsd == 0 && c.lin == c.m) {
+        Res2Args a{c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, c.a_rp, c.a_ci, c.a_v, c.nn_h,
+                   c.rx, c.rb, c.rr, c.rstate, c.n, c.m, c.dim, c.zero_dim, nrhs};
+        kkt_resid2<<<red_grid(c.dim), kThreads, 0, c.stream>>>(a, c.partials, c.counter);
+        c.launches++;
+        return;
+    }
+    for (int q = 0; q < nrhs; ++q) k_kkt_residual_one(c, q);
+}
+
+// after the refinement loop: the last step's iterate, if it improved on the best
+void k_refine_finish(Ctx& c, int nrhs) {
+    for (int q = 0; q < nrhs; ++q)
+        copy_if_improved<<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rx + (int64_t)q * c.dim,
+                                                                     c.rbest + (int64_t)q * c.dim,
+                                                                     c.rstate + 8 * q, c.dim);
+    c.launches += nrhs;
 }
 
 // the matvec part of k_kkt_residual_one only (bench timing: no controller state change)
