@@ -419,7 +419,11 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     if (st->stream) {
         c.stream = (cudaStream_t)st->stream;
     } else {
-        CIPM_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        // highest priority: the critical path of the dense tail (diagonal blocks, next
+        // panel) is preferred over the side streams' bulk work
+        int lo = 0, hi = 0;
+        CIPM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CIPM_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, hi));
         c.own_stream = true;
     }
     c.n = d->n;
@@ -685,6 +689,20 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     {
         int64_t inv_total = 0, flag_total = 0;
         tail_setup(c, &inv_total, &flag_total);
+        size_t widest = 0;
+        for (const auto& lv : c.tail_levels) widest = std::max(widest, lv.size());
+        if (widest > 1) {
+            const int P = (int)std::min<size_t>(widest, 8);
+            c.tail_pool.resize(P);
+            c.tail_pool_side.resize(P);
+            c.tail_pool_ev.resize(4 * P);
+            for (int k = 0; k < P; ++k) {
+                CIPM_CUDA(cudaStreamCreateWithFlags(&c.tail_pool[k], cudaStreamNonBlocking));
+                CIPM_CUDA(cudaStreamCreateWithFlags(&c.tail_pool_side[k], cudaStreamNonBlocking));
+            }
+            for (auto& e : c.tail_pool_ev) CIPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CIPM_CUDA(cudaEventCreateWithFlags(&c.tail_fork, cudaEventDisableTiming));
+        }
         void* p = nullptr;
         CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(inv_total, 1)));
         c.allocations.push_back(p);
@@ -721,6 +739,8 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     CIPM_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
     CIPM_CUDA(cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming));
     CIPM_CUDA(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
+    CIPM_CUDA(cudaStreamCreateWithFlags(&c.tail_side, cudaStreamNonBlocking));
+    for (auto& e : c.tail_ev) CIPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.factor_blocks = factor_grid(c);
     c.solve_blocks = solve_grid(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
@@ -831,6 +851,13 @@ void cipm_ctx_destroy(cipm_ctx* h) {
     if (c.fork_ev) cudaEventDestroy(c.fork_ev);
     if (c.join_ev) cudaEventDestroy(c.join_ev);
     if (c.side) cudaStreamDestroy(c.side);
+    for (auto e : c.tail_ev)
+        if (e) cudaEventDestroy(e);
+    if (c.tail_side) cudaStreamDestroy(c.tail_side);
+    for (auto e : c.tail_pool_ev) cudaEventDestroy(e);
+    for (auto st : c.tail_pool) cudaStreamDestroy(st);
+    for (auto st : c.tail_pool_side) cudaStreamDestroy(st);
+    if (c.tail_fork) cudaEventDestroy(c.tail_fork);
     for (auto& g : c.refine_graph)
         if (g) cudaGraphExecDestroy(g);
     if (c.factor_graph) cudaGraphExecDestroy(c.factor_graph);

@@ -74,6 +74,16 @@ struct Ctx {
     // side stream: the solve-form pass runs beside the dense tail factorisation
     cudaStream_t side = nullptr;
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // dense-tail look-ahead: the bulk of each trailing update runs on tail_side
+    // while the next panel is factored on the main stream
+    cudaStream_t tail_side = nullptr;
+    cudaEvent_t tail_ev[3] = {nullptr, nullptr, nullptr};
+    // independent tail nodes of one level run as parallel branches: slot k has a
+    // main stream, a look-ahead side stream and 4 events (look-ahead x3, join)
+    std::vector<std::vector<int>> tail_levels;
+    std::vector<cudaStream_t> tail_pool, tail_pool_side;
+    std::vector<cudaEvent_t> tail_pool_ev;
+    cudaEvent_t tail_fork = nullptr;
     bool own_stream = false;
     int64_t n = 0, m = 0, dim = 0;
     int precision = CIPM_FULL;

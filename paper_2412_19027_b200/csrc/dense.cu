@@ -1010,17 +1010,27 @@ void tail_factor_t(Ctx& c) {
     T* inbox = (T*)c.inbox;
     T* inv = (T*)c.tinv;
     const Symbolic& S = c.host_sym;
-    for (const TailNode& t : c.tail) {
+    auto run_node = [&](const TailNode& t, cudaStream_t ms, cudaStream_t ss, cudaEvent_t* ev) {
         T* P = L + t.loff;
         const int r = t.r, w = t.w, o = r - w;
-        tail_gather<T><<<(r + 7) / 8, 256, 0, c.stream>>>(P, r, c.sym.irow_ptr + t.r0, c.sym.inbox_tgt, inbox);
+        tail_gather<T><<<(r + 7) / 8, 256, 0, ms>>>(P, r, c.sym.irow_ptr + t.r0, c.sym.inbox_tgt, inbox);
         c.launches++;
+        // right-looking by 64-column panels with look-ahead: panel k's trailing update
+        // is split into "next" (the columns of panel k+1, main stream: they gate
+        // panel k+1's diagonal block), "rest1" (panel k+2's columns) and "rest2" (the
+        // remainder), both on tail_side, so the diagonal block and TRSM of panel k+1
+        // overlap the bulk of panel k's update.  Events: T = panel k's TRSM done
+        // (side may start), E1 = rest1(k) done (next(k+1) writes the same columns;
+        // side-stream order also puts rest2(k-1) before it).
+        static const bool lookahead_env = !getenv("CIPM_TAIL_NO_LOOKAHEAD");
+        const bool la = lookahead_env && w > 2 * TB;
+        bool e1_pending = false, side_used = false;
         for (int kb = 0; kb < w; kb += TB) {
             const int nb = std::min(TB, w - kb);
             const int b = kb / TB;
             T* inv_rm = inv + t.inv_off + (int64_t)b * TB * TB;
             T* inv_cm = inv + t.inv_off + (int64_t)(t.nbd + b) * TB * TB;
-            tail_diag<T><<<1, 256, diag_smem<T>(), c.stream>>>(P, r, kb, nb, t.c0, D, c.sym.sign, c.sn_maxd + t.J,
+            tail_diag<T><<<1, 256, diag_smem<T>(), ms>>>(P, r, kb, nb, t.c0, D, c.sym.sign, c.sn_maxd + t.J,
                                                               c.bumps, c.err, c.delta_s, c.delta_d, inv_rm, inv_cm);
             c.launches++;
             const int below = r - kb - nb;
@@ -1028,29 +1038,79 @@ void tail_factor_t(Ctx& c) {
                 // L21 = A21 L11^-T D^-1 as a GEMM with the column-major inverse (DMMA in FP64)
                 T* A21 = P + (int64_t)kb * r + kb + nb;
                 dim3 g((below + GB - 1) / GB, 1);
-                tail_gemm<T, 2><<<g, 128, gemm_smem<T>(), c.stream>>>(A21, r, inv_cm, TB, nullptr, below, nb, nb, 1 << 30, A21, r,
+                tail_gemm<T, 2><<<g, 128, gemm_smem<T>(), ms>>>(A21, r, inv_cm, TB, nullptr, below, nb, nb, 1 << 30, A21, r,
                                                          nullptr, nullptr, D + t.c0 + kb);
                 c.launches++;
             }
             const int Mr = r - kb - nb, Nc = w - kb - nb;
-            if (Nc > 0) {
-                const T* A = P + (int64_t)kb * r + kb + nb;
-                dim3 g((Mr + GB - 1) / GB, (Nc + GB - 1) / GB);
-                tail_gemm<T, 0><<<g, 128, gemm_smem<T>(), c.stream>>>(A, r, A, r, D + t.c0 + kb, Mr, Nc, nb, 0,
-                                                         P + (int64_t)(kb + nb) * r + kb + nb, r, nullptr, nullptr,
-                                                         nullptr);
+            if (Nc <= 0) continue;
+            const T* A = P + (int64_t)kb * r + kb + nb;
+            const T* Dk = D + t.c0 + kb;
+            T* C0 = P + (int64_t)(kb + nb) * r + kb + nb;
+            // trailing update of the columns [j0, j1) of the trailing block (rows j0.. of A)
+            auto update = [&](cudaStream_t st, int j0, int j1) {
+                const int M = Mr - j0, N = j1 - j0;
+                if (M <= 0 || N <= 0) return;
+                dim3 g((M + GB - 1) / GB, (N + GB - 1) / GB);
+                tail_gemm<T, 0><<<g, 128, gemm_smem<T>(), st>>>(A + j0, r, A + j0, r, Dk, M, N, nb, 0,
+                                                               C0 + (int64_t)j0 * r + j0, r, nullptr, nullptr, nullptr);
                 c.launches++;
+            };
+            if (!la) {
+                update(ms, 0, Nc);
+                continue;
             }
+            // side: rest1 / rest2 of this panel, after its TRSM
+            if (Nc > TB) {
+                cudaEventRecord(ev[0], ms);
+                cudaStreamWaitEvent(ss, ev[0], 0);
+            }
+            // main: next (panel k+1's columns), after rest1 of panel k-1
+            if (e1_pending) cudaStreamWaitEvent(ms, ev[1], 0);
+            update(ms, 0, std::min(TB, Nc));
+            if (Nc > TB) {
+                update(ss, TB, std::min(2 * TB, Nc));
+                cudaEventRecord(ev[1], ss);
+                e1_pending = true;
+                update(ss, 2 * TB, Nc);
+                side_used = true;
+            } else {
+                e1_pending = false;
+            }
+        }
+        if (side_used) {
+            cudaEventRecord(ev[2], ss);
+            cudaStreamWaitEvent(ms, ev[2], 0);
         }
         if (o > 0) {
             const T* A = P + w;
             dim3 g((o + GB - 1) / GB, (o + GB - 1) / GB);
-            tail_gemm<T, 1><<<g, 128, gemm_smem<T>(), c.stream>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
+            tail_gemm<T, 1><<<g, 128, gemm_smem<T>(), ms>>>(A, r, A, r, D + t.c0, o, o, w, 0, nullptr, 0,
                                                      c.sym.push_pos + S.cb_off[t.J], inbox, nullptr);
             c.launches++;
         }
-        tail_finish<<<1, 1, 0, c.stream>>>(c.sn_maxd, c.fac_count, t.J, t.parent);
+        tail_finish<<<1, 1, 0, ms>>>(c.sn_maxd, c.fac_count, t.J, t.parent);
         c.launches++;
+    };
+    static const bool par_env = !getenv("CIPM_TAIL_SERIAL_LEVELS");
+    for (const auto& level : c.tail_levels) {
+        if (level.size() == 1 || !par_env || c.tail_pool.empty()) {
+            for (int i : level) run_node(c.tail[i], c.stream, c.tail_side, c.tail_ev);
+            continue;
+        }
+        // independent nodes: parallel branches (fork / join through events)
+        const int P = (int)c.tail_pool.size();
+        cudaEventRecord(c.tail_fork, c.stream);
+        const int used = std::min<int>(P, (int)level.size());
+        for (int k = 0; k < used; ++k) cudaStreamWaitEvent(c.tail_pool[k], c.tail_fork, 0);
+        for (size_t q = 0; q < level.size(); ++q) {
+            const int k = (int)(q % P);
+            run_node(c.tail[level[q]], c.tail_pool[k], c.tail_pool_side[k], &c.tail_pool_ev[4 * k]);
+        }
+        for (int k = 0; k < used; ++k) {
+            cudaEventRecord(c.tail_pool_ev[4 * k + 3], c.tail_pool[k]);
+            cudaStreamWaitEvent(c.stream, c.tail_pool_ev[4 * k + 3], 0);
+        }
     }
 }
 
@@ -1142,6 +1202,18 @@ void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total) {
     c.tflag_total = fo;
     *inv_total = io;
     *flag_total = fo;
+    // levels of the tail forest (children first): nodes of one level are independent
+    std::vector<int> lev(c.tail.size(), 0);
+    std::vector<int> idx_of(S.nsuper, -1);
+    for (size_t i = 0; i < c.tail.size(); ++i) idx_of[c.tail[i].J] = (int)i;
+    int nlev = 0;
+    for (size_t i = 0; i < c.tail.size(); ++i) {
+        const int p = c.tail[i].parent >= 0 ? idx_of[c.tail[i].parent] : -1;
+        if (p >= 0) lev[p] = std::max(lev[p], lev[i] + 1);
+        nlev = std::max(nlev, lev[i] + 1);
+    }
+    c.tail_levels.assign(nlev, {});
+    for (size_t i = 0; i < c.tail.size(); ++i) c.tail_levels[lev[i]].push_back((int)i);
 }
 
 void k_tail_factor(Ctx& c) {
