@@ -1202,14 +1202,35 @@ TailSolveArgs tail_args(Ctx& c, const TailNode& t, int which, int act0, int act1
     return a;
 }
 
+// the nodes of one tail level (mutually independent): one node on the main
+// stream, several as parallel branches over the stream pool (fork / join)
+template <typename F>
+void tail_level_run(Ctx& c, const std::vector<int>& level, F&& one) {
+    static const bool par_env = !getenv("CIPM_TAIL_SERIAL_LEVELS");
+    if (level.size() == 1 || !par_env || c.tail_pool.empty()) {
+        for (int i : level) one(c.tail[i], c.stream);
+        return;
+    }
+    const int P = (int)c.tail_pool.size();
+    cudaEventRecord(c.tail_fork, c.stream);
+    const int used = std::min<int>(P, (int)level.size());
+    for (int k = 0; k < used; ++k) cudaStreamWaitEvent(c.tail_pool[k], c.tail_fork, 0);
+    for (size_t q = 0; q < level.size(); ++q) one(c.tail[level[q]], c.tail_pool[q % P]);
+    for (int k = 0; k < used; ++k) {
+        cudaEventRecord(c.tail_pool_ev[4 * k + 3], c.tail_pool[k]);
+        cudaStreamWaitEvent(c.stream, c.tail_pool_ev[4 * k + 3], 0);
+    }
+}
+
 template <typename T>
 void tail_forward_t(Ctx& c, T* x, int act0, int act1) {
-    for (const TailNode& t : c.tail) {
+    auto one = [&](const TailNode& t, cudaStream_t st) {
         const int blocks = t.nbd + (t.r - t.w + TB - 1) / TB;
-        tail_fwd<T><<<blocks, 256, 0, c.stream>>>(tail_args(c, t, 0, act0, act1), (const T*)c.lval + t.loff,
-                                                  (const T*)c.tinv + t.inv_off, x, (T*)c.vin);
+        tail_fwd<T><<<blocks, 256, 0, st>>>(tail_args(c, t, 0, act0, act1), (const T*)c.lval + t.loff,
+                                            (const T*)c.tinv + t.inv_off, x, (T*)c.vin);
         c.launches++;
-    }
+    };
+    for (size_t l = 0; l < c.tail_levels.size(); ++l) tail_level_run(c, c.tail_levels[l], one);
 }
 
 template <typename T>
@@ -1234,12 +1255,12 @@ void root_solve_t(Ctx& c, T* x, int act0, int act1) {
 
 template <typename T>
 void tail_backward_t(Ctx& c, T* x, int act0, int act1) {
-    for (auto it = c.tail.rbegin(); it != c.tail.rend(); ++it) {
-        const TailNode& t = *it;
-        tail_bwd<T><<<t.nbd, 256, 0, c.stream>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
-                                                 (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x);
+    auto one = [&](const TailNode& t, cudaStream_t st) {
+        tail_bwd<T><<<t.nbd, 256, 0, st>>>(tail_args(c, t, 1, act0, act1), (const T*)c.lval + t.loff,
+                                           (const T*)c.tinv + t.inv_off, (const T*)c.dvec, x);
         c.launches++;
-    }
+    };
+    for (size_t l = c.tail_levels.size(); l-- > 0;) tail_level_run(c, c.tail_levels[l], one);
 }
 
 }  // namespace

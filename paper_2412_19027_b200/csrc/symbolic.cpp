@@ -1089,10 +1089,12 @@ int analyze(int64_t n, int64_t m, const int64_t* prp, const int64_t* pci, const 
     // finish it before the tail starts.
     S.is_tail.assign(ns, 0);
     const int64_t tail_w = std::min<int64_t>(opt.tail_width, 64);   // the persistent kernels hold w < 64 columns
+    int64_t tail_off = opt.tail_offrows;
+    if (const char* e = getenv("CIPM_TAIL_OFFROWS")) tail_off = atoll(e);   // experiments
     for (int32_t J = 0; J < ns; ++J) {
         int64_t w = S.sn_col[J + 1] - S.sn_col[J];
         int64_t o = (S.sn_rptr[J + 1] - S.sn_rptr[J]) - w;
-        if (w >= tail_w || o >= opt.tail_offrows) S.is_tail[J] = 1;
+        if (w >= tail_w || o >= tail_off) S.is_tail[J] = 1;
     }
     for (int32_t J = 0; J < ns; ++J)       // parents have larger indices (postorder)
         if (S.is_tail[J] && S.sn_parent[J] >= 0) S.is_tail[S.sn_parent[J]] = 1;
