@@ -1829,7 +1829,24 @@ int factor_grid(Ctx& c) {
 int solve_grid(Ctx& c) {
     // per-warp panel slice: up to 8 KiB (three 8-warp CTAs per SM); larger panels are read from L2/HBM
     const int64_t es = c.precision == CIPM_FULL ? 8 : 4;
-    c.solve_slice = std::max<int64_t>(64, std::min<int64_t>((c.host_sym.max_panel_main + 3) & ~int64_t(3), 8192 / es));
+    // Staging every panel (slice = the largest non-tail panel) pays when a level
+    // holds fewer tasks than the GPU has warps; wide levels want occupancy instead
+    // (smaller slices, more CTAs per SM).  Measured on the B200: C2 / C5a stage
+    // everything (pair -10 % / -15 %), C3 (65k leaf-level warp tasks) wants 6 KB.
+    {
+        const Symbolic& S = c.host_sym;
+        std::vector<int64_t> per_level(S.height + 1, 0);
+        std::vector<char> tiny(S.nsuper, 0);
+        for (int32_t J : S.tiny) tiny[J] = 1;
+        for (int32_t J = 0; J < S.nsuper; ++J)
+            if (!S.is_tail[J] && !tiny[J]) per_level[S.level[J]]++;
+        const int64_t widest = *std::max_element(per_level.begin(), per_level.end());
+        const int64_t warps_1cta = (int64_t)sm_count() * SW;          // one 8-warp CTA per SM
+        const int64_t full = (c.host_sym.max_panel_main + 3) & ~int64_t(3);
+        const int64_t cap = (200 * 1024 / SW) / es;                     // one CTA per SM at most
+        if (widest <= 8 * warps_1cta) c.solve_slice = std::max<int64_t>(64, std::min<int64_t>(full, cap));
+        else c.solve_slice = std::max<int64_t>(64, std::min<int64_t>(full, 6144 / es));
+    }
     if (const char* e = getenv("CIPM_SOLVE_SLICE")) c.solve_slice = std::max<int64_t>(4, atoll(e) & ~int64_t(3));   // experiments
     const int ssm = (int)(es * c.solve_slice * SW);
     int per = 0, per2 = 0;
