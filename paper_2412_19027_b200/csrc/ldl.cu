@@ -452,40 +452,56 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
 // instead of one per column.
 template <typename T, int NB>
 __device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, const int8_t* sSg, T* sD,
-                                               double& s_runmax, const FactorArgs& a, T* sLt, T* sInv) {
+                                               double& s_runmax, const FactorArgs& a, T* sLt, T* sInv, T* sCol) {
     const int lane = threadIdx.x & 31;
     double runmax = s_runmax;
+    double ds_r = a.delta_s, dd_r = a.delta_d;
+    asm volatile("" : "+d"(ds_r), "+d"(dd_r));
     T x[NB];
 #pragma unroll
     for (int c = 0; c < NB; ++c)
         x[c] = (lane < nbk && c < nbk && c <= lane) ? Pk[c * r + k0 + lane] : (T)0;
+    const unsigned pos = __ballot_sync(0xffffffffu, lane < nbk && sSg[k0 + lane] > 0);
+    T d_mine = (T)0, inv_mine = (T)0;
+    bool bump_mine = false;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
         if (j < nbk) {
-            double dd = (double)__shfl_sync(0xffffffffu, x[j], j);
-            const double bound = a.delta_s + a.delta_d * runmax;
+            // column j through shared memory (one store + broadcast loads instead of
+            // NB - 1 shuffles: the shorter pivot chain of tools/micro/diag16.cu)
+            T* col = sCol + (j & 1) * 32;
+            col[lane] = x[j];
+            __syncwarp();
+            double dd = (double)col[j];
+            const double bound = ds_r + dd_r * runmax;
             const bool bump = fabs(dd) < bound;
-            if (bump) dd = sSg[k0 + j] > 0 ? bound : -bound;
+            dd = bump ? (((pos >> j) & 1u) ? bound : -bound) : dd;
             const T dt = (T)dd;
             runmax = fmax(runmax, fabs(dd));
             const T inv = (T)1 / dt;
-            if (lane == 0) {
-                if (bump) atomicAdd(a.bumps, 1);
-                if (dt == (T)0) set_error(a.err, CIPM_E_FACTOR);
-                sD[k0 + j] = dt;
-                sInv[j] = inv;
+            if (lane == j) {
+                d_mine = dt;
+                inv_mine = inv;
+                bump_mine = bump;
             }
-            const T xj = x[j];                   // unscaled a_ij (lanes i > j)
+            const T lj = x[j] * inv;                 // l_ij (lanes i > j)
 #pragma unroll
             for (int c = j + 1; c < NB; ++c) {
-                const T acj = __shfl_sync(0xffffffffu, xj, c);   // unscaled a_cj
-                if (lane >= c) x[c] -= xj * (acj * inv);
+                const T acj = col[c];                 // unscaled a_cj
+                if (lane >= c) x[c] -= lj * acj;
             }
-            x[j] = lane > j ? xj * inv : (lane == j ? (T)1 : x[j]);
-        } else if (lane == 0) {
-            sInv[j] = (T)0;
+            x[j] = lane > j ? lj : (lane == j ? (T)1 : x[j]);
         }
     }
+    if (lane < NB) {
+        sInv[lane] = lane < nbk ? inv_mine : (T)0;
+        if (lane < nbk) {
+            sD[k0 + lane] = d_mine;
+            if (d_mine == (T)0) set_error(a.err, CIPM_E_FACTOR);
+        }
+    }
+    const unsigned nb_bumps = __popc(__ballot_sync(0xffffffffu, bump_mine));
+    if (lane == 0 && nb_bumps) atomicAdd(a.bumps, (int)nb_bumps);
     int row = k0 + lane;
     asm volatile("" : "+r"(row));            // recompute the store addresses (no 32 live pointers)
 #pragma unroll
@@ -530,7 +546,7 @@ __device__ __forceinline__ void cta_below_rows(T* Pk, int r, int i0, int nbk, co
 // instead of one per column.
 template <typename T>
 __device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const int8_t* sSg, T* sD, double& s_runmax,
-                                              const FactorArgs& a, T* __restrict__ dvec, T* sLt, T* sInv) {
+                                              const FactorArgs& a, T* __restrict__ dvec, T* sLt, T* sInv, T* sCol) {
     // block width 16: a row of the block in registers, 2 CTAs / SM without spills
     constexpr int KB = 16;
     const int tid = threadIdx.x, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -538,8 +554,8 @@ __device__ __forceinline__ void cta_panel_ldl(T* P, int r, int w, int c0, const 
         const int nbk = min(KB, w - k0);
         T* Pk = P + k0 * r;               // column k0 of the panel
         if (wid == 0) {
-            if (nbk <= 8) cta_diag_block<T, 8>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
-            else cta_diag_block<T, KB>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv);
+            if (nbk <= 8) cta_diag_block<T, 8>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv, sCol);
+            else cta_diag_block<T, KB>(Pk, r, k0, nbk, sSg, sD, s_runmax, a, sLt, sInv, sCol);
         }
         __syncthreads();
         // (b) rows below the diagonal block
@@ -611,6 +627,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
     __shared__ T sD[64];
     __shared__ __align__(16) T sLt[64 * 16];    // blocked LDL: L11' of a 16-column block / d_k l_ck
     __shared__ T sInv[16];
+    __shared__ T sCol[64];
     __shared__ int8_t sSg[64];
     __shared__ int32_t s_d32[8];
     __shared__ int64_t s_d64[8];
@@ -670,8 +687,8 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
         __syncthreads();
         if (a.trace && tid == 0) a.trace[6 * J + 3] = gtimer();
         // 2. dense LDL' of the panel: blocked by 16 columns (cta_panel_ldl)
-        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
-        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv);
+        if (in_smem) cta_panel_ldl(sp, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv, sCol);
+        else cta_panel_ldl(L, r, w, c0, sSg, sD, s_runmax, a, dvec, sLt, sInv, sCol);
         if (a.trace && tid == 0) a.trace[6 * J + 4] = gtimer();
         // 3. push C_J = L_off D L_off' (the factor is written back after the signal:
         //    the ancestors only read the inbox, so the release does not wait for it)
