@@ -220,16 +220,90 @@ __device__ __forceinline__ void unpack_lower(int e, int o, int& bb, int& aa) {
 
 // warp-tier task body: gather, panel LDL', write-back, contribution push.
 // Forced inline so P keeps its address space at each call site.
+constexpr bool kWarpPanelSmem = false;   // true: the original shared-memory right-looking loop
+
+// warp-tier panel LDL' with the panel in registers: lane l owns rows l and l + 32
+// (r <= 64), all w <= 16 columns; column j's top entries a_cj are broadcast through
+// shared memory (the short pivot chain of tools/micro/diag16.cu), l_ij = a_ij / d_j
+// as a multiply by the reciprocal, then a_ic -= l_ij a_cj for c in (j, w).
+template <typename T, int NW>
+__device__ __forceinline__ void warp_panel_regs(T* P, int c0, int w, int r, double& runmax, T* sDw,
+                                                const int8_t* sSgw, const FactorArgs& a, T* __restrict__ dvec,
+                                                T* sCol) {
+    const int lane = threadIdx.x & 31;
+    const bool h0 = lane < r, h1 = lane + 32 < r;
+    T x0[NW], x1[NW];
+#pragma unroll
+    for (int c = 0; c < NW; ++c) {
+        x0[c] = (c < w && h0) ? P[c * r + lane] : (T)0;
+        x1[c] = (c < w && h1) ? P[c * r + lane + 32] : (T)0;
+    }
+    double ds_r = a.delta_s, dd_r = a.delta_d;
+    asm volatile("" : "+d"(ds_r), "+d"(dd_r));
+    const unsigned pos = __ballot_sync(0xffffffffu, lane < w && sSgw[lane] > 0);
+    T d_mine = (T)0;
+    int nbump = 0;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        if (j < w) {
+            T* col = sCol + (j & 1) * 32;
+            col[lane] = x0[j];                         // a_lj for lanes l < w (top rows)
+            __syncwarp();
+            double dd = (double)col[j];
+            const double bound = ds_r + dd_r * runmax;
+            const bool bump = fabs(dd) < bound;
+            dd = bump ? (((pos >> j) & 1u) ? bound : -bound) : dd;
+            const T dt = (T)dd;
+            runmax = fmax(runmax, fabs(dd));
+            nbump += bump ? 1 : 0;
+            const T inv = (T)1 / dt;
+            if (lane == j) d_mine = dt;
+            const T l0 = x0[j] * inv, l1 = x1[j] * inv;
+#pragma unroll
+            for (int c = j + 1; c < NW; ++c) {
+                if (c < w) {
+                    const T acj = col[c];
+                    if (lane >= c) x0[c] -= l0 * acj;
+                    x1[c] -= l1 * acj;                  // rows 32.. are below every top row
+                }
+            }
+            x0[j] = lane > j ? l0 : (lane == j ? (T)1 : x0[j]);
+            x1[j] = l1;
+        }
+    }
+    if (lane < w) {
+        sDw[lane] = d_mine;
+        dvec[c0 + lane] = d_mine;
+        if (d_mine == (T)0) set_error(a.err, CIPM_E_FACTOR);
+    }
+    if (lane == 0 && nbump) atomicAdd(a.bumps, nbump);
+    int row = lane;
+    asm volatile("" : "+r"(row));
+#pragma unroll
+    for (int c = 0; c < NW; ++c) {
+        if (c < w && h0 && c <= row) P[c * r + row] = x0[c];
+        if (c < w && h1) P[c * r + row + 32] = x1[c];
+    }
+    __syncwarp();
+}
+
 template <typename T>
 __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const Desc& d, int c0, int w, int r, int o,
                                                double& runmax, T* sDw, const int8_t* sSgw, const FactorArgs& a,
-                                               T* __restrict__ dvec, T* __restrict__ inbox, int J) {
+                                               T* __restrict__ dvec, T* __restrict__ inbox, int J, T* sCol) {
     const int lane = threadIdx.x & 31;
     const int psize = r * w;
     // 1. gather the inbox of all r rows (one contiguous, target-sorted range)
     warp_gather_sub(P, a.inbox_tgt, inbox, d.ilo, d.ihi);
     if (a.trace && lane == 0) a.trace[6 * J + 3] = gtimer();
     // 2. dense LDL' of the panel (right-looking, lanes over rows)
+    static_assert(true, "");
+    // (2 x NW values per lane within the 64-register budget: FP64 up to 8 columns)
+    if (r <= 64 && w <= 8 && !kWarpPanelSmem) {
+        warp_panel_regs<T, 8>(P, c0, w, r, runmax, sDw, sSgw, a, dvec, sCol);
+    } else if (sizeof(T) == 4 && r <= 64 && w <= 16 && !kWarpPanelSmem) {
+        warp_panel_regs<T, 16>(P, c0, w, r, runmax, sDw, sSgw, a, dvec, sCol);
+    } else {
     int nbump = 0;
     for (int j = 0; j < w; ++j) {
         T* Pj = P + j * r;
@@ -257,6 +331,7 @@ __device__ __forceinline__ void warp_task_body(T* P, T* L, bool in_smem, const D
         __syncwarp();
     }
     if (lane == 0 && nbump) atomicAdd(a.bumps, nbump);
+    }
     if (a.trace && lane == 0) a.trace[6 * J + 4] = gtimer();
     // 3. push C_J = L_off D L_off' into the ancestors' inboxes, then write the factor back
     if (o > 0) {
@@ -364,7 +439,7 @@ __device__ __forceinline__ int factor_tiny_lane(int J, const FactorArgs& a, T* _
 template <typename T>
 __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T* __restrict__ lval,
                                                   T* __restrict__ dvec, T* __restrict__ inbox, T* sp, T* sDw,
-                                                  int8_t* sSgw, uint64_t* bar, uint32_t& phase) {
+                                                  int8_t* sSgw, uint64_t* bar, uint32_t& phase, T* sCol) {
     const int lane = threadIdx.x & 31;
     double carry_max = 0.0;      // the child's runmax when continuing (its atomic max may still be in flight)
     while (J >= 0) {
@@ -384,8 +459,8 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
         const int psize = r * w;
         T* P = stage_panel(L, psize, sp, (int)a.smem_cap, bar, phase);
         if (a.trace && lane == 0) a.trace[6 * J + 2] = gtimer();
-        if (P != L) warp_task_body(sp, L, true, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
-        else warp_task_body(L, L, false, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J);
+        if (P != L) warp_task_body(sp, L, true, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J, sCol);
+        else warp_task_body(L, L, false, d, c0, w, r, o, runmax, sDw, sSgw, a, dvec, inbox, J, sCol);
         __syncwarp();
         int cont = -1;
         if (lane == 0) {
@@ -420,6 +495,7 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
                                                          T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ T sD[FW][64];
+    __shared__ T sColw[FW][64];
     __shared__ int8_t sSg[FW][64];
     __shared__ uint64_t bars[FW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -436,7 +512,7 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
         }
         J = __shfl_sync(0xffffffffu, J, 0);
         if (J < 0) return;
-        factor_warp_chain(J, a, lval, dvec, inbox, sp, sD[wid], sSg[wid], &bars[wid], phase);
+        factor_warp_chain(J, a, lval, dvec, inbox, sp, sD[wid], sSg[wid], &bars[wid], phase, sColw[wid]);
     }
 }
 
