@@ -539,6 +539,7 @@ struct PsdArgs {
 };
 
 constexpr int PW_MATS = 6;
+constexpr bool kPsdCyclicJacobi = false;   // true: the cyclic ordering everywhere
 
 struct PwView {
     double* M[PW_MATS];
@@ -709,7 +710,9 @@ __device__ __forceinline__ double psd_step_w(const pw::Grp& G, const double* v, 
     else __syncwarp();
     pw::mm(H, Li, D, ld, T, 0);
     pw::mm(H, T, Li, ld, X, 2);                      // Li D Li'
-    const double lmin = pw::sym_min_eig(H, X, ld);
+    // parallel-ordered Jacobi with D's slice as the rotation table (cyclic for tiny sides)
+    static_assert(PW_MATS >= 4, "psd_step_w uses four matrices");
+    const double lmin = (G.nu >= 3 && !kPsdCyclicJacobi) ? pw::sym_min_eig_par(H, X, ld, D) : pw::sym_min_eig(H, X, ld);
     if (!ok) return -1.0;
     return lmin >= 0.0 ? INFINITY : -1.0 / lmin;
 }

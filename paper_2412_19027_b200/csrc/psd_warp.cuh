@@ -202,6 +202,90 @@ __device__ __forceinline__ double sym_min_eig(const Grp& G, double* A, int ld) {
     return gmin(k < n ? A[k * ld + k] : INFINITY, G.g);
 }
 
+// Same eigenvalues by parallel-ordered two-sided Jacobi: a sweep is mu - 1 rounds
+// of the round-robin tournament over mu = nu rounded up to even indices; the
+// rotations of one round act on disjoint index pairs, so they are applied
+// together (all column pairs, then all row pairs) — the sequential chain per
+// sweep is mu - 1 rotation solves instead of mu (mu - 1) / 2.  The rotation of
+// each pair is the cyclic one (same angle formula, zeroes its a_pq), and the
+// stopping test is the same.  scr: 3 * mu doubles of the group's slice.
+__device__ __forceinline__ double sym_min_eig_par(const Grp& G, double* A, int ld, double* scr) {
+    const int k = G.i, n = G.n;
+    const int mu = (G.nu + 1) & ~1, m1 = mu - 1, half = mu >> 1;
+    double* pc = scr;
+    double* ps = scr + mu;
+    int* pq = reinterpret_cast<int*>(scr + 2 * mu);
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0, tot = 0.0;
+        if (k < n)
+            for (int j = 0; j < n; ++j) {
+                const double a2 = A[k * ld + j] * A[k * ld + j];
+                tot += a2;
+                if (j != k) off += a2;
+            }
+        off = gsum(off, G.g);
+        tot = gsum(tot, G.g);
+        const bool done = n == 0 || off <= 1e-32 * tot || off == 0.0;
+        if (__all_sync(0xffffffffu, done)) break;
+        for (int rnd = 0; rnd < m1; ++rnd) {
+            // partner of index k in round rnd (index mu - 1 is the fixed player)
+            int q = -1;
+            if (k < mu) {
+                if (k == mu - 1) q = (rnd * half) % m1;
+                else {
+                    q = ((rnd - k) % m1 + m1) % m1;
+                    if (q == k) q = mu - 1;
+                }
+            }
+            double c = 1.0, sn = 0.0;
+            if (k < mu) {
+                const int p0 = k < q ? k : q, q0 = k < q ? q : k;
+                const bool act = !done && q0 < n;
+                const double apq = act ? A[p0 * ld + q0] : 0.0;
+                if (act && apq != 0.0) {
+                    const double app = A[p0 * ld + p0], aqq = A[q0 * ld + q0];
+                    const double theta = (aqq - app) / (2.0 * apq);
+                    const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    sn = t * c;
+                }
+                pc[k] = c;
+                ps[k] = sn;
+                pq[2 * k] = q;
+            }
+            __syncwarp();
+            if (!done && k < n) {                       // columns: A[k][p], A[k][q] for every pair
+                for (int p = 0; p < n; ++p) {
+                    const int qq = pq[2 * p];
+                    if (qq <= p || qq >= n) continue;
+                    const double cc = pc[p], ss = ps[p];
+                    const double akp = A[k * ld + p], akq = A[k * ld + qq];
+                    A[k * ld + p] = cc * akp - ss * akq;
+                    A[k * ld + qq] = ss * akp + cc * akq;
+                }
+            }
+            __syncwarp();
+            if (!done && k < n) {                       // rows: A[p][k], A[q][k] for every pair
+                for (int p = 0; p < n; ++p) {
+                    const int qq = pq[2 * p];
+                    if (qq <= p || qq >= n) continue;
+                    const double cc = pc[p], ss = ps[p];
+                    const double apk = A[p * ld + k], aqk = A[qq * ld + k];
+                    A[p * ld + k] = cc * apk - ss * aqk;
+                    A[qq * ld + k] = ss * apk + cc * aqk;
+                }
+            }
+            __syncwarp();
+            if (!done && k < n && q > k && q < n && ps[k] != 0.0) {   // the rotated pairs' a_pq = 0
+                A[k * ld + q] = 0.0;
+                A[q * ld + k] = 0.0;
+            }
+            __syncwarp();
+        }
+    }
+    return gmin(k < n ? A[k * ld + k] : INFINITY, G.g);
+}
+
 // NT factor (psdcone.py:98-117): R = Ls V diag(sig^-1/2), R^-1 = diag(sig^1/2) V' Ls^-1,
 // lam = sig; uses the work matrices W0..W3 of the group slice
 __device__ __forceinline__ bool nt_factor(const Grp& G, const double* s, const double* z, int ld, double* W0,
