@@ -24,6 +24,7 @@ void k_nb_resolve(Ctx& c, int g0, int nk);
 void k_kkt_residual_one(Ctx& c, int q);
 void k_kkt_residual(Ctx& c, int nrhs);
 void k_refine_finish(Ctx& c, int nrhs);
+void k_refine_gather(Ctx& c, int nrhs);
 void k_kkt_matvec_only(Ctx& c, int q);
 void k_refine_init_one(Ctx& c, int q);
 void k_copy(Ctx& c, const double* src, double* dst, int64_t n);
@@ -119,7 +120,7 @@ int refine_graph(Ctx& c, int nrhs, int* steps_out) {
         const int64_t l0 = c.launches;
         CIPM_CUDA(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         int active[2] = {1, nrhs > 1 ? 1 : 0};
-        k_refine_step(c, nrhs, active);
+        k_refine_step(c, nrhs, active, !c.resid_gathers);
         k_kkt_residual(c, nrhs);
         k_refine_continue(c, h, nrhs);
         cudaGraph_t captured = nullptr;
@@ -135,6 +136,7 @@ int refine_graph(Ctx& c, int nrhs, int* steps_out) {
         c.launches = l0;
     }
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    if (c.resid_gathers) k_refine_gather(c, nrhs);
     CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
     CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
     k_refine_finish(c, nrhs);
@@ -154,10 +156,11 @@ int refine_graph(Ctx& c, int nrhs, int* steps_out) {
 int refine(Ctx& c, int nrhs, int* steps_out) {
     if (c.use_graphs && !c.profile && !c.trace) return refine_graph(c, nrhs, steps_out);
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    if (c.resid_gathers) k_refine_gather(c, nrhs);
     int active[2] = {1, nrhs > 1 ? 1 : 0};
     int steps = 0;
     for (int step = 1; step <= c.refine_max; ++step) {
-        k_refine_step(c, nrhs, active);
+        k_refine_step(c, nrhs, active, !c.resid_gathers);
         k_kkt_residual(c, nrhs);
         c.d2h_bytes += sizeof(double) * 16 + sizeof(int);
         CIPM_CUDA(cudaMemcpyAsync(c.h_rstate, c.rstate, sizeof(double) * 16, cudaMemcpyDeviceToHost, c.stream));
@@ -240,6 +243,7 @@ int refine_async(Ctx& c, int nrhs, int slot) {
         return CIPM_OK;
     }
     for (int q = 0; q < nrhs; ++q) k_refine_init_one(c, q);
+    if (c.resid_gathers) k_refine_gather(c, nrhs);
     CIPM_CUDA(cudaMemsetAsync(c.refine_iter, 0, sizeof(int), c.stream));
     CIPM_CUDA(cudaGraphLaunch(c.refine_graph[nrhs], c.stream));
     k_refine_finish(c, nrhs);
@@ -597,6 +601,11 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     c.sym.nsuper = S.nsuper;
     c.sym.nnz_storage = S.nnz_storage;
     TRY(upload(c, &c.sym.perm, S.perm.data(), c.dim));
+    {
+        std::vector<int32_t> ip(c.dim);
+        for (int64_t k = 0; k < c.dim; ++k) ip[S.perm[k]] = (int32_t)k;
+        TRY(upload(c, &c.sym.iperm, ip.data(), c.dim));
+    }
     TRY(upload(c, &c.sym.sn_col, S.sn_col.data(), S.nsuper + 1));
     TRY(upload(c, &c.sym.sn_rptr, S.sn_rptr.data(), S.nsuper + 1));
     TRY(upload(c, &c.sym.sn_rows, S.sn_rows.data(), (int64_t)S.sn_rows.size()));
@@ -741,6 +750,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     CIPM_CUDA(cudaEventCreateWithFlags(&c.join_ev, cudaEventDisableTiming));
     CIPM_CUDA(cudaStreamCreateWithFlags(&c.tail_side, cudaStreamNonBlocking));
     for (auto& e : c.tail_ev) CIPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.resid_gathers = fused_resid_ok(c) && !getenv("CIPM_NO_RESID_GATHER");
     c.factor_blocks = factor_grid(c);
     c.solve_blocks = solve_grid(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));

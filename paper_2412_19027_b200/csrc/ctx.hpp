@@ -21,6 +21,7 @@ namespace cipm {
 struct DevSymbolic {
     int32_t nsuper = 0;
     int32_t* perm = nullptr;        // dim: permuted position -> original index
+    int32_t* iperm = nullptr;       // dim: original index -> permuted position
     int32_t* sn_col = nullptr;      // nsuper+1
     int64_t* sn_rptr = nullptr;     // nsuper+1
     int32_t* sn_rows = nullptr;
@@ -173,6 +174,7 @@ struct Ctx {
     void* tinv = nullptr;            // inverses of the 64x64 diagonal blocks (T)
     int32_t* tflags = nullptr;       // per tail node: fwd flags, bwd flags, 2 tickets
     int64_t tflag_total = 0;
+    bool resid_gathers = false;      // LP/QP: the fused residual writes the permuted RHS (no gather pass)
 
     // refinement (up to 2 right-hand sides, [rhs][dim])
     double *rb = nullptr, *rx = nullptr, *rr = nullptr, *rbest = nullptr;
@@ -269,7 +271,8 @@ void k_scaling_values(Ctx& c, double* diag, double* blocks);
 void k_build_base(Ctx& c);
 void k_assemble(Ctx& c);
 int k_factor(Ctx& c);
-void k_refine_step(Ctx& c, int nrhs, const int* active_host);
+void k_refine_step(Ctx& c, int nrhs, const int* active_host, bool gather = true);
+bool fused_resid_ok(const Ctx& c);
 // setup.cu
 int k_set_problem(Ctx& c, bool equilibrate);
 // dense.cu

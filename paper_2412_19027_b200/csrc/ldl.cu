@@ -1780,11 +1780,11 @@ struct PhaseTimer {
 };
 
 template <typename T>
-void refine_solve_t(Ctx& c, int act0, int act1) {
+void refine_solve_t(Ctx& c, int act0, int act1, bool gather) {
     PhaseTimer pt(c);
     T* t = (T*)c.rt;
     cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * 8, c.stream);
-    gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1, c.rstate,
+    if (gather) gather_perm<T><<<grid_for(c.dim), kThreads, 0, c.stream>>>(c.rr, t, c.sym.perm, c.dim, act0, act1, c.rstate,
                                                                c.fac_count, c.sym.nsuper, c.bwd_done, c.sym.nsuper,
                                                                c.tflags, c.tflag_total);
     int e0 = 0;
@@ -1858,11 +1858,26 @@ int k_factor(Ctx& c) {
 }
 
 // one refinement correction: x += solve(r) for the active right-hand sides
-void k_refine_step(Ctx& c, int nrhs, const int* active) {
+void k_refine_step(Ctx& c, int nrhs, const int* active, bool gather) {
     const int a0 = active[0], a1 = nrhs > 1 ? active[1] : 0;
     if (c.profile) c.solve_rhs += a0 + a1;
-    if (c.precision == CIPM_FULL) refine_solve_t<double>(c, a0, a1);
-    else refine_solve_t<float>(c, a0, a1);
+    if (c.precision == CIPM_FULL) refine_solve_t<double>(c, a0, a1, gather);
+    else refine_solve_t<float>(c, a0, a1, gather);
+}
+
+// the first step's permuted right-hand side (and the sweep counters' reset) when the
+// fused residual gathers for the later steps
+void k_refine_gather(Ctx& c, int nrhs) {
+    const int a1 = nrhs > 1 ? 1 : 0;
+    if (c.precision == CIPM_FULL)
+        gather_perm<double><<<grid_for(c.dim), kThreads, 0, c.stream>>>(
+            c.rr, (double*)c.rt, c.sym.perm, c.dim, 1, a1, c.rstate, c.fac_count, c.sym.nsuper, c.bwd_done,
+            c.sym.nsuper, c.tflags, c.tflag_total);
+    else
+        gather_perm<float><<<grid_for(c.dim), kThreads, 0, c.stream>>>(
+            c.rr, (float*)c.rt, c.sym.perm, c.dim, 1, a1, c.rstate, c.fac_count, c.sym.nsuper, c.bwd_done,
+            c.sym.nsuper, c.tflags, c.tflag_total);
+    c.launches++;
 }
 
 }  // namespace cipm

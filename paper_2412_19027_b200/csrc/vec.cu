@@ -476,8 +476,15 @@ struct Res2Args {
     double* st;                  // rstate (8 per rhs)
     int64_t n, m, dim, zero_dim;
     int nrhs;
+    // the next step's permuted right-hand side t[iperm[i]] = r_i (T = the factor's
+    // precision), and the sweeps' counters reset (what gather_perm does otherwise)
+    void* t;
+    const int32_t* iperm;
+    int32_t *z0, *z1, *z2;
+    int64_t n0, n1, n2;
 };
 
+template <typename T>
 __global__ void __launch_bounds__(kThreads) kkt_resid2(Res2Args a, double* partials, unsigned int* counter) {
     const bool act0 = a.st[4] == 0.0, act1 = a.nrhs > 1 && a.st[12] == 0.0;
     if (!act0 && !act1) return;          // uniform across the grid: no block enters the reduction
@@ -512,16 +519,26 @@ __global__ void __launch_bounds__(kThreads) kkt_resid2(Res2Args a, double* parti
             k0 -= hj * x0[i];
             if (act1) k1 -= hj * x1[i];
         }
+        T* t = reinterpret_cast<T*>(a.t);
+        const int32_t pi = a.t ? a.iperm[i] : 0;
         if (act0) {
             const double r0 = a.b[i] - k0;
             a.r[i] = r0;
+            if (a.t) t[pi] = (T)r0;
             v[0] = fmax(v[0], fabs(r0));
         }
         if (act1) {
             const double r1 = a.b[a.dim + i] - k1;
             a.r[a.dim + i] = r1;
+            if (a.t) t[a.dim + pi] = (T)r1;
             v[1] = fmax(v[1], fabs(r1));
         }
+    }
+    if (a.t) {
+        const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t i = k; i < a.n0; i += st) a.z0[i] = 0;
+        for (int64_t i = k; i < a.n1; i += st) a.z1[i] = 0;
+        for (int64_t i = k; i < a.n2; i += st) a.z2[i] = 0;
     }
     double out[2];
     if (grid_reduce<2>(v, ops, partials, counter, out)) {
@@ -832,15 +849,23 @@ void k_kkt_residual_one(Ctx& c, int q) {
     c.launches++;
 }
 
+// zero / nonneg cones only: the fused residual (and its gather of the next RHS)
+bool fused_resid_ok(const Ctx& c) {
+    static const bool fused_env = !getenv("CIPM_NO_FUSED_RESID");
+    return fused_env && c.nsoc == 0 && c.nsym == 0 && c.npsd == 0 && c.lin == c.m;
+}
+
 // the residual step of one refinement step for the active right-hand sides q < nrhs
 // (the improved iterate is copied to rbest by the next step's scatter, or by
 // k_refine_finish after the last step)
 void k_kkt_residual(Ctx& c, int nrhs) {
-    static const bool fused_env = !getenv("CIPM_NO_FUSED_RESID");
-    if (fused_env && c.nsoc == 0 && c.nsym == 0 && c.npsd == 0 && c.lin == c.m) {
+    if (fused_resid_ok(c)) {
         Res2Args a{c.p_rp, c.p_ci, c.p_v, c.at_rp, c.at_ci, c.at_v, c.a_rp, c.a_ci, c.a_v, c.nn_h,
-                   c.rx, c.rb, c.rr, c.rstate, c.n, c.m, c.dim, c.zero_dim, nrhs};
-        kkt_resid2<<<red_grid(c.dim), kThreads, 0, c.stream>>>(a, c.partials, c.counter);
+                   c.rx, c.rb, c.rr, c.rstate, c.n, c.m, c.dim, c.zero_dim, nrhs,
+                   c.resid_gathers ? c.rt : nullptr, c.sym.iperm, c.fac_count, c.bwd_done, c.tflags,
+                   c.sym.nsuper, c.sym.nsuper, c.tflag_total};
+        if (c.precision == CIPM_FULL) kkt_resid2<double><<<red_grid(c.dim), kThreads, 0, c.stream>>>(a, c.partials, c.counter);
+        else kkt_resid2<float><<<red_grid(c.dim), kThreads, 0, c.stream>>>(a, c.partials, c.counter);
         c.launches++;
         return;
     }
