@@ -490,6 +490,11 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         psd_deg += (double)sd;
     }
     c.hblk_total = hp;
+    {
+        bool uni = c.npsd > 0 && c.psd_max_side <= 8 && !getenv("CIPM_PSD_WARP");
+        for (int64_t i = 0; i < c.npsd && uni; ++i) uni = d->psd_side[i] == c.psd_max_side;
+        c.psd_uni = uni ? c.psd_max_side : 0;
+    }
     for (int64_t i = 0; i < c.nsoc; ++i) c.host_blocks.emplace_back(0, (int)d->soc_dim[i]);
     for (int64_t i = 0; i < c.npsd; ++i) c.host_blocks.emplace_back(3, (int)d->psd_side[i]);
     c.psd_mat_total = mp;

@@ -19,6 +19,7 @@
 #include "ctx.hpp"
 #include "nsym.cuh"
 #include "psd_warp.cuh"
+#include "psd_reg.cuh"
 #include <algorithm>
 
 namespace cipm {
@@ -797,6 +798,138 @@ __global__ void psd_membership_w(PsdArgs a, const double* s, const double* z, in
     }
 }
 
+// ---- equal sides N <= 8: one thread per cone, matrices in registers (psd_reg.cuh) ----
+
+template <int N>
+__global__ void __launch_bounds__(64) psd_step_bound_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                       const double* z, const double* s, const double* dz,
+                                                       const double* ds, double* sc, int* err) {
+    // two threads per cone (even lane: z, odd lane: s), each a full step_bound
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t c = t >> 1;
+    double b = INFINITY;
+    bool bad = false;
+    if (c < npsd) {
+        const int off = off_[c];
+        const double bb = (t & 1) ? pr::step_bound<N>(s + off, ds + off) : pr::step_bound<N>(z + off, dz + off);
+        bad = bb < 0.0;
+        b = bb;
+    }
+    // the cone's DomainError when either bound failed (psdcone.py), else its min
+    const bool bad2 = bad || __shfl_xor_sync(0xffffffffu, (int)bad, 1);
+    if (bad2) {
+        if (bad && c < npsd) set_error(err, CIPM_E_DOMAIN);
+        b = INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if ((threadIdx.x & 31) == 0 && b < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, b);
+}
+
+// out = alpha u + beta svec(Q smat(v) Q)
+template <int N>
+__global__ void __launch_bounds__(128) psd_apply_h_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                     const int64_t* __restrict__ mptr, const double* Q,
+                                                     const double* v, double* out, double alpha, const double* u,
+                                                     double beta, const double* skip) {
+    if (skip && *skip != 0.0) return;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= npsd) return;
+    const int off = off_[c];
+    const double* Qc = Q + mptr[c];
+    double Qs[pr::Tri<N>::T], X[pr::Tri<N>::T], Y[pr::Tri<N>::T];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) Qs[pr::P(i, j)] = Qc[i * N + j];
+    pr::smat<N>(v + off, X);
+    pr::congr_sym<N>(Qs, X, Y);
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = j; i < N; ++i) {
+            const int k = pr::SV(i, j, N);
+            const double hv = i == j ? Y[pr::P(i, i)] : pr::kR2 * Y[pr::P(i, j)];
+            const double b0 = u ? alpha * u[off + k] : 0.0;
+            out[off + k] = b0 + beta * hv;
+        }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) psd_neighborhood_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                          const double* s, const double* z, const double* ds,
+                                                          const double* dz, const double* nb, int nk, double beta,
+                                                          unsigned int* mask, int* err) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned int bits = (1u << nk) - 1u;
+    if (c < npsd) {
+        const int off = off_[c];
+        constexpr int T = pr::Tri<N>::T;
+        bits = 0u;
+        for (int k = 0; k < nk; ++k) {
+            const double step = nb[16 + k];
+            double sv[T], zv[T];
+#pragma unroll
+            for (int e = 0; e < T; ++e) {
+                sv[e] = s[off + e] + step * ds[off + e];
+                zv[e] = z[off + e] + step * dz[off + e];
+            }
+            double Si[T], Zi[T];
+            const bool ok1 = pr::sym_inv<N>(sv, Si);
+            const bool ok2 = pr::sym_inv<N>(zv, Zi);
+            if (!ok1 || !ok2) {
+                set_error(err, CIPM_E_DOMAIN);
+                continue;
+            }
+            double tr = 0.0;                             // tr(S^-1 Z^-1), row by row as the warp version
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc += Si[pr::P(i, j)] * Zi[pr::P(j, i)];
+                tr += acc;
+            }
+            if (!((double)N / tr < beta * nb[k])) bits |= 1u << k;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bits &= __shfl_xor_sync(0xffffffffu, bits, o);
+    if ((threadIdx.x & 31) == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) psd_membership_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                        const double* s, const double* z, int* err) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= npsd) return;
+    const int off = off_[c];
+    double A[pr::Tri<N>::T], B[pr::Tri<N>::T];
+    pr::smat<N>(s + off, A);
+    pr::smat<N>(z + off, B);
+    const bool ok1 = pr::chol<N>(A), ok2 = pr::chol<N>(B);
+    if (!ok1 || !ok2) set_error(err, CIPM_E_INTERIOR);
+}
+
+// dispatch on the uniform side (returns false: use the lane-group kernels)
+#define PSD_REG_DISPATCH(KERNEL, ...) PSD_REG_DISPATCH_T(KERNEL, 1, 128, __VA_ARGS__)
+#define PSD_REG_DISPATCH_T(KERNEL, TPC, BS, ...)                                              \
+    ([&]() -> bool {                                                                          \
+        const int g_ = (int)((c.npsd * (TPC) + (BS) - 1) / (BS));                             \
+        switch (c.psd_uni) {                                                                  \
+            case 1: KERNEL<1><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 2: KERNEL<2><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 3: KERNEL<3><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 4: KERNEL<4><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 5: KERNEL<5><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 6: KERNEL<6><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 7: KERNEL<7><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            case 8: KERNEL<8><<<g_, BS, 0, c.stream>>>(__VA_ARGS__); break;                  \
+            default: return false;                                                            \
+        }                                                                                     \
+        c.launches++;                                                                         \
+        return true;                                                                          \
+    }())
+
 // ============================== launch glue ================================
 
 SocArgs soc_args(Ctx& c) {
@@ -942,7 +1075,8 @@ void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double*
         nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta, skip);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_apply_h_w, pa_, c.psd_q, v, out, alpha, u, beta, skip);
+    if (c.npsd && !PSD_REG_DISPATCH(psd_apply_h_r, c.npsd, c.psd_off, c.psd_mptr, c.psd_q, v, out, alpha, u, beta, skip))
+        PSD_DISPATCH(psd_apply_h_w, pa_, c.psd_q, v, out, alpha, u, beta, skip);
 }
 
 void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a) {
@@ -974,7 +1108,8 @@ void k_step_bound(Ctx& c, const double* dz, const double* ds) {
         soc_step_bound<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.z, c.s, dz, ds, c.sc);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_step_bound_w, pa_, c.z, c.s, dz, ds, c.sc, c.err);
+    if (c.npsd && !PSD_REG_DISPATCH_T(psd_step_bound_r, 2, 64, c.npsd, c.psd_off, c.z, c.s, dz, ds, c.sc, c.err))
+        PSD_DISPATCH(psd_step_bound_w, pa_, c.z, c.s, dz, ds, c.sc, c.err);
 }
 
 void k_nsym_feasible_mask(Ctx& c, const double* dz, const double* ds, int k0) {
@@ -997,7 +1132,8 @@ void k_neighborhood_mask(Ctx& c, int k0, int nk) {
                                                                        c.nb, nk, c.beta, c.mask, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_neighborhood_w, pa_, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err);
+    if (c.npsd && !PSD_REG_DISPATCH(psd_neighborhood_r, c.npsd, c.psd_off, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err))
+        PSD_DISPATCH(psd_neighborhood_w, pa_, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err);
 }
 
 void k_membership(Ctx& c) {
@@ -1013,7 +1149,8 @@ void k_membership(Ctx& c) {
         nsym_membership<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_membership_w, pa_, c.s, c.z, c.err);
+    if (c.npsd && !PSD_REG_DISPATCH(psd_membership_r, c.npsd, c.psd_off, c.s, c.z, c.err))
+        PSD_DISPATCH(psd_membership_w, pa_, c.s, c.z, c.err);
 }
 
 void k_soc_residuals(Ctx& c, const double* x, double* out) {
