@@ -800,83 +800,135 @@ __global__ void psd_membership_w(PsdArgs a, const double* s, const double* z, in
 
 // ---- equal sides N <= 8: one thread per cone, matrices in registers (psd_reg.cuh) ----
 
+// cone data of a warp's cones is contiguous (svec blocks and N x N blocks in cone
+// order): staged through shared memory with coalesced loads, one padded (odd
+// stride, few bank conflicts) row per cone, then each thread works on its own row
+template <int PER, int STRIDE>
+__device__ __forceinline__ void stage_rows(const double* __restrict__ src, int cnt, double* dst) {
+    const int lane = threadIdx.x & 31, tot = cnt * PER;
+    double v[PER];                                   // every load of the lane in flight at once
+#pragma unroll
+    for (int u = 0; u < PER; ++u) v[u] = lane + 32 * u < tot ? src[lane + 32 * u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const int e = lane + 32 * u;
+        if (e < tot) dst[(e / PER) * STRIDE + e % PER] = v[u];
+    }
+}
+
 template <int N>
-__global__ void __launch_bounds__(64) psd_step_bound_r(int64_t npsd, const int32_t* __restrict__ off_,
+__global__ void __launch_bounds__(32) psd_step_bound_r(int64_t npsd, const int32_t* __restrict__ off_,
                                                        const double* z, const double* s, const double* dz,
                                                        const double* ds, double* sc, int* err) {
-    // two threads per cone (even lane: z, odd lane: s), each a full step_bound
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t c = t >> 1;
+    // two threads per cone (even lane: z, odd lane: s), 16 cones per warp
+    constexpr int T = pr::Tri<N>::T, ST = T | 1;
+    __shared__ double sv[1][2][16 * ST], sd[1][2][16 * ST];
+    const int lane = threadIdx.x & 31, w = 0;     // one warp per block (the staging buffers)
+    const int64_t c0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) >> 1;
+    const int cnt = (int)(npsd - c0 < 16 ? npsd - c0 : 16);
+    if (cnt <= 0) return;
+    const int o0 = off_[c0];
+    stage_rows<T, ST>(z + o0, cnt, sv[w][0]);
+    stage_rows<T, ST>(s + o0, cnt, sv[w][1]);
+    stage_rows<T, ST>(dz + o0, cnt, sd[w][0]);
+    stage_rows<T, ST>(ds + o0, cnt, sd[w][1]);
+    __syncwarp();
+    const int k = lane >> 1, which = lane & 1;
     double b = INFINITY;
     bool bad = false;
-    if (c < npsd) {
-        const int off = off_[c];
-        const double bb = (t & 1) ? pr::step_bound<N>(s + off, ds + off) : pr::step_bound<N>(z + off, dz + off);
+    if (k < cnt) {
+        const double bb = pr::step_bound<N>(sv[w][which] + k * ST, sd[w][which] + k * ST);
         bad = bb < 0.0;
         b = bb;
     }
     // the cone's DomainError when either bound failed (psdcone.py), else its min
     const bool bad2 = bad || __shfl_xor_sync(0xffffffffu, (int)bad, 1);
     if (bad2) {
-        if (bad && c < npsd) set_error(err, CIPM_E_DOMAIN);
+        if (bad) set_error(err, CIPM_E_DOMAIN);
         b = INFINITY;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(0xffffffffu, b, o));
-    if ((threadIdx.x & 31) == 0 && b < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, b);
+    if (lane == 0 && b < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, b);
 }
 
 // out = alpha u + beta svec(Q smat(v) Q)
 template <int N>
-__global__ void __launch_bounds__(128) psd_apply_h_r(int64_t npsd, const int32_t* __restrict__ off_,
-                                                     const int64_t* __restrict__ mptr, const double* Q,
-                                                     const double* v, double* out, double alpha, const double* u,
-                                                     double beta, const double* skip) {
+__global__ void __launch_bounds__(32) psd_apply_h_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                    const int64_t* __restrict__ mptr, const double* Q,
+                                                    const double* v, double* out, double alpha, const double* u,
+                                                    double beta, const double* skip) {
     if (skip && *skip != 0.0) return;
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c >= npsd) return;
-    const int off = off_[c];
-    const double* Qc = Q + mptr[c];
-    double Qs[pr::Tri<N>::T], X[pr::Tri<N>::T], Y[pr::Tri<N>::T];
+    constexpr int T = pr::Tri<N>::T, ST = T | 1, NN = N * N, SQ = NN | 1;
+    __shared__ double sQ[1][32 * SQ], sV[1][32 * ST];
+    const int lane = threadIdx.x & 31, w = 0;     // one warp per block (the staging buffers)
+    const int64_t c0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31);
+    const int cnt = (int)(npsd - c0 < 32 ? npsd - c0 : 32);
+    if (cnt <= 0) return;
+    const int o0 = off_[c0];
+    stage_rows<NN, SQ>(Q + mptr[c0], cnt, sQ[w]);
+    stage_rows<T, ST>(v + o0, cnt, sV[w]);
+    __syncwarp();
+    if (lane < cnt) {
+        const double* Qr = sQ[w] + lane * SQ;
+        double Qs[T], X[T], Y[T];
 #pragma unroll
-    for (int i = 0; i < N; ++i)
+        for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int j = 0; j <= i; ++j) Qs[pr::P(i, j)] = Qc[i * N + j];
-    pr::smat<N>(v + off, X);
-    pr::congr_sym<N>(Qs, X, Y);
+            for (int j = 0; j <= i; ++j) Qs[pr::P(i, j)] = Qr[i * N + j];
+        pr::smat<N>(sV[w] + lane * ST, X);
+        pr::congr_sym<N>(Qs, X, Y);
+        double* Vr = sV[w] + lane * ST;
 #pragma unroll
-    for (int j = 0; j < N; ++j)
+        for (int j = 0; j < N; ++j)
 #pragma unroll
-        for (int i = j; i < N; ++i) {
-            const int k = pr::SV(i, j, N);
-            const double hv = i == j ? Y[pr::P(i, i)] : pr::kR2 * Y[pr::P(i, j)];
-            const double b0 = u ? alpha * u[off + k] : 0.0;
-            out[off + k] = b0 + beta * hv;
+            for (int i = j; i < N; ++i) Vr[pr::SV(i, j, N)] = i == j ? Y[pr::P(i, i)] : pr::kR2 * Y[pr::P(i, j)];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+        const int e = lane + 32 * k;
+        if (e < cnt * T) {
+            const double hv = sV[w][(e / T) * ST + e % T];
+            const double b0 = u ? alpha * u[o0 + e] : 0.0;
+            out[o0 + e] = b0 + beta * hv;
         }
+    }
 }
 
 template <int N>
-__global__ void __launch_bounds__(128) psd_neighborhood_r(int64_t npsd, const int32_t* __restrict__ off_,
-                                                          const double* s, const double* z, const double* ds,
-                                                          const double* dz, const double* nb, int nk, double beta,
-                                                          unsigned int* mask, int* err) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(32) psd_neighborhood_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                         const double* s, const double* z, const double* ds,
+                                                         const double* dz, const double* nb, int nk, double beta,
+                                                         unsigned int* mask, int* err) {
+    constexpr int T = pr::Tri<N>::T, ST = T | 1;
+    __shared__ double sS[1][32 * ST], sZ[1][32 * ST], sDS[1][32 * ST], sDZ[1][32 * ST];
+    const int lane = threadIdx.x & 31, w = 0;     // one warp per block (the staging buffers)
+    const int64_t c0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31);
+    const int cnt = (int)(npsd - c0 < 32 ? npsd - c0 : 32);
+    if (cnt <= 0) return;
+    const int o0 = off_[c0];
+    stage_rows<T, ST>(s + o0, cnt, sS[w]);
+    stage_rows<T, ST>(z + o0, cnt, sZ[w]);
+    stage_rows<T, ST>(ds + o0, cnt, sDS[w]);
+    stage_rows<T, ST>(dz + o0, cnt, sDZ[w]);
+    __syncwarp();
     unsigned int bits = (1u << nk) - 1u;
-    if (c < npsd) {
-        const int off = off_[c];
-        constexpr int T = pr::Tri<N>::T;
+    if (lane < cnt) {
+        const double *sr = sS[w] + lane * ST, *zr = sZ[w] + lane * ST;
+        const double *dsr = sDS[w] + lane * ST, *dzr = sDZ[w] + lane * ST;
         bits = 0u;
         for (int k = 0; k < nk; ++k) {
             const double step = nb[16 + k];
-            double sv[T], zv[T];
+            double svk[T], zvk[T];
 #pragma unroll
             for (int e = 0; e < T; ++e) {
-                sv[e] = s[off + e] + step * ds[off + e];
-                zv[e] = z[off + e] + step * dz[off + e];
+                svk[e] = sr[e] + step * dsr[e];
+                zvk[e] = zr[e] + step * dzr[e];
             }
             double Si[T], Zi[T];
-            const bool ok1 = pr::sym_inv<N>(sv, Si);
-            const bool ok2 = pr::sym_inv<N>(zv, Zi);
+            const bool ok1 = pr::sym_inv<N>(svk, Si);
+            const bool ok2 = pr::sym_inv<N>(zvk, Zi);
             if (!ok1 || !ok2) {
                 set_error(err, CIPM_E_DOMAIN);
                 continue;
@@ -894,7 +946,7 @@ __global__ void __launch_bounds__(128) psd_neighborhood_r(int64_t npsd, const in
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bits &= __shfl_xor_sync(0xffffffffu, bits, o);
-    if ((threadIdx.x & 31) == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
+    if (lane == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
 }
 
 template <int N>
@@ -1075,7 +1127,7 @@ void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double*
         nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta, skip);
         c.launches++;
     }
-    if (c.npsd && !PSD_REG_DISPATCH(psd_apply_h_r, c.npsd, c.psd_off, c.psd_mptr, c.psd_q, v, out, alpha, u, beta, skip))
+    if (c.npsd && !PSD_REG_DISPATCH_T(psd_apply_h_r, 1, 32, c.npsd, c.psd_off, c.psd_mptr, c.psd_q, v, out, alpha, u, beta, skip))
         PSD_DISPATCH(psd_apply_h_w, pa_, c.psd_q, v, out, alpha, u, beta, skip);
 }
 
@@ -1108,7 +1160,7 @@ void k_step_bound(Ctx& c, const double* dz, const double* ds) {
         soc_step_bound<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.z, c.s, dz, ds, c.sc);
         c.launches++;
     }
-    if (c.npsd && !PSD_REG_DISPATCH_T(psd_step_bound_r, 2, 64, c.npsd, c.psd_off, c.z, c.s, dz, ds, c.sc, c.err))
+    if (c.npsd && !PSD_REG_DISPATCH_T(psd_step_bound_r, 2, 32, c.npsd, c.psd_off, c.z, c.s, dz, ds, c.sc, c.err))
         PSD_DISPATCH(psd_step_bound_w, pa_, c.z, c.s, dz, ds, c.sc, c.err);
 }
 
@@ -1132,7 +1184,7 @@ void k_neighborhood_mask(Ctx& c, int k0, int nk) {
                                                                        c.nb, nk, c.beta, c.mask, c.err);
         c.launches++;
     }
-    if (c.npsd && !PSD_REG_DISPATCH(psd_neighborhood_r, c.npsd, c.psd_off, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err))
+    if (c.npsd && !PSD_REG_DISPATCH_T(psd_neighborhood_r, 1, 32, c.npsd, c.psd_off, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err))
         PSD_DISPATCH(psd_neighborhood_w, pa_, c.s, c.z, c.ds[1], c.dz[1], c.nb, nk, c.beta, c.mask, c.err);
 }
 
