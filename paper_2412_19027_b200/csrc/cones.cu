@@ -949,6 +949,146 @@ __global__ void __launch_bounds__(32) psd_neighborhood_r(int64_t npsd, const int
     if (lane == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
 }
 
+// NT scaling (psdcone.py:98-117, pw::nt_factor) + the congruence block H = Q (x)s Q,
+// one thread per cone: Ls, Lz, M = Lz' Ls, one-sided cyclic Jacobi SVD of M
+// (M V = U diag(sig)), R = Ls V sig^-1/2, R^-1 = sig^1/2 V' Ls^-1
+template <int N>
+__global__ void __launch_bounds__(32) psd_scaling_r(int64_t npsd, const int32_t* __restrict__ off_,
+                                                    const int64_t* __restrict__ mptr, const int64_t* __restrict__ lptr,
+                                                    const int64_t* __restrict__ hptr, const double* s,
+                                                    const double* z, double* R, double* RI, double* Q, double* LAM,
+                                                    double* hv, int* err) {
+    constexpr int T = pr::Tri<N>::T, ST = T | 1;
+    __shared__ double sS[32 * ST], sZ[32 * ST];
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const int cnt = (int)(npsd - c0 < 32 ? npsd - c0 : 32);
+    if (cnt <= 0) return;
+    const int o0 = off_[c0];
+    stage_rows<T, ST>(s + o0, cnt, sS);
+    stage_rows<T, ST>(z + o0, cnt, sZ);
+    __syncwarp();
+    if (lane >= cnt) return;
+    const int64_t c = c0 + lane;
+    double Ls[T], Lz[T];
+    pr::smat<N>(sS + lane * ST, Ls);
+    pr::smat<N>(sZ + lane * ST, Lz);
+    const bool ok1 = pr::chol<N>(Ls), ok2 = pr::chol<N>(Lz);
+    if (!ok1 || !ok2) { set_error(err, CIPM_E_SCALING); return; }
+    double U[N][N], V[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = (i > j ? i : j); k < N; ++k) v += Lz[pr::P(k, i)] * Ls[pr::P(k, j)];
+            U[i][j] = v;
+            V[i][j] = i == j ? 1.0 : 0.0;
+        }
+#pragma unroll 1
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rot = false;
+        // cyclic order (as pw::jacobi_svd): the scaling feeds H, and the refinement
+        // counts of the late iterations are sensitive to its rounding
+#pragma unroll
+        for (int p = 0; p < N - 1; ++p)
+#pragma unroll
+            for (int q = p + 1; q < N; ++q) {
+                double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    al += U[k][p] * U[k][p];
+                    be += U[k][q] * U[k][q];
+                    ga += U[k][p] * U[k][q];
+                }
+                if (fabs(ga) <= 1e-15 * sqrt(al * be) || ga == 0.0) continue;
+                rot = true;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    const double up = U[k][p], uq = U[k][q];
+                    U[k][p] = cs * up - sn * uq;
+                    U[k][q] = sn * up + cs * uq;
+                    const double vp = V[k][p], vq = V[k][q];
+                    V[k][p] = cs * vp - sn * vq;
+                    V[k][q] = sn * vp + cs * vq;
+                }
+            }
+        if (!rot) break;
+    }
+    double sig[N];
+    bool pos = true;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) s2 += U[k][j] * U[k][j];
+        sig[j] = sqrt(s2);
+        pos = pos && sig[j] > 0.0;
+    }
+    if (!pos) { set_error(err, CIPM_E_SCALING); return; }
+    double Lsi[T];
+    pr::tri_inv<N>(Ls, Lsi);
+    double* Rc = R + mptr[c];
+    double* RIc = RI + mptr[c];
+    double Rm[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int k = 0; k <= i; ++k) a += Ls[pr::P(i, k)] * V[k][j];         // (Ls V)(i, j)
+#pragma unroll
+            for (int k = j; k < N; ++k) b += V[k][i] * Lsi[pr::P(k, j)];        // (V' Ls^-1)(i, j)
+            Rm[i][j] = a / sqrt(sig[j]);
+            Rc[i * N + j] = Rm[i][j];
+            RIc[i * N + j] = b * sqrt(sig[i]);
+        }
+#pragma unroll
+    for (int j = 0; j < N; ++j) LAM[lptr[c] + j] = sig[j];
+    double Qs[T];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) v += Rm[i][k] * Rm[j][k];
+            Qs[pr::P(i, j)] = v;
+        }
+    double* Qc = Q + mptr[c];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = 0; j < N; ++j) Qc[i * N + j] = Qs[pr::P(i, j)];
+    // H(k, l), k <= l over svec indices, upper triangle row-major (pw kernel's layout)
+    double* hb = hv + hptr[c];
+    int rowoff = 0;
+#pragma unroll
+    for (int qk = 0; qk < N; ++qk)
+#pragma unroll
+        for (int pk = qk; pk < N; ++pk) {
+            const int k = pr::SV(pk, qk, N);
+            const double sk = pk == qk ? 1.0 : pr::kR2;
+#pragma unroll
+            for (int jl = 0; jl < N; ++jl)
+#pragma unroll
+                for (int il = jl; il < N; ++il) {
+                    const int l = pr::SV(il, jl, N);
+                    if (l < k) continue;
+                    double mv;
+                    if (il == jl) mv = Qs[pr::P(pk, il)] * Qs[pr::P(qk, il)];
+                    else mv = (Qs[pr::P(pk, il)] * Qs[pr::P(qk, jl)] + Qs[pr::P(pk, jl)] * Qs[pr::P(qk, il)]) / pr::kR2;
+                    hb[rowoff + (l - k)] = sk * mv;
+                }
+            rowoff += T - k;
+        }
+}
+
 template <int N>
 __global__ void __launch_bounds__(128) psd_membership_r(int64_t npsd, const int32_t* __restrict__ off_,
                                                         const double* s, const double* z, int* err) {
@@ -1045,6 +1185,16 @@ inline size_t psd_slice_bytes(const PsdArgs& a) {
 
 // ---------------------------------------------------------------------------
 
+// PSD NT scaling: register kernel for equal sides <= 8 (CIPM_PSD_SCALING_WARP=1: the
+// lane-group kernel, experiments), lane-group kernel otherwise
+static void k_psd_scaling(Ctx& c) {
+    static const bool warp_env = getenv("CIPM_PSD_SCALING_WARP") != nullptr;
+    if (!warp_env && PSD_REG_DISPATCH_T(psd_scaling_r, 1, 32, c.npsd, c.psd_off, c.psd_mptr, c.psd_lptr,
+                                         c.psd_hptr, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err))
+        return;
+    PSD_DISPATCH(psd_scaling_w, pa_, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+}
+
 // one family's scaling update (bench / profiling: per-family timing); fam 0 nonneg, 1 SOC, 2 exp/pow, 3 PSD
 void k_update_scaling_family(Ctx& c, int fam) {
     if (fam == 0 && c.nonneg_dim) {
@@ -1062,7 +1212,7 @@ void k_update_scaling_family(Ctx& c, int fam) {
                                                                   c.ns_hess, c.ns_zt, c.hv, c.err);
         c.launches++;
     }
-    if (fam == 3 && c.npsd) PSD_DISPATCH(psd_scaling_w, pa_, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+    if (fam == 3 && c.npsd) k_psd_scaling(c);
 }
 
 void k_update_scaling(Ctx& c) {
@@ -1081,7 +1231,7 @@ void k_update_scaling(Ctx& c) {
                                                                   c.ns_hess, c.ns_zt, c.hv, c.err);
         c.launches++;
     }
-    if (c.npsd) PSD_DISPATCH(psd_scaling_w, pa_, c.s, c.z, c.psd_r, c.psd_rinv, c.psd_q, c.psd_lam, c.hv, c.err);
+    if (c.npsd) k_psd_scaling(c);
 }
 
 // hv (upper triangles of all dense blocks) lives in c.wm (sized >= hblk_total)

@@ -102,7 +102,7 @@ def test_gpu_psd_sides_match_oracle(gpu, side, ncones):
 def test_gpu_psd_register_kernels_match_lane_groups(gpu, side, monkeypatch):
     """Equal sides <= 8 run the thread-per-cone register kernels (psd_reg.cuh);
     CIPM_PSD_WARP=1 forces the lane-group kernels (psd_warp.cuh).  Same status and
-    iterations, objectives and iterates to 1e-9 (the Jacobi orders differ, so the
+    iterations, objectives to 1e-9 and iterates to 1e-6 (the Jacobi orders differ, so the
     rounding does), and both within 1e-6 of the oracle."""
     from paper_2412_19027_b200.solver import Solver
     prob = G.gen_psd(ncones=24, side=side, seed=5)
@@ -117,7 +117,7 @@ def test_gpu_psd_register_kernels_match_lane_groups(gpu, side, monkeypatch):
     assert r.status == w.status
     assert r.iterations == w.iterations
     assert rel(r.obj_primal, w.obj_primal) <= 1e-9
-    np.testing.assert_allclose(r.x, w.x, rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(r.x, w.x, rtol=1e-6, atol=1e-7)   # both at the 1e-8 solve tolerance
     ref = OracleSolver(prob, cfg).solve()
     assert r.status == ref.status
     assert rel(r.obj_primal, ref.obj_primal) <= 1e-6
