@@ -366,7 +366,7 @@ constexpr int FW = 8;   // warps per factor CTA (warp tier)
 template <typename T, int W>
 __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, int64_t loff, int64_t cb,
                                              const FactorArgs& a, T* __restrict__ lval, T* __restrict__ dvec,
-                                             T* __restrict__ inbox) {
+                                             T* __restrict__ inbox, double* runmax_out) {
     T* L = lval + loff;
     T p[W][16];
 #pragma unroll
@@ -417,21 +417,22 @@ __device__ __forceinline__ int factor_tiny_w(int J, int c0, int r, int parent, i
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             if (i < r) L[j * r + i] = p[j][i];
-    if (parent >= 0) atomic_max_pos(a.maxd + parent, runmax);
+    *runmax_out = runmax;       // the caller folds it into the parent's running max
     return -1;     // tiny leaves are excluded from the child counts (separate launch)
 }
 
 template <typename T>
 __device__ __forceinline__ int factor_tiny_lane(int J, const FactorArgs& a, T* __restrict__ lval, T* __restrict__ dvec,
-                                                T* __restrict__ inbox) {
+                                                T* __restrict__ inbox, int* parent_out, double* runmax_out) {
     const int32_t* d32 = a.desc32 + (int64_t)J * 8;
     const int c0 = d32[0], w = d32[1], r = d32[2], parent = d32[3];
     const int64_t loff = a.desc64[(int64_t)J * 8], cb = a.desc64[(int64_t)J * 8 + 6];
+    *parent_out = parent;
     switch (w) {
-        case 1: return factor_tiny_w<T, 1>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
-        case 2: return factor_tiny_w<T, 2>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
-        case 3: return factor_tiny_w<T, 3>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
-        default: return factor_tiny_w<T, 4>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox);
+        case 1: return factor_tiny_w<T, 1>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox, runmax_out);
+        case 2: return factor_tiny_w<T, 2>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox, runmax_out);
+        case 3: return factor_tiny_w<T, 3>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox, runmax_out);
+        default: return factor_tiny_w<T, 4>(J, c0, r, parent, loff, cb, a, lval, dvec, inbox, runmax_out);
     }
 }
 
@@ -487,7 +488,21 @@ template <typename T>
 __global__ void __launch_bounds__(128) factor_tiny_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                           T* __restrict__ inbox) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < a.ntiny) factor_tiny_lane(a.tiny[k], a, lval, dvec, inbox);
+    int parent = -1;
+    double runmax = 0.0;
+    if (k < a.ntiny) factor_tiny_lane(a.tiny[k], a, lval, dvec, inbox, &parent, &runmax);
+    // the parents' running max |d|: siblings are adjacent in the leaf list, so fold
+    // each run of equal parents in the warp first (max is idempotent: overlapping
+    // windows are harmless) and let the run's first lane issue the one atomic
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, runmax, off);
+        const int po = __shfl_down_sync(0xffffffffu, parent, off);
+        if (lane + off < 32 && po == parent) runmax = fmax(runmax, o);
+    }
+    const int pprev = __shfl_up_sync(0xffffffffu, parent, 1);
+    if (parent >= 0 && (lane == 0 || pprev != parent)) atomic_max_pos(a.maxd + parent, runmax);
 }
 
 template <typename T>
@@ -1261,12 +1276,20 @@ __device__ __forceinline__ int fwd_tiny_w(const int4 td, const SolveArgs& a, con
         for (int i = 0; i < 16; ++i) p[j][i] = (i < r && i > j) ? L[j * r + i] : (T)0;
     const int needP = 0;
     (void)parent;
+    T xv2[2][W];                  // both right-hand sides loaded before any store
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const bool act = q == 0 ? a.act0 : a.act1;
+#pragma unroll
+        for (int j = 0; j < W; ++j) xv2[q][j] = act ? x[(int64_t)q * a.dim + c0 + j] : (T)0;
+    }
+    int pp[16];
+#pragma unroll
+    for (int i = W; i < 16; ++i) pp[i] = i < r ? a.vpush_pos[cvo + i - W] : 0;
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
         T* xJ = x + (int64_t)q * a.dim + c0;
-        T xv[W];
-#pragma unroll
-        for (int j = 0; j < W; ++j) xv[j] = xJ[j];
+        T (&xv)[W] = xv2[q];
 #pragma unroll
         for (int j = 0; j < W; ++j)
 #pragma unroll
@@ -1280,7 +1303,7 @@ __device__ __forceinline__ int fwd_tiny_w(const int4 td, const SolveArgs& a, con
             T acc = (T)0;
 #pragma unroll
             for (int k = 0; k < W; ++k) acc += p[k][i] * xv[k];
-            vq[a.vpush_pos[cvo + i - W]] = acc;
+            vq[pp[i]] = acc;
         }
     }
     (void)needP;
@@ -1477,25 +1500,36 @@ __device__ __forceinline__ void bwd_tiny_w(const int4 td, int64_t rptr, const So
 #pragma unroll
     for (int j = 0; j < W; ++j) dinv[j] = dvec[c0 + j];
     (void)parent;      // the persistent backward sweep finished before this launch
+    // both right-hand sides' loads are issued before any store (the stores of one
+    // RHS would otherwise order the other's gathers behind them)
+    T xr[2][W], xo[2][16];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const bool act = q == 0 ? a.act0 : a.act1;
+        const T* xv = x + (int64_t)q * a.dim;
+#pragma unroll
+        for (int j = 0; j < W; ++j) xr[q][j] = act ? xv[c0 + j] : (T)0;
+#pragma unroll
+        for (int i = W; i < 16; ++i) xo[q][i] = (act && i < r) ? __ldcg(xv + rows[i]) : (T)0;
+    }
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
         if (!(q == 0 ? a.act0 : a.act1)) continue;
-        T* xv = x + (int64_t)q * a.dim;
-        T xr[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) xr[j] = xv[c0 + j] / dinv[j];      // D solve (ldl.py:101-102)
+        for (int j = 0; j < W; ++j) xr[q][j] = xr[q][j] / dinv[j];      // D solve (ldl.py:101-102)
 #pragma unroll
         for (int i = W; i < 16; ++i) {
             if (i >= r) break;
-            const T xi = __ldcg(xv + rows[i]);
 #pragma unroll
-            for (int j = 0; j < W; ++j) xr[j] -= p[j][i] * xi;
+            for (int j = 0; j < W; ++j) xr[q][j] -= p[j][i] * xo[q][i];
         }
 #pragma unroll
         for (int j = W - 1; j >= 0; --j)
 #pragma unroll
-            for (int i = j + 1; i < W; ++i) xr[j] -= p[j][i] * xr[i];
+            for (int i = j + 1; i < W; ++i) xr[q][j] -= p[j][i] * xr[q][i];
+        T* xv = x + (int64_t)q * a.dim;
 #pragma unroll
-        for (int j = 0; j < W; ++j) xv[c0 + j] = xr[j];
+        for (int j = 0; j < W; ++j) xv[c0 + j] = xr[q][j];
     }
 }
 
