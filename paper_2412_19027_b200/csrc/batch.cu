@@ -34,7 +34,7 @@ namespace cipm {
 
 namespace {
 
-constexpr int BT = 128;            // threads per instance CTA
+constexpr int BT = 256;            // threads per instance CTA
 constexpr int NW = BT / 32;
 
 enum BStatus {
