@@ -208,9 +208,13 @@ class BatchSolver:
                                                   pdbl(res), pdbl(x), pdbl(z), pdbl(s)), "batch results")
         secs = self.last_kernel_ms / 1e3 if secs is None else secs
         out = []
+        # plain Python scalars in one conversion each (2048 instances: the per-element
+        # numpy scalar conversions were most of the host time of a batched solve)
+        sts = [_STATUS[v] for v in status.tolist()]
+        rows = res.tolist()
         for k in range(c):
-            st = _STATUS[int(status[k])]
-            g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = res[k]
+            st = sts[k]
+            g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = rows[k]
             # the device returned unscaled, user-row-order iterates (divided by tau unless a certificate)
             x_o, z_o, s_o = x[k], z[k], s[k]
             cert = None
@@ -218,11 +222,10 @@ class BatchSolver:
                 cert = z_o / abs(float(self.problems[k].b @ z_o))
             elif st == Status.DUAL_INFEASIBLE:
                 cert = x_o / abs(float(self.problems[k].q @ x_o))
-            out.append(SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=float(g_p),
-                                   obj_dual=float(g_d), iterations=int(iters), setup_seconds=self.setup_seconds,
-                                   solve_seconds=secs, norm_rp=float(rp), norm_rd=float(rd),
-                                   gap=abs(float(g_p) - float(g_d)), tau=float(tau), kappa=float(kappa),
-                                   mu_initial=float(mu0), mu_final=float(mu)))
+            out.append(SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=g_p,
+                                   obj_dual=g_d, iterations=int(iters), setup_seconds=self.setup_seconds,
+                                   solve_seconds=secs, norm_rp=rp, norm_rd=rd, gap=abs(g_p - g_d), tau=tau,
+                                   kappa=kappa, mu_initial=mu0, mu_final=mu))
         return out
 
     def solve(self):
