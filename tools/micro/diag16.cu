@@ -131,6 +131,27 @@ __global__ void bench(const T* src, T* dst, long long* cyc) {
     for (int i = threadIdx.x; i < TB * TB; i += blockDim.x) S[i] = src[i];
     if (threadIdx.x < TB) sSg[threadIdx.x] = threadIdx.x % 3 ? 1 : -1;
     __syncthreads();
+    if (V == 5) {
+        // V4 + warp 0 runs an unrelated 4 KB+ unrolled code block between sub-blocks
+        // (as tail_diag's (b)/(c) phases do): does the pivot chain slow down?
+        long long acc = 0;
+        double junk = threadIdx.x;
+        for (int k0 = 0; k0 < TB; k0 += SB) {
+            const long long ta = clock64();
+            if ((threadIdx.x >> 5) == 0)
+                cipm::diag_sub<T, true>(S + k0 * TB, k0, SB, sSg, colbuf, g_ds, g_dd, &s_rm, sD, sInv, g_dvec, 0, 0, g_err, g_bumps, sLt);
+            __syncwarp();
+            acc += clock64() - ta;
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 400; ++u) junk = junk * 1.0000001 + (double)(u & 7) * S[(u * 7 + threadIdx.x) & 4095];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) cyc[0] = acc;            // the diagonal sub-blocks only
+        if (junk == 12345.678) dst[0] = junk;
+        for (int i = threadIdx.x; i < TB * TB; i += blockDim.x) dst[i] = S[i];
+        return;
+    }
     if (V == 4) {
         // tail_diag's context: warp 0 inside a divergent branch, the others at a barrier
         long long t0 = clock64();
@@ -164,7 +185,7 @@ template <typename T, int V>
 void run(const char* tag, const T* src, T* dst, long long* cyc) {
     long long best = 1LL << 60;
     for (int rep = 0; rep < 5; ++rep) {
-        bench<T, V><<<1, V == 4 ? 256 : 64>>>(src, dst, cyc);
+        bench<T, V><<<1, V >= 4 ? 256 : 64>>>(src, dst, cyc);
         long long h;
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         if (h < best) best = h;
@@ -193,6 +214,7 @@ void all(const char* tag) {
     run<T, 2>(tag, src, dst, cyc);
     run<T, 3>(tag, src, dst, cyc);
     run<T, 4>(tag, src, dst, cyc);
+    run<T, 5>(tag, src, dst, cyc);
 }
 
 int main() {
