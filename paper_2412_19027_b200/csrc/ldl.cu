@@ -27,6 +27,14 @@
 #include <type_traits>
 
 #include "common.cuh"
+
+// tiny-leaf kernels: threads per block and minimum resident blocks (launch bounds)
+#ifndef TINY_T
+#define TINY_T 128
+#endif
+#ifndef TINY_MINB
+#define TINY_MINB 1
+#endif
 #include "ctx.hpp"
 
 namespace cipm {
@@ -485,7 +493,7 @@ __device__ __forceinline__ void factor_warp_chain(int J, const FactorArgs& a, T*
 
 // tiny leaves: one thread each (launched before the warp tier)
 template <typename T>
-__global__ void __launch_bounds__(128) factor_tiny_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
+__global__ void __launch_bounds__(TINY_T, TINY_MINB) factor_tiny_kernel(FactorArgs a, T* __restrict__ lval, T* __restrict__ dvec,
                                                           T* __restrict__ inbox) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int parent = -1;
@@ -1414,7 +1422,7 @@ __global__ void __launch_bounds__(256) tiny_fold_kernel(SolveArgs a0, const int3
 
 // tiny leaves, forward: one thread each (launched before the persistent sweep)
 template <typename T>
-__global__ void __launch_bounds__(128) fwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
+__global__ void __launch_bounds__(TINY_T, TINY_MINB) fwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval, T* x, T* vin) {
     SolveArgs a = a0;
     resolve_act(a.rstate, a.act0, a.act1);
     if (!a.act0 && !a.act1) return;
@@ -1464,7 +1472,7 @@ __device__ __forceinline__ void bwd_tiny_w(const int4 td, int64_t rptr, const So
                                            const T* __restrict__ dvec, T* x);
 
 template <typename T>
-__global__ void __launch_bounds__(128) bwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval,
+__global__ void __launch_bounds__(TINY_T, TINY_MINB) bwd_tiny_kernel(SolveArgs a0, const T* __restrict__ lval,
                                                        const T* __restrict__ dvec, T* x) {
     SolveArgs a = a0;
     resolve_act(a.rstate, a.act0, a.act1);
@@ -1722,7 +1730,7 @@ int factor_t(Ctx& c) {
     if (ntiny > 0) {
         a.ntiny = ntiny;
         a.tiny = c.sym.tiny;
-        factor_tiny_kernel<T><<<grid_for(ntiny, 128), 128, 0, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
+        factor_tiny_kernel<T><<<grid_for(ntiny, TINY_T), TINY_T, 0, c.stream>>>(a, (T*)c.lval, (T*)c.dvec, (T*)c.inbox);
         c.launches++;
     }
     if (ns_warp > 0) {
@@ -1831,7 +1839,7 @@ void refine_solve_t(Ctx& c, int act0, int act1, bool gather) {
     f.trace = c.trace;
     const size_t ssm = sizeof(T) * (size_t)c.solve_slice * SW;
     if (f.ntiny > 0) {
-        fwd_tiny_kernel<T><<<grid_for(f.ntiny, 128), 128, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
+        fwd_tiny_kernel<T><<<grid_for(f.ntiny, TINY_T), TINY_T, 0, c.stream>>>(f, (const T*)c.lval, t, (T*)c.vin);
         c.launches++;
     }
     pt.mark("gather+fwd_tiny");
@@ -1860,7 +1868,7 @@ void refine_solve_t(Ctx& c, int act0, int act1, bool gather) {
         backward_kernel<T><<<c.solve_blocks, SW * 32, ssm, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
     pt.mark("backward");
     if (b.ntiny > 0) {
-        bwd_tiny_kernel<T><<<grid_for(b.ntiny, 128), 128, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
+        bwd_tiny_kernel<T><<<grid_for(b.ntiny, TINY_T), TINY_T, 0, c.stream>>>(b, (const T*)c.lval, (const T*)c.dvec, t);
         c.launches++;
     }
     if (c.profile) {
