@@ -467,10 +467,12 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     std::vector<int64_t> soc_h(c.nsoc), psd_m(c.npsd), psd_l(c.npsd), psd_h(c.npsd);
     int64_t hp = 0;
     c.soc_rows = 0;
+    int64_t soc_maxd = 0;
     for (int64_t i = 0; i < c.nsoc; ++i) {
         soc_h[i] = hp;
         hp += d->soc_dim[i] * (d->soc_dim[i] + 1) / 2;
         c.soc_rows += d->soc_dim[i];
+        soc_maxd = std::max<int64_t>(soc_maxd, d->soc_dim[i]);
     }
     c.nsym_hbase = hp;
     hp += 6 * c.nsym;
@@ -489,6 +491,9 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         c.psd_max_side = std::max<int>(c.psd_max_side, (int)sd);
         psd_deg += (double)sd;
     }
+    // lanes per SOC cone (entries 1..d-1 strided over the group): 8 up to 17 rows
+    c.soc_group = soc_maxd <= 17 ? 8 : (soc_maxd <= 33 ? 16 : 32);
+    if (getenv("CIPM_SOC_WARP")) c.soc_group = 32;
     c.hblk_total = hp;
     {
         bool uni = c.npsd > 0 && c.psd_max_side <= 8 && !getenv("CIPM_PSD_WARP");

@@ -125,49 +125,69 @@ struct SocArgs {
     const int64_t* hptr;
 };
 
+// lane group of G lanes per cone (G = 8 / 16 / 32 by the largest SOC dimension:
+// C3's dims 3-10 use 8, four cones per warp); every lane runs the group sums (no
+// early exit: groups of one warp stay in lockstep), stores are guarded
+template <int G>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+#define SOC_GROUP_SETUP                                                                  \
+    const int gl = threadIdx.x & (G - 1);                                               \
+    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;             \
+    if (((blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) / G) >= a.nsoc) return; \
+    const bool live = c < a.nsoc;                                                        \
+    const int off = live ? a.off[c] : 0, d = live ? a.dim[c] : 0;
+
+template <int G>
 __global__ void soc_scaling(SocArgs a, const double* s, const double* z, double* W, double* LAM, double* ETA,
                             double* hv, int* err) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
-    const int off = a.off[c], d = a.dim[c];
+    SOC_GROUP_SETUP
     const double* sv = s + off;
     const double* zv = z + off;
     double ss = 0.0, zz = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) { ss += sv[j] * sv[j]; zz += zv[j] * zv[j]; }
-    ss = warp_sum(ss);
-    zz = warp_sum(zz);
-    const double rs = sv[0] * sv[0] - ss, rz = zv[0] * zv[0] - zz;
-    if (rs <= 0.0 || rz <= 0.0 || sv[0] <= 0.0 || zv[0] <= 0.0 || !(rs == rs) || !(rz == rz)) {
-        if (lane == 0) set_error(err, CIPM_E_SCALING);
-        return;
-    }
-    const double aa = sqrt(rs), bb = sqrt(rz);
+    for (int j = 1 + gl; j < d; j += G) { ss += sv[j] * sv[j]; zz += zv[j] * zv[j]; }
+    ss = gsum<G>(ss);
+    zz = gsum<G>(zz);
+    const double s0 = live ? sv[0] : 1.0, z0 = live ? zv[0] : 1.0;
+    const double rs = s0 * s0 - ss, rz = z0 * z0 - zz;
+    const bool bad = live && (rs <= 0.0 || rz <= 0.0 || s0 <= 0.0 || z0 <= 0.0 || !(rs == rs) || !(rz == rz));
+    if (bad && gl == 0) set_error(err, CIPM_E_SCALING);
+    const bool ok = live && !bad;
+    const double aa = ok ? sqrt(rs) : 1.0, bb = ok ? sqrt(rz) : 1.0;
     double sbzb = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) sbzb += (sv[j] / aa) * (zv[j] / bb);
-    sbzb = warp_sum(sbzb) + (sv[0] / aa) * (zv[0] / bb);
+    if (ok)
+        for (int j = 1 + gl; j < d; j += G) sbzb += (sv[j] / aa) * (zv[j] / bb);
+    sbzb = gsum<G>(sbzb) + (s0 / aa) * (z0 / bb);
     const double gamma = sqrt((1.0 + sbzb) / 2.0);
     const double eta = sqrt(aa / bb);
     double* w = W + (off - a.base);
-    const double w0 = (sv[0] / aa + zv[0] / bb) / (2.0 * gamma);
-    for (int j = 1 + lane; j < d; j += 32) w[j] = (sv[j] / aa + (-(zv[j] / bb))) / (2.0 * gamma);
-    if (lane == 0) w[0] = w0;
+    const double w0 = (s0 / aa + z0 / bb) / (2.0 * gamma);
+    if (ok) {
+        for (int j = 1 + gl; j < d; j += G) w[j] = (sv[j] / aa + (-(zv[j] / bb))) / (2.0 * gamma);
+        if (gl == 0) w[0] = w0;
+    }
     __syncwarp();
     // λ = η W̄ z
     double cz = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) cz += w[j] * zv[j];
-    cz = warp_sum(cz);
+    if (ok)
+        for (int j = 1 + gl; j < d; j += G) cz += w[j] * zv[j];
+    cz = gsum<G>(cz);
+    if (!ok) return;                                   // no group sums below
     double* lam = LAM + (off - a.base);
-    for (int j = 1 + lane; j < d; j += 32) lam[j] = eta * ((zv[0] * w[j] + zv[j]) + (cz / (1.0 + w0)) * w[j]);
-    if (lane == 0) {
-        lam[0] = eta * (w0 * zv[0] + cz);
+    for (int j = 1 + gl; j < d; j += G) lam[j] = eta * ((z0 * w[j] + zv[j]) + (cz / (1.0 + w0)) * w[j]);
+    if (gl == 0) {
+        lam[0] = eta * (w0 * z0 + cz);
         ETA[c] = eta;
     }
     // dense block values η²(2ww' + I − 2e0e0'), upper triangle row-major
     const double e2 = eta * eta;
     double* hb = hv + a.hptr[c];
     const int tot = d * (d + 1) / 2;
-    for (int k = lane; k < tot; k += 32) {
+    for (int k = gl; k < tot; k += G) {
         // invert k -> (rl, cl) with rl <= cl
         int rl = 0, rem = k;
         while (rem >= d - rl) { rem -= d - rl; ++rl; }
@@ -181,19 +201,19 @@ __global__ void soc_scaling(SocArgs a, const double* s, const double* z, double*
 }
 
 // out = alpha*u + beta*H v on SOC rows
+template <int G>
 __global__ void soc_apply_h(SocArgs a, const double* W, const double* ETA, const double* v, double* out,
                             double alpha, const double* u, double beta, const double* skip) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc || (skip && *skip != 0.0)) return;
-    const int off = a.off[c], d = a.dim[c];
+    if (skip && *skip != 0.0) return;
+    SOC_GROUP_SETUP
     const double* w = W + (off - a.base);
     const double* vv = v + off;
     double dot = 0.0;
-    for (int j = lane; j < d; j += 32) dot += w[j] * vv[j];
-    dot = warp_sum(dot);
+    for (int j = gl; j < d; j += G) dot += w[j] * vv[j];
+    dot = gsum<G>(dot);
+    if (!live) return;
     const double e2 = ETA[c] * ETA[c];
-    for (int j = lane; j < d; j += 32) {
+    for (int j = gl; j < d; j += G) {
         const double jv = j == 0 ? vv[0] : -vv[j];
         const double hv = e2 * ((2.0 * w[j]) * dot - jv);
         const double base = u ? alpha * u[off + j] : 0.0;
@@ -201,58 +221,56 @@ __global__ void soc_apply_h(SocArgs a, const double* W, const double* ETA, const
     }
 }
 
+template <int G>
 __global__ void soc_combined_ds(SocArgs a, const double* W, const double* ETA, const double* LAM,
                                 const double* dz_a, const double* ds_a, const double* sc, double* out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
-    const int off = a.off[c], d = a.dim[c];
+    SOC_GROUP_SETUP
     const double* w = W + (off - a.base);
     const double* lam = LAM + (off - a.base);
     const double* dsv = ds_a + off;
     const double* dzv = dz_a + off;
-    const double eta = ETA[c];
-    const double w0 = w[0];
+    const double eta = live ? ETA[c] : 1.0;
+    const double w0 = live ? w[0] : 0.0;
+    const double ds0 = live ? dsv[0] : 0.0, dz0 = live ? dzv[0] : 0.0, lam0 = live ? lam[0] : 1.0;
     const double sigma = sc[CIPM_SC_SIGMA], mu = sc[CIPM_SC_MU];
     double c1 = 0.0, c2 = 0.0, ll = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) { c1 += w[j] * dsv[j]; c2 += w[j] * dzv[j]; ll += lam[j] * lam[j]; }
-    c1 = warp_sum(c1);
-    c2 = warp_sum(c2);
-    ll = warp_sum(ll);
+    for (int j = 1 + gl; j < d; j += G) { c1 += w[j] * dsv[j]; c2 += w[j] * dzv[j]; ll += lam[j] * lam[j]; }
+    c1 = gsum<G>(c1);
+    c2 = gsum<G>(c2);
+    ll = gsum<G>(ll);
     // A = W̄^-1 ds / η, B = η W̄ dz
-    const double A0 = (w0 * dsv[0] - c1) / eta;
-    const double B0 = eta * (w0 * dzv[0] + c2);
+    const double A0 = (w0 * ds0 - c1) / eta;
+    const double B0 = eta * (w0 * dz0 + c2);
     double ab = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) {
-        const double Aj = ((-dsv[0] * w[j] + dsv[j]) + (c1 / (1.0 + w0)) * w[j]) / eta;
-        const double Bj = eta * ((dzv[0] * w[j] + dzv[j]) + (c2 / (1.0 + w0)) * w[j]);
+    for (int j = 1 + gl; j < d; j += G) {
+        const double Aj = ((-ds0 * w[j] + dsv[j]) + (c1 / (1.0 + w0)) * w[j]) / eta;
+        const double Bj = eta * ((dz0 * w[j] + dzv[j]) + (c2 / (1.0 + w0)) * w[j]);
         ab += Aj * Bj;
     }
-    ab = warp_sum(ab);
+    ab = gsum<G>(ab);
     double* o = out + off;
     // rhs = λ∘λ + A∘B, rhs0 -= σμ  (stored in out as scratch)
-    const double lam0 = lam[0];
     const double r0 = ((lam0 * lam0 + ll) + (A0 * B0 + ab)) - sigma * mu;
-    for (int j = 1 + lane; j < d; j += 32) {
-        const double Aj = ((-dsv[0] * w[j] + dsv[j]) + (c1 / (1.0 + w0)) * w[j]) / eta;
-        const double Bj = eta * ((dzv[0] * w[j] + dzv[j]) + (c2 / (1.0 + w0)) * w[j]);
+    for (int j = 1 + gl; j < d; j += G) {
+        const double Aj = ((-ds0 * w[j] + dsv[j]) + (c1 / (1.0 + w0)) * w[j]) / eta;
+        const double Bj = eta * ((dz0 * w[j] + dzv[j]) + (c2 / (1.0 + w0)) * w[j]);
         o[j] = (lam0 * lam[j] + lam0 * lam[j]) + (A0 * Bj + B0 * Aj);
     }
     __syncwarp();
     // arrow solve λ ∘ u = rhs
     double lr = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) lr += lam[j] * o[j];
-    lr = warp_sum(lr);
+    for (int j = 1 + gl; j < d; j += G) lr += lam[j] * o[j];
+    lr = gsum<G>(lr);
     const double res = lam0 * lam0 - ll;
     const double u0 = (lam0 * r0 - lr) / res;
-    for (int j = 1 + lane; j < d; j += 32) o[j] = (o[j] - u0 * lam[j]) / lam0;
+    for (int j = 1 + gl; j < d; j += G) o[j] = (o[j] - u0 * lam[j]) / lam0;
     __syncwarp();
     // out = η W̄ u
     double cu = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) cu += w[j] * o[j];
-    cu = warp_sum(cu);
-    for (int j = 1 + lane; j < d; j += 32) o[j] = eta * ((u0 * w[j] + o[j]) + (cu / (1.0 + w0)) * w[j]);
-    if (lane == 0) o[0] = eta * (w0 * u0 + cu);
+    for (int j = 1 + gl; j < d; j += G) cu += w[j] * o[j];
+    cu = gsum<G>(cu);
+    for (int j = 1 + gl; j < d; j += G) o[j] = eta * ((u0 * w[j] + o[j]) + (cu / (1.0 + w0)) * w[j]);
+    if (live && gl == 0) o[0] = eta * (w0 * u0 + cu);
 }
 
 __device__ inline double soc_bound(double c, double b, double aa, double v0, double dv0) {
@@ -278,70 +296,72 @@ __device__ inline double soc_bound(double c, double b, double aa, double v0, dou
     return bound;
 }
 
+template <int G>
 __global__ void soc_step_bound(SocArgs a, const double* z, const double* s, const double* dz, const double* ds,
                                double* sc) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
-    const int off = a.off[c], d = a.dim[c];
+    SOC_GROUP_SETUP
     double res = INFINITY;
     for (int side = 0; side < 2; ++side) {
         const double* v = (side == 0 ? z : s) + off;
         const double* dv = (side == 0 ? dz : ds) + off;
         double vv = 0.0, vd = 0.0, dd = 0.0;
-        for (int j = 1 + lane; j < d; j += 32) { vv += v[j] * v[j]; vd += v[j] * dv[j]; dd += dv[j] * dv[j]; }
-        vv = warp_sum(vv);
-        vd = warp_sum(vd);
-        dd = warp_sum(dd);
-        const double cc = v[0] * v[0] - vv;
-        const double bb = 2.0 * (v[0] * dv[0] - vd);
-        const double aa = dv[0] * dv[0] - dd;
-        res = fmin(res, soc_bound(cc, bb, aa, v[0], dv[0]));
+        for (int j = 1 + gl; j < d; j += G) { vv += v[j] * v[j]; vd += v[j] * dv[j]; dd += dv[j] * dv[j]; }
+        vv = gsum<G>(vv);
+        vd = gsum<G>(vd);
+        dd = gsum<G>(dd);
+        if (live) {
+            const double cc = v[0] * v[0] - vv;
+            const double bb = 2.0 * (v[0] * dv[0] - vd);
+            const double aa = dv[0] * dv[0] - dd;
+            res = fmin(res, soc_bound(cc, bb, aa, v[0], dv[0]));
+        }
     }
-    if (lane == 0 && res < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, res);
+    // one atomic per warp (the minimum is order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) res = fmin(res, __shfl_xor_sync(0xffffffffu, res, o));
+    if ((threadIdx.x & 31) == 0 && res < INFINITY) atomic_min_pos(sc + CIPM_SC_ALPHA_WORK, res);
 }
 
 // neighbourhood per SOC: rs*rz/(s'z) >= β μ_k for each candidate of the batch
+template <int G>
 __global__ void soc_neighborhood(SocArgs a, const double* s, const double* z, const double* ds, const double* dz,
                                  const double* nb, int nk, double beta, unsigned int* mask, int* err) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
-    const int off = a.off[c], d = a.dim[c];
-    unsigned int bits = 0u;
+    SOC_GROUP_SETUP
+    unsigned int bits = live ? 0u : (1u << nk) - 1u;
     for (int k = 0; k < nk; ++k) {
         const double step = nb[16 + k];
         double ss = 0.0, zz = 0.0, sz = 0.0;
-        for (int j = 1 + lane; j < d; j += 32) {
+        for (int j = 1 + gl; j < d; j += G) {
             const double st = s[off + j] + step * ds[off + j];
             const double zt = z[off + j] + step * dz[off + j];
             ss += st * st; zz += zt * zt; sz += st * zt;
         }
-        ss = warp_sum(ss);
-        zz = warp_sum(zz);
-        sz = warp_sum(sz);
+        ss = gsum<G>(ss);
+        zz = gsum<G>(zz);
+        sz = gsum<G>(sz);
+        if (!live) continue;
         const double s0 = s[off] + step * ds[off], z0 = z[off] + step * dz[off];
         const double rs = s0 * s0 - ss, rz = z0 * z0 - zz;
         if (rs <= 0.0 || rz <= 0.0 || s0 <= 0.0 || z0 <= 0.0) {
-            if (lane == 0) set_error(err, CIPM_E_DOMAIN);
+            if (gl == 0) set_error(err, CIPM_E_DOMAIN);
             continue;
         }
         const double dot = s0 * z0 + sz;
         if (!(rs * rz / dot < beta * nb[k])) bits |= 1u << k;
     }
-    if (lane == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bits &= __shfl_xor_sync(0xffffffffu, bits, o);
+    if ((threadIdx.x & 31) == 0 && bits != (1u << nk) - 1u) atomicAnd(mask, bits | ~((1u << nk) - 1u));
 }
 
+template <int G>
 __global__ void soc_membership(SocArgs a, const double* s, const double* z, int* err) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= a.nsoc) return;
-    const int off = a.off[c], d = a.dim[c];
+    SOC_GROUP_SETUP
     double ss = 0.0, zz = 0.0;
-    for (int j = 1 + lane; j < d; j += 32) { ss += s[off + j] * s[off + j]; zz += z[off + j] * z[off + j]; }
-    ss = warp_sum(ss);
-    zz = warp_sum(zz);
-    if (lane == 0 && (!(s[off] > sqrt(ss)) || !(z[off] > sqrt(zz)))) set_error(err, CIPM_E_INTERIOR);
+    for (int j = 1 + gl; j < d; j += G) { ss += s[off + j] * s[off + j]; zz += z[off + j] * z[off + j]; }
+    ss = gsum<G>(ss);
+    zz = gsum<G>(zz);
+    if (live && gl == 0 && (!(s[off] > sqrt(ss)) || !(z[off] > sqrt(zz)))) set_error(err, CIPM_E_INTERIOR);
 }
 
 // bit-exact batched residual (steps.py:136-175): chunks of 8 left to right,
@@ -1185,6 +1205,17 @@ inline size_t psd_slice_bytes(const PsdArgs& a) {
 
 // ---------------------------------------------------------------------------
 
+// SOC launch: G lanes per cone (c.soc_group), 256-thread blocks
+#define SOC_LAUNCH(KERNEL, ...)                                                                       \
+    do {                                                                                              \
+        const int g_ = c.soc_group;                                                                   \
+        const int nb_ = (int)((c.nsoc * g_ + kThreads - 1) / kThreads);                               \
+        if (g_ == 8) KERNEL<8><<<nb_, kThreads, 0, c.stream>>>(__VA_ARGS__);                          \
+        else if (g_ == 16) KERNEL<16><<<nb_, kThreads, 0, c.stream>>>(__VA_ARGS__);                   \
+        else KERNEL<32><<<nb_, kThreads, 0, c.stream>>>(__VA_ARGS__);                                 \
+        c.launches++;                                                                                 \
+    } while (0)
+
 // PSD NT scaling: register kernel for equal sides <= 8 (CIPM_PSD_SCALING_WARP=1: the
 // lane-group kernel, experiments), lane-group kernel otherwise
 static void k_psd_scaling(Ctx& c) {
@@ -1203,9 +1234,8 @@ void k_update_scaling_family(Ctx& c, int fam) {
         c.launches++;
     }
     if (fam == 1 && c.nsoc) {
-        soc_scaling<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.s, c.z, c.soc_w, c.soc_lam,
+        SOC_LAUNCH(soc_scaling, soc_args(c), c.s, c.z, c.soc_w, c.soc_lam,
                                                                   c.soc_eta, c.hv, c.err);
-        c.launches++;
     }
     if (fam == 2 && c.nsym) {
         nsym_scaling<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.sc, c.ns_h, c.ns_grad,
@@ -1222,9 +1252,8 @@ void k_update_scaling(Ctx& c) {
         c.launches++;
     }
     if (c.nsoc) {
-        soc_scaling<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.s, c.z, c.soc_w, c.soc_lam,
+        SOC_LAUNCH(soc_scaling, soc_args(c), c.s, c.z, c.soc_w, c.soc_lam,
                                                                   c.soc_eta, c.hv, c.err);
-        c.launches++;
     }
     if (c.nsym) {
         nsym_scaling<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.sc, c.ns_h, c.ns_grad,
@@ -1269,9 +1298,8 @@ void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double*
         c.launches++;
     }
     if (c.nsoc) {
-        soc_apply_h<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.soc_w, c.soc_eta, v, out, alpha, u,
+        SOC_LAUNCH(soc_apply_h, soc_args(c), c.soc_w, c.soc_eta, v, out, alpha, u,
                                                                   beta, skip);
-        c.launches++;
     }
     if (c.nsym) {
         nsym_apply_h<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.ns_h, v, out, alpha, u, beta, skip);
@@ -1288,9 +1316,8 @@ void k_combined_ds(Ctx& c, const double* dz_a, const double* ds_a) {
         c.launches++;
     }
     if (c.nsoc) {
-        soc_combined_ds<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.soc_w, c.soc_eta, c.soc_lam,
+        SOC_LAUNCH(soc_combined_ds, soc_args(c), c.soc_w, c.soc_eta, c.soc_lam,
                                                                       dz_a, ds_a, c.sc, c.dsc);
-        c.launches++;
     }
     if (c.nsym) {
         nsym_combined_ds<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, dz_a, ds_a, c.ns_grad,
@@ -1307,8 +1334,7 @@ void k_step_bound(Ctx& c, const double* dz, const double* ds) {
         c.launches++;
     }
     if (c.nsoc) {
-        soc_step_bound<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.z, c.s, dz, ds, c.sc);
-        c.launches++;
+        SOC_LAUNCH(soc_step_bound, soc_args(c), c.z, c.s, dz, ds, c.sc);
     }
     if (c.npsd && !PSD_REG_DISPATCH_T(psd_step_bound_r, 2, 32, c.npsd, c.psd_off, c.z, c.s, dz, ds, c.sc, c.err))
         PSD_DISPATCH(psd_step_bound_w, pa_, c.z, c.s, dz, ds, c.sc, c.err);
@@ -1325,9 +1351,8 @@ void k_nsym_feasible_mask(Ctx& c, const double* dz, const double* ds, int k0) {
 void k_neighborhood_mask(Ctx& c, int k0, int nk) {
     (void)k0;
     if (c.nsoc) {
-        soc_neighborhood<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.s, c.z, c.ds[1], c.dz[1], c.nb,
+        SOC_LAUNCH(soc_neighborhood, soc_args(c), c.s, c.z, c.ds[1], c.dz[1], c.nb,
                                                                        nk, c.beta, c.mask, c.err);
-        c.launches++;
     }
     if (c.nsym) {
         nsym_neighborhood<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.ds[1], c.dz[1],
@@ -1344,8 +1369,7 @@ void k_membership(Ctx& c) {
         c.launches++;
     }
     if (c.nsoc) {
-        soc_membership<<<warp_grid(c.nsoc), kThreads, 0, c.stream>>>(soc_args(c), c.s, c.z, c.err);
-        c.launches++;
+        SOC_LAUNCH(soc_membership, soc_args(c), c.s, c.z, c.err);
     }
     if (c.nsym) {
         nsym_membership<<<grid_for(c.nsym, 128), 128, 0, c.stream>>>(nsym_args(c), c.s, c.z, c.err);

@@ -95,7 +95,8 @@ struct Ctx {
     int64_t nsoc = 0, nexp = 0, npow = 0, npsd = 0, soc_rows = 0, nsym = 0;
     int64_t psd_mat_total = 0, psd_lam_total = 0, hblk_total = 0;
     int psd_max_side = 0;
-    int psd_uni = 0;                 // all PSD sides equal and <= 8: thread-per-cone kernels (psd_reg.cuh)
+    int psd_uni = 0;
+    int soc_group = 32;              // lanes per SOC cone: 8 / 16 / 32 by the largest SOC dimension                 // all PSD sides equal and <= 8: thread-per-cone kernels (psd_reg.cuh)
     double nu = 0.0;                 // barrier degree
     double c_obj = 1.0;
     int64_t p_nnz = 0, a_nnz = 0;
