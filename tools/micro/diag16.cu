@@ -122,7 +122,12 @@ template <> __device__ float* dv<float>() { return g_dvec_f; }
 template <typename T, int V>
 __global__ void bench(const T* src, T* dst, long long* cyc) {
     T* g_dvec = dv<T>();
+#ifdef DYN_S
+    extern __shared__ __align__(16) unsigned char dyn_raw[];
+    T* S = reinterpret_cast<T*>(dyn_raw);
+#else
     __shared__ T S[TB * TB];
+#endif
     __shared__ T sD[TB], sInv[SB], colbuf[64];
     __shared__ int8_t sSg[TB];
     __shared__ T sLt[SB * SB];
@@ -185,7 +190,12 @@ template <typename T, int V>
 void run(const char* tag, const T* src, T* dst, long long* cyc) {
     long long best = 1LL << 60;
     for (int rep = 0; rep < 5; ++rep) {
+        #ifdef DYN_S
+        cudaFuncSetAttribute(bench<T, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(T) * TB * TB));
+        bench<T, V><<<1, V >= 4 ? 256 : 64, sizeof(T) * TB * TB>>>(src, dst, cyc);
+#else
         bench<T, V><<<1, V >= 4 ? 256 : 64>>>(src, dst, cyc);
+#endif
         long long h;
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
         if (h < best) best = h;
