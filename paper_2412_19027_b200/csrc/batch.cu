@@ -335,8 +335,8 @@ __device__ void bfactor_cta(const BatchPattern& pt, Inst& I, double ds, double d
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
             double acc = 0.0;
-#pragma unroll
             if (i < nbk)
+#pragma unroll
                 for (int k = 0; k < i; ++k) acc += R[(k0 + k) * W + k0 + i] * v[k];
             v[i] = (i < nbk && lane < nbk) ? (i == lane ? 1.0 : (i < lane ? 0.0 : -acc)) : 0.0;
         }
@@ -460,7 +460,6 @@ __global__ void __launch_bounds__(BT) batch_ipm(BatchPattern pt, BatchData bd, i
     extern __shared__ __align__(16) double bsm[];
     __shared__ double sred[NW * 16];
     __shared__ Ctl C;
-    __shared__ double sv[8];
     __shared__ double sblk[RB * RB + RB];   // root: L11 of the current block + 1/d (factor), block vector (solve)
     const int inst = blockIdx.x;
     if (inst >= count) return;

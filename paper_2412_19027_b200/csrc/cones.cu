@@ -26,12 +26,6 @@ namespace cipm {
 
 namespace {
 
-constexpr int kNbBatch = 8;   // neighbourhood candidates per batch
-
-__device__ __forceinline__ double warp_sum(double v) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 // ============================== nonneg =====================================
 
@@ -1179,8 +1173,6 @@ PsdArgs psd_args(Ctx& c) {
     a.gw = c.psd_max_side <= 8 ? 8 : (c.psd_max_side <= 16 ? 16 : 32);
     return a;
 }
-
-inline int warp_grid(int64_t nwarps) { return grid_for(nwarps * 32); }
 
 // group-per-cone PSD launch: slices per warp = 32 / gw; warps per CTA from the slice
 // size (<= 96 KiB per CTA)

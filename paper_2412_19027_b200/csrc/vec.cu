@@ -150,13 +150,6 @@ __global__ void resid_m(ResidM a, double* sc, double* partials, unsigned int* co
     }
 }
 
-// ------------------------------ copies -------------------------------------
-
-__global__ void copy2(const double* a, double* b, int64_t n) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) b[i] = a[i];
-}
-
 // ----------------------------- rhs build -----------------------------------
 
 // rb0 = [-q; b] (col2), rb1 = [gx; -(gz - s)] (affine)
