@@ -354,9 +354,17 @@ def run_batch(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the sharded path on a one-GPU box: every rank on cuda:0,
+    # gloo for the (timing-only) collectives — NCCL refuses two ranks per device
+    one_dev = os.environ.get("CIPM_BENCH_ONE_DEVICE", "0") != "0"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec, desc = workload(args.config)
     total = G.CONFIGS[args.config]["instances"]
     lo, hi = shard(total, world, rank)

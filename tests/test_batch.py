@@ -196,3 +196,34 @@ def test_gpu_batch_c5b_all_2048_match_reference(gpu):
             bad.append((k, r.status, r.iterations, r.obj_primal, doc["status"][k], doc["iterations"][k]))
     assert not bad, bad[:10]
     assert sum(r.iterations for r in out) == pytest.approx(sum(doc["iterations"]), abs=len(out) // 100)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 8])
+def test_gpu_batch_shards_equal_the_whole_batch(gpu, world):
+    """The multi-GPU bench shards the instances contiguously (bench.shard) with no
+    collective on the solve path: every shard solved on its own returns, bit for
+    bit, what the whole batch returns for those instances (one CTA per instance,
+    nothing shared between instances)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2412_19027_b200.batch import BatchSolver
+    total = 256
+    cfg = SolverSettings(eps_feas=1e-8)
+    probs = G.build_instances("c5b_mpc", 0, total)
+    bs = BatchSolver(probs, cfg)
+    whole = bs.solve()
+    bs.close()
+    for rank in range(world):
+        lo, hi = bench.shard(total, world, rank)
+        part = BatchSolver(G.build_instances("c5b_mpc", lo, hi), cfg)
+        got = part.solve()
+        part.close()
+        for k, r in enumerate(got):
+            w = whole[lo + k]
+            assert r.status == w.status and r.iterations == w.iterations
+            np.testing.assert_array_equal(r.x, w.x)
+            np.testing.assert_array_equal(r.z, w.z)
+            assert r.obj_primal == w.obj_primal
