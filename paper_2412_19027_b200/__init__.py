@@ -18,6 +18,13 @@ from .model import (ConeSpec, Equilibration, ProblemData, equilibrate, exp_cone,
                     psd_cone, reorder_cones, scale_values, soc_cone, unscale_solution, validate, zero_cone)
 from .settings import (FULL, MIXED, RefinementSettings, SolveResult, SolverSettings, Status, TERMINAL_OK,
                        centering)
+from .families import (GenSpec, InfeasibleBoxBudget, gen_entropy, gen_huber, gen_multistage_portfolio,
+                       gen_portfolio)
+from .io import read_problem, write_problem
+from .metrics import perf_profiles, shifted_geomean
+# the reference's cone-level functions, computed by the device cone kernels (cones.py)
+from .cones import (ConeSet, ScalingState, StepLengthRequest, apply_H, combined_ds, degree, is_in_cone,
+                    is_in_dual_cone, neighborhood_ok, soc_residuals_batch, step_length, update_scaling)
 
 __version__ = "0.1.0"
 
