@@ -170,6 +170,17 @@ int cipm_set_iterate(cipm_ctx *ctx, const double *x, const double *z, const doub
 /* --- operator-level seams (tests / observers) --- */
 /* refined KKT solve of K x = rhs with the current factor (system.py:279-314) */
 int cipm_kkt_solve(cipm_ctx *ctx, const double *rhs, double *x, int *steps, double *residual);
+/* KKTSystem seam (kkt/system.py:64-314; a device-backed drop-in for the class):
+ * set_scaling(diag, blocks) — H from the host: diag over the zero + nonneg rows, blocks
+ * packed upper triangles in the order of cipm_scaling_values; the factorisation and the
+ * refinement residual then use these values (replaces system.py:166-184).
+ * matvec — the unregularised K x (system.py:273-277).
+ * solve_ex — cipm_kkt_solve plus RefineResult.stalled (system.py:279-314).
+ * set_refinement — RefinementSettings t_abs, t_rel, t_max (system.py:45-54). */
+int cipm_kkt_set_scaling(cipm_ctx *ctx, const double *diag, const double *blocks);
+int cipm_kkt_matvec(cipm_ctx *ctx, const double *x, double *out);
+int cipm_kkt_solve_ex(cipm_ctx *ctx, const double *rhs, double *x, int *steps, double *residual, int *stalled);
+int cipm_set_refinement(cipm_ctx *ctx, double t_abs, double t_rel, int t_max);
 /* H v with the current scaling (scaling.py:254-274) */
 int cipm_apply_h(cipm_ctx *ctx, const double *v, double *out);
 /* dense -H block values as scattered into the factor (for tests): returns the

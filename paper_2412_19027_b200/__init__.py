@@ -34,6 +34,9 @@ def __getattr__(name):
     if name in ("Solver", "solve", "IterateState", "Residuals"):
         from . import solver as _s
         return getattr(_s, name)
+    if name in ("KKTSystem", "assemble", "RefineResult"):
+        from . import kkt as _k
+        return getattr(_k, name)
     if name == "BatchSolver":
         from . import batch as _b
         return _b.BatchSolver

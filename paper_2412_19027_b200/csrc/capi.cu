@@ -496,6 +496,24 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     if (getenv("CIPM_SOC_WARP")) c.soc_group = 32;
     c.hblk_total = hp;
     {
+        // dense H blocks in hv (SOC, exp, pow, PSD): row offset, size, packed upper start
+        std::vector<int32_t> bo, bdim;
+        std::vector<int64_t> bh;
+        for (int64_t i = 0; i < c.nsoc; ++i) { bo.push_back((int32_t)d->soc_off[i]); bdim.push_back((int32_t)d->soc_dim[i]); bh.push_back(soc_h[i]); }
+        for (int64_t i = 0; i < d->n_exp; ++i) { bo.push_back((int32_t)d->exp_off[i]); bdim.push_back(3); bh.push_back(c.nsym_hbase + 6 * i); }
+        for (int64_t i = 0; i < d->n_pow; ++i) { bo.push_back((int32_t)d->pow_off[i]); bdim.push_back(3); bh.push_back(c.nsym_hbase + 6 * (d->n_exp + i)); }
+        for (int64_t i = 0; i < c.npsd; ++i) {
+            const int64_t sd = d->psd_side[i];
+            bo.push_back((int32_t)d->psd_off[i]); bdim.push_back((int32_t)(sd * (sd + 1) / 2)); bh.push_back(psd_h[i]);
+        }
+        c.nblk = (int64_t)bo.size();
+        if (c.nblk) {
+            TRY(upload(c, &c.blk_off, bo.data(), c.nblk));
+            TRY(upload(c, &c.blk_dim, bdim.data(), c.nblk));
+            TRY(upload(c, &c.blk_hptr, bh.data(), c.nblk));
+        }
+    }
+    {
         bool uni = c.npsd > 0 && c.psd_max_side <= 8 && !getenv("CIPM_PSD_WARP");
         for (int64_t i = 0; i < c.npsd && uni; ++i) uni = d->psd_side[i] == c.psd_max_side;
         c.psd_uni = uni ? c.psd_max_side : 0;
@@ -1181,6 +1199,61 @@ int cipm_kkt_solve(cipm_ctx* h, const double* rhs, double* x, int* steps, double
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
     CIPM_CUDA(copy_sync(c, x, c.rbest, sizeof(double) * c.dim, cudaMemcpyDeviceToHost));
     if (residual) *residual = c.h_rstate[7];
+    return CIPM_OK;
+}
+
+// KKTSystem seam (kkt/system.py:152-314): H from the host, K x, refined solves
+// with the stall flag, refinement settings
+int cipm_kkt_set_scaling(cipm_ctx* h, const double* diag, const double* blocks) {
+    if (!h) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    if (c.nonneg_dim && diag)
+        CIPM_CUDA(cudaMemcpyAsync(c.nn_h, diag + c.zero_dim, sizeof(double) * c.nonneg_dim, cudaMemcpyHostToDevice,
+                                  c.stream));
+    if (c.hblk_total && blocks)
+        CIPM_CUDA(cudaMemcpyAsync(c.hv, blocks, sizeof(double) * c.hblk_total, cudaMemcpyHostToDevice, c.stream));
+    c.h2d_bytes += (int64_t)sizeof(double) * (c.nonneg_dim + c.hblk_total);
+    c.host_scaling = true;
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    return CIPM_OK;
+}
+
+int cipm_kkt_matvec(cipm_ctx* h, const double* x, double* out) {
+    if (!h || !x || !out) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    CIPM_CUDA(cudaMemcpyAsync(c.rx, x, sizeof(double) * c.dim, cudaMemcpyHostToDevice, c.stream));
+    CIPM_CUDA(cudaMemsetAsync(c.rb, 0, sizeof(double) * c.dim, c.stream));
+    CIPM_CUDA(cudaMemsetAsync(c.rstate, 0, sizeof(double) * 8, c.stream));   // rhs 0 active
+    k_kkt_matvec_only(c, 0);                                                 // rr = 0 - K x
+    std::vector<double> r(c.dim);
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    CIPM_CUDA(copy_sync(c, r.data(), c.rr, sizeof(double) * c.dim, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < c.dim; ++i) out[i] = -r[i];
+    return CIPM_OK;
+}
+
+int cipm_kkt_solve_ex(cipm_ctx* h, const double* rhs, double* x, int* steps, double* residual, int* stalled) {
+    int e = cipm_kkt_solve(h, rhs, x, steps, residual);
+    if (e) return e;
+    if (stalled) *stalled = h->c.h_rstate[4] == 2.0 ? 1 : 0;
+    return CIPM_OK;
+}
+
+int cipm_set_refinement(cipm_ctx* h, double t_abs, double t_rel, int t_max) {
+    if (!h || !(t_abs > 0.0) || !(t_rel > 0.0) || t_max < 1) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    c.refine_abs = t_abs;
+    c.refine_rel = t_rel;
+    if (t_max != c.refine_max) {
+        c.refine_max = t_max;
+        for (auto& g : c.refine_graph)          // the step bound is captured in the graphs
+            if (g) {
+                cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
+    }
     return CIPM_OK;
 }
 

@@ -1197,6 +1197,32 @@ inline size_t psd_slice_bytes(const PsdArgs& a) {
 
 // ---------------------------------------------------------------------------
 
+// KKTSystem seam: H v from the dense blocks in hv (packed upper triangle per block,
+// the layout cipm_scaling_values returns), one thread per conic row past the
+// zero / nonneg span (binary search of the row's block)
+__global__ void blk_apply_h(const int32_t* __restrict__ boff, const int32_t* __restrict__ bdim,
+                            const int64_t* __restrict__ bh, int64_t nblk, const double* __restrict__ hv,
+                            const double* v, double* out, double alpha, const double* u, double beta, int64_t lin,
+                            int64_t m, const double* skip) {
+    const int64_t r = lin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= m || (skip && *skip != 0.0)) return;
+    int64_t lo = 0, hi = nblk - 1;
+    while (lo < hi) {                                  // last block with offset <= r
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (boff[mid] <= r) lo = mid;
+        else hi = mid - 1;
+    }
+    const int off = boff[lo], d = bdim[lo], i = (int)(r - off);
+    const double* H = hv + bh[lo];
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) {
+        const int a = i < j ? i : j, b = i < j ? j : i;          // upper entry (a, b), a <= b
+        acc += H[a * d - a * (a - 1) / 2 + (b - a)] * v[off + j];
+    }
+    const double base = u ? alpha * u[r] : 0.0;
+    out[r] = base + beta * acc;
+}
+
 // SOC launch: G lanes per cone (c.soc_group), 256-thread blocks
 #define SOC_LAUNCH(KERNEL, ...)                                                                       \
     do {                                                                                              \
@@ -1284,6 +1310,20 @@ void k_scatter_h(Ctx& c) {
 
 void k_apply_h(Ctx& c, const double* v, double* out, double alpha, const double* u, double beta,
                const double* skip) {
+    if (c.host_scaling) {                 // H set by the host (cipm_kkt_set_scaling): the stored blocks
+        if (c.lin) {
+            nn_apply_h<<<grid_for(c.lin), kThreads, 0, c.stream>>>(c.nn_h, v, out, alpha, u, beta, c.zero_dim, c.lin,
+                                                                   skip);
+            c.launches++;
+        }
+        if (c.nblk) {
+            blk_apply_h<<<grid_for(c.m - c.lin), kThreads, 0, c.stream>>>(c.blk_off, c.blk_dim, c.blk_hptr, c.nblk,
+                                                                          c.hv, v, out, alpha, u, beta, c.lin, c.m,
+                                                                          skip);
+            c.launches++;
+        }
+        return;
+    }
     if (c.lin) {
         nn_apply_h<<<grid_for(c.lin), kThreads, 0, c.stream>>>(c.nn_h, v, out, alpha, u, beta, c.zero_dim, c.lin,
                                                                skip);

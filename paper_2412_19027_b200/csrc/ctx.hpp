@@ -96,6 +96,11 @@ struct Ctx {
     int64_t psd_mat_total = 0, psd_lam_total = 0, hblk_total = 0;
     int psd_max_side = 0;
     int psd_uni = 0;
+    // KKTSystem seam: H given by the host (cipm_kkt_set_scaling); the block tables of hv
+    int32_t *blk_off = nullptr, *blk_dim = nullptr;
+    int64_t* blk_hptr = nullptr;
+    int64_t nblk = 0;
+    bool host_scaling = false;
     int soc_group = 32;              // lanes per SOC cone: 8 / 16 / 32 by the largest SOC dimension                 // all PSD sides equal and <= 8: thread-per-cone kernels (psd_reg.cuh)
     double nu = 0.0;                 // barrier degree
     double c_obj = 1.0;

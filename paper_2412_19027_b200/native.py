@@ -94,6 +94,11 @@ _SIGS = {
     "cipm_scaling_values": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
     "cipm_get_direction": ([c_void_p, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_get_vector": ([c_void_p, ctypes.c_char_p, P_DBL, P_I64], ctypes.c_int),
+    "cipm_kkt_set_scaling": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_kkt_matvec": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_kkt_solve_ex": ([c_void_p, P_DBL, P_DBL, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
+                           ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "cipm_set_refinement": ([c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_int], ctypes.c_int),
     "cipm_soc_residuals": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),
     "cipm_set_direction": ([c_void_p, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_step_length": ([c_void_p, ctypes.c_int, P_DBL], ctypes.c_int),
