@@ -37,7 +37,7 @@ def __getattr__(name):
     if name in ("KKTSystem", "assemble", "RefineResult"):
         from . import kkt as _k
         return getattr(_k, name)
-    if name == "BatchSolver":
+    if name in ("BatchSolver", "solve_many"):
         from . import batch as _b
-        return _b.BatchSolver
+        return getattr(_b, name)
     raise AttributeError(name)

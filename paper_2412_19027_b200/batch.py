@@ -259,3 +259,43 @@ def _user_rows(v, perm):
     out = np.empty_like(v)
     out[perm] = v
     return out
+
+
+def _pattern_key(p: ProblemData):
+    """Instances with equal keys share one sparsity pattern and cone list."""
+    return (p.n, p.m, p.P.rowptr.tobytes(), p.P.colidx.tobytes(), p.A.rowptr.tobytes(), p.A.colidx.tobytes(),
+            tuple((c.kind, c.dim, c.alpha, c.side) for c in p.cones))
+
+
+def solve_many(problems, settings: SolverSettings | None = None, device: int = 0):
+    """Solve a heterogeneous list of problems on one GPU: instances are grouped by
+    sparsity pattern and cone list; each group of zero / nonneg (LP / QP) instances
+    in full precision runs as one ``BatchSolver`` launch (a CTA per instance), every
+    other instance (SOC / exp / pow / PSD cones, mixed precision, singletons) through
+    the single-problem device path.  Returns the ``SolveResult`` list in input
+    order — what ``Solver(p).solve()`` returns for each instance."""
+    from .solver import Solver
+    st = settings or SolverSettings()
+    groups: dict = {}
+    for k, p in enumerate(problems):
+        groups.setdefault(_pattern_key(p), []).append(k)
+    out = [None] * len(problems)
+    for idx in groups.values():
+        first = problems[idx[0]]
+        batchable = (len(idx) > 1 and st.precision == FULL
+                     and all(c.kind in (ZERO, NONNEG) for c in first.cones))
+        if batchable:
+            bs = BatchSolver([problems[k] for k in idx], st, device=device)
+            try:
+                for k, r in zip(idx, bs.solve()):
+                    out[k] = r
+            finally:
+                bs.close()
+            continue
+        for k in idx:
+            s = Solver(problems[k], st)
+            try:
+                out[k] = s.solve()
+            finally:
+                s.close()
+    return out

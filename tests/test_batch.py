@@ -227,3 +227,25 @@ def test_gpu_batch_shards_equal_the_whole_batch(gpu, world):
             np.testing.assert_array_equal(r.x, w.x)
             np.testing.assert_array_equal(r.z, w.z)
             assert r.obj_primal == w.obj_primal
+
+
+@pytest.mark.gpu
+def test_gpu_solve_many_heterogeneous_equals_per_instance(gpu):
+    """solve_many groups instances by pattern: the MPC QPs and the LP family run
+    batched, the SOCP / exp-pow / PSD instances through the single-problem path;
+    every result equals the per-instance Solver result (status, iterations,
+    objectives to 1e-9)."""
+    from paper_2412_19027_b200.batch import solve_many
+    from paper_2412_19027_b200.solver import Solver
+    probs = (G.build_instances("c5b_mpc", 0, 6) + [G.gen_socp(ncones=20, seed=s) for s in range(2)] + [G.gen_lp(n=20, m=40, seed=3)]
+             + G.build_instances("c5b_mpc", 6, 9) + [G.gen_psd(ncones=3, side=3, seed=1)])
+    cfg = SolverSettings(eps_feas=1e-8)
+    got = solve_many(probs, cfg)
+    assert len(got) == len(probs)
+    for p, r in zip(probs, got):
+        s = Solver(p, cfg)
+        w = s.solve()
+        s.close()
+        assert r.status == w.status
+        assert abs(r.iterations - w.iterations) <= 1
+        assert abs(r.obj_primal - w.obj_primal) <= 1e-9 * max(1.0, abs(w.obj_primal))
