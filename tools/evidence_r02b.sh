@@ -2,7 +2,7 @@
 # round-2 final evidence pass: GPU tests, bench lines for every config (reference CPU
 # baselines on the host cores), C5b, the reference arm for C2, the C2 launch list,
 # the ncu sweep-traffic capture, the batched kernel's ncu, racecheck
-O=gpurun_out/ev3; mkdir -p $O gpurun_out/ncu
+O=gpurun_out/ev4; mkdir -p $O gpurun_out/ncu
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > $O/gputests.log 2>&1; echo "tests rc=$?"; tail -1 $O/gputests.log
 timeout 900 python bench.py > $O/bench_c2_lasso.json 2> $O/bench_c2_lasso.err; echo "c2 rc=$?"
 timeout 900 python bench.py --config c5b_mpc --steps 3 --warmup 3 > $O/bench_c5b_mpc.json 2> $O/bench_c5b_mpc.err; echo "c5b rc=$?"
