@@ -166,6 +166,11 @@ int cipm_read_scalars(cipm_ctx *ctx, double *out);
 /* which: 0 = current iterate, 1 = best iterate.  x (n), z (m), s (m), tkm[3] = τ, κ, μ */
 int cipm_get_iterate(cipm_ctx *ctx, int which, double *x, double *z, double *s, double *tkm);
 int cipm_set_iterate(cipm_ctx *ctx, const double *x, const double *z, const double *s, const double *tkm);
+/* solution recovery on the device (ipm.py:383-407, replaces the host unscale + row scatter):
+ * x = Dc x' (/ τ), z = Dr z' / c (/ τ), s = s' / Dr (/ τ) in the user's row order; no
+ * division by τ when certificate != 0.  which: 0 = current, 1 = best iterate; tkm[3] = τ, κ, μ
+ * of that iterate (may be NULL). */
+int cipm_get_solution(cipm_ctx *ctx, int which, int certificate, double *x, double *z, double *s, double *tkm);
 
 /* --- operator-level seams (tests / observers) --- */
 /* refined KKT solve of K x = rhs with the current factor (system.py:279-314) */

@@ -1174,6 +1174,31 @@ int cipm_get_iterate(cipm_ctx* h, int which, double* x, double* z, double* s, do
     return CIPM_OK;
 }
 
+int cipm_get_solution(cipm_ctx* h, int which, int certificate, double* x, double* z, double* s, double* tkm) {
+    CIPM_NVTX("cipm_get_solution");
+    if (!h || (h && h->c.n && !x) || (h->c.m && (!z || !s))) return CIPM_E_ARG;
+    Ctx& c = h->c;
+    CIPM_CUDA(cudaSetDevice(c.device));
+    double* out = c.rb;                          // refinement scratch, 2 (n + m) >= n + 2 m doubles
+    k_recover_solution(c, which, certificate, out);
+    CIPM_CUDA(cudaGetLastError());
+    if (c.n) CIPM_CUDA(cudaMemcpyAsync(x, out, sizeof(double) * c.n, cudaMemcpyDeviceToHost, c.stream));
+    if (c.m) {
+        CIPM_CUDA(cudaMemcpyAsync(z, out + c.n, sizeof(double) * c.m, cudaMemcpyDeviceToHost, c.stream));
+        CIPM_CUDA(cudaMemcpyAsync(s, out + c.n + c.m, sizeof(double) * c.m, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (tkm) CIPM_CUDA(cudaMemcpyAsync(c.h_sc, c.sc, sizeof(double) * CIPM_SC_COUNT, cudaMemcpyDeviceToHost, c.stream));
+    CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    c.d2h_bytes += (int64_t)sizeof(double) * (c.n + 2 * c.m + (tkm ? CIPM_SC_COUNT : 0));
+    if (tkm) {
+        const bool best = which != 0;
+        tkm[0] = c.h_sc[best ? CIPM_SC_BEST_TAU : CIPM_SC_TAU];
+        tkm[1] = c.h_sc[best ? CIPM_SC_BEST_KAPPA : CIPM_SC_KAPPA];
+        tkm[2] = c.h_sc[best ? CIPM_SC_BEST_MU : CIPM_SC_MU];
+    }
+    return CIPM_OK;
+}
+
 int cipm_set_iterate(cipm_ctx* h, const double* x, const double* z, const double* s, const double* tkm) {
     Ctx& c = h->c;
     CIPM_CUDA(cudaStreamSynchronize(c.stream));

@@ -250,6 +250,7 @@ void k_affine_rhs(Ctx& c);                   // rb[1] = [gx; -(gz - s)], rb[0] =
 void k_combined_rhs(Ctx& c);                 // rb[0] = [f gx; -(f gz - dsc)]
 void k_recover_direction(Ctx& c, int which, const double* sol, double dkappa_rhs_slot_is_combined);
 void k_take_step(Ctx& c);
+void k_recover_solution(Ctx& c, int which, int cert, double* out);   // ipm.py:383-407 into out[n + 2m]
 void k_step_init(Ctx& c, int which);         // α bound from τ/κ
 void k_step_finish(Ctx& c, int which);       // α check + σ
 void k_kkt_residual(Ctx& c, int nrhs, const int* active_host);

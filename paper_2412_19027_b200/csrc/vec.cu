@@ -8,6 +8,7 @@
 // A-class passes in the reference.  All reductions are two-level with a fixed
 // grid (bitwise reproducible).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -932,6 +933,41 @@ void k_refine_init_one(Ctx& c, int q) {
     cudaMemcpyAsync(c.rr + (int64_t)q * c.dim, bv, sizeof(double) * c.dim, cudaMemcpyDeviceToDevice, c.stream);
     refine_init<<<red_grid(c.dim), kThreads, 0, c.stream>>>(bv, c.dim, c.rstate + 8 * q, c.refine_abs, c.refine_rel,
                                                             c.partials, c.counter);
+    c.launches++;
+}
+
+// solution recovery (reference ipm.py:383-407): unscale x = Dc x', z = Dr z' / c,
+// s = s' / Dr, divide by τ unless the result is a certificate, and scatter the
+// rows back to the user's cone order (row perm[k] <- reordered row k).  Same
+// operation order as the host's unscale_solution (no additions: no contraction).
+__global__ void recover_solution(const double* __restrict__ x, const double* __restrict__ z,
+                                 const double* __restrict__ s, const double* __restrict__ dc,
+                                 const double* __restrict__ dr, const int64_t* __restrict__ perm,
+                                 const double* __restrict__ sc, int tau_slot, int cert, double c_obj, int64_t n,
+                                 int64_t m, double* __restrict__ out) {
+    const double tau = sc[tau_slot];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n + m; k += (int64_t)gridDim.x * blockDim.x) {
+        if (k < n) {
+            const double v = dc[k] * x[k];
+            out[k] = cert ? v : v / tau;
+        } else {
+            const int64_t r = k - n, u = perm ? perm[r] : r;
+            const double zu = dr[r] * z[r] / c_obj, su = s[r] / dr[r];
+            out[n + u] = cert ? zu : zu / tau;
+            out[n + m + u] = cert ? su : su / tau;
+        }
+    }
+}
+
+void k_recover_solution(Ctx& c, int which, int cert, double* out) {
+    const int64_t tot = c.n + c.m;
+    if (tot == 0) return;
+    const int tb = 256;
+    const int grid = (int)std::min<int64_t>((tot + tb - 1) / tb, 148 * 8);
+    recover_solution<<<grid, tb, 0, c.stream>>>(which ? c.bx : c.x, which ? c.bz : c.z, which ? c.bs : c.s, c.dc,
+                                                c.dr, c.have_reorder ? c.b_src : nullptr, c.sc,
+                                                which ? CIPM_SC_BEST_TAU : CIPM_SC_TAU, cert, c.c_obj, c.n, c.m,
+                                                out);
     c.launches++;
 }
 

@@ -88,6 +88,7 @@ _SIGS = {
     "cipm_take_step": ([c_void_p], ctypes.c_int),
     "cipm_read_scalars": ([c_void_p, P_DBL], ctypes.c_int),
     "cipm_get_iterate": ([c_void_p, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
+    "cipm_get_solution": ([c_void_p, ctypes.c_int, ctypes.c_int, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_set_iterate": ([c_void_p, P_DBL, P_DBL, P_DBL, P_DBL], ctypes.c_int),
     "cipm_kkt_solve": ([c_void_p, P_DBL, P_DBL, ctypes.POINTER(ctypes.c_int), P_DBL], ctypes.c_int),
     "cipm_apply_h": ([c_void_p, P_DBL, P_DBL], ctypes.c_int),

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .exceptions import ConicError, DeviceError, PatternMismatch
-from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, unscale_solution, validate,
+from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, validate,
                     validate_values)
 from .native import P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, require_device
 from .settings import (ALMOST_OPTIMAL_FACTOR, FULL, MIXED, STALL_IMPROVEMENT, STALL_WINDOW, SolveResult,
@@ -316,27 +316,23 @@ class Solver:
     # -- recovery -------------------------------------------------------------
 
     def _recover(self, which, res: Residuals, status, iterations, secs, tkm=None) -> SolveResult:
-        st = self._state(which)
-        if tkm is not None:
-            st.tau, st.kappa, st.mu = tkm
-        if self._equil.d_row is None:
-            d_row, d_col, c_obj = np.empty(self.m), np.empty(self.n), ctypes.c_double(1.0)
-            self._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
-            self._equil = Equilibration(d_row, d_col, float(c_obj.value))
-        x_u, z_u, s_u = unscale_solution(st.x, st.z, st.s, self._equil)
+        """Result assembly (reference ipm.py:383-407).  Unscaling, the division by τ and
+        the scatter back to the user's row order run on the device (cipm_get_solution);
+        only x, z and s cross PCIe."""
+        cert_mode = status in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE)
+        x_o, z_o, s_o = np.empty(self.n), np.empty(self.m), np.empty(self.m)
+        t = np.zeros(3)
+        self._ctx.call("cipm_get_solution", which, 1 if cert_mode else 0, pdbl(x_o), pdbl(z_o), pdbl(s_o), pdbl(t))
+        tau, kappa, mu = (float(v) for v in (tkm if tkm is not None else t))
         cert = None
-        if status not in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE):
-            x_o, z_o, s_o = x_u / st.tau, self._to_user_rows(z_u / st.tau), self._to_user_rows(s_u / st.tau)
-        else:
-            x_o, z_o, s_o = x_u, self._to_user_rows(z_u), self._to_user_rows(s_u)
-            if status == Status.PRIMAL_INFEASIBLE:
-                cert = z_o / abs(float(self._original.b @ z_o))
-            else:
-                cert = x_o / abs(float(self._original.q @ x_o))
+        if status == Status.PRIMAL_INFEASIBLE:
+            cert = z_o / abs(float(self._original.b @ z_o))
+        elif status == Status.DUAL_INFEASIBLE:
+            cert = x_o / abs(float(self._original.q @ x_o))
         return SolveResult(status=status, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=res.g_p,
                            obj_dual=res.g_d, iterations=iterations, setup_seconds=self.setup_seconds,
                            solve_seconds=secs, norm_rp=res.norm_rp, norm_rd=res.norm_rd, gap=res.gap,
-                           tau=st.tau, kappa=st.kappa, mu_initial=self._mu_initial, mu_final=st.mu)
+                           tau=tau, kappa=kappa, mu_initial=self._mu_initial, mu_final=mu)
 
     # -- main loop ------------------------------------------------------------
 

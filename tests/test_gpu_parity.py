@@ -201,3 +201,32 @@ def test_gpu_device_loop_equals_host_loop(gpu, name, monkeypatch):
     np.testing.assert_array_equal([r_dev.obj_primal, r_dev.obj_dual], [r_host.obj_primal, r_host.obj_dual])
     np.testing.assert_array_equal(r_dev.x, r_host.x)       # NaN-aware: the insufficient-progress exits
     np.testing.assert_array_equal(r_dev.z, r_host.z)
+
+
+@pytest.mark.parametrize("name", ["lp_150x300", "socp_40", "psd_6x4", "primal_infeasible_lp", "dual_infeasible_lp"])
+def test_gpu_device_recovery_matches_host_unscale(name, gpu):
+    """cipm_get_solution (unscale, / τ, row scatter on the device) equals the host's
+    unscale_solution + _to_user_rows of the same iterate bit for bit (ipm.py:383-407)."""
+    import ctypes
+    from paper_2412_19027_b200.model import Equilibration, unscale_solution
+    from paper_2412_19027_b200.native import pdbl
+    from paper_2412_19027_b200.solver import Solver
+    doc = load_instance(name)
+    s = Solver(problem_from_doc(doc), settings_of(doc))
+    res = s.solve()
+    which = 0 if res.status in ("optimal", "primal_infeasible", "dual_infeasible") else 1   # best iterate
+    st = s._state(which)
+    tau = st.tau if which == 0 else res.tau
+    d_row, d_col, c_obj = np.empty(s.m), np.empty(s.n), ctypes.c_double(1.0)
+    s._ctx.call("cipm_ctx_get_equilibration", pdbl(d_row), pdbl(d_col), ctypes.byref(c_obj))
+    x_u, z_u, s_u = unscale_solution(st.x, st.z, st.s, Equilibration(d_row, d_col, float(c_obj.value)))
+    s.close()
+    if res.status in ("primal_infeasible", "dual_infeasible"):
+        x_o, z_o, s_o = x_u, s._to_user_rows(z_u), s._to_user_rows(s_u)
+    else:
+        x_o, z_o, s_o = x_u / tau, s._to_user_rows(z_u / tau), s._to_user_rows(s_u / tau)
+    np.testing.assert_array_equal(res.x, x_o)
+    np.testing.assert_array_equal(res.z, z_o)
+    np.testing.assert_array_equal(res.s, s_o)
+    if which == 0:
+        assert res.tau == st.tau and res.kappa == st.kappa and res.mu_final == st.mu
