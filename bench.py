@@ -413,7 +413,7 @@ def run_batch(args):
         bs.update_data(q=q_host, b=b_host)
         out = bs.solve()
         e2e.append(time.perf_counter() - t1)
-        e2e_it += sum(r.iterations for r in out)
+        e2e_it += int(out.iterations.sum())
     lib().cipm_batch_io_bytes(bs.handle, ctypes.byref(h2d), ctypes.byref(d2h), 1)
     e2e_s = sum(e2e)
     vals = torch.tensor([dev_s, e2e_s, float(iters), float(e2e_it), float(len(probs))], dtype=torch.float64,

@@ -19,12 +19,13 @@ from __future__ import annotations
 
 import ctypes
 import time
+from collections.abc import Sequence
 
 import numpy as np
 
 from .exceptions import ConicError, NonFiniteData, PatternMismatch, raise_for_status
 from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, reorder_cones, validate
-from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, pi64, require_device
+from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, pi64, pinned_copy, pinned_empty, require_device
 from .settings import FULL, SolveResult, SolverSettings, Status, default_dynamic_reg, default_static_reg
 
 RUIZ_ITERS = 10
@@ -74,6 +75,66 @@ def equilibrate_batch(P, A, pv, av, q, b, iters=RUIZ_ITERS):
     return pv, av, qc, bc, d_row, d_col, c_obj
 
 
+class BatchResults(Sequence):
+    """The per-instance results of one batched solve: a sequence of reference
+    ``SolveResult`` objects backed by the host arrays of one device-to-host copy.
+    Each ``SolveResult`` is built when it is first accessed; whole-batch columns
+    (``status``, ``iterations``, ``obj_primal``, ``obj_dual``, ``x``, ``z``, ``s``)
+    are available as arrays without building them."""
+
+    def __init__(self, status_codes, res, x, z, s, q, b, setup_seconds, solve_seconds):
+        self._codes, self._res, self.x, self.z, self.s = status_codes, res, x, z, s
+        self._q, self._b = q, b
+        self._setup, self._secs = setup_seconds, solve_seconds
+        self._cache: dict = {}
+
+    def __len__(self) -> int:
+        return len(self._codes)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        r = self._cache.get(k)
+        if r is None:
+            r = self._cache[k] = self._build(k)
+        return r
+
+    @property
+    def status(self) -> list:
+        return [_STATUS[v] for v in self._codes.tolist()]
+
+    @property
+    def iterations(self) -> np.ndarray:
+        return self._res[:, 8].astype(np.int64)
+
+    @property
+    def obj_primal(self) -> np.ndarray:
+        return self._res[:, 0]
+
+    @property
+    def obj_dual(self) -> np.ndarray:
+        return self._res[:, 1]
+
+    def _build(self, k: int) -> SolveResult:
+        st = _STATUS[int(self._codes[k])]
+        g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = self._res[k].tolist()
+        # the device returned unscaled, user-row-order iterates (divided by tau unless a certificate)
+        x_o, z_o, s_o = self.x[k], self.z[k], self.s[k]
+        cert = None
+        if st == Status.PRIMAL_INFEASIBLE:
+            cert = z_o / abs(float(self._b[k] @ z_o))
+        elif st == Status.DUAL_INFEASIBLE:
+            cert = x_o / abs(float(self._q[k] @ x_o))
+        return SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=g_p, obj_dual=g_d,
+                           iterations=int(iters), setup_seconds=self._setup, solve_seconds=self._secs,
+                           norm_rp=rp, norm_rd=rd, gap=abs(g_p - g_d), tau=tau, kappa=kappa, mu_initial=mu0,
+                           mu_final=mu)
+
+
 class BatchSolver:
     """Many same-pattern instances, one device launch (one CTA per instance)."""
 
@@ -97,6 +158,9 @@ class BatchSolver:
             raise ConicError("batched instances support zero + nonnegative cones only")
         self.problems = [p.copy() for p in problems]
         self.count = len(problems)
+        # current q / b of every instance (user row order); update_data replaces them
+        self._q_cur = np.stack([p.q for p in self.problems])
+        self._b_cur = np.stack([p.b for p in self.problems])
         ref0, self._perm = reorder_cones(first)
         self._pattern = ref0
         self.layout = Layout(ref0.cones)
@@ -117,6 +181,9 @@ class BatchSolver:
         raise_for_status(rc, "batch creation")
         self.handle = h
         self._upload()
+        c, n, m = self.count, self.n, self.m             # warm torch's pinned host cache (see Solver)
+        _warm = [pinned_empty(sh) for _ in range(3) for sh in ((c, n), (c, m), (c, n), (c, m), (c, m))]
+        del _warm
         self.setup_seconds = time.perf_counter() - t0
         self.last_kernel_ms = 0.0
 
@@ -130,8 +197,7 @@ class BatchSolver:
             self._reorder_set = True
         V = np.concatenate([np.stack([p.P.values for p in self.problems]),
                             np.stack([p.A.values for p in self.problems])], axis=1)
-        self._host = [np.ascontiguousarray(a) for a in
-                      (V, np.stack([p.q for p in self.problems]), np.stack([p.b for p in self.problems]))]
+        self._host = [np.ascontiguousarray(a) for a in (V, self._q_cur, self._b_cur)]
         rc = lib().cipm_batch_set_raw_values(self.handle, *[pdbl(a) for a in self._host],
                                              1 if self.settings.do_equilibrate else 0)
         raise_for_status(rc, "batch upload")
@@ -144,8 +210,8 @@ class BatchSolver:
         a_src = _take_rows_src(self.problems[0].A, perm)
         pv = np.stack([p.P.values for p in self.problems])
         av = np.stack([p.A.values[a_src] for p in self.problems])
-        q = np.stack([p.q for p in self.problems])
-        b = np.stack([p.b[perm] for p in self.problems])
+        q = self._q_cur
+        b = self._b_cur[:, perm]
         norm_q = np.max(np.abs(q), axis=1) if self.n else np.zeros(self.count)
         norm_b = np.max(np.abs(b), axis=1) if self.m else np.zeros(self.count)
         pv_s, av_s, q_s, b_s, d_row, d_col, c_obj = equilibrate_batch(P, A, pv, av, q, b)
@@ -158,8 +224,8 @@ class BatchSolver:
     def update_data(self, q=None, b=None):
         """Parametric re-solve of every instance (same patterns): q, b as (count, n) / (count, m).
         Only the given arrays are sent; the device keeps the raw P / A values."""
-        qs = np.array(q, dtype=np.float64, order="C") if q is not None else None
-        bs = np.array(b, dtype=np.float64, order="C") if b is not None else None
+        qs = np.asarray(q, dtype=np.float64) if q is not None else None
+        bs = np.asarray(b, dtype=np.float64) if b is not None else None
         if qs is not None and qs.shape != (self.count, self.n):
             raise ValueError(f"q must be ({self.count}, {self.n})")
         if bs is not None and bs.shape != (self.count, self.m):
@@ -169,15 +235,11 @@ class BatchSolver:
             raise NonFiniteData("q")
         if bs is not None and not np.all(np.isfinite(bs)):
             raise NonFiniteData("b")
-        for k, p in enumerate(self.problems):          # per-instance views (certificates, results)
-            if qs is not None:
-                p.q = qs[k]
-            if bs is not None:
-                p.b = bs[k]
+        # own page-locked copies: the H2D is one DMA, and they back the results' certificates
         if qs is not None:
-            self._host[1] = qs
+            self._q_cur = pinned_copy(qs)
         if bs is not None:
-            self._host[2] = bs
+            self._b_cur = pinned_copy(bs)
         if not getattr(self, "_raw_on_device", True):
             self._upload()                  # after a host-equilibrated upload: re-send the raw arrays
             return
@@ -203,30 +265,11 @@ class BatchSolver:
         c, n, m = self.count, self.n, self.m
         status = np.zeros(c, dtype=np.int32)
         res = np.zeros((c, 9))
-        x, z, s = np.zeros((c, n)), np.zeros((c, m)), np.zeros((c, m))
+        x, z, s = pinned_empty((c, n)), pinned_empty((c, m)), pinned_empty((c, m))   # D2H by DMA
         raise_for_status(lib().cipm_batch_results(self.handle, status.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                                   pdbl(res), pdbl(x), pdbl(z), pdbl(s)), "batch results")
         secs = self.last_kernel_ms / 1e3 if secs is None else secs
-        out = []
-        # plain Python scalars in one conversion each (2048 instances: the per-element
-        # numpy scalar conversions were most of the host time of a batched solve)
-        sts = [_STATUS[v] for v in status.tolist()]
-        rows = res.tolist()
-        for k in range(c):
-            st = sts[k]
-            g_p, g_d, rp, rd, tau, kappa, mu, mu0, iters = rows[k]
-            # the device returned unscaled, user-row-order iterates (divided by tau unless a certificate)
-            x_o, z_o, s_o = x[k], z[k], s[k]
-            cert = None
-            if st == Status.PRIMAL_INFEASIBLE:
-                cert = z_o / abs(float(self.problems[k].b @ z_o))
-            elif st == Status.DUAL_INFEASIBLE:
-                cert = x_o / abs(float(self.problems[k].q @ x_o))
-            out.append(SolveResult(status=st, x=x_o, z=z_o, s=s_o, certificate=cert, obj_primal=g_p,
-                                   obj_dual=g_d, iterations=int(iters), setup_seconds=self.setup_seconds,
-                                   solve_seconds=secs, norm_rp=rp, norm_rd=rd, gap=abs(g_p - g_d), tau=tau,
-                                   kappa=kappa, mu_initial=mu0, mu_final=mu))
-        return out
+        return BatchResults(status, res, x, z, s, self._q_cur, self._b_cur, self.setup_seconds, secs)
 
     def solve(self):
         t0 = time.perf_counter()

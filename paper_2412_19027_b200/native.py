@@ -325,3 +325,19 @@ def require_device():
     if not torch.cuda.is_available():
         raise ConicError("no CUDA device: the B200 solver path has no CPU fallback")
     return torch
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """Page-locked float64 host array from torch's caching host allocator.  Device
+    copies into / out of it are plain DMA (no driver staging through pageable
+    memory), and results are handed to the caller in it without another host copy.
+    The ndarray keeps its tensor (and so the pinned block) alive."""
+    torch = require_device()
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
+def pinned_copy(a) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    out = pinned_empty(a.shape)
+    np.copyto(out, a)
+    return out

@@ -23,7 +23,8 @@ import numpy as np
 from .exceptions import ConicError, DeviceError, PatternMismatch
 from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, validate,
                     validate_values)
-from .native import P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, require_device
+from .native import (P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, pinned_copy,
+                     pinned_empty, require_device)
 from .settings import (ALMOST_OPTIMAL_FACTOR, FULL, MIXED, STALL_IMPROVEMENT, STALL_WINDOW, SolveResult,
                        SolverSettings, Status, default_dynamic_reg, default_static_reg)
 
@@ -174,6 +175,11 @@ class Solver:
         self._a_src = np.ascontiguousarray(csr_row_gather_src(problem.A, perm), dtype=np.int64)
         self._ctx.call("cipm_ctx_set_reorder", pi64(self._row_perm) or P_I64(), pi64(self._a_src) or P_I64())
         self._upload_values()
+        # page-locked blocks for the parametric updates (q, b) and the results (x, z, s)
+        # in torch's host cache (three generations alive at once: the current data and
+        # results, the next ones, slack), so no solve pays for pinning them
+        _warm = [pinned_empty(k) for _ in range(3) for k in (self.n, self.m, self.n, self.m, self.m)]
+        del _warm
         self.setup_seconds = time.perf_counter() - t0
         self._sc = np.zeros(64)
         self.last_refine_steps = []
@@ -215,8 +221,8 @@ class Solver:
         if b is not None and len(b) != prob.m:
             raise PatternMismatch("b length changed")
         new = ProblemData(P.copy() if P is not None else prob.P, A.copy() if A is not None else prob.A,
-                          np.asarray(q, dtype=np.float64).copy() if q is not None else prob.q,
-                          np.asarray(b, dtype=np.float64).copy() if b is not None else prob.b, prob.cones)
+                          pinned_copy(q) if q is not None else prob.q,
+                          pinned_copy(b) if b is not None else prob.b, prob.cones)
         validate_values(new, P is not None, A is not None, q is not None, b is not None)
         self._original = new
         self._upload_values((P is not None, A is not None, q is not None, b is not None))
@@ -320,7 +326,7 @@ class Solver:
         the scatter back to the user's row order run on the device (cipm_get_solution);
         only x, z and s cross PCIe."""
         cert_mode = status in (Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE)
-        x_o, z_o, s_o = np.empty(self.n), np.empty(self.m), np.empty(self.m)
+        x_o, z_o, s_o = pinned_empty(self.n), pinned_empty(self.m), pinned_empty(self.m)
         t = np.zeros(3)
         self._ctx.call("cipm_get_solution", which, 1 if cert_mode else 0, pdbl(x_o), pdbl(z_o), pdbl(s_o), pdbl(t))
         tau, kappa, mu = (float(v) for v in (tkm if tkm is not None else t))

@@ -25,7 +25,7 @@ def main():
     s = Solver(prob, SolverSettings(eps_feas=1e-8, precision=G.CONFIGS[cfg]["precision"]))
     s.solve()
     q, b = np.ascontiguousarray(prob.q), np.ascontiguousarray(prob.b)
-    for _ in range(2):
+    for _ in range(6):
         t0 = time.perf_counter()
         s.update_data(q=q, b=b)
         t1 = time.perf_counter()
