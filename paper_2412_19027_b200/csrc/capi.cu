@@ -568,8 +568,9 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     TRY(dalloc(c, &c.b_src, c.m));
     TRY(dalloc(c, &c.eq_cnorm, c.n));
     TRY(dalloc(c, &c.eq_rnorm, c.m));
-    TRY(dalloc(c, &c.eq_cstep, c.n));
-    TRY(dalloc(c, &c.eq_rstep, c.m));
+    TRY(dalloc(c, &c.eq_cstep, 10 * c.n));      // per Ruiz pass (replayed on q / b-only updates)
+    TRY(dalloc(c, &c.eq_rstep, 10 * c.m));
+    TRY(dalloc(c, &c.eq_p_ruiz, c.p_nnz));
     TRY(dalloc(c, &c.eq_cobj, 1));
     {
         std::vector<int64_t> bo, bd;
@@ -792,6 +793,7 @@ int cipm_ctx_set_values(cipm_ctx* h, const double* pv, const double* av, const d
     CIPM_NVTX("cipm_ctx_set_values");
     if (!h) return CIPM_E_ARG;
     Ctx& c = h->c;
+    c.eq_valid = false;                          // host-scaled values: no recorded Ruiz passes
     CIPM_CUDA(cudaSetDevice(c.device));
     if (c.p_nnz) CIPM_CUDA(cudaMemcpyAsync(c.p_v, pv, sizeof(double) * c.p_nnz, cudaMemcpyHostToDevice, c.stream));
     if (c.a_nnz) {
@@ -852,11 +854,14 @@ int cipm_ctx_set_problem(cipm_ctx* h, const double* p_values, const double* a_va
         c.h2d_bytes += (int64_t)sizeof(double) * c.m;
     }
     c.have_user_values = true;
-    if (c.p_nnz)
+    // q / b-only update of an equilibrated problem: replay the recorded Ruiz passes
+    const bool replay = equilibrate && c.eq_valid && !p_values && !a_values && !getenv("CIPM_NO_RUIZ_REPLAY");
+    if (c.p_nnz && !replay)
         CIPM_CUDA(cudaMemcpyAsync(c.p_v, c.p_user, sizeof(double) * c.p_nnz, cudaMemcpyDeviceToDevice, c.stream));
     if (c.n) CIPM_CUDA(cudaMemcpyAsync(c.q, c.q_user, sizeof(double) * c.n, cudaMemcpyDeviceToDevice, c.stream));
-    int rc = k_set_problem(c, equilibrate != 0);
+    int rc = k_set_problem(c, equilibrate != 0, replay);
     if (rc) return rc;
+    c.eq_valid = equilibrate != 0;
     CIPM_CUDA(cudaMemcpyAsync(&c.c_obj, c.eq_cobj, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
     CIPM_CUDA(cudaGetLastError());

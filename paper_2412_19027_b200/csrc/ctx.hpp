@@ -131,6 +131,8 @@ struct Ctx {
     int64_t *a_src = nullptr, *b_src = nullptr;
     bool have_reorder = false;
     double *eq_cnorm = nullptr, *eq_rnorm = nullptr, *eq_cstep = nullptr, *eq_rstep = nullptr, *eq_cobj = nullptr;
+    double* eq_p_ruiz = nullptr;   // Ruiz-scaled P before the cost scaling (q / b-only replay)
+    bool eq_valid = false;         // eq_cstep / eq_rstep (10 passes) and eq_p_ruiz match the device P, A
     int32_t *eq_boff = nullptr, *eq_bdim = nullptr;
     int64_t eq_nblocks = 0;
     double one = 1.0;
@@ -282,7 +284,7 @@ int k_factor(Ctx& c);
 void k_refine_step(Ctx& c, int nrhs, const int* active_host, bool gather = true);
 bool fused_resid_ok(const Ctx& c);
 // setup.cu
-int k_set_problem(Ctx& c, bool equilibrate);
+int k_set_problem(Ctx& c, bool equilibrate, bool replay);
 // dense.cu
 void tail_setup(Ctx& c, int64_t* inv_total, int64_t* flag_total);
 void k_tail_factor(Ctx& c);

@@ -16,6 +16,7 @@ namespace cipm {
 namespace {
 
 constexpr double kScaleMin = 1e-4, kScaleMax = 1e4;   // problem.py:36-40
+constexpr int kRuizIters = 10;                        // RUIZ_ITERS, problem.py:36
 
 __global__ void gather_reorder(const double* __restrict__ a_user, const int64_t* __restrict__ a_src,
                                double* __restrict__ a_v, int64_t nnz, const double* __restrict__ b_user,
@@ -119,6 +120,23 @@ __global__ void cost_scale(double* pv, int64_t nnzp, double* q, int64_t n, const
     if (i < n) q[i] = q[i] * c;
 }
 
+// q / b through the recorded Ruiz passes: the same per-pass products q_i *= c_i^(k),
+// b_r *= r_r^(k) in the same order as ruiz_scale, so bitwise the full run's q, b
+__global__ void ruiz_replay(int64_t n, int64_t m, double* q, double* b, const double* __restrict__ csteps,
+                            const double* __restrict__ rsteps, int iters) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        double v = q[i];
+        for (int k = 0; k < iters; ++k) v *= csteps[(int64_t)k * n + i];
+        q[i] = v;
+    } else if (i < n + m) {
+        const int64_t r = i - n;
+        double v = b[r];
+        for (int k = 0; k < iters; ++k) v *= rsteps[(int64_t)k * m + r];
+        b[r] = v;
+    }
+}
+
 __global__ void transpose_vals(const double* __restrict__ av, const int64_t* __restrict__ at_src,
                                double* __restrict__ at_v, int64_t nnz) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -128,25 +146,45 @@ __global__ void transpose_vals(const double* __restrict__ av, const int64_t* __r
 }  // namespace
 
 // raw user-order values -> reordered, equilibrated device problem (+ factor base image)
-int k_set_problem(Ctx& c, bool equilibrate) {
+int k_set_problem(Ctx& c, bool equilibrate, bool replay) {
     const int64_t n = c.n, m = c.m, nb = std::max<int64_t>(c.a_nnz, m);
+    if (replay) {
+        // q / b changed, P / A raw values did not: D_r, D_c, the Ruiz-scaled P, A and A'
+        // are the previous run's (the passes depend on P and A only, problem.py:232-260);
+        // replay the recorded per-pass steps on the fresh q / b, then the cost scaling
+        gather_reorder<<<grid_for(std::max<int64_t>(m, 1)), kThreads, 0, c.stream>>>(c.a_user, c.a_src, c.a_v, 0,
+                                                                                     c.b_user, c.b_src, c.b, m);
+        ruiz_replay<<<grid_for(n + m), kThreads, 0, c.stream>>>(n, m, c.q, c.b, c.eq_cstep, c.eq_rstep, kRuizIters);
+        if (c.p_nnz)
+            cudaMemcpyAsync(c.p_v, c.eq_p_ruiz, sizeof(double) * c.p_nnz, cudaMemcpyDeviceToDevice, c.stream);
+        qmax_kernel<<<red_grid(n), kThreads, 0, c.stream>>>(c.q, n, c.eq_cobj, c.partials, c.counter);
+        cost_scale<<<grid_for(std::max(c.p_nnz, n)), kThreads, 0, c.stream>>>(c.p_v, c.p_nnz, c.q, n, c.eq_cobj);
+        c.launches += 4;
+        k_build_base(c);
+        return CIPM_OK;
+    }
     gather_reorder<<<grid_for(nb), kThreads, 0, c.stream>>>(c.a_user, c.a_src, c.a_v, c.a_nnz, c.b_user, c.b_src,
                                                             c.b, m);
     set_ones<<<grid_for(std::max(n, m)), kThreads, 0, c.stream>>>(c.dc, n, c.dr, m);
     c.launches += 2;
     if (equilibrate) {
-        for (int it = 0; it < 10; ++it) {   // RUIZ_ITERS, problem.py:36
+        for (int it = 0; it < kRuizIters; ++it) {   // RUIZ_ITERS, problem.py:36
+            // per-pass steps kept (eq_cstep[it], eq_rstep[it]) for the q / b-only replay
+            double* cst = c.eq_cstep + (int64_t)it * n;
+            double* rst = c.eq_rstep + (int64_t)it * m;
             ruiz_norms<<<grid_for(n + m), kThreads, 0, c.stream>>>(n, m, c.p_rp, c.p_v, c.at_rp, c.at_src, c.a_rp,
                                                                    c.a_v, c.eq_cnorm, c.eq_rnorm);
             if (c.eq_nblocks)
                 ruiz_blocks<<<grid_for(c.eq_nblocks), kThreads, 0, c.stream>>>(c.eq_rnorm, c.eq_boff, c.eq_bdim,
                                                                                c.eq_nblocks);
-            ruiz_steps<<<grid_for(n + m), kThreads, 0, c.stream>>>(n, m, c.eq_cnorm, c.eq_rnorm, c.dc, c.dr,
-                                                                   c.eq_cstep, c.eq_rstep);
+            ruiz_steps<<<grid_for(n + m), kThreads, 0, c.stream>>>(n, m, c.eq_cnorm, c.eq_rnorm, c.dc, c.dr, cst,
+                                                                   rst);
             ruiz_scale<<<grid_for(n + m), kThreads, 0, c.stream>>>(n, m, c.p_rp, c.p_ci, c.p_v, c.a_rp, c.a_ci,
-                                                                   c.a_v, c.q, c.b, c.eq_cstep, c.eq_rstep);
+                                                                   c.a_v, c.q, c.b, cst, rst);
             c.launches += c.eq_nblocks ? 4 : 3;
         }
+        if (c.p_nnz)
+            cudaMemcpyAsync(c.eq_p_ruiz, c.p_v, sizeof(double) * c.p_nnz, cudaMemcpyDeviceToDevice, c.stream);
         qmax_kernel<<<red_grid(n), kThreads, 0, c.stream>>>(c.q, n, c.eq_cobj, c.partials, c.counter);
         cost_scale<<<grid_for(std::max(c.p_nnz, n)), kThreads, 0, c.stream>>>(c.p_v, c.p_nnz, c.q, n, c.eq_cobj);
         c.launches += 2;

@@ -165,6 +165,8 @@ def test_gpu_partial_updates_match_fresh_solver(gpu):
         dict(A=CsrMatrix(cur.A.nrows, cur.A.ncols, cur.A.rowptr, cur.A.colidx,
                          cur.A.values * (1.0 + 0.05 * rng.standard_normal(cur.A.nnz)))),
         dict(P=CsrMatrix(cur.P.nrows, cur.P.ncols, cur.P.rowptr, cur.P.colidx, cur.P.values * 1.5)),
+        # q / b only after a P / A change: the device replays the new Ruiz passes
+        dict(q=cur.q * (1.0 + 0.1 * rng.standard_normal(cur.n)), b=cur.b * (1.0 + 0.1 * rng.standard_normal(cur.m))),
     ]
     for upd in steps:
         s.update_data(**upd)
