@@ -708,9 +708,6 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
         CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(S.nnz_storage, 1)));
         c.allocations.push_back(p);
         c.lval = p;
-        CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(S.nnz_storage, 1)));
-        c.allocations.push_back(p);
-        c.lbase = p;
         CIPM_CUDA(cudaMalloc(&p, es * std::max<int64_t>(c.dim, 1)));
         c.allocations.push_back(p);
         c.dvec = p;

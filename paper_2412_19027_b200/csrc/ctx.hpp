@@ -159,7 +159,6 @@ struct Ctx {
     Symbolic host_sym;               // copy kept for stats / host-side checks
     DevSymbolic sym;
     void* lval = nullptr;            // panels (T)
-    void* lbase = nullptr;           // base image: P, A, static regularisation (T)
     void* dvec = nullptr;            // D (T), permuted order
     int32_t* fac_count = nullptr;    // children finished (factor / forward solve)
     int32_t* bwd_done = nullptr;     // backward solve completion flags

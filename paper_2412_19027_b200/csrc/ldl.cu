@@ -1683,9 +1683,12 @@ SolveArgs solve_args(Ctx& c, int32_t* count, int32_t* ticket, int act0, int act1
     return a;
 }
 
+// the factor storage's base image (zeros, P and A values, the static +-delta on the
+// diagonal), written straight into the factor storage at every assembly: a
+// write-only memset plus three small scatters instead of a read + write copy of a
+// kept image (the graph's memcpy node ran at ~2 TB/s: C3 170 us per factorisation)
 template <typename T>
-void build_base_t(Ctx& c) {
-    T* base = (T*)c.lbase;
+void build_base_t(Ctx& c, T* base) {
     cudaMemsetAsync(base, 0, sizeof(T) * c.sym.nnz_storage, c.stream);
     if (c.p_nnz) {
         scatter_vals<T><<<grid_for(c.p_nnz), kThreads, 0, c.stream>>>(base, c.sym.map_p, c.p_v, c.p_nnz);
@@ -1884,14 +1887,14 @@ void refine_solve_t(Ctx& c, int act0, int act1, bool gather) {
 
 }  // namespace
 
-void k_build_base(Ctx& c) {
-    if (c.precision == CIPM_FULL) build_base_t<double>(c);
-    else build_base_t<float>(c);
+void k_build_base(Ctx&) {
+    // nothing to precompute: k_assemble rebuilds the base image from the current P / A
+    // values (p_v, a_v) in place at every factorisation
 }
 
 void k_assemble(Ctx& c) {
-    const size_t es = c.precision == CIPM_FULL ? sizeof(double) : sizeof(float);
-    cudaMemcpyAsync(c.lval, c.lbase, es * c.sym.nnz_storage, cudaMemcpyDeviceToDevice, c.stream);
+    if (c.precision == CIPM_FULL) build_base_t<double>(c, (double*)c.lval);
+    else build_base_t<float>(c, (float*)c.lval);
     k_scatter_h(c);
 }
 
