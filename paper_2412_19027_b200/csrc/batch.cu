@@ -270,10 +270,16 @@ __device__ void bfactor_cta(const BatchPattern& pt, Inst& I, double ds, double d
             double x[RB];
 #pragma unroll
             for (int c = 0; c < RB; ++c) x[c] = (c < nbk && lane < nbk && c <= lane) ? R[(k0 + c) * W + k0 + lane] : 0.0;
+            // column j is published through shared memory (one store, broadcast loads;
+            // double-buffered in sblk, which the block's L11 overwrites afterwards)
+            // instead of 32 shuffles on the pivot chain — the same values
 #pragma unroll
             for (int j = 0; j < RB; ++j) {
                 if (j < nbk) {
-                    double dj = __shfl_sync(0xffffffffu, x[j], j);
+                    double* col = sblk + (j & 1) * 32;
+                    col[lane] = x[j];
+                    __syncwarp();
+                    double dj = col[j];
                     dj = root_bump(dj, ds, ddc, runmax, pt.sign[s0 + k0 + j], bumped);
                     if (dj == 0.0 && lane == 0) *s_err = 1;
                     runmax = fmax(runmax, fabs(dj));
@@ -285,12 +291,13 @@ __device__ void bfactor_cta(const BatchPattern& pt, Inst& I, double ds, double d
                     const double xj = x[j];
 #pragma unroll
                     for (int c = j + 1; c < RB; ++c) {
-                        const double acj = __shfl_sync(0xffffffffu, xj, c) * inv;
+                        const double acj = col[c] * inv;
                         if (lane >= c) x[c] -= xj * acj;
                     }
                     x[j] = lane > j ? xj * inv : (lane == j ? 1.0 : 0.0);
                 }
             }
+            __syncwarp();
 #pragma unroll
             for (int c = 0; c < RB; ++c) {
                 if (c < nbk && lane < nbk && c <= lane) R[(k0 + c) * W + k0 + lane] = x[c];
