@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -30,6 +31,25 @@ void k_refine_init_one(Ctx& c, int q);
 void k_copy(Ctx& c, const double* src, double* dst, int64_t n);
 int factor_grid(Ctx& c);
 int solve_grid(Ctx& c);
+void k_warm_grids();
+
+int occupancy_blocks(const void* kernel, int threads) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& e : cache)
+        if (e.first == kernel) return e.second;
+    static const bool plain = getenv("CIPM_RED_GRID_PLAIN") != nullptr;   // A/B probe: the 1184-block grid
+    if (plain) return kMaxRedBlocks;
+    int dev = 0, sms = 148, per_sm = 8;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int blocks = per_sm * sms;
+    cache.emplace_back(kernel, blocks);
+    return blocks;
+}
 }  // namespace cipm
 
 using namespace cipm;
@@ -780,6 +800,7 @@ int cipm_ctx_create(const cipm_problem_desc* d, const cipm_symbolic* symh, const
     c.factor_blocks = factor_grid(c);
     c.solve_blocks = solve_grid(c);
     CIPM_CUDA(cudaStreamSynchronize(c.stream));
+    k_warm_grids();
     *out = h;
 #undef TRY
     return CIPM_OK;

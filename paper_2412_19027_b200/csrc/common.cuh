@@ -214,6 +214,24 @@ inline int red_grid(int64_t n) {
     return (int)b;
 }
 
+// grid of a grid-stride reduction kernel: at most ONE wave of the kernel's resident
+// blocks (occupancy API, cached per kernel).  For the division-heavy neighbourhood
+// candidates over nonneg rows (16 sums, 86 registers, 1184 blocks = 4 waves) fewer
+// block reductions and partials win (C2: 42 -> 20 us); memory-bound passes — the
+// thread-per-row SpMVs (kkt_resid2, resid_n), the same candidates over mostly
+// cone rows (C5a: -7 % per solve) — measured slower with it and keep the plain grid.
+// Fixed per kernel and device, so the reductions stay deterministic.
+int occupancy_blocks(const void* kernel, int threads);   // blocks per SM x SMs (capi.cu)
+template <typename K>
+inline int red_grid(int64_t n, K* kernel) {
+    int64_t b = (n + kThreads - 1) / kThreads;
+    const int wave = occupancy_blocks(reinterpret_cast<const void*>(kernel), kThreads);
+    if (b > wave) b = wave;
+    if (b < 1) b = 1;
+    if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+    return (int)b;
+}
+
 inline int grid_for(int64_t n, int threads = kThreads) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;

@@ -805,10 +805,16 @@ void k_step_store(Ctx& c, int which) {
     c.launches++;
 }
 
+// the occupancy query of red_grid(n, kernel) outside any stream capture
+void k_warm_grids() { (void)red_grid(1, mu_candidates); }
+
 void k_mu_candidates(Ctx& c, int g0, int nk, double mu_fixed) {
     MuCand a{c.s, c.z, c.ds[1], c.dz[1], c.m, c.zero_dim, c.nonneg_dim, c.nu + 1.0, c.beta, c.backtrack,
              c.step_scale, nk, g0, mu_fixed};
-    mu_candidates<<<red_grid(c.m), kThreads, 0, c.stream>>>(a, c.sc, c.nb, c.mask, c.err, c.partials, c.counter);
+    // one wave when the nonneg rows (eight divisions each per candidate batch) dominate;
+    // a light pass over mostly cone rows keeps the memory-parallel plain grid (C5a)
+    const int grid = 2 * c.nonneg_dim >= c.m ? red_grid(c.m, mu_candidates) : red_grid(c.m);
+    mu_candidates<<<grid, kThreads, 0, c.stream>>>(a, c.sc, c.nb, c.mask, c.err, c.partials, c.counter);
     c.launches++;
 }
 
