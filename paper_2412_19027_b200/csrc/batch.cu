@@ -393,41 +393,76 @@ __device__ void bsolve_cta(const BatchPattern& pt, Inst& I, const double* r, dou
         t[s0 + i] -= acc;
     }
     __syncthreads();
-    // root, forward: y_b = inv(L_bb) (t_b - sum_{k<b} L_bk y_k)
+    // root, forward: y_b = inv(L_bb) (t_b - sum_{k<b} L_bk y_k).  The block GEMVs run
+    // as NW (diagonal block) / RP (rows below) strided partial sums per row, combined
+    // in a fixed order, instead of one 32-term chain per thread on 32-56 threads
+    constexpr int RP = BT / 64;                                    // partials per row below
+    static_assert(NW * RB <= RB * RB && RP * 64 <= RB * RB, "sblk holds the partials");
+    const int prow = tid & (RB - 1), part = tid / RB;
     for (int k0 = 0; k0 < W; k0 += RB) {
         const int nbk = min(RB, W - k0), k1 = k0 + nbk;
+        {
+            double acc = 0.0;
+            if (prow < nbk)
+                for (int k = part; k <= prow; k += NW) acc += R[(k0 + k) * W + k0 + prow] * t[s0 + k0 + k];
+            sblk[part * RB + prow] = acc;
+        }
+        __syncthreads();
         if (tid < nbk) {
             double acc = 0.0;
-            for (int k = 0; k <= tid; ++k) acc += R[(k0 + k) * W + k0 + tid] * t[s0 + k0 + k];
-            sblk[tid] = acc;
+            for (int q = 0; q < NW; ++q) acc += sblk[q * RB + tid];
+            t[s0 + k0 + tid] = acc;
         }
         __syncthreads();
-        if (tid < nbk) t[s0 + k0 + tid] = sblk[tid];
-        __syncthreads();
-        for (int i = k1 + tid; i < W; i += BT) {
+        for (int i0 = k1; i0 < W; i0 += 64) {
+            const int i = i0 + (tid & 63), q = tid >> 6;
             double acc = 0.0;
-            for (int k = 0; k < nbk; ++k) acc += R[(k0 + k) * W + i] * t[s0 + k0 + k];
-            t[s0 + i] -= acc;
+            if (i < W)
+                for (int k = q; k < nbk; k += RP) acc += R[(k0 + k) * W + i] * t[s0 + k0 + k];
+            sblk[q * 64 + (tid & 63)] = acc;
+            __syncthreads();
+            if (tid < 64 && i0 + tid < W) {
+                double a2 = 0.0;
+                for (int qq = 0; qq < RP; ++qq) a2 += sblk[qq * 64 + tid];
+                t[s0 + i0 + tid] -= a2;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     for (int i = tid; i < W; i += BT) t[s0 + i] /= I.d[s0 + i];
     __syncthreads();
     // root, backward: x_b = inv(L_bb)' (t_b - sum_{i>=k1} L_ib' x_i), last block first
     const int nb = (W + RB - 1) / RB;
+    double* bvec = sblk + NW * RB;                     // the block's right-hand side
     for (int kb = nb - 1; kb >= 0; --kb) {
         const int k0 = kb * RB, nbk = min(RB, W - k0), k1 = k0 + nbk;
-        if (tid < nbk) {
-            const double* Ck = R + (k0 + tid) * W;
+        {
             double acc = 0.0;
-            for (int i = k1; i < W; ++i) acc += Ck[i] * t[s0 + i];
-            sblk[tid] = t[s0 + k0 + tid] - acc;
+            if (prow < nbk) {
+                const double* Ck = R + (k0 + prow) * W;
+                for (int i = k1 + part; i < W; i += NW) acc += Ck[i] * t[s0 + i];
+            }
+            sblk[part * RB + prow] = acc;
         }
         __syncthreads();
         if (tid < nbk) {
-            const double* Cj = R + (k0 + tid) * W + k0;     // column tid of the inverse block
             double acc = 0.0;
-            for (int i = tid; i < nbk; ++i) acc += Cj[i] * sblk[i];
+            for (int q = 0; q < NW; ++q) acc += sblk[q * RB + tid];
+            bvec[tid] = t[s0 + k0 + tid] - acc;
+        }
+        __syncthreads();
+        {
+            double acc = 0.0;
+            if (prow < nbk) {
+                const double* Cj = R + (k0 + prow) * W + k0;   // column prow of the inverse block
+                for (int i = prow + part; i < nbk; i += NW) acc += Cj[i] * bvec[i];
+            }
+            sblk[part * RB + prow] = acc;
+        }
+        __syncthreads();
+        if (tid < nbk) {
+            double acc = 0.0;
+            for (int q = 0; q < NW; ++q) acc += sblk[q * RB + tid];
             t[s0 + k0 + tid] = acc;
         }
         __syncthreads();
