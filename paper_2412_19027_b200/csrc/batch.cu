@@ -323,15 +323,18 @@ __device__ void bfactor_cta(const BatchPattern& pt, Inst& I, double ds, double d
         }
         __syncthreads();
         // trailing update of the lower triangle
+        // (d_k l_ck for the warp's column c formed once per column in the warp's slice of
+        // sblk — free between the row solve and the next diagonal block — not per row i)
         for (int c = k1 + warp; c < W; c += NW) {
+            double* dl = sblk + warp * RB;
+            if (lane < nbk) dl[lane] = I.d[s0 + k0 + lane] * R[(k0 + lane) * W + c];
+            __syncwarp();
             for (int i = c + lane; i < W; i += 32) {
                 double acc = 0.0;
-                for (int k = 0; k < nbk; ++k) {
-                    const double* Ck = R + (k0 + k) * W;
-                    acc += Ck[i] * (I.d[s0 + k0 + k] * Ck[c]);
-                }
+                for (int k = 0; k < nbk; ++k) acc += R[(k0 + k) * W + i] * dl[k];
                 R[c * W + i] -= acc;
             }
+            __syncwarp();
         }
         __syncthreads();
     }
