@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .exceptions import ConicError, DeviceError, PatternMismatch
-from .model import (Equilibration, ProblemData, csr_row_gather_src, reorder_cones, validate,
+from .model import (Equilibration, ProblemData, csr_row_gather_src, max_abs, reorder_cones, validate,
                     validate_values)
 from .native import (P_I64, SC, DeviceContext, Layout, Settings, SymbolicAnalysis, pdbl, pi64, pinned_copy,
                      pinned_empty, require_device)
@@ -202,8 +202,8 @@ class Solver:
         self._ctx.call("cipm_ctx_get_equilibration", None, None, ctypes.byref(c_obj))
         self._equil = Equilibration(None, None, float(c_obj.value))
         # termination norms use the reordered unscaled data (ipm.py:184-185); max is order-free
-        self._norm_q = float(np.max(np.abs(prob.q))) if prob.q.size else 0.0
-        self._norm_b = float(np.max(np.abs(prob.b))) if prob.b.size else 0.0
+        self._norm_q = max_abs(prob.q)
+        self._norm_b = max_abs(prob.b)
 
     def update_data(self, P=None, A=None, q=None, b=None) -> None:
         """Parametric re-solve (reference ipm.py:187-221): same patterns, fresh
