@@ -24,7 +24,7 @@ from collections.abc import Sequence
 import numpy as np
 
 from .exceptions import ConicError, NonFiniteData, PatternMismatch, raise_for_status
-from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, reorder_cones, validate
+from .model import NONNEG, SCALE_MAX, SCALE_MIN, ZERO, ProblemData, max_abs, reorder_cones, validate
 from .native import Layout, Settings, c_void_p, lib, make_desc, pdbl, pi64, pinned_copy, pinned_empty, require_device
 from .settings import FULL, SolveResult, SolverSettings, Status, default_dynamic_reg, default_static_reg
 
@@ -231,9 +231,9 @@ class BatchSolver:
         if bs is not None and bs.shape != (self.count, self.m):
             raise ValueError(f"b must be ({self.count}, {self.m})")
         # the reference's update_data re-validates (problem.py:149-174): non-finite data raises
-        if qs is not None and not np.all(np.isfinite(qs)):
+        if qs is not None and not np.isfinite(max_abs(qs)):
             raise NonFiniteData("q")
-        if bs is not None and not np.all(np.isfinite(bs)):
+        if bs is not None and not np.isfinite(max_abs(bs)):
             raise NonFiniteData("b")
         # own page-locked copies: the H2D is one DMA, and they back the results' certificates
         if qs is not None:
