@@ -249,3 +249,44 @@ def test_gpu_solve_many_heterogeneous_equals_per_instance(gpu):
         assert r.status == w.status
         assert abs(r.iterations - w.iterations) <= 1
         assert abs(r.obj_primal - w.obj_primal) <= 1e-9 * max(1.0, abs(w.obj_primal))
+
+
+def test_batch_results_sequence_cpu():
+    """BatchResults: a lazy sequence of reference SolveResults over the host arrays of
+    one batched D2H (len, indexing, slices, iteration, cached objects, whole-batch
+    columns, certificates as the reference normalises them, ipm.py:401-407)."""
+    from paper_2412_19027_b200.batch import BatchResults
+    from paper_2412_19027_b200.settings import Status
+    c, n, m = 4, 3, 5
+    rng = np.random.default_rng(0)
+    codes = np.array([0, 1, 2, 3], dtype=np.int32)          # optimal, primal / dual infeasible, almost
+    res = rng.standard_normal((c, 9))
+    res[:, 8] = [7, 11, 13, 9]
+    x, z, s = rng.standard_normal((c, n)), rng.standard_normal((c, m)), rng.standard_normal((c, m))
+    q, b = rng.standard_normal((c, n)), rng.standard_normal((c, m))
+    out = BatchResults(codes, res, x, z, s, q, b, 0.5, 0.25)
+    assert len(out) == c
+    assert out.status == [Status.OPTIMAL, Status.PRIMAL_INFEASIBLE, Status.DUAL_INFEASIBLE, Status.ALMOST_OPTIMAL]
+    np.testing.assert_array_equal(out.iterations, [7, 11, 13, 9])
+    np.testing.assert_array_equal(out.obj_primal, res[:, 0])
+    r0 = out[0]
+    assert r0 is out[0] and out[-4] is r0                   # built once, cached
+    assert r0.iterations == 7 and r0.obj_primal == res[0, 0] and r0.certificate is None
+    assert r0.gap == abs(res[0, 0] - res[0, 1]) and r0.setup_seconds == 0.5 and r0.solve_seconds == 0.25
+    np.testing.assert_array_equal(out[1].certificate, z[1] / abs(float(b[1] @ z[1])))
+    np.testing.assert_array_equal(out[2].certificate, x[2] / abs(float(q[2] @ x[2])))
+    assert [r.iterations for r in out] == [7, 11, 13, 9]
+    assert [r.iterations for r in out[1:3]] == [11, 13]
+    with pytest.raises(IndexError):
+        out[4]
+
+
+def test_max_abs_is_the_finiteness_test():
+    a = np.random.default_rng(1).standard_normal(1000)
+    assert model.max_abs(a) == np.max(np.abs(a))
+    assert model.max_abs(np.zeros(0)) == 0.0
+    for bad in (np.nan, np.inf, -np.inf):
+        for pos in (0, 500, 999):
+            v = a.copy()
+            v[pos] = bad
+            assert not np.isfinite(model.max_abs(v))
