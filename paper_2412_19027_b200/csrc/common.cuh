@@ -1,6 +1,7 @@
 // Shared device-side definitions for libcipm (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <cstdint>
 #include <cstdio>
 
@@ -48,6 +49,17 @@ __device__ __forceinline__ void atomic_min_pos(double* addr, double val) {
 }
 
 __device__ __forceinline__ void set_error(int* err, int code) { atomicCAS(err, 0, code); }
+
+// a pivot column published in shared memory (16-byte aligned), read back as one
+// burst of 16-byte broadcast loads (N a multiple of 16 / sizeof(T))
+template <typename T, int N>
+__device__ __forceinline__ void load_col(T (&cc)[N], const T* col) {
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    constexpr int VW = 16 / (int)sizeof(T);
+    static_assert(N % VW == 0, "column length");
+#pragma unroll
+    for (int c = 0; c < N; c += VW) *reinterpret_cast<V*>(&cc[c]) = *reinterpret_cast<const V*>(col + c);
+}
 
 // Dependency flags between CTAs/warps of one persistent launch.  Poll with a
 // relaxed load (no per-poll L1 invalidation — ld.acquire compiles to

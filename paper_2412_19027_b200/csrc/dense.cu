@@ -140,7 +140,12 @@ __device__ __forceinline__ void diag_sub(T* Sk, int k0, int nbk_rt, const int8_t
             T* col = sCol + (j & 1) * 32;
             col[lane] = x[j];
             __syncwarp();
-            double dd = (double)col[j];
+            // the whole column in one burst of 16-byte broadcast loads, so the
+            // operands of the update are in flight with the pivot's own load
+            // (tools/micro/diag_bench.cu: pivot chains -5 % FP64, -11 % FP32)
+            T cc[SB];
+            load_col<T, SB>(cc, col);
+            double dd = (double)cc[j];
             const double bound = ds_r + dd_r * runmax;
             const bool bump = fabs(dd) < bound;
             dd = bump ? (((pos >> j) & 1u) ? bound : -bound) : dd;
@@ -155,7 +160,7 @@ __device__ __forceinline__ void diag_sub(T* Sk, int k0, int nbk_rt, const int8_t
             const T lj = x[j] * inv;
 #pragma unroll
             for (int c = j + 1; c < SB; ++c) {
-                const T acj = col[c];
+                const T acj = cc[c];
                 if (lane >= c) x[c] -= lj * acj;
             }
             x[j] = lane > j ? lj : (lane == j ? (T)1 : x[j]);
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(256) tail_diag(T* __restrict__ L, int r, int k
     __shared__ T sD[TB];
     __shared__ T sInv[SB];
     __shared__ __align__(16) T sLt[SB * SB];
-    __shared__ T sCol[64];
+    __shared__ __align__(16) T sCol[64];
     __shared__ int8_t sSg[TB];
     __shared__ double s_runmax;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;

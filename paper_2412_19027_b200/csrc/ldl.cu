@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(FW * 32) factor_kernel(FactorArgs a, T* __rest
                                                          T* __restrict__ inbox) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ T sD[FW][64];
-    __shared__ T sColw[FW][64];
+    __shared__ __align__(16) T sColw[FW][64];
     __shared__ int8_t sSg[FW][64];
     __shared__ uint64_t bars[FW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -571,7 +571,9 @@ __device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, co
             T* col = sCol + (j & 1) * 32;
             col[lane] = x[j];
             __syncwarp();
-            double dd = (double)col[j];
+            T cc[NB];
+            load_col<T, NB>(cc, col);                  // one burst (common.cuh)
+            double dd = (double)cc[j];
             const double bound = ds_r + dd_r * runmax;
             const bool bump = fabs(dd) < bound;
             dd = bump ? (((pos >> j) & 1u) ? bound : -bound) : dd;
@@ -586,7 +588,7 @@ __device__ __forceinline__ void cta_diag_block(T* Pk, int r, int k0, int nbk, co
             const T lj = x[j] * inv;                 // l_ij (lanes i > j)
 #pragma unroll
             for (int c = j + 1; c < NB; ++c) {
-                const T acj = col[c];                 // unscaled a_cj
+                const T acj = cc[c];                  // unscaled a_cj
                 if (lane >= c) x[c] -= lj * acj;
             }
             x[j] = lane > j ? lj : (lane == j ? (T)1 : x[j]);
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(256, 2) factor_cta_kernel(FactorArgs a, T* __r
     __shared__ T sD[64];
     __shared__ __align__(16) T sLt[64 * 16];    // blocked LDL: L11' of a 16-column block / d_k l_ck
     __shared__ T sInv[16];
-    __shared__ T sCol[64];
+    __shared__ __align__(16) T sCol[64];
     __shared__ int8_t sSg[64];
     __shared__ int32_t s_d32[8];
     __shared__ int64_t s_d64[8];
