@@ -2,7 +2,7 @@
 # round-2 (session 3) final evidence pass, one fresh box: GPU tests, smoke, bench lines of
 # every config with the reference CPU baselines, the reference arm for C2, the C2 launch
 # list, the ncu sweep-traffic capture, the CUPTI timeline and the e2e host probes
-O=gpurun_out/ev9; mkdir -p $O gpurun_out/ncu
+O=gpurun_out/ev10; mkdir -p $O gpurun_out/ncu
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > $O/gputests.log 2>&1; echo "tests rc=$?"; tail -1 $O/gputests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > $O/bench_c2_lasso.json 2> $O/bench_c2_lasso.err; echo "c2 rc=$?"
